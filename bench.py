@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""Benchmark: FMM particle velocity evaluations per second (fp64) on B200.
+
+Workload (BASELINE.json configs[2], the configuration the metric is quoted on
+at 1/2/4/8 B200): N = 1,048,576 particles on a 1024 x 1024 lattice over
+[-1, 1]^2, two opposite-sign Lamb-Oseen vortices, sigma = h/0.8, l = 7,
+p = 17, GAUSSIAN kernel, synthetic seeded inputs.
+
+A step is one full ``evaluate`` (tree build, P2M, M2M, M2L, L2L, P2P, L2P,
+combine) over the resident particle set.  ``value`` = N / mean step time with
+inputs resident in HBM (CUDA graph replay of the C-ABI call; L2 flushed
+between steps by writing a 256 MiB buffer outside the timed events).
+``e2e`` = the same metric through the public API call with pinned HOST
+buffers: H2D of x, y, gamma, sigma and D2H of (u, v) inside the timed region.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+numpy oracle port in oracle/, the reference being pure Python) on a bounded
+config-2-shaped sample on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "FMM particle velocity evals/sec (fp64)"
+UNIT = "particle-evals/s"
+P2P_FLOP_PER_PAIR_GAUSS = 42  # 14 basic + divide (8) + exp (20)
+NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: 64 DFMA/clk/SM at max clock
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2, choices=[0, 1, 2, 3])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def workload(idx):
+    from paper_0809_1810_b200 import workloads as W
+
+    return W.by_index(idx)
+
+
+def cpu_sample_workload():
+    """Bounded CPU sample with config 2's shape: lattice Lamb-Oseen pair, 64 particles
+    per leaf, p = 17, at 1/16 of the particle count (m = 256, l = 5)."""
+    from paper_0809_1810_b200 import workloads as W
+
+    x, y, h = W.lattice(256)
+    g = (W.lamb_oseen(x, y, 0.0, 0.0) - W.lamb_oseen(x, y, 0.5, 0.0)) * h * h
+    return W.Workload("config2_shape_m256_l5_p17", x, y, g, np.full(x.size, h / 0.8), 5, 17)
+
+
+def time_oracle(w, repeats=1):
+    from threadpoolctl import threadpool_limits
+
+    from oracle import fmm_oracle as O
+
+    with threadpool_limits(limits=1):
+        times = []
+        for _ in range(repeats):
+            _, st = O.evaluate(w.x, w.y, w.gamma, w.sigma, w.levels, w.order, True, (-1.0, -1.0, 2.0))
+            times.append(st["t_total"])
+    return times
+
+
+# ----------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    w = cpu_sample_workload()
+    for _ in range(args.warmup):
+        time_oracle(w)
+    t = []
+    for _ in range(args.steps):
+        t += time_oracle(w)
+    mean = statistics.fmean(t)
+    value = w.n / mean
+    sample = f"{w.name}: N={w.n} per step (config 2 is N=1048576, l=7)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": "config2 shape (bounded CPU sample)", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- our arm
+def fp64_peak(lib, torch, dev):
+    """Measured DFMA throughput (TFLOP/s) of a dependent-chain probe filling all SMs."""
+    sink = torch.zeros(1, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    flops = ctypes.c_double()
+    blocks, iters = 148 * 8, 4096
+    for _ in range(2):
+        lib.vfmm_fp64_probe(sink.data_ptr(), blocks, iters, ctypes.byref(flops), stream.cuda_stream)
+    torch.cuda.synchronize(dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 0.0
+    for _ in range(5):
+        a.record(stream)
+        lib.vfmm_fp64_probe(sink.data_ptr(), blocks, iters, ctypes.byref(flops), stream.cuda_stream)
+        b.record(stream)
+        b.synchronize()
+        best = max(best, flops.value / (a.elapsed_time(b) * 1e-3) / 1e12)
+    return best
+
+
+def run_ours(args):
+    import torch
+
+    import paper_0809_1810_b200 as vf
+    from paper_0809_1810_b200 import _lib
+    from paper_0809_1810_b200.engine import Workspace
+
+    rank, world, local = dist_env()
+    if world > 1:
+        from paper_0809_1810_b200 import distributed
+
+        return distributed.bench_main(args)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = _lib.load()
+    w = workload(args.config)
+    n = w.n
+    cfg = vf.FmmConfig(w.levels, w.order, vf.KernelKind.GAUSSIAN_BLOB)
+    dom = vf.Domain(-1.0, -1.0, 2.0)
+    xd, yd, gd, sd = (torch.from_numpy(a).to(dev) for a in (w.x, w.y, w.gamma, w.sigma))
+    out = torch.empty((2, n), dtype=torch.float64, device=dev)
+
+    # warm-up with stats: counts, and the live per-phase CUDA-event times
+    _, st = vf.evaluate_arrays(xd, yd, gd, sd, cfg, dom, out=out)
+    ws = Workspace.get(n, w.levels, w.order, dev)
+    phase = []
+    for _ in range(5):
+        _, s = vf.evaluate_arrays(xd, yd, gd, sd, cfg, dom, out=out)
+        phase.append(s)
+    t_near = statistics.fmean(p.t_near for p in phase)
+    t_m2l = statistics.fmean(p.t_m2l for p in phase)
+
+    # kernel launches per evaluate (host-side counter of the library)
+    c0 = lib.vfmm_launch_count()
+    stream = torch.cuda.Stream(dev)
+    flags = _lib.FLAG_OVERLAP
+
+    def call(s):
+        rc = lib.vfmm_evaluate(xd.data_ptr(), yd.data_ptr(), gd.data_ptr(), sd.data_ptr(), n,
+                               dom.xmin, dom.ymin, dom.side, w.levels, w.order, _lib.KERNEL_GAUSSIAN,
+                               out[0].data_ptr(), out[1].data_ptr(), ws.ptr, ws.nbytes, flags, None,
+                               s.cuda_stream)
+        assert rc == 0, rc
+
+    with torch.cuda.stream(stream):
+        call(stream)
+    torch.cuda.synchronize(dev)
+    launches_per_step = lib.vfmm_launch_count() - c0
+
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        call(torch.cuda.current_stream(dev))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(max(3, args.warmup)):
+        flush.zero_()
+        graph.replay()
+    torch.cuda.synchronize(dev)
+    ref_vel = out.clone()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    cur = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for a, b in ev:
+            flush.zero_()
+            a.record(cur)
+            graph.replay()
+            b.record(cur)
+        torch.cuda.synchronize(dev)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = statistics.fmean(step_ms)
+    assert torch.equal(out, ref_vel), "graph replays are not bitwise reproducible"
+
+    # end to end through the public API from pinned host buffers
+    hx, hy, hg, hs = (torch.from_numpy(a).pin_memory() for a in (w.x, w.y, w.gamma, w.sigma))
+    host_out = torch.empty((2, n), dtype=torch.float64).pin_memory()
+    e2e_ms = []
+    for i in range(args.e2e_steps + 2):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cur)
+        vel, _ = vf.evaluate_arrays(hx, hy, hg, hs, cfg, dom, overlap=True)
+        host_out.copy_(vel, non_blocking=True)
+        b.record(cur)
+        b.synchronize()
+        if i >= 2:
+            e2e_ms.append(a.elapsed_time(b))
+    assert torch.equal(host_out, ref_vel.cpu())
+    e2e = statistics.fmean(e2e_ms)
+
+    peak = fp64_peak(lib, torch, dev)
+    achieved = P2P_FLOP_PER_PAIR_GAUSS * st.near_pair_count / t_near / 1e12  # t_near in s
+    traffic = None
+    prof = os.path.join(REPO, "profiles", f"p2p_traffic_config{args.config}.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    m2l_flops = 8 * (w.order + 1) ** 2 * st.m2l_count
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        tt = time_oracle(w)[0]
+        cpu = {"value": n / tt, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"one full {w.name} evaluate (N={n}) by the numpy oracle port, 1 BLAS thread"}
+
+    line = {
+        "metric": METRIC, "value": n / (ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "n": n, "levels": w.levels, "order": w.order, "kernel": "gaussian",
+                   "domain": [-1.0, -1.0, 2.0], "l2": "flushed between steps (256 MiB write)",
+                   "graph": "CUDA graph replay, near field overlapped with far-field chain",
+                   "m2l_count": st.m2l_count, "near_pair_count": st.near_pair_count},
+        "e2e": {"value": n / (e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 4 * 8 * n,
+                "d2h_bytes_per_step": 2 * 8 * n, "ms_per_step": e2e},
+        "gpu_launches": int(launches_per_step) * args.steps,
+        "roofline": {"bound": "fp64", "kernel": "k_p2p (near field)", "achieved": achieved,
+                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "peak_source": "measured live: DFMA probe (vfmm_fp64_probe), 148x8 CTAs",
+                     "nominal_peak": NOMINAL_FP64_TFLOPS,
+                     "traffic": traffic, "p2p_ms": t_near * 1e3,
+                     "flop_per_pair": P2P_FLOP_PER_PAIR_GAUSS,
+                     "m2l": {"achieved": m2l_flops / t_m2l / 1e12, "ms": t_m2l * 1e3,
+                             "flop_per_translation": 8 * (w.order + 1) ** 2}},
+        "phases_ms": {k: statistics.fmean(getattr(p, k) for p in phase) * 1e3 for k in
+                      ("t_build", "t_upward", "t_m2l", "t_downward", "t_eval", "t_near", "t_total")},
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,137 @@
+/*
+ * vfmm.h — C ABI of the B200-native FMM velocity evaluation for 2-D
+ * Gaussian-regularised vortex particles (drop-in for the reference package
+ * `vortexfmm`, arXiv 0809.1810).
+ *
+ * Every entry point takes plain pointers and sizes; all particle / velocity
+ * buffers are caller-owned DEVICE memory and all work is enqueued on the
+ * caller's CUDA stream (`stream` is a cudaStream_t passed as void*, NULL =
+ * legacy default stream).  No torch types cross this boundary.
+ *
+ * Reference interfaces replaced (paths relative to the reference package
+ * `pkg/src/vortexfmm/`):
+ *   vfmm_evaluate        <- engine.evaluate            engine.py:335-398
+ *   vfmm_evaluate_at     <- engine.evaluate_at         engine.py:401-460
+ *   vfmm_direct          <- kernels.velocity_direct    kernels.py:52-94
+ *   vfmm_workspace_size  <- (no reference analogue: numpy allocates inside
+ *                            engine.upward_pass/translate_pass, engine.py:114-187)
+ *   vfmm_layout          <- read-only views that the reference exposes as
+ *                           Tree.order / Tree.leaf_starts (quadtree.py:116-134)
+ *                           and the per-level multipole / local lists returned
+ *                           by upward_pass / translate_pass (engine.py:114-187)
+ *   vfmm_stats           <- engine.FmmRunStats         engine.py:58-74
+ *
+ * Status codes (return value of every function):
+ */
+#ifndef VFMM_H
+#define VFMM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VFMM_OK 0
+#define VFMM_EINVAL 1        /* bad argument: FmmConfig.validate / empty input (engine.py:49-55,346-347) */
+#define VFMM_EDOMAIN 2       /* particle or target outside the closed domain square (quadtree.py:191-198) */
+#define VFMM_ECUDA 3         /* CUDA runtime error */
+#define VFMM_EWORKSPACE 4    /* workspace pointer NULL or smaller than vfmm_workspace_size() */
+
+#define VFMM_KERNEL_POINT 0     /* KernelKind.POINT_VORTEX  (kernels.py:27-29) */
+#define VFMM_KERNEL_GAUSSIAN 1  /* KernelKind.GAUSSIAN_BLOB (kernels.py:27-29) */
+
+#define VFMM_ORDER_CAP 60       /* expansions.ORDER_CAP (expansions.py:39) */
+#define VFMM_LEVELS_CAP 13      /* 4^13 leaves; int32 leaf keys */
+
+/* Flags for vfmm_evaluate */
+#define VFMM_FLAG_STATS 1u      /* synchronise the stream at the end and fill *stats (timings, counters) */
+#define VFMM_FLAG_OVERLAP 2u    /* run the near field (P2P) on a side stream concurrently with the
+                                   far-field chain; phase timings then overlap */
+#define VFMM_FLAG_FAR_ONLY 4u   /* build the tree and the local expansions only (no near field, no
+                                   evaluation at the particles); used before vfmm_evaluate_at */
+
+/* engine.FmmRunStats (engine.py:58-74).  Times in milliseconds (CUDA events). */
+typedef struct vfmm_stats {
+    int64_t n;
+    int64_t m2l_count;        /* translations performed, engine.py:173-180 */
+    int64_t near_pair_count;  /* sum over leaves of n_leaf*(n_nbhd-1), engine.py:284 */
+    int32_t levels;
+    int32_t order;
+    int32_t sigma_guard_ok;   /* engine.py:361-370 (GAUSSIAN only) */
+    int32_t bad_count;        /* number of out-of-domain particles (status VFMM_EDOMAIN) */
+    int64_t first_bad;        /* smallest out-of-domain index, -1 if none */
+    double max_sigma;         /* max core radius seen (sigma guard input) */
+    double sigma_guard;       /* leaf half-width / 2 */
+    float t_build, t_upward, t_m2l, t_downward, t_eval, t_near, t_total;
+    int32_t overlapped;       /* 1 if VFMM_FLAG_OVERLAP was used */
+} vfmm_stats;
+
+/* Byte offsets of the internal arrays inside the workspace (debug / parity
+ * views).  All arrays are in leaf-sorted particle order unless noted.      */
+typedef struct vfmm_layout {
+    size_t perm;          /* int32 [n]       Tree.order: sorted -> original index */
+    size_t leaf_key;      /* int32 [n]       Tree.sorted_leaf (row-major leaf key) */
+    size_t leaf_starts;   /* int32 [4^l+1]   Tree.leaf_starts */
+    size_t sources;       /* double4 [n]     (x, y, gamma, -1/(2 sigma^2 ln2)) sorted */
+    size_t near_uv;       /* double2 [n]     near-field (u, v), sorted order */
+    size_t mult;          /* double2 [sum_{k=2..l} 4^k (p+1)]  scaled multipoles, level 2 first */
+    size_t loc;           /* double2 [same]  scaled locals, level 2 first */
+    size_t counts;        /* int32  [sum_{k=0..l} 4^k] per-level occupancy, level 0 first */
+    size_t total;         /* workspace bytes */
+} vfmm_layout;
+
+/* Workspace bytes needed for one evaluate of n particles. */
+int vfmm_workspace_size(int64_t n, int levels, int order, size_t* bytes);
+int vfmm_layout_of(int64_t n, int levels, int order, vfmm_layout* out);
+
+/* engine.evaluate (engine.py:335-398), device arrays, original particle order.
+ *   x, y, gamma, sigma : double[n] device
+ *   (xmin, ymin, side) : model.Domain (model.py:39-65); side > 0
+ *   u, v               : double[n] device outputs, original particle order
+ *   stats              : host pointer, filled when flags has VFMM_FLAG_STATS
+ * Without VFMM_FLAG_STATS the call is fully asynchronous and CUDA-graph
+ * capturable (no allocation, no synchronisation); the domain check and the
+ * counters can then be read with vfmm_read_stats after synchronising.      */
+int vfmm_evaluate(const double* x, const double* y, const double* gamma, const double* sigma,
+                  int64_t n, double xmin, double ymin, double side, int levels, int order,
+                  int kernel, double* u, double* v, void* workspace, size_t workspace_bytes,
+                  unsigned flags, vfmm_stats* stats, void* stream);
+
+/* Read the device counters of the last evaluate that used `workspace`
+ * (synchronises `stream`).  Timings are left at 0.                          */
+int vfmm_read_stats(int64_t n, int levels, int order, int kernel, double side,
+                    const void* workspace, vfmm_stats* stats, void* stream);
+
+/* engine.evaluate_at (engine.py:401-460): velocity at m arbitrary in-domain
+ * targets (tx, ty) from the particle set already processed by the LAST
+ * vfmm_evaluate on this workspace (same n, levels, order, kernel, domain).  */
+int vfmm_evaluate_at(const double* tx, const double* ty, int64_t m, int64_t n,
+                     double xmin, double ymin, double side, int levels, int order, int kernel,
+                     double* u, double* v, void* workspace, int64_t* bad_count, void* stream);
+
+/* kernels.velocity_direct (kernels.py:52-94): O(m*n) direct sum in ascending
+ * source index order.  Self terms excluded by r^2 > 0.                      */
+int vfmm_direct_workspace_size(int64_t m, int64_t n, size_t* bytes);
+int vfmm_direct(const double* tx, const double* ty, int64_t m,
+                const double* x, const double* y, const double* gamma, const double* sigma,
+                int64_t n, int kernel, double* u, double* v, void* workspace,
+                size_t workspace_bytes, void* stream);
+
+/* Library self-test helpers (benchmarks): peak FP64 FMA throughput probe.
+ * Runs `iters` DFMA chains on `blocks` x 256 threads; returns the number of
+ * FP64 flops executed via *flops.  Asynchronous on `stream`.              */
+int vfmm_fp64_probe(double* sink, int blocks, int iters, double* flops, void* stream);
+
+/* Total kernel launches issued by this library in this process (host-side
+ * counter; CUDA-graph replays are not counted).                           */
+int64_t vfmm_launch_count(void);
+
+/* Version / build string. */
+const char* vfmm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VFMM_H */

@@ -1,0 +1,183 @@
+// Downward pass (north-star item 4): L2L to the leaves, then L2P fused with
+// the near/far combine and the un-permutation to the caller's order.
+//
+// Replaces engine.downward_pass (engine.py:190-202),
+// expansions.local_shift_matrix (expansions.py:148-155), engine.far_field
+// (engine.py:205-213), expansions.f_to_velocity (expansions.py:217-225), the
+// combine in engine.evaluate (engine.py:394-396) and the far + near parts of
+// engine.evaluate_at (engine.py:434-459).
+#include "vfmm_internal.cuh"
+
+namespace vfmm {
+
+namespace {
+
+// One warp per child cell at `level`, lane = output coefficient n:
+//   Lh'_n += sum_{m>=n} (2^{-m} Lh_m) F_q[m-n]     (exact re-centring)
+__global__ void __launch_bounds__(256)
+    k_l2l(const double2* __restrict__ parent, double2* __restrict__ child, int level, int P,
+          const Tables* __restrict__ T) {
+    __shared__ double2 sF[4][kOrderCap + 16];
+    __shared__ double s2[kOrderCap + 16];
+    for (int i = threadIdx.x; i < 4 * P; i += blockDim.x) sF[i / P][i % P] = T->F[i / P][i % P];
+    for (int i = threadIdx.x; i < P; i += blockDim.x) s2[i] = T->pow2neg[i];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mc = 1 << level, mp = mc >> 1;
+    const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (c >= (int64_t)mc * mc) return;
+    const int cx = (int)(c % mc), cy = (int)(c / mc);
+    const int q = 2 * (cy & 1) + (cx & 1);
+    const double2* L = parent + ((int64_t)(cy >> 1) * mp + (cx >> 1)) * P;
+    for (int nb = 0; nb < P; nb += 32) {
+        const int nn = nb + lane;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int m = nb; m < P; ++m) {
+            const double2 a = L[m];
+            if (m >= nn && nn < P) {
+                const double sc = s2[m];
+                const double2 f = sF[q][m - nn];
+                const double axs = a.x * sc, ays = a.y * sc;
+                acc.x = fma(axs, f.x, fma(-ays, f.y, acc.x));
+                acc.y = fma(axs, f.y, fma(ays, f.x, acc.y));
+            }
+        }
+        if (nn < P) {
+            double2 cur = child[c * P + nn];
+            cur.x += acc.x;
+            cur.y += acc.y;
+            child[c * P + nn] = cur;
+        }
+    }
+}
+
+// Horner evaluation of the leaf local expansion at z:
+//   f(z) = sum_m Lh_m / m! (-w)^m,  w = (z - c) / r
+__device__ __forceinline__ double2 eval_local(const double2* __restrict__ Lh, int P, double wx,
+                                              double wy, const double* __restrict__ invfact) {
+    const double nx = -wx, ny = -wy;
+    double ax = Lh[P - 1].x * invfact[P - 1], ay = Lh[P - 1].y * invfact[P - 1];
+    for (int k = P - 2; k >= 0; --k) {
+        const double2 c = Lh[k];
+        const double f = invfact[k];
+        const double tx = fma(ax, nx, fma(-ay, ny, c.x * f));
+        const double ty = fma(ax, ny, fma(ay, nx, c.y * f));
+        ax = tx;
+        ay = ty;
+    }
+    return make_double2(ax, ay);
+}
+
+__global__ void __launch_bounds__(256)
+    k_l2p_combine(const Src* __restrict__ src, const int* __restrict__ keys,
+                  const int* __restrict__ perm, const double2* __restrict__ loc,
+                  const double2* __restrict__ near_uv, int64_t n, int levels, int P, double xmin,
+                  double ymin, double side, const Tables* __restrict__ T, double* __restrict__ u,
+                  double* __restrict__ v) {
+    __shared__ double sfact[kOrderCap + 16];
+    for (int i = threadIdx.x; i < P; i += blockDim.x) sfact[i] = T->invfact[i];
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int m = 1 << levels;
+    const int leaf = keys[i];
+    const int ix = leaf % m, iy = leaf / m;
+    const double r = side / m;
+    const double cx = cell_center(xmin, ix, r), cy = cell_center(ymin, iy, r);
+    const double inv_r = 1.0 / r;
+    const Src s = src[i];
+    const double2 f =
+        eval_local(loc + (int64_t)leaf * P, P, (s.x - cx) * inv_r, (s.y - cy) * inv_r, sfact);
+    const double2 nv = near_uv[i];
+    // f_to_velocity: u = Im f / 2pi, v = Re f / 2pi; then far + near
+    const int o = perm[i];
+    u[o] = f.y * kInv2Pi + nv.x;
+    v[o] = f.x * kInv2Pi + nv.y;
+}
+
+// evaluate_at: one thread per target, far field from the target's leaf local
+// expansion, then the near field over the 3x3 neighbourhood (engine.py:434-459).
+template <bool GAUSS>
+__global__ void __launch_bounds__(256)
+    k_eval_at(const double* __restrict__ tx, const double* __restrict__ ty, int64_t mt,
+              const Src* __restrict__ src, const int* __restrict__ ls,
+              const double2* __restrict__ loc, int levels, int P, double xmin, double ymin,
+              double side, const Tables* __restrict__ T, double* __restrict__ u,
+              double* __restrict__ v, Counters* ctr) {
+    __shared__ double sfact[kOrderCap + 16];
+    __shared__ double stab[32];
+    for (int i = threadIdx.x; i < P; i += blockDim.x) sfact[i] = T->invfact[i];
+    for (int i = threadIdx.x; i < 32; i += blockDim.x) stab[i] = T->exp2tab[i];
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= mt) return;
+    const double x = tx[i], y = ty[i];
+    const double xmax = xmin + side, ymax = ymin + side;
+    if (!((x >= xmin) && (x <= xmax) && (y >= ymin) && (y <= ymax))) {
+        atomicAdd(&ctr->bad_count, 1);
+        atomicMin(&ctr->first_bad, (int)i);
+        u[i] = 0.0;
+        v[i] = 0.0;
+        return;
+    }
+    const int m = 1 << levels;
+    int ix = (int)((x - xmin) / side * (double)m);
+    int iy = (int)((y - ymin) / side * (double)m);
+    ix = ix < m - 1 ? ix : m - 1;
+    iy = iy < m - 1 ? iy : m - 1;
+    const double r = side / m;
+    const double cx = cell_center(xmin, ix, r), cy = cell_center(ymin, iy, r);
+    const double inv_r = 1.0 / r;
+    const double2 f = eval_local(loc + ((int64_t)iy * m + ix) * P, P, (x - cx) * inv_r,
+                                 (y - cy) * inv_r, sfact);
+    double nu = 0.0, nv = 0.0;
+    const int xlo = ix > 0 ? ix - 1 : 0, xhi = ix < m - 1 ? ix + 1 : m - 1;
+    for (int ny = iy - 1; ny <= iy + 1; ++ny) {
+        if (ny < 0 || ny >= m) continue;
+        const int lo = ls[(int64_t)ny * m + xlo], hi = ls[(int64_t)ny * m + xhi + 1];
+        for (int jj = lo; jj < hi; ++jj) {
+            const Src s = src[jj];
+            pair_acc<GAUSS>(x, y, s.x, s.y, s.g, s.q2, stab, nu, nv);
+        }
+    }
+    u[i] = f.y * kInv2Pi + nu * kInv2Pi;
+    v[i] = f.x * kInv2Pi + nv * kInv2Pi;
+}
+
+}  // namespace
+
+void launch_l2l(const Layout& L, const Tables* T, double2* loc, cudaStream_t s) {
+    for (int level = 3; level <= L.levels; ++level) {
+        const int64_t nc = 1ll << (2 * level);
+        const double2* parent = loc + L.level_cell_off[level - 1] * L.P;
+        double2* child = loc + L.level_cell_off[level] * L.P;
+        k_l2l<<<(unsigned)((nc + 7) / 8), 256, 0, s>>>(parent, child, level, L.P, T);
+        note_launches(1);
+    }
+}
+
+void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const int* keys,
+                        const int* perm, const double2* loc, const double2* near_uv, double xmin,
+                        double ymin, double side, double* u, double* v, cudaStream_t s) {
+    const double2* leaf_loc = loc + L.level_cell_off[L.levels] * L.P;
+    k_l2p_combine<<<(unsigned)((L.n + 255) / 256), 256, 0, s>>>(
+        src, keys, perm, leaf_loc, near_uv, L.n, L.levels, L.P, xmin, ymin, side, T, u, v);
+    note_launches(1);
+}
+
+void launch_eval_at(const Layout& L, const Tables* T, const double* tx, const double* ty,
+                    int64_t m, const Src* src, const int* leaf_starts, const double2* loc,
+                    double xmin, double ymin, double side, int kernel, double* u, double* v,
+                    Counters* ctr, cudaStream_t s) {
+    const double2* leaf_loc = loc + L.level_cell_off[L.levels] * L.P;
+    const unsigned g = (unsigned)((m + 255) / 256);
+    if (kernel == VFMM_KERNEL_GAUSSIAN)
+        k_eval_at<true><<<g, 256, 0, s>>>(tx, ty, m, src, leaf_starts, leaf_loc, L.levels, L.P,
+                                          xmin, ymin, side, T, u, v, ctr);
+    else
+        k_eval_at<false><<<g, 256, 0, s>>>(tx, ty, m, src, leaf_starts, leaf_loc, L.levels, L.P,
+                                           xmin, ymin, side, T, u, v, ctr);
+    note_launches(1);
+}
+
+}  // namespace vfmm

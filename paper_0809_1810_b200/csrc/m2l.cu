@@ -1,0 +1,164 @@
+// M2L over every cell's interaction list, all levels in ONE launch
+// (north-star item 3).
+//
+// Replaces engine.translate_pass (engine.py:150-187), engine._il_offsets
+// (engine.py:77-89), engine._parity_grid (engine.py:92-98) and
+// expansions.m2l_matrix (expansions.py:133-145).
+//
+// In the scaled representation the translation of offset o = (dx, dy) is a
+// Hankel product  Lh_m = sum_n H_o[m+n] M_n,  H_o[q] = q! tau^{-(q+1)},
+// tau = -(dx + i dy), identical at every level.  A block owns one
+// (level, parity class, m-chunk); its 27 offsets' H rows sit in shared memory
+// and every lane (one destination cell) reads them as warp-wide broadcasts.
+// Each thread keeps TN complex accumulators (outputs m0..m0+TN-1) in
+// registers across all 27 offsets, so a loaded multipole coefficient feeds
+// TN complex FMAs.  Per destination, offsets apply in row-major source order
+// (the accumulation order of engine.py:166-185); empty sources are skipped
+// when a whole warp's sources are empty and multiply as exact zeros otherwise.
+#include "vfmm_internal.cuh"
+
+namespace vfmm {
+
+namespace {
+
+constexpr int kM2LThreads = 128;
+
+template <int TN>
+__global__ void __launch_bounds__(kM2LThreads)
+    k_m2l(const double2* __restrict__ mult, const int* __restrict__ counts, double2* __restrict__ loc,
+          int levels, int P, int nchunks, const size_t* __restrict__ dummy, const Tables* __restrict__ T,
+          unsigned long long* __restrict__ m2l_count, size_t off2) {
+    extern __shared__ double2 sH[];  // [27][TN + P - 1]
+    (void)dummy;
+    // ---- decode (level, parity, chunk, block-in-class) from blockIdx.x ----
+    int64_t b = blockIdx.x;
+    int level = 2;
+    size_t cell_off = 0;   // cells before this level in mult/loc (level 2 first)
+    size_t cnt_off = 0;    // cells before this level in counts (level 0 first)
+    for (int k = 0; k < 2; ++k) cnt_off += (size_t)1 << (2 * k);
+    int64_t bpc = 0;  // blocks per (parity, chunk) at this level
+    for (;;) {
+        const int64_t dests = 1ll << (2 * (level - 1));
+        bpc = (dests + kM2LThreads - 1) / kM2LThreads;
+        const int64_t nb = bpc * 4 * nchunks;
+        if (b < nb || level == levels) break;
+        b -= nb;
+        cell_off += (size_t)1 << (2 * level);
+        cnt_off += (size_t)1 << (2 * level);
+        ++level;
+    }
+    (void)off2;
+    const int chunk = (int)(b / (4 * bpc));
+    const int parity = (int)((b / bpc) % 4);
+    const int64_t blk = b % bpc;
+    const int px = parity & 1, py = parity >> 1;
+    const int m0 = chunk * TN;
+    const int HL = TN + P - 1;
+
+    // ---- stage the 27 H rows of this parity class ----
+    for (int i = threadIdx.x; i < 27 * HL; i += blockDim.x) {
+        const int o = i / HL, q = i % HL;
+        // o-th offset of _il_offsets(px, py): dy outer, dx inner, max(|dx|,|dy|) >= 2
+        int idx = 0, dxo = 0, dyo = 0;
+        for (int dy = -2 - py; dy < 4 - py; ++dy)
+            for (int dx = -2 - px; dx < 4 - px; ++dx) {
+                const int adx = dx < 0 ? -dx : dx, ady = dy < 0 ? -dy : dy;
+                if ((adx > ady ? adx : ady) >= 2) {
+                    if (idx == o) { dxo = dx; dyo = dy; }
+                    ++idx;
+                }
+            }
+        sH[i] = T->H[(dyo + 3) * 7 + (dxo + 3)][m0 + q];
+    }
+    __syncthreads();
+
+    const int mk = 1 << level, half = mk >> 1;
+    const int64_t j = blk * kM2LThreads + threadIdx.x;
+    const bool active = j < (int64_t)half * half;
+    const int ix = active ? 2 * (int)(j % half) + px : 0;
+    const int iy = active ? 2 * (int)(j / half) + py : 0;
+    const double2* M = mult + cell_off * P;
+    const int* cnt = counts + cnt_off;
+
+    double ax[TN], ay[TN];
+#pragma unroll
+    for (int t = 0; t < TN; ++t) ax[t] = ay[t] = 0.0;
+    int ntrans = 0;
+    int o = 0;
+    for (int dy = -2 - py; dy < 4 - py; ++dy) {
+        for (int dx = -2 - px; dx < 4 - px; ++dx) {
+            const int adx = dx < 0 ? -dx : dx, ady = dy < 0 ? -dy : dy;
+            if ((adx > ady ? adx : ady) < 2) continue;
+            const int sx = ix + dx, sy = iy + dy;
+            const bool inr = active && sx >= 0 && sx < mk && sy >= 0 && sy < mk;
+            const int64_t sidx = (int64_t)sy * mk + sx;
+            const bool live = inr && cnt[inr ? sidx : 0] > 0;
+            ntrans += live ? 1 : 0;
+            const double2* h = sH + o * HL;
+            ++o;
+            if (!__any_sync(0xffffffffu, live)) continue;
+            const double2* Ms = M + (live ? sidx : 0) * P;
+            for (int n = 0; n < P; ++n) {
+                double2 a = Ms[n];
+                if (!live) a = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int t = 0; t < TN; ++t) {
+                    const double2 hh = h[t + n];
+                    ax[t] = fma(hh.x, a.x, fma(-hh.y, a.y, ax[t]));
+                    ay[t] = fma(hh.x, a.y, fma(hh.y, a.x, ay[t]));
+                }
+            }
+        }
+    }
+    if (active) {
+        double2* out = loc + (cell_off + (size_t)iy * mk + ix) * P;
+#pragma unroll
+        for (int t = 0; t < TN; ++t)
+            if (m0 + t < P) out[m0 + t] = make_double2(ax[t], ay[t]);
+    }
+    if (chunk == 0) {
+        // m2l_count counts (destination, nonempty source) pairs at every level
+        // including empty destinations (engine.py:173-180)
+        for (int s = 16; s > 0; s >>= 1) ntrans += __shfl_xor_sync(0xffffffffu, ntrans, s);
+        if ((threadIdx.x & 31) == 0 && ntrans) atomicAdd(m2l_count, (unsigned long long)ntrans);
+    }
+}
+
+template <int TN>
+void launch_tn(const Layout& L, const Tables* T, const double2* mult, const int* counts,
+               double2* loc, Counters* ctr, cudaStream_t s) {
+    const int nchunks = (L.P + TN - 1) / TN;
+    int64_t blocks = 0;
+    for (int level = 2; level <= L.levels; ++level) {
+        const int64_t dests = 1ll << (2 * (level - 1));
+        blocks += (dests + kM2LThreads - 1) / kM2LThreads * 4 * nchunks;
+    }
+    const size_t shm = (size_t)27 * (TN + L.P - 1) * sizeof(double2);
+    k_m2l<TN><<<(unsigned)blocks, kM2LThreads, shm, s>>>(mult, counts, loc, L.levels, L.P, nchunks,
+                                                       nullptr, T, &ctr->m2l_count, 0);
+    note_launches(1);
+}
+
+}  // namespace
+
+int m2l_chunk(int P) {
+    int best = 8, waste = 1 << 30;
+    for (int tn = 8; tn >= 4; --tn) {
+        const int w = (P + tn - 1) / tn * tn - P;
+        if (w < waste) { waste = w; best = tn; }
+    }
+    return best;
+}
+
+void launch_m2l(const Layout& L, const Tables* T, const double2* mult, const int* counts,
+                double2* loc, Counters* ctr, cudaStream_t s) {
+    switch (m2l_chunk(L.P)) {
+        case 4: launch_tn<4>(L, T, mult, counts, loc, ctr, s); break;
+        case 5: launch_tn<5>(L, T, mult, counts, loc, ctr, s); break;
+        case 6: launch_tn<6>(L, T, mult, counts, loc, ctr, s); break;
+        case 7: launch_tn<7>(L, T, mult, counts, loc, ctr, s); break;
+        default: launch_tn<8>(L, T, mult, counts, loc, ctr, s); break;
+    }
+}
+
+}  // namespace vfmm

@@ -1,0 +1,139 @@
+// Upward pass (north-star item 2): P2M at the leaves, then M2M up to level 2.
+//
+// Replaces engine.upward_pass (engine.py:114-147), expansions.p2m
+// (expansions.py:88-101) and expansions.multipole_shift_matrix
+// (expansions.py:119-130).  Coefficients are stored in the scaled form
+// M_n = a_n / (r^{n+1} n!) (vfmm_internal.cuh), which makes the shift
+// operator level independent:  P_m = 2^{-(m+1)} sum_{k<=m} M_k E_q[m-k].
+#include "vfmm_internal.cuh"
+
+namespace vfmm {
+
+namespace {
+
+constexpr int kP2MWarps = 2;
+
+// One warp per leaf.  Lanes own particles; the powers Gamma w^k of a round of
+// 32 particles are transposed through shared memory so that lane k sums
+// coefficient k over the particles in sorted order (np.add.reduceat order).
+__global__ void __launch_bounds__(kP2MWarps * 32)
+    k_p2m(const Src* __restrict__ src, const int* __restrict__ ls, int levels, int P, double xmin,
+          double ymin, double side, const Tables* __restrict__ T, double2* __restrict__ mult) {
+    __shared__ double2 buf[kP2MWarps][32][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m = 1 << levels;
+    const int64_t leaf = (int64_t)blockIdx.x * kP2MWarps + warp;
+    if (leaf >= (int64_t)m * m) return;
+    const int lo = ls[leaf], hi = ls[leaf + 1];
+    double2* out = mult + leaf * P;
+    if (lo == hi) {
+        for (int k = lane; k < P; k += 32) out[k] = make_double2(0.0, 0.0);
+        return;
+    }
+    const int ix = (int)(leaf % m), iy = (int)(leaf / m);
+    const double r = side / m;  // Tree.cell_side (quadtree.py:140-141)
+    const double cx = cell_center(xmin, ix, r), cy = cell_center(ymin, iy, r);
+    const double inv_r = 1.0 / r;
+    const int ngroups = (P + 31) >> 5;  // <= 2 for P <= 61
+    double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+    for (int base = lo; base < hi; base += 32) {
+        const int j = base + lane;
+        double2 term = make_double2(0.0, 0.0), w = make_double2(0.0, 0.0);
+        if (j < hi) {
+            const Src s = src[j];
+            term.x = s.g;
+            w.x = (s.x - cx) * inv_r;
+            w.y = (s.y - cy) * inv_r;
+        }
+        for (int g = 0; g < ngroups; ++g) {
+            const int kmax = min(32, P - g * 32);
+            for (int kk = 0; kk < kmax; ++kk) {
+                buf[warp][kk][lane] = term;
+                const double tx = term.x * w.x - term.y * w.y;
+                const double ty = term.x * w.y + term.y * w.x;
+                term.x = tx;
+                term.y = ty;
+            }
+            __syncwarp();
+            if (lane < kmax) {
+                double2 a = g == 0 ? acc0 : acc1;
+                const int cnt = min(32, hi - base);
+                for (int q = 0; q < cnt; ++q) {
+                    const double2 t = buf[warp][lane][q];
+                    a.x += t.x;
+                    a.y += t.y;
+                }
+                if (g == 0) acc0 = a; else acc1 = a;
+            }
+            __syncwarp();
+        }
+    }
+    for (int g = 0; g < ngroups; ++g) {
+        const int k = g * 32 + lane;
+        if (k < P) {
+            const double2 a = g == 0 ? acc0 : acc1;
+            const double sc = T->invfact[k] * inv_r;
+            out[k] = make_double2(a.x * sc, a.y * sc);
+        }
+    }
+}
+
+// One warp per parent cell at level `level-1`, lane = output coefficient m.
+// Children in quadrant order (0,0), (1,0), (0,1), (1,1) like engine.py:140-145.
+__global__ void __launch_bounds__(256)
+    k_m2m(const double2* __restrict__ child, double2* __restrict__ parent, int level, int P,
+          const Tables* __restrict__ T) {
+    __shared__ double2 sE[4][kOrderCap + 16];
+    __shared__ double s2[kOrderCap + 16];
+    for (int i = threadIdx.x; i < 4 * P; i += blockDim.x) sE[i / P][i % P] = T->E[i / P][i % P];
+    for (int i = threadIdx.x; i <= P; i += blockDim.x) s2[i] = T->pow2neg[i];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mc = 1 << level, mp = mc >> 1;
+    const int64_t par = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (par >= (int64_t)mp * mp) return;
+    const int jx = (int)(par % mp), jy = (int)(par / mp);
+    for (int mb = 0; mb < P; mb += 32) {
+        const int mm = mb + lane;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int q = 0; q < 4; ++q) {
+            const int cxq = q & 1, cyq = q >> 1;
+            const double2* M = child + ((int64_t)(2 * jy + cyq) * mc + 2 * jx + cxq) * P;
+            const int kend = min(P - 1, mb + 31);
+            for (int k = 0; k <= kend; ++k) {
+                const double2 a = M[k];
+                if (k <= mm && mm < P) {
+                    const double2 e = sE[q][mm - k];
+                    acc.x = fma(a.x, e.x, fma(-a.y, e.y, acc.x));
+                    acc.y = fma(a.x, e.y, fma(a.y, e.x, acc.y));
+                }
+            }
+        }
+        if (mm < P) {
+            const double sc = s2[mm + 1];
+            parent[par * P + mm] = make_double2(acc.x * sc, acc.y * sc);
+        }
+    }
+}
+
+}  // namespace
+
+void launch_p2m(const Layout& L, const Src* src, const int* leaf_starts, double xmin, double ymin,
+                double side, double2* mult_leaf, const Tables* T, cudaStream_t s) {
+    const int64_t nl = (int64_t)L.nleaves;
+    k_p2m<<<(unsigned)((nl + kP2MWarps - 1) / kP2MWarps), kP2MWarps * 32, 0, s>>>(
+        src, leaf_starts, L.levels, L.P, xmin, ymin, side, T, mult_leaf);
+    note_launches(1);
+}
+
+void launch_m2m(const Layout& L, const Tables* T, double2* mult, cudaStream_t s) {
+    for (int level = L.levels; level >= 3; --level) {
+        const int64_t np = 1ll << (2 * (level - 1));
+        double2* child = mult + L.level_cell_off[level] * L.P;
+        double2* parent = mult + L.level_cell_off[level - 1] * L.P;
+        k_m2m<<<(unsigned)((np + 7) / 8), 256, 0, s>>>(child, parent, level, L.P, T);
+        note_launches(1);
+    }
+}
+
+}  // namespace vfmm

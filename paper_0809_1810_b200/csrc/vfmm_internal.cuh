@@ -1,0 +1,174 @@
+// Internal declarations shared by the vfmm CUDA translation units.
+//
+// Representation: every expansion is stored in a
+// level-independent scaled form so that all translation operators are the
+// same at every level and fit in a few KB of tables:
+//   multipole  M_n = a_n / (r^{n+1} n!)          a_n as in expansions.py:88-101
+//   local      Lh_m = (-1)^m m! r^m L_m           L_m as in expansions.py:148-155
+// with r the cell side of the level.  Then (derivation in DESIGN.md):
+//   M2M  P_m  = 2^{-(m+1)} sum_{k<=m} M_k  E_q[m-k],   E_q[j] = d_q^j / j!
+//   M2L  Lh_m = sum_n H_o[m+n] M_n,                    H_o[q] = q! tau_o^{-(q+1)}
+//   L2L  Lh'_n += sum_{m>=n} 2^{-m} Lh_m F_q[m-n],     F_q[j] = (-d_q)^j / j!
+//   L2P  f(z)  = sum_m Lh_m / m! (-w)^m,               w = (z - c) / r
+// d_q = (cx-1/2) + i(cy-1/2) for child quadrant q = 2*cy + cx and
+// tau_o = -(dx + i dy) for the interaction-list offset o = (dx, dy).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/vfmm.h"
+
+namespace vfmm {
+
+constexpr int kOrderCap = VFMM_ORDER_CAP;
+constexpr int kQMax = 2 * kOrderCap + 16;  // H table length (padded for m-chunks)
+constexpr int kOffsets = 49;               // 7x7 offset grid (dy+3)*7 + (dx+3)
+
+// Packed per-particle source record in leaf-sorted order: x, y, gamma and
+// q2 = -1 / (2 sigma^2 ln 2) so that exp(-r^2/(2 sigma^2)) = 2^(r^2 q2).
+struct __align__(16) Src {
+    double x, y, g, q2;
+};
+
+// Device-side counters (one struct at a fixed workspace offset).
+struct Counters {
+    unsigned long long m2l_count;
+    unsigned long long near_pairs;
+    unsigned long long sigma_max_bits;  // ordered-bits encoding of max sigma
+    int bad_count;
+    int first_bad;
+    int ntasks;
+    int pad;
+};
+
+// Translation tables (device globals, uploaded once per device).
+struct Tables {
+    double2 H[kOffsets][kQMax];      // M2L Hankel generators
+    double2 E[4][kOrderCap + 16];    // M2M
+    double2 F[4][kOrderCap + 16];    // L2L
+    double invfact[kOrderCap + 16];
+    double pow2neg[2 * kOrderCap + 16];  // 2^-k
+    double exp2tab[32];              // 2^(j/32)
+};
+
+const Tables* device_tables();   // device pointer (uploaded on first use)
+
+struct Layout {
+    int64_t n;
+    int levels, order, P;  // P = order + 1
+    int digit_bits, passes, wc, nchunks;
+    size_t nleaves;
+    size_t key_a, key_b, val_a, val_b, hist, task_scratch, scan_aux, src, near_uv, leaf_starts,
+        counts, mult, loc, tasks, counters, total;
+    size_t level_cell_off[VFMM_LEVELS_CAP + 2];  // cells before level k (k>=2) in mult/loc
+    size_t count_off[VFMM_LEVELS_CAP + 2];       // cells before level k in counts
+    size_t max_tasks;
+    size_t scan_aux_elems;
+};
+
+bool make_layout(int64_t n, int levels, int order, Layout* L);
+
+// Host-side count of kernel launches issued by the library (bench evidence).
+void note_launches(int k);
+
+// ---- kernels launchers (each enqueues on `s`) ----
+void launch_keys(const double* x, const double* y, const double* sigma, int64_t n, double xmin,
+                 double ymin, double side, int levels, int* key, int* val, Counters* ctr,
+                 cudaStream_t s);
+void launch_sort(const Layout& L, char* ws, cudaStream_t s, int** keys_out, int** perm_out);
+void launch_scan_i32(int* data, int64_t n, int* aux, cudaStream_t s);  // in-place exclusive
+void launch_pack(const double* x, const double* y, const double* g, const double* sigma,
+                 const int* perm, int64_t n, Src* src, cudaStream_t s);
+void launch_leaf_starts(const int* sorted_keys, int64_t n, int nleaves, int* leaf_starts,
+                        cudaStream_t s);
+void launch_counts(const Layout& L, const int* leaf_starts, int* counts, cudaStream_t s);
+void launch_tasks(const Layout& L, const int* leaf_starts, int* task_scratch, int2* tasks,
+                  int* aux, Counters* ctr, cudaStream_t s);
+void launch_p2m(const Layout& L, const Src* src, const int* leaf_starts, double xmin, double ymin,
+                double side, double2* mult_leaf, const Tables* T, cudaStream_t s);
+void launch_init_counters(Counters* ctr, cudaStream_t s);
+size_t scan_aux_elems(int64_t n);
+void launch_m2m(const Layout& L, const Tables* T, double2* mult, cudaStream_t s);
+void launch_m2l(const Layout& L, const Tables* T, const double2* mult, const int* counts,
+                double2* loc, Counters* ctr, cudaStream_t s);
+void launch_l2l(const Layout& L, const Tables* T, double2* loc, cudaStream_t s);
+void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
+                const int2* tasks, Counters* ctr, int kernel, double2* near_uv, cudaStream_t s);
+void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const int* keys,
+                        const int* perm, const double2* loc, const double2* near_uv, double xmin,
+                        double ymin, double side, double* u, double* v, cudaStream_t s);
+void launch_eval_at(const Layout& L, const Tables* T, const double* tx, const double* ty,
+                    int64_t m, const Src* src, const int* leaf_starts, const double2* loc,
+                    double xmin, double ymin, double side, int kernel, double* u, double* v,
+                    Counters* ctr, cudaStream_t s);
+int direct_nsplit(int64_t m, int64_t n);
+void launch_direct(const double* tx, const double* ty, int64_t m, const double* x,
+                   const double* y, const double* g, const double* sigma, int64_t n, int kernel,
+                   double* pu, double* pv, int nsplit, double* u, double* v, const Tables* T,
+                   cudaStream_t s);
+
+// Cell centre exactly as Tree.centers (quadtree.py:146-152): xmin + (i + 0.5) * s
+// with two roundings (no FMA contraction).
+__device__ __forceinline__ double cell_center(double lo, int i, double s) {
+    return __dadd_rn(lo, __dmul_rn((double)i + 0.5, s));
+}
+
+// ---- shared device math ----
+
+// e = 2^y for y in [-60, 0] (callers clamp), table-driven: 2^(j/32) * 2^k * 2^r
+// with |r| <= 1/64 and a degree-6 Taylor polynomial of 2^r = e^(r ln2).
+// Truncation error (ln2/64)^7/7! < 4e-18 relative; total error ~1 ulp.
+__device__ __forceinline__ double exp2_neg(double y, const double* __restrict__ tab) {
+    const double kShift = 6755399441055744.0;  // 1.5 * 2^52
+    double t = fma(y, 32.0, kShift);
+    int n = __double2loint(t);
+    double nf = t - kShift;
+    double r = fma(nf, -0.03125, y);  // exact
+    // coefficients ln2^k / k!, k = 1..6
+    double p = 1.540353039338161e-4;
+    p = fma(p, r, 1.3333558146428443e-3);
+    p = fma(p, r, 9.618129107628477e-3);
+    p = fma(p, r, 5.550410866482158e-2);
+    p = fma(p, r, 2.4022650695910072e-1);
+    p = fma(p, r, 6.931471805599453e-1);
+    double T = tab[n & 31];
+    double res = fma(T, r * p, T);
+    int hi = __double2hiint(res) + ((n >> 5) << 20);
+    return __hiloint2double(hi, __double2loint(res));
+}
+
+// 1/x via the MUFU reciprocal seed and one cubically convergent refinement.
+__device__ __forceinline__ double rcp_fast(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    e = fma(e, e, e);
+    return fma(y, e, y);
+}
+
+// Accumulate the pair interaction of source (sx, sy, g, q2) on target (tx, ty):
+// (u, v) += g (1 - exp(-r^2/(2 sigma^2))) / r^2 * (-dy, dx)  [times 1/2pi later]
+// Same arithmetic structure as kernels.kernel_eval (kernels.py:39-49) and
+// engine._pair_velocity (engine.py:245-257); r^2 == 0 contributes 0.
+template <bool GAUSS>
+__device__ __forceinline__ void pair_acc(double tx, double ty, double sx, double sy, double g,
+                                         double q2, const double* __restrict__ tab, double& u,
+                                         double& v) {
+    double dx = tx - sx;
+    double dy = ty - sy;
+    double r2 = fma(dy, dy, dx * dx);
+    double c = g * rcp_fast(r2);
+    if (GAUSS) {
+        double y = fmax(r2 * q2, -60.0);
+        c = c * (1.0 - exp2_neg(y, tab));
+    }
+    c = (r2 > 0.0) ? c : 0.0;
+    u = fma(-c, dy, u);
+    v = fma(c, dx, v);
+}
+
+constexpr double kInv2Pi = 0.15915494309189535;  // 1 / (2 pi)
+constexpr double kTwoPi = 6.283185307179586;
+
+}  // namespace vfmm

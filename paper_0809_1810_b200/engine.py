@@ -1,0 +1,279 @@
+"""Drop-in FMM engine: ``evaluate`` / ``evaluate_at`` on the B200.
+
+Mirrors ``vortexfmm.engine`` (reference ``engine.py:41-74,335-460``):
+same ``FmmConfig`` / ``FmmRunStats`` fields, same argument validation and
+error types (``ValueError``, ``OutOfDomainError``), the same sigma-guard
+``UserWarning`` text, and the same return value -- an (N, 2) float64 array of
+(u, v) in the caller's particle order plus the run statistics.
+
+Every phase runs in the CUDA library (``libvfmm.so``, ``csrc/``) through the
+C ABI of ``include/vfmm.h``; this module only converts inputs, owns the
+device workspace and maps status codes to the reference's exceptions.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import warnings
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from ._device import as_device_f64, device_of, require_cuda, stream_ptr, torch
+from .kernels import KernelKind, kernel_code
+from .model import Domain, enclosing_domain_of, to_arrays
+from .quadtree import OutOfDomainError
+
+ORDER_CAP = _lib.ORDER_CAP
+
+
+@dataclass(frozen=True)
+class FmmConfig:
+    """Run parameters: tree depth, truncation order, near-field kernel (engine.py:41-55)."""
+
+    levels: int
+    order: int
+    kernel: KernelKind = KernelKind.POINT_VORTEX
+
+    def validate(self) -> None:
+        validate_config(self)
+
+
+def validate_config(config) -> None:
+    """FmmConfig.validate (engine.py:49-55) for our or the reference's config."""
+    if config.levels < 2:
+        raise ValueError(f"levels must be >= 2, got {config.levels}")
+    if config.order < 0:
+        raise ValueError(f"order must be >= 0, got {config.order}")
+    if config.order > ORDER_CAP:
+        raise ValueError(f"order {config.order} exceeds cap {ORDER_CAP}")
+    if config.levels > _lib.LEVELS_CAP:
+        raise ValueError(f"levels {config.levels} exceeds the GPU tree cap {_lib.LEVELS_CAP}")
+    kernel_code(config.kernel)
+
+
+@dataclass
+class FmmRunStats:
+    """Phase timings (seconds, CUDA events) and exact counters (engine.py:58-74)."""
+
+    n: int
+    levels: int
+    order: int
+    t_build: float = 0.0
+    t_upward: float = 0.0
+    t_m2l: float = 0.0
+    t_downward: float = 0.0
+    t_eval: float = 0.0
+    t_near: float = 0.0
+    t_total: float = 0.0
+    m2l_count: int = 0
+    near_pair_count: int = 0
+    sigma_guard_ok: bool = True
+
+
+class Workspace:
+    """Device scratch for one (n, levels, order) shape, reused across calls."""
+
+    _cache: dict = {}
+
+    def __init__(self, n: int, levels: int, order: int, device: torch.device):
+        self.n, self.levels, self.order, self.device = n, levels, order, device
+        self.nbytes = _lib.workspace_size(n, levels, order)
+        self.buffer = torch.empty(self.nbytes, dtype=torch.uint8, device=device)
+        self.layout = _lib.layout(n, levels, order)
+
+    @property
+    def ptr(self) -> int:
+        return self.buffer.data_ptr()
+
+    @classmethod
+    def get(cls, n: int, levels: int, order: int, device: torch.device) -> "Workspace":
+        key = (device.index, n, levels, order)
+        ws = cls._cache.get(key)
+        if ws is None:
+            if len(cls._cache) >= 2:
+                cls._cache.pop(next(iter(cls._cache)))
+            ws = cls(n, levels, order, device)
+            cls._cache[key] = ws
+        return ws
+
+    # ---- typed views of the internal arrays (parity tests / debugging) ----
+    def view(self, name: str, dtype: torch.dtype, count: int) -> torch.Tensor:
+        off = getattr(self.layout, name)
+        esize = torch.empty(0, dtype=dtype).element_size()
+        return self.buffer[off: off + count * esize].view(dtype)
+
+
+def _bad_indices(x, y, domain) -> np.ndarray:
+    x = x.cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
+    y = y.cpu().numpy() if isinstance(y, torch.Tensor) else np.asarray(y)
+    inside = (x >= domain.xmin) & (x <= domain.xmax) & (y >= domain.ymin) & (y <= domain.ymax)
+    return np.flatnonzero(~inside)
+
+
+def _stats_from(c: _lib.VfmmStats) -> FmmRunStats:
+    return FmmRunStats(
+        n=int(c.n),
+        levels=int(c.levels),
+        order=int(c.order),
+        t_build=c.t_build * 1e-3,
+        t_upward=c.t_upward * 1e-3,
+        t_m2l=c.t_m2l * 1e-3,
+        t_downward=c.t_downward * 1e-3,
+        t_eval=c.t_eval * 1e-3,
+        t_near=c.t_near * 1e-3,
+        t_total=c.t_total * 1e-3,
+        m2l_count=int(c.m2l_count),
+        near_pair_count=int(c.near_pair_count),
+        sigma_guard_ok=bool(c.sigma_guard_ok),
+    )
+
+
+def evaluate_arrays(
+    x,
+    y,
+    gamma,
+    sigma,
+    config,
+    domain=None,
+    *,
+    device=None,
+    overlap: bool = False,
+    out: torch.Tensor | None = None,
+    stacklevel: int = 2,
+):
+    """Array fast path of :func:`evaluate`.
+
+    ``x, y, gamma, sigma`` are length-N numpy arrays or torch tensors (CUDA
+    tensors are used in place).  Returns ``(vel, stats)`` where ``vel`` is a
+    (2, N) float64 CUDA tensor holding u (row 0) and v (row 1) in the input
+    order.  ``overlap=True`` runs the near field concurrently with the
+    far-field chain (phase timings then overlap in time).
+    """
+    validate_config(config)
+    require_cuda()
+    lib = _lib.load()
+    dev = device_of(device, x)
+    xd, yd, gd = (as_device_f64(a, dev) for a in (x, y, gamma))
+    n = int(xd.numel())
+    if n == 0:
+        raise ValueError("need at least one particle")
+    code = kernel_code(config.kernel)
+    sd = as_device_f64(sigma, dev) if code == _lib.KERNEL_GAUSSIAN else None
+    if domain is None:
+        domain = enclosing_domain_of(xd.cpu().numpy(), yd.cpu().numpy())
+    ws = Workspace.get(n, config.levels, config.order, dev)
+    if out is None:
+        out = torch.empty((2, n), dtype=torch.float64, device=dev)
+    st = _lib.VfmmStats()
+    flags = _lib.FLAG_STATS | (_lib.FLAG_OVERLAP if overlap else 0)
+    status = lib.vfmm_evaluate(
+        xd.data_ptr(), yd.data_ptr(), gd.data_ptr(), sd.data_ptr() if sd is not None else None, n,
+        float(domain.xmin), float(domain.ymin), float(domain.side), config.levels, config.order,
+        code, out[0].data_ptr(), out[1].data_ptr(), ws.ptr, ws.nbytes, flags, ctypes.byref(st),
+        stream_ptr(dev),
+    )
+    if status == _lib.VFMM_EDOMAIN:
+        bad = _bad_indices(xd, yd, domain)
+        raise OutOfDomainError(
+            f"{bad.size} particle(s) outside domain {domain}, first indices {bad[:5].tolist()}"
+        )
+    _lib.check(status, "vfmm_evaluate")
+    stats = _stats_from(st)
+    if code == _lib.KERNEL_GAUSSIAN and not st.sigma_guard_ok:
+        warnings.warn(
+            f"max core radius {st.max_sigma:g} exceeds leaf half-width/2 = {st.sigma_guard:g}; "
+            "the far field treats blobs as point vortices, so expect extra error",
+            stacklevel=stacklevel + 1,
+        )
+    return out, stats
+
+
+def evaluate(
+    particles: Sequence,
+    config,
+    domain=None,
+    *,
+    overlap: bool = False,
+) -> tuple[np.ndarray, FmmRunStats]:
+    """Velocity induced at every particle position, with run statistics (engine.py:335-398).
+
+    Returns an (N, 2) float64 array of (u, v) rows in the original particle
+    order.  When no domain is given, the smallest enclosing square is used.
+    """
+    validate_config(config)
+    if len(particles) == 0:
+        raise ValueError("need at least one particle")
+    x, y, gamma, sigma = to_arrays(particles)
+    if domain is None:
+        domain = enclosing_domain_of(x, y)
+    vel, stats = evaluate_arrays(x, y, gamma, sigma, config, domain, overlap=overlap, stacklevel=3)
+    return np.ascontiguousarray(vel.cpu().numpy().T), stats
+
+
+def evaluate_at(targets, particles: Sequence, config, domain=None) -> np.ndarray:
+    """Velocity at arbitrary in-domain target points (engine.py:401-460)."""
+    validate_config(config)
+    x, y, gamma, sigma = to_arrays(particles)
+    if domain is None:
+        domain = enclosing_domain_of(x, y) if len(x) else Domain(0.0, 0.0, 1.0)
+    pts = np.asarray(targets, dtype=np.float64)
+    if pts.ndim != 2 or pts.shape[1] != 2:
+        raise ValueError(f"targets must have shape (M, 2), got {pts.shape}")
+    inside = (
+        (pts[:, 0] >= domain.xmin)
+        & (pts[:, 0] <= domain.xmax)
+        & (pts[:, 1] >= domain.ymin)
+        & (pts[:, 1] <= domain.ymax)
+    )
+    if not inside.all():
+        raise OutOfDomainError(f"{np.count_nonzero(~inside)} target(s) outside domain {domain}")
+    u, v = evaluate_at_arrays(
+        np.ascontiguousarray(pts[:, 0]), np.ascontiguousarray(pts[:, 1]),
+        x, y, gamma, sigma, config, domain,
+    )
+    return np.stack((u.cpu().numpy(), v.cpu().numpy()), axis=1)
+
+
+def evaluate_at_arrays(tx, ty, x, y, gamma, sigma, config, domain, *, device=None):
+    """Device-array form of :func:`evaluate_at`; returns (u, v) CUDA tensors."""
+    validate_config(config)
+    require_cuda()
+    lib = _lib.load()
+    dev = device_of(device, tx, x)
+    txd, tyd = as_device_f64(tx, dev), as_device_f64(ty, dev)
+    m = int(txd.numel())
+    u = torch.zeros(m, dtype=torch.float64, device=dev)
+    v = torch.zeros(m, dtype=torch.float64, device=dev)
+    xd, yd, gd = (as_device_f64(a, dev) for a in (x, y, gamma))
+    n = int(xd.numel())
+    if n == 0 or m == 0:
+        return u, v
+    code = kernel_code(config.kernel)
+    sd = as_device_f64(sigma, dev) if code == _lib.KERNEL_GAUSSIAN else None
+    ws = Workspace.get(n, config.levels, config.order, dev)
+    st = _lib.VfmmStats()
+    status = lib.vfmm_evaluate(
+        xd.data_ptr(), yd.data_ptr(), gd.data_ptr(), sd.data_ptr() if sd is not None else None, n,
+        float(domain.xmin), float(domain.ymin), float(domain.side), config.levels, config.order,
+        code, None, None, ws.ptr, ws.nbytes, _lib.FLAG_STATS | _lib.FLAG_FAR_ONLY,
+        ctypes.byref(st), stream_ptr(dev),
+    )
+    if status == _lib.VFMM_EDOMAIN:
+        bad = _bad_indices(xd, yd, domain)
+        raise OutOfDomainError(
+            f"{bad.size} particle(s) outside domain {domain}, first indices {bad[:5].tolist()}"
+        )
+    _lib.check(status, "vfmm_evaluate(far only)")
+    nbad = ctypes.c_int64(0)
+    status = lib.vfmm_evaluate_at(
+        txd.data_ptr(), tyd.data_ptr(), m, n, float(domain.xmin), float(domain.ymin),
+        float(domain.side), config.levels, config.order, code, u.data_ptr(), v.data_ptr(), ws.ptr,
+        ctypes.byref(nbad), stream_ptr(dev),
+    )
+    if status == _lib.VFMM_EDOMAIN:
+        raise OutOfDomainError(f"{nbad.value} target(s) outside domain {domain}")
+    _lib.check(status, "vfmm_evaluate_at")
+    return u, v

@@ -1,0 +1,81 @@
+"""Input types of the drop-in API: ``Particle``, ``Domain`` and the array helpers.
+
+Mirrors ``vortexfmm.model`` (reference ``model.py:29-65,125-153``): frozen
+value types with the same field names, the closed-square ``Domain`` with
+``xmax = xmin + side``, and the smallest-enclosing-square default domain.
+Objects of the reference package are accepted anywhere these are (duck typed
+on the field names).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from operator import attrgetter
+from typing import Sequence
+
+import numpy as np
+
+
+@dataclass(frozen=True, slots=True)
+class Particle:
+    """One regularised vortex (model.py:29-36)."""
+
+    x: float
+    y: float
+    gamma: float
+    sigma: float
+
+
+@dataclass(frozen=True, slots=True)
+class Domain:
+    """Axis-aligned square ``[xmin, xmin+side] x [ymin, ymin+side]`` (model.py:39-65)."""
+
+    xmin: float
+    ymin: float
+    side: float
+
+    def __post_init__(self) -> None:
+        if not (self.side > 0.0):
+            raise ValueError(f"domain side must be > 0, got {self.side}")
+
+    @property
+    def xmax(self) -> float:
+        return self.xmin + self.side
+
+    @property
+    def ymax(self) -> float:
+        return self.ymin + self.side
+
+    @property
+    def center(self) -> tuple[float, float]:
+        return (self.xmin + 0.5 * self.side, self.ymin + 0.5 * self.side)
+
+    def contains(self, x: float, y: float) -> bool:
+        return self.xmin <= x <= self.xmax and self.ymin <= y <= self.ymax
+
+
+_FIELDS = attrgetter("x", "y", "gamma", "sigma")
+_ROW = np.dtype((np.float64, 4))
+
+
+def to_arrays(particles: Sequence) -> tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray]:
+    """Unpack particles into contiguous (x, y, gamma, sigma) float64 arrays (model.py:125-137)."""
+    n = len(particles)
+    rows = np.fromiter(map(_FIELDS, particles), dtype=_ROW, count=n).reshape(n, 4)
+    cols = np.ascontiguousarray(rows.T)
+    return cols[0], cols[1], cols[2], cols[3]
+
+
+def enclosing_domain_of(x: np.ndarray, y: np.ndarray) -> Domain:
+    """Smallest enclosing square, unit side when degenerate (model.py:140-153)."""
+    xmin = float(np.min(x))
+    ymin = float(np.min(y))
+    side = float(max(np.max(x) - xmin, np.max(y) - ymin))
+    if side <= 0.0:
+        side = 1.0
+    return Domain(xmin, ymin, side)
+
+
+def enclosing_domain(particles: Sequence) -> Domain:
+    x, y, _, _ = to_arrays(particles)
+    return enclosing_domain_of(x, y)

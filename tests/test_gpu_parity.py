@@ -1,0 +1,240 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle.  Bar (BASELINE.json north_star): fp64 velocities
+within 1e-12 of the reference FMM relative to max|v| (the reference's own
+global normalisation, errors.py:64-73), exact m2l_count / near_pair_count, exact
+tree structure, bitwise run-to-run determinism."""
+import math
+import warnings
+
+import numpy as np
+import pytest
+import torch
+
+import paper_0809_1810_b200 as vf
+from paper_0809_1810_b200 import workloads as W
+from paper_0809_1810_b200.engine import Workspace
+from _golden import CASES, DIRECT_CASES, GOLDEN, eval_case, enclosing
+from oracle import fmm_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-12  # north_star: within 1e-12 relative (summation-order differences only)
+G = vf.KernelKind.GAUSSIAN_BLOB
+PT = vf.KernelKind.POINT_VORTEX
+
+
+def run(x, y, g, s, levels, order, gauss, domain, overlap=False):
+    cfg = vf.FmmConfig(levels, order, G if gauss else PT)
+    dom = vf.Domain(*domain) if domain is not None else None
+    with warnings.catch_warnings(record=True) as rec:
+        warnings.simplefilter("always")
+        vel, st = vf.evaluate_arrays(x, y, g, s, cfg, dom, overlap=overlap)
+    return vel.cpu().numpy().T.copy(), st, rec
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_evaluate_matches_reference_golden(name):
+    c = eval_case(name)
+    vel, st, rec = run(c["x"], c["y"], c["gamma"], c["sigma"], c["levels"], c["order"], c["gauss"],
+                       c["domain"] or enclosing(c["x"], c["y"]))
+    assert st.m2l_count == c["m2l_count"]
+    assert st.near_pair_count == c["near_pair_count"]
+    assert st.sigma_guard_ok == c["sigma_guard_ok"]
+    if not c["sigma_guard_ok"]:
+        assert any("core radius" in str(w.message) for w in rec)
+    got = vel if c["sample"] is None else vel[c["sample"]]
+    ref = c["vel"]
+    if c["vmax"] == 0.0:
+        assert np.all(got == 0.0)
+    else:
+        err = np.abs(got - ref).max() / c["vmax"]
+        assert err <= REL_TOL, f"{name}: max rel err {err:.3e}"
+
+
+@pytest.mark.parametrize("name", ["config0", "config1", "big_leaf_l3", "cluster_corner_l4", "boundary_edges"])
+def test_tree_structure_exact(name):
+    """Stable leaf permutation, leaf starts and per-level counts equal the oracle bit for bit."""
+    c = eval_case(name)
+    dom = c["domain"] or enclosing(c["x"], c["y"])
+    run(c["x"], c["y"], c["gamma"], c["sigma"], c["levels"], c["order"], c["gauss"], dom)
+    n, lv, p = c["x"].size, c["levels"], c["order"]
+    ws = Workspace.get(n, lv, p, torch.device("cuda", torch.cuda.current_device()))
+    tree = O.Tree(O.leaf_keys(c["x"], c["y"], lv, *dom), lv, *dom)
+    perm = ws.view("perm", torch.int32, n).cpu().numpy()
+    keys = ws.view("leaf_key", torch.int32, n).cpu().numpy()
+    starts = ws.view("leaf_starts", torch.int32, 4**lv + 1).cpu().numpy()
+    assert np.array_equal(perm, tree.order)
+    assert np.array_equal(keys, tree.sorted_leaf)
+    assert np.array_equal(starts, tree.leaf_starts)
+    counts = ws.view("counts", torch.int32, sum(4**k for k in range(lv + 1))).cpu().numpy()
+    off = 0
+    for k in range(lv + 1):
+        assert np.array_equal(counts[off: off + 4**k], tree.counts[k])
+        off += 4**k
+
+
+def _unscale(ws, c, dom):
+    """GPU multipoles/locals converted back to the reference convention."""
+    n, lv, p = c["x"].size, c["levels"], c["order"]
+    P = p + 1
+    cells = sum(4**k for k in range(2, lv + 1))
+    mult = ws.view("mult", torch.float64, cells * P * 2).cpu().numpy().reshape(-1, 2)
+    loc = ws.view("loc", torch.float64, cells * P * 2).cpu().numpy().reshape(-1, 2)
+    mult = (mult[:, 0] + 1j * mult[:, 1]).reshape(cells, P)
+    loc = (loc[:, 0] + 1j * loc[:, 1]).reshape(cells, P)
+    fact = np.array([math.factorial(k) for k in range(P)], dtype=np.float64)
+    out_m, out_l, off = {}, {}, 0
+    for k in range(2, lv + 1):
+        r = dom[2] / 2**k
+        kk = np.arange(P)
+        out_m[k] = mult[off: off + 4**k] * (r ** (kk + 1) * fact)[None, :]
+        out_l[k] = loc[off: off + 4**k] * (((-1.0) ** kk) / (fact * r**kk))[None, :]
+        off += 4**k
+    return out_m, out_l
+
+
+@pytest.mark.parametrize("name", ["config1", "gauss_patch5000_l6_p4", "cluster_corner_l4"])
+def test_expansions_match_oracle(name):
+    """Every level's multipole and (completed) local coefficients vs the oracle."""
+    c = eval_case(name)
+    dom = c["domain"] or enclosing(c["x"], c["y"])
+    run(c["x"], c["y"], c["gamma"], c["sigma"], c["levels"], c["order"], c["gauss"], dom)
+    ws = Workspace.get(c["x"].size, c["levels"], c["order"], torch.device("cuda", torch.cuda.current_device()))
+    _, st = O.evaluate(c["x"], c["y"], c["gamma"], c["sigma"], c["levels"], c["order"], c["gauss"], dom)
+    gm, gl = _unscale(ws, c, dom)
+    for k in range(2, c["levels"] + 1):
+        om, ol = st["mult"][k], st["loc"][k]
+        sm = np.abs(om).max(axis=0) + 1e-300
+        sl = np.abs(ol).max(axis=0) + 1e-300
+        assert (np.abs(gm[k] - om) / sm).max() <= 1e-12, f"mult level {k}"
+        assert (np.abs(gl[k] - ol) / sl).max() <= 1e-11, f"loc level {k}"
+
+
+@pytest.mark.parametrize("name", ["config0", "config1", "coincident", "big_leaf_l3", "point_kernel_l5"])
+def test_near_field_matches_oracle(name):
+    c = eval_case(name)
+    dom = c["domain"] or enclosing(c["x"], c["y"])
+    run(c["x"], c["y"], c["gamma"], c["sigma"], c["levels"], c["order"], c["gauss"], dom)
+    n = c["x"].size
+    ws = Workspace.get(n, c["levels"], c["order"], torch.device("cuda", torch.cuda.current_device()))
+    near = ws.view("near_uv", torch.float64, 2 * n).cpu().numpy().reshape(n, 2)
+    _, st = O.evaluate(c["x"], c["y"], c["gamma"], c["sigma"], c["levels"], c["order"], c["gauss"], dom)
+    ref = st["near_sorted"]
+    assert np.abs(near - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("overlap", [False, True])
+def test_bitwise_determinism(overlap):
+    w = W.config1()
+    a, s1, _ = run(w.x, w.y, w.gamma, w.sigma, w.levels, w.order, True, W.DOMAIN, overlap=overlap)
+    b, s2, _ = run(w.x, w.y, w.gamma, w.sigma, w.levels, w.order, True, W.DOMAIN, overlap=not overlap)
+    assert np.array_equal(a, b)
+    assert s1.m2l_count == s2.m2l_count and s1.near_pair_count == s2.near_pair_count
+
+
+def test_drop_in_api_and_errors():
+    parts = [vf.Particle(0.4, 0.6, 2.0, 0.01)]
+    vel, st = vf.evaluate(parts, vf.FmmConfig(3, 6), vf.Domain(0.0, 0.0, 1.0))
+    assert vel.shape == (1, 2) and np.all(vel == 0.0) and st.n == 1
+    with pytest.raises(ValueError):
+        vf.evaluate([], vf.FmmConfig(3, 4))
+    bad = [vf.Particle(0.5, 0.5, 1.0, 0.01), vf.Particle(1.5, 0.5, 1.0, 0.01), vf.Particle(0.2, -0.1, 1.0, 0.01)]
+    with pytest.raises(vf.OutOfDomainError, match=r"2 particle\(s\) outside domain .* first indices \[1, 2\]"):
+        vf.evaluate(bad, vf.FmmConfig(3, 4), vf.Domain(0.0, 0.0, 1.0))
+    with pytest.warns(UserWarning, match="core radius"):
+        vf.evaluate([vf.Particle(0.5, 0.5, 1.0, 0.3), vf.Particle(0.6, 0.5, 1.0, 0.3)],
+                    vf.FmmConfig(3, 4, G), vf.Domain(0.0, 0.0, 1.0))
+    # stats contract of test_engine.py:272-285
+    rng = np.random.default_rng(4)
+    parts = [vf.Particle(float(a), float(b), float(c), 0.005) for a, b, c in rng.uniform(0, 1, (512, 3))]
+    vel, st = vf.evaluate(parts, vf.FmmConfig(3, 6), vf.Domain(0.0, 0.0, 1.0))
+    phases = st.t_build + st.t_upward + st.t_m2l + st.t_downward + st.t_eval + st.t_near
+    assert st.t_total >= 0.95 * phases and st.t_total > 0
+    assert st.m2l_count <= 27 * 4**3 and len(vel) == 512
+
+
+@pytest.mark.parametrize("name", DIRECT_CASES)
+def test_direct_matches_reference_golden(name):
+    pre = f"direct/{name}/"
+    tg = GOLDEN[pre + "targets"]
+    if pre + "x" in GOLDEN:
+        x, y, g, s = (GOLDEN[pre + k] for k in ("x", "y", "gamma", "sigma"))
+    else:
+        w = W.config0()
+        x, y, g, s = w.x, w.y, w.gamma, w.sigma
+    kind = G if int(GOLDEN[pre + "kind"]) else PT
+    u, v = vf.velocity_direct_arrays(np.ascontiguousarray(tg[:, 0]), np.ascontiguousarray(tg[:, 1]), x, y, g, s, kind)
+    got = np.stack((u.cpu().numpy(), v.cpu().numpy()), axis=1)
+    ref = GOLDEN[pre + "vel"]
+    assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_direct_reference_signature():
+    parts = [vf.Particle(0.0, 0.0, 2 * math.pi, 1.0)]
+    vel = vf.velocity_direct([(1.0, 0.0)], parts, G)
+    assert vel[0, 0] == 0.0 and abs(vel[0, 1] - 0.3934693402873666) <= 1e-15
+    vel = vf.velocity_direct([(1.0, 0.0)], [vf.Particle(0.0, 0.0, 2 * math.pi, 0.1)], PT)
+    assert abs(vel[0, 1] - 1.0) <= 1e-15 and vel[0, 0] == 0.0
+
+
+@pytest.mark.parametrize("gauss", [False, True])
+def test_evaluate_at_matches_reference_golden(gauss):
+    key = "at/grid_gauss/" if gauss else "at/grid/"
+    x, y, g, s = (GOLDEN["at/grid/" + k] for k in ("x", "y", "gamma", "sigma"))
+    tg = GOLDEN[key + "targets"]
+    parts = [vf.Particle(*map(float, r)) for r in zip(x, y, g, s)]
+    got = vf.evaluate_at(tg, parts, vf.FmmConfig(3, 20, G if gauss else PT), vf.Domain(0.0, 0.0, 1.0))
+    ref = GOLDEN[key + "vel"]
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+    with pytest.raises(vf.OutOfDomainError):
+        vf.evaluate_at([(1.5, 0.5)], parts, vf.FmmConfig(2, 4), vf.Domain(0.0, 0.0, 1.0))
+
+
+# ---------------------------------------------------------------- full sizes
+def _sampled_direct_check(w, vel, k=128, seed=0):
+    """GPU direct sum at sampled targets == oracle direct (summation order only),
+    and FMM close to the direct sum (truncation error only)."""
+    sel = np.sort(np.random.default_rng(seed).choice(w.n, k, replace=False))
+    u, v = vf.velocity_direct_arrays(w.x[sel], w.y[sel], w.x, w.y, w.gamma, w.sigma, G)
+    gd = np.stack((u.cpu().numpy(), v.cpu().numpy()), axis=1)
+    od = O.direct_blocked(w.x[sel], w.y[sel], w.x, w.y, w.gamma, w.sigma, True, block=1 << 16)
+    vmax = np.abs(od).max()
+    assert np.abs(gd - od).max() <= 1e-12 * vmax
+    return np.abs(vel[sel] - gd).max() / vmax
+
+
+def test_config2_full_size_properties():
+    w = W.config2()
+    vel, st, _ = run(w.x, w.y, w.gamma, w.sigma, w.levels, w.order, True, W.DOMAIN)
+    assert st.m2l_count == 568_872 and st.near_pair_count == 596_656_128
+    fmm_err = _sampled_direct_check(w, vel)
+    assert fmm_err <= 1e-6
+    # exact circulation scaling (every operation is linear in gamma)
+    v2, _, _ = run(w.x, w.y, 2.0 * w.gamma, w.sigma, w.levels, w.order, True, W.DOMAIN)
+    assert np.array_equal(v2, 2.0 * vel)
+    # linearity and permutation invariance to round-off
+    g1 = w.gamma * np.cos(3 * w.x)
+    va, _, _ = run(w.x, w.y, g1, w.sigma, w.levels, w.order, True, W.DOMAIN)
+    vb, _, _ = run(w.x, w.y, w.gamma - g1, w.sigma, w.levels, w.order, True, W.DOMAIN)
+    vmax = np.abs(vel).max()
+    assert np.abs(va + vb - vel).max() <= 1e-13 * vmax
+    perm = np.random.default_rng(5).permutation(w.n)
+    vp, _, _ = run(w.x[perm], w.y[perm], w.gamma[perm], w.sigma[perm], w.levels, w.order, True, W.DOMAIN)
+    assert np.abs(vp - vel[perm]).max() <= 1e-13 * vmax
+
+
+@pytest.mark.slow
+def test_config2_full_size_oracle_parity():
+    w = W.config2()
+    vel, st, _ = run(w.x, w.y, w.gamma, w.sigma, w.levels, w.order, True, W.DOMAIN)
+    ov, ost = O.evaluate(w.x, w.y, w.gamma, w.sigma, w.levels, w.order, True, W.DOMAIN)
+    assert st.m2l_count == ost["m2l_count"] and st.near_pair_count == ost["near_pair_count"]
+    assert np.abs(vel - ov).max() <= REL_TOL * np.abs(ov).max()
+
+
+@pytest.mark.slow
+def test_config3_full_size_counts_and_sampled_direct():
+    w = W.config3()
+    vel, st, _ = run(w.x, w.y, w.gamma, w.sigma, w.levels, w.order, True, W.DOMAIN)
+    assert st.m2l_count == 9_351_840 and st.near_pair_count == 9_638_451_922
+    assert _sampled_direct_check(w, vel, k=24) <= 1e-6
