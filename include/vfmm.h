@@ -75,7 +75,7 @@ typedef struct vfmm_layout {
     size_t leaf_key;      /* int32 [n]       Tree.sorted_leaf (row-major leaf key) */
     size_t leaf_starts;   /* int32 [4^l+1]   Tree.leaf_starts */
     size_t sources;       /* double4 [n]     (x, y, gamma, -1/(2 sigma^2 ln2)) sorted */
-    size_t near_uv;       /* double2 [n]     near-field (u, v), sorted order */
+    size_t near_uv;       /* double2 [3][n]  near-field (u, v) partial sums per neighbourhood row, sorted order */
     size_t mult;          /* double2 [sum_{k=2..l} 4^k (p+1)]  scaled multipoles, level 2 first */
     size_t loc;           /* double2 [same]  scaled locals, level 2 first */
     size_t counts;        /* int32  [sum_{k=0..l} 4^k] per-level occupancy, level 0 first */

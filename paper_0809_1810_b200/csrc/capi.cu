@@ -75,7 +75,8 @@ void build_tables(Tables* t) {
     }
     for (int j = 0; j < kOrderCap + 16; ++j) t->invfact[j] = (double)(1.0L / fact[j]);
     for (int j = 0; j < 2 * kOrderCap + 16; ++j) t->pow2neg[j] = std::ldexp(1.0, -j);
-    for (int j = 0; j < 32; ++j) t->exp2tab[j] = (double)exp2l((long double)j / 32.0L);
+    for (int j = 0; j < kExpTabN; ++j)
+        t->exp2tab[j] = (double)exp2l((long double)(j - (kExpTabN - 1)) / (long double)kExpSteps);
 }
 
 int current_device_of(const void* p, int* dev) {
@@ -210,7 +211,7 @@ bool make_layout(int64_t n, int levels, int order, Layout* L) {
     L->task_scratch = take(sizeof(int) * L->nleaves);
     L->scan_aux = take(sizeof(int) * L->scan_aux_elems);
     L->src = take(sizeof(Src) * n);
-    L->near_uv = take(sizeof(double2) * n);
+    L->near_uv = take(sizeof(double2) * n * kNearRows);
     L->leaf_starts = take(sizeof(int) * (L->nleaves + 1));
     L->counts = take(sizeof(int) * cc);
     L->mult = take(sizeof(double2) * cells * L->P);

@@ -88,7 +88,9 @@ __global__ void __launch_bounds__(256)
     const Src s = src[i];
     const double2 f =
         eval_local(loc + (int64_t)leaf * P, P, (s.x - cx) * inv_r, (s.y - cy) * inv_r, sfact);
-    const double2 nv = near_uv[i];
+    // near field = the three neighbourhood-row partial sums, in row order
+    const double2 n0 = near_uv[i], n1 = near_uv[n + i], n2 = near_uv[2 * n + i];
+    const double2 nv = make_double2((n0.x + n1.x) + n2.x, (n0.y + n1.y) + n2.y);
     // f_to_velocity: u = Im f / 2pi, v = Re f / 2pi; then far + near
     const int o = perm[i];
     u[o] = f.y * kInv2Pi + nv.x;
@@ -105,9 +107,9 @@ __global__ void __launch_bounds__(256)
               double side, const Tables* __restrict__ T, double* __restrict__ u,
               double* __restrict__ v, Counters* ctr) {
     __shared__ double sfact[kOrderCap + 16];
-    __shared__ double stab[32];
+    __shared__ double sexp[kExpTab];
     for (int i = threadIdx.x; i < P; i += blockDim.x) sfact[i] = T->invfact[i];
-    for (int i = threadIdx.x; i < 32; i += blockDim.x) stab[i] = T->exp2tab[i];
+    const double* stab = stage_exp_table(sexp, T->exp2tab);
     __syncthreads();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= mt) return;

@@ -12,6 +12,8 @@
 // streamed through shared memory in tiles shared by the warps of the block
 // that work on the same leaf, otherwise read as warp-uniform (broadcast)
 // loads through L1.  The 1/(2 pi) factor is applied once per target.
+#include <cstdlib>
+
 #include "vfmm_internal.cuh"
 
 namespace vfmm {
@@ -19,57 +21,106 @@ namespace vfmm {
 namespace {
 
 constexpr int kP2PWarps = 8;
+constexpr int kP2PBlocksPerSM = 4;
+
+// One lane's targets against one contiguous source slice [a, b).
+template <bool GAUSS>
+__device__ __forceinline__ void slice_1(const Src* __restrict__ src, int a, int b, double tx,
+                                        double ty, const double* __restrict__ tab, double& u,
+                                        double& v) {
+    int j = a;
+    for (; j + 4 <= b; j += 4) {
+        const Src s0 = src[j], s1 = src[j + 1], s2 = src[j + 2], s3 = src[j + 3];
+        pair_acc<GAUSS>(tx, ty, s0.x, s0.y, s0.g, s0.q2, tab, u, v);
+        pair_acc<GAUSS>(tx, ty, s1.x, s1.y, s1.g, s1.q2, tab, u, v);
+        pair_acc<GAUSS>(tx, ty, s2.x, s2.y, s2.g, s2.q2, tab, u, v);
+        pair_acc<GAUSS>(tx, ty, s3.x, s3.y, s3.g, s3.q2, tab, u, v);
+    }
+    for (; j < b; ++j) {
+        const Src s0 = src[j];
+        pair_acc<GAUSS>(tx, ty, s0.x, s0.y, s0.g, s0.q2, tab, u, v);
+    }
+}
 
 template <bool GAUSS>
-__global__ void __launch_bounds__(kP2PWarps * 32)
+__device__ __forceinline__ void slice_2(const Src* __restrict__ src, int a, int b, double tx0,
+                                        double ty0, double tx1, double ty1,
+                                        const double* __restrict__ tab, double& u0, double& v0,
+                                        double& u1, double& v1) {
+    int j = a;
+    for (; j + 2 <= b; j += 2) {
+        const Src s0 = src[j], s1 = src[j + 1];
+        pair_acc<GAUSS>(tx0, ty0, s0.x, s0.y, s0.g, s0.q2, tab, u0, v0);
+        pair_acc<GAUSS>(tx1, ty1, s0.x, s0.y, s0.g, s0.q2, tab, u1, v1);
+        pair_acc<GAUSS>(tx0, ty0, s1.x, s1.y, s1.g, s1.q2, tab, u0, v0);
+        pair_acc<GAUSS>(tx1, ty1, s1.x, s1.y, s1.g, s1.q2, tab, u1, v1);
+    }
+    if (j < b) {
+        const Src s0 = src[j];
+        pair_acc<GAUSS>(tx0, ty0, s0.x, s0.y, s0.g, s0.q2, tab, u0, v0);
+        pair_acc<GAUSS>(tx1, ty1, s0.x, s0.y, s0.g, s0.q2, tab, u1, v1);
+    }
+}
+
+// Persistent grid; warps pull (task, neighbourhood row) work items from a
+// global cursor (dynamic balance; every item's arithmetic is fixed, so results
+// do not depend on which warp runs it).  A task is 32*TPT consecutive targets
+// of one leaf, TPT per lane (each loaded source feeds TPT pairs).  Row dy of
+// the 3x3 neighbourhood is one contiguous slice of the sorted sources; its
+// partial sums go to near_uv[dy + 1][i] and are added in row order by the
+// combine kernel.
+template <bool GAUSS, int TPT>
+__global__ void __launch_bounds__(kP2PWarps * 32, kP2PBlocksPerSM)
     k_p2p(const Src* __restrict__ src, const int* __restrict__ ls, const int2* __restrict__ tasks,
-          const Counters* __restrict__ ctr_in, int levels, const Tables* __restrict__ T,
+          Counters* __restrict__ ctr, int levels, int64_t n, const Tables* __restrict__ T,
           double2* __restrict__ near_uv, unsigned long long* __restrict__ pairs) {
-    __shared__ double stab[32];
-    if (threadIdx.x < 32) stab[threadIdx.x] = T->exp2tab[threadIdx.x];
+    __shared__ double sexp[kExpTab];
+    const double* tab = stage_exp_table(sexp, T->exp2tab);
     __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int task = blockIdx.x * kP2PWarps + warp;
-    if (task >= ctr_in->ntasks) return;
-    const int2 tk = tasks[task];
-    const int leaf = tk.x;
+    const int lane = threadIdx.x & 31;
+    const int nitems = ctr->ntasks * kNearRows;
     const int m = 1 << levels;
-    const int lo = ls[leaf], hi = ls[leaf + 1];
-    const int i = lo + tk.y + lane;
-    const bool active = i < hi;
-    double tx = 0.0, ty = 0.0;
-    if (active) {
-        const Src t = src[i];
-        tx = t.x;
-        ty = t.y;
-    }
-    const int cx = leaf % m, cy = leaf / m;
-    const int xlo = cx > 0 ? cx - 1 : 0, xhi = cx < m - 1 ? cx + 1 : m - 1;
-    double u = 0.0, v = 0.0;
-    int nsrc = 0;
-    for (int ny = cy - 1; ny <= cy + 1; ++ny) {
-        if (ny < 0 || ny >= m) continue;
-        const int a = ls[(int64_t)ny * m + xlo], b = ls[(int64_t)ny * m + xhi + 1];
-        nsrc += b - a;
-        int j = a;
-        for (; j + 4 <= b; j += 4) {
-            const Src s0 = src[j], s1 = src[j + 1], s2 = src[j + 2], s3 = src[j + 3];
-            pair_acc<GAUSS>(tx, ty, s0.x, s0.y, s0.g, s0.q2, stab, u, v);
-            pair_acc<GAUSS>(tx, ty, s1.x, s1.y, s1.g, s1.q2, stab, u, v);
-            pair_acc<GAUSS>(tx, ty, s2.x, s2.y, s2.g, s2.q2, stab, u, v);
-            pair_acc<GAUSS>(tx, ty, s3.x, s3.y, s3.g, s3.q2, stab, u, v);
+    long long my_pairs = 0;
+    for (;;) {
+        int item = 0;
+        if (lane == 0) item = atomicAdd(&ctr->task_cursor, 1);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= nitems) break;
+        const int row = item % kNearRows;
+        const int2 tk = tasks[item / kNearRows];
+        const int leaf = tk.x;
+        const int lo = ls[leaf], hi = ls[leaf + 1];
+        const int i0 = lo + tk.y + lane, i1 = i0 + 32;
+        const bool act0 = i0 < hi, act1 = TPT == 2 && i1 < hi;
+        double tx0 = 0.0, ty0 = 0.0, tx1 = 0.0, ty1 = 0.0;
+        if (act0) {
+            const double2 t = *reinterpret_cast<const double2*>(&src[i0]);
+            tx0 = t.x;
+            ty0 = t.y;
         }
-        for (; j < b; ++j) {
-            const Src s0 = src[j];
-            pair_acc<GAUSS>(tx, ty, s0.x, s0.y, s0.g, s0.q2, stab, u, v);
+        if (act1) {
+            const double2 t = *reinterpret_cast<const double2*>(&src[i1]);
+            tx1 = t.x;
+            ty1 = t.y;
         }
+        const int cx = leaf & (m - 1), cy = leaf >> levels;
+        const int ny = cy + row - 1;
+        double u0 = 0.0, v0 = 0.0, u1 = 0.0, v1 = 0.0;
+        if (ny >= 0 && ny < m) {
+            const int xlo = cx > 0 ? cx - 1 : 0, xhi = cx < m - 1 ? cx + 1 : m - 1;
+            const int a = ls[(int64_t)ny * m + xlo], b = ls[(int64_t)ny * m + xhi + 1];
+            if (TPT == 2 && __any_sync(0xffffffffu, act1))
+                slice_2<GAUSS>(src, a, b, tx0, ty0, tx1, ty1, tab, u0, v0, u1, v1);
+            else
+                slice_1<GAUSS>(src, a, b, tx0, ty0, tab, u0, v0);
+            // engine.py:284: pairs += n_leaf * (n_nbhd - 1), split over tasks and rows
+            const long long cnt = min(32 * TPT, hi - lo - tk.y);
+            my_pairs += cnt * (long long)(b - a) - (row == 1 ? cnt : 0);
+        }
+        if (act0) near_uv[(int64_t)row * n + i0] = make_double2(u0 * kInv2Pi, v0 * kInv2Pi);
+        if (act1) near_uv[(int64_t)row * n + i1] = make_double2(u1 * kInv2Pi, v1 * kInv2Pi);
     }
-    if (active) near_uv[i] = make_double2(u * kInv2Pi, v * kInv2Pi);
-    if (lane == 0) {
-        // engine.py:284: pairs += n_leaf * (n_nbhd - 1), split over the leaf's tasks
-        const int cnt = min(32, hi - lo - tk.y);
-        atomicAdd(pairs, (unsigned long long)cnt * (unsigned long long)(nsrc - 1));
-    }
+    if (lane == 0 && my_pairs) atomicAdd(pairs, (unsigned long long)my_pairs);
 }
 
 // Direct sum: one thread per target, sources in ascending index order through
@@ -86,8 +137,8 @@ __global__ void __launch_bounds__(kDirThreads)
              int64_t slice_len, const Tables* __restrict__ T, double* __restrict__ pu,
              double* __restrict__ pv) {
     __shared__ Src tile[kDirThreads];
-    __shared__ double stab[32];
-    if (threadIdx.x < 32) stab[threadIdx.x] = T->exp2tab[threadIdx.x];
+    __shared__ double sexp[kExpTab];
+    const double* stab = stage_exp_table(sexp, T->exp2tab);
     const int64_t i = (int64_t)blockIdx.x * kDirThreads + threadIdx.x;
     const int slice = blockIdx.y;
     const int64_t s0 = (int64_t)slice * slice_len;
@@ -144,15 +195,31 @@ __global__ void k_direct_reduce(const double* __restrict__ pu, const double* __r
 
 }  // namespace
 
+int p2p_targets_per_lane() {
+    static int tpt = 0;
+    if (!tpt) {
+        const char* e = getenv("VFMM_P2P_TPT");
+        tpt = (e && e[0] == '1') ? 1 : 2;
+    }
+    return tpt;
+}
+
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
                 const int2* tasks, Counters* ctr, int kernel, double2* near_uv, cudaStream_t s) {
-    const unsigned blocks = (unsigned)((L.max_tasks + kP2PWarps - 1) / kP2PWarps);
-    if (kernel == VFMM_KERNEL_GAUSSIAN)
-        k_p2p<true><<<blocks, kP2PWarps * 32, 0, s>>>(src, leaf_starts, tasks, ctr, L.levels, T,
-                                                      near_uv, &ctr->near_pairs);
-    else
-        k_p2p<false><<<blocks, kP2PWarps * 32, 0, s>>>(src, leaf_starts, tasks, ctr, L.levels, T,
-                                                       near_uv, &ctr->near_pairs);
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const size_t need = (L.max_tasks * kNearRows + kP2PWarps - 1) / kP2PWarps;
+    const size_t cap = (size_t)num_sms * kP2PBlocksPerSM;
+    const unsigned blocks = (unsigned)(need < cap ? need : cap);
+    const bool g = kernel == VFMM_KERNEL_GAUSSIAN;
+    auto* fn = p2p_targets_per_lane() == 2 ? (g ? k_p2p<true, 2> : k_p2p<false, 2>)
+                                           : (g ? k_p2p<true, 1> : k_p2p<false, 1>);
+    fn<<<blocks, kP2PWarps * 32, 0, s>>>(src, leaf_starts, tasks, ctr, L.levels, L.n, T, near_uv,
+                                         &ctr->near_pairs);
     note_launches(1);
 }
 

@@ -236,21 +236,22 @@ __global__ void k_counts(const int* __restrict__ ls, int levels, int64_t total_c
     counts[t] = c;
 }
 
-__global__ void k_tasks_count(const int* __restrict__ ls, int nleaves, int* __restrict__ nt) {
+__global__ void k_tasks_count(const int* __restrict__ ls, int nleaves, int chunk,
+                              int* __restrict__ nt) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nleaves) return;
     const int c = ls[i + 1] - ls[i];
-    nt[i] = (c + 31) >> 5;
+    nt[i] = (c + chunk - 1) / chunk;
 }
 
-__global__ void k_tasks_fill(const int* __restrict__ ls, int nleaves, const int* __restrict__ off,
-                             int2* __restrict__ tasks, Counters* ctr) {
+__global__ void k_tasks_fill(const int* __restrict__ ls, int nleaves, int chunk,
+                             const int* __restrict__ off, int2* __restrict__ tasks, Counters* ctr) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nleaves) return;
     const int c = ls[i + 1] - ls[i];
-    const int nt = (c + 31) >> 5;
+    const int nt = (c + chunk - 1) / chunk;
     const int o = off[i];
-    for (int t = 0; t < nt; ++t) tasks[o + t] = make_int2(i, 32 * t);
+    for (int t = 0; t < nt; ++t) tasks[o + t] = make_int2(i, chunk * t);
     if (i == nleaves - 1) ctr->ntasks = o + nt;
 }
 
@@ -261,6 +262,7 @@ __global__ void k_init_counters(Counters* ctr) {
     ctr->bad_count = 0;
     ctr->first_bad = INT_MAX;
     ctr->ntasks = 0;
+    ctr->task_cursor = 0;
 }
 
 inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
@@ -340,10 +342,12 @@ void launch_counts(const Layout& L, const int* leaf_starts, int* counts, cudaStr
 void launch_tasks(const Layout& L, const int* leaf_starts, int* task_scratch, int2* tasks,
                   int* aux, Counters* ctr, cudaStream_t s) {
     const int nl = (int)L.nleaves;
-    k_tasks_count<<<grid_for(nl, 256), 256, 0, s>>>(leaf_starts, nl, task_scratch);
+    k_tasks_count<<<grid_for(nl, 256), 256, 0, s>>>(leaf_starts, nl, 32 * p2p_targets_per_lane(),
+                                                  task_scratch);
     note_launches(1);
     launch_scan_i32(task_scratch, nl, aux, s);
-    k_tasks_fill<<<grid_for(nl, 256), 256, 0, s>>>(leaf_starts, nl, task_scratch, tasks, ctr);
+    k_tasks_fill<<<grid_for(nl, 256), 256, 0, s>>>(leaf_starts, nl, 32 * p2p_targets_per_lane(),
+                                                 task_scratch, tasks, ctr);
     note_launches(1);
 }
 

@@ -24,6 +24,9 @@ namespace vfmm {
 constexpr int kOrderCap = VFMM_ORDER_CAP;
 constexpr int kQMax = 2 * kOrderCap + 16;  // H table length (padded for m-chunks)
 constexpr int kOffsets = 49;               // 7x7 offset grid (dy+3)*7 + (dx+3)
+constexpr int kExpSteps = 64;              // exp table resolution: 2^(n/64)
+constexpr int kExpTabN = 60 * kExpSteps + 1;  // exp table entries, n = -3840..0
+constexpr int kNearRows = 3;               // P2P partial sums: one per neighbourhood row
 
 // Packed per-particle source record in leaf-sorted order: x, y, gamma and
 // q2 = -1 / (2 sigma^2 ln 2) so that exp(-r^2/(2 sigma^2)) = 2^(r^2 q2).
@@ -39,7 +42,7 @@ struct Counters {
     int bad_count;
     int first_bad;
     int ntasks;
-    int pad;
+    int task_cursor;  // dynamic P2P work distribution
 };
 
 // Translation tables (device globals, uploaded once per device).
@@ -49,7 +52,7 @@ struct Tables {
     double2 F[4][kOrderCap + 16];    // L2L
     double invfact[kOrderCap + 16];
     double pow2neg[2 * kOrderCap + 16];  // 2^-k
-    double exp2tab[32];              // 2^(j/32)
+    double exp2tab[kExpTabN];        // 2^(n/64), n = -3840..0
 };
 
 const Tables* device_tables();   // device pointer (uploaded on first use)
@@ -93,6 +96,7 @@ void launch_m2m(const Layout& L, const Tables* T, double2* mult, cudaStream_t s)
 void launch_m2l(const Layout& L, const Tables* T, const double2* mult, const int* counts,
                 double2* loc, Counters* ctr, cudaStream_t s);
 void launch_l2l(const Layout& L, const Tables* T, double2* loc, cudaStream_t s);
+int p2p_targets_per_lane();  // 1 or 2 (env VFMM_P2P_TPT, default 2)
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
                 const int2* tasks, Counters* ctr, int kernel, double2* near_uv, cudaStream_t s);
 void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const int* keys,
@@ -116,30 +120,58 @@ __device__ __forceinline__ double cell_center(double lo, int i, double s) {
 
 // ---- shared device math ----
 
-// e = 2^y for y in [-60, 0] (callers clamp), table-driven: 2^(j/32) * 2^k * 2^r
-// with |r| <= 1/64 and a degree-6 Taylor polynomial of 2^r = e^(r ln2).
-// Truncation error (ln2/64)^7/7! < 4e-18 relative; total error ~1 ulp.
-__device__ __forceinline__ double exp2_neg(double y, const double* __restrict__ tab) {
+// Exponential table: 2^(n/64) for n = -3840..0 (y in [-60, 0]); kernels stage
+// it in shared memory (30 KB) and pass a pointer to the n = 0 entry (the last).
+constexpr int kExpTab = kExpTabN;
+
+// Clamp y <= 0 to y >= -60 with ONE integer op: for non-positive doubles the
+// unsigned high word grows with |y|, so min(hi(y), hi(-60)) caps |y| near 60
+// (the low word is kept; the result lies in [-60 - 1e-14, -60] when clamped).
+// Below -54, 2^y < 2^-54 and 1 - 2^y rounds to 1.0 exactly, as in the reference.
+__device__ __forceinline__ double clamp_neg60(double y) {
+    const unsigned hi = min((unsigned)__double2hiint(y), 0xC04E0000u);
+    return __hiloint2double((int)hi, __double2loint(y));
+}
+
+// Taylor coefficients ln2^k / k!, k = 1..5, in the constant bank so that the
+// DFMAs take them as c[][] operands (no per-iteration register moves).
+static __constant__ double c_exp2_poly[5] = {6.931471805599453e-1, 2.4022650695910072e-1,
+                                             5.550410866482158e-2, 9.618129107628477e-3,
+                                             1.3333558146428443e-3};
+
+// e = 2^y for y in [-60, 0]: n = round(64 y) via the 1.5*2^52 shifter,
+// r = y - n/64 (exact, |r| <= 1/128), 2^y = T[n] * (1 + r P(r)) with the
+// degree-5 Taylor polynomial of 2^r = e^(r ln2).  Truncation error
+// (ln2/128)^6/6! < 3.6e-17 relative (0.32 ulp); total error ~1 ulp.
+// Returns (T, r P(r)) so the caller can fold 1 - e into one FMA.
+__device__ __forceinline__ double exp2_neg_parts(double y, const double* __restrict__ tab_end,
+                                                 double& T) {
     const double kShift = 6755399441055744.0;  // 1.5 * 2^52
-    double t = fma(y, 32.0, kShift);
-    int n = __double2loint(t);
-    double nf = t - kShift;
-    double r = fma(nf, -0.03125, y);  // exact
-    // coefficients ln2^k / k!, k = 1..6
-    double p = 1.540353039338161e-4;
-    p = fma(p, r, 1.3333558146428443e-3);
-    p = fma(p, r, 9.618129107628477e-3);
-    p = fma(p, r, 5.550410866482158e-2);
-    p = fma(p, r, 2.4022650695910072e-1);
-    p = fma(p, r, 6.931471805599453e-1);
-    double T = tab[n & 31];
-    double res = fma(T, r * p, T);
-    int hi = __double2hiint(res) + ((n >> 5) << 20);
-    return __hiloint2double(hi, __double2loint(res));
+    const double t = fma(y, (double)kExpSteps, kShift);
+    const int n = __double2loint(t);
+    const double nf = t - kShift;
+    const double r = fma(nf, -1.0 / kExpSteps, y);  // exact
+    double p = c_exp2_poly[4];
+    p = fma(p, r, c_exp2_poly[3]);
+    p = fma(p, r, c_exp2_poly[2]);
+    p = fma(p, r, c_exp2_poly[1]);
+    p = fma(p, r, c_exp2_poly[0]);
+    T = tab_end[n];
+    return r * p;
+}
+
+__device__ __forceinline__ double exp2_neg(double y, const double* __restrict__ tab_end) {
+    double T;
+    const double rp = exp2_neg_parts(y, tab_end, T);
+    return fma(T, rp, T);
 }
 
 // 1/x via the MUFU reciprocal seed and one cubically convergent refinement.
+// x = +0 is first raised to 2^-930 (integer max on the high word), so the
+// reciprocal stays finite (~1e280); x >= 2^-930 is unchanged.
 __device__ __forceinline__ double rcp_fast(double x) {
+    const unsigned hi = max((unsigned)__double2hiint(x), 0x05D00000u);
+    x = __hiloint2double((int)hi, __double2loint(x));
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
     double e = fma(-x, y, 1.0);
@@ -150,22 +182,26 @@ __device__ __forceinline__ double rcp_fast(double x) {
 // Accumulate the pair interaction of source (sx, sy, g, q2) on target (tx, ty):
 // (u, v) += g (1 - exp(-r^2/(2 sigma^2))) / r^2 * (-dy, dx)  [times 1/2pi later]
 // Same arithmetic structure as kernels.kernel_eval (kernels.py:39-49) and
-// engine._pair_velocity (engine.py:245-257); r^2 == 0 contributes 0.
+// engine._pair_velocity (engine.py:245-257).  A coincident pair (r^2 == 0)
+// contributes exactly zero: dx = dy = 0 multiply a finite c (the reference's
+// r^2 > 0 mask, without a per-pair select).
 template <bool GAUSS>
 __device__ __forceinline__ void pair_acc(double tx, double ty, double sx, double sy, double g,
-                                         double q2, const double* __restrict__ tab, double& u,
+                                         double q2, const double* __restrict__ tab_end, double& u,
                                          double& v) {
-    double dx = tx - sx;
-    double dy = ty - sy;
-    double r2 = fma(dy, dy, dx * dx);
+    const double dx = tx - sx;
+    const double dy = ty - sy;
+    const double r2 = fma(dy, dy, dx * dx);
     double c = g * rcp_fast(r2);
-    if (GAUSS) {
-        double y = fmax(r2 * q2, -60.0);
-        c = c * (1.0 - exp2_neg(y, tab));
-    }
-    c = (r2 > 0.0) ? c : 0.0;
+    if (GAUSS) c = fma(-c, exp2_neg(clamp_neg60(r2 * q2), tab_end), c);  // c (1 - e)
     u = fma(-c, dy, u);
     v = fma(c, dx, v);
+}
+
+// Stage the exponential table in shared memory (all threads of the block).
+__device__ __forceinline__ const double* stage_exp_table(double* smem, const double* __restrict__ g) {
+    for (int i = threadIdx.x; i < kExpTab; i += blockDim.x) smem[i] = g[i];
+    return smem + (kExpTab - 1);
 }
 
 constexpr double kInv2Pi = 0.15915494309189535;  // 1 / (2 pi)

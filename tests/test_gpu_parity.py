@@ -117,7 +117,8 @@ def test_near_field_matches_oracle(name):
     run(c["x"], c["y"], c["gamma"], c["sigma"], c["levels"], c["order"], c["gauss"], dom)
     n = c["x"].size
     ws = Workspace.get(n, c["levels"], c["order"], torch.device("cuda", torch.cuda.current_device()))
-    near = ws.view("near_uv", torch.float64, 2 * n).cpu().numpy().reshape(n, 2)
+    rows = ws.view("near_uv", torch.float64, 6 * n).cpu().numpy().reshape(3, n, 2)
+    near = (rows[0] + rows[1]) + rows[2]
     _, st = O.evaluate(c["x"], c["y"], c["gamma"], c["sigma"], c["levels"], c["order"], c["gauss"], dom)
     ref = st["near_sorted"]
     assert np.abs(near - ref).max() <= 1e-13 * np.abs(ref).max()
