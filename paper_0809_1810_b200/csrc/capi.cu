@@ -28,8 +28,9 @@ bool g_tables_ready[kMaxDevices];
 
 struct Resources {
     bool ready = false;
-    cudaStream_t side = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaStream_t far = nullptr;   // far-field chain (highest priority)
+    cudaStream_t near = nullptr;  // near field (lowest priority)
+    cudaEvent_t fork = nullptr, join_far = nullptr, join_near = nullptr;
     cudaEvent_t ev[9] = {};
 };
 Resources g_res[kMaxDevices];
@@ -110,9 +111,15 @@ Resources* resources_for(int dev) {
     if (dev < 0 || dev >= kMaxDevices) return nullptr;
     Resources& r = g_res[dev];
     if (!r.ready) {
-        if (cudaStreamCreateWithFlags(&r.side, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (cudaStreamCreateWithPriority(&r.far, cudaStreamNonBlocking, hi) != cudaSuccess)
+            return nullptr;
+        if (cudaStreamCreateWithPriority(&r.near, cudaStreamNonBlocking, lo) != cudaSuccess)
+            return nullptr;
         cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&r.join_far, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&r.join_near, cudaEventDisableTiming);
         for (auto& e : r.ev) cudaEventCreate(&e);
         r.ready = true;
     }
@@ -320,32 +327,37 @@ int vfmm_evaluate(const double* x, const double* y, const double* gamma, const d
     if (!far_only)
         launch_tasks(L, ls, (int*)(ws + L.task_scratch), tasks, (int*)(ws + L.scan_aux), ctr, s);
     rec(1, s);
-    cudaStream_t ns = s;
+    // Overlap: the far-field chain runs on a high-priority stream and the near
+    // field on a low-priority one; P2P CTAs are short-lived, so far-field CTAs
+    // are scheduled as soon as any SM slot frees up.
+    cudaStream_t fs = s;
     if (overlap) {
         cudaEventRecord(R->fork, s);
-        cudaStreamWaitEvent(R->side, R->fork, 0);
-        ns = R->side;
-        rec(7, ns);
-        launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, ns);
-        rec(8, ns);
-        cudaEventRecord(R->join, ns);
+        cudaStreamWaitEvent(R->far, R->fork, 0);
+        cudaStreamWaitEvent(R->near, R->fork, 0);
+        fs = R->far;
     }
     // ---- upward ----
-    launch_p2m(L, src, ls, xmin, ymin, side, mult + L.level_cell_off[levels] * L.P, T, s);
-    launch_m2m(L, T, mult, s);
-    rec(2, s);
+    launch_p2m(L, src, ls, xmin, ymin, side, mult + L.level_cell_off[levels] * L.P, T, fs);
+    launch_m2m(L, T, mult, fs);
+    rec(2, fs);
     // ---- M2L (all levels, one launch) ----
-    launch_m2l(L, T, mult, counts, loc, ctr, s);
-    rec(3, s);
+    launch_m2l(L, T, mult, counts, loc, ctr, fs);
+    rec(3, fs);
     // ---- downward ----
-    launch_l2l(L, T, loc, s);
-    rec(4, s);
+    launch_l2l(L, T, loc, fs);
+    rec(4, fs);
+    if (overlap) {
+        cudaEventRecord(R->join_far, fs);
+        rec(7, R->near);
+        launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, R->near);
+        rec(8, R->near);
+        cudaEventRecord(R->join_near, R->near);
+        cudaStreamWaitEvent(s, R->join_far, 0);
+        cudaStreamWaitEvent(s, R->join_near, 0);
+    }
     if (!far_only) {
-        if (!overlap) {
-            launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, s);
-        } else {
-            cudaStreamWaitEvent(s, R->join, 0);
-        }
+        if (!overlap) launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, s);
         rec(5, s);
         launch_l2p_combine(L, T, src, keys, perm, loc, near_uv, xmin, ymin, side, u, v, s);
     }

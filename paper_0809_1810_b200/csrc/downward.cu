@@ -12,53 +12,86 @@ namespace vfmm {
 
 namespace {
 
-// One warp per child cell at `level`, lane = output coefficient n:
+constexpr int kL2LThreads = 128;
+
+// Thread = (child cell, chunk of TN output coefficients); a block covers one
+// child parity plane (= quadrant q), so F_q is block-uniform.  Child j of
+// plane q is cell (2 jx + qx, 2 jy + qy) whose parent is (jx, jy):
 //   Lh'_n += sum_{m>=n} (2^{-m} Lh_m) F_q[m-n]     (exact re-centring)
-__global__ void __launch_bounds__(256)
+template <int TN>
+__global__ void __launch_bounds__(kL2LThreads)
     k_l2l(const double2* __restrict__ parent, double2* __restrict__ child, int level, int P,
           const Tables* __restrict__ T) {
-    __shared__ double2 sF[4][kOrderCap + 16];
+    __shared__ double2 sF[kOrderCap + 16];
     __shared__ double s2[kOrderCap + 16];
-    for (int i = threadIdx.x; i < 4 * P; i += blockDim.x) sF[i / P][i % P] = T->F[i / P][i % P];
-    for (int i = threadIdx.x; i < P; i += blockDim.x) s2[i] = T->pow2neg[i];
+    const int half = 1 << (level - 1);
+    const int64_t np = (int64_t)half * half;  // cells per child plane
+    const int64_t bpp = (np + kL2LThreads - 1) / kL2LThreads;
+    const int q = (int)((blockIdx.x / bpp) & 3);
+    const int chunk = (int)(blockIdx.x / (4 * bpp));
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        sF[i] = T->F[q][i];
+        s2[i] = T->pow2neg[i];
+    }
     __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int mc = 1 << level, mp = mc >> 1;
-    const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    if (c >= (int64_t)mc * mc) return;
-    const int cx = (int)(c % mc), cy = (int)(c / mc);
-    const int q = 2 * (cy & 1) + (cx & 1);
-    const double2* L = parent + ((int64_t)(cy >> 1) * mp + (cx >> 1)) * P;
-    for (int nb = 0; nb < P; nb += 32) {
-        const int nn = nb + lane;
-        double2 acc = make_double2(0.0, 0.0);
-        for (int m = nb; m < P; ++m) {
-            const double2 a = L[m];
-            if (m >= nn && nn < P) {
-                const double sc = s2[m];
-                const double2 f = sF[q][m - nn];
-                const double axs = a.x * sc, ays = a.y * sc;
-                acc.x = fma(axs, f.x, fma(-ays, f.y, acc.x));
-                acc.y = fma(axs, f.y, fma(ays, f.x, acc.y));
+    const int64_t j = (blockIdx.x % bpp) * kL2LThreads + threadIdx.x;
+    if (j >= np) return;
+    const int jx = (int)(j % half), jy = (int)(j / half);
+    const double2* L = parent + coef_base(level - 1, jx, jy);
+    const int64_t ps = coef_stride(level - 1);
+    const int n0 = chunk * TN;
+    double ax[TN], ay[TN];
+#pragma unroll
+    for (int t = 0; t < TN; ++t) ax[t] = ay[t] = 0.0;
+    for (int m = n0; m < P; ++m) {
+        const double2 a = L[m * ps];
+        const double axs = a.x * s2[m], ays = a.y * s2[m];
+#pragma unroll
+        for (int t = 0; t < TN; ++t) {
+            if (m >= n0 + t) {
+                const double2 f = sF[m - n0 - t];
+                ax[t] = fma(axs, f.x, fma(-ays, f.y, ax[t]));
+                ay[t] = fma(axs, f.y, fma(ays, f.x, ay[t]));
             }
         }
+    }
+    double2* out = child + q * np + j;
+    const int64_t cs = 4 * np;
+#pragma unroll
+    for (int t = 0; t < TN; ++t) {
+        const int nn = n0 + t;
         if (nn < P) {
-            double2 cur = child[c * P + nn];
-            cur.x += acc.x;
-            cur.y += acc.y;
-            child[c * P + nn] = cur;
+            double2 cur = out[nn * cs];
+            cur.x += ax[t];
+            cur.y += ay[t];
+            out[nn * cs] = cur;
         }
+    }
+}
+
+template <int TN>
+void launch_l2l_tn(const Layout& L, const Tables* T, double2* loc, cudaStream_t s) {
+    const int nchunks = (L.P + TN - 1) / TN;
+    for (int level = 3; level <= L.levels; ++level) {
+        const int64_t np = 1ll << (2 * (level - 1));
+        const int64_t bpp = (np + kL2LThreads - 1) / kL2LThreads;
+        const double2* parent = loc + L.level_cell_off[level - 1] * L.P;
+        double2* child = loc + L.level_cell_off[level] * L.P;
+        k_l2l<TN><<<(unsigned)(bpp * 4 * nchunks), kL2LThreads, 0, s>>>(parent, child, level, L.P, T);
+        note_launches(1);
     }
 }
 
 // Horner evaluation of the leaf local expansion at z:
 //   f(z) = sum_m Lh_m / m! (-w)^m,  w = (z - c) / r
-__device__ __forceinline__ double2 eval_local(const double2* __restrict__ Lh, int P, double wx,
-                                              double wy, const double* __restrict__ invfact) {
+__device__ __forceinline__ double2 eval_local(const double2* __restrict__ Lh, int64_t stride, int P,
+                                              double wx, double wy,
+                                              const double* __restrict__ invfact) {
     const double nx = -wx, ny = -wy;
-    double ax = Lh[P - 1].x * invfact[P - 1], ay = Lh[P - 1].y * invfact[P - 1];
+    const double2 top = Lh[(P - 1) * stride];
+    double ax = top.x * invfact[P - 1], ay = top.y * invfact[P - 1];
     for (int k = P - 2; k >= 0; --k) {
-        const double2 c = Lh[k];
+        const double2 c = Lh[k * stride];
         const double f = invfact[k];
         const double tx = fma(ax, nx, fma(-ay, ny, c.x * f));
         const double ty = fma(ax, ny, fma(ay, nx, c.y * f));
@@ -87,7 +120,8 @@ __global__ void __launch_bounds__(256)
     const double inv_r = 1.0 / r;
     const Src s = src[i];
     const double2 f =
-        eval_local(loc + (int64_t)leaf * P, P, (s.x - cx) * inv_r, (s.y - cy) * inv_r, sfact);
+        eval_local(loc + coef_base(levels, ix, iy), coef_stride(levels), P, (s.x - cx) * inv_r,
+                   (s.y - cy) * inv_r, sfact);
     // near field = the three neighbourhood-row partial sums, in row order
     const double2 n0 = near_uv[i], n1 = near_uv[n + i], n2 = near_uv[2 * n + i];
     const double2 nv = make_double2((n0.x + n1.x) + n2.x, (n0.y + n1.y) + n2.y);
@@ -130,8 +164,8 @@ __global__ void __launch_bounds__(256)
     const double r = side / m;
     const double cx = cell_center(xmin, ix, r), cy = cell_center(ymin, iy, r);
     const double inv_r = 1.0 / r;
-    const double2 f = eval_local(loc + ((int64_t)iy * m + ix) * P, P, (x - cx) * inv_r,
-                                 (y - cy) * inv_r, sfact);
+    const double2 f = eval_local(loc + coef_base(levels, ix, iy), coef_stride(levels), P,
+                                 (x - cx) * inv_r, (y - cy) * inv_r, sfact);
     double nu = 0.0, nv = 0.0;
     const int xlo = ix > 0 ? ix - 1 : 0, xhi = ix < m - 1 ? ix + 1 : m - 1;
     for (int ny = iy - 1; ny <= iy + 1; ++ny) {
@@ -149,12 +183,12 @@ __global__ void __launch_bounds__(256)
 }  // namespace
 
 void launch_l2l(const Layout& L, const Tables* T, double2* loc, cudaStream_t s) {
-    for (int level = 3; level <= L.levels; ++level) {
-        const int64_t nc = 1ll << (2 * level);
-        const double2* parent = loc + L.level_cell_off[level - 1] * L.P;
-        double2* child = loc + L.level_cell_off[level] * L.P;
-        k_l2l<<<(unsigned)((nc + 7) / 8), 256, 0, s>>>(parent, child, level, L.P, T);
-        note_launches(1);
+    switch (coef_chunk(L.P)) {
+        case 4: launch_l2l_tn<4>(L, T, loc, s); break;
+        case 5: launch_l2l_tn<5>(L, T, loc, s); break;
+        case 6: launch_l2l_tn<6>(L, T, loc, s); break;
+        case 7: launch_l2l_tn<7>(L, T, loc, s); break;
+        default: launch_l2l_tn<8>(L, T, loc, s); break;
     }
 }
 

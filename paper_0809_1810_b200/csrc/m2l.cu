@@ -23,20 +23,37 @@ namespace {
 
 constexpr int kM2LThreads = 128;
 
+// Offsets of the interaction list of parity class (px, py) in row-major
+// order (engine._il_offsets, engine.py:77-89), as (dx, dy) pairs.
+__device__ __forceinline__ void il_offset(int px, int py, int o, int& dx, int& dy) {
+    int idx = 0;
+    for (int yy = -2 - py; yy < 4 - py; ++yy)
+        for (int xx = -2 - px; xx < 4 - px; ++xx) {
+            const int ax = xx < 0 ? -xx : xx, ay = yy < 0 ? -yy : yy;
+            if ((ax > ay ? ax : ay) >= 2) {
+                if (idx == o) { dx = xx; dy = yy; }
+                ++idx;
+            }
+        }
+}
+
+// Thread = (destination j of one parity plane, chunk of TN outputs).  With the
+// planar layout the source of offset (dx, dy) for consecutive destinations is
+// a run of consecutive cells of one source plane, so each multipole
+// coefficient load is coalesced; the Hankel rows are block-uniform smem
+// broadcasts.  Output written to the destination plane, coalesced.
 template <int TN>
 __global__ void __launch_bounds__(kM2LThreads)
     k_m2l(const double2* __restrict__ mult, const int* __restrict__ counts, double2* __restrict__ loc,
-          int levels, int P, int nchunks, const size_t* __restrict__ dummy, const Tables* __restrict__ T,
-          unsigned long long* __restrict__ m2l_count, size_t off2) {
+          int levels, int P, int nchunks, const Tables* __restrict__ T,
+          unsigned long long* __restrict__ m2l_count) {
     extern __shared__ double2 sH[];  // [27][TN + P - 1]
-    (void)dummy;
     // ---- decode (level, parity, chunk, block-in-class) from blockIdx.x ----
     int64_t b = blockIdx.x;
     int level = 2;
-    size_t cell_off = 0;   // cells before this level in mult/loc (level 2 first)
-    size_t cnt_off = 0;    // cells before this level in counts (level 0 first)
-    for (int k = 0; k < 2; ++k) cnt_off += (size_t)1 << (2 * k);
-    int64_t bpc = 0;  // blocks per (parity, chunk) at this level
+    size_t cell_off = 0;  // cells before this level in mult/loc (level 2 first)
+    size_t cnt_off = 5;   // cells before this level in counts (levels 0, 1 first)
+    int64_t bpc = 0;      // blocks per (parity, chunk) at this level
     for (;;) {
         const int64_t dests = 1ll << (2 * (level - 1));
         bpc = (dests + kM2LThreads - 1) / kM2LThreads;
@@ -47,7 +64,6 @@ __global__ void __launch_bounds__(kM2LThreads)
         cnt_off += (size_t)1 << (2 * level);
         ++level;
     }
-    (void)off2;
     const int chunk = (int)(b / (4 * bpc));
     const int parity = (int)((b / bpc) % 4);
     const int64_t blk = b % bpc;
@@ -58,27 +74,22 @@ __global__ void __launch_bounds__(kM2LThreads)
     // ---- stage the 27 H rows of this parity class ----
     for (int i = threadIdx.x; i < 27 * HL; i += blockDim.x) {
         const int o = i / HL, q = i % HL;
-        // o-th offset of _il_offsets(px, py): dy outer, dx inner, max(|dx|,|dy|) >= 2
-        int idx = 0, dxo = 0, dyo = 0;
-        for (int dy = -2 - py; dy < 4 - py; ++dy)
-            for (int dx = -2 - px; dx < 4 - px; ++dx) {
-                const int adx = dx < 0 ? -dx : dx, ady = dy < 0 ? -dy : dy;
-                if ((adx > ady ? adx : ady) >= 2) {
-                    if (idx == o) { dxo = dx; dyo = dy; }
-                    ++idx;
-                }
-            }
+        int dxo = 0, dyo = 0;
+        il_offset(px, py, o, dxo, dyo);
         sH[i] = T->H[(dyo + 3) * 7 + (dxo + 3)][m0 + q];
     }
     __syncthreads();
 
     const int mk = 1 << level, half = mk >> 1;
+    const int64_t psz = (int64_t)half * half;  // cells per plane
     const int64_t j = blk * kM2LThreads + threadIdx.x;
-    const bool active = j < (int64_t)half * half;
-    const int ix = active ? 2 * (int)(j % half) + px : 0;
-    const int iy = active ? 2 * (int)(j / half) + py : 0;
+    const bool active = j < psz;
+    const int jx = active ? (int)(j % half) : 0;
+    const int jy = active ? (int)(j / half) : 0;
+    const int ix = 2 * jx + px, iy = 2 * jy + py;
     const double2* M = mult + cell_off * P;
     const int* cnt = counts + cnt_off;
+    const int64_t cstride = 4 * psz;
 
     double ax[TN], ay[TN];
 #pragma unroll
@@ -91,15 +102,16 @@ __global__ void __launch_bounds__(kM2LThreads)
             if ((adx > ady ? adx : ady) < 2) continue;
             const int sx = ix + dx, sy = iy + dy;
             const bool inr = active && sx >= 0 && sx < mk && sy >= 0 && sy < mk;
-            const int64_t sidx = (int64_t)sy * mk + sx;
-            const bool live = inr && cnt[inr ? sidx : 0] > 0;
+            const bool live = inr && cnt[(int64_t)sy * mk + sx] > 0;
             ntrans += live ? 1 : 0;
             const double2* h = sH + o * HL;
             ++o;
             if (!__any_sync(0xffffffffu, live)) continue;
-            const double2* Ms = M + (live ? sidx : 0) * P;
+            // source plane / index (floor division of the shifted coordinates)
+            const int sp = ((sy & 1) << 1) | (sx & 1);
+            const double2* Ms = M + sp * psz + (live ? (int64_t)(sy >> 1) * half + (sx >> 1) : 0);
             for (int n = 0; n < P; ++n) {
-                double2 a = Ms[n];
+                double2 a = Ms[n * cstride];
                 if (!live) a = make_double2(0.0, 0.0);
 #pragma unroll
                 for (int t = 0; t < TN; ++t) {
@@ -111,10 +123,10 @@ __global__ void __launch_bounds__(kM2LThreads)
         }
     }
     if (active) {
-        double2* out = loc + (cell_off + (size_t)iy * mk + ix) * P;
+        double2* out = loc + cell_off * P + parity * psz + j;
 #pragma unroll
         for (int t = 0; t < TN; ++t)
-            if (m0 + t < P) out[m0 + t] = make_double2(ax[t], ay[t]);
+            if (m0 + t < P) out[(m0 + t) * cstride] = make_double2(ax[t], ay[t]);
     }
     if (chunk == 0) {
         // m2l_count counts (destination, nonempty source) pairs at every level
@@ -135,24 +147,15 @@ void launch_tn(const Layout& L, const Tables* T, const double2* mult, const int*
     }
     const size_t shm = (size_t)27 * (TN + L.P - 1) * sizeof(double2);
     k_m2l<TN><<<(unsigned)blocks, kM2LThreads, shm, s>>>(mult, counts, loc, L.levels, L.P, nchunks,
-                                                       nullptr, T, &ctr->m2l_count, 0);
+                                                       T, &ctr->m2l_count);
     note_launches(1);
 }
 
 }  // namespace
 
-int m2l_chunk(int P) {
-    int best = 8, waste = 1 << 30;
-    for (int tn = 8; tn >= 4; --tn) {
-        const int w = (P + tn - 1) / tn * tn - P;
-        if (w < waste) { waste = w; best = tn; }
-    }
-    return best;
-}
-
 void launch_m2l(const Layout& L, const Tables* T, const double2* mult, const int* counts,
                 double2* loc, Counters* ctr, cudaStream_t s) {
-    switch (m2l_chunk(L.P)) {
+    switch (coef_chunk(L.P)) {
         case 4: launch_tn<4>(L, T, mult, counts, loc, ctr, s); break;
         case 5: launch_tn<5>(L, T, mult, counts, loc, ctr, s); break;
         case 6: launch_tn<6>(L, T, mult, counts, loc, ctr, s); break;

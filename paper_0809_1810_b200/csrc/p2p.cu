@@ -23,42 +23,68 @@ namespace {
 constexpr int kP2PWarps = 8;
 constexpr int kP2PBlocksPerSM = 4;
 
-// One lane's targets against one contiguous source slice [a, b).
-template <bool GAUSS>
-__device__ __forceinline__ void slice_1(const Src* __restrict__ src, int a, int b, double tx,
-                                        double ty, const double* __restrict__ tab, double& u,
-                                        double& v) {
-    int j = a;
-    for (; j + 4 <= b; j += 4) {
-        const Src s0 = src[j], s1 = src[j + 1], s2 = src[j + 2], s3 = src[j + 3];
-        pair_acc<GAUSS>(tx, ty, s0.x, s0.y, s0.g, s0.q2, tab, u, v);
-        pair_acc<GAUSS>(tx, ty, s1.x, s1.y, s1.g, s1.q2, tab, u, v);
-        pair_acc<GAUSS>(tx, ty, s2.x, s2.y, s2.g, s2.q2, tab, u, v);
-        pair_acc<GAUSS>(tx, ty, s3.x, s3.y, s3.g, s3.q2, tab, u, v);
-    }
-    for (; j < b; ++j) {
-        const Src s0 = src[j];
-        pair_acc<GAUSS>(tx, ty, s0.x, s0.y, s0.g, s0.q2, tab, u, v);
-    }
+// Asynchronous global->shared copy of 16 bytes (LDGSTS), bypassing registers.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <bool GAUSS>
-__device__ __forceinline__ void slice_2(const Src* __restrict__ src, int a, int b, double tx0,
-                                        double ty0, double tx1, double ty1,
-                                        const double* __restrict__ tab, double& u0, double& v0,
-                                        double& u1, double& v1) {
-    int j = a;
-    for (; j + 2 <= b; j += 2) {
-        const Src s0 = src[j], s1 = src[j + 1];
-        pair_acc<GAUSS>(tx0, ty0, s0.x, s0.y, s0.g, s0.q2, tab, u0, v0);
-        pair_acc<GAUSS>(tx1, ty1, s0.x, s0.y, s0.g, s0.q2, tab, u1, v1);
-        pair_acc<GAUSS>(tx0, ty0, s1.x, s1.y, s1.g, s1.q2, tab, u0, v0);
-        pair_acc<GAUSS>(tx1, ty1, s1.x, s1.y, s1.g, s1.q2, tab, u1, v1);
+constexpr int kChunk = 32;  // sources per staged chunk (one per lane)
+
+// One warp's targets (TPT per lane) against the contiguous source slice
+// [a, b): the slice streams through a per-warp double buffer in shared memory
+// (cp.async, one 32-byte record per lane per chunk) so the arithmetic reads
+// warp-uniform broadcasts from smem while the next chunk is in flight.
+template <bool GAUSS, int TPT>
+__device__ __forceinline__ void slice_acc(const Src* __restrict__ src, int a, int b,
+                                          Src (*buf)[kChunk], const double* __restrict__ tab,
+                                          double tx0, double ty0, double tx1, double ty1,
+                                          double& u0, double& v0, double& u1, double& v1) {
+    const int lane = threadIdx.x & 31;
+    const int nch = (b - a + kChunk - 1) / kChunk;
+    if (nch == 0) return;
+    if (a + lane < b) {
+        cp_async16(&buf[0][lane], &src[a + lane]);
+        cp_async16(reinterpret_cast<char*>(&buf[0][lane]) + 16,
+                   reinterpret_cast<const char*>(&src[a + lane]) + 16);
     }
-    if (j < b) {
-        const Src s0 = src[j];
-        pair_acc<GAUSS>(tx0, ty0, s0.x, s0.y, s0.g, s0.q2, tab, u0, v0);
-        pair_acc<GAUSS>(tx1, ty1, s0.x, s0.y, s0.g, s0.q2, tab, u1, v1);
+    cp_async_commit();
+    for (int c = 0; c < nch; ++c) {
+        const int base = a + c * kChunk;
+        if (c + 1 < nch) {
+            const int j = base + kChunk + lane;
+            if (j < b) {
+                Src* d = &buf[(c + 1) & 1][lane];
+                cp_async16(d, &src[j]);
+                cp_async16(reinterpret_cast<char*>(d) + 16, reinterpret_cast<const char*>(&src[j]) + 16);
+            }
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        const Src* sb = buf[c & 1];
+        const int cnt = min(kChunk, b - base);
+        int k = 0;
+        for (; k + 2 <= cnt; k += 2) {
+            const Src s0 = sb[k], s1 = sb[k + 1];
+            pair_acc<GAUSS>(tx0, ty0, s0.x, s0.y, s0.g, s0.q2, tab, u0, v0);
+            if (TPT == 2) pair_acc<GAUSS>(tx1, ty1, s0.x, s0.y, s0.g, s0.q2, tab, u1, v1);
+            pair_acc<GAUSS>(tx0, ty0, s1.x, s1.y, s1.g, s1.q2, tab, u0, v0);
+            if (TPT == 2) pair_acc<GAUSS>(tx1, ty1, s1.x, s1.y, s1.g, s1.q2, tab, u1, v1);
+        }
+        if (k < cnt) {
+            const Src s0 = sb[k];
+            pair_acc<GAUSS>(tx0, ty0, s0.x, s0.y, s0.g, s0.q2, tab, u0, v0);
+            if (TPT == 2) pair_acc<GAUSS>(tx1, ty1, s0.x, s0.y, s0.g, s0.q2, tab, u1, v1);
+        }
+        __syncwarp();
     }
 }
 
@@ -73,15 +99,19 @@ template <bool GAUSS, int TPT>
 __global__ void __launch_bounds__(kP2PWarps * 32, kP2PBlocksPerSM)
     k_p2p(const Src* __restrict__ src, const int* __restrict__ ls, const int2* __restrict__ tasks,
           Counters* __restrict__ ctr, int levels, int64_t n, const Tables* __restrict__ T,
-          double2* __restrict__ near_uv, unsigned long long* __restrict__ pairs) {
+          double2* __restrict__ near_uv, unsigned long long* __restrict__ pairs, int items_per_warp) {
+    const int nitems = ctr->ntasks * kNearRows;
+    if (items_per_warp < (1 << 30) && (int64_t)blockIdx.x * kP2PWarps * items_per_warp >= nitems)
+        return;  // spare CTA
     __shared__ double sexp[kExpTab];
+    __shared__ __align__(16) Src sbuf[kP2PWarps][2][kChunk];
     const double* tab = stage_exp_table(sexp, T->exp2tab);
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const int nitems = ctr->ntasks * kNearRows;
+    Src(*buf)[kChunk] = sbuf[threadIdx.x >> 5];
     const int m = 1 << levels;
     long long my_pairs = 0;
-    for (;;) {
+    for (int it = 0; it < items_per_warp; ++it) {
         int item = 0;
         if (lane == 0) item = atomicAdd(&ctr->task_cursor, 1);
         item = __shfl_sync(0xffffffffu, item, 0);
@@ -110,9 +140,9 @@ __global__ void __launch_bounds__(kP2PWarps * 32, kP2PBlocksPerSM)
             const int xlo = cx > 0 ? cx - 1 : 0, xhi = cx < m - 1 ? cx + 1 : m - 1;
             const int a = ls[(int64_t)ny * m + xlo], b = ls[(int64_t)ny * m + xhi + 1];
             if (TPT == 2 && __any_sync(0xffffffffu, act1))
-                slice_2<GAUSS>(src, a, b, tx0, ty0, tx1, ty1, tab, u0, v0, u1, v1);
+                slice_acc<GAUSS, 2>(src, a, b, buf, tab, tx0, ty0, tx1, ty1, u0, v0, u1, v1);
             else
-                slice_1<GAUSS>(src, a, b, tx0, ty0, tab, u0, v0);
+                slice_acc<GAUSS, 1>(src, a, b, buf, tab, tx0, ty0, tx1, ty1, u0, v0, u1, v1);
             // engine.py:284: pairs += n_leaf * (n_nbhd - 1), split over tasks and rows
             const long long cnt = min(32 * TPT, hi - lo - tk.y);
             my_pairs += cnt * (long long)(b - a) - (row == 1 ? cnt : 0);
@@ -199,27 +229,45 @@ int p2p_targets_per_lane() {
     static int tpt = 0;
     if (!tpt) {
         const char* e = getenv("VFMM_P2P_TPT");
-        tpt = (e && e[0] == '1') ? 1 : 2;
+        tpt = (e && e[0] == '2') ? 2 : 1;
     }
     return tpt;
 }
 
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
                 const int2* tasks, Counters* ctr, int kernel, double2* near_uv, cudaStream_t s) {
-    static int num_sms = 0;
-    if (!num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    // Items per warp: short-lived CTAs (default 2) let far-field CTAs in as SM
+    // slots free up; the grid covers the upper bound of work items and CTAs
+    // beyond the actual count exit at once.  VFMM_P2P_K overrides (tuning).
+    static int K = 0;
+    if (!K) {
+        const char* e = getenv("VFMM_P2P_K");
+        K = e ? atoi(e) : 2;
+        if (K < 1) K = 2;
     }
-    const size_t need = (L.max_tasks * kNearRows + kP2PWarps - 1) / kP2PWarps;
-    const size_t cap = (size_t)num_sms * kP2PBlocksPerSM;
-    const unsigned blocks = (unsigned)(need < cap ? need : cap);
+    static int persist = -1;
+    if (persist < 0) {
+        const char* e = getenv("VFMM_P2P_PERSIST");
+        persist = e ? atoi(e) : 0;
+        if (persist > 0) {
+            int dev = 0, sms = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            persist *= sms;
+        }
+    }
+    const size_t per_block = (size_t)kP2PWarps * K;
+    unsigned blocks = (unsigned)((L.max_tasks * kNearRows + per_block - 1) / per_block);
+    int kk = K;
+    if (persist > 0) {  // persistent grid of `persist` CTAs, no per-warp item cap
+        blocks = (unsigned)persist;
+        kk = 1 << 30;
+    }
     const bool g = kernel == VFMM_KERNEL_GAUSSIAN;
     auto* fn = p2p_targets_per_lane() == 2 ? (g ? k_p2p<true, 2> : k_p2p<false, 2>)
                                            : (g ? k_p2p<true, 1> : k_p2p<false, 1>);
     fn<<<blocks, kP2PWarps * 32, 0, s>>>(src, leaf_starts, tasks, ctr, L.levels, L.n, T, near_uv,
-                                         &ctr->near_pairs);
+                                         &ctr->near_pairs, kk);
     note_launches(1);
 }
 

@@ -50,12 +50,18 @@ __global__ void k_keys(const double* __restrict__ x, const double* __restrict__ 
         val[i] = (int)i;
         if (sigma) sbits = ordered_bits(sigma[i]);
     }
-    // block max of the sigma bits, one atomic per warp
+    // block max of the sigma bits, one atomic per block
+    __shared__ unsigned long long wmax[32];
     for (int o = 16; o > 0; o >>= 1) {
         unsigned long long t = __shfl_xor_sync(0xffffffffu, sbits, o);
         sbits = t > sbits ? t : sbits;
     }
-    if ((threadIdx.x & 31) == 0 && sbits) atomicMax(&ctr->sigma_max_bits, sbits);
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = sbits;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) sbits = wmax[w] > sbits ? wmax[w] : sbits;
+        if (sbits) atomicMax(&ctr->sigma_max_bits, sbits);
+    }
 }
 
 constexpr int kWPB = 8;  // warps per block in the radix kernels

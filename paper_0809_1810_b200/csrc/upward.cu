@@ -4,7 +4,8 @@
 // (expansions.py:88-101) and expansions.multipole_shift_matrix
 // (expansions.py:119-130).  Coefficients are stored in the scaled form
 // M_n = a_n / (r^{n+1} n!) (vfmm_internal.cuh), which makes the shift
-// operator level independent:  P_m = 2^{-(m+1)} sum_{k<=m} M_k E_q[m-k].
+// operator level independent:  P_m = 2^{-(m+1)} sum_{k<=m} M_k E_q[m-k],
+// in the planar coefficient layout (coef_base / coef_stride).
 #include "vfmm_internal.cuh"
 
 namespace vfmm {
@@ -25,12 +26,13 @@ __global__ void __launch_bounds__(kP2MWarps * 32)
     const int64_t leaf = (int64_t)blockIdx.x * kP2MWarps + warp;
     if (leaf >= (int64_t)m * m) return;
     const int lo = ls[leaf], hi = ls[leaf + 1];
-    double2* out = mult + leaf * P;
+    const int ix = (int)(leaf % m), iy = (int)(leaf / m);
+    double2* out = mult + coef_base(levels, ix, iy);
+    const int64_t cs = coef_stride(levels);
     if (lo == hi) {
-        for (int k = lane; k < P; k += 32) out[k] = make_double2(0.0, 0.0);
+        for (int k = lane; k < P; k += 32) out[k * cs] = make_double2(0.0, 0.0);
         return;
     }
-    const int ix = (int)(leaf % m), iy = (int)(leaf / m);
     const double r = side / m;  // Tree.cell_side (quadtree.py:140-141)
     const double cx = cell_center(xmin, ix, r), cy = cell_center(ymin, iy, r);
     const double inv_r = 1.0 / r;
@@ -73,50 +75,85 @@ __global__ void __launch_bounds__(kP2MWarps * 32)
         if (k < P) {
             const double2 a = g == 0 ? acc0 : acc1;
             const double sc = T->invfact[k] * inv_r;
-            out[k] = make_double2(a.x * sc, a.y * sc);
+            out[k * cs] = make_double2(a.x * sc, a.y * sc);
         }
     }
 }
 
-// One warp per parent cell at level `level-1`, lane = output coefficient m.
+constexpr int kM2MThreads = 128;
+
+// Thread = (parent cell, chunk of TN output coefficients).  The four children
+// of parent (jx, jy) sit at index j = jy*mp + jx of the child level's four
+// planes, so every child coefficient load is coalesced across the warp.
 // Children in quadrant order (0,0), (1,0), (0,1), (1,1) like engine.py:140-145.
-__global__ void __launch_bounds__(256)
+template <int TN>
+__global__ void __launch_bounds__(kM2MThreads)
     k_m2m(const double2* __restrict__ child, double2* __restrict__ parent, int level, int P,
-          const Tables* __restrict__ T) {
+          int nchunks, const Tables* __restrict__ T) {
     __shared__ double2 sE[4][kOrderCap + 16];
     __shared__ double s2[kOrderCap + 16];
     for (int i = threadIdx.x; i < 4 * P; i += blockDim.x) sE[i / P][i % P] = T->E[i / P][i % P];
     for (int i = threadIdx.x; i <= P; i += blockDim.x) s2[i] = T->pow2neg[i];
     __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int mc = 1 << level, mp = mc >> 1;
-    const int64_t par = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    if (par >= (int64_t)mp * mp) return;
-    const int jx = (int)(par % mp), jy = (int)(par / mp);
-    for (int mb = 0; mb < P; mb += 32) {
-        const int mm = mb + lane;
-        double2 acc = make_double2(0.0, 0.0);
-        for (int q = 0; q < 4; ++q) {
-            const int cxq = q & 1, cyq = q >> 1;
-            const double2* M = child + ((int64_t)(2 * jy + cyq) * mc + 2 * jx + cxq) * P;
-            const int kend = min(P - 1, mb + 31);
-            for (int k = 0; k <= kend; ++k) {
-                const double2 a = M[k];
-                if (k <= mm && mm < P) {
-                    const double2 e = sE[q][mm - k];
-                    acc.x = fma(a.x, e.x, fma(-a.y, e.y, acc.x));
-                    acc.y = fma(a.x, e.y, fma(a.y, e.x, acc.y));
+    const int mp = 1 << (level - 1);
+    const int64_t np = (int64_t)mp * mp;
+    const int64_t bpc = (np + kM2MThreads - 1) / kM2MThreads;
+    const int chunk = (int)(blockIdx.x / bpc);
+    const int64_t pidx = (blockIdx.x % bpc) * kM2MThreads + threadIdx.x;
+    if (pidx >= np) return;
+    const int m0 = chunk * TN;
+    const int kend = min(P - 1, m0 + TN - 1);
+    double ax[TN], ay[TN];
+#pragma unroll
+    for (int t = 0; t < TN; ++t) ax[t] = ay[t] = 0.0;
+    for (int q = 0; q < 4; ++q) {
+        const double2* M = child + q * np + pidx;
+        for (int k = 0; k <= kend; ++k) {
+            const double2 a = M[(int64_t)k * 4 * np];
+#pragma unroll
+            for (int t = 0; t < TN; ++t) {
+                if (k <= m0 + t) {
+                    const double2 e = sE[q][m0 + t - k];
+                    ax[t] = fma(a.x, e.x, fma(-a.y, e.y, ax[t]));
+                    ay[t] = fma(a.x, e.y, fma(a.y, e.x, ay[t]));
                 }
             }
         }
-        if (mm < P) {
-            const double sc = s2[mm + 1];
-            parent[par * P + mm] = make_double2(acc.x * sc, acc.y * sc);
-        }
+    }
+    const int jx = (int)(pidx % mp), jy = (int)(pidx / mp);
+    double2* out = parent + coef_base(level - 1, jx, jy);
+    const int64_t cs = coef_stride(level - 1);
+#pragma unroll
+    for (int t = 0; t < TN; ++t) {
+        const int mm = m0 + t;
+        if (mm < P) out[mm * cs] = make_double2(ax[t] * s2[mm + 1], ay[t] * s2[mm + 1]);
+    }
+}
+
+template <int TN>
+void launch_m2m_tn(const Layout& L, const Tables* T, double2* mult, cudaStream_t s) {
+    const int nchunks = (L.P + TN - 1) / TN;
+    for (int level = L.levels; level >= 3; --level) {
+        const int64_t np = 1ll << (2 * (level - 1));
+        const int64_t bpc = (np + kM2MThreads - 1) / kM2MThreads;
+        double2* child = mult + L.level_cell_off[level] * L.P;
+        double2* parent = mult + L.level_cell_off[level - 1] * L.P;
+        k_m2m<TN><<<(unsigned)(bpc * nchunks), kM2MThreads, 0, s>>>(child, parent, level, L.P,
+                                                                    nchunks, T);
+        note_launches(1);
     }
 }
 
 }  // namespace
+
+int coef_chunk(int P) {
+    int best = 8, waste = 1 << 30;
+    for (int tn = 8; tn >= 4; --tn) {
+        const int w = (P + tn - 1) / tn * tn - P;
+        if (w < waste) { waste = w; best = tn; }
+    }
+    return best;
+}
 
 void launch_p2m(const Layout& L, const Src* src, const int* leaf_starts, double xmin, double ymin,
                 double side, double2* mult_leaf, const Tables* T, cudaStream_t s) {
@@ -127,12 +164,12 @@ void launch_p2m(const Layout& L, const Src* src, const int* leaf_starts, double 
 }
 
 void launch_m2m(const Layout& L, const Tables* T, double2* mult, cudaStream_t s) {
-    for (int level = L.levels; level >= 3; --level) {
-        const int64_t np = 1ll << (2 * (level - 1));
-        double2* child = mult + L.level_cell_off[level] * L.P;
-        double2* parent = mult + L.level_cell_off[level - 1] * L.P;
-        k_m2m<<<(unsigned)((np + 7) / 8), 256, 0, s>>>(child, parent, level, L.P, T);
-        note_launches(1);
+    switch (coef_chunk(L.P)) {
+        case 4: launch_m2m_tn<4>(L, T, mult, s); break;
+        case 5: launch_m2m_tn<5>(L, T, mult, s); break;
+        case 6: launch_m2m_tn<6>(L, T, mult, s); break;
+        case 7: launch_m2m_tn<7>(L, T, mult, s); break;
+        default: launch_m2m_tn<8>(L, T, mult, s); break;
     }
 }
 

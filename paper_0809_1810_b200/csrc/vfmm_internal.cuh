@@ -96,7 +96,7 @@ void launch_m2m(const Layout& L, const Tables* T, double2* mult, cudaStream_t s)
 void launch_m2l(const Layout& L, const Tables* T, const double2* mult, const int* counts,
                 double2* loc, Counters* ctr, cudaStream_t s);
 void launch_l2l(const Layout& L, const Tables* T, double2* loc, cudaStream_t s);
-int p2p_targets_per_lane();  // 1 or 2 (env VFMM_P2P_TPT, default 2)
+int p2p_targets_per_lane();  // 1 or 2 (env VFMM_P2P_TPT, default 1)
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
                 const int2* tasks, Counters* ctr, int kernel, double2* near_uv, cudaStream_t s);
 void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const int* keys,
@@ -117,6 +117,24 @@ void launch_direct(const double* tx, const double* ty, int64_t m, const double* 
 __device__ __forceinline__ double cell_center(double lo, int i, double s) {
     return __dadd_rn(lo, __dmul_rn((double)i + 0.5, s));
 }
+
+// Planar coefficient layout of one level k >= 2 (2^k cells per side):
+//   [P coefficients][4 parity planes][half^2 cells],  half = 2^(k-1),
+//   plane = 2*(iy & 1) + (ix & 1),  j = (iy >> 1) * half + (ix >> 1).
+// Threads enumerating j within a plane touch consecutive addresses for every
+// coefficient, so the M2L / M2M / L2L sweeps are fully coalesced.
+__host__ __device__ __forceinline__ int64_t coef_plane_size(int k) {
+    return (int64_t)1 << (2 * (k - 1));
+}
+__host__ __device__ __forceinline__ int64_t coef_base(int k, int ix, int iy) {
+    const int64_t half = (int64_t)1 << (k - 1);
+    return (int64_t)(((iy & 1) << 1) | (ix & 1)) * half * half + (int64_t)(iy >> 1) * half + (ix >> 1);
+}
+__host__ __device__ __forceinline__ int64_t coef_stride(int k) {  // between coefficients
+    return (int64_t)4 << (2 * (k - 1));
+}
+
+int coef_chunk(int P);  // TN of the chunked coefficient kernels (4..8)
 
 // ---- shared device math ----
 

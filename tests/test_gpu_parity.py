@@ -83,13 +83,20 @@ def _unscale(ws, c, dom):
     mult = (mult[:, 0] + 1j * mult[:, 1]).reshape(cells, P)
     loc = (loc[:, 0] + 1j * loc[:, 1]).reshape(cells, P)
     fact = np.array([math.factorial(k) for k in range(P)], dtype=np.float64)
+    mult, loc = mult.reshape(-1), loc.reshape(-1)
     out_m, out_l, off = {}, {}, 0
+
+    def cell_major(a, k):
+        # planar [P][py][px][jy][jx] -> row-major cells [iy*m + ix][P]
+        h = 2 ** (k - 1)
+        return a.reshape(P, 2, 2, h, h).transpose(3, 1, 4, 2, 0).reshape(4**k, P)
+
     for k in range(2, lv + 1):
         r = dom[2] / 2**k
         kk = np.arange(P)
-        out_m[k] = mult[off: off + 4**k] * (r ** (kk + 1) * fact)[None, :]
-        out_l[k] = loc[off: off + 4**k] * (((-1.0) ** kk) / (fact * r**kk))[None, :]
-        off += 4**k
+        out_m[k] = cell_major(mult[off: off + 4**k * P], k) * (r ** (kk + 1) * fact)[None, :]
+        out_l[k] = cell_major(loc[off: off + 4**k * P], k) * (((-1.0) ** kk) / (fact * r**kk))[None, :]
+        off += 4**k * P
     return out_m, out_l
 
 
