@@ -77,7 +77,8 @@ typedef struct vfmm_layout {
     size_t sources;       /* double4 [n]     (x, y, gamma, -1/(2 sigma^2 ln2)) sorted */
     size_t near_uv;       /* double2 [3][n]  near-field (u, v) partial sums per neighbourhood row, sorted order */
     size_t mult;          /* double2 [sum_{k=2..l} 4^k (p+1)]  scaled multipoles, level 2 first */
-    size_t loc;           /* double2 [same]  scaled locals, level 2 first */
+    size_t loc;           /* double2 [same]  scaled locals (M2L part at the leaf level), level 2 first */
+    size_t leaf_loc;      /* double2 [4^l][p+1] completed leaf locals, cell-major */
     size_t counts;        /* int32  [sum_{k=0..l} 4^k] per-level occupancy, level 0 first */
     size_t total;         /* workspace bytes */
 } vfmm_layout;

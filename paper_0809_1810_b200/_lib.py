@@ -77,6 +77,7 @@ class VfmmLayout(ctypes.Structure):
         ("near_uv", ctypes.c_size_t),
         ("mult", ctypes.c_size_t),
         ("loc", ctypes.c_size_t),
+        ("leaf_loc", ctypes.c_size_t),
         ("counts", ctypes.c_size_t),
         ("total", ctypes.c_size_t),
     ]

@@ -200,8 +200,10 @@ bool make_layout(int64_t n, int levels, int order, Layout* L) {
     L->count_off[levels + 1] = cc;
     L->max_tasks = (size_t)((n + 31) / 32) + ((size_t)n < L->nleaves ? (size_t)n : L->nleaves);
     const size_t hist_elems = B * (size_t)L->nchunks;
-    const size_t a1 = scan_aux_elems((int64_t)hist_elems), a2 = scan_aux_elems((int64_t)L->nleaves);
-    L->scan_aux_elems = a1 > a2 ? a1 : a2;
+    const size_t t1 = scan_tiles((int64_t)hist_elems), t2 = scan_tiles((int64_t)L->nleaves);
+    L->scan_state_tiles = t1 > t2 ? t1 : t2;
+    // one look-back state per radix pass + one for the task scan
+    L->scan_state_bytes = sizeof(unsigned long long) * (L->scan_state_tiles + 1) * (L->passes + 1);
 
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -214,15 +216,16 @@ bool make_layout(int64_t n, int levels, int order, Layout* L) {
     L->key_b = take(sizeof(int) * n);
     L->val_a = take(sizeof(int) * n);
     L->val_b = take(sizeof(int) * n);
-    L->hist = take(sizeof(int) * hist_elems);
+    L->hist = take(sizeof(int) * hist_elems * L->passes);
     L->task_scratch = take(sizeof(int) * L->nleaves);
-    L->scan_aux = take(sizeof(int) * L->scan_aux_elems);
+    L->scan_state = take(L->scan_state_bytes);
     L->src = take(sizeof(Src) * n);
     L->near_uv = take(sizeof(double2) * n * kNearRows);
     L->leaf_starts = take(sizeof(int) * (L->nleaves + 1));
     L->counts = take(sizeof(int) * cc);
     L->mult = take(sizeof(double2) * cells * L->P);
     L->loc = take(sizeof(double2) * cells * L->P);
+    L->leaf_loc = take(sizeof(double2) * L->nleaves * L->P);
     L->tasks = take(sizeof(int2) * L->max_tasks);
     L->total = off;
     return true;
@@ -274,6 +277,7 @@ int vfmm_layout_of(int64_t n, int levels, int order, vfmm_layout* out) {
     out->near_uv = L.near_uv;
     out->mult = L.mult;
     out->loc = L.loc;
+    out->leaf_loc = L.leaf_loc;
     out->counts = L.counts;
     out->total = L.total;
     return VFMM_OK;
@@ -316,16 +320,11 @@ int vfmm_evaluate(const double* x, const double* y, const double* gamma, const d
     rec(0, s);
     // ---- build: binning, stable sort, pack, leaf starts, occupancy, tasks ----
     launch_init_counters(ctr, s);
-    launch_keys(x, y, kernel == VFMM_KERNEL_GAUSSIAN ? sigma : nullptr, n, xmin, ymin, side, levels,
-                (int*)(ws + L.key_a), (int*)(ws + L.val_a), ctr, s);
     int* keys = nullptr;
     int* perm = nullptr;
-    launch_sort(L, ws, s, &keys, &perm);
-    launch_pack(x, y, gamma, kernel == VFMM_KERNEL_GAUSSIAN ? sigma : nullptr, perm, n, src, s);
-    launch_leaf_starts(keys, n, (int)L.nleaves, ls, s);
-    launch_counts(L, ls, counts, s);
-    if (!far_only)
-        launch_tasks(L, ls, (int*)(ws + L.task_scratch), tasks, (int*)(ws + L.scan_aux), ctr, s);
+    launch_build(L, x, y, gamma, kernel == VFMM_KERNEL_GAUSSIAN ? sigma : nullptr, xmin, ymin, side,
+                 ws, ctr, s, &keys, &perm);
+    launch_counts_tasks(L, ws, ctr, !far_only, s);
     rec(1, s);
     // Overlap: the far-field chain runs on a high-priority stream and the near
     // field on a low-priority one; P2P CTAs are short-lived, so far-field CTAs
@@ -345,7 +344,7 @@ int vfmm_evaluate(const double* x, const double* y, const double* gamma, const d
     launch_m2l(L, T, mult, counts, loc, ctr, fs);
     rec(3, fs);
     // ---- downward ----
-    launch_l2l(L, T, loc, fs);
+    launch_l2l(L, T, loc, (double2*)(ws + L.leaf_loc), fs);
     rec(4, fs);
     if (overlap) {
         cudaEventRecord(R->join_far, fs);
@@ -359,7 +358,7 @@ int vfmm_evaluate(const double* x, const double* y, const double* gamma, const d
     if (!far_only) {
         if (!overlap) launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, s);
         rec(5, s);
-        launch_l2p_combine(L, T, src, keys, perm, loc, near_uv, xmin, ymin, side, u, v, s);
+        launch_l2p_combine(L, T, src, keys, perm, (const double2*)(ws + L.leaf_loc), near_uv, xmin, ymin, side, u, v, s);
     }
     rec(6, s);
     if (cudaGetLastError() != cudaSuccess) return VFMM_ECUDA;
@@ -425,7 +424,7 @@ int vfmm_evaluate_at(const double* tx, const double* ty, int64_t m, int64_t n, d
     Counters* ctr = (Counters*)(ws + L.counters);
     launch_init_counters(ctr, s);
     launch_eval_at(L, T, tx, ty, m, (const Src*)(ws + L.src), (const int*)(ws + L.leaf_starts),
-                   (const double2*)(ws + L.loc), xmin, ymin, side, kernel, u, v, ctr, s);
+                   (const double2*)(ws + L.leaf_loc), xmin, ymin, side, kernel, u, v, ctr, s);
     if (cudaGetLastError() != cudaSuccess) return VFMM_ECUDA;
     if (bad_count) {
         if (cudaStreamSynchronize(s) != cudaSuccess) return VFMM_ECUDA;

@@ -21,7 +21,7 @@ constexpr int kL2LThreads = 128;
 template <int TN>
 __global__ void __launch_bounds__(kL2LThreads)
     k_l2l(const double2* __restrict__ parent, double2* __restrict__ child, int level, int P,
-          const Tables* __restrict__ T) {
+          const Tables* __restrict__ T, double2* __restrict__ leaf_out) {
     __shared__ double2 sF[kOrderCap + 16];
     __shared__ double s2[kOrderCap + 16];
     const int half = 1 << (level - 1);
@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(kL2LThreads)
     double ax[TN], ay[TN];
 #pragma unroll
     for (int t = 0; t < TN; ++t) ax[t] = ay[t] = 0.0;
+#pragma unroll 4
     for (int m = n0; m < P; ++m) {
         const double2 a = L[m * ps];
         const double axs = a.x * s2[m], ays = a.y * s2[m];
@@ -55,29 +56,52 @@ __global__ void __launch_bounds__(kL2LThreads)
             }
         }
     }
-    double2* out = child + q * np + j;
+    const double2* in = child + q * np + j;
     const int64_t cs = 4 * np;
+    // final level: completed leaf locals go to the cell-major leaf array
+    // (contiguous per leaf for L2P); otherwise accumulate in place
+    double2* out = child + q * np + j;
+    int64_t os = cs;
+    if (leaf_out) {
+        const int mc = 2 * half;
+        out = leaf_out + ((int64_t)(2 * jy + (q >> 1)) * mc + 2 * jx + (q & 1)) * P;
+        os = 1;
+    }
 #pragma unroll
     for (int t = 0; t < TN; ++t) {
         const int nn = n0 + t;
         if (nn < P) {
-            double2 cur = out[nn * cs];
+            double2 cur = in[nn * cs];
             cur.x += ax[t];
             cur.y += ay[t];
-            out[nn * cs] = cur;
+            out[nn * os] = cur;
         }
     }
 }
 
+// levels == 2 has no L2L: copy the level-2 planar locals to the cell-major leaf array
+__global__ void k_leaf_locals_copy(const double2* __restrict__ loc2, int P, double2* __restrict__ out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 16 * P) return;
+    const int cell = t / P, n = t % P;
+    out[t] = loc2[n * coef_stride(2) + coef_base(2, cell & 3, cell >> 2)];
+}
+
 template <int TN>
-void launch_l2l_tn(const Layout& L, const Tables* T, double2* loc, cudaStream_t s) {
+void launch_l2l_tn(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc,
+                   cudaStream_t s) {
     const int nchunks = (L.P + TN - 1) / TN;
     for (int level = 3; level <= L.levels; ++level) {
         const int64_t np = 1ll << (2 * (level - 1));
         const int64_t bpp = (np + kL2LThreads - 1) / kL2LThreads;
         const double2* parent = loc + L.level_cell_off[level - 1] * L.P;
         double2* child = loc + L.level_cell_off[level] * L.P;
-        k_l2l<TN><<<(unsigned)(bpp * 4 * nchunks), kL2LThreads, 0, s>>>(parent, child, level, L.P, T);
+        k_l2l<TN><<<(unsigned)(bpp * 4 * nchunks), kL2LThreads, 0, s>>>(
+            parent, child, level, L.P, T, level == L.levels ? leaf_loc : nullptr);
+        note_launches(1);
+    }
+    if (L.levels == 2) {
+        k_leaf_locals_copy<<<(16 * L.P + 127) / 128, 128, 0, s>>>(loc, L.P, leaf_loc);
         note_launches(1);
     }
 }
@@ -120,8 +144,7 @@ __global__ void __launch_bounds__(256)
     const double inv_r = 1.0 / r;
     const Src s = src[i];
     const double2 f =
-        eval_local(loc + coef_base(levels, ix, iy), coef_stride(levels), P, (s.x - cx) * inv_r,
-                   (s.y - cy) * inv_r, sfact);
+        eval_local(loc + (int64_t)leaf * P, 1, P, (s.x - cx) * inv_r, (s.y - cy) * inv_r, sfact);
     // near field = the three neighbourhood-row partial sums, in row order
     const double2 n0 = near_uv[i], n1 = near_uv[n + i], n2 = near_uv[2 * n + i];
     const double2 nv = make_double2((n0.x + n1.x) + n2.x, (n0.y + n1.y) + n2.y);
@@ -164,8 +187,8 @@ __global__ void __launch_bounds__(256)
     const double r = side / m;
     const double cx = cell_center(xmin, ix, r), cy = cell_center(ymin, iy, r);
     const double inv_r = 1.0 / r;
-    const double2 f = eval_local(loc + coef_base(levels, ix, iy), coef_stride(levels), P,
-                                 (x - cx) * inv_r, (y - cy) * inv_r, sfact);
+    const double2 f = eval_local(loc + ((int64_t)iy * m + ix) * P, 1, P, (x - cx) * inv_r,
+                                 (y - cy) * inv_r, sfact);
     double nu = 0.0, nv = 0.0;
     const int xlo = ix > 0 ? ix - 1 : 0, xhi = ix < m - 1 ? ix + 1 : m - 1;
     for (int ny = iy - 1; ny <= iy + 1; ++ny) {
@@ -182,20 +205,20 @@ __global__ void __launch_bounds__(256)
 
 }  // namespace
 
-void launch_l2l(const Layout& L, const Tables* T, double2* loc, cudaStream_t s) {
+void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc, cudaStream_t s) {
     switch (coef_chunk(L.P)) {
-        case 4: launch_l2l_tn<4>(L, T, loc, s); break;
-        case 5: launch_l2l_tn<5>(L, T, loc, s); break;
-        case 6: launch_l2l_tn<6>(L, T, loc, s); break;
-        case 7: launch_l2l_tn<7>(L, T, loc, s); break;
-        default: launch_l2l_tn<8>(L, T, loc, s); break;
+        case 4: launch_l2l_tn<4>(L, T, loc, leaf_loc, s); break;
+        case 5: launch_l2l_tn<5>(L, T, loc, leaf_loc, s); break;
+        case 6: launch_l2l_tn<6>(L, T, loc, leaf_loc, s); break;
+        case 7: launch_l2l_tn<7>(L, T, loc, leaf_loc, s); break;
+        default: launch_l2l_tn<8>(L, T, loc, leaf_loc, s); break;
     }
 }
 
 void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const int* keys,
                         const int* perm, const double2* loc, const double2* near_uv, double xmin,
                         double ymin, double side, double* u, double* v, cudaStream_t s) {
-    const double2* leaf_loc = loc + L.level_cell_off[L.levels] * L.P;
+    const double2* leaf_loc = loc;
     k_l2p_combine<<<(unsigned)((L.n + 255) / 256), 256, 0, s>>>(
         src, keys, perm, leaf_loc, near_uv, L.n, L.levels, L.P, xmin, ymin, side, T, u, v);
     note_launches(1);
@@ -205,7 +228,7 @@ void launch_eval_at(const Layout& L, const Tables* T, const double* tx, const do
                     int64_t m, const Src* src, const int* leaf_starts, const double2* loc,
                     double xmin, double ymin, double side, int kernel, double* u, double* v,
                     Counters* ctr, cudaStream_t s) {
-    const double2* leaf_loc = loc + L.level_cell_off[L.levels] * L.P;
+    const double2* leaf_loc = loc;
     const unsigned g = (unsigned)((m + 255) / 256);
     if (kernel == VFMM_KERNEL_GAUSSIAN)
         k_eval_at<true><<<g, 256, 0, s>>>(tx, ty, m, src, leaf_starts, leaf_loc, L.levels, L.P,

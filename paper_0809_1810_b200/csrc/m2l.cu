@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(kM2LThreads)
             // source plane / index (floor division of the shifted coordinates)
             const int sp = ((sy & 1) << 1) | (sx & 1);
             const double2* Ms = M + sp * psz + (live ? (int64_t)(sy >> 1) * half + (sx >> 1) : 0);
+#pragma unroll 2
             for (int n = 0; n < P; ++n) {
                 double2 a = Ms[n * cstride];
                 if (!live) a = make_double2(0.0, 0.0);

@@ -2,13 +2,16 @@
 //
 // Replaces quadtree.build_tree / grid_indices / Tree.__init__
 // (quadtree.py:39-46, 116-134, 182-201) and the permutation in
-// engine.evaluate (engine.py:355-358):
-//   k_keys        floor-rule binning with max-edge clamp + domain check + max sigma
-//   LSD radix     stable sort of the row-major leaf keys (== np.argsort(kind="stable"))
-//   k_pack        gather x, y, gamma, sigma into the sorted Src records
-//   k_leaf_starts leaf_starts[4^l + 1] (== concatenate([0], cumsum(bincount)))
-//   k_counts      per-level occupancy pyramid (Tree.counts)
-//   k_tasks_*     32-target warp tasks for the near-field kernel
+// engine.evaluate (engine.py:355-358).  Kernel sequence (config 2: 9 launches):
+//   k_keys_hist     floor-rule binning with max-edge clamp + domain check + max
+//                   sigma + digit-0 histogram per warp chunk; zeroes scratch
+//   k_scan          single-pass exclusive scan (decoupled look-back)
+//   k_radix_scatter stable LSD scatter; also histograms the next digit per
+//                   output chunk; the last pass gathers x, y, gamma, sigma
+//                   into the sorted Src records (np.argsort(kind="stable"))
+//   k_leaf_starts   leaf_starts[4^l + 1] (== concatenate([0], cumsum(bincount)))
+//   k_counts_tasks  per-level occupancy pyramid (Tree.counts) + P2P task counts
+//   k_scan, k_tasks_fill   near-field warp task list
 #include <climits>
 
 #include "vfmm_internal.cuh"
@@ -17,79 +20,91 @@ namespace vfmm {
 
 namespace {
 
+constexpr int kWPB = 8;  // warps per block in the radix kernels
+
 __device__ __forceinline__ unsigned long long ordered_bits(double d) {
     unsigned long long b = (unsigned long long)__double_as_longlong(d);
     return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
 }
 
-__global__ void k_keys(const double* __restrict__ x, const double* __restrict__ y,
-                       const double* __restrict__ sigma, int64_t n, double xmin, double ymin,
-                       double side, int levels, int* __restrict__ key, int* __restrict__ val,
-                       Counters* ctr) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long sbits = 0ull;
-    if (i < n) {
-        const double xi = x[i], yi = y[i];
-        const double xmax = xmin + side, ymax = ymin + side;  // Domain.xmax (model.py:51-57)
-        const bool inside = (xi >= xmin) && (xi <= xmax) && (yi >= ymin) && (yi <= ymax);
-        const int m = 1 << levels;
-        int ix = 0, iy = 0;
-        if (inside) {
-            // quadtree.py:44-45: min(int((x - xmin) / side * m), m - 1)
-            const double tx = (xi - xmin) / side * (double)m;
-            const double ty = (yi - ymin) / side * (double)m;
-            ix = (int)tx;
-            iy = (int)ty;
-            ix = ix < m - 1 ? ix : m - 1;
-            iy = iy < m - 1 ? iy : m - 1;
-        } else {
-            atomicAdd(&ctr->bad_count, 1);
-            atomicMin(&ctr->first_bad, (int)i);
-        }
-        key[i] = iy * m + ix;
-        val[i] = (int)i;
-        if (sigma) sbits = ordered_bits(sigma[i]);
-    }
-    // block max of the sigma bits, one atomic per block
-    __shared__ unsigned long long wmax[32];
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long t = __shfl_xor_sync(0xffffffffu, sbits, o);
-        sbits = t > sbits ? t : sbits;
-    }
-    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = sbits;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) sbits = wmax[w] > sbits ? wmax[w] : sbits;
-        if (sbits) atomicMax(&ctr->sigma_max_bits, sbits);
-    }
-}
-
-constexpr int kWPB = 8;  // warps per block in the radix kernels
-
-__global__ void k_radix_hist(const int* __restrict__ keys, int64_t n, int shift, int bits, int wc,
-                             int nchunks, int* __restrict__ hist) {
+// Warp chunk c = elements [c*wc, (c+1)*wc).  Also zeroes the scratch words
+// (later histograms, scan look-back state) with a grid-stride loop.
+__global__ void __launch_bounds__(kWPB * 32)
+    k_keys_hist(const double* __restrict__ x, const double* __restrict__ y,
+                const double* __restrict__ sigma, int64_t n, double xmin, double ymin, double side,
+                int levels, int bits, int wc, int nchunks, int* __restrict__ key,
+                int* __restrict__ hist0, unsigned* __restrict__ zero, int64_t nzero,
+                Counters* __restrict__ ctr) {
     extern __shared__ int sh[];
+    __shared__ unsigned long long wmax[kWPB];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t z = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; z < nzero;
+         z += (int64_t)gridDim.x * blockDim.x)
+        zero[z] = 0u;
     const int B = 1 << bits;
     int* h = sh + warp * B;
     for (int d = lane; d < B; d += 32) h[d] = 0;
     __syncwarp();
+    const int m = 1 << levels;
+    const double xmax = xmin + side, ymax = ymin + side;  // Domain.xmax (model.py:51-57)
+    unsigned long long sbits = 0ull;
     const int64_t chunk = (int64_t)blockIdx.x * kWPB + warp;
     if (chunk < nchunks) {
         const int64_t beg = chunk * wc;
         const int64_t end = beg + wc < n ? beg + wc : n;
-        for (int64_t i = beg + lane; i < end; i += 32) atomicAdd(&h[(keys[i] >> shift) & (B - 1)], 1);
+#pragma unroll 4
+        for (int64_t i = beg + lane; i < end; i += 32) {
+            const double xi = x[i], yi = y[i];
+            const bool inside = (xi >= xmin) && (xi <= xmax) && (yi >= ymin) && (yi <= ymax);
+            int ix = 0, iy = 0;
+            if (inside) {
+                // quadtree.py:44-45: min(int((x - xmin) / side * m), m - 1)
+                const double tx = (xi - xmin) / side * (double)m;
+                const double ty = (yi - ymin) / side * (double)m;
+                ix = (int)tx;
+                iy = (int)ty;
+                ix = ix < m - 1 ? ix : m - 1;
+                iy = iy < m - 1 ? iy : m - 1;
+            } else {
+                atomicAdd(&ctr->bad_count, 1);
+                atomicMin(&ctr->first_bad, (int)i);
+            }
+            const int k = iy * m + ix;
+            key[i] = k;
+            atomicAdd(&h[k & (B - 1)], 1);
+            if (sigma) {
+                const unsigned long long b = ordered_bits(sigma[i]);
+                sbits = b > sbits ? b : sbits;
+            }
+        }
         __syncwarp();
-        for (int d = lane; d < B; d += 32) hist[(int64_t)d * nchunks + chunk] = h[d];
+        for (int d = lane; d < B; d += 32) hist0[(int64_t)d * nchunks + chunk] = h[d];
+    }
+    // block max of the sigma bits, one atomic per block
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, sbits, o);
+        sbits = t > sbits ? t : sbits;
+    }
+    if (lane == 0) wmax[warp] = sbits;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kWPB; ++w) sbits = wmax[w] > sbits ? wmax[w] : sbits;
+        if (sbits) atomicMax(&ctr->sigma_max_bits, sbits);
     }
 }
 
-// Stable scatter: warp chunks are processed in index order, lanes in index
-// order within a round, equal digits ranked by lane (match_any), so the
-// relative order of equal keys is preserved (LSD radix => stable argsort).
-__global__ void k_radix_scatter(const int* __restrict__ kin, const int* __restrict__ vin,
-                                int* __restrict__ kout, int* __restrict__ vout, int64_t n, int shift,
-                                int bits, int wc, int nchunks, const int* __restrict__ offs) {
+// Stable scatter of one LSD pass: warp chunks are processed in index order,
+// lanes in index order within a round, equal digits ranked by lane
+// (match_any), so the relative order of equal keys is preserved.  Non-final
+// passes histogram the next digit per OUTPUT chunk (integer atomics: the
+// counts are exact); the final pass writes the packed Src records.
+__global__ void __launch_bounds__(kWPB * 32)
+    k_radix_scatter(const int* __restrict__ kin, const int* __restrict__ vin,
+                    int* __restrict__ kout, int* __restrict__ vout, int64_t n, int shift, int bits,
+                    int wc, int nchunks, const int* __restrict__ offs, int* __restrict__ hist_next,
+                    const double* __restrict__ x, const double* __restrict__ y,
+                    const double* __restrict__ g, const double* __restrict__ sigma,
+                    Src* __restrict__ src) {
     extern __shared__ int sh[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int B = 1 << bits;
@@ -101,32 +116,54 @@ __global__ void k_radix_scatter(const int* __restrict__ kin, const int* __restri
     const unsigned lt = (1u << lane) - 1u;
     const int64_t beg = chunk * wc;
     const int64_t end = beg + wc < n ? beg + wc : n;
-    for (int64_t base = beg; base < end; base += 32) {
+    constexpr int R = 4;  // rounds whose loads are issued together
+    for (int64_t base0 = beg; base0 < end; base0 += 32 * R) {
+    int kr[R], vr[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = base0 + 32 * r + lane;
+        kr[r] = i < end ? kin[i] : 0;
+        vr[r] = i < end ? (vin ? vin[i] : (int)i) : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t base = base0 + 32 * r;
         const int64_t i = base + lane;
         const bool valid = i < end;
-        int k = 0, v = 0, d = B + lane;
-        if (valid) {
-            k = kin[i];
-            v = vin[i];
-            d = (k >> shift) & (B - 1);
-        }
+        const int k = kr[r], v = vr[r];
+        const int d = valid ? (k >> shift) & (B - 1) : B + lane;
         const unsigned peers = __match_any_sync(0xffffffffu, d);
         const int rank = __popc(peers & lt);
         if (valid) {
             const int pos = run[d] + rank;
             kout[pos] = k;
             vout[pos] = v;
+            if (hist_next) {
+                atomicAdd(&hist_next[(int64_t)((k >> (shift + bits)) & (B - 1)) * nchunks + pos / wc], 1);
+            } else {
+                const double s = sigma ? sigma[v] : 1.0;
+                Src r;
+                r.x = x[v];
+                r.y = y[v];
+                r.g = g[v];
+                // -r^2 / (2 sigma^2) (engine.py:256) expressed in log2 units
+                r.q2 = -1.4426950408889634 / (2.0 * s * s);
+                src[pos] = r;
+            }
         }
         __syncwarp();
         if (valid && rank == __popc(peers) - 1) run[d] += __popc(peers);
         __syncwarp();
     }
+    }
 }
 
-// ---- exclusive scan (int32, in place): block scan + top scan + add ----
+// ---- single-pass exclusive scan (int32, in place), decoupled look-back ----
 constexpr int kScanThreads = 512;
 constexpr int kScanItems = 4;
 constexpr int kScanTile = kScanThreads * kScanItems;
+constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
 __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_sums, int* total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -152,10 +189,19 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_sums, int* 
     return warp_sums[warp] + incl - v;
 }
 
-__global__ void k_scan_local(int* __restrict__ data, int64_t n, int* __restrict__ block_sums) {
+// state[0] = tile ticket, state[1 + t] = status of tile t (all zero on entry).
+// Tiles are numbered by ticket, so every predecessor of a running tile has
+// started and the look-back always terminates.
+__global__ void __launch_bounds__(kScanThreads)
+    k_scan(int* __restrict__ data, int64_t n, unsigned long long* __restrict__ state) {
     __shared__ int warp_sums[32];
     __shared__ int total;
-    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    __shared__ int tile_s;
+    __shared__ long long prefix_s;
+    if (threadIdx.x == 0) tile_s = (int)atomicAdd(&state[0], 1ull);
+    __syncthreads();
+    const int tile = tile_s;
+    const int64_t base = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
     int vals[kScanItems];
     int s = 0;
 #pragma unroll
@@ -164,50 +210,34 @@ __global__ void k_scan_local(int* __restrict__ data, int64_t n, int* __restrict_
         s += vals[j];
     }
     int run = block_exclusive_scan(s, warp_sums, &total);
+    if (threadIdx.x == 0) {
+        volatile unsigned long long* st = state + 1;
+        long long prefix = 0;
+        if (tile == 0) {
+            __threadfence();
+            st[0] = kFlagIncl | (unsigned long long)total;
+        } else {
+            st[tile] = kFlagAgg | (unsigned long long)total;
+            __threadfence();
+            for (int j = tile - 1; j >= 0;) {
+                const unsigned long long w = st[j];
+                if ((w >> 62) == 0) continue;  // predecessor not published yet
+                prefix += (long long)(w & kValMask);
+                if (w & kFlagIncl) break;
+                --j;
+            }
+            __threadfence();
+            st[tile] = kFlagIncl | (unsigned long long)(prefix + total);
+        }
+        prefix_s = prefix;
+    }
+    __syncthreads();
+    run += (int)prefix_s;
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
         if (base + j < n) data[base + j] = run;
         run += vals[j];
     }
-    if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
-}
-
-__global__ void k_scan_top(int* __restrict__ sums, int nb) {
-    __shared__ int warp_sums[32];
-    __shared__ int total;
-    int carry = 0;
-    for (int base = 0; base < nb; base += blockDim.x) {
-        const int i = base + threadIdx.x;
-        const int v = i < nb ? sums[i] : 0;
-        const int ex = block_exclusive_scan(v, warp_sums, &total);
-        if (i < nb) sums[i] = ex + carry;
-        carry += total;
-        __syncthreads();
-    }
-}
-
-__global__ void k_scan_add(int* __restrict__ data, int64_t n, const int* __restrict__ block_sums) {
-    const int64_t base = (int64_t)blockIdx.x * kScanTile;
-    const int add = block_sums[blockIdx.x];
-    for (int j = threadIdx.x; j < kScanTile; j += blockDim.x) {
-        if (base + j < n) data[base + j] += add;
-    }
-}
-
-__global__ void k_pack(const double* __restrict__ x, const double* __restrict__ y,
-                       const double* __restrict__ g, const double* __restrict__ sigma,
-                       const int* __restrict__ perm, int64_t n, Src* __restrict__ src) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int j = perm[i];
-    const double s = sigma ? sigma[j] : 1.0;
-    Src r;
-    r.x = x[j];
-    r.y = y[j];
-    r.g = g[j];
-    // -r^2 / (2 sigma^2) (engine.py:256) expressed in log2 units
-    r.q2 = -1.4426950408889634 / (2.0 * s * s);
-    src[i] = r;
 }
 
 __global__ void k_leaf_starts(const int* __restrict__ keys, int64_t n, int nleaves,
@@ -219,8 +249,11 @@ __global__ void k_leaf_starts(const int* __restrict__ keys, int64_t n, int nleav
     for (int k = prev + 1; k <= cur; ++k) ls[k] = (int)i;
 }
 
-__global__ void k_counts(const int* __restrict__ ls, int levels, int64_t total_cells,
-                         int* __restrict__ counts) {
+// Occupancy of every cell of every level (level 0 first) from leaf_starts:
+// a level-k cell covers 2^(l-k) leaf rows, each a contiguous leaf range.
+// Leaf cells also emit their P2P task count ceil(count / chunk).
+__global__ void k_counts_tasks(const int* __restrict__ ls, int levels, int64_t total_cells,
+                               int chunk, int* __restrict__ counts, int* __restrict__ ntask) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= total_cells) return;
     int k = 0;
@@ -240,14 +273,7 @@ __global__ void k_counts(const int* __restrict__ ls, int levels, int64_t total_c
         c += ls[row + (int64_t)(ix + 1) * s] - ls[row + (int64_t)ix * s];
     }
     counts[t] = c;
-}
-
-__global__ void k_tasks_count(const int* __restrict__ ls, int nleaves, int chunk,
-                              int* __restrict__ nt) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nleaves) return;
-    const int c = ls[i + 1] - ls[i];
-    nt[i] = (c + chunk - 1) / chunk;
+    if (k == levels) ntask[cell] = (c + chunk - 1) / chunk;
 }
 
 __global__ void k_tasks_fill(const int* __restrict__ ls, int nleaves, int chunk,
@@ -280,56 +306,49 @@ void launch_init_counters(Counters* ctr, cudaStream_t s) {
     note_launches(1);
 }
 
-void launch_keys(const double* x, const double* y, const double* sigma, int64_t n, double xmin,
-                 double ymin, double side, int levels, int* key, int* val, Counters* ctr,
-                 cudaStream_t s) {
-    k_keys<<<grid_for(n, 256), 256, 0, s>>>(x, y, sigma, n, xmin, ymin, side, levels, key, val, ctr);
-    note_launches(1);
-}
+size_t scan_tiles(int64_t n) { return (size_t)((n + kScanTile - 1) / kScanTile); }
 
-void launch_scan_i32(int* data, int64_t n, int* aux, cudaStream_t s) {
+void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream_t s) {
     if (n <= 0) return;
-    const int64_t nb = (n + kScanTile - 1) / kScanTile;
-    k_scan_local<<<(unsigned)nb, kScanThreads, 0, s>>>(data, n, aux);
-    note_launches(1);
-    k_scan_top<<<1, 1024, 0, s>>>(aux, (int)nb);
-    note_launches(1);
-    if (nb > 1) k_scan_add<<<(unsigned)nb, 256, 0, s>>>(data, n, aux);
+    k_scan<<<(unsigned)scan_tiles(n), kScanThreads, 0, s>>>(data, n, state);
     note_launches(1);
 }
 
-size_t scan_aux_elems(int64_t n) { return (size_t)((n + kScanTile - 1) / kScanTile) + 1; }
-
-void launch_sort(const Layout& L, char* ws, cudaStream_t s, int** keys_out, int** perm_out) {
-    int* ka = (int*)(ws + L.key_a);
-    int* kb = (int*)(ws + L.key_b);
-    int* va = (int*)(ws + L.val_a);
-    int* vb = (int*)(ws + L.val_b);
-    int* hist = (int*)(ws + L.hist);
-    int* aux = (int*)(ws + L.scan_aux);
+void launch_build(const Layout& L, const double* x, const double* y, const double* g,
+                  const double* sigma, double xmin, double ymin, double side, char* ws,
+                  Counters* ctr, cudaStream_t s, int** keys_out, int** perm_out) {
+    int* kbuf[2] = {(int*)(ws + L.key_a), (int*)(ws + L.key_b)};
+    int* vbuf[2] = {(int*)(ws + L.val_a), (int*)(ws + L.val_b)};
     const int bits = L.digit_bits;
     const int B = 1 << bits;
+    const int64_t hsize = (int64_t)B * L.nchunks;
+    auto hist = [&](int p) { return (int*)(ws + L.hist) + p * hsize; };
+    auto state = [&](int i) {
+        return (unsigned long long*)(ws + L.scan_state) + (size_t)i * (L.scan_state_tiles + 1);
+    };
     const unsigned blocks = (unsigned)((L.nchunks + kWPB - 1) / kWPB);
     const size_t shm = (size_t)kWPB * B * sizeof(int);
-    for (int pass = 0; pass < L.passes; ++pass) {
-        const int shift = pass * bits;
-        k_radix_hist<<<blocks, kWPB * 32, shm, s>>>(ka, L.n, shift, bits, L.wc, L.nchunks, hist);
-        note_launches(1);
-        launch_scan_i32(hist, (int64_t)B * L.nchunks, aux, s);
-        k_radix_scatter<<<blocks, kWPB * 32, shm, s>>>(ka, va, kb, vb, L.n, shift, bits, L.wc,
-                                                      L.nchunks, hist);
-        note_launches(1);
-        int* t = ka; ka = kb; kb = t;
-        t = va; va = vb; vb = t;
-    }
-    *keys_out = ka;
-    *perm_out = va;
-}
-
-void launch_pack(const double* x, const double* y, const double* g, const double* sigma,
-                 const int* perm, int64_t n, Src* src, cudaStream_t s) {
-    k_pack<<<grid_for(n, 256), 256, 0, s>>>(x, y, g, sigma, perm, n, src);
+    // scratch zeroed by the first kernel: histograms of passes 1.. and all scan states
+    unsigned* zero = (unsigned*)(ws + L.hist) + hsize;
+    const int64_t nzero_hist = hsize * (L.passes - 1);
+    k_keys_hist<<<blocks, kWPB * 32, shm, s>>>(x, y, sigma, L.n, xmin, ymin, side, L.levels, bits,
+                                              L.wc, L.nchunks, kbuf[0], hist(0), zero, nzero_hist,
+                                              ctr);
     note_launches(1);
+    cudaMemsetAsync(ws + L.scan_state, 0, L.scan_state_bytes, s);
+    for (int p = 0; p < L.passes; ++p) {
+        launch_scan_i32(hist(p), hsize, state(p), s);
+        const bool last = p == L.passes - 1;
+        k_radix_scatter<<<blocks, kWPB * 32, shm, s>>>(
+            kbuf[p & 1], p == 0 ? nullptr : vbuf[p & 1], kbuf[(p + 1) & 1], vbuf[(p + 1) & 1], L.n,
+            p * bits, bits, L.wc, L.nchunks, hist(p), last ? nullptr : hist(p + 1), x, y, g, sigma,
+            (Src*)(ws + L.src));
+        note_launches(1);
+    }
+    *keys_out = kbuf[L.passes & 1];
+    *perm_out = vbuf[L.passes & 1];
+    int* ls = (int*)(ws + L.leaf_starts);
+    launch_leaf_starts(*keys_out, L.n, (int)L.nleaves, ls, s);
 }
 
 void launch_leaf_starts(const int* sorted_keys, int64_t n, int nleaves, int* leaf_starts,
@@ -338,22 +357,20 @@ void launch_leaf_starts(const int* sorted_keys, int64_t n, int nleaves, int* lea
     note_launches(1);
 }
 
-void launch_counts(const Layout& L, const int* leaf_starts, int* counts, cudaStream_t s) {
+void launch_counts_tasks(const Layout& L, char* ws, Counters* ctr, bool tasks, cudaStream_t s) {
+    const int* ls = (const int*)(ws + L.leaf_starts);
+    int* counts = (int*)(ws + L.counts);
+    int* nt = (int*)(ws + L.task_scratch);
     int64_t total = 0;
     for (int k = 0; k <= L.levels; ++k) total += 1ll << (2 * k);
-    k_counts<<<grid_for(total, 256), 256, 0, s>>>(leaf_starts, L.levels, total, counts);
+    const int chunk = 32 * p2p_targets_per_lane();
+    k_counts_tasks<<<grid_for(total, 256), 256, 0, s>>>(ls, L.levels, total, chunk, counts, nt);
     note_launches(1);
-}
-
-void launch_tasks(const Layout& L, const int* leaf_starts, int* task_scratch, int2* tasks,
-                  int* aux, Counters* ctr, cudaStream_t s) {
+    if (!tasks) return;
     const int nl = (int)L.nleaves;
-    k_tasks_count<<<grid_for(nl, 256), 256, 0, s>>>(leaf_starts, nl, 32 * p2p_targets_per_lane(),
-                                                  task_scratch);
-    note_launches(1);
-    launch_scan_i32(task_scratch, nl, aux, s);
-    k_tasks_fill<<<grid_for(nl, 256), 256, 0, s>>>(leaf_starts, nl, 32 * p2p_targets_per_lane(),
-                                                 task_scratch, tasks, ctr);
+    launch_scan_i32(nt, nl, (unsigned long long*)(ws + L.scan_state) +
+                                (size_t)L.passes * (L.scan_state_tiles + 1), s);
+    k_tasks_fill<<<grid_for(nl, 256), 256, 0, s>>>(ls, nl, chunk, nt, (int2*)(ws + L.tasks), ctr);
     note_launches(1);
 }
 

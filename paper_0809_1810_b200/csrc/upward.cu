@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(kM2MThreads)
     for (int t = 0; t < TN; ++t) ax[t] = ay[t] = 0.0;
     for (int q = 0; q < 4; ++q) {
         const double2* M = child + q * np + pidx;
+#pragma unroll 4
         for (int k = 0; k <= kend; ++k) {
             const double2 a = M[(int64_t)k * 4 * np];
 #pragma unroll

@@ -62,12 +62,12 @@ struct Layout {
     int levels, order, P;  // P = order + 1
     int digit_bits, passes, wc, nchunks;
     size_t nleaves;
-    size_t key_a, key_b, val_a, val_b, hist, task_scratch, scan_aux, src, near_uv, leaf_starts,
-        counts, mult, loc, tasks, counters, total;
+    size_t key_a, key_b, val_a, val_b, hist, task_scratch, scan_state, src, near_uv, leaf_starts,
+        counts, mult, loc, leaf_loc, tasks, counters, total;
+    size_t scan_state_tiles, scan_state_bytes;  // per scan instance: 1 ticket + tiles
     size_t level_cell_off[VFMM_LEVELS_CAP + 2];  // cells before level k (k>=2) in mult/loc
     size_t count_off[VFMM_LEVELS_CAP + 2];       // cells before level k in counts
     size_t max_tasks;
-    size_t scan_aux_elems;
 };
 
 bool make_layout(int64_t n, int levels, int order, Layout* L);
@@ -76,26 +76,21 @@ bool make_layout(int64_t n, int levels, int order, Layout* L);
 void note_launches(int k);
 
 // ---- kernels launchers (each enqueues on `s`) ----
-void launch_keys(const double* x, const double* y, const double* sigma, int64_t n, double xmin,
-                 double ymin, double side, int levels, int* key, int* val, Counters* ctr,
-                 cudaStream_t s);
-void launch_sort(const Layout& L, char* ws, cudaStream_t s, int** keys_out, int** perm_out);
-void launch_scan_i32(int* data, int64_t n, int* aux, cudaStream_t s);  // in-place exclusive
-void launch_pack(const double* x, const double* y, const double* g, const double* sigma,
-                 const int* perm, int64_t n, Src* src, cudaStream_t s);
+void launch_build(const Layout& L, const double* x, const double* y, const double* g,
+                  const double* sigma, double xmin, double ymin, double side, char* ws,
+                  Counters* ctr, cudaStream_t s, int** keys_out, int** perm_out);
+void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream_t s);
+size_t scan_tiles(int64_t n);
 void launch_leaf_starts(const int* sorted_keys, int64_t n, int nleaves, int* leaf_starts,
                         cudaStream_t s);
-void launch_counts(const Layout& L, const int* leaf_starts, int* counts, cudaStream_t s);
-void launch_tasks(const Layout& L, const int* leaf_starts, int* task_scratch, int2* tasks,
-                  int* aux, Counters* ctr, cudaStream_t s);
+void launch_counts_tasks(const Layout& L, char* ws, Counters* ctr, bool tasks, cudaStream_t s);
 void launch_p2m(const Layout& L, const Src* src, const int* leaf_starts, double xmin, double ymin,
                 double side, double2* mult_leaf, const Tables* T, cudaStream_t s);
 void launch_init_counters(Counters* ctr, cudaStream_t s);
-size_t scan_aux_elems(int64_t n);
 void launch_m2m(const Layout& L, const Tables* T, double2* mult, cudaStream_t s);
 void launch_m2l(const Layout& L, const Tables* T, const double2* mult, const int* counts,
                 double2* loc, Counters* ctr, cudaStream_t s);
-void launch_l2l(const Layout& L, const Tables* T, double2* loc, cudaStream_t s);
+void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc, cudaStream_t s);
 int p2p_targets_per_lane();  // 1 or 2 (env VFMM_P2P_TPT, default 1)
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
                 const int2* tasks, Counters* ctr, int kernel, double2* near_uv, cudaStream_t s);

@@ -95,7 +95,11 @@ def _unscale(ws, c, dom):
         r = dom[2] / 2**k
         kk = np.arange(P)
         out_m[k] = cell_major(mult[off: off + 4**k * P], k) * (r ** (kk + 1) * fact)[None, :]
-        out_l[k] = cell_major(loc[off: off + 4**k * P], k) * (((-1.0) ** kk) / (fact * r**kk))[None, :]
+        lk = cell_major(loc[off: off + 4**k * P], k)
+        if k == lv:  # completed leaf locals live in the cell-major leaf array
+            ll = ws.view("leaf_loc", torch.float64, 4**lv * P * 2).cpu().numpy().reshape(-1, 2)
+            lk = (ll[:, 0] + 1j * ll[:, 1]).reshape(4**lv, P)
+        out_l[k] = lk * (((-1.0) ** kk) / (fact * r**kk))[None, :]
         off += 4**k * P
     return out_m, out_l
 
