@@ -51,6 +51,9 @@ extern "C" {
                                    far-field chain; phase timings then overlap */
 #define VFMM_FLAG_FAR_ONLY 4u   /* build the tree and the local expansions only (no near field, no
                                    evaluation at the particles); used before vfmm_evaluate_at */
+#define VFMM_FLAG_PHASE_UP 8u   /* vfmm_evaluate_shard: build + P2M + M2M only */
+#define VFMM_FLAG_PHASE_DOWN 16u /* vfmm_evaluate_shard: M2L + L2L + P2P + L2P on the workspace of a
+                                    previous PHASE_UP call (after the caller reduced the multipoles) */
 
 /* engine.FmmRunStats (engine.py:58-74).  Times in milliseconds (CUDA events). */
 typedef struct vfmm_stats {
@@ -99,6 +102,32 @@ int vfmm_evaluate(const double* x, const double* y, const double* gamma, const d
                   int64_t n, double xmin, double ymin, double side, int levels, int order,
                   int kernel, double* u, double* v, void* workspace, size_t workspace_bytes,
                   unsigned flags, vfmm_stats* stats, void* stream);
+
+/* Sharded evaluate (one process per GPU; leaves sharded in row strips).
+ * The local arrays hold this rank's owned particles (leaf rows [row_lo,
+ * row_hi) of the 2^levels x 2^levels leaf grid) plus halo copies of the
+ * particles in leaf rows row_lo-1 and row_hi.  Two phases:
+ *   PHASE_UP   : tree over the local particles; P2M over owned leaves only;
+ *                M2M over the whole pyramid -> partial multipoles.
+ *   (caller)   : sum-all-reduce the multipole region (vfmm_mult_region) and the
+ *                int32 occupancy region (vfmm_counts_region) across ranks --
+ *                multipoles are linear in gamma and each rank counts only its
+ *                owned rows, so the sums are the global pyramids.
+ *   PHASE_DOWN : M2L / L2L for cells touching the owned strip, P2P for owned
+ *                leaves, L2P + combine for owned particles (u, v of halo
+ *                particles are left untouched).
+ * Counters: m2l_count counts destinations whose first leaf row is owned and
+ * near_pair_count owned leaves, so their sums over ranks equal the
+ * single-GPU values.  Replaces engine.evaluate (engine.py:335-398) per shard. */
+int vfmm_evaluate_shard(const double* x, const double* y, const double* gamma, const double* sigma,
+                        int64_t n, double xmin, double ymin, double side, int levels, int order,
+                        int kernel, int row_lo, int row_hi, double* u, double* v, void* workspace,
+                        size_t workspace_bytes, unsigned flags, vfmm_stats* stats, void* stream);
+
+/* Byte ranges of the multipole pyramid (complex128, all levels) and of the
+ * occupancy pyramid (int32, levels 0..l) inside the workspace. */
+int vfmm_mult_region(int64_t n, int levels, int order, size_t* offset, size_t* bytes);
+int vfmm_counts_region(int64_t n, int levels, int order, size_t* offset, size_t* bytes);
 
 /* Read the device counters of the last evaluate that used `workspace`
  * (synchronises `stream`).  Timings are left at 0.                          */

@@ -26,6 +26,8 @@ KERNEL_GAUSSIAN = 1
 FLAG_STATS = 1
 FLAG_OVERLAP = 2
 FLAG_FAR_ONLY = 4
+FLAG_PHASE_UP = 8
+FLAG_PHASE_DOWN = 16
 
 ORDER_CAP = 60
 LEVELS_CAP = 13
@@ -35,6 +37,9 @@ EXPORTED_SYMBOLS = (
     "vfmm_workspace_size",
     "vfmm_layout_of",
     "vfmm_evaluate",
+    "vfmm_evaluate_shard",
+    "vfmm_mult_region",
+    "vfmm_counts_region",
     "vfmm_read_stats",
     "vfmm_evaluate_at",
     "vfmm_direct_workspace_size",
@@ -109,6 +114,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.vfmm_layout_of.argtypes = [_I64, _I, _I, ctypes.POINTER(VfmmLayout)]
         lib.vfmm_evaluate.argtypes = [_P, _P, _P, _P, _I64, _D, _D, _D, _I, _I, _I, _P, _P, _P, _SZ,
                                       ctypes.c_uint, ctypes.POINTER(VfmmStats), _P]
+        lib.vfmm_evaluate_shard.argtypes = [_P, _P, _P, _P, _I64, _D, _D, _D, _I, _I, _I, _I, _I, _P,
+                                            _P, _P, _SZ, ctypes.c_uint, ctypes.POINTER(VfmmStats), _P]
+        lib.vfmm_mult_region.argtypes = [_I64, _I, _I, ctypes.POINTER(_SZ), ctypes.POINTER(_SZ)]
+        lib.vfmm_counts_region.argtypes = [_I64, _I, _I, ctypes.POINTER(_SZ), ctypes.POINTER(_SZ)]
         lib.vfmm_read_stats.argtypes = [_I64, _I, _I, _I, _D, _P, ctypes.POINTER(VfmmStats), _P]
         lib.vfmm_evaluate_at.argtypes = [_P, _P, _I64, _I64, _D, _D, _D, _I, _I, _I, _P, _P, _P,
                                          ctypes.POINTER(_I64), _P]
@@ -136,6 +145,14 @@ def workspace_size(n: int, levels: int, order: int) -> int:
     out = _SZ()
     check(load().vfmm_workspace_size(n, levels, order, ctypes.byref(out)), "vfmm_workspace_size")
     return out.value
+
+
+def region(name: str, n: int, levels: int, order: int) -> tuple[int, int]:
+    """(offset, bytes) of the 'mult' or 'counts' region of a workspace."""
+    off, nbytes = _SZ(), _SZ()
+    fn = getattr(load(), f"vfmm_{name}_region")
+    check(fn(max(n, 1), levels, order, ctypes.byref(off), ctypes.byref(nbytes)), f"vfmm_{name}_region")
+    return off.value, nbytes.value
 
 
 def layout(n: int, levels: int, order: int) -> VfmmLayout:

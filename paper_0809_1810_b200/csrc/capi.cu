@@ -283,18 +283,24 @@ int vfmm_layout_of(int64_t n, int levels, int order, vfmm_layout* out) {
     return VFMM_OK;
 }
 
-int vfmm_evaluate(const double* x, const double* y, const double* gamma, const double* sigma,
+namespace {
+
+// One evaluate (or one phase of a sharded evaluate) over leaf rows [row_lo, row_hi).
+int evaluate_impl(const double* x, const double* y, const double* gamma, const double* sigma,
                   int64_t n, double xmin, double ymin, double side, int levels, int order,
                   int kernel, double* u, double* v, void* workspace, size_t workspace_bytes,
-                  unsigned flags, vfmm_stats* stats, void* stream) {
+                  unsigned flags, Rows rows, vfmm_stats* stats, void* stream) {
     const bool timed = (flags & VFMM_FLAG_STATS) != 0;
     const bool far_only = (flags & VFMM_FLAG_FAR_ONLY) != 0;
-    const bool overlap = (flags & VFMM_FLAG_OVERLAP) != 0 && !far_only;
-    if (!x || !y || !gamma || (!far_only && (!u || !v))) return VFMM_EINVAL;
+    bool up = (flags & VFMM_FLAG_PHASE_UP) != 0, down = (flags & VFMM_FLAG_PHASE_DOWN) != 0;
+    if (!up && !down) up = down = true;
+    const bool overlap = (flags & VFMM_FLAG_OVERLAP) != 0 && !far_only && up && down;
+    if (!x || !y || !gamma || (down && !far_only && (!u || !v))) return VFMM_EINVAL;
     if (kernel == VFMM_KERNEL_GAUSSIAN && !sigma) return VFMM_EINVAL;
     if (timed && !stats) return VFMM_EINVAL;
     if (!args_ok(n, levels, order, side, kernel) || !std::isfinite(xmin) || !std::isfinite(ymin))
         return VFMM_EINVAL;
+    if (rows.lo < 0 || rows.hi > (1 << levels) || rows.lo > rows.hi) return VFMM_EINVAL;
     Layout L;
     make_layout(n, levels, order, &L);
     if (!workspace || workspace_bytes < L.total) return VFMM_EWORKSPACE;
@@ -313,52 +319,60 @@ int vfmm_evaluate(const double* x, const double* y, const double* gamma, const d
     double2* loc = (double2*)(ws + L.loc);
     double2* near_uv = (double2*)(ws + L.near_uv);
     int2* tasks = (int2*)(ws + L.tasks);
+    const bool odd = (L.passes & 1) != 0;
+    int* keys = (int*)(ws + (odd ? L.key_b : L.key_a));
+    int* perm = (int*)(ws + (odd ? L.val_b : L.val_a));
     auto rec = [&](int i, cudaStream_t st) {
         if (timed) cudaEventRecord(R->ev[i], st);
     };
+    for (int i = 0; i < 9; ++i) rec(i, s);  // every event defined even for a single phase
 
-    rec(0, s);
-    // ---- build: binning, stable sort, pack, leaf starts, occupancy, tasks ----
-    launch_init_counters(ctr, s);
-    int* keys = nullptr;
-    int* perm = nullptr;
-    launch_build(L, x, y, gamma, kernel == VFMM_KERNEL_GAUSSIAN ? sigma : nullptr, xmin, ymin, side,
-                 ws, ctr, s, &keys, &perm);
-    launch_counts_tasks(L, ws, ctr, !far_only, s);
-    rec(1, s);
-    // Overlap: the far-field chain runs on a high-priority stream and the near
-    // field on a low-priority one; P2P CTAs are short-lived, so far-field CTAs
-    // are scheduled as soon as any SM slot frees up.
     cudaStream_t fs = s;
-    if (overlap) {
-        cudaEventRecord(R->fork, s);
-        cudaStreamWaitEvent(R->far, R->fork, 0);
-        cudaStreamWaitEvent(R->near, R->fork, 0);
-        fs = R->far;
+    if (up) {
+        rec(0, s);
+        // ---- build: binning, stable sort, pack, leaf starts, occupancy, tasks ----
+        launch_init_counters(ctr, s);
+        launch_build(L, x, y, gamma, kernel == VFMM_KERNEL_GAUSSIAN ? sigma : nullptr, xmin, ymin,
+                     side, ws, ctr, s, &keys, &perm);
+        launch_counts_tasks(L, ws, ctr, !far_only, rows, s);
+        rec(1, s);
+        // Overlap: the far-field chain runs on a high-priority stream and the near
+        // field on a low-priority one; P2P CTAs are short-lived, so far-field CTAs
+        // are scheduled as soon as any SM slot frees up.
+        if (overlap) {
+            cudaEventRecord(R->fork, s);
+            cudaStreamWaitEvent(R->far, R->fork, 0);
+            cudaStreamWaitEvent(R->near, R->fork, 0);
+            fs = R->far;
+        }
+        // ---- upward ----
+        launch_p2m(L, src, ls, xmin, ymin, side, mult + L.level_cell_off[levels] * L.P, T, rows, fs);
+        launch_m2m(L, T, mult, fs);
+        rec(2, fs);
     }
-    // ---- upward ----
-    launch_p2m(L, src, ls, xmin, ymin, side, mult + L.level_cell_off[levels] * L.P, T, fs);
-    launch_m2m(L, T, mult, fs);
-    rec(2, fs);
-    // ---- M2L (all levels, one launch) ----
-    launch_m2l(L, T, mult, counts, loc, ctr, fs);
-    rec(3, fs);
-    // ---- downward ----
-    launch_l2l(L, T, loc, (double2*)(ws + L.leaf_loc), fs);
-    rec(4, fs);
-    if (overlap) {
-        cudaEventRecord(R->join_far, fs);
-        rec(7, R->near);
-        launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, R->near);
-        rec(8, R->near);
-        cudaEventRecord(R->join_near, R->near);
-        cudaStreamWaitEvent(s, R->join_far, 0);
-        cudaStreamWaitEvent(s, R->join_near, 0);
-    }
-    if (!far_only) {
-        if (!overlap) launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, s);
-        rec(5, s);
-        launch_l2p_combine(L, T, src, keys, perm, (const double2*)(ws + L.leaf_loc), near_uv, xmin, ymin, side, u, v, s);
+    if (down) {
+        if (!up) rec(2, s);
+        // ---- M2L (all levels, one launch) ----
+        launch_m2l(L, T, mult, counts, loc, ctr, rows, fs);
+        rec(3, fs);
+        // ---- downward ----
+        launch_l2l(L, T, loc, (double2*)(ws + L.leaf_loc), rows, fs);
+        rec(4, fs);
+        if (overlap) {
+            cudaEventRecord(R->join_far, fs);
+            rec(7, R->near);
+            launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, R->near);
+            rec(8, R->near);
+            cudaEventRecord(R->join_near, R->near);
+            cudaStreamWaitEvent(s, R->join_far, 0);
+            cudaStreamWaitEvent(s, R->join_near, 0);
+        }
+        if (!far_only) {
+            if (!overlap) launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, s);
+            rec(5, s);
+            launch_l2p_combine(L, T, src, keys, perm, (const double2*)(ws + L.leaf_loc), near_uv,
+                               xmin, ymin, side, u, v, rows, s);
+        }
     }
     rec(6, s);
     if (cudaGetLastError() != cudaSuccess) return VFMM_ECUDA;
@@ -369,23 +383,65 @@ int vfmm_evaluate(const double* x, const double* y, const double* gamma, const d
     if (cudaMemcpy(&c, ctr, sizeof c, cudaMemcpyDeviceToHost) != cudaSuccess) return VFMM_ECUDA;
     std::memset(stats, 0, sizeof(*stats));
     fill_stats(L, c, kernel, side, stats);
-    stats->t_build = elapsed(R->ev[0], R->ev[1]);
-    stats->t_upward = elapsed(R->ev[1], R->ev[2]);
-    stats->t_m2l = elapsed(R->ev[2], R->ev[3]);
-    stats->t_downward = elapsed(R->ev[3], R->ev[4]);
-    if (far_only) {
-        stats->t_near = 0.f;
-        stats->t_eval = 0.f;
-    } else if (overlap) {
-        stats->t_near = elapsed(R->ev[7], R->ev[8]);
-        stats->t_eval = elapsed(R->ev[5], R->ev[6]);
-        stats->overlapped = 1;
-    } else {
-        stats->t_near = elapsed(R->ev[4], R->ev[5]);
-        stats->t_eval = elapsed(R->ev[5], R->ev[6]);
+    if (up) {
+        stats->t_build = elapsed(R->ev[0], R->ev[1]);
+        stats->t_upward = elapsed(R->ev[1], R->ev[2]);
     }
-    stats->t_total = elapsed(R->ev[0], R->ev[6]);
+    if (down) {
+        stats->t_m2l = elapsed(R->ev[2], R->ev[3]);
+        stats->t_downward = elapsed(R->ev[3], R->ev[4]);
+        if (far_only) {
+            stats->t_near = 0.f;
+            stats->t_eval = 0.f;
+        } else if (overlap) {
+            stats->t_near = elapsed(R->ev[7], R->ev[8]);
+            stats->t_eval = elapsed(R->ev[5], R->ev[6]);
+            stats->overlapped = 1;
+        } else {
+            stats->t_near = elapsed(R->ev[4], R->ev[5]);
+            stats->t_eval = elapsed(R->ev[5], R->ev[6]);
+        }
+    }
+    stats->t_total = elapsed(R->ev[up ? 0 : 2], R->ev[6]);
     return c.bad_count ? VFMM_EDOMAIN : VFMM_OK;
+}
+
+}  // namespace
+
+int vfmm_evaluate(const double* x, const double* y, const double* gamma, const double* sigma,
+                  int64_t n, double xmin, double ymin, double side, int levels, int order,
+                  int kernel, double* u, double* v, void* workspace, size_t workspace_bytes,
+                  unsigned flags, vfmm_stats* stats, void* stream) {
+    if (levels < 2 || levels > VFMM_LEVELS_CAP) return VFMM_EINVAL;
+    return evaluate_impl(x, y, gamma, sigma, n, xmin, ymin, side, levels, order, kernel, u, v,
+                         workspace, workspace_bytes, flags & ~(VFMM_FLAG_PHASE_UP | VFMM_FLAG_PHASE_DOWN),
+                         Rows{0, 1 << levels}, stats, stream);
+}
+
+int vfmm_evaluate_shard(const double* x, const double* y, const double* gamma, const double* sigma,
+                        int64_t n, double xmin, double ymin, double side, int levels, int order,
+                        int kernel, int row_lo, int row_hi, double* u, double* v, void* workspace,
+                        size_t workspace_bytes, unsigned flags, vfmm_stats* stats, void* stream) {
+    if (levels < 2 || levels > VFMM_LEVELS_CAP) return VFMM_EINVAL;
+    return evaluate_impl(x, y, gamma, sigma, n, xmin, ymin, side, levels, order, kernel, u, v,
+                         workspace, workspace_bytes, flags & ~VFMM_FLAG_OVERLAP,
+                         Rows{row_lo, row_hi}, stats, stream);
+}
+
+int vfmm_counts_region(int64_t n, int levels, int order, size_t* offset, size_t* bytes) {
+    Layout L;
+    if (!offset || !bytes || !make_layout(n, levels, order, &L)) return VFMM_EINVAL;
+    *offset = L.counts;
+    *bytes = sizeof(int) * L.count_off[levels + 1];
+    return VFMM_OK;
+}
+
+int vfmm_mult_region(int64_t n, int levels, int order, size_t* offset, size_t* bytes) {
+    Layout L;
+    if (!offset || !bytes || !make_layout(n, levels, order, &L)) return VFMM_EINVAL;
+    *offset = L.mult;
+    *bytes = sizeof(double2) * L.level_cell_off[levels + 1] * L.P;
+    return VFMM_OK;
 }
 
 int vfmm_read_stats(int64_t n, int levels, int order, int kernel, double side,

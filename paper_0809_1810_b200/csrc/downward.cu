@@ -20,8 +20,8 @@ constexpr int kL2LThreads = 128;
 //   Lh'_n += sum_{m>=n} (2^{-m} Lh_m) F_q[m-n]     (exact re-centring)
 template <int TN>
 __global__ void __launch_bounds__(kL2LThreads)
-    k_l2l(const double2* __restrict__ parent, double2* __restrict__ child, int level, int P,
-          const Tables* __restrict__ T, double2* __restrict__ leaf_out) {
+    k_l2l(const double2* __restrict__ parent, double2* __restrict__ child, int level, int levels,
+          int P, const Tables* __restrict__ T, double2* __restrict__ leaf_out, Rows rows) {
     __shared__ double2 sF[kOrderCap + 16];
     __shared__ double s2[kOrderCap + 16];
     const int half = 1 << (level - 1);
@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(kL2LThreads)
     const int64_t j = (blockIdx.x % bpp) * kL2LThreads + threadIdx.x;
     if (j >= np) return;
     const int jx = (int)(j % half), jy = (int)(j / half);
+    if (!rows_touch(rows, 2 * jy + (q >> 1), levels - level)) return;  // outside the owned strip
     const double2* L = parent + coef_base(level - 1, jx, jy);
     const int64_t ps = coef_stride(level - 1);
     const int n0 = chunk * TN;
@@ -88,7 +89,7 @@ __global__ void k_leaf_locals_copy(const double2* __restrict__ loc2, int P, doub
 }
 
 template <int TN>
-void launch_l2l_tn(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc,
+void launch_l2l_tn(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc, Rows rows,
                    cudaStream_t s) {
     const int nchunks = (L.P + TN - 1) / TN;
     for (int level = 3; level <= L.levels; ++level) {
@@ -97,7 +98,7 @@ void launch_l2l_tn(const Layout& L, const Tables* T, double2* loc, double2* leaf
         const double2* parent = loc + L.level_cell_off[level - 1] * L.P;
         double2* child = loc + L.level_cell_off[level] * L.P;
         k_l2l<TN><<<(unsigned)(bpp * 4 * nchunks), kL2LThreads, 0, s>>>(
-            parent, child, level, L.P, T, level == L.levels ? leaf_loc : nullptr);
+            parent, child, level, L.levels, L.P, T, level == L.levels ? leaf_loc : nullptr, rows);
         note_launches(1);
     }
     if (L.levels == 2) {
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(256)
                   const int* __restrict__ perm, const double2* __restrict__ loc,
                   const double2* __restrict__ near_uv, int64_t n, int levels, int P, double xmin,
                   double ymin, double side, const Tables* __restrict__ T, double* __restrict__ u,
-                  double* __restrict__ v) {
+                  double* __restrict__ v, Rows rows) {
     __shared__ double sfact[kOrderCap + 16];
     for (int i = threadIdx.x; i < P; i += blockDim.x) sfact[i] = T->invfact[i];
     __syncthreads();
@@ -139,6 +140,7 @@ __global__ void __launch_bounds__(256)
     const int m = 1 << levels;
     const int leaf = keys[i];
     const int ix = leaf % m, iy = leaf / m;
+    if (iy < rows.lo || iy >= rows.hi) return;  // halo particle of a sharded run
     const double r = side / m;
     const double cx = cell_center(xmin, ix, r), cy = cell_center(ymin, iy, r);
     const double inv_r = 1.0 / r;
@@ -205,22 +207,23 @@ __global__ void __launch_bounds__(256)
 
 }  // namespace
 
-void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc, cudaStream_t s) {
+void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc, Rows rows,
+                cudaStream_t s) {
     switch (coef_chunk(L.P)) {
-        case 4: launch_l2l_tn<4>(L, T, loc, leaf_loc, s); break;
-        case 5: launch_l2l_tn<5>(L, T, loc, leaf_loc, s); break;
-        case 6: launch_l2l_tn<6>(L, T, loc, leaf_loc, s); break;
-        case 7: launch_l2l_tn<7>(L, T, loc, leaf_loc, s); break;
-        default: launch_l2l_tn<8>(L, T, loc, leaf_loc, s); break;
+        case 4: launch_l2l_tn<4>(L, T, loc, leaf_loc, rows, s); break;
+        case 5: launch_l2l_tn<5>(L, T, loc, leaf_loc, rows, s); break;
+        case 6: launch_l2l_tn<6>(L, T, loc, leaf_loc, rows, s); break;
+        case 7: launch_l2l_tn<7>(L, T, loc, leaf_loc, rows, s); break;
+        default: launch_l2l_tn<8>(L, T, loc, leaf_loc, rows, s); break;
     }
 }
 
 void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const int* keys,
                         const int* perm, const double2* loc, const double2* near_uv, double xmin,
-                        double ymin, double side, double* u, double* v, cudaStream_t s) {
+                        double ymin, double side, double* u, double* v, Rows rows, cudaStream_t s) {
     const double2* leaf_loc = loc;
     k_l2p_combine<<<(unsigned)((L.n + 255) / 256), 256, 0, s>>>(
-        src, keys, perm, leaf_loc, near_uv, L.n, L.levels, L.P, xmin, ymin, side, T, u, v);
+        src, keys, perm, leaf_loc, near_uv, L.n, L.levels, L.P, xmin, ymin, side, T, u, v, rows);
     note_launches(1);
 }
 

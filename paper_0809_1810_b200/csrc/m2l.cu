@@ -46,7 +46,7 @@ template <int TN>
 __global__ void __launch_bounds__(kM2LThreads)
     k_m2l(const double2* __restrict__ mult, const int* __restrict__ counts, double2* __restrict__ loc,
           int levels, int P, int nchunks, const Tables* __restrict__ T,
-          unsigned long long* __restrict__ m2l_count) {
+          unsigned long long* __restrict__ m2l_count, Rows rows) {
     extern __shared__ double2 sH[];  // [27][TN + P - 1]
     // ---- decode (level, parity, chunk, block-in-class) from blockIdx.x ----
     int64_t b = blockIdx.x;
@@ -83,10 +83,14 @@ __global__ void __launch_bounds__(kM2LThreads)
     const int mk = 1 << level, half = mk >> 1;
     const int64_t psz = (int64_t)half * half;  // cells per plane
     const int64_t j = blk * kM2LThreads + threadIdx.x;
-    const bool active = j < psz;
-    const int jx = active ? (int)(j % half) : 0;
-    const int jy = active ? (int)(j / half) : 0;
+    const int jx = j < psz ? (int)(j % half) : 0;
+    const int jy = j < psz ? (int)(j / half) : 0;
     const int ix = 2 * jx + px, iy = 2 * jy + py;
+    // destinations whose leaf rows touch the owned strip; a destination is
+    // counted by the strip that owns its first leaf row (sharded runs)
+    const int shift = levels - level;
+    const bool active = j < psz && rows_touch(rows, iy, shift);
+    const bool counts_here = active && (iy << shift) >= rows.lo;
     const double2* M = mult + cell_off * P;
     const int* cnt = counts + cnt_off;
     const int64_t cstride = 4 * psz;
@@ -103,7 +107,7 @@ __global__ void __launch_bounds__(kM2LThreads)
             const int sx = ix + dx, sy = iy + dy;
             const bool inr = active && sx >= 0 && sx < mk && sy >= 0 && sy < mk;
             const bool live = inr && cnt[(int64_t)sy * mk + sx] > 0;
-            ntrans += live ? 1 : 0;
+            ntrans += (live && counts_here) ? 1 : 0;
             const double2* h = sH + o * HL;
             ++o;
             if (!__any_sync(0xffffffffu, live)) continue;
@@ -139,7 +143,7 @@ __global__ void __launch_bounds__(kM2LThreads)
 
 template <int TN>
 void launch_tn(const Layout& L, const Tables* T, const double2* mult, const int* counts,
-               double2* loc, Counters* ctr, cudaStream_t s) {
+               double2* loc, Counters* ctr, Rows rows, cudaStream_t s) {
     const int nchunks = (L.P + TN - 1) / TN;
     int64_t blocks = 0;
     for (int level = 2; level <= L.levels; ++level) {
@@ -148,20 +152,20 @@ void launch_tn(const Layout& L, const Tables* T, const double2* mult, const int*
     }
     const size_t shm = (size_t)27 * (TN + L.P - 1) * sizeof(double2);
     k_m2l<TN><<<(unsigned)blocks, kM2LThreads, shm, s>>>(mult, counts, loc, L.levels, L.P, nchunks,
-                                                       T, &ctr->m2l_count);
+                                                       T, &ctr->m2l_count, rows);
     note_launches(1);
 }
 
 }  // namespace
 
 void launch_m2l(const Layout& L, const Tables* T, const double2* mult, const int* counts,
-                double2* loc, Counters* ctr, cudaStream_t s) {
+                double2* loc, Counters* ctr, Rows rows, cudaStream_t s) {
     switch (coef_chunk(L.P)) {
-        case 4: launch_tn<4>(L, T, mult, counts, loc, ctr, s); break;
-        case 5: launch_tn<5>(L, T, mult, counts, loc, ctr, s); break;
-        case 6: launch_tn<6>(L, T, mult, counts, loc, ctr, s); break;
-        case 7: launch_tn<7>(L, T, mult, counts, loc, ctr, s); break;
-        default: launch_tn<8>(L, T, mult, counts, loc, ctr, s); break;
+        case 4: launch_tn<4>(L, T, mult, counts, loc, ctr, rows, s); break;
+        case 5: launch_tn<5>(L, T, mult, counts, loc, ctr, rows, s); break;
+        case 6: launch_tn<6>(L, T, mult, counts, loc, ctr, rows, s); break;
+        case 7: launch_tn<7>(L, T, mult, counts, loc, ctr, rows, s); break;
+        default: launch_tn<8>(L, T, mult, counts, loc, ctr, rows, s); break;
     }
 }
 

@@ -249,11 +249,13 @@ __global__ void k_leaf_starts(const int* __restrict__ keys, int64_t n, int nleav
     for (int k = prev + 1; k <= cur; ++k) ls[k] = (int)i;
 }
 
-// Occupancy of every cell of every level (level 0 first) from leaf_starts:
+// Occupancy of every cell of every level (level 0 first) from leaf_starts
+// (Tree.counts, quadtree.py:126-134):
 // a level-k cell covers 2^(l-k) leaf rows, each a contiguous leaf range.
 // Leaf cells also emit their P2P task count ceil(count / chunk).
 __global__ void k_counts_tasks(const int* __restrict__ ls, int levels, int64_t total_cells,
-                               int chunk, int* __restrict__ counts, int* __restrict__ ntask) {
+                               int chunk, Rows rows, int* __restrict__ counts,
+                               int* __restrict__ ntask) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= total_cells) return;
     int k = 0;
@@ -267,21 +269,27 @@ __global__ void k_counts_tasks(const int* __restrict__ ls, int levels, int64_t t
     const int ix = (int)(cell % mk), iy = (int)(cell / mk);
     const int m = 1 << levels;
     const int s = 1 << (levels - k);
+    // only owned leaf rows are counted, so per-rank pyramids of a sharded run
+    // are disjoint and their sum is the global occupancy
+    const int r0 = max(iy * s, rows.lo), r1 = min((iy + 1) * s, rows.hi);
     int c = 0;
-    for (int r = iy * s; r < (iy + 1) * s; ++r) {
+    for (int r = r0; r < r1; ++r) {
         const int64_t row = (int64_t)r * m;
         c += ls[row + (int64_t)(ix + 1) * s] - ls[row + (int64_t)ix * s];
     }
     counts[t] = c;
-    if (k == levels) ntask[cell] = (c + chunk - 1) / chunk;
+    // only leaves of the owned row strip get near-field tasks
+    if (k == levels) ntask[cell] = (iy >= rows.lo && iy < rows.hi) ? (c + chunk - 1) / chunk : 0;
 }
 
-__global__ void k_tasks_fill(const int* __restrict__ ls, int nleaves, int chunk,
+__global__ void k_tasks_fill(const int* __restrict__ ls, int levels, int chunk, Rows rows,
                              const int* __restrict__ off, int2* __restrict__ tasks, Counters* ctr) {
+    const int nleaves = 1 << (2 * levels);
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nleaves) return;
+    const int iy = i >> levels;
     const int c = ls[i + 1] - ls[i];
-    const int nt = (c + chunk - 1) / chunk;
+    const int nt = (iy >= rows.lo && iy < rows.hi) ? (c + chunk - 1) / chunk : 0;
     const int o = off[i];
     for (int t = 0; t < nt; ++t) tasks[o + t] = make_int2(i, chunk * t);
     if (i == nleaves - 1) ctr->ntasks = o + nt;
@@ -357,20 +365,23 @@ void launch_leaf_starts(const int* sorted_keys, int64_t n, int nleaves, int* lea
     note_launches(1);
 }
 
-void launch_counts_tasks(const Layout& L, char* ws, Counters* ctr, bool tasks, cudaStream_t s) {
+void launch_counts_tasks(const Layout& L, char* ws, Counters* ctr, bool tasks, Rows rows,
+                         cudaStream_t s) {
     const int* ls = (const int*)(ws + L.leaf_starts);
     int* counts = (int*)(ws + L.counts);
     int* nt = (int*)(ws + L.task_scratch);
     int64_t total = 0;
     for (int k = 0; k <= L.levels; ++k) total += 1ll << (2 * k);
     const int chunk = 32 * p2p_targets_per_lane();
-    k_counts_tasks<<<grid_for(total, 256), 256, 0, s>>>(ls, L.levels, total, chunk, counts, nt);
+    k_counts_tasks<<<grid_for(total, 256), 256, 0, s>>>(ls, L.levels, total, chunk, rows, counts,
+                                                       nt);
     note_launches(1);
     if (!tasks) return;
     const int nl = (int)L.nleaves;
     launch_scan_i32(nt, nl, (unsigned long long*)(ws + L.scan_state) +
                                 (size_t)L.passes * (L.scan_state_tiles + 1), s);
-    k_tasks_fill<<<grid_for(nl, 256), 256, 0, s>>>(ls, nl, chunk, nt, (int2*)(ws + L.tasks), ctr);
+    k_tasks_fill<<<grid_for(nl, 256), 256, 0, s>>>(ls, L.levels, chunk, rows, nt,
+                                                 (int2*)(ws + L.tasks), ctr);
     note_launches(1);
 }
 

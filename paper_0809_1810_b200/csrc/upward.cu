@@ -19,7 +19,8 @@ constexpr int kP2MWarps = 2;
 // coefficient k over the particles in sorted order (np.add.reduceat order).
 __global__ void __launch_bounds__(kP2MWarps * 32)
     k_p2m(const Src* __restrict__ src, const int* __restrict__ ls, int levels, int P, double xmin,
-          double ymin, double side, const Tables* __restrict__ T, double2* __restrict__ mult) {
+          double ymin, double side, const Tables* __restrict__ T, Rows rows,
+          double2* __restrict__ mult) {
     __shared__ double2 buf[kP2MWarps][32][33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m = 1 << levels;
@@ -29,7 +30,9 @@ __global__ void __launch_bounds__(kP2MWarps * 32)
     const int ix = (int)(leaf % m), iy = (int)(leaf / m);
     double2* out = mult + coef_base(levels, ix, iy);
     const int64_t cs = coef_stride(levels);
-    if (lo == hi) {
+    // empty leaves, and leaves outside the owned row strip (sharded run: their
+    // particles are halo copies owned by a neighbour rank), carry zero
+    if (lo == hi || iy < rows.lo || iy >= rows.hi) {
         for (int k = lane; k < P; k += 32) out[k * cs] = make_double2(0.0, 0.0);
         return;
     }
@@ -157,10 +160,10 @@ int coef_chunk(int P) {
 }
 
 void launch_p2m(const Layout& L, const Src* src, const int* leaf_starts, double xmin, double ymin,
-                double side, double2* mult_leaf, const Tables* T, cudaStream_t s) {
+                double side, double2* mult_leaf, const Tables* T, Rows rows, cudaStream_t s) {
     const int64_t nl = (int64_t)L.nleaves;
     k_p2m<<<(unsigned)((nl + kP2MWarps - 1) / kP2MWarps), kP2MWarps * 32, 0, s>>>(
-        src, leaf_starts, L.levels, L.P, xmin, ymin, side, T, mult_leaf);
+        src, leaf_starts, L.levels, L.P, xmin, ymin, side, T, rows, mult_leaf);
     note_launches(1);
 }
 

@@ -72,6 +72,16 @@ struct Layout {
 
 bool make_layout(int64_t n, int levels, int order, Layout* L);
 
+// Leaf rows [lo, hi) owned by this call (a row strip of the leaf grid; the
+// full grid for a single-GPU evaluate).  Coarser cells are processed when
+// their leaf-row span intersects [lo, hi).
+struct Rows {
+    int lo, hi;
+};
+__host__ __device__ __forceinline__ bool rows_touch(Rows r, int level_row, int shift) {
+    return (level_row << shift) < r.hi && ((level_row + 1) << shift) > r.lo;
+}
+
 // Host-side count of kernel launches issued by the library (bench evidence).
 void note_launches(int k);
 
@@ -83,20 +93,22 @@ void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream
 size_t scan_tiles(int64_t n);
 void launch_leaf_starts(const int* sorted_keys, int64_t n, int nleaves, int* leaf_starts,
                         cudaStream_t s);
-void launch_counts_tasks(const Layout& L, char* ws, Counters* ctr, bool tasks, cudaStream_t s);
+void launch_counts_tasks(const Layout& L, char* ws, Counters* ctr, bool tasks, Rows rows,
+                         cudaStream_t s);
 void launch_p2m(const Layout& L, const Src* src, const int* leaf_starts, double xmin, double ymin,
-                double side, double2* mult_leaf, const Tables* T, cudaStream_t s);
+                double side, double2* mult_leaf, const Tables* T, Rows rows, cudaStream_t s);
 void launch_init_counters(Counters* ctr, cudaStream_t s);
 void launch_m2m(const Layout& L, const Tables* T, double2* mult, cudaStream_t s);
 void launch_m2l(const Layout& L, const Tables* T, const double2* mult, const int* counts,
-                double2* loc, Counters* ctr, cudaStream_t s);
-void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc, cudaStream_t s);
+                double2* loc, Counters* ctr, Rows rows, cudaStream_t s);
+void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc, Rows rows,
+                cudaStream_t s);
 int p2p_targets_per_lane();  // 1 or 2 (env VFMM_P2P_TPT, default 1)
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
                 const int2* tasks, Counters* ctr, int kernel, double2* near_uv, cudaStream_t s);
 void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const int* keys,
                         const int* perm, const double2* loc, const double2* near_uv, double xmin,
-                        double ymin, double side, double* u, double* v, cudaStream_t s);
+                        double ymin, double side, double* u, double* v, Rows rows, cudaStream_t s);
 void launch_eval_at(const Layout& L, const Tables* T, const double* tx, const double* ty,
                     int64_t m, const Src* src, const int* leaf_starts, const double2* loc,
                     double xmin, double ymin, double side, int kernel, double* u, double* v,

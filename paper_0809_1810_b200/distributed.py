@@ -1,0 +1,308 @@
+"""Multi-GPU sharded evaluate: one process per GPU, leaves sharded in row strips.
+
+SURVEY.md §8(e).  The leaf grid (2^l x 2^l, row-major keys) is cut into
+``world`` contiguous strips of leaf rows, so a strip is a contiguous range of
+leaf keys (the row-major analogue of a Morton range).  Per evaluate:
+
+1. **redistribution** -- every particle goes to the rank owning its leaf row
+   (``all_to_all_single``; the binning is the reference floor rule,
+   quadtree.py:39-46, evaluated with the same IEEE operations as the kernel);
+2. **halo** -- each rank sends the particles of its first / last owned row to
+   the neighbour below / above (``all_to_all_single``), which is exactly what
+   the P2P of its boundary leaves needs (3x3 neighbourhoods, engine.py:216-235);
+3. **upward** on the GPU (``vfmm_evaluate_shard`` PHASE_UP): P2M over owned
+   leaves only, M2M over the whole pyramid, occupancy of owned rows;
+4. **all-reduce** (SUM, NCCL over NVLink) of the multipole pyramid and of the
+   int32 occupancy pyramid -- multipoles are linear in Gamma and the per-rank
+   occupancies are disjoint, so the sums are the global pyramids;
+5. **downward** on the GPU (PHASE_DOWN): M2L / L2L for cells touching the
+   strip, P2P for owned leaves, L2P + combine for owned particles;
+6. **counters** -- int64 all-reduce; each rank counts only what it owns, so the
+   sums equal the single-GPU ``m2l_count`` / ``near_pair_count``.
+
+The host orchestration is backend-agnostic: the CUDA backend calls the C ABI;
+tests inject a CPU backend built on the oracle to check the decomposition on
+``gloo`` (tests/test_distributed.py).  There is no silent fallback: the
+default backend is CUDA and raises without a GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from ._device import require_cuda, stream_ptr
+from .engine import FmmRunStats, Workspace, validate_config
+from .kernels import kernel_code
+from .quadtree import OutOfDomainError
+
+
+def row_bounds(levels: int, world: int) -> list[tuple[int, int]]:
+    """Equal strips of the 2^levels leaf rows: rank r owns [r*m//world, (r+1)*m//world)."""
+    m = 2**levels
+    return [(r * m // world, (r + 1) * m // world) for r in range(world)]
+
+
+def leaf_rows(y: torch.Tensor, domain, levels: int) -> torch.Tensor:
+    """Leaf row of each particle: min(int((y - ymin) / side * m), m - 1) (quadtree.py:44-45)."""
+    m = 2**levels
+    return torch.clamp(((y - domain.ymin) / domain.side * m).to(torch.int64), max=m - 1)
+
+
+def owner_of_rows(rows: torch.Tensor, bounds) -> torch.Tensor:
+    starts = torch.tensor([lo for lo, _ in bounds], dtype=torch.int64, device=rows.device)
+    return torch.searchsorted(starts, rows, right=True) - 1
+
+
+def _exchange(cols: torch.Tensor, dest: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """Send column j of ``cols`` [k, n] to rank dest[j]; returns the received [k, n'] in
+    (source rank, original position) order."""
+    order = torch.argsort(dest, stable=True)
+    send = cols[:, order].t().contiguous()  # [n, k] rows grouped by destination
+    counts = torch.bincount(dest, minlength=world).to(torch.int64)
+    recv_counts = torch.empty_like(counts)
+    dist.all_to_all_single(recv_counts, counts, group=group)
+    k = cols.shape[0]
+    recv = torch.empty((int(recv_counts.sum()), k), dtype=cols.dtype, device=cols.device)
+    dist.all_to_all_single(recv, send, output_split_sizes=recv_counts.tolist(),
+                           input_split_sizes=counts.tolist(), group=group)
+    return recv.t().contiguous()
+
+
+@dataclass
+class Shard:
+    """This rank's particles after redistribution: owned first, then halo."""
+
+    cols: torch.Tensor  # [5, n_local] float64: x, y, gamma, sigma, global id
+    n_owned: int
+    rows: tuple[int, int]
+
+
+def redistribute(x, y, gamma, sigma, ids, domain, levels: int, group=None) -> Shard:
+    """Steps 1-2: owner redistribution and one-row halo exchange."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    bounds = row_bounds(levels, world)
+    cols = torch.stack([x, y, gamma, sigma, ids.to(torch.float64)])
+    owned = _exchange(cols, owner_of_rows(leaf_rows(cols[1], domain, levels), bounds), world, group)
+    lo, hi = bounds[rank]
+    r = leaf_rows(owned[1], domain, levels)
+    none = torch.zeros_like(r, dtype=torch.bool)
+    # halo: my first owned row goes to rank-1, my last owned row to rank+1
+    down = (r == lo) & (rank > 0) if hi > lo else none
+    up = (r == hi - 1) & (rank < world - 1) if hi > lo else none
+    idx = torch.cat([torch.nonzero(down).flatten(), torch.nonzero(up).flatten()])
+    dest = torch.cat([torch.full((int(down.sum()),), rank - 1, dtype=torch.int64, device=r.device),
+                      torch.full((int(up.sum()),), rank + 1, dtype=torch.int64, device=r.device)])
+    halo = _exchange(owned[:, idx], dest, world, group)
+    return Shard(torch.cat([owned, halo], dim=1), owned.shape[1], (lo, hi))
+
+
+class CudaShardBackend:
+    """PHASE_UP / PHASE_DOWN of ``vfmm_evaluate_shard`` on this rank's GPU."""
+
+    def __init__(self, device: torch.device, private_workspace: bool = False):
+        require_cuda()
+        self.device = device
+        self.private = private_workspace
+        self.lib = _lib.load()
+        self.ws = None
+
+    def _args(self, shard: Shard, config, domain):
+        c = shard.cols
+        return (c[0].data_ptr(), c[1].data_ptr(), c[2].data_ptr(), c[3].data_ptr(), c.shape[1],
+                float(domain.xmin), float(domain.ymin), float(domain.side), config.levels,
+                config.order, kernel_code(config.kernel), shard.rows[0], shard.rows[1])
+
+    def regions(self, n: int, config):
+        mo, mb = _lib.region("mult", n, config.levels, config.order)
+        co, cb = _lib.region("counts", n, config.levels, config.order)
+        return (mo, mb), (co, cb)
+
+    def up(self, shard: Shard, config, domain):
+        """Returns (multipoles as float64, occupancy as int32) views to be sum-reduced."""
+        nl = shard.cols.shape[1]
+        (mo, mb), (co, cb) = self.regions(nl, config)
+        if nl == 0:  # nothing local: contribute zeros to the reductions
+            self.ws = None
+            return (torch.zeros(mb // 8, dtype=torch.float64, device=self.device),
+                    torch.zeros(cb // 4, dtype=torch.int32, device=self.device))
+        self.ws = (Workspace(nl, config.levels, config.order, self.device) if self.private
+                   else Workspace.get(nl, config.levels, config.order, self.device))
+        st = _lib.VfmmStats()
+        rc = self.lib.vfmm_evaluate_shard(*self._args(shard, config, domain), None, None,
+                                          self.ws.ptr, self.ws.nbytes,
+                                          _lib.FLAG_PHASE_UP | _lib.FLAG_STATS, ctypes.byref(st),
+                                          stream_ptr(self.device))
+        _lib.check(rc, "vfmm_evaluate_shard(up)")
+        buf = self.ws.buffer
+        return buf[mo: mo + mb].view(torch.float64), buf[co: co + cb].view(torch.int32)
+
+    def down(self, shard: Shard, config, domain):
+        """(2, n_local) velocities (owned columns valid), m2l_count, near_pair_count."""
+        n = shard.cols.shape[1]
+        vel = torch.zeros((2, n), dtype=torch.float64, device=self.device)
+        if n == 0:
+            return vel, 0, 0
+        st = _lib.VfmmStats()
+        rc = self.lib.vfmm_evaluate_shard(*self._args(shard, config, domain), vel[0].data_ptr(),
+                                          vel[1].data_ptr(), self.ws.ptr, self.ws.nbytes,
+                                          _lib.FLAG_PHASE_DOWN | _lib.FLAG_STATS, ctypes.byref(st),
+                                          stream_ptr(self.device))
+        _lib.check(rc, "vfmm_evaluate_shard(down)")
+        return vel, int(st.m2l_count), int(st.near_pair_count)
+
+
+def evaluate_sharded(x, y, gamma, sigma, ids, config, domain, *, backend=None, group=None):
+    """Sharded evaluate on this rank's input slice.
+
+    ``x, y, gamma, sigma, ids`` are this rank's input particles (any subset of
+    the global set; ``ids`` are their global indices).  Returns
+    ``(owned_ids, vel, stats)``: the global ids of the particles this rank now
+    owns, their (2, n_owned) velocities and the global ``FmmRunStats`` counters.
+    """
+    validate_config(config)
+    if backend is None:
+        backend = CudaShardBackend(x.device)
+    inside = (x >= domain.xmin) & (x <= domain.xmax) & (y >= domain.ymin) & (y <= domain.ymax)
+    bad = torch.tensor([int((~inside).sum())], dtype=torch.int64, device=x.device)
+    dist.all_reduce(bad, group=group)
+    if int(bad):
+        raise OutOfDomainError(f"{int(bad)} particle(s) outside domain {domain}")
+    shard = redistribute(x, y, gamma, sigma, ids, domain, config.levels, group)
+    mult, occ = backend.up(shard, config, domain)
+    dist.all_reduce(mult, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(occ, op=dist.ReduceOp.SUM, group=group)
+    vel, m2l, near = backend.down(shard, config, domain)
+    cnt = torch.tensor([m2l, near, shard.n_owned], dtype=torch.int64, device=mult.device)
+    dist.all_reduce(cnt, op=dist.ReduceOp.SUM, group=group)
+    stats = FmmRunStats(n=int(cnt[2]), levels=config.levels, order=config.order,
+                        m2l_count=int(cnt[0]), near_pair_count=int(cnt[1]))
+    k = shard.n_owned
+    return shard.cols[4, :k].to(torch.int64), vel[:, :k], stats
+
+
+def gather_velocities(owned_ids, vel, n_total: int, group=None, dst: int = 0):
+    """Assemble the (N, 2) velocities in global order on rank ``dst`` (None elsewhere)."""
+    world = dist.get_world_size(group)
+    cnt = torch.tensor([owned_ids.numel()], dtype=torch.int64, device=vel.device)
+    sizes = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(sizes, cnt, group=group)
+    mx = max(int(s) for s in sizes)
+    pad = torch.zeros((3, mx), dtype=torch.float64, device=vel.device)
+    pad[0, : owned_ids.numel()] = owned_ids.to(torch.float64)
+    pad[1:, : owned_ids.numel()] = vel
+    bufs = [torch.zeros_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    if dist.get_rank(group) != dst:
+        return None
+    out = torch.empty((n_total, 2), dtype=torch.float64, device=vel.device)
+    for s, b in zip(sizes, bufs):
+        k = int(s)
+        out[b[0, :k].to(torch.int64)] = b[1:, :k].t()
+    return out
+
+
+def make_shards(x, y, gamma, sigma, domain, levels: int, world: int) -> list[Shard]:
+    """The shards ``redistribute`` produces, built locally for ``world`` logical ranks."""
+    bounds = row_bounds(levels, world)
+    rows = leaf_rows(y, domain, levels)
+    owner = owner_of_rows(rows, bounds)
+    ids = torch.arange(x.numel(), device=x.device)
+    m = 2**levels
+    shards = []
+    for r, (lo, hi) in enumerate(bounds):
+        own = torch.nonzero(owner == r).flatten()
+        below = torch.nonzero((rows == lo - 1) & (lo > 0) & (hi > lo)).flatten()
+        above = torch.nonzero((rows == hi) & (hi < m) & (hi > lo)).flatten()
+        idx = torch.cat([own, below, above])
+        cols = torch.stack([x[idx], y[idx], gamma[idx], sigma[idx], ids[idx].to(torch.float64)])
+        shards.append(Shard(cols.contiguous(), own.numel(), (lo, hi)))
+    return shards
+
+
+def evaluate_emulated(x, y, gamma, sigma, config, domain, world: int, backend_factory=None):
+    """``world`` logical ranks run one after another on one device, with the
+    reductions done locally: every rank's PHASE_UP, the pyramids summed, then
+    every rank's PHASE_DOWN.  Exercises the row-restricted kernels of the
+    sharded path on a single GPU (R logical ranks sequentially).
+    Returns ((2, N) velocities, m2l_count, near_pair_count)."""
+    validate_config(config)
+    if backend_factory is None:
+        def backend_factory():
+            return CudaShardBackend(x.device, private_workspace=True)
+    shards = make_shards(x, y, gamma, sigma, domain, config.levels, world)
+    backends = [backend_factory() for _ in shards]
+    parts = [b.up(sh, config, domain) for b, sh in zip(backends, shards)]
+    mult = torch.stack([p[0].clone() for p in parts]).sum(dim=0)
+    occ = torch.stack([p[1].clone() for p in parts]).sum(dim=0)
+    for p in parts:
+        p[0].copy_(mult)
+        p[1].copy_(occ)
+    out = torch.zeros((2, x.numel()), dtype=torch.float64, device=x.device)
+    m2l = near = 0
+    for sh, b in zip(shards, backends):
+        vel, c1, c2 = b.down(sh, config, domain)
+        m2l += c1
+        near += c2
+        k = sh.n_owned
+        out[:, sh.cols[4, :k].to(torch.int64)] = vel[:, :k]
+    return out, m2l, near
+
+
+# ----------------------------------------------------------------------------- bench
+def bench_main(args):
+    """``bench.py --gpus N`` under torchrun: the sharded evaluate of a BASELINE config.
+
+    Every rank generates the same seeded workload and starts from its
+    contiguous 1/N slice of the particle index range; a step is the full
+    sharded evaluate (redistribution, halo, upward, all-reduces, downward,
+    counter reduction).  Timed with CUDA events between barriers; the max over
+    ranks is reported.
+    """
+    import json
+
+    from . import workloads as W
+    from .engine import FmmConfig
+    from .kernels import KernelKind
+    from .model import Domain
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    w = W.by_index(args.config)
+    cfg = FmmConfig(w.levels, w.order, KernelKind.GAUSSIAN_BLOB)
+    dom = Domain(*W.DOMAIN)
+    lo, hi = rank * w.n // world, (rank + 1) * w.n // world
+    x, y, g, s = (torch.from_numpy(a[lo:hi]).to(dev) for a in (w.x, w.y, w.gamma, w.sigma))
+    ids = torch.arange(lo, hi, device=dev)
+    for _ in range(max(3, args.warmup)):
+        evaluate_sharded(x, y, g, s, ids, cfg, dom)
+    torch.cuda.synchronize()
+    dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        _, _, st = evaluate_sharded(x, y, g, s, ids, cfg, dom)
+    b.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([a.elapsed_time(b) / args.steps], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({
+            "metric": "FMM particle velocity evals/sec (fp64)", "value": w.n / (float(ms) * 1e-3),
+            "unit": "particle-evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": float(ms), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "n": w.n, "levels": w.levels, "order": w.order,
+                       "sharding": f"{world} row strips of leaves", "m2l_count": st.m2l_count,
+                       "near_pair_count": st.near_pair_count},
+        }), flush=True)
+    dist.destroy_process_group()
