@@ -220,7 +220,7 @@ bool make_layout(int64_t n, int levels, int order, Layout* L) {
     L->task_scratch = take(sizeof(int) * L->nleaves);
     L->scan_state = take(L->scan_state_bytes);
     L->src = take(sizeof(Src) * n);
-    L->near_uv = take(sizeof(double2) * n * kNearRows);
+    L->near_uv = take(sizeof(double2) * n * kNearSlots);
     L->leaf_starts = take(sizeof(int) * (L->nleaves + 1));
     L->counts = take(sizeof(int) * cc);
     L->mult = take(sizeof(double2) * cells * L->P);
@@ -361,17 +361,17 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         if (overlap) {
             cudaEventRecord(R->join_far, fs);
             rec(7, R->near);
-            launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, R->near);
+            launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, rows, R->near);
             rec(8, R->near);
             cudaEventRecord(R->join_near, R->near);
             cudaStreamWaitEvent(s, R->join_far, 0);
             cudaStreamWaitEvent(s, R->join_near, 0);
         }
         if (!far_only) {
-            if (!overlap) launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, s);
+            if (!overlap) launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, rows, s);
             rec(5, s);
             launch_l2p_combine(L, T, src, keys, perm, (const double2*)(ws + L.leaf_loc), near_uv,
-                               xmin, ymin, side, u, v, rows, s);
+                               xmin, ymin, side, u, v, rows, ls, ctr, kernel, s);
         }
     }
     rec(6, s);

@@ -131,7 +131,8 @@ __global__ void __launch_bounds__(256)
                   const int* __restrict__ perm, const double2* __restrict__ loc,
                   const double2* __restrict__ near_uv, int64_t n, int levels, int P, double xmin,
                   double ymin, double side, const Tables* __restrict__ T, double* __restrict__ u,
-                  double* __restrict__ v, Rows rows) {
+                  double* __restrict__ v, Rows rows, const int* __restrict__ ls,
+                  const Counters* __restrict__ ctr, bool gauss, int sym_enabled) {
     __shared__ double sfact[kOrderCap + 16];
     for (int i = threadIdx.x; i < P; i += blockDim.x) sfact[i] = T->invfact[i];
     __syncthreads();
@@ -147,9 +148,24 @@ __global__ void __launch_bounds__(256)
     const Src s = src[i];
     const double2 f =
         eval_local(loc + (int64_t)leaf * P, 1, P, (s.x - cx) * inv_r, (s.y - cy) * inv_r, sfact);
-    // near field = the three neighbourhood-row partial sums, in row order
-    const double2 n0 = near_uv[i], n1 = near_uv[n + i], n2 = near_uv[2 * n + i];
-    const double2 nv = make_double2((n0.x + n1.x) + n2.x, (n0.y + n1.y) + n2.y);
+    double2 nv = make_double2(0.0, 0.0);
+    if (sym_enabled && p2p_symmetric(ctr, gauss)) {
+        // symmetric kernel: one slot per existing non-empty neighbour leaf, direction order
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int nx = ix + dx, ny = iy + dy;
+                if (nx < 0 || nx >= m || ny < 0 || ny >= m) continue;
+                const int nl = ny * m + nx;
+                if (ls[nl + 1] == ls[nl]) continue;
+                const double2 t = near_uv[(int64_t)((dy + 1) * 3 + dx + 1) * n + i];
+                nv.x += t.x;
+                nv.y += t.y;
+            }
+    } else {
+        // generic kernel: the three neighbourhood-row partial sums, in row order
+        const double2 n0 = near_uv[i], n1 = near_uv[n + i], n2 = near_uv[2 * n + i];
+        nv = make_double2((n0.x + n1.x) + n2.x, (n0.y + n1.y) + n2.y);
+    }
     // f_to_velocity: u = Im f / 2pi, v = Re f / 2pi; then far + near
     const int o = perm[i];
     u[o] = f.y * kInv2Pi + nv.x;
@@ -220,10 +236,12 @@ void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_lo
 
 void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const int* keys,
                         const int* perm, const double2* loc, const double2* near_uv, double xmin,
-                        double ymin, double side, double* u, double* v, Rows rows, cudaStream_t s) {
+                        double ymin, double side, double* u, double* v, Rows rows,
+                        const int* leaf_starts, const Counters* ctr, int kernel, cudaStream_t s) {
     const double2* leaf_loc = loc;
     k_l2p_combine<<<(unsigned)((L.n + 255) / 256), 256, 0, s>>>(
-        src, keys, perm, leaf_loc, near_uv, L.n, L.levels, L.P, xmin, ymin, side, T, u, v, rows);
+        src, keys, perm, leaf_loc, near_uv, L.n, L.levels, L.P, xmin, ymin, side, T, u, v, rows,
+        leaf_starts, ctr, kernel == VFMM_KERNEL_GAUSSIAN, sym_disabled() ? 0 : 1);
     note_launches(1);
 }
 

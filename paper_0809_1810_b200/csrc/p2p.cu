@@ -99,7 +99,9 @@ template <bool GAUSS, int TPT>
 __global__ void __launch_bounds__(kP2PWarps * 32, kP2PBlocksPerSM)
     k_p2p(const Src* __restrict__ src, const int* __restrict__ ls, const int2* __restrict__ tasks,
           Counters* __restrict__ ctr, int levels, int64_t n, const Tables* __restrict__ T,
-          double2* __restrict__ near_uv, unsigned long long* __restrict__ pairs, int items_per_warp) {
+          double2* __restrict__ near_uv, unsigned long long* __restrict__ pairs, int items_per_warp,
+          int sym_enabled) {
+    if (sym_enabled && p2p_symmetric(ctr, GAUSS)) return;  // the symmetric kernel handles it
     const int nitems = ctr->ntasks * kNearRows;
     if (items_per_warp < (1 << 30) && (int64_t)blockIdx.x * kP2PWarps * items_per_warp >= nitems)
         return;  // spare CTA
@@ -149,6 +151,156 @@ __global__ void __launch_bounds__(kP2PWarps * 32, kP2PBlocksPerSM)
         }
         if (act0) near_uv[(int64_t)row * n + i0] = make_double2(u0 * kInv2Pi, v0 * kInv2Pi);
         if (act1) near_uv[(int64_t)row * n + i1] = make_double2(u1 * kInv2Pi, v1 * kInv2Pi);
+    }
+    if (lane == 0 && my_pairs) atomicAdd(pairs, (unsigned long long)my_pairs);
+}
+
+// ---------------------------------------------------------------------------
+// Symmetric near field (Newton's third law).  With one core size for every
+// particle the pair kernel K(r) = (1 - exp(-r^2/(2 sigma^2))) / r^2 is shared
+// by (a <- b) and (b <- a): u_a += -G_b K dy, v_a += G_b K dx and
+// u_b += G_a K dy, v_b += -G_a K dx (dx, dy = a - b).  Each leaf A owns its
+// self block (A, A) and the four "forward" blocks (A, A+d),
+// d in {(1,0), (-1,1), (0,1), (1,1)}, so every neighbouring leaf pair is
+// visited once.  One warp evaluates a whole block: lanes hold 32 targets of A,
+// the 32 sources of a B chunk rotate through the lanes by shuffles together
+// with their accumulators, so after 32 steps every (a, b) pair has been seen
+// exactly once and each B accumulator is back in its home lane.  B-chunk
+// accumulators persist in shared memory across A chunks.  Contributions are
+// written once per (particle, neighbour direction) into nine slots that the
+// combine kernel adds in direction order: deterministic, no atomics.
+// Work per ordered pair: 12 FP64 instructions (21 in the generic kernel).
+constexpr int kSymWarps = 8;
+constexpr int kSymBlocksPerSM = 4;
+
+__device__ __forceinline__ int slot_of(int dx, int dy) { return (dy + 1) * 3 + (dx + 1); }
+
+__device__ __forceinline__ void load_lane(const Src* __restrict__ src, int lo, int cnt, int lane,
+                                          double& x, double& y, double& g) {
+    // ghosts (lane >= cnt) sit on the chunk's first particle with zero circulation
+    const Src& s = src[lo + (lane < cnt ? lane : 0)];
+    x = s.x;
+    y = s.y;
+    g = lane < cnt ? s.g : 0.0;
+}
+
+template <bool GAUSS>
+__device__ __forceinline__ double pair_kernel(double dx, double dy, double& r2, double q2,
+                                              const double* __restrict__ tab) {
+    r2 = fma(dy, dy, dx * dx);
+    const double inv = rcp_fast(r2);
+    if (!GAUSS) return inv;
+    return fma(-inv, exp2_neg(clamp_neg60(r2 * q2), tab), inv);  // (1 - e) / r^2
+}
+
+template <bool GAUSS>
+__global__ void __launch_bounds__(kSymWarps * 32, kSymBlocksPerSM)
+    k_p2p_sym(const Src* __restrict__ src, const int* __restrict__ ls, Counters* __restrict__ ctr,
+              int levels, int64_t n, Rows rows, const Tables* __restrict__ T,
+              double2* __restrict__ near9, unsigned long long* __restrict__ pairs,
+              int items_per_warp) {
+    if (!p2p_symmetric(ctr, GAUSS)) return;  // the generic kernel handles it
+    const int m = 1 << levels;
+    const int nitems = 5 << (2 * levels);
+    if ((int64_t)blockIdx.x * kSymWarps * items_per_warp >= nitems) return;  // spare CTA
+    __shared__ double sexp[kExpTab];
+    __shared__ double2 accB[kSymWarps][kSymMaxLeaf];
+    const double* tab = stage_exp_table(sexp, T->exp2tab);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    double2* acc = accB[threadIdx.x >> 5];
+    const int from = (lane + 1) & 31;
+    const double q2 = GAUSS ? src[0].q2 : 0.0;  // uniform core size
+    long long my_pairs = 0;
+    for (int it = 0; it < items_per_warp; ++it) {
+        int item = 0;
+        if (lane == 0) item = atomicAdd(&ctr->task_cursor, 1);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= nitems) break;
+        const int leaf = item / 5, kind = item % 5;
+        const int loA = ls[leaf], nA = ls[leaf + 1] - loA;
+        if (nA == 0) continue;
+        const int cx = leaf & (m - 1), cy = leaf >> levels;
+        const bool ownA = cy >= rows.lo && cy < rows.hi;
+        if (kind == 0) {
+            if (!ownA) continue;
+            // self block: a <- b for all b in A (r^2 == 0 pairs contribute exactly 0)
+            for (int i0 = 0; i0 < nA; i0 += 32) {
+                double ax, ay, ag;
+                load_lane(src, loA + i0, min(32, nA - i0), lane, ax, ay, ag);
+                double ua = 0.0, va = 0.0;
+                for (int j0 = 0; j0 < nA; j0 += 32) {
+                    double bx, by, bg;
+                    load_lane(src, loA + j0, min(32, nA - j0), lane, bx, by, bg);
+#pragma unroll 2
+                    for (int st = 0; st < 32; ++st) {
+                        const double dx = ax - bx, dy = ay - by;
+                        double r2;
+                        const double c = bg * pair_kernel<GAUSS>(dx, dy, r2, q2, tab);
+                        ua = fma(-c, dy, ua);
+                        va = fma(c, dx, va);
+                        bx = __shfl_sync(0xffffffffu, bx, from);
+                        by = __shfl_sync(0xffffffffu, by, from);
+                        bg = __shfl_sync(0xffffffffu, bg, from);
+                    }
+                }
+                if (i0 + lane < nA)
+                    near9[(int64_t)slot_of(0, 0) * n + loA + i0 + lane] =
+                        make_double2(ua * kInv2Pi, va * kInv2Pi);
+            }
+            my_pairs += (long long)nA * nA - nA;
+            continue;
+        }
+        const int dx_ = kind == 2 ? -1 : (kind == 3 ? 0 : 1), dy_ = kind == 1 ? 0 : 1;
+        const int bxc = cx + dx_, byc = cy + dy_;
+        if (bxc < 0 || bxc >= m || byc >= m) continue;
+        const bool ownB = byc >= rows.lo && byc < rows.hi;
+        if (!ownA && !ownB) continue;
+        const int lb = byc * m + bxc;
+        const int loB = ls[lb], nB = ls[lb + 1] - loB;
+        if (nB == 0) continue;
+        for (int i0 = 0; i0 < nA; i0 += 32) {
+            double ax, ay, ag;
+            load_lane(src, loA + i0, min(32, nA - i0), lane, ax, ay, ag);
+            double ua = 0.0, va = 0.0;
+            for (int j0 = 0; j0 < nB; j0 += 32) {
+                double bx, by, bg;
+                load_lane(src, loB + j0, min(32, nB - j0), lane, bx, by, bg);
+                double ub = 0.0, vb = 0.0;
+                if (i0 > 0) {
+                    const double2 t = acc[j0 + lane];
+                    ub = t.x;
+                    vb = t.y;
+                }
+#pragma unroll 2
+                for (int st = 0; st < 32; ++st) {
+                    const double dx = ax - bx, dy = ay - by;
+                    double r2;
+                    const double K = pair_kernel<GAUSS>(dx, dy, r2, q2, tab);
+                    const double ca = bg * K, cb = ag * K;
+                    ua = fma(-ca, dy, ua);
+                    va = fma(ca, dx, va);
+                    ub = fma(cb, dy, ub);
+                    vb = fma(-cb, dx, vb);
+                    bx = __shfl_sync(0xffffffffu, bx, from);
+                    by = __shfl_sync(0xffffffffu, by, from);
+                    bg = __shfl_sync(0xffffffffu, bg, from);
+                    ub = __shfl_sync(0xffffffffu, ub, from);
+                    vb = __shfl_sync(0xffffffffu, vb, from);
+                }
+                acc[j0 + lane] = make_double2(ub, vb);
+            }
+            if (i0 + lane < nA)
+                near9[(int64_t)slot_of(dx_, dy_) * n + loA + i0 + lane] =
+                    make_double2(ua * kInv2Pi, va * kInv2Pi);
+        }
+        __syncwarp();
+        for (int j = lane; j < nB; j += 32) {
+            const double2 t = acc[j];
+            near9[(int64_t)slot_of(-dx_, -dy_) * n + loB + j] = make_double2(t.x * kInv2Pi, t.y * kInv2Pi);
+        }
+        __syncwarp();
+        my_pairs += (long long)nA * nB * ((ownA ? 1 : 0) + (ownB ? 1 : 0));
     }
     if (lane == 0 && my_pairs) atomicAdd(pairs, (unsigned long long)my_pairs);
 }
@@ -234,8 +386,18 @@ int p2p_targets_per_lane() {
     return tpt;
 }
 
+bool sym_disabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("VFMM_P2P_SYM");
+        v = (e && e[0] == '0') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
-                const int2* tasks, Counters* ctr, int kernel, double2* near_uv, cudaStream_t s) {
+                const int2* tasks, Counters* ctr, int kernel, double2* near_uv, Rows rows,
+                cudaStream_t s) {
     // Items per warp: short-lived CTAs (default 2) let far-field CTAs in as SM
     // slots free up; the grid covers the upper bound of work items and CTAs
     // beyond the actual count exit at once.  VFMM_P2P_K overrides (tuning).
@@ -267,8 +429,23 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
     auto* fn = p2p_targets_per_lane() == 2 ? (g ? k_p2p<true, 2> : k_p2p<false, 2>)
                                            : (g ? k_p2p<true, 1> : k_p2p<false, 1>);
     fn<<<blocks, kP2PWarps * 32, 0, s>>>(src, leaf_starts, tasks, ctr, L.levels, L.n, T, near_uv,
-                                         &ctr->near_pairs, kk);
+                                         &ctr->near_pairs, kk, sym_disabled() ? 0 : 1);
     note_launches(1);
+    // symmetric kernel: runs instead when the device-side mode check allows it
+    static int KS = 0;
+    if (!KS) {
+        const char* e = getenv("VFMM_P2P_SYM_K");
+        KS = e ? atoi(e) : 4;
+        if (KS < 1) KS = 4;
+    }
+    const int64_t sym_items = 5ll << (2 * L.levels);
+    const unsigned sblocks = (unsigned)((sym_items + kSymWarps * KS - 1) / (kSymWarps * KS));
+    auto* sfn = g ? k_p2p_sym<true> : k_p2p_sym<false>;
+    if (!sym_disabled()) {
+        sfn<<<sblocks, kSymWarps * 32, 0, s>>>(src, leaf_starts, ctr, L.levels, L.n, rows, T, near_uv,
+                                               &ctr->near_pairs, KS);
+        note_launches(1);
+    }
 }
 
 int direct_nsplit(int64_t m, int64_t n) {

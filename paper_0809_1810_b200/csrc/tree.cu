@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(kWPB * 32)
                 int* __restrict__ hist0, unsigned* __restrict__ zero, int64_t nzero,
                 Counters* __restrict__ ctr) {
     extern __shared__ int sh[];
-    __shared__ unsigned long long wmax[kWPB];
+    __shared__ unsigned long long wmax[kWPB], wmin[kWPB];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t z = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; z < nzero;
          z += (int64_t)gridDim.x * blockDim.x)
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kWPB * 32)
     __syncwarp();
     const int m = 1 << levels;
     const double xmax = xmin + side, ymax = ymin + side;  // Domain.xmax (model.py:51-57)
-    unsigned long long sbits = 0ull;
+    unsigned long long sbits = 0ull, smin = ~0ull;
     const int64_t chunk = (int64_t)blockIdx.x * kWPB + warp;
     if (chunk < nchunks) {
         const int64_t beg = chunk * wc;
@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(kWPB * 32)
             if (sigma) {
                 const unsigned long long b = ordered_bits(sigma[i]);
                 sbits = b > sbits ? b : sbits;
+                smin = b < smin ? b : smin;
             }
         }
         __syncwarp();
@@ -84,12 +85,21 @@ __global__ void __launch_bounds__(kWPB * 32)
     for (int o = 16; o > 0; o >>= 1) {
         const unsigned long long t = __shfl_xor_sync(0xffffffffu, sbits, o);
         sbits = t > sbits ? t : sbits;
+        const unsigned long long u = __shfl_xor_sync(0xffffffffu, smin, o);
+        smin = u < smin ? u : smin;
     }
-    if (lane == 0) wmax[warp] = sbits;
+    if (lane == 0) {
+        wmax[warp] = sbits;
+        wmin[warp] = smin;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int w = 1; w < kWPB; ++w) sbits = wmax[w] > sbits ? wmax[w] : sbits;
+        for (int w = 1; w < kWPB; ++w) {
+            sbits = wmax[w] > sbits ? wmax[w] : sbits;
+            smin = wmin[w] < smin ? wmin[w] : smin;
+        }
         if (sbits) atomicMax(&ctr->sigma_max_bits, sbits);
+        if (smin != ~0ull) atomicMin(&ctr->sigma_min_bits, smin);
     }
 }
 
@@ -255,7 +265,7 @@ __global__ void k_leaf_starts(const int* __restrict__ keys, int64_t n, int nleav
 // Leaf cells also emit their P2P task count ceil(count / chunk).
 __global__ void k_counts_tasks(const int* __restrict__ ls, int levels, int64_t total_cells,
                                int chunk, Rows rows, int* __restrict__ counts,
-                               int* __restrict__ ntask) {
+                               int* __restrict__ ntask, Counters* __restrict__ ctr) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= total_cells) return;
     int k = 0;
@@ -279,7 +289,14 @@ __global__ void k_counts_tasks(const int* __restrict__ ls, int levels, int64_t t
     }
     counts[t] = c;
     // only leaves of the owned row strip get near-field tasks
-    if (k == levels) ntask[cell] = (iy >= rows.lo && iy < rows.hi) ? (c + chunk - 1) / chunk : 0;
+    int full = 0;
+    if (k == levels) {
+        ntask[cell] = (iy >= rows.lo && iy < rows.hi) ? (c + chunk - 1) / chunk : 0;
+        full = ls[cell + 1] - ls[cell];  // owned and halo rows (the symmetric P2P touches both)
+    }
+    // largest leaf: one atomic per warp
+    full = __reduce_max_sync(__activemask(), full);
+    if ((threadIdx.x & 31) == (__ffs(__activemask()) - 1) && full > 0) atomicMax(&ctr->max_leaf, full);
 }
 
 __global__ void k_tasks_fill(const int* __restrict__ ls, int levels, int chunk, Rows rows,
@@ -299,6 +316,8 @@ __global__ void k_init_counters(Counters* ctr) {
     ctr->m2l_count = 0ull;
     ctr->near_pairs = 0ull;
     ctr->sigma_max_bits = 0ull;
+    ctr->sigma_min_bits = ~0ull;
+    ctr->max_leaf = 0;
     ctr->bad_count = 0;
     ctr->first_bad = INT_MAX;
     ctr->ntasks = 0;
@@ -374,7 +393,7 @@ void launch_counts_tasks(const Layout& L, char* ws, Counters* ctr, bool tasks, R
     for (int k = 0; k <= L.levels; ++k) total += 1ll << (2 * k);
     const int chunk = 32 * p2p_targets_per_lane();
     k_counts_tasks<<<grid_for(total, 256), 256, 0, s>>>(ls, L.levels, total, chunk, rows, counts,
-                                                       nt);
+                                                       nt, ctr);
     note_launches(1);
     if (!tasks) return;
     const int nl = (int)L.nleaves;

@@ -26,7 +26,9 @@ constexpr int kQMax = 2 * kOrderCap + 16;  // H table length (padded for m-chunk
 constexpr int kOffsets = 49;               // 7x7 offset grid (dy+3)*7 + (dx+3)
 constexpr int kExpSteps = 64;              // exp table resolution: 2^(n/64)
 constexpr int kExpTabN = 60 * kExpSteps + 1;  // exp table entries, n = -3840..0
-constexpr int kNearRows = 3;               // P2P partial sums: one per neighbourhood row
+constexpr int kNearRows = 3;               // generic P2P: one partial sum per neighbourhood row
+constexpr int kNearSlots = 9;              // symmetric P2P: one per neighbour direction
+constexpr int kSymMaxLeaf = 128;           // symmetric P2P needs leaves of <= 128 particles
 
 // Packed per-particle source record in leaf-sorted order: x, y, gamma and
 // q2 = -1 / (2 sigma^2 ln 2) so that exp(-r^2/(2 sigma^2)) = 2^(r^2 q2).
@@ -39,10 +41,13 @@ struct Counters {
     unsigned long long m2l_count;
     unsigned long long near_pairs;
     unsigned long long sigma_max_bits;  // ordered-bits encoding of max sigma
+    unsigned long long sigma_min_bits;  // ordered-bits encoding of min sigma (~0 = none)
     int bad_count;
     int first_bad;
     int ntasks;
     int task_cursor;  // dynamic P2P work distribution
+    int max_leaf;     // largest leaf occupancy (owned rows)
+    int pad2;
 };
 
 // Translation tables (device globals, uploaded once per device).
@@ -105,10 +110,13 @@ void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_lo
                 cudaStream_t s);
 int p2p_targets_per_lane();  // 1 or 2 (env VFMM_P2P_TPT, default 1)
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
-                const int2* tasks, Counters* ctr, int kernel, double2* near_uv, cudaStream_t s);
+                const int2* tasks, Counters* ctr, int kernel, double2* near_uv, Rows rows,
+                cudaStream_t s);
+bool sym_disabled();  // env VFMM_P2P_SYM=0 forces the generic near-field kernel
 void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const int* keys,
                         const int* perm, const double2* loc, const double2* near_uv, double xmin,
-                        double ymin, double side, double* u, double* v, Rows rows, cudaStream_t s);
+                        double ymin, double side, double* u, double* v, Rows rows,
+                        const int* leaf_starts, const Counters* ctr, int kernel, cudaStream_t s);
 void launch_eval_at(const Layout& L, const Tables* T, const double* tx, const double* ty,
                     int64_t m, const Src* src, const int* leaf_starts, const double2* loc,
                     double xmin, double ymin, double side, int kernel, double* u, double* v,
@@ -142,6 +150,14 @@ __host__ __device__ __forceinline__ int64_t coef_stride(int k) {  // between coe
 }
 
 int coef_chunk(int P);  // TN of the chunked coefficient kernels (4..8)
+
+// Near-field mode, decided on the device after the build: the symmetric
+// (Newton's third law) block kernel needs one core size for every particle
+// (the blob factor uses the SOURCE sigma, engine.py:256) and small leaves.
+__device__ __forceinline__ bool p2p_symmetric(const Counters* c, bool gauss) {
+    const bool uniform = !gauss || c->sigma_min_bits == c->sigma_max_bits;
+    return uniform && c->max_leaf <= kSymMaxLeaf;
+}
 
 // ---- shared device math ----
 

@@ -4,6 +4,7 @@ within 1e-12 of the reference FMM relative to max|v| (the reference's own
 global normalisation, errors.py:64-73), exact m2l_count / near_pair_count, exact
 tree structure, bitwise run-to-run determinism."""
 import math
+import os
 import warnings
 
 import numpy as np
@@ -121,6 +122,36 @@ def test_expansions_match_oracle(name):
         assert (np.abs(gl[k] - ol) / sl).max() <= 1e-11, f"loc level {k}"
 
 
+def _symmetric_mode(c, n):
+    """Mirror of p2p_symmetric (vfmm_internal.cuh): uniform sigma (or point kernel)
+    and leaves of at most 128 particles select the symmetric near-field kernel."""
+    if os.environ.get("VFMM_P2P_SYM") == "0":
+        return False
+    uniform = (not c["gauss"]) or np.all(c["sigma"] == c["sigma"][0])
+    return uniform and np.bincount(O.leaf_keys(c["x"], c["y"], c["levels"], *(c["domain"] or enclosing(c["x"], c["y"])))).max() <= 128
+
+
+def _near_from_slots(ws, c, n):
+    lv = c["levels"]
+    m = 2**lv
+    if not _symmetric_mode(c, n):
+        rows = ws.view("near_uv", torch.float64, 6 * n).cpu().numpy().reshape(3, n, 2)
+        return (rows[0] + rows[1]) + rows[2]
+    slots = ws.view("near_uv", torch.float64, 18 * n).cpu().numpy().reshape(9, n, 2)
+    keys = ws.view("leaf_key", torch.int32, n).cpu().numpy()
+    ls = ws.view("leaf_starts", torch.int32, 4**lv + 1).cpu().numpy()
+    occ = np.diff(ls) > 0
+    iy, ix = keys // m, keys % m
+    near = np.zeros((n, 2))
+    for dy in (-1, 0, 1):
+        for dx in (-1, 0, 1):
+            nx, ny = ix + dx, iy + dy
+            ok = (nx >= 0) & (nx < m) & (ny >= 0) & (ny < m)
+            ok[ok] &= occ[(ny * m + nx)[ok]]
+            near[ok] += slots[(dy + 1) * 3 + dx + 1][ok]
+    return near
+
+
 @pytest.mark.parametrize("name", ["config0", "config1", "coincident", "big_leaf_l3", "point_kernel_l5"])
 def test_near_field_matches_oracle(name):
     c = eval_case(name)
@@ -128,8 +159,7 @@ def test_near_field_matches_oracle(name):
     run(c["x"], c["y"], c["gamma"], c["sigma"], c["levels"], c["order"], c["gauss"], dom)
     n = c["x"].size
     ws = Workspace.get(n, c["levels"], c["order"], torch.device("cuda", torch.cuda.current_device()))
-    rows = ws.view("near_uv", torch.float64, 6 * n).cpu().numpy().reshape(3, n, 2)
-    near = (rows[0] + rows[1]) + rows[2]
+    near = _near_from_slots(ws, c, n)
     _, st = O.evaluate(c["x"], c["y"], c["gamma"], c["sigma"], c["levels"], c["order"], c["gauss"], dom)
     ref = st["near_sorted"]
     assert np.abs(near - ref).max() <= 1e-13 * np.abs(ref).max()
@@ -142,6 +172,16 @@ def test_bitwise_determinism(overlap):
     b, s2, _ = run(w.x, w.y, w.gamma, w.sigma, w.levels, w.order, True, W.DOMAIN, overlap=not overlap)
     assert np.array_equal(a, b)
     assert s1.m2l_count == s2.m2l_count and s1.near_pair_count == s2.near_pair_count
+
+
+def test_generic_near_field_path_nonuniform_sigma():
+    """Non-uniform core sizes select the generic (row-slice) near-field kernel."""
+    w = W.config1()
+    sig = w.sigma * (1.0 + 0.01 * np.cos(7 * w.x))
+    vel, st, _ = run(w.x, w.y, w.gamma, sig, w.levels, w.order, True, W.DOMAIN)
+    ref, ost = O.evaluate(w.x, w.y, w.gamma, sig, w.levels, w.order, True, W.DOMAIN)
+    assert st.near_pair_count == ost["near_pair_count"] and st.m2l_count == ost["m2l_count"]
+    assert np.abs(vel - ref).max() <= REL_TOL * np.abs(ref).max()
 
 
 def test_drop_in_api_and_errors():
