@@ -8,6 +8,7 @@ The public names mirror ``vortexfmm/__init__.py:9-20`` for the hot path:
 hand-written sm_100a CUDA library ``libvfmm.so`` (C ABI: ``include/vfmm.h``).
 """
 
+from . import errors
 from .engine import (
     FmmConfig,
     FmmRunStats,
@@ -25,6 +26,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "Domain",
+    "errors",
     "FmmConfig",
     "FmmRunStats",
     "KernelKind",

@@ -193,6 +193,72 @@ __device__ __forceinline__ double pair_kernel(double dx, double dy, double& r2, 
     return fma(-inv, exp2_neg(clamp_neg60(r2 * q2), tab), inv);  // (1 - e) / r^2
 }
 
+// 32 rotation steps of one B chunk against one or two targets per lane
+// (TPL = 2: a0 = A[i0 + lane], a1 = A[i0 + 32 + lane]; each rotated source then
+// serves two symmetric pairs, halving the shuffles per pair).
+template <bool GAUSS, int TPL>
+__device__ __forceinline__ void rotate_sym(double a0x, double a0y, double a0g, double a1x,
+                                           double a1y, double a1g, double& bx, double& by,
+                                           double& bg, double& ub, double& vb, double q2,
+                                           const double* __restrict__ tab, int from, double& u0,
+                                           double& v0, double& u1, double& v1) {
+#pragma unroll 2
+    for (int st = 0; st < 32; ++st) {
+        {
+            const double dx = a0x - bx, dy = a0y - by;
+            double r2;
+            const double K = pair_kernel<GAUSS>(dx, dy, r2, q2, tab);
+            const double ca = bg * K, cb = a0g * K;
+            u0 = fma(-ca, dy, u0);
+            v0 = fma(ca, dx, v0);
+            ub = fma(cb, dy, ub);
+            vb = fma(-cb, dx, vb);
+        }
+        if (TPL == 2) {
+            const double dx = a1x - bx, dy = a1y - by;
+            double r2;
+            const double K = pair_kernel<GAUSS>(dx, dy, r2, q2, tab);
+            const double ca = bg * K, cb = a1g * K;
+            u1 = fma(-ca, dy, u1);
+            v1 = fma(ca, dx, v1);
+            ub = fma(cb, dy, ub);
+            vb = fma(-cb, dx, vb);
+        }
+        bx = __shfl_sync(0xffffffffu, bx, from);
+        by = __shfl_sync(0xffffffffu, by, from);
+        bg = __shfl_sync(0xffffffffu, bg, from);
+        ub = __shfl_sync(0xffffffffu, ub, from);
+        vb = __shfl_sync(0xffffffffu, vb, from);
+    }
+}
+
+template <bool GAUSS, int TPL>
+__device__ __forceinline__ void rotate_self(double a0x, double a0y, double a1x, double a1y,
+                                            double& bx, double& by, double& bg, double q2,
+                                            const double* __restrict__ tab, int from, double& u0,
+                                            double& v0, double& u1, double& v1) {
+#pragma unroll 2
+    for (int st = 0; st < 32; ++st) {
+        {
+            const double dx = a0x - bx, dy = a0y - by;
+            double r2;
+            const double c = bg * pair_kernel<GAUSS>(dx, dy, r2, q2, tab);
+            u0 = fma(-c, dy, u0);
+            v0 = fma(c, dx, v0);
+        }
+        if (TPL == 2) {
+            const double dx = a1x - bx, dy = a1y - by;
+            double r2;
+            const double c = bg * pair_kernel<GAUSS>(dx, dy, r2, q2, tab);
+            u1 = fma(-c, dy, u1);
+            v1 = fma(c, dx, v1);
+        }
+        bx = __shfl_sync(0xffffffffu, bx, from);
+        by = __shfl_sync(0xffffffffu, by, from);
+        bg = __shfl_sync(0xffffffffu, bg, from);
+    }
+}
+
 template <bool GAUSS>
 __global__ void __launch_bounds__(kSymWarps * 32, kSymBlocksPerSM)
     k_p2p_sym(const Src* __restrict__ src, const int* __restrict__ ls, Counters* __restrict__ ctr,
@@ -224,29 +290,26 @@ __global__ void __launch_bounds__(kSymWarps * 32, kSymBlocksPerSM)
         const bool ownA = cy >= rows.lo && cy < rows.hi;
         if (kind == 0) {
             if (!ownA) continue;
-            // self block: a <- b for all b in A (r^2 == 0 pairs contribute exactly 0)
-            for (int i0 = 0; i0 < nA; i0 += 32) {
-                double ax, ay, ag;
-                load_lane(src, loA + i0, min(32, nA - i0), lane, ax, ay, ag);
-                double ua = 0.0, va = 0.0;
+            // self block: a <- b for all b in A (r^2 == 0 pairs contribute exactly 0);
+            // two targets per lane when the chunk has more than 32
+            for (int i0 = 0; i0 < nA; i0 += 64) {
+                const int cntA = min(64, nA - i0);
+                double a0x, a0y, a0g, a1x, a1y, a1g;
+                load_lane(src, loA + i0, min(32, cntA), lane, a0x, a0y, a0g);
+                load_lane(src, loA + i0 + (cntA > 32 ? 32 : 0), max(cntA - 32, 0), lane, a1x, a1y, a1g);
+                double u0 = 0.0, v0 = 0.0, u1 = 0.0, v1 = 0.0;
+                const bool two = cntA > 32;
                 for (int j0 = 0; j0 < nA; j0 += 32) {
                     double bx, by, bg;
                     load_lane(src, loA + j0, min(32, nA - j0), lane, bx, by, bg);
-#pragma unroll 2
-                    for (int st = 0; st < 32; ++st) {
-                        const double dx = ax - bx, dy = ay - by;
-                        double r2;
-                        const double c = bg * pair_kernel<GAUSS>(dx, dy, r2, q2, tab);
-                        ua = fma(-c, dy, ua);
-                        va = fma(c, dx, va);
-                        bx = __shfl_sync(0xffffffffu, bx, from);
-                        by = __shfl_sync(0xffffffffu, by, from);
-                        bg = __shfl_sync(0xffffffffu, bg, from);
-                    }
+                    if (two)
+                        rotate_self<GAUSS, 2>(a0x, a0y, a1x, a1y, bx, by, bg, q2, tab, from, u0, v0, u1, v1);
+                    else
+                        rotate_self<GAUSS, 1>(a0x, a0y, a1x, a1y, bx, by, bg, q2, tab, from, u0, v0, u1, v1);
                 }
-                if (i0 + lane < nA)
-                    near9[(int64_t)slot_of(0, 0) * n + loA + i0 + lane] =
-                        make_double2(ua * kInv2Pi, va * kInv2Pi);
+                double2* out = near9 + (int64_t)slot_of(0, 0) * n + loA + i0;
+                if (lane < cntA) out[lane] = make_double2(u0 * kInv2Pi, v0 * kInv2Pi);
+                if (32 + lane < cntA) out[32 + lane] = make_double2(u1 * kInv2Pi, v1 * kInv2Pi);
             }
             my_pairs += (long long)nA * nA - nA;
             continue;
@@ -259,10 +322,13 @@ __global__ void __launch_bounds__(kSymWarps * 32, kSymBlocksPerSM)
         const int lb = byc * m + bxc;
         const int loB = ls[lb], nB = ls[lb + 1] - loB;
         if (nB == 0) continue;
-        for (int i0 = 0; i0 < nA; i0 += 32) {
-            double ax, ay, ag;
-            load_lane(src, loA + i0, min(32, nA - i0), lane, ax, ay, ag);
-            double ua = 0.0, va = 0.0;
+        for (int i0 = 0; i0 < nA; i0 += 64) {
+            const int cntA = min(64, nA - i0);
+            double a0x, a0y, a0g, a1x, a1y, a1g;
+            load_lane(src, loA + i0, min(32, cntA), lane, a0x, a0y, a0g);
+            load_lane(src, loA + i0 + (cntA > 32 ? 32 : 0), max(cntA - 32, 0), lane, a1x, a1y, a1g);
+            double u0 = 0.0, v0 = 0.0, u1 = 0.0, v1 = 0.0;
+            const bool two = cntA > 32;
             for (int j0 = 0; j0 < nB; j0 += 32) {
                 double bx, by, bg;
                 load_lane(src, loB + j0, min(32, nB - j0), lane, bx, by, bg);
@@ -272,27 +338,17 @@ __global__ void __launch_bounds__(kSymWarps * 32, kSymBlocksPerSM)
                     ub = t.x;
                     vb = t.y;
                 }
-#pragma unroll 2
-                for (int st = 0; st < 32; ++st) {
-                    const double dx = ax - bx, dy = ay - by;
-                    double r2;
-                    const double K = pair_kernel<GAUSS>(dx, dy, r2, q2, tab);
-                    const double ca = bg * K, cb = ag * K;
-                    ua = fma(-ca, dy, ua);
-                    va = fma(ca, dx, va);
-                    ub = fma(cb, dy, ub);
-                    vb = fma(-cb, dx, vb);
-                    bx = __shfl_sync(0xffffffffu, bx, from);
-                    by = __shfl_sync(0xffffffffu, by, from);
-                    bg = __shfl_sync(0xffffffffu, bg, from);
-                    ub = __shfl_sync(0xffffffffu, ub, from);
-                    vb = __shfl_sync(0xffffffffu, vb, from);
-                }
+                if (two)
+                    rotate_sym<GAUSS, 2>(a0x, a0y, a0g, a1x, a1y, a1g, bx, by, bg, ub, vb, q2, tab,
+                                         from, u0, v0, u1, v1);
+                else
+                    rotate_sym<GAUSS, 1>(a0x, a0y, a0g, a1x, a1y, a1g, bx, by, bg, ub, vb, q2, tab,
+                                         from, u0, v0, u1, v1);
                 acc[j0 + lane] = make_double2(ub, vb);
             }
-            if (i0 + lane < nA)
-                near9[(int64_t)slot_of(dx_, dy_) * n + loA + i0 + lane] =
-                    make_double2(ua * kInv2Pi, va * kInv2Pi);
+            double2* out = near9 + (int64_t)slot_of(dx_, dy_) * n + loA + i0;
+            if (lane < cntA) out[lane] = make_double2(u0 * kInv2Pi, v0 * kInv2Pi);
+            if (32 + lane < cntA) out[32 + lane] = make_double2(u1 * kInv2Pi, v1 * kInv2Pi);
         }
         __syncwarp();
         for (int j = lane; j < nB; j += 32) {
