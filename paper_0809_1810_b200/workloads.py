@@ -93,3 +93,35 @@ CONFIG4_GRID = [
 
 def by_index(i: int) -> Workload:
     return (config0, config1, config2, config3)[i]()
+
+
+def generate_particles(distribution: str, n: int, seed: int, domain=(0.0, 0.0, 1.0),
+                       sigma: float = 0.005):
+    """Seeded particle sets of the reference generator (model.py:71-122), as arrays.
+
+    One (n, 2) uniform position draw, then the circulation draw:
+    ``uniform_random`` Gamma ~ U(-1, 1); ``gaussian_patch`` Gamma =
+    exp(-r^2 / (2 s^2)) side^2 / n about the centre, s = side / 8;
+    ``two_patches`` the difference of two such patches at (1/4, 1/2) and
+    (3/4, 1/2) of the domain.  Used by the acceptance tests that reproduce
+    the reference's published numbers (test_output.txt:11-19).
+    """
+    xmin, ymin, side = domain
+    rng = np.random.default_rng(seed)
+    pos = rng.uniform(size=(n, 2))
+    x = xmin + side * pos[:, 0]
+    y = ymin + side * pos[:, 1]
+    s = side / 8.0
+    if distribution == "uniform_random":
+        g = rng.uniform(-1.0, 1.0, n)
+    elif distribution == "gaussian_patch":
+        cx, cy = xmin + 0.5 * side, ymin + 0.5 * side
+        g = np.exp(-((x - cx) ** 2 + (y - cy) ** 2) / (2.0 * s * s)) * side**2 / n
+    elif distribution == "two_patches":
+        cy = ymin + 0.5 * side
+        ra = (x - (xmin + 0.25 * side)) ** 2 + (y - cy) ** 2
+        rb = (x - (xmin + 0.75 * side)) ** 2 + (y - cy) ** 2
+        g = (np.exp(-ra / (2.0 * s * s)) - np.exp(-rb / (2.0 * s * s))) * side**2 / n
+    else:
+        raise ValueError(f"unknown distribution {distribution!r}")
+    return x, y, g, np.full(n, float(sigma))
