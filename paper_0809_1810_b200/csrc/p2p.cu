@@ -103,8 +103,7 @@ __global__ void __launch_bounds__(kP2PWarps * 32, kP2PBlocksPerSM)
           int sym_enabled) {
     if (sym_enabled && p2p_symmetric(ctr, GAUSS)) return;  // the symmetric kernel handles it
     const int nitems = ctr->ntasks * kNearRows;
-    if (items_per_warp < (1 << 30) && (int64_t)blockIdx.x * kP2PWarps * items_per_warp >= nitems)
-        return;  // spare CTA
+    if ((int64_t)blockIdx.x * kP2PWarps * items_per_warp >= nitems) return;  // spare CTA
     __shared__ double sexp[kExpTab];
     __shared__ __align__(16) Src sbuf[kP2PWarps][2][kChunk];
     const double* tab = stage_exp_table(sexp, T->exp2tab);
@@ -259,8 +258,8 @@ __device__ __forceinline__ void rotate_self(double a0x, double a0y, double a1x, 
     }
 }
 
-template <bool GAUSS>
-__global__ void __launch_bounds__(kSymWarps * 32, kSymBlocksPerSM)
+template <bool GAUSS, int MINB>
+__global__ void __launch_bounds__(kSymWarps * 32, MINB)
     k_p2p_sym(const Src* __restrict__ src, const int* __restrict__ ls, Counters* __restrict__ ctr,
               int levels, int64_t n, Rows rows, const Tables* __restrict__ T,
               double2* __restrict__ near9, unsigned long long* __restrict__ pairs,
@@ -278,11 +277,13 @@ __global__ void __launch_bounds__(kSymWarps * 32, kSymBlocksPerSM)
     const int from = (lane + 1) & 31;
     const double q2 = GAUSS ? src[0].q2 : 0.0;  // uniform core size
     long long my_pairs = 0;
+    // the next item index is fetched one item ahead to hide the atomic's latency
+    int next = 0;
+    if (lane == 0) next = atomicAdd(&ctr->task_cursor, 1);
     for (int it = 0; it < items_per_warp; ++it) {
-        int item = 0;
-        if (lane == 0) item = atomicAdd(&ctr->task_cursor, 1);
-        item = __shfl_sync(0xffffffffu, item, 0);
+        const int item = __shfl_sync(0xffffffffu, next, 0);
         if (item >= nitems) break;
+        if (lane == 0 && it + 1 < items_per_warp) next = atomicAdd(&ctr->task_cursor, 1);
         const int leaf = item / 5, kind = item % 5;
         const int loA = ls[leaf], nA = ls[leaf + 1] - loA;
         if (nA == 0) continue;
@@ -299,9 +300,11 @@ __global__ void __launch_bounds__(kSymWarps * 32, kSymBlocksPerSM)
                 load_lane(src, loA + i0 + (cntA > 32 ? 32 : 0), max(cntA - 32, 0), lane, a1x, a1y, a1g);
                 double u0 = 0.0, v0 = 0.0, u1 = 0.0, v1 = 0.0;
                 const bool two = cntA > 32;
+                double nbx, nby, nbg;
+                load_lane(src, loA, min(32, nA), lane, nbx, nby, nbg);
                 for (int j0 = 0; j0 < nA; j0 += 32) {
-                    double bx, by, bg;
-                    load_lane(src, loA + j0, min(32, nA - j0), lane, bx, by, bg);
+                    double bx = nbx, by = nby, bg = nbg;
+                    if (j0 + 32 < nA) load_lane(src, loA + j0 + 32, min(32, nA - j0 - 32), lane, nbx, nby, nbg);
                     if (two)
                         rotate_self<GAUSS, 2>(a0x, a0y, a1x, a1y, bx, by, bg, q2, tab, from, u0, v0, u1, v1);
                     else
@@ -329,9 +332,11 @@ __global__ void __launch_bounds__(kSymWarps * 32, kSymBlocksPerSM)
             load_lane(src, loA + i0 + (cntA > 32 ? 32 : 0), max(cntA - 32, 0), lane, a1x, a1y, a1g);
             double u0 = 0.0, v0 = 0.0, u1 = 0.0, v1 = 0.0;
             const bool two = cntA > 32;
+            double nbx, nby, nbg;  // B chunk data, prefetched one chunk ahead
+            load_lane(src, loB, min(32, nB), lane, nbx, nby, nbg);
             for (int j0 = 0; j0 < nB; j0 += 32) {
-                double bx, by, bg;
-                load_lane(src, loB + j0, min(32, nB - j0), lane, bx, by, bg);
+                double bx = nbx, by = nby, bg = nbg;
+                if (j0 + 32 < nB) load_lane(src, loB + j0 + 32, min(32, nB - j0 - 32), lane, nbx, nby, nbg);
                 double ub = 0.0, vb = 0.0;
                 if (i0 > 0) {
                     const double2 t = acc[j0 + lane];
@@ -463,24 +468,9 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
         K = e ? atoi(e) : 2;
         if (K < 1) K = 2;
     }
-    static int persist = -1;
-    if (persist < 0) {
-        const char* e = getenv("VFMM_P2P_PERSIST");
-        persist = e ? atoi(e) : 0;
-        if (persist > 0) {
-            int dev = 0, sms = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            persist *= sms;
-        }
-    }
     const size_t per_block = (size_t)kP2PWarps * K;
-    unsigned blocks = (unsigned)((L.max_tasks * kNearRows + per_block - 1) / per_block);
-    int kk = K;
-    if (persist > 0) {  // persistent grid of `persist` CTAs, no per-warp item cap
-        blocks = (unsigned)persist;
-        kk = 1 << 30;
-    }
+    const unsigned blocks = (unsigned)((L.max_tasks * kNearRows + per_block - 1) / per_block);
+    const int kk = K;
     const bool g = kernel == VFMM_KERNEL_GAUSSIAN;
     auto* fn = p2p_targets_per_lane() == 2 ? (g ? k_p2p<true, 2> : k_p2p<false, 2>)
                                            : (g ? k_p2p<true, 1> : k_p2p<false, 1>);
@@ -491,15 +481,22 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
     static int KS = 0;
     if (!KS) {
         const char* e = getenv("VFMM_P2P_SYM_K");
-        KS = e ? atoi(e) : 4;
-        if (KS < 1) KS = 4;
+        KS = e ? atoi(e) : 2;
+        if (KS < 1) KS = 2;
     }
     const int64_t sym_items = 5ll << (2 * L.levels);
     const unsigned sblocks = (unsigned)((sym_items + kSymWarps * KS - 1) / (kSymWarps * KS));
-    auto* sfn = g ? k_p2p_sym<true> : k_p2p_sym<false>;
+    const int ks = KS;
+    static int minb = 0;
+    if (!minb) {
+        const char* e = getenv("VFMM_P2P_SYM_MINB");
+        minb = (e && e[0] == '4') ? 4 : 3;
+    }
+    auto* sfn = minb == 3 ? (g ? k_p2p_sym<true, 3> : k_p2p_sym<false, 3>)
+                          : (g ? k_p2p_sym<true, 4> : k_p2p_sym<false, 4>);
     if (!sym_disabled()) {
         sfn<<<sblocks, kSymWarps * 32, 0, s>>>(src, leaf_starts, ctr, L.levels, L.n, rows, T, near_uv,
-                                               &ctr->near_pairs, KS);
+                                               &ctr->near_pairs, ks);
         note_launches(1);
     }
 }
