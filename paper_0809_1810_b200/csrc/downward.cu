@@ -12,99 +12,12 @@ namespace vfmm {
 
 namespace {
 
-constexpr int kL2LThreads = 128;
-
-// Thread = (child cell, chunk of TN output coefficients); a block covers one
-// child parity plane (= quadrant q), so F_q is block-uniform.  Child j of
-// plane q is cell (2 jx + qx, 2 jy + qy) whose parent is (jx, jy):
-//   Lh'_n += sum_{m>=n} (2^{-m} Lh_m) F_q[m-n]     (exact re-centring)
-template <int TN>
-__global__ void __launch_bounds__(kL2LThreads)
-    k_l2l(const double2* __restrict__ parent, double2* __restrict__ child, int level, int levels,
-          int P, const Tables* __restrict__ T, double2* __restrict__ leaf_out, Rows rows) {
-    __shared__ double2 sF[kOrderCap + 16];
-    __shared__ double s2[kOrderCap + 16];
-    const int half = 1 << (level - 1);
-    const int64_t np = (int64_t)half * half;  // cells per child plane
-    const int64_t bpp = (np + kL2LThreads - 1) / kL2LThreads;
-    const int q = (int)((blockIdx.x / bpp) & 3);
-    const int chunk = (int)(blockIdx.x / (4 * bpp));
-    for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        sF[i] = T->F[q][i];
-        s2[i] = T->pow2neg[i];
-    }
-    __syncthreads();
-    const int64_t j = (blockIdx.x % bpp) * kL2LThreads + threadIdx.x;
-    if (j >= np) return;
-    const int jx = (int)(j % half), jy = (int)(j / half);
-    if (!rows_touch(rows, 2 * jy + (q >> 1), levels - level)) return;  // outside the owned strip
-    const double2* L = parent + coef_base(level - 1, jx, jy);
-    const int64_t ps = coef_stride(level - 1);
-    const int n0 = chunk * TN;
-    double ax[TN], ay[TN];
-#pragma unroll
-    for (int t = 0; t < TN; ++t) ax[t] = ay[t] = 0.0;
-#pragma unroll 4
-    for (int m = n0; m < P; ++m) {
-        const double2 a = L[m * ps];
-        const double axs = a.x * s2[m], ays = a.y * s2[m];
-#pragma unroll
-        for (int t = 0; t < TN; ++t) {
-            if (m >= n0 + t) {
-                const double2 f = sF[m - n0 - t];
-                ax[t] = fma(axs, f.x, fma(-ays, f.y, ax[t]));
-                ay[t] = fma(axs, f.y, fma(ays, f.x, ay[t]));
-            }
-        }
-    }
-    const double2* in = child + q * np + j;
-    const int64_t cs = 4 * np;
-    // final level: completed leaf locals go to the cell-major leaf array
-    // (contiguous per leaf for L2P); otherwise accumulate in place
-    double2* out = child + q * np + j;
-    int64_t os = cs;
-    if (leaf_out) {
-        const int mc = 2 * half;
-        out = leaf_out + ((int64_t)(2 * jy + (q >> 1)) * mc + 2 * jx + (q & 1)) * P;
-        os = 1;
-    }
-#pragma unroll
-    for (int t = 0; t < TN; ++t) {
-        const int nn = n0 + t;
-        if (nn < P) {
-            double2 cur = in[nn * cs];
-            cur.x += ax[t];
-            cur.y += ay[t];
-            out[nn * os] = cur;
-        }
-    }
-}
-
 // levels == 2 has no L2L: copy the level-2 planar locals to the cell-major leaf array
 __global__ void k_leaf_locals_copy(const double2* __restrict__ loc2, int P, double2* __restrict__ out) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= 16 * P) return;
     const int cell = t / P, n = t % P;
     out[t] = loc2[n * coef_stride(2) + coef_base(2, cell & 3, cell >> 2)];
-}
-
-template <int TN>
-void launch_l2l_tn(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc, Rows rows,
-                   cudaStream_t s) {
-    const int nchunks = (L.P + TN - 1) / TN;
-    for (int level = 3; level <= L.levels; ++level) {
-        const int64_t np = 1ll << (2 * (level - 1));
-        const int64_t bpp = (np + kL2LThreads - 1) / kL2LThreads;
-        const double2* parent = loc + L.level_cell_off[level - 1] * L.P;
-        double2* child = loc + L.level_cell_off[level] * L.P;
-        k_l2l<TN><<<(unsigned)(bpp * 4 * nchunks), kL2LThreads, 0, s>>>(
-            parent, child, level, L.levels, L.P, T, level == L.levels ? leaf_loc : nullptr, rows);
-        note_launches(1);
-    }
-    if (L.levels == 2) {
-        k_leaf_locals_copy<<<(16 * L.P + 127) / 128, 128, 0, s>>>(loc, L.P, leaf_loc);
-        note_launches(1);
-    }
 }
 
 // Horner evaluation of the leaf local expansion at z:
@@ -223,15 +136,9 @@ __global__ void __launch_bounds__(256)
 
 }  // namespace
 
-void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc, Rows rows,
-                cudaStream_t s) {
-    switch (coef_chunk(L.P)) {
-        case 4: launch_l2l_tn<4>(L, T, loc, leaf_loc, rows, s); break;
-        case 5: launch_l2l_tn<5>(L, T, loc, leaf_loc, rows, s); break;
-        case 6: launch_l2l_tn<6>(L, T, loc, leaf_loc, rows, s); break;
-        case 7: launch_l2l_tn<7>(L, T, loc, leaf_loc, rows, s); break;
-        default: launch_l2l_tn<8>(L, T, loc, leaf_loc, rows, s); break;
-    }
+void launch_leaf_locals_copy(const Layout& L, const double2* loc, double2* leaf_loc, cudaStream_t s) {
+    k_leaf_locals_copy<<<(16 * L.P + 127) / 128, 128, 0, s>>>(loc, L.P, leaf_loc);
+    note_launches(1);
 }
 
 void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const int* keys,

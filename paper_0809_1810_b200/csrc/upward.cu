@@ -83,71 +83,6 @@ __global__ void __launch_bounds__(kP2MWarps * 32)
     }
 }
 
-constexpr int kM2MThreads = 128;
-
-// Thread = (parent cell, chunk of TN output coefficients).  The four children
-// of parent (jx, jy) sit at index j = jy*mp + jx of the child level's four
-// planes, so every child coefficient load is coalesced across the warp.
-// Children in quadrant order (0,0), (1,0), (0,1), (1,1) like engine.py:140-145.
-template <int TN>
-__global__ void __launch_bounds__(kM2MThreads)
-    k_m2m(const double2* __restrict__ child, double2* __restrict__ parent, int level, int P,
-          int nchunks, const Tables* __restrict__ T) {
-    __shared__ double2 sE[4][kOrderCap + 16];
-    __shared__ double s2[kOrderCap + 16];
-    for (int i = threadIdx.x; i < 4 * P; i += blockDim.x) sE[i / P][i % P] = T->E[i / P][i % P];
-    for (int i = threadIdx.x; i <= P; i += blockDim.x) s2[i] = T->pow2neg[i];
-    __syncthreads();
-    const int mp = 1 << (level - 1);
-    const int64_t np = (int64_t)mp * mp;
-    const int64_t bpc = (np + kM2MThreads - 1) / kM2MThreads;
-    const int chunk = (int)(blockIdx.x / bpc);
-    const int64_t pidx = (blockIdx.x % bpc) * kM2MThreads + threadIdx.x;
-    if (pidx >= np) return;
-    const int m0 = chunk * TN;
-    const int kend = min(P - 1, m0 + TN - 1);
-    double ax[TN], ay[TN];
-#pragma unroll
-    for (int t = 0; t < TN; ++t) ax[t] = ay[t] = 0.0;
-    for (int q = 0; q < 4; ++q) {
-        const double2* M = child + q * np + pidx;
-#pragma unroll 4
-        for (int k = 0; k <= kend; ++k) {
-            const double2 a = M[(int64_t)k * 4 * np];
-#pragma unroll
-            for (int t = 0; t < TN; ++t) {
-                if (k <= m0 + t) {
-                    const double2 e = sE[q][m0 + t - k];
-                    ax[t] = fma(a.x, e.x, fma(-a.y, e.y, ax[t]));
-                    ay[t] = fma(a.x, e.y, fma(a.y, e.x, ay[t]));
-                }
-            }
-        }
-    }
-    const int jx = (int)(pidx % mp), jy = (int)(pidx / mp);
-    double2* out = parent + coef_base(level - 1, jx, jy);
-    const int64_t cs = coef_stride(level - 1);
-#pragma unroll
-    for (int t = 0; t < TN; ++t) {
-        const int mm = m0 + t;
-        if (mm < P) out[mm * cs] = make_double2(ax[t] * s2[mm + 1], ay[t] * s2[mm + 1]);
-    }
-}
-
-template <int TN>
-void launch_m2m_tn(const Layout& L, const Tables* T, double2* mult, cudaStream_t s) {
-    const int nchunks = (L.P + TN - 1) / TN;
-    for (int level = L.levels; level >= 3; --level) {
-        const int64_t np = 1ll << (2 * (level - 1));
-        const int64_t bpc = (np + kM2MThreads - 1) / kM2MThreads;
-        double2* child = mult + L.level_cell_off[level] * L.P;
-        double2* parent = mult + L.level_cell_off[level - 1] * L.P;
-        k_m2m<TN><<<(unsigned)(bpc * nchunks), kM2MThreads, 0, s>>>(child, parent, level, L.P,
-                                                                    nchunks, T);
-        note_launches(1);
-    }
-}
-
 }  // namespace
 
 int coef_chunk(int P) {
@@ -165,16 +100,6 @@ void launch_p2m(const Layout& L, const Src* src, const int* leaf_starts, double 
     k_p2m<<<(unsigned)((nl + kP2MWarps - 1) / kP2MWarps), kP2MWarps * 32, 0, s>>>(
         src, leaf_starts, L.levels, L.P, xmin, ymin, side, T, rows, mult_leaf);
     note_launches(1);
-}
-
-void launch_m2m(const Layout& L, const Tables* T, double2* mult, cudaStream_t s) {
-    switch (coef_chunk(L.P)) {
-        case 4: launch_m2m_tn<4>(L, T, mult, s); break;
-        case 5: launch_m2m_tn<5>(L, T, mult, s); break;
-        case 6: launch_m2m_tn<6>(L, T, mult, s); break;
-        case 7: launch_m2m_tn<7>(L, T, mult, s); break;
-        default: launch_m2m_tn<8>(L, T, mult, s); break;
-    }
 }
 
 }  // namespace vfmm
