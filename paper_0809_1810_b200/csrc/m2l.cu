@@ -21,7 +21,6 @@ namespace vfmm {
 
 namespace {
 
-constexpr int kM2LThreads = 128;
 
 // Offsets of the interaction list of parity class (px, py) in row-major
 // order (engine._il_offsets, engine.py:77-89), as (dx, dy) pairs.
@@ -37,17 +36,26 @@ __device__ __forceinline__ void il_offset(int px, int py, int o, int& dx, int& d
         }
 }
 
-// Thread = (destination j of one parity plane, chunk of TN outputs).  With the
-// planar layout the source of offset (dx, dy) for consecutive destinations is
-// a run of consecutive cells of one source plane, so each multipole
-// coefficient load is coalesced; the Hankel rows are block-uniform smem
-// broadcasts.  Output written to the destination plane, coalesced.
+// Block = 32 destinations j of one parity plane x one chunk of TN outputs, as
+// kGroups warps: warp g accumulates the offsets [9g, 9g + 9) of the parity
+// class (row-major order, engine.py:166-185) and the partial sums are added
+// in group order through shared memory (deterministic).  With the planar
+// layout the source of offset (dx, dy) for consecutive destinations is a run
+// of consecutive cells of one source plane, so each multipole coefficient
+// load is coalesced; the Hankel rows are block-uniform smem broadcasts.
+constexpr int kGroups = 3;
+constexpr int kDestPerBlock = 32;
+
+// Multipole source for destinations whose source is empty / outside the grid:
+// a zero coefficient read with stride 0 (no per-coefficient select).
+__device__ const double2 g_zero_coef = {0.0, 0.0};
+
 template <int TN>
-__global__ void __launch_bounds__(kM2LThreads)
+__global__ void __launch_bounds__(kDestPerBlock * kGroups, 8)
     k_m2l(const double2* __restrict__ mult, const int* __restrict__ counts, double2* __restrict__ loc,
           int levels, int P, int nchunks, const Tables* __restrict__ T,
           unsigned long long* __restrict__ m2l_count, Rows rows) {
-    extern __shared__ double2 sH[];  // [27][TN + P - 1]
+    extern __shared__ double2 sH[];  // [27][TN + P - 1], then [kGroups - 1][TN][32] partials
     // ---- decode (level, parity, chunk, block-in-class) from blockIdx.x ----
     int64_t b = blockIdx.x;
     int level = 2;
@@ -56,7 +64,7 @@ __global__ void __launch_bounds__(kM2LThreads)
     int64_t bpc = 0;      // blocks per (parity, chunk) at this level
     for (;;) {
         const int64_t dests = 1ll << (2 * (level - 1));
-        bpc = (dests + kM2LThreads - 1) / kM2LThreads;
+        bpc = (dests + kDestPerBlock - 1) / kDestPerBlock;
         const int64_t nb = bpc * 4 * nchunks;
         if (b < nb || level == levels) break;
         b -= nb;
@@ -70,19 +78,26 @@ __global__ void __launch_bounds__(kM2LThreads)
     const int px = parity & 1, py = parity >> 1;
     const int m0 = chunk * TN;
     const int HL = TN + P - 1;
+    const int group = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    // ---- stage the 27 H rows of this parity class ----
+    // ---- stage the 27 offsets and their H rows of this parity class ----
+    __shared__ int2 soff[27];
+    if (threadIdx.x < 27) {
+        int dxo = 0, dyo = 0;
+        il_offset(px, py, threadIdx.x, dxo, dyo);
+        soff[threadIdx.x] = make_int2(dxo, dyo);
+    }
+    __syncthreads();
     for (int i = threadIdx.x; i < 27 * HL; i += blockDim.x) {
         const int o = i / HL, q = i % HL;
-        int dxo = 0, dyo = 0;
-        il_offset(px, py, o, dxo, dyo);
-        sH[i] = T->H[(dyo + 3) * 7 + (dxo + 3)][m0 + q];
+        const int2 d = soff[o];
+        sH[i] = T->H[(d.y + 3) * 7 + (d.x + 3)][m0 + q];
     }
     __syncthreads();
 
     const int mk = 1 << level, half = mk >> 1;
     const int64_t psz = (int64_t)half * half;  // cells per plane
-    const int64_t j = blk * kM2LThreads + threadIdx.x;
+    const int64_t j = blk * kDestPerBlock + lane;
     const int jx = j < psz ? (int)(j % half) : 0;
     const int jy = j < psz ? (int)(j / half) : 0;
     const int ix = 2 * jx + px, iy = 2 * jy + py;
@@ -99,45 +114,56 @@ __global__ void __launch_bounds__(kM2LThreads)
 #pragma unroll
     for (int t = 0; t < TN; ++t) ax[t] = ay[t] = 0.0;
     int ntrans = 0;
-    int o = 0;
-    for (int dy = -2 - py; dy < 4 - py; ++dy) {
-        for (int dx = -2 - px; dx < 4 - px; ++dx) {
-            const int adx = dx < 0 ? -dx : dx, ady = dy < 0 ? -dy : dy;
-            if ((adx > ady ? adx : ady) < 2) continue;
-            const int sx = ix + dx, sy = iy + dy;
-            const bool inr = active && sx >= 0 && sx < mk && sy >= 0 && sy < mk;
-            const bool live = inr && cnt[(int64_t)sy * mk + sx] > 0;
-            ntrans += (live && counts_here) ? 1 : 0;
-            const double2* h = sH + o * HL;
-            ++o;
-            if (!__any_sync(0xffffffffu, live)) continue;
-            // source plane / index (floor division of the shifted coordinates)
-            const int sp = ((sy & 1) << 1) | (sx & 1);
-            const double2* Ms = M + sp * psz + (live ? (int64_t)(sy >> 1) * half + (sx >> 1) : 0);
-#pragma unroll 2
-            for (int n = 0; n < P; ++n) {
-                double2 a = Ms[n * cstride];
-                if (!live) a = make_double2(0.0, 0.0);
+    for (int o = 9 * group; o < 9 * group + 9; ++o) {
+        const int2 d = soff[o];
+        const int sx = ix + d.x, sy = iy + d.y;
+        const bool inr = active && sx >= 0 && sx < mk && sy >= 0 && sy < mk;
+        const bool live = inr && cnt[(int64_t)sy * mk + sx] > 0;
+        ntrans += (live && counts_here) ? 1 : 0;
+        if (!__any_sync(0xffffffffu, live)) continue;
+        const double2* h = sH + o * HL;
+        // source plane / index (floor division of the shifted coordinates)
+        const int sp = ((sy & 1) << 1) | (sx & 1);
+        const double2* Ms =
+            live ? M + sp * psz + (int64_t)(sy >> 1) * half + (sx >> 1) : &g_zero_coef;
+        const int64_t step = live ? cstride : 0;
+#pragma unroll 3
+        for (int n = 0; n < P; ++n) {
+            const double2 a = *Ms;
+            Ms += step;
 #pragma unroll
-                for (int t = 0; t < TN; ++t) {
-                    const double2 hh = h[t + n];
-                    ax[t] = fma(hh.x, a.x, fma(-hh.y, a.y, ax[t]));
-                    ay[t] = fma(hh.x, a.y, fma(hh.y, a.x, ay[t]));
-                }
+            for (int t = 0; t < TN; ++t) {
+                const double2 hh = h[t + n];
+                ax[t] = fma(hh.x, a.x, fma(-hh.y, a.y, ax[t]));
+                ay[t] = fma(hh.x, a.y, fma(hh.y, a.x, ay[t]));
             }
         }
     }
-    if (active) {
+    // ---- combine the group partials in group order ----
+    double2* part = sH + 27 * HL;
+    if (group > 0) {
+#pragma unroll
+        for (int t = 0; t < TN; ++t) part[((group - 1) * TN + t) * 32 + lane] = make_double2(ax[t], ay[t]);
+    }
+    __syncthreads();
+    if (group == 0 && active) {
         double2* out = loc + cell_off * P + parity * psz + j;
 #pragma unroll
-        for (int t = 0; t < TN; ++t)
-            if (m0 + t < P) out[(m0 + t) * cstride] = make_double2(ax[t], ay[t]);
+        for (int t = 0; t < TN; ++t) {
+            double sx = ax[t], sy = ay[t];
+            for (int g = 1; g < kGroups; ++g) {
+                const double2 p = part[((g - 1) * TN + t) * 32 + lane];
+                sx += p.x;
+                sy += p.y;
+            }
+            if (m0 + t < P) out[(m0 + t) * cstride] = make_double2(sx, sy);
+        }
     }
     if (chunk == 0) {
         // m2l_count counts (destination, nonempty source) pairs at every level
         // including empty destinations (engine.py:173-180)
         for (int s = 16; s > 0; s >>= 1) ntrans += __shfl_xor_sync(0xffffffffu, ntrans, s);
-        if ((threadIdx.x & 31) == 0 && ntrans) atomicAdd(m2l_count, (unsigned long long)ntrans);
+        if (lane == 0 && ntrans) atomicAdd(m2l_count, (unsigned long long)ntrans);
     }
 }
 
@@ -148,11 +174,12 @@ void launch_tn(const Layout& L, const Tables* T, const double2* mult, const int*
     int64_t blocks = 0;
     for (int level = 2; level <= L.levels; ++level) {
         const int64_t dests = 1ll << (2 * (level - 1));
-        blocks += (dests + kM2LThreads - 1) / kM2LThreads * 4 * nchunks;
+        blocks += (dests + kDestPerBlock - 1) / kDestPerBlock * 4 * nchunks;
     }
-    const size_t shm = (size_t)27 * (TN + L.P - 1) * sizeof(double2);
-    k_m2l<TN><<<(unsigned)blocks, kM2LThreads, shm, s>>>(mult, counts, loc, L.levels, L.P, nchunks,
-                                                       T, &ctr->m2l_count, rows);
+    const size_t shm = (size_t)27 * (TN + L.P - 1) * sizeof(double2) +
+                       (size_t)(kGroups - 1) * TN * 32 * sizeof(double2);
+    k_m2l<TN><<<(unsigned)blocks, kDestPerBlock * kGroups, shm, s>>>(
+        mult, counts, loc, L.levels, L.P, nchunks, T, &ctr->m2l_count, rows);
     note_launches(1);
 }
 
