@@ -5,6 +5,7 @@
 // build (quadtree.py:182-201 + engine.py:355-358), upward (engine.py:114-147),
 // m2l (engine.py:150-187), downward (engine.py:190-202), near
 // (engine.py:260-285), eval = far field + combine (engine.py:205-213, 394-396).
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -153,7 +154,7 @@ void fill_stats(const Layout& L, const Counters& c, int kernel, double side, vfm
     st->m2l_count = (int64_t)c.m2l_count;
     st->near_pair_count = (int64_t)c.near_pairs;
     st->bad_count = c.bad_count;
-    st->first_bad = c.bad_count ? (int64_t)c.first_bad : -1;
+    st->first_bad = c.bad_count ? (int64_t)(INT_MAX - c.first_bad_neg) : -1;
     st->max_sigma = decode_sigma(c.sigma_max_bits);
     // engine.py:362: tree.half_width(levels) / 2 = side / 2^(levels+1) / 2
     st->sigma_guard = side / std::ldexp(1.0, L.levels + 1) / 2.0;
@@ -180,9 +181,7 @@ bool make_layout(int64_t n, int levels, int order, Layout* L) {
     const int bits = 2 * levels;
     L->passes = (bits + 7) / 8;
     L->digit_bits = (bits + L->passes - 1) / L->passes;
-    int64_t wc = (n + 148 * 16 - 1) / (148 * 16);
-    wc = (wc + 31) / 32 * 32;
-    if (wc < 512) wc = 512;
+    const int64_t wc = 512;  // elements per radix warp chunk (16 rounds of 32)
     L->wc = (int)wc;
     L->nchunks = (int)((n + wc - 1) / wc);
     const size_t B = (size_t)1 << L->digit_bits;

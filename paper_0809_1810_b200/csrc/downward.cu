@@ -6,6 +6,8 @@
 // (engine.py:205-213), expansions.f_to_velocity (expansions.py:217-225), the
 // combine in engine.evaluate (engine.py:394-396) and the far + near parts of
 // engine.evaluate_at (engine.py:434-459).
+#include <climits>
+
 #include "vfmm_internal.cuh"
 
 namespace vfmm {
@@ -105,7 +107,7 @@ __global__ void __launch_bounds__(256)
     const double xmax = xmin + side, ymax = ymin + side;
     if (!((x >= xmin) && (x <= xmax) && (y >= ymin) && (y <= ymax))) {
         atomicAdd(&ctr->bad_count, 1);
-        atomicMin(&ctr->first_bad, (int)i);
+        atomicMax(&ctr->first_bad_neg, INT_MAX - (int)i);
         u[i] = 0.0;
         v[i] = 0.0;
         return;

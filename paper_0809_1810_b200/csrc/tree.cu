@@ -52,30 +52,43 @@ __global__ void __launch_bounds__(kWPB * 32)
     if (chunk < nchunks) {
         const int64_t beg = chunk * wc;
         const int64_t end = beg + wc < n ? beg + wc : n;
-#pragma unroll 4
-        for (int64_t i = beg + lane; i < end; i += 32) {
-            const double xi = x[i], yi = y[i];
-            const bool inside = (xi >= xmin) && (xi <= xmax) && (yi >= ymin) && (yi <= ymax);
-            int ix = 0, iy = 0;
-            if (inside) {
-                // quadtree.py:44-45: min(int((x - xmin) / side * m), m - 1)
-                const double tx = (xi - xmin) / side * (double)m;
-                const double ty = (yi - ymin) / side * (double)m;
-                ix = (int)tx;
-                iy = (int)ty;
-                ix = ix < m - 1 ? ix : m - 1;
-                iy = iy < m - 1 ? iy : m - 1;
-            } else {
-                atomicAdd(&ctr->bad_count, 1);
-                atomicMin(&ctr->first_bad, (int)i);
+        constexpr int R = 8;  // rounds whose loads are issued together
+        for (int64_t b0 = beg; b0 < end; b0 += 32 * R) {
+            double xr[R], yr[R], sr[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int64_t i = b0 + 32 * r + lane;
+                xr[r] = i < end ? x[i] : 0.0;
+                yr[r] = i < end ? y[i] : 0.0;
+                sr[r] = (sigma && i < end) ? sigma[i] : 0.0;
             }
-            const int k = iy * m + ix;
-            key[i] = k;
-            atomicAdd(&h[k & (B - 1)], 1);
-            if (sigma) {
-                const unsigned long long b = ordered_bits(sigma[i]);
-                sbits = b > sbits ? b : sbits;
-                smin = b < smin ? b : smin;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int64_t i = b0 + 32 * r + lane;
+                if (i >= end) continue;
+                const double xi = xr[r], yi = yr[r];
+                const bool inside = (xi >= xmin) && (xi <= xmax) && (yi >= ymin) && (yi <= ymax);
+                int ix = 0, iy = 0;
+                if (inside) {
+                    // quadtree.py:44-45: min(int((x - xmin) / side * m), m - 1)
+                    const double tx = (xi - xmin) / side * (double)m;
+                    const double ty = (yi - ymin) / side * (double)m;
+                    ix = (int)tx;
+                    iy = (int)ty;
+                    ix = ix < m - 1 ? ix : m - 1;
+                    iy = iy < m - 1 ? iy : m - 1;
+                } else {
+                    atomicAdd(&ctr->bad_count, 1);
+                    atomicMax(&ctr->first_bad_neg, INT_MAX - (int)i);
+                }
+                const int k = iy * m + ix;
+                key[i] = k;
+                atomicAdd(&h[k & (B - 1)], 1);
+                if (sigma) {
+                    const unsigned long long b = ordered_bits(sr[r]);
+                    sbits = b > sbits ? b : sbits;
+                    smin = b < smin ? b : smin;
+                }
             }
         }
         __syncwarp();
@@ -99,7 +112,7 @@ __global__ void __launch_bounds__(kWPB * 32)
             smin = wmin[w] < smin ? wmin[w] : smin;
         }
         if (sbits) atomicMax(&ctr->sigma_max_bits, sbits);
-        if (smin != ~0ull) atomicMin(&ctr->sigma_min_bits, smin);
+        if (smin != ~0ull) atomicMax(&ctr->sigma_min_neg, ~smin);
     }
 }
 
@@ -126,7 +139,7 @@ __global__ void __launch_bounds__(kWPB * 32)
     const unsigned lt = (1u << lane) - 1u;
     const int64_t beg = chunk * wc;
     const int64_t end = beg + wc < n ? beg + wc : n;
-    constexpr int R = 4;  // rounds whose loads are issued together
+    constexpr int R = 8;  // rounds whose loads are issued together
     for (int64_t base0 = beg; base0 < end; base0 += 32 * R) {
     int kr[R], vr[R];
 #pragma unroll
@@ -171,7 +184,8 @@ __global__ void __launch_bounds__(kWPB * 32)
 // ---- single-pass exclusive scan (int32, in place), decoupled look-back ----
 constexpr int kScanThreads = 512;
 constexpr int kScanItems = 4;
-constexpr int kScanTile = kScanThreads * kScanItems;
+constexpr int kScanSub = 4;
+constexpr int kScanTile = kScanThreads * kScanItems * kScanSub;
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
 constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
@@ -202,6 +216,9 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_sums, int* 
 // state[0] = tile ticket, state[1 + t] = status of tile t (all zero on entry).
 // Tiles are numbered by ticket, so every predecessor of a running tile has
 // started and the look-back always terminates.
+// A tile is kScanSub sub-tiles of kScanThreads x 4 consecutive ints (int4
+// loads, fully coalesced), scanned one after another with a running carry;
+// one look-back per tile keeps the serial chain short (~n / 8192 tiles).
 __global__ void __launch_bounds__(kScanThreads)
     k_scan(int* __restrict__ data, int64_t n, unsigned long long* __restrict__ state) {
     __shared__ int warp_sums[32];
@@ -211,23 +228,39 @@ __global__ void __launch_bounds__(kScanThreads)
     if (threadIdx.x == 0) tile_s = (int)atomicAdd(&state[0], 1ull);
     __syncthreads();
     const int tile = tile_s;
-    const int64_t base = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
-    int vals[kScanItems];
-    int s = 0;
+    const int64_t tile_base = (int64_t)tile * kScanTile;
+    int vals[kScanSub][kScanItems];
+    int run[kScanSub];
+    int carry = 0;
 #pragma unroll
-    for (int j = 0; j < kScanItems; ++j) {
-        vals[j] = (base + j < n) ? data[base + j] : 0;
-        s += vals[j];
+    for (int sub = 0; sub < kScanSub; ++sub) {
+        const int64_t base = tile_base + (int64_t)sub * kScanThreads * kScanItems +
+                             (int64_t)threadIdx.x * kScanItems;
+        if (base + kScanItems <= n && (reinterpret_cast<uintptr_t>(data + base) & 15) == 0) {
+            const int4 q = *reinterpret_cast<const int4*>(data + base);
+            vals[sub][0] = q.x;
+            vals[sub][1] = q.y;
+            vals[sub][2] = q.z;
+            vals[sub][3] = q.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < kScanItems; ++j) vals[sub][j] = (base + j < n) ? data[base + j] : 0;
+        }
+        int s = 0;
+#pragma unroll
+        for (int j = 0; j < kScanItems; ++j) s += vals[sub][j];
+        run[sub] = carry + block_exclusive_scan(s, warp_sums, &total);
+        carry += total;
+        __syncthreads();
     }
-    int run = block_exclusive_scan(s, warp_sums, &total);
     if (threadIdx.x == 0) {
         volatile unsigned long long* st = state + 1;
         long long prefix = 0;
         if (tile == 0) {
             __threadfence();
-            st[0] = kFlagIncl | (unsigned long long)total;
+            st[0] = kFlagIncl | (unsigned long long)carry;
         } else {
-            st[tile] = kFlagAgg | (unsigned long long)total;
+            st[tile] = kFlagAgg | (unsigned long long)carry;
             __threadfence();
             for (int j = tile - 1; j >= 0;) {
                 const unsigned long long w = st[j];
@@ -237,16 +270,22 @@ __global__ void __launch_bounds__(kScanThreads)
                 --j;
             }
             __threadfence();
-            st[tile] = kFlagIncl | (unsigned long long)(prefix + total);
+            st[tile] = kFlagIncl | (unsigned long long)(prefix + carry);
         }
         prefix_s = prefix;
     }
     __syncthreads();
-    run += (int)prefix_s;
+    const int pre = (int)prefix_s;
 #pragma unroll
-    for (int j = 0; j < kScanItems; ++j) {
-        if (base + j < n) data[base + j] = run;
-        run += vals[j];
+    for (int sub = 0; sub < kScanSub; ++sub) {
+        const int64_t base = tile_base + (int64_t)sub * kScanThreads * kScanItems +
+                             (int64_t)threadIdx.x * kScanItems;
+        int r = run[sub] + pre;
+#pragma unroll
+        for (int j = 0; j < kScanItems; ++j) {
+            if (base + j < n) data[base + j] = r;
+            r += vals[sub][j];
+        }
     }
 }
 
@@ -312,25 +351,13 @@ __global__ void k_tasks_fill(const int* __restrict__ ls, int levels, int chunk, 
     if (i == nleaves - 1) ctr->ntasks = o + nt;
 }
 
-__global__ void k_init_counters(Counters* ctr) {
-    ctr->m2l_count = 0ull;
-    ctr->near_pairs = 0ull;
-    ctr->sigma_max_bits = 0ull;
-    ctr->sigma_min_bits = ~0ull;
-    ctr->max_leaf = 0;
-    ctr->bad_count = 0;
-    ctr->first_bad = INT_MAX;
-    ctr->ntasks = 0;
-    ctr->task_cursor = 0;
-}
 
 inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
 
 }  // namespace
 
 void launch_init_counters(Counters* ctr, cudaStream_t s) {
-    k_init_counters<<<1, 1, 0, s>>>(ctr);
-    note_launches(1);
+    cudaMemsetAsync(ctr, 0, sizeof(Counters), s);
 }
 
 size_t scan_tiles(int64_t n) { return (size_t)((n + kScanTile - 1) / kScanTile); }

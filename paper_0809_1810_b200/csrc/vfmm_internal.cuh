@@ -36,14 +36,15 @@ struct __align__(16) Src {
     double x, y, g, q2;
 };
 
-// Device-side counters (one struct at a fixed workspace offset).
+// Device-side counters (one struct at a fixed workspace offset).  Every field
+// is zero-initialised (a memset node) and reduced with max/add atomics.
 struct Counters {
     unsigned long long m2l_count;
     unsigned long long near_pairs;
     unsigned long long sigma_max_bits;  // ordered-bits encoding of max sigma
-    unsigned long long sigma_min_bits;  // ordered-bits encoding of min sigma (~0 = none)
+    unsigned long long sigma_min_neg;   // ~(ordered bits) of min sigma, max-reduced (0 = none)
     int bad_count;
-    int first_bad;
+    int first_bad_neg;  // INT_MAX - smallest out-of-domain index, max-reduced
     int ntasks;
     int task_cursor;  // dynamic P2P work distribution
     int max_leaf;     // largest leaf occupancy (owned rows)
@@ -156,7 +157,7 @@ int coef_chunk(int P);  // TN of the chunked coefficient kernels (4..8)
 // (Newton's third law) block kernel needs one core size for every particle
 // (the blob factor uses the SOURCE sigma, engine.py:256) and small leaves.
 __device__ __forceinline__ bool p2p_symmetric(const Counters* c, bool gauss) {
-    const bool uniform = !gauss || c->sigma_min_bits == c->sigma_max_bits;
+    const bool uniform = !gauss || ~c->sigma_min_neg == c->sigma_max_bits;
     return uniform && c->max_leaf <= kSymMaxLeaf;
 }
 
