@@ -333,7 +333,7 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         launch_init_counters(ctr, s);
         launch_build(L, x, y, gamma, kernel == VFMM_KERNEL_GAUSSIAN ? sigma : nullptr, xmin, ymin,
                      side, ws, ctr, s, &keys, &perm);
-        launch_counts_tasks(L, ws, ctr, !far_only, rows, s);
+        launch_counts_tasks(L, ws, ctr, !far_only, rows, kernel == VFMM_KERNEL_GAUSSIAN, s);
         rec(1, s);
         // Overlap: the far-field chain runs on a high-priority stream and the near
         // field on a low-priority one; P2P CTAs are short-lived, so far-field CTAs

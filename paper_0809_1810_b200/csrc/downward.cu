@@ -30,6 +30,7 @@ __device__ __forceinline__ double2 eval_local(const double2* __restrict__ Lh, in
     const double nx = -wx, ny = -wy;
     const double2 top = Lh[(P - 1) * stride];
     double ax = top.x * invfact[P - 1], ay = top.y * invfact[P - 1];
+#pragma unroll 6
     for (int k = P - 2; k >= 0; --k) {
         const double2 c = Lh[k * stride];
         const double f = invfact[k];
@@ -60,27 +61,31 @@ __global__ void __launch_bounds__(256)
     const double r = side / m;
     const double cx = cell_center(xmin, ix, r), cy = cell_center(ymin, iy, r);
     const double inv_r = 1.0 / r;
-    const Src s = src[i];
-    const double2 f =
-        eval_local(loc + (int64_t)leaf * P, 1, P, (s.x - cx) * inv_r, (s.y - cy) * inv_r, sfact);
     double2 nv = make_double2(0.0, 0.0);
     if (sym_enabled && p2p_symmetric(ctr, gauss)) {
-        // symmetric kernel: one slot per existing non-empty neighbour leaf, direction order
-        for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx) {
-                const int nx = ix + dx, ny = iy + dy;
-                if (nx < 0 || nx >= m || ny < 0 || ny >= m) continue;
-                const int nl = ny * m + nx;
-                if (ls[nl + 1] == ls[nl]) continue;
-                const double2 t = near_uv[(int64_t)((dy + 1) * 3 + dx + 1) * n + i];
-                nv.x += t.x;
-                nv.y += t.y;
+        // symmetric kernel: one slot per existing non-empty neighbour leaf, in
+        // direction order; all nine loads are issued before any is consumed
+        double2 t[kNearSlots];
+#pragma unroll
+        for (int k = 0; k < kNearSlots; ++k) t[k] = near_uv[(int64_t)k * n + i];
+#pragma unroll
+        for (int k = 0; k < kNearSlots; ++k) {
+            const int nx = ix + k % 3 - 1, ny = iy + k / 3 - 1;
+            const bool ok = nx >= 0 && nx < m && ny >= 0 && ny < m &&
+                            ls[ny * m + nx + 1] != ls[ny * m + nx];
+            if (ok) {
+                nv.x += t[k].x;
+                nv.y += t[k].y;
             }
+        }
     } else {
         // generic kernel: the three neighbourhood-row partial sums, in row order
         const double2 n0 = near_uv[i], n1 = near_uv[n + i], n2 = near_uv[2 * n + i];
         nv = make_double2((n0.x + n1.x) + n2.x, (n0.y + n1.y) + n2.y);
     }
+    const Src s = src[i];
+    const double2 f =
+        eval_local(loc + (int64_t)leaf * P, 1, P, (s.x - cx) * inv_r, (s.y - cy) * inv_r, sfact);
     // f_to_velocity: u = Im f / 2pi, v = Re f / 2pi; then far + near
     const int o = perm[i];
     u[o] = f.y * kInv2Pi + nv.x;

@@ -220,7 +220,10 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_sums, int* 
 // loads, fully coalesced), scanned one after another with a running carry;
 // one look-back per tile keeps the serial chain short (~n / 8192 tiles).
 __global__ void __launch_bounds__(kScanThreads)
-    k_scan(int* __restrict__ data, int64_t n, unsigned long long* __restrict__ state) {
+    k_scan(int* __restrict__ data, int64_t n, unsigned long long* __restrict__ state,
+           const Counters* __restrict__ sym_skip, bool gauss) {
+    // the near-field task list is not needed when the symmetric P2P kernel runs
+    if (sym_skip && p2p_symmetric(sym_skip, gauss)) return;
     __shared__ int warp_sums[32];
     __shared__ int total;
     __shared__ int tile_s;
@@ -339,7 +342,9 @@ __global__ void k_counts_tasks(const int* __restrict__ ls, int levels, int64_t t
 }
 
 __global__ void k_tasks_fill(const int* __restrict__ ls, int levels, int chunk, Rows rows,
-                             const int* __restrict__ off, int2* __restrict__ tasks, Counters* ctr) {
+                             const int* __restrict__ off, int2* __restrict__ tasks, Counters* ctr,
+                             bool gauss, bool sym_enabled) {
+    if (sym_enabled && p2p_symmetric(ctr, gauss)) return;  // symmetric P2P: no task list
     const int nleaves = 1 << (2 * levels);
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nleaves) return;
@@ -362,9 +367,10 @@ void launch_init_counters(Counters* ctr, cudaStream_t s) {
 
 size_t scan_tiles(int64_t n) { return (size_t)((n + kScanTile - 1) / kScanTile); }
 
-void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream_t s) {
+void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream_t s,
+                     const Counters* sym_skip, bool gauss) {
     if (n <= 0) return;
-    k_scan<<<(unsigned)scan_tiles(n), kScanThreads, 0, s>>>(data, n, state);
+    k_scan<<<(unsigned)scan_tiles(n), kScanThreads, 0, s>>>(data, n, state, sym_skip, gauss);
     note_launches(1);
 }
 
@@ -391,7 +397,7 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     note_launches(1);
     cudaMemsetAsync(ws + L.scan_state, 0, L.scan_state_bytes, s);
     for (int p = 0; p < L.passes; ++p) {
-        launch_scan_i32(hist(p), hsize, state(p), s);
+        launch_scan_i32(hist(p), hsize, state(p), s, nullptr, false);
         const bool last = p == L.passes - 1;
         k_radix_scatter<<<blocks, kWPB * 32, shm, s>>>(
             kbuf[p & 1], p == 0 ? nullptr : vbuf[p & 1], kbuf[(p + 1) & 1], vbuf[(p + 1) & 1], L.n,
@@ -412,7 +418,7 @@ void launch_leaf_starts(const int* sorted_keys, int64_t n, int nleaves, int* lea
 }
 
 void launch_counts_tasks(const Layout& L, char* ws, Counters* ctr, bool tasks, Rows rows,
-                         cudaStream_t s) {
+                         bool gauss, cudaStream_t s) {
     const int* ls = (const int*)(ws + L.leaf_starts);
     int* counts = (int*)(ws + L.counts);
     int* nt = (int*)(ws + L.task_scratch);
@@ -424,10 +430,12 @@ void launch_counts_tasks(const Layout& L, char* ws, Counters* ctr, bool tasks, R
     note_launches(1);
     if (!tasks) return;
     const int nl = (int)L.nleaves;
+    const bool sym = !sym_disabled();
     launch_scan_i32(nt, nl, (unsigned long long*)(ws + L.scan_state) +
-                                (size_t)L.passes * (L.scan_state_tiles + 1), s);
+                                (size_t)L.passes * (L.scan_state_tiles + 1), s,
+                    sym ? ctr : nullptr, gauss);
     k_tasks_fill<<<grid_for(nl, 256), 256, 0, s>>>(ls, L.levels, chunk, rows, nt,
-                                                 (int2*)(ws + L.tasks), ctr);
+                                                 (int2*)(ws + L.tasks), ctr, gauss, sym);
     note_launches(1);
 }
 

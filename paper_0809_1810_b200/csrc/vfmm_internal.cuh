@@ -95,12 +95,13 @@ void note_launches(int k);
 void launch_build(const Layout& L, const double* x, const double* y, const double* g,
                   const double* sigma, double xmin, double ymin, double side, char* ws,
                   Counters* ctr, cudaStream_t s, int** keys_out, int** perm_out);
-void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream_t s);
+void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream_t s,
+                     const Counters* sym_skip, bool gauss);
 size_t scan_tiles(int64_t n);
 void launch_leaf_starts(const int* sorted_keys, int64_t n, int nleaves, int* leaf_starts,
                         cudaStream_t s);
 void launch_counts_tasks(const Layout& L, char* ws, Counters* ctr, bool tasks, Rows rows,
-                         cudaStream_t s);
+                         bool gauss, cudaStream_t s);
 void launch_p2m(const Layout& L, const Src* src, const int* leaf_starts, double xmin, double ymin,
                 double side, double2* mult_leaf, const Tables* T, Rows rows, cudaStream_t s);
 void launch_init_counters(Counters* ctr, cudaStream_t s);
