@@ -10,8 +10,9 @@ A step is one full ``evaluate`` (tree build, P2M, M2M, M2L, L2L, P2P, L2P,
 combine) over the resident particle set.  ``value`` = N / mean step time with
 inputs resident in HBM (CUDA graph replay of the C-ABI call; L2 flushed
 between steps by writing a 256 MiB buffer outside the timed events).
-``e2e`` = the same metric through the public API call with pinned HOST
-buffers: H2D of x, y, gamma, sigma and D2H of (u, v) inside the timed region.
+``e2e`` = the same metric through the public host-buffer API call
+(``evaluate_host`` -> ``vfmm_evaluate_host``) with pinned HOST buffers: H2D of
+x, y, gamma, sigma and D2H of (u, v) inside the timed region.
 
 ``--impl reference`` times the reference algorithm's CPU implementation (the
 numpy oracle port in oracle/, the reference being pure Python) on a bounded
@@ -263,8 +264,7 @@ def run_ours(args):
     for i in range(args.e2e_steps + 2):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(cur)
-        vel, _ = vf.evaluate_arrays(hx, hy, hg, hs, cfg, dom, overlap=True)
-        host_out.copy_(vel, non_blocking=True)
+        vf.evaluate_host(hx, hy, hg, hs, cfg, dom, out=host_out, overlap=True)
         b.record(cur)
         b.synchronize()
         if i >= 2:

@@ -103,6 +103,17 @@ int vfmm_evaluate(const double* x, const double* y, const double* gamma, const d
                   int kernel, double* u, double* v, void* workspace, size_t workspace_bytes,
                   unsigned flags, vfmm_stats* stats, void* stream);
 
+/* engine.evaluate with HOST buffers (the reference's numpy-in / numpy-out
+ * contract, engine.py:335-398): x, y, gamma, sigma and u, v are host arrays
+ * (pinned for full speed).  The copies are staged through the workspace and
+ * overlapped with the build: positions first (binning / sort need only them),
+ * gamma and sigma while the sort runs; u, v are copied back at the end.
+ * Synchronous on `stream` only if VFMM_FLAG_STATS is set.                   */
+int vfmm_evaluate_host(const double* x, const double* y, const double* gamma, const double* sigma,
+                       int64_t n, double xmin, double ymin, double side, int levels, int order,
+                       int kernel, double* u, double* v, void* workspace, size_t workspace_bytes,
+                       unsigned flags, vfmm_stats* stats, void* stream);
+
 /* Sharded evaluate (one process per GPU; leaves sharded in row strips).
  * The local arrays hold this rank's owned particles (leaf rows [row_lo,
  * row_hi) of the 2^levels x 2^levels leaf grid) plus halo copies of the

@@ -17,6 +17,7 @@ from .engine import (
     evaluate_arrays,
     evaluate_at,
     evaluate_at_arrays,
+    evaluate_host,
 )
 from .kernels import TWO_PI, KernelKind, velocity_direct, velocity_direct_arrays
 from .model import Domain, Particle, enclosing_domain, to_arrays
@@ -39,6 +40,7 @@ __all__ = [
     "evaluate_arrays",
     "evaluate_at",
     "evaluate_at_arrays",
+    "evaluate_host",
     "grid_indices",
     "to_arrays",
     "velocity_direct",

@@ -37,6 +37,7 @@ EXPORTED_SYMBOLS = (
     "vfmm_workspace_size",
     "vfmm_layout_of",
     "vfmm_evaluate",
+    "vfmm_evaluate_host",
     "vfmm_evaluate_shard",
     "vfmm_mult_region",
     "vfmm_counts_region",
@@ -114,6 +115,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.vfmm_layout_of.argtypes = [_I64, _I, _I, ctypes.POINTER(VfmmLayout)]
         lib.vfmm_evaluate.argtypes = [_P, _P, _P, _P, _I64, _D, _D, _D, _I, _I, _I, _P, _P, _P, _SZ,
                                       ctypes.c_uint, ctypes.POINTER(VfmmStats), _P]
+        lib.vfmm_evaluate_host.argtypes = lib.vfmm_evaluate.argtypes
         lib.vfmm_evaluate_shard.argtypes = [_P, _P, _P, _P, _I64, _D, _D, _D, _I, _I, _I, _I, _I, _P,
                                             _P, _P, _SZ, ctypes.c_uint, ctypes.POINTER(VfmmStats), _P]
         lib.vfmm_mult_region.argtypes = [_I64, _I, _I, ctypes.POINTER(_SZ), ctypes.POINTER(_SZ)]

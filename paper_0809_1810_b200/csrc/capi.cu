@@ -31,7 +31,9 @@ struct Resources {
     bool ready = false;
     cudaStream_t far = nullptr;   // far-field chain (highest priority)
     cudaStream_t near = nullptr;  // near field (lowest priority)
+    cudaStream_t comp = nullptr;  // compute stream of host-buffer evaluates
     cudaEvent_t fork = nullptr, join_far = nullptr, join_near = nullptr;
+    cudaEvent_t xy = nullptr, gs = nullptr, done = nullptr;
     cudaEvent_t ev[9] = {};
 };
 Resources g_res[kMaxDevices];
@@ -118,6 +120,10 @@ Resources* resources_for(int dev) {
             return nullptr;
         if (cudaStreamCreateWithPriority(&r.near, cudaStreamNonBlocking, lo) != cudaSuccess)
             return nullptr;
+        if (cudaStreamCreateWithFlags(&r.comp, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        cudaEventCreateWithFlags(&r.xy, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&r.gs, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&r.join_far, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&r.join_near, cudaEventDisableTiming);
@@ -226,6 +232,7 @@ bool make_layout(int64_t n, int levels, int order, Layout* L) {
     L->loc = take(sizeof(double2) * cells * L->P);
     L->leaf_loc = take(sizeof(double2) * L->nleaves * L->P);
     L->tasks = take(sizeof(int2) * L->max_tasks);
+    L->stage = take(sizeof(double) * 6 * n);  // host-mode staging: x, y, gamma, sigma, u, v
     L->total = off;
     return true;
 }
@@ -285,10 +292,18 @@ int vfmm_layout_of(int64_t n, int levels, int order, vfmm_layout* out) {
 namespace {
 
 // One evaluate (or one phase of a sharded evaluate) over leaf rows [row_lo, row_hi).
+// Host-buffer I/O of vfmm_evaluate_host: staged through the workspace.
+struct HostIO {
+    const double *hx, *hy, *hg, *hs;
+    double *hu, *hv;
+};
+
+// One evaluate (or one phase of a sharded evaluate) over leaf rows [row_lo, row_hi).
 int evaluate_impl(const double* x, const double* y, const double* gamma, const double* sigma,
                   int64_t n, double xmin, double ymin, double side, int levels, int order,
                   int kernel, double* u, double* v, void* workspace, size_t workspace_bytes,
-                  unsigned flags, Rows rows, vfmm_stats* stats, void* stream) {
+                  unsigned flags, Rows rows, vfmm_stats* stats, void* stream,
+                  const HostIO* hio = nullptr) {
     const bool timed = (flags & VFMM_FLAG_STATS) != 0;
     const bool far_only = (flags & VFMM_FLAG_FAR_ONLY) != 0;
     bool up = (flags & VFMM_FLAG_PHASE_UP) != 0, down = (flags & VFMM_FLAG_PHASE_DOWN) != 0;
@@ -304,7 +319,7 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
     make_layout(n, levels, order, &L);
     if (!workspace || workspace_bytes < L.total) return VFMM_EWORKSPACE;
     int dev = 0;
-    if (current_device_of(x, &dev) != 0) return VFMM_ECUDA;
+    if (current_device_of(hio ? workspace : (const void*)x, &dev) != 0) return VFMM_ECUDA;
     const Tables* T = tables_for(dev);
     Resources* R = resources_for(dev);
     if (!T || !R) return VFMM_ECUDA;
@@ -326,20 +341,46 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
     };
     for (int i = 0; i < 9; ++i) rec(i, s);  // every event defined even for a single phase
 
-    cudaStream_t fs = s;
+    // Host mode: x, y are copied first (the keys only need positions); gamma
+    // and sigma follow on the copy engine while the sort runs, and only the
+    // last radix pass waits for them.  Compute runs on an internal stream.
+    cudaStream_t cs = s;
+    cudaEvent_t gs_ready = nullptr;
+    if (hio) {
+        double* st = (double*)(ws + L.stage);
+        const size_t b = sizeof(double) * (size_t)n;
+        double *dx = st, *dy = st + n, *dg = st + 2 * n, *dsg = st + 3 * n;
+        cudaMemcpyAsync(dx, hio->hx, b, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(dy, hio->hy, b, cudaMemcpyHostToDevice, s);
+        cudaEventRecord(R->xy, s);
+        cudaMemcpyAsync(dg, hio->hg, b, cudaMemcpyHostToDevice, s);
+        if (hio->hs) cudaMemcpyAsync(dsg, hio->hs, b, cudaMemcpyHostToDevice, s);
+        cudaEventRecord(R->gs, s);
+        cudaStreamWaitEvent(R->comp, R->xy, 0);
+        cs = R->comp;
+        gs_ready = R->gs;
+        x = dx;
+        y = dy;
+        gamma = dg;
+        sigma = hio->hs ? dsg : nullptr;
+        u = st + 4 * n;
+        v = st + 5 * n;
+    }
+
+    cudaStream_t fs = cs;
     if (up) {
-        rec(0, s);
+        if (!hio) rec(0, cs);
         // ---- build: binning, stable sort, pack, leaf starts, occupancy, tasks ----
-        launch_init_counters(ctr, s);
+        launch_init_counters(ctr, cs);
         launch_build(L, x, y, gamma, kernel == VFMM_KERNEL_GAUSSIAN ? sigma : nullptr, xmin, ymin,
-                     side, ws, ctr, s, &keys, &perm);
-        launch_counts_tasks(L, ws, ctr, !far_only, rows, kernel == VFMM_KERNEL_GAUSSIAN, s);
-        rec(1, s);
+                     side, ws, ctr, cs, &keys, &perm, gs_ready);
+        launch_counts_tasks(L, ws, ctr, !far_only, rows, kernel == VFMM_KERNEL_GAUSSIAN, cs);
+        rec(1, cs);
         // Overlap: the far-field chain runs on a high-priority stream and the near
         // field on a low-priority one; P2P CTAs are short-lived, so far-field CTAs
         // are scheduled as soon as any SM slot frees up.
         if (overlap) {
-            cudaEventRecord(R->fork, s);
+            cudaEventRecord(R->fork, cs);
             cudaStreamWaitEvent(R->far, R->fork, 0);
             cudaStreamWaitEvent(R->near, R->fork, 0);
             fs = R->far;
@@ -350,7 +391,7 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         rec(2, fs);
     }
     if (down) {
-        if (!up) rec(2, s);
+        if (!up) rec(2, cs);
         // ---- M2L (all levels, one launch) ----
         launch_m2l(L, T, mult, counts, loc, ctr, rows, fs);
         rec(3, fs);
@@ -363,15 +404,22 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
             launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, rows, R->near);
             rec(8, R->near);
             cudaEventRecord(R->join_near, R->near);
-            cudaStreamWaitEvent(s, R->join_far, 0);
-            cudaStreamWaitEvent(s, R->join_near, 0);
+            cudaStreamWaitEvent(cs, R->join_far, 0);
+            cudaStreamWaitEvent(cs, R->join_near, 0);
         }
         if (!far_only) {
-            if (!overlap) launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, rows, s);
-            rec(5, s);
+            if (!overlap) launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, rows, cs);
+            rec(5, cs);
             launch_l2p_combine(L, T, src, keys, perm, (const double2*)(ws + L.leaf_loc), near_uv,
-                               xmin, ymin, side, u, v, rows, ls, ctr, kernel, s);
+                               xmin, ymin, side, u, v, rows, ls, ctr, kernel, cs);
         }
+    }
+    if (hio) {
+        const size_t b = sizeof(double) * (size_t)n;
+        cudaMemcpyAsync(hio->hu, u, b, cudaMemcpyDeviceToHost, cs);
+        cudaMemcpyAsync(hio->hv, v, b, cudaMemcpyDeviceToHost, cs);
+        cudaEventRecord(R->done, cs);
+        cudaStreamWaitEvent(s, R->done, 0);
     }
     rec(6, s);
     if (cudaGetLastError() != cudaSuccess) return VFMM_ECUDA;
@@ -415,6 +463,21 @@ int vfmm_evaluate(const double* x, const double* y, const double* gamma, const d
     return evaluate_impl(x, y, gamma, sigma, n, xmin, ymin, side, levels, order, kernel, u, v,
                          workspace, workspace_bytes, flags & ~(VFMM_FLAG_PHASE_UP | VFMM_FLAG_PHASE_DOWN),
                          Rows{0, 1 << levels}, stats, stream);
+}
+
+int vfmm_evaluate_host(const double* x, const double* y, const double* gamma, const double* sigma,
+                       int64_t n, double xmin, double ymin, double side, int levels, int order,
+                       int kernel, double* u, double* v, void* workspace, size_t workspace_bytes,
+                       unsigned flags, vfmm_stats* stats, void* stream) {
+    if (levels < 2 || levels > VFMM_LEVELS_CAP) return VFMM_EINVAL;
+    if (!x || !y || !gamma || !u || !v || (kernel == VFMM_KERNEL_GAUSSIAN && !sigma))
+        return VFMM_EINVAL;
+    const HostIO io{x, y, gamma, kernel == VFMM_KERNEL_GAUSSIAN ? sigma : nullptr, u, v};
+    // staging pointers are substituted inside; pass the host ones for the argument checks
+    return evaluate_impl(x, y, gamma, sigma, n, xmin, ymin, side, levels, order, kernel, u, v,
+                         workspace, workspace_bytes,
+                         flags & ~(VFMM_FLAG_PHASE_UP | VFMM_FLAG_PHASE_DOWN | VFMM_FLAG_FAR_ONLY),
+                         Rows{0, 1 << levels}, stats, stream, &io);
 }
 
 int vfmm_evaluate_shard(const double* x, const double* y, const double* gamma, const double* sigma,

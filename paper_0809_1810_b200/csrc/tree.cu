@@ -30,13 +30,12 @@ __device__ __forceinline__ unsigned long long ordered_bits(double d) {
 // Warp chunk c = elements [c*wc, (c+1)*wc).  Also zeroes the scratch words
 // (later histograms, scan look-back state) with a grid-stride loop.
 __global__ void __launch_bounds__(kWPB * 32)
-    k_keys_hist(const double* __restrict__ x, const double* __restrict__ y,
-                const double* __restrict__ sigma, int64_t n, double xmin, double ymin, double side,
+    k_keys_hist(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                double xmin, double ymin, double side,
                 int levels, int bits, int wc, int nchunks, int* __restrict__ key,
                 int* __restrict__ hist0, unsigned* __restrict__ zero, int64_t nzero,
                 Counters* __restrict__ ctr) {
     extern __shared__ int sh[];
-    __shared__ unsigned long long wmax[kWPB], wmin[kWPB];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t z = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; z < nzero;
          z += (int64_t)gridDim.x * blockDim.x)
@@ -47,20 +46,18 @@ __global__ void __launch_bounds__(kWPB * 32)
     __syncwarp();
     const int m = 1 << levels;
     const double xmax = xmin + side, ymax = ymin + side;  // Domain.xmax (model.py:51-57)
-    unsigned long long sbits = 0ull, smin = ~0ull;
     const int64_t chunk = (int64_t)blockIdx.x * kWPB + warp;
     if (chunk < nchunks) {
         const int64_t beg = chunk * wc;
         const int64_t end = beg + wc < n ? beg + wc : n;
         constexpr int R = 8;  // rounds whose loads are issued together
         for (int64_t b0 = beg; b0 < end; b0 += 32 * R) {
-            double xr[R], yr[R], sr[R];
+            double xr[R], yr[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int64_t i = b0 + 32 * r + lane;
                 xr[r] = i < end ? x[i] : 0.0;
                 yr[r] = i < end ? y[i] : 0.0;
-                sr[r] = (sigma && i < end) ? sigma[i] : 0.0;
             }
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -84,35 +81,10 @@ __global__ void __launch_bounds__(kWPB * 32)
                 const int k = iy * m + ix;
                 key[i] = k;
                 atomicAdd(&h[k & (B - 1)], 1);
-                if (sigma) {
-                    const unsigned long long b = ordered_bits(sr[r]);
-                    sbits = b > sbits ? b : sbits;
-                    smin = b < smin ? b : smin;
-                }
             }
         }
         __syncwarp();
         for (int d = lane; d < B; d += 32) hist0[(int64_t)d * nchunks + chunk] = h[d];
-    }
-    // block max of the sigma bits, one atomic per block
-    for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long t = __shfl_xor_sync(0xffffffffu, sbits, o);
-        sbits = t > sbits ? t : sbits;
-        const unsigned long long u = __shfl_xor_sync(0xffffffffu, smin, o);
-        smin = u < smin ? u : smin;
-    }
-    if (lane == 0) {
-        wmax[warp] = sbits;
-        wmin[warp] = smin;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < kWPB; ++w) {
-            sbits = wmax[w] > sbits ? wmax[w] : sbits;
-            smin = wmin[w] < smin ? wmin[w] : smin;
-        }
-        if (sbits) atomicMax(&ctr->sigma_max_bits, sbits);
-        if (smin != ~0ull) atomicMax(&ctr->sigma_min_neg, ~smin);
     }
 }
 
@@ -127,13 +99,15 @@ __global__ void __launch_bounds__(kWPB * 32)
                     int wc, int nchunks, const int* __restrict__ offs, int* __restrict__ hist_next,
                     const double* __restrict__ x, const double* __restrict__ y,
                     const double* __restrict__ g, const double* __restrict__ sigma,
-                    Src* __restrict__ src) {
+                    Src* __restrict__ src, Counters* __restrict__ ctr) {
     extern __shared__ int sh[];
+    __shared__ unsigned long long wmax[kWPB], wmin[kWPB];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int B = 1 << bits;
     int* run = sh + warp * B;
     const int64_t chunk = (int64_t)blockIdx.x * kWPB + warp;
-    if (chunk >= nchunks) return;
+    unsigned long long sbits = 0ull, smin = ~0ull;  // max / min core size (final pass)
+    if (chunk < nchunks) {
     for (int d = lane; d < B; d += 32) run[d] = offs[(int64_t)d * nchunks + chunk];
     __syncwarp();
     const unsigned lt = (1u << lane) - 1u;
@@ -165,6 +139,11 @@ __global__ void __launch_bounds__(kWPB * 32)
                 atomicAdd(&hist_next[(int64_t)((k >> (shift + bits)) & (B - 1)) * nchunks + pos / wc], 1);
             } else {
                 const double s = sigma ? sigma[v] : 1.0;
+                if (sigma) {
+                    const unsigned long long b = ordered_bits(s);
+                    sbits = b > sbits ? b : sbits;
+                    smin = b < smin ? b : smin;
+                }
                 Src r;
                 r.x = x[v];
                 r.y = y[v];
@@ -178,6 +157,27 @@ __global__ void __launch_bounds__(kWPB * 32)
         if (valid && rank == __popc(peers) - 1) run[d] += __popc(peers);
         __syncwarp();
     }
+    }
+    }
+    if (hist_next || !sigma) return;  // block-uniform: sigma statistics in the final pass only
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, sbits, o);
+        sbits = t > sbits ? t : sbits;
+        const unsigned long long u = __shfl_xor_sync(0xffffffffu, smin, o);
+        smin = u < smin ? u : smin;
+    }
+    if (lane == 0) {
+        wmax[warp] = sbits;
+        wmin[warp] = smin;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kWPB; ++w) {
+            sbits = wmax[w] > sbits ? wmax[w] : sbits;
+            smin = wmin[w] < smin ? wmin[w] : smin;
+        }
+        if (sbits) atomicMax(&ctr->sigma_max_bits, sbits);
+        if (smin != ~0ull) atomicMax(&ctr->sigma_min_neg, ~smin);
     }
 }
 
@@ -376,7 +376,8 @@ void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream
 
 void launch_build(const Layout& L, const double* x, const double* y, const double* g,
                   const double* sigma, double xmin, double ymin, double side, char* ws,
-                  Counters* ctr, cudaStream_t s, int** keys_out, int** perm_out) {
+                  Counters* ctr, cudaStream_t s, int** keys_out, int** perm_out,
+                  cudaEvent_t gs_ready) {
     int* kbuf[2] = {(int*)(ws + L.key_a), (int*)(ws + L.key_b)};
     int* vbuf[2] = {(int*)(ws + L.val_a), (int*)(ws + L.val_b)};
     const int bits = L.digit_bits;
@@ -391,7 +392,7 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     // scratch zeroed by the first kernel: histograms of passes 1.. and all scan states
     unsigned* zero = (unsigned*)(ws + L.hist) + hsize;
     const int64_t nzero_hist = hsize * (L.passes - 1);
-    k_keys_hist<<<blocks, kWPB * 32, shm, s>>>(x, y, sigma, L.n, xmin, ymin, side, L.levels, bits,
+    k_keys_hist<<<blocks, kWPB * 32, shm, s>>>(x, y, L.n, xmin, ymin, side, L.levels, bits,
                                               L.wc, L.nchunks, kbuf[0], hist(0), zero, nzero_hist,
                                               ctr);
     note_launches(1);
@@ -399,10 +400,13 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     for (int p = 0; p < L.passes; ++p) {
         launch_scan_i32(hist(p), hsize, state(p), s, nullptr, false);
         const bool last = p == L.passes - 1;
+        // gamma and sigma are first read by the last pass (host mode: their
+        // copies overlap the key / sort work)
+        if (last && gs_ready) cudaStreamWaitEvent(s, gs_ready, 0);
         k_radix_scatter<<<blocks, kWPB * 32, shm, s>>>(
             kbuf[p & 1], p == 0 ? nullptr : vbuf[p & 1], kbuf[(p + 1) & 1], vbuf[(p + 1) & 1], L.n,
             p * bits, bits, L.wc, L.nchunks, hist(p), last ? nullptr : hist(p + 1), x, y, g, sigma,
-            (Src*)(ws + L.src));
+            (Src*)(ws + L.src), ctr);
         note_launches(1);
     }
     *keys_out = kbuf[L.passes & 1];

@@ -69,7 +69,7 @@ struct Layout {
     int digit_bits, passes, wc, nchunks;
     size_t nleaves;
     size_t key_a, key_b, val_a, val_b, hist, task_scratch, scan_state, src, near_uv, leaf_starts,
-        counts, mult, loc, leaf_loc, tasks, counters, total;
+        counts, mult, loc, leaf_loc, tasks, stage, counters, total;
     size_t scan_state_tiles, scan_state_bytes;  // per scan instance: 1 ticket + tiles
     size_t level_cell_off[VFMM_LEVELS_CAP + 2];  // cells before level k (k>=2) in mult/loc
     size_t count_off[VFMM_LEVELS_CAP + 2];       // cells before level k in counts
@@ -94,7 +94,8 @@ void note_launches(int k);
 // ---- kernels launchers (each enqueues on `s`) ----
 void launch_build(const Layout& L, const double* x, const double* y, const double* g,
                   const double* sigma, double xmin, double ymin, double side, char* ws,
-                  Counters* ctr, cudaStream_t s, int** keys_out, int** perm_out);
+                  Counters* ctr, cudaStream_t s, int** keys_out, int** perm_out,
+                  cudaEvent_t gs_ready = nullptr);
 void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream_t s,
                      const Counters* sym_skip, bool gauss);
 size_t scan_tiles(int64_t n);

@@ -191,6 +191,78 @@ def evaluate_arrays(
     return out, stats
 
 
+def _host_f64(a) -> tuple[object, int]:
+    """(keep-alive object, data pointer) of a contiguous float64 host array."""
+    if isinstance(a, torch.Tensor):
+        t = a.detach().to(torch.float64).contiguous()
+        if t.is_cuda:
+            raise ValueError("evaluate_host takes host arrays; use evaluate_arrays for device data")
+        return t, t.data_ptr()
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    return arr, arr.ctypes.data
+
+
+def evaluate_host(
+    x,
+    y,
+    gamma,
+    sigma,
+    config,
+    domain=None,
+    *,
+    device=None,
+    out: torch.Tensor | None = None,
+    overlap: bool = True,
+    stacklevel: int = 2,
+):
+    """Host-buffer fast path (``vfmm_evaluate_host``): numpy arrays or CPU (ideally
+    pinned) tensors in, a (2, N) float64 host tensor (u row, v row) out.
+
+    The library stages the copies itself and overlaps them with the tree
+    build (positions first; circulations and core sizes while the sort runs).
+    """
+    validate_config(config)
+    require_cuda()
+    lib = _lib.load()
+    dev = device_of(device)
+    keep = [_host_f64(a) for a in (x, y, gamma, sigma)]
+    n = int(np.asarray(keep[0][0]).size) if not isinstance(keep[0][0], torch.Tensor) else keep[0][0].numel()
+    if n == 0:
+        raise ValueError("need at least one particle")
+    if domain is None:
+        xs = keep[0][0].numpy() if isinstance(keep[0][0], torch.Tensor) else keep[0][0]
+        ys = keep[1][0].numpy() if isinstance(keep[1][0], torch.Tensor) else keep[1][0]
+        domain = enclosing_domain_of(xs, ys)
+    code = kernel_code(config.kernel)
+    ws = Workspace.get(n, config.levels, config.order, dev)
+    if out is None:
+        out = torch.empty((2, n), dtype=torch.float64, pin_memory=True)
+    st = _lib.VfmmStats()
+    flags = _lib.FLAG_STATS | (_lib.FLAG_OVERLAP if overlap else 0)
+    status = lib.vfmm_evaluate_host(
+        keep[0][1], keep[1][1], keep[2][1], keep[3][1] if code == _lib.KERNEL_GAUSSIAN else None, n,
+        float(domain.xmin), float(domain.ymin), float(domain.side), config.levels, config.order,
+        code, out[0].data_ptr(), out[1].data_ptr(), ws.ptr, ws.nbytes, flags, ctypes.byref(st),
+        stream_ptr(dev),
+    )
+    if status == _lib.VFMM_EDOMAIN:
+        xs = keep[0][0].numpy() if isinstance(keep[0][0], torch.Tensor) else keep[0][0]
+        ys = keep[1][0].numpy() if isinstance(keep[1][0], torch.Tensor) else keep[1][0]
+        bad = _bad_indices(xs, ys, domain)
+        raise OutOfDomainError(
+            f"{bad.size} particle(s) outside domain {domain}, first indices {bad[:5].tolist()}"
+        )
+    _lib.check(status, "vfmm_evaluate_host")
+    stats = _stats_from(st)
+    if code == _lib.KERNEL_GAUSSIAN and not st.sigma_guard_ok:
+        warnings.warn(
+            f"max core radius {st.max_sigma:g} exceeds leaf half-width/2 = {st.sigma_guard:g}; "
+            "the far field treats blobs as point vortices, so expect extra error",
+            stacklevel=stacklevel + 1,
+        )
+    return out, stats
+
+
 def evaluate(
     particles: Sequence,
     config,
@@ -209,8 +281,9 @@ def evaluate(
     x, y, gamma, sigma = to_arrays(particles)
     if domain is None:
         domain = enclosing_domain_of(x, y)
-    vel, stats = evaluate_arrays(x, y, gamma, sigma, config, domain, overlap=overlap, stacklevel=3)
-    return np.ascontiguousarray(vel.cpu().numpy().T), stats
+    vel, stats = evaluate_host(x, y, gamma, sigma, config, domain, overlap=overlap, stacklevel=3,
+                               out=torch.empty((2, len(x)), dtype=torch.float64))
+    return np.ascontiguousarray(vel.numpy().T), stats
 
 
 def evaluate_at(targets, particles: Sequence, config, domain=None) -> np.ndarray:

@@ -290,3 +290,18 @@ def test_config3_full_size_counts_and_sampled_direct():
     vel, st, _ = run(w.x, w.y, w.gamma, w.sigma, w.levels, w.order, True, W.DOMAIN)
     assert st.m2l_count == 9_351_840 and st.near_pair_count == 9_638_451_922
     assert _sampled_direct_check(w, vel, k=24) <= 1e-6
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_buffer_entry_point_matches_device_path(pinned):
+    """vfmm_evaluate_host (staged, overlapped copies) == vfmm_evaluate bit for bit."""
+    w = W.config1()
+    cfg = vf.FmmConfig(w.levels, w.order, G)
+    dom = vf.Domain(*W.DOMAIN)
+    ref, st = vf.evaluate_arrays(w.x, w.y, w.gamma, w.sigma, cfg, dom, overlap=True)
+    arrs = (w.x, w.y, w.gamma, w.sigma)
+    if pinned:
+        arrs = tuple(torch.from_numpy(a).pin_memory() for a in arrs)
+    got, st2 = vf.evaluate_host(*arrs, cfg, dom)
+    assert torch.equal(got, ref.cpu())
+    assert st2.m2l_count == st.m2l_count and st2.near_pair_count == st.near_pair_count
