@@ -192,69 +192,114 @@ __device__ __forceinline__ double pair_kernel(double dx, double dy, double& r2, 
     return fma(-inv, exp2_neg(clamp_neg60(r2 * q2), tab), inv);  // (1 - e) / r^2
 }
 
-// 32 rotation steps of one B chunk against one or two targets per lane
-// (TPL = 2: a0 = A[i0 + lane], a1 = A[i0 + 32 + lane]; each rotated source then
-// serves two symmetric pairs, halving the shuffles per pair).
-template <bool GAUSS, int TPL>
-__device__ __forceinline__ void rotate_sym(double a0x, double a0y, double a0g, double a1x,
-                                           double a1y, double a1g, double& bx, double& by,
-                                           double& bg, double& ub, double& vb, double q2,
-                                           const double* __restrict__ tab, int from, double& u0,
-                                           double& v0, double& u1, double& v1) {
+// One ring rotation: the B chunk (R sources) is replicated in every R-lane
+// segment of the warp ("ring"); lanes hold one or two A targets each, so a
+// rotation of R steps pairs every lane-resident target with every source of
+// the chunk exactly once.  Sources and their (u, v) accumulators move one lane
+// per step within the ring (shuffle with width R); the rings' partial source
+// sums are added in a fixed xor order at the end.  R < 32 serves the ragged
+// last chunk of a leaf (R = 8 / 16 instead of 32 mostly-ghost lanes).
+template <bool GAUSS, int TPL, int R, bool SYM>
+__device__ __forceinline__ void rotate_ring(double a0x, double a0y, double a0g, double a1x,
+                                            double a1y, double a1g, double bx, double by, double bg,
+                                            double& ub, double& vb, double q2,
+                                            const double* __restrict__ tab, double& u0, double& v0,
+                                            double& u1, double& v1) {
+    const int from = ((threadIdx.x & 31) + 1) & (R - 1);
 #pragma unroll 2
-    for (int st = 0; st < 32; ++st) {
+    for (int st = 0; st < R; ++st) {
         {
             const double dx = a0x - bx, dy = a0y - by;
             double r2;
             const double K = pair_kernel<GAUSS>(dx, dy, r2, q2, tab);
-            const double ca = bg * K, cb = a0g * K;
+            const double ca = bg * K;
             u0 = fma(-ca, dy, u0);
             v0 = fma(ca, dx, v0);
-            ub = fma(cb, dy, ub);
-            vb = fma(-cb, dx, vb);
+            if (SYM) {
+                const double cb = a0g * K;
+                ub = fma(cb, dy, ub);
+                vb = fma(-cb, dx, vb);
+            }
         }
         if (TPL == 2) {
             const double dx = a1x - bx, dy = a1y - by;
             double r2;
             const double K = pair_kernel<GAUSS>(dx, dy, r2, q2, tab);
-            const double ca = bg * K, cb = a1g * K;
+            const double ca = bg * K;
             u1 = fma(-ca, dy, u1);
             v1 = fma(ca, dx, v1);
-            ub = fma(cb, dy, ub);
-            vb = fma(-cb, dx, vb);
+            if (SYM) {
+                const double cb = a1g * K;
+                ub = fma(cb, dy, ub);
+                vb = fma(-cb, dx, vb);
+            }
         }
-        bx = __shfl_sync(0xffffffffu, bx, from);
-        by = __shfl_sync(0xffffffffu, by, from);
-        bg = __shfl_sync(0xffffffffu, bg, from);
-        ub = __shfl_sync(0xffffffffu, ub, from);
-        vb = __shfl_sync(0xffffffffu, vb, from);
+        bx = __shfl_sync(0xffffffffu, bx, from, R);
+        by = __shfl_sync(0xffffffffu, by, from, R);
+        bg = __shfl_sync(0xffffffffu, bg, from, R);
+        if (SYM) {
+            ub = __shfl_sync(0xffffffffu, ub, from, R);
+            vb = __shfl_sync(0xffffffffu, vb, from, R);
+        }
+    }
+    if (SYM) {
+#pragma unroll
+        for (int off = R; off < 32; off <<= 1) {
+            ub += __shfl_xor_sync(0xffffffffu, ub, off);
+            vb += __shfl_xor_sync(0xffffffffu, vb, off);
+        }
     }
 }
 
-template <bool GAUSS, int TPL>
-__device__ __forceinline__ void rotate_self(double a0x, double a0y, double a1x, double a1y,
-                                            double& bx, double& by, double& bg, double q2,
-                                            const double* __restrict__ tab, int from, double& u0,
-                                            double& v0, double& u1, double& v1) {
-#pragma unroll 2
-    for (int st = 0; st < 32; ++st) {
-        {
-            const double dx = a0x - bx, dy = a0y - by;
-            double r2;
-            const double c = bg * pair_kernel<GAUSS>(dx, dy, r2, q2, tab);
-            u0 = fma(-c, dy, u0);
-            v0 = fma(c, dx, v0);
+// One A chunk (cntA <= 64 targets, TPL = 1 or 2 per lane) against all of B in
+// chunks of 32 / 16 / 8 sources.  SYM: B accumulators are read from and
+// written back to `acc` (shared memory, per warp).
+template <bool GAUSS, bool SYM>
+__device__ __forceinline__ void chunk_vs_leaf(const Src* __restrict__ src, int loA, int cntA, int loB,
+                                              int nB, bool first, double2* acc, double q2,
+                                              const double* __restrict__ tab, double& u0,
+                                              double& v0, double& u1, double& v1) {
+    const int lane = threadIdx.x & 31;
+    double a0x, a0y, a0g, a1x, a1y, a1g;
+    load_lane(src, loA, min(32, cntA), lane, a0x, a0y, a0g);
+    load_lane(src, loA + (cntA > 32 ? 32 : 0), max(cntA - 32, 0), lane, a1x, a1y, a1g);
+    const bool two = cntA > 32;
+    // B chunk data is prefetched one chunk ahead (registers)
+    auto ring_of = [](int rem) { return rem > 24 ? 32 : (rem > 8 ? 16 : 8); };
+    double nbx, nby, nbg;
+    {
+        const int R = ring_of(nB);
+        load_lane(src, loB, min(R, nB), lane & (R - 1), nbx, nby, nbg);
+    }
+    for (int j0 = 0; j0 < nB;) {
+        const int rem = nB - j0;
+        const int R = ring_of(rem);
+        const int cnt = min(R, rem);
+        const int li = lane & (R - 1);
+        double bx = nbx, by = nby, bg = nbg;
+        if (rem > R) {
+            const int R2 = ring_of(rem - R);
+            load_lane(src, loB + j0 + R, min(R2, rem - R), lane & (R2 - 1), nbx, nby, nbg);
         }
-        if (TPL == 2) {
-            const double dx = a1x - bx, dy = a1y - by;
-            double r2;
-            const double c = bg * pair_kernel<GAUSS>(dx, dy, r2, q2, tab);
-            u1 = fma(-c, dy, u1);
-            v1 = fma(c, dx, v1);
+        double ub = 0.0, vb = 0.0;
+        if (SYM && !first && li < cnt) {
+            const double2 t = acc[j0 + li];
+            if (lane < R) {
+                ub = t.x;
+                vb = t.y;
+            }
         }
-        bx = __shfl_sync(0xffffffffu, bx, from);
-        by = __shfl_sync(0xffffffffu, by, from);
-        bg = __shfl_sync(0xffffffffu, bg, from);
+#define VFMM_RING(TPLV, RV)                                                                      \
+    rotate_ring<GAUSS, TPLV, RV, SYM>(a0x, a0y, a0g, a1x, a1y, a1g, bx, by, bg, ub, vb, q2, tab, \
+                                      u0, v0, u1, v1)
+        if (two) {
+            if (R == 32) VFMM_RING(2, 32); else if (R == 16) VFMM_RING(2, 16); else VFMM_RING(2, 8);
+        } else {
+            if (R == 32) VFMM_RING(1, 32); else if (R == 16) VFMM_RING(1, 16); else VFMM_RING(1, 8);
+        }
+#undef VFMM_RING
+        if (SYM && lane < cnt) acc[j0 + lane] = make_double2(ub, vb);
+        j0 += R;
     }
 }
 
@@ -274,7 +319,6 @@ __global__ void __launch_bounds__(kSymWarps * 32, MINB)
     __syncthreads();
     const int lane = threadIdx.x & 31;
     double2* acc = accB[threadIdx.x >> 5];
-    const int from = (lane + 1) & 31;
     const double q2 = GAUSS ? src[0].q2 : 0.0;  // uniform core size
     long long my_pairs = 0;
     // the next item index is fetched one item ahead to hide the atomic's latency
@@ -289,71 +333,38 @@ __global__ void __launch_bounds__(kSymWarps * 32, MINB)
         if (nA == 0) continue;
         const int cx = leaf & (m - 1), cy = leaf >> levels;
         const bool ownA = cy >= rows.lo && cy < rows.hi;
+        int dx_ = 0, dy_ = 0, loB = loA, nB = nA;
+        bool ownB = false;
         if (kind == 0) {
-            if (!ownA) continue;
-            // self block: a <- b for all b in A (r^2 == 0 pairs contribute exactly 0);
-            // two targets per lane when the chunk has more than 32
-            for (int i0 = 0; i0 < nA; i0 += 64) {
-                const int cntA = min(64, nA - i0);
-                double a0x, a0y, a0g, a1x, a1y, a1g;
-                load_lane(src, loA + i0, min(32, cntA), lane, a0x, a0y, a0g);
-                load_lane(src, loA + i0 + (cntA > 32 ? 32 : 0), max(cntA - 32, 0), lane, a1x, a1y, a1g);
-                double u0 = 0.0, v0 = 0.0, u1 = 0.0, v1 = 0.0;
-                const bool two = cntA > 32;
-                double nbx, nby, nbg;
-                load_lane(src, loA, min(32, nA), lane, nbx, nby, nbg);
-                for (int j0 = 0; j0 < nA; j0 += 32) {
-                    double bx = nbx, by = nby, bg = nbg;
-                    if (j0 + 32 < nA) load_lane(src, loA + j0 + 32, min(32, nA - j0 - 32), lane, nbx, nby, nbg);
-                    if (two)
-                        rotate_self<GAUSS, 2>(a0x, a0y, a1x, a1y, bx, by, bg, q2, tab, from, u0, v0, u1, v1);
-                    else
-                        rotate_self<GAUSS, 1>(a0x, a0y, a1x, a1y, bx, by, bg, q2, tab, from, u0, v0, u1, v1);
-                }
-                double2* out = near9 + (int64_t)slot_of(0, 0) * n + loA + i0;
-                if (lane < cntA) out[lane] = make_double2(u0 * kInv2Pi, v0 * kInv2Pi);
-                if (32 + lane < cntA) out[32 + lane] = make_double2(u1 * kInv2Pi, v1 * kInv2Pi);
-            }
-            my_pairs += (long long)nA * nA - nA;
-            continue;
+            if (!ownA) continue;  // self block: a <- b for all b in A (r^2 == 0 adds exactly 0)
+        } else {
+            dx_ = kind == 2 ? -1 : (kind == 3 ? 0 : 1);
+            dy_ = kind == 1 ? 0 : 1;
+            const int bxc = cx + dx_, byc = cy + dy_;
+            if (bxc < 0 || bxc >= m || byc >= m) continue;
+            ownB = byc >= rows.lo && byc < rows.hi;
+            if (!ownA && !ownB) continue;
+            const int lb = byc * m + bxc;
+            loB = ls[lb];
+            nB = ls[lb + 1] - loB;
+            if (nB == 0) continue;
         }
-        const int dx_ = kind == 2 ? -1 : (kind == 3 ? 0 : 1), dy_ = kind == 1 ? 0 : 1;
-        const int bxc = cx + dx_, byc = cy + dy_;
-        if (bxc < 0 || bxc >= m || byc >= m) continue;
-        const bool ownB = byc >= rows.lo && byc < rows.hi;
-        if (!ownA && !ownB) continue;
-        const int lb = byc * m + bxc;
-        const int loB = ls[lb], nB = ls[lb + 1] - loB;
-        if (nB == 0) continue;
         for (int i0 = 0; i0 < nA; i0 += 64) {
             const int cntA = min(64, nA - i0);
-            double a0x, a0y, a0g, a1x, a1y, a1g;
-            load_lane(src, loA + i0, min(32, cntA), lane, a0x, a0y, a0g);
-            load_lane(src, loA + i0 + (cntA > 32 ? 32 : 0), max(cntA - 32, 0), lane, a1x, a1y, a1g);
             double u0 = 0.0, v0 = 0.0, u1 = 0.0, v1 = 0.0;
-            const bool two = cntA > 32;
-            double nbx, nby, nbg;  // B chunk data, prefetched one chunk ahead
-            load_lane(src, loB, min(32, nB), lane, nbx, nby, nbg);
-            for (int j0 = 0; j0 < nB; j0 += 32) {
-                double bx = nbx, by = nby, bg = nbg;
-                if (j0 + 32 < nB) load_lane(src, loB + j0 + 32, min(32, nB - j0 - 32), lane, nbx, nby, nbg);
-                double ub = 0.0, vb = 0.0;
-                if (i0 > 0) {
-                    const double2 t = acc[j0 + lane];
-                    ub = t.x;
-                    vb = t.y;
-                }
-                if (two)
-                    rotate_sym<GAUSS, 2>(a0x, a0y, a0g, a1x, a1y, a1g, bx, by, bg, ub, vb, q2, tab,
-                                         from, u0, v0, u1, v1);
-                else
-                    rotate_sym<GAUSS, 1>(a0x, a0y, a0g, a1x, a1y, a1g, bx, by, bg, ub, vb, q2, tab,
-                                         from, u0, v0, u1, v1);
-                acc[j0 + lane] = make_double2(ub, vb);
-            }
+            if (kind == 0)
+                chunk_vs_leaf<GAUSS, false>(src, loA + i0, cntA, loB, nB, true, acc, q2, tab, u0,
+                                            v0, u1, v1);
+            else
+                chunk_vs_leaf<GAUSS, true>(src, loA + i0, cntA, loB, nB, i0 == 0, acc, q2, tab, u0,
+                                           v0, u1, v1);
             double2* out = near9 + (int64_t)slot_of(dx_, dy_) * n + loA + i0;
             if (lane < cntA) out[lane] = make_double2(u0 * kInv2Pi, v0 * kInv2Pi);
             if (32 + lane < cntA) out[32 + lane] = make_double2(u1 * kInv2Pi, v1 * kInv2Pi);
+        }
+        if (kind == 0) {
+            my_pairs += (long long)nA * nA - nA;
+            continue;
         }
         __syncwarp();
         for (int j = lane; j < nB; j += 32) {
