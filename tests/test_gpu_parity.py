@@ -305,3 +305,17 @@ def test_host_buffer_entry_point_matches_device_path(pinned):
     got, st2 = vf.evaluate_host(*arrs, cfg, dom)
     assert torch.equal(got, ref.cpu())
     assert st2.m2l_count == st.m2l_count and st2.near_pair_count == st.near_pair_count
+
+
+@pytest.mark.parametrize("levels,order,n", [(2, 60, 300), (4, 60, 2000), (10, 4, 10000), (11, 2, 3000)])
+def test_extreme_orders_and_depths_match_oracle(levels, order, n):
+    """ORDER_CAP (p = 60, depth-2 subtrees, long Hankel rows) and deep, mostly
+    empty trees (up to 4^11 leaves) against the oracle."""
+    rng = np.random.default_rng(levels * 100 + order)
+    x, y = rng.uniform(0, 1, n), rng.uniform(0, 1, n)
+    g = rng.uniform(-1, 1, n)
+    s = np.full(n, 1e-4)
+    vel, st, _ = run(x, y, g, s, levels, order, True, (0.0, 0.0, 1.0))
+    ref, ost = O.evaluate(x, y, g, s, levels, order, True, (0.0, 0.0, 1.0))
+    assert st.m2l_count == ost["m2l_count"] and st.near_pair_count == ost["near_pair_count"]
+    assert np.abs(vel - ref).max() <= REL_TOL * np.abs(ref).max()
