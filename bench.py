@@ -220,11 +220,13 @@ def run_ours(args):
     stream = torch.cuda.Stream(dev)
     flags = _lib.FLAG_OVERLAP
 
+    vel = torch.empty((n, 2), dtype=torch.float64, device=dev)  # (u, v) rows, the reference layout
+    flags |= _lib.FLAG_UV_PAIRS
+
     def call(s):
         rc = lib.vfmm_evaluate(xd.data_ptr(), yd.data_ptr(), gd.data_ptr(), sd.data_ptr(), n,
                                dom.xmin, dom.ymin, dom.side, w.levels, w.order, _lib.KERNEL_GAUSSIAN,
-                               out[0].data_ptr(), out[1].data_ptr(), ws.ptr, ws.nbytes, flags, None,
-                               s.cuda_stream)
+                               vel.data_ptr(), None, ws.ptr, ws.nbytes, flags, None, s.cuda_stream)
         assert rc == 0, rc
 
     with torch.cuda.stream(stream):
@@ -240,7 +242,8 @@ def run_ours(args):
         flush.zero_()
         graph.replay()
     torch.cuda.synchronize(dev)
-    ref_vel = out.clone()
+    ref_vel = vel.clone()
+    assert torch.equal(vel.t(), out), "pair layout differs from the (2, N) layout"
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -255,11 +258,11 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = statistics.fmean(step_ms)
-    assert torch.equal(out, ref_vel), "graph replays are not bitwise reproducible"
+    assert torch.equal(vel, ref_vel), "graph replays are not bitwise reproducible"
 
     # end to end through the public API from pinned host buffers
     hx, hy, hg, hs = (torch.from_numpy(a).pin_memory() for a in (w.x, w.y, w.gamma, w.sigma))
-    host_out = torch.empty((2, n), dtype=torch.float64).pin_memory()
+    host_out = torch.empty((n, 2), dtype=torch.float64).pin_memory()
     e2e_ms = []
     for i in range(args.e2e_steps + 2):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -52,6 +52,8 @@ extern "C" {
 #define VFMM_FLAG_FAR_ONLY 4u   /* build the tree and the local expansions only (no near field, no
                                    evaluation at the particles); used before vfmm_evaluate_at */
 #define VFMM_FLAG_PHASE_UP 8u   /* vfmm_evaluate_shard: build + P2M + M2M only */
+#define VFMM_FLAG_UV_PAIRS 32u  /* u is an interleaved (N, 2) array of (u, v) rows -- the reference's
+                                   return layout (engine.py:394-398); v is ignored */
 #define VFMM_FLAG_PHASE_DOWN 16u /* vfmm_evaluate_shard: M2L + L2L + P2P + L2P on the workspace of a
                                     previous PHASE_UP call (after the caller reduced the multipoles) */
 

@@ -28,6 +28,7 @@ FLAG_OVERLAP = 2
 FLAG_FAR_ONLY = 4
 FLAG_PHASE_UP = 8
 FLAG_PHASE_DOWN = 16
+FLAG_UV_PAIRS = 32
 
 ORDER_CAP = 60
 LEVELS_CAP = 13

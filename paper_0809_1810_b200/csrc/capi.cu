@@ -309,7 +309,9 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
     bool up = (flags & VFMM_FLAG_PHASE_UP) != 0, down = (flags & VFMM_FLAG_PHASE_DOWN) != 0;
     if (!up && !down) up = down = true;
     const bool overlap = (flags & VFMM_FLAG_OVERLAP) != 0 && !far_only && up && down;
-    if (!x || !y || !gamma || (down && !far_only && (!u || !v))) return VFMM_EINVAL;
+    const bool pairs = (flags & VFMM_FLAG_UV_PAIRS) != 0;
+    if (pairs) v = nullptr;  // u is an interleaved (N, 2) array
+    if (!x || !y || !gamma || (down && !far_only && (!u || (!pairs && !v)))) return VFMM_EINVAL;
     if (kernel == VFMM_KERNEL_GAUSSIAN && !sigma) return VFMM_EINVAL;
     if (timed && !stats) return VFMM_EINVAL;
     if (!args_ok(n, levels, order, side, kernel) || !std::isfinite(xmin) || !std::isfinite(ymin))
@@ -364,7 +366,7 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         gamma = dg;
         sigma = hio->hs ? dsg : nullptr;
         u = st + 4 * n;
-        v = st + 5 * n;
+        v = pairs ? nullptr : st + 5 * n;
     }
 
     cudaStream_t fs = cs;
@@ -416,8 +418,12 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
     }
     if (hio) {
         const size_t b = sizeof(double) * (size_t)n;
-        cudaMemcpyAsync(hio->hu, u, b, cudaMemcpyDeviceToHost, cs);
-        cudaMemcpyAsync(hio->hv, v, b, cudaMemcpyDeviceToHost, cs);
+        if (pairs) {
+            cudaMemcpyAsync(hio->hu, u, 2 * b, cudaMemcpyDeviceToHost, cs);
+        } else {
+            cudaMemcpyAsync(hio->hu, u, b, cudaMemcpyDeviceToHost, cs);
+            cudaMemcpyAsync(hio->hv, v, b, cudaMemcpyDeviceToHost, cs);
+        }
         cudaEventRecord(R->done, cs);
         cudaStreamWaitEvent(s, R->done, 0);
     }
@@ -470,7 +476,8 @@ int vfmm_evaluate_host(const double* x, const double* y, const double* gamma, co
                        int kernel, double* u, double* v, void* workspace, size_t workspace_bytes,
                        unsigned flags, vfmm_stats* stats, void* stream) {
     if (levels < 2 || levels > VFMM_LEVELS_CAP) return VFMM_EINVAL;
-    if (!x || !y || !gamma || !u || !v || (kernel == VFMM_KERNEL_GAUSSIAN && !sigma))
+    if (!x || !y || !gamma || !u || (!v && !(flags & VFMM_FLAG_UV_PAIRS)) ||
+        (kernel == VFMM_KERNEL_GAUSSIAN && !sigma))
         return VFMM_EINVAL;
     const HostIO io{x, y, gamma, kernel == VFMM_KERNEL_GAUSSIAN ? sigma : nullptr, u, v};
     // staging pointers are substituted inside; pass the host ones for the argument checks

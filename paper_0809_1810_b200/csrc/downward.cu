@@ -88,8 +88,13 @@ __global__ void __launch_bounds__(256)
         eval_local(loc + (int64_t)leaf * P, 1, P, (s.x - cx) * inv_r, (s.y - cy) * inv_r, sfact);
     // f_to_velocity: u = Im f / 2pi, v = Re f / 2pi; then far + near
     const int o = perm[i];
-    u[o] = f.y * kInv2Pi + nv.x;
-    v[o] = f.x * kInv2Pi + nv.y;
+    const double uo = f.y * kInv2Pi + nv.x, vo = f.x * kInv2Pi + nv.y;
+    if (v) {
+        u[o] = uo;
+        v[o] = vo;
+    } else {  // interleaved (N, 2) output: one 16-byte store per particle
+        reinterpret_cast<double2*>(u)[o] = make_double2(uo, vo);
+    }
 }
 
 // evaluate_at: one thread per target, far field from the target's leaf local

@@ -206,7 +206,9 @@ __device__ __forceinline__ void rotate_ring(double a0x, double a0y, double a0g, 
                                             const double* __restrict__ tab, double& u0, double& v0,
                                             double& u1, double& v1) {
     const int from = ((threadIdx.x & 31) + 1) & (R - 1);
-#pragma unroll 2
+    // full rings are the hot loop; partial rings (ragged leaf tails) are kept
+    // compact so the six ring instances do not crowd the instruction cache
+#pragma unroll(R == 32 ? 2 : 1)
     for (int st = 0; st < R; ++st) {
         {
             const double dx = a0x - bx, dy = a0y - by;

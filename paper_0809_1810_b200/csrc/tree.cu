@@ -88,6 +88,50 @@ __global__ void __launch_bounds__(kWPB * 32)
     }
 }
 
+// Source records in ORIGINAL order (coalesced), with the sigma statistics;
+// the last radix pass then moves whole 32-byte records instead of gathering
+// four arrays element by element.
+__global__ void __launch_bounds__(256)
+    k_pack_orig(const double* __restrict__ x, const double* __restrict__ y,
+                const double* __restrict__ g, const double* __restrict__ sigma, int64_t n,
+                Src* __restrict__ out, Counters* __restrict__ ctr) {
+    __shared__ unsigned long long wmax[8], wmin[8];
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long sbits = 0ull, smin = ~0ull;
+    if (i < n) {
+        const double s = sigma ? sigma[i] : 1.0;
+        if (sigma) sbits = smin = ordered_bits(s);
+        Src r;
+        r.x = x[i];
+        r.y = y[i];
+        r.g = g[i];
+        // -r^2 / (2 sigma^2) (engine.py:256) expressed in log2 units
+        r.q2 = -1.4426950408889634 / (2.0 * s * s);
+        out[i] = r;
+    }
+    if (!sigma) return;
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, sbits, o);
+        sbits = t > sbits ? t : sbits;
+        const unsigned long long u = __shfl_xor_sync(0xffffffffu, smin, o);
+        smin = u < smin ? u : smin;
+    }
+    const int warp = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        wmax[warp] = sbits;
+        wmin[warp] = smin;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            sbits = wmax[w] > sbits ? wmax[w] : sbits;
+            smin = wmin[w] < smin ? wmin[w] : smin;
+        }
+        if (sbits) atomicMax(&ctr->sigma_max_bits, sbits);
+        if (smin != ~0ull) atomicMax(&ctr->sigma_min_neg, ~smin);
+    }
+}
+
 // Stable scatter of one LSD pass: warp chunks are processed in index order,
 // lanes in index order within a round, equal digits ranked by lane
 // (match_any), so the relative order of equal keys is preserved.  Non-final
@@ -97,17 +141,13 @@ __global__ void __launch_bounds__(kWPB * 32)
     k_radix_scatter(const int* __restrict__ kin, const int* __restrict__ vin,
                     int* __restrict__ kout, int* __restrict__ vout, int64_t n, int shift, int bits,
                     int wc, int nchunks, const int* __restrict__ offs, int* __restrict__ hist_next,
-                    const double* __restrict__ x, const double* __restrict__ y,
-                    const double* __restrict__ g, const double* __restrict__ sigma,
-                    Src* __restrict__ src, Counters* __restrict__ ctr) {
+                    const Src* __restrict__ packed, Src* __restrict__ src) {
     extern __shared__ int sh[];
-    __shared__ unsigned long long wmax[kWPB], wmin[kWPB];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int B = 1 << bits;
     int* run = sh + warp * B;
     const int64_t chunk = (int64_t)blockIdx.x * kWPB + warp;
-    unsigned long long sbits = 0ull, smin = ~0ull;  // max / min core size (final pass)
-    if (chunk < nchunks) {
+    if (chunk >= nchunks) return;
     for (int d = lane; d < B; d += 32) run[d] = offs[(int64_t)d * nchunks + chunk];
     __syncwarp();
     const unsigned lt = (1u << lane) - 1u;
@@ -115,69 +155,34 @@ __global__ void __launch_bounds__(kWPB * 32)
     const int64_t end = beg + wc < n ? beg + wc : n;
     constexpr int R = 8;  // rounds whose loads are issued together
     for (int64_t base0 = beg; base0 < end; base0 += 32 * R) {
-    int kr[R], vr[R];
+        int kr[R], vr[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int64_t i = base0 + 32 * r + lane;
-        kr[r] = i < end ? kin[i] : 0;
-        vr[r] = i < end ? (vin ? vin[i] : (int)i) : 0;
-    }
+        for (int r = 0; r < R; ++r) {
+            const int64_t i = base0 + 32 * r + lane;
+            kr[r] = i < end ? kin[i] : 0;
+            vr[r] = i < end ? (vin ? vin[i] : (int)i) : 0;
+        }
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int64_t base = base0 + 32 * r;
-        const int64_t i = base + lane;
-        const bool valid = i < end;
-        const int k = kr[r], v = vr[r];
-        const int d = valid ? (k >> shift) & (B - 1) : B + lane;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        const int rank = __popc(peers & lt);
-        if (valid) {
-            const int pos = run[d] + rank;
-            kout[pos] = k;
-            vout[pos] = v;
-            if (hist_next) {
-                atomicAdd(&hist_next[(int64_t)((k >> (shift + bits)) & (B - 1)) * nchunks + pos / wc], 1);
-            } else {
-                const double s = sigma ? sigma[v] : 1.0;
-                if (sigma) {
-                    const unsigned long long b = ordered_bits(s);
-                    sbits = b > sbits ? b : sbits;
-                    smin = b < smin ? b : smin;
-                }
-                Src r;
-                r.x = x[v];
-                r.y = y[v];
-                r.g = g[v];
-                // -r^2 / (2 sigma^2) (engine.py:256) expressed in log2 units
-                r.q2 = -1.4426950408889634 / (2.0 * s * s);
-                src[pos] = r;
+        for (int r = 0; r < R; ++r) {
+            const int64_t i = base0 + 32 * r + lane;
+            const bool valid = i < end;
+            const int k = kr[r], v = vr[r];
+            const int d = valid ? (k >> shift) & (B - 1) : B + lane;
+            const unsigned peers = __match_any_sync(0xffffffffu, d);
+            const int rank = __popc(peers & lt);
+            if (valid) {
+                const int pos = run[d] + rank;
+                kout[pos] = k;
+                vout[pos] = v;
+                if (hist_next)
+                    atomicAdd(&hist_next[(int64_t)((k >> (shift + bits)) & (B - 1)) * nchunks + pos / wc], 1);
+                else
+                    src[pos] = packed[v];  // one 32-byte record
             }
+            __syncwarp();
+            if (valid && rank == __popc(peers) - 1) run[d] += __popc(peers);
+            __syncwarp();
         }
-        __syncwarp();
-        if (valid && rank == __popc(peers) - 1) run[d] += __popc(peers);
-        __syncwarp();
-    }
-    }
-    }
-    if (hist_next || !sigma) return;  // block-uniform: sigma statistics in the final pass only
-    for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long t = __shfl_xor_sync(0xffffffffu, sbits, o);
-        sbits = t > sbits ? t : sbits;
-        const unsigned long long u = __shfl_xor_sync(0xffffffffu, smin, o);
-        smin = u < smin ? u : smin;
-    }
-    if (lane == 0) {
-        wmax[warp] = sbits;
-        wmin[warp] = smin;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < kWPB; ++w) {
-            sbits = wmax[w] > sbits ? wmax[w] : sbits;
-            smin = wmin[w] < smin ? wmin[w] : smin;
-        }
-        if (sbits) atomicMax(&ctr->sigma_max_bits, sbits);
-        if (smin != ~0ull) atomicMax(&ctr->sigma_min_neg, ~smin);
     }
 }
 
@@ -389,6 +394,7 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     };
     const unsigned blocks = (unsigned)((L.nchunks + kWPB - 1) / kWPB);
     const size_t shm = (size_t)kWPB * B * sizeof(int);
+    Src* packed = (Src*)(ws + L.near_uv);  // free until the near field runs (9 x 16 B >= 32 B per particle)
     // scratch zeroed by the first kernel: histograms of passes 1.. and all scan states
     unsigned* zero = (unsigned*)(ws + L.hist) + hsize;
     const int64_t nzero_hist = hsize * (L.passes - 1);
@@ -400,13 +406,17 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     for (int p = 0; p < L.passes; ++p) {
         launch_scan_i32(hist(p), hsize, state(p), s, nullptr, false);
         const bool last = p == L.passes - 1;
-        // gamma and sigma are first read by the last pass (host mode: their
-        // copies overlap the key / sort work)
-        if (last && gs_ready) cudaStreamWaitEvent(s, gs_ready, 0);
+        // gamma and sigma are first read by the record pack before the last
+        // pass (host mode: their copies overlap the key / sort work)
+        if (last) {
+            if (gs_ready) cudaStreamWaitEvent(s, gs_ready, 0);
+            k_pack_orig<<<grid_for(L.n, 256), 256, 0, s>>>(x, y, g, sigma, L.n, packed, ctr);
+            note_launches(1);
+        }
         k_radix_scatter<<<blocks, kWPB * 32, shm, s>>>(
             kbuf[p & 1], p == 0 ? nullptr : vbuf[p & 1], kbuf[(p + 1) & 1], vbuf[(p + 1) & 1], L.n,
-            p * bits, bits, L.wc, L.nchunks, hist(p), last ? nullptr : hist(p + 1), x, y, g, sigma,
-            (Src*)(ws + L.src), ctr);
+            p * bits, bits, L.wc, L.nchunks, hist(p), last ? nullptr : hist(p + 1), packed,
+            (Src*)(ws + L.src));
         note_launches(1);
     }
     *keys_out = kbuf[L.passes & 1];

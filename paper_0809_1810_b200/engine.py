@@ -216,7 +216,8 @@ def evaluate_host(
     stacklevel: int = 2,
 ):
     """Host-buffer fast path (``vfmm_evaluate_host``): numpy arrays or CPU (ideally
-    pinned) tensors in, a (2, N) float64 host tensor (u row, v row) out.
+    pinned) tensors in, an (N, 2) float64 host tensor of (u, v) rows out (the
+    reference's return layout, engine.py:394-398).
 
     The library stages the copies itself and overlaps them with the tree
     build (positions first; circulations and core sizes while the sort runs).
@@ -236,14 +237,15 @@ def evaluate_host(
     code = kernel_code(config.kernel)
     ws = Workspace.get(n, config.levels, config.order, dev)
     if out is None:
-        out = torch.empty((2, n), dtype=torch.float64, pin_memory=True)
+        out = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
+    if tuple(out.shape) != (n, 2) or not out.is_contiguous() or out.is_cuda:
+        raise ValueError("out must be a contiguous host (N, 2) float64 tensor")
     st = _lib.VfmmStats()
-    flags = _lib.FLAG_STATS | (_lib.FLAG_OVERLAP if overlap else 0)
+    flags = _lib.FLAG_STATS | _lib.FLAG_UV_PAIRS | (_lib.FLAG_OVERLAP if overlap else 0)
     status = lib.vfmm_evaluate_host(
         keep[0][1], keep[1][1], keep[2][1], keep[3][1] if code == _lib.KERNEL_GAUSSIAN else None, n,
         float(domain.xmin), float(domain.ymin), float(domain.side), config.levels, config.order,
-        code, out[0].data_ptr(), out[1].data_ptr(), ws.ptr, ws.nbytes, flags, ctypes.byref(st),
-        stream_ptr(dev),
+        code, out.data_ptr(), None, ws.ptr, ws.nbytes, flags, ctypes.byref(st), stream_ptr(dev),
     )
     if status == _lib.VFMM_EDOMAIN:
         xs = keep[0][0].numpy() if isinstance(keep[0][0], torch.Tensor) else keep[0][0]
@@ -282,8 +284,8 @@ def evaluate(
     if domain is None:
         domain = enclosing_domain_of(x, y)
     vel, stats = evaluate_host(x, y, gamma, sigma, config, domain, overlap=overlap, stacklevel=3,
-                               out=torch.empty((2, len(x)), dtype=torch.float64))
-    return np.ascontiguousarray(vel.numpy().T), stats
+                               out=torch.empty((len(x), 2), dtype=torch.float64))
+    return vel.numpy(), stats
 
 
 def evaluate_at(targets, particles: Sequence, config, domain=None) -> np.ndarray:
