@@ -26,8 +26,20 @@ from .engine import FmmConfig, evaluate_arrays
 from .kernels import KernelKind, velocity_direct_arrays
 from .model import Domain
 
-HEADER = ["n", "levels", "p", "max_abs", "max_rel", "rms_abs", "rms_rel", "violations",
-          "t_fmm_ms", "t_direct_ms", "m2l_count", "near_pair_count", "sigma_guard_ok"]
+# the reference's sweep schema (harness.SWEEP_HEADER, harness.py:44-47)
+HEADER = ["n", "l", "p", "seed", "distribution", "kernel", "max_abs", "max_rel", "rms_rel",
+          "bound_violations", "sampled", "t_fmm_ms", "t_direct_ms", "m2l_count", "near_pair_count",
+          "generator_id"]
+
+
+def csv_row(n, levels, order, rep, violations, t_fmm_ms, t_direct_ms, st) -> list[str]:
+    """One sweep row in the reference's formatting (harness.CaseResult.csv_row, harness.py:186-208)."""
+    def g(v):
+        return "NA" if v != v else format(v, ".10g")
+
+    return [str(n), str(levels), str(order), "0", "lamb_oseen_lattice", "gaussian", g(rep.max_abs),
+            g(rep.max_rel), g(rep.rms_rel), str(violations), "0", format(t_fmm_ms, ".3f"),
+            format(t_direct_ms, ".3f"), str(st.m2l_count), str(st.near_pair_count), "lattice"]
 
 
 def run_case(m: int, levels: int, order: int, grid: int = 8, device=None, budgets: bool = True):
@@ -68,9 +80,7 @@ def main(argv=None):
                 continue
             rep, emap, st, t_dir = run_case(m, lv, p, args.grid)
             viol = len(errors.bound_check(rep)) if rep.bound_budget is not None else -1
-            wr.writerow([m * m, lv, p, rep.max_abs, rep.max_rel, rep.rms_abs, rep.rms_rel, viol,
-                         format(st.t_total * 1e3, ".3f"), format(t_dir, ".3f"), st.m2l_count,
-                         st.near_pair_count, int(st.sigma_guard_ok)])
+            wr.writerow(csv_row(m * m, lv, p, rep, viol, st.t_total * 1e3, t_dir, st))
             fh.flush()
             if args.maps:
                 errors.write_error_map_csv(emap, os.path.join(args.maps, f"map_n{m * m}_l{lv}_p{p}.csv"))
