@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--config", type=int, default=2, choices=[0, 1, 2, 3])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU sharded path even for one rank (path check)")
     return ap.parse_args()
 
 
@@ -191,7 +193,7 @@ def run_ours(args):
     from paper_0809_1810_b200.engine import Workspace
 
     rank, world, local = dist_env()
-    if world > 1:
+    if world > 1 or args.sharded:
         from paper_0809_1810_b200 import distributed
 
         return distributed.bench_main(args)

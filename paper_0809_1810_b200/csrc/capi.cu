@@ -308,7 +308,11 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
     const bool far_only = (flags & VFMM_FLAG_FAR_ONLY) != 0;
     bool up = (flags & VFMM_FLAG_PHASE_UP) != 0, down = (flags & VFMM_FLAG_PHASE_DOWN) != 0;
     if (!up && !down) up = down = true;
-    const bool overlap = (flags & VFMM_FLAG_OVERLAP) != 0 && !far_only && up && down;
+    // Overlap: the near field runs on a side stream concurrently with the
+    // far-field chain.  In a sharded run (separate phases) the near field is
+    // launched at the end of PHASE_UP -- it needs only the local tree -- so it
+    // also hides the caller's multipole all-reduce; PHASE_DOWN joins it.
+    const bool overlap = (flags & VFMM_FLAG_OVERLAP) != 0 && !far_only;
     const bool pairs = (flags & VFMM_FLAG_UV_PAIRS) != 0;
     if (pairs) v = nullptr;  // u is an interleaved (N, 2) array
     if (!x || !y || !gamma || (down && !far_only && (!u || (!pairs && !v)))) return VFMM_EINVAL;
@@ -387,6 +391,13 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
             cudaStreamWaitEvent(R->near, R->fork, 0);
             fs = R->far;
         }
+        if (overlap && !down) {  // sharded PHASE_UP: start the near field now
+            rec(7, R->near);
+            launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, rows, R->near);
+            rec(8, R->near);
+            cudaEventRecord(R->join_near, R->near);
+            fs = cs;  // the far chain stays on the caller's stream (the all-reduce follows it)
+        }
         // ---- upward ----
         launch_p2m(L, src, ls, xmin, ymin, side, mult + L.level_cell_off[levels] * L.P, T, rows, fs);
         launch_m2m(L, T, mult, fs);
@@ -400,13 +411,15 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         // ---- downward ----
         launch_l2l(L, T, loc, (double2*)(ws + L.leaf_loc), rows, fs);
         rec(4, fs);
-        if (overlap) {
+        if (overlap && up) {
             cudaEventRecord(R->join_far, fs);
             rec(7, R->near);
             launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, rows, R->near);
             rec(8, R->near);
             cudaEventRecord(R->join_near, R->near);
             cudaStreamWaitEvent(cs, R->join_far, 0);
+            cudaStreamWaitEvent(cs, R->join_near, 0);
+        } else if (overlap) {  // sharded PHASE_DOWN: join the near field started in PHASE_UP
             cudaStreamWaitEvent(cs, R->join_near, 0);
         }
         if (!far_only) {
@@ -493,8 +506,7 @@ int vfmm_evaluate_shard(const double* x, const double* y, const double* gamma, c
                         size_t workspace_bytes, unsigned flags, vfmm_stats* stats, void* stream) {
     if (levels < 2 || levels > VFMM_LEVELS_CAP) return VFMM_EINVAL;
     return evaluate_impl(x, y, gamma, sigma, n, xmin, ymin, side, levels, order, kernel, u, v,
-                         workspace, workspace_bytes, flags & ~VFMM_FLAG_OVERLAP,
-                         Rows{row_lo, row_hi}, stats, stream);
+                         workspace, workspace_bytes, flags, Rows{row_lo, row_hi}, stats, stream);
 }
 
 int vfmm_counts_region(int64_t n, int levels, int order, size_t* offset, size_t* bytes) {

@@ -50,7 +50,7 @@ class OracleShardBackend:
             np.concatenate([occ[k] for k in range(lv + 1)]).astype(np.int32))
         return self.mult_flat, self.occ_flat
 
-    def down(self, shard, config, domain):
+    def down(self, shard, config, domain, counters=True):
         lv, p = config.levels, config.order
         t = self.tree
         lo, hi = shard.rows
