@@ -83,6 +83,67 @@ __global__ void __launch_bounds__(kP2MWarps * 32)
     }
 }
 
+
+// Sub-warp P2M for P <= PMAX (the common orders): G lanes per leaf, each lane
+// sums Gamma w^k over a strided subset of the leaf's particles into PMAX
+// register accumulators, then one butterfly over the G lanes combines them.
+// No shared-memory transpose, so the kernel is bound by its (small) FP64
+// work and the source reads rather than by shared-memory wavefronts.
+template <int G, int PMAX>
+__global__ void __launch_bounds__(128)
+    k_p2m_grp(const Src* __restrict__ src, const int* __restrict__ ls, int levels, int P,
+              double xmin, double ymin, double side, const Tables* __restrict__ T, Rows rows,
+              double2* __restrict__ mult) {
+    const int sub = threadIdx.x & (G - 1);
+    const int m = 1 << levels;
+    const int64_t leaf = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const bool valid = leaf < (int64_t)m * m;  // whole groups are (in)valid together
+    if (!valid) return;
+    const int lo = ls[leaf], hi = ls[leaf + 1];
+    const int ix = (int)(leaf % m), iy = (int)(leaf / m);
+    double2* out = mult + coef_base(levels, ix, iy);
+    const int64_t cs = coef_stride(levels);
+    const bool live = lo < hi && iy >= rows.lo && iy < rows.hi;  // uniform per group
+    double ax[PMAX], ay[PMAX];
+#pragma unroll
+    for (int k = 0; k < PMAX; ++k) ax[k] = ay[k] = 0.0;
+    const double r = side / m;  // Tree.cell_side (quadtree.py:140-141)
+    const double cx = cell_center(xmin, ix, r), cy = cell_center(ymin, iy, r);
+    const double inv_r = 1.0 / r;
+    if (live) {
+        for (int j = lo + sub; j < hi; j += G) {
+            const Src s = src[j];
+            const double wx = (s.x - cx) * inv_r, wy = (s.y - cy) * inv_r;
+            double tx = s.g, ty = 0.0;
+#pragma unroll
+            for (int k = 0; k < PMAX; ++k) {
+                if (k < P) {
+                    ax[k] += tx;
+                    ay[k] += ty;
+                    const double nx = tx * wx - ty * wy;
+                    ty = tx * wy + ty * wx;
+                    tx = nx;
+                }
+            }
+        }
+    }
+    // the group's lanes are consecutive and G-aligned: xor butterflies stay inside it
+#pragma unroll
+    for (int k = 0; k < PMAX; ++k) {
+        if (k < P) {
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) {
+                ax[k] += __shfl_xor_sync(0xffffffffu, ax[k], o, G);
+                ay[k] += __shfl_xor_sync(0xffffffffu, ay[k], o, G);
+            }
+            if ((k & (G - 1)) == sub) {
+                const double sc = T->invfact[k] * inv_r;
+                out[k * cs] = make_double2(ax[k] * sc, ay[k] * sc);
+            }
+        }
+    }
+}
+
 }  // namespace
 
 int coef_chunk(int P) {
@@ -97,8 +158,25 @@ int coef_chunk(int P) {
 void launch_p2m(const Layout& L, const Src* src, const int* leaf_starts, double xmin, double ymin,
                 double side, double2* mult_leaf, const Tables* T, Rows rows, cudaStream_t s) {
     const int64_t nl = (int64_t)L.nleaves;
-    k_p2m<<<(unsigned)((nl + kP2MWarps - 1) / kP2MWarps), kP2MWarps * 32, 0, s>>>(
-        src, leaf_starts, L.levels, L.P, xmin, ymin, side, T, rows, mult_leaf);
+    // sub-warp groups while leaves are small enough for 8 lanes to sweep them
+    // (mean occupancy <= 256); the warp-per-leaf transpose kernel otherwise
+    const bool grp = L.P <= 32 && L.n <= 256 * nl;
+    if (grp) {
+        constexpr int G = 8;
+        const unsigned blocks = (unsigned)((nl * G + 127) / 128);
+        if (L.P <= 16)
+            k_p2m_grp<G, 16><<<blocks, 128, 0, s>>>(src, leaf_starts, L.levels, L.P, xmin, ymin,
+                                                    side, T, rows, mult_leaf);
+        else if (L.P <= 24)
+            k_p2m_grp<G, 24><<<blocks, 128, 0, s>>>(src, leaf_starts, L.levels, L.P, xmin, ymin,
+                                                    side, T, rows, mult_leaf);
+        else
+            k_p2m_grp<G, 32><<<blocks, 128, 0, s>>>(src, leaf_starts, L.levels, L.P, xmin, ymin,
+                                                    side, T, rows, mult_leaf);
+    } else {
+        k_p2m<<<(unsigned)((nl + kP2MWarps - 1) / kP2MWarps), kP2MWarps * 32, 0, s>>>(
+            src, leaf_starts, L.levels, L.P, xmin, ymin, side, T, rows, mult_leaf);
+    }
     note_launches(1);
 }
 
