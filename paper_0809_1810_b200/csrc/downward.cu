@@ -63,16 +63,17 @@ __global__ void __launch_bounds__(256)
     const double inv_r = 1.0 / r;
     double2 nv = make_double2(0.0, 0.0);
     if (sym_enabled && p2p_symmetric(ctr, gauss)) {
-        // symmetric kernel: one slot per existing non-empty neighbour leaf, in
-        // direction order; all nine loads are issued before any is consumed
+        // symmetric kernel: slot 0 = the leaf's own blocks (self + forward),
+        // slots 1..4 = reactions from the backward neighbours, in kind order
         double2 t[kNearSlots];
 #pragma unroll
         for (int k = 0; k < kNearSlots; ++k) t[k] = near_uv[(int64_t)k * n + i];
+        nv = t[0];
 #pragma unroll
-        for (int k = 0; k < kNearSlots; ++k) {
-            const int nx = ix + k % 3 - 1, ny = iy + k / 3 - 1;
-            const bool ok = nx >= 0 && nx < m && ny >= 0 && ny < m &&
-                            ls[ny * m + nx + 1] != ls[ny * m + nx];
+        for (int k = 1; k < kNearSlots; ++k) {
+            // the item of leaf (ix, iy) - d_k wrote slot k; d = (1,0), (-1,1), (0,1), (1,1)
+            const int ax = ix - (k == 2 ? -1 : (k == 3 ? 0 : 1)), ay = iy - (k == 1 ? 0 : 1);
+            const bool ok = ax >= 0 && ax < m && ay >= 0 && ls[ay * m + ax + 1] != ls[ay * m + ax];
             if (ok) {
                 nv.x += t[k].x;
                 nv.y += t[k].y;

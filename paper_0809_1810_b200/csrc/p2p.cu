@@ -12,6 +12,7 @@
 // streamed through shared memory in tiles shared by the warps of the block
 // that work on the same leaf, otherwise read as warp-uniform (broadcast)
 // loads through L1.  The 1/(2 pi) factor is applied once per target.
+#include <atomic>
 #include <cstdlib>
 
 #include "vfmm_internal.cuh"
@@ -165,14 +166,16 @@ __global__ void __launch_bounds__(kP2PWarps * 32, kP2PBlocksPerSM)
 // the 32 sources of a B chunk rotate through the lanes by shuffles together
 // with their accumulators, so after 32 steps every (a, b) pair has been seen
 // exactly once and each B accumulator is back in its home lane.  B-chunk
-// accumulators persist in shared memory across A chunks.  Contributions are
-// written once per (particle, neighbour direction) into nine slots that the
-// combine kernel adds in direction order: deterministic, no atomics.
+// accumulators persist in shared memory across A chunks.  A work item is a
+// whole leaf A (self + four forward blocks, in that order): A's own targets
+// accumulate across the five blocks (registers / shared memory) and are
+// written once into slot 0; the reaction on each forward neighbour B goes to
+// B's slot `kind` (1..4).  The combine adds slot 0 and the reaction slots in
+// kind order: deterministic, no atomics, 80 bytes of slots per particle.
 // Work per ordered pair: 12 FP64 instructions (21 in the generic kernel).
 constexpr int kSymWarps = 8;
-constexpr int kSymBlocksPerSM = 4;
-
-__device__ __forceinline__ int slot_of(int dx, int dy) { return (dy + 1) * 3 + (dx + 1); }
+constexpr int kSymExpBytes = (kExpTab * 8 + 15) / 16 * 16;
+constexpr int kSymSmem = kSymExpBytes + 2 * kSymWarps * kSymMaxLeaf * 16;  // 62 KB
 
 __device__ __forceinline__ void load_lane(const Src* __restrict__ src, int lo, int cnt, int lane,
                                           double& x, double& y, double& g) {
@@ -309,72 +312,91 @@ template <bool GAUSS, int MINB>
 __global__ void __launch_bounds__(kSymWarps * 32, MINB)
     k_p2p_sym(const Src* __restrict__ src, const int* __restrict__ ls, Counters* __restrict__ ctr,
               int levels, int64_t n, Rows rows, const Tables* __restrict__ T,
-              double2* __restrict__ near9, unsigned long long* __restrict__ pairs,
+              double2* __restrict__ near5, unsigned long long* __restrict__ pairs,
               int items_per_warp) {
     if (!p2p_symmetric(ctr, GAUSS)) return;  // the generic kernel handles it
     const int m = 1 << levels;
-    const int nitems = 5 << (2 * levels);
+    const int nitems = 1 << (2 * levels);  // one item per leaf
     if ((int64_t)blockIdx.x * kSymWarps * items_per_warp >= nitems) return;  // spare CTA
-    __shared__ double sexp[kExpTab];
-    __shared__ double2 accB[kSymWarps][kSymMaxLeaf];
+    // dynamic shared memory: exp table | per-warp B accumulators | per-warp A accumulators
+    extern __shared__ __align__(16) unsigned char sym_smem[];
+    double* sexp = reinterpret_cast<double*>(sym_smem);
+    double2* accB = reinterpret_cast<double2*>(sym_smem + kSymExpBytes);
+    double2* accA = accB + kSymWarps * kSymMaxLeaf;
     const double* tab = stage_exp_table(sexp, T->exp2tab);
     __syncthreads();
-    const int lane = threadIdx.x & 31;
-    double2* acc = accB[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double2* acc = accB + warp * kSymMaxLeaf;
+    double2* accAw = accA + warp * kSymMaxLeaf;
     const double q2 = GAUSS ? src[0].q2 : 0.0;  // uniform core size
     long long my_pairs = 0;
     // the next item index is fetched one item ahead to hide the atomic's latency
     int next = 0;
     if (lane == 0) next = atomicAdd(&ctr->task_cursor, 1);
     for (int it = 0; it < items_per_warp; ++it) {
-        const int item = __shfl_sync(0xffffffffu, next, 0);
-        if (item >= nitems) break;
+        const int leaf = __shfl_sync(0xffffffffu, next, 0);
+        if (leaf >= nitems) break;
         if (lane == 0 && it + 1 < items_per_warp) next = atomicAdd(&ctr->task_cursor, 1);
-        const int leaf = item / 5, kind = item % 5;
         const int loA = ls[leaf], nA = ls[leaf + 1] - loA;
         if (nA == 0) continue;
         const int cx = leaf & (m - 1), cy = leaf >> levels;
         const bool ownA = cy >= rows.lo && cy < rows.hi;
-        int dx_ = 0, dy_ = 0, loB = loA, nB = nA;
-        bool ownB = false;
-        if (kind == 0) {
-            if (!ownA) continue;  // self block: a <- b for all b in A (r^2 == 0 adds exactly 0)
-        } else {
-            dx_ = kind == 2 ? -1 : (kind == 3 ? 0 : 1);
-            dy_ = kind == 1 ? 0 : 1;
-            const int bxc = cx + dx_, byc = cy + dy_;
-            if (bxc < 0 || bxc >= m || byc >= m) continue;
-            ownB = byc >= rows.lo && byc < rows.hi;
-            if (!ownA && !ownB) continue;
-            const int lb = byc * m + bxc;
-            loB = ls[lb];
-            nB = ls[lb + 1] - loB;
-            if (nB == 0) continue;
+        bool startedA = false;  // A accumulators hold a partial sum (warp-uniform)
+        for (int kind = 0; kind < 5; ++kind) {
+            int dx_ = 0, dy_ = 0, loB = loA, nB = nA;
+            bool ownB = false;
+            if (kind == 0) {
+                if (!ownA) continue;  // self block: a <- b for all b in A (r^2 == 0 adds exactly 0)
+            } else {
+                dx_ = kind == 2 ? -1 : (kind == 3 ? 0 : 1);
+                dy_ = kind == 1 ? 0 : 1;
+                const int bxc = cx + dx_, byc = cy + dy_;
+                if (bxc < 0 || bxc >= m || byc >= m) continue;
+                ownB = byc >= rows.lo && byc < rows.hi;
+                if (!ownA && !ownB) continue;
+                const int lb = byc * m + bxc;
+                loB = ls[lb];
+                nB = ls[lb + 1] - loB;
+                if (nB == 0) continue;
+            }
+            for (int i0 = 0; i0 < nA; i0 += 64) {
+                const int cntA = min(64, nA - i0);
+                double u0 = 0.0, v0 = 0.0, u1 = 0.0, v1 = 0.0;
+                if (startedA) {
+                    const double2 a0 = accAw[i0 + lane], a1 = accAw[i0 + 32 + lane];
+                    u0 = a0.x; v0 = a0.y; u1 = a1.x; v1 = a1.y;
+                }
+                if (kind == 0)
+                    chunk_vs_leaf<GAUSS, false>(src, loA + i0, cntA, loB, nB, true, acc, q2, tab,
+                                                u0, v0, u1, v1);
+                else
+                    chunk_vs_leaf<GAUSS, true>(src, loA + i0, cntA, loB, nB, i0 == 0, acc, q2,
+                                               tab, u0, v0, u1, v1);
+                accAw[i0 + lane] = make_double2(u0, v0);
+                accAw[i0 + 32 + lane] = make_double2(u1, v1);
+            }
+            startedA = true;
+            if (kind == 0) {
+                my_pairs += (long long)nA * nA - nA;
+                continue;
+            }
+            // reaction on B: slot `kind` (B's backward neighbour in direction kind)
+            __syncwarp();
+            for (int j = lane; j < nB; j += 32) {
+                const double2 t = acc[j];
+                near5[(int64_t)kind * n + loB + j] = make_double2(t.x * kInv2Pi, t.y * kInv2Pi);
+            }
+            __syncwarp();
+            my_pairs += (long long)nA * nB * ((ownA ? 1 : 0) + (ownB ? 1 : 0));
         }
-        for (int i0 = 0; i0 < nA; i0 += 64) {
-            const int cntA = min(64, nA - i0);
-            double u0 = 0.0, v0 = 0.0, u1 = 0.0, v1 = 0.0;
-            if (kind == 0)
-                chunk_vs_leaf<GAUSS, false>(src, loA + i0, cntA, loB, nB, true, acc, q2, tab, u0,
-                                            v0, u1, v1);
-            else
-                chunk_vs_leaf<GAUSS, true>(src, loA + i0, cntA, loB, nB, i0 == 0, acc, q2, tab, u0,
-                                           v0, u1, v1);
-            double2* out = near9 + (int64_t)slot_of(dx_, dy_) * n + loA + i0;
-            if (lane < cntA) out[lane] = make_double2(u0 * kInv2Pi, v0 * kInv2Pi);
-            if (32 + lane < cntA) out[32 + lane] = make_double2(u1 * kInv2Pi, v1 * kInv2Pi);
+        // A's own targets: self + forward blocks, summed in kind order -> slot 0
+        if (startedA) {
+            __syncwarp();
+            for (int j = lane; j < nA; j += 32) {
+                const double2 t = accAw[j];
+                near5[loA + j] = make_double2(t.x * kInv2Pi, t.y * kInv2Pi);
+            }
         }
-        if (kind == 0) {
-            my_pairs += (long long)nA * nA - nA;
-            continue;
-        }
-        __syncwarp();
-        for (int j = lane; j < nB; j += 32) {
-            const double2 t = acc[j];
-            near9[(int64_t)slot_of(-dx_, -dy_) * n + loB + j] = make_double2(t.x * kInv2Pi, t.y * kInv2Pi);
-        }
-        __syncwarp();
-        my_pairs += (long long)nA * nB * ((ownA ? 1 : 0) + (ownB ? 1 : 0));
     }
     if (lane == 0 && my_pairs) atomicAdd(pairs, (unsigned long long)my_pairs);
 }
@@ -497,19 +519,28 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
         KS = e ? atoi(e) : 2;
         if (KS < 1) KS = 2;
     }
-    const int64_t sym_items = 5ll << (2 * L.levels);
+    const int64_t sym_items = 1ll << (2 * L.levels);  // one item per leaf
     const unsigned sblocks = (unsigned)((sym_items + kSymWarps * KS - 1) / (kSymWarps * KS));
     const int ks = KS;
     static int minb = 0;
     if (!minb) {
         const char* e = getenv("VFMM_P2P_SYM_MINB");
-        minb = (e && e[0] == '4') ? 4 : 3;
+        minb = (e && e[0] == '2') ? 2 : 3;
     }
     auto* sfn = minb == 3 ? (g ? k_p2p_sym<true, 3> : k_p2p_sym<false, 3>)
-                          : (g ? k_p2p_sym<true, 4> : k_p2p_sym<false, 4>);
+                          : (g ? k_p2p_sym<true, 2> : k_p2p_sym<false, 2>);
+    static std::atomic<unsigned long long> attr_set{0};  // per device ordinal
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !(attr_set.load() >> dev & 1ull)) {
+        for (auto* f : {k_p2p_sym<true, 3>, k_p2p_sym<false, 3>, k_p2p_sym<true, 2>,
+                        k_p2p_sym<false, 2>})
+            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
+        attr_set.fetch_or(1ull << dev);
+    }
     if (!sym_disabled()) {
-        sfn<<<sblocks, kSymWarps * 32, 0, s>>>(src, leaf_starts, ctr, L.levels, L.n, rows, T, near_uv,
-                                               &ctr->near_pairs, ks);
+        sfn<<<sblocks, kSymWarps * 32, kSymSmem, s>>>(src, leaf_starts, ctr, L.levels, L.n, rows, T,
+                                                      near_uv, &ctr->near_pairs, ks);
         note_launches(1);
     }
 }

@@ -27,7 +27,7 @@ constexpr int kOffsets = 49;               // 7x7 offset grid (dy+3)*7 + (dx+3)
 constexpr int kExpSteps = 64;              // exp table resolution: 2^(n/64)
 constexpr int kExpTabN = 60 * kExpSteps + 1;  // exp table entries, n = -3840..0
 constexpr int kNearRows = 3;               // generic P2P: one partial sum per neighbourhood row
-constexpr int kNearSlots = 9;              // symmetric P2P: one per neighbour direction
+constexpr int kNearSlots = 5;              // symmetric P2P: own blocks + 4 reactions
 constexpr int kSymMaxLeaf = 128;           // symmetric P2P needs leaves of <= 128 particles
 
 // Packed per-particle source record in leaf-sorted order: x, y, gamma and

@@ -137,18 +137,18 @@ def _near_from_slots(ws, c, n):
     if not _symmetric_mode(c, n):
         rows = ws.view("near_uv", torch.float64, 6 * n).cpu().numpy().reshape(3, n, 2)
         return (rows[0] + rows[1]) + rows[2]
-    slots = ws.view("near_uv", torch.float64, 18 * n).cpu().numpy().reshape(9, n, 2)
+    slots = ws.view("near_uv", torch.float64, 10 * n).cpu().numpy().reshape(5, n, 2)
     keys = ws.view("leaf_key", torch.int32, n).cpu().numpy()
     ls = ws.view("leaf_starts", torch.int32, 4**lv + 1).cpu().numpy()
     occ = np.diff(ls) > 0
     iy, ix = keys // m, keys % m
-    near = np.zeros((n, 2))
-    for dy in (-1, 0, 1):
-        for dx in (-1, 0, 1):
-            nx, ny = ix + dx, iy + dy
-            ok = (nx >= 0) & (nx < m) & (ny >= 0) & (ny < m)
-            ok[ok] &= occ[(ny * m + nx)[ok]]
-            near[ok] += slots[(dy + 1) * 3 + dx + 1][ok]
+    # slot 0: the leaf's own blocks; slot k: reaction from the leaf at offset -d_k
+    near = slots[0].copy()
+    for k, (dx, dy) in enumerate([(1, 0), (-1, 1), (0, 1), (1, 1)], start=1):
+        ax, ay = ix - dx, iy - dy
+        ok = (ax >= 0) & (ax < m) & (ay >= 0) & (ay < m)
+        ok[ok] &= occ[(ay * m + ax)[ok]]
+        near[ok] += slots[k][ok]
     return near
 
 
