@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvfmm.so")
+# VFMM_LIB: alternative build of the same library (kernel tuning variants)
+LIB_PATH = os.environ.get("VFMM_LIB") or os.path.join(_HERE, "libvfmm.so")
 
 VFMM_OK = 0
 VFMM_EINVAL = 1

@@ -173,6 +173,14 @@ __global__ void __launch_bounds__(kP2PWarps * 32, kP2PBlocksPerSM)
 // B's slot `kind` (1..4).  The combine adds slot 0 and the reaction slots in
 // kind order: deterministic, no atomics, 80 bytes of slots per particle.
 // Work per ordered pair: 12 FP64 instructions (21 in the generic kernel).
+#ifndef VFMM_RING_UNROLL
+#define VFMM_RING_UNROLL 1
+#endif
+constexpr int kRingUnroll = VFMM_RING_UNROLL;
+#ifndef VFMM_REP_RING
+#define VFMM_REP_RING 1
+#endif
+constexpr bool kRepRing = VFMM_REP_RING;  // replicated-target ring for 33..64-particle leaves  // steps of a full ring per loop iteration
 constexpr int kSymWarps = 8;
 constexpr int kSymExpBytes = (kExpTab * 8 + 15) / 16 * 16;
 constexpr int kSymSmem = kSymExpBytes + 2 * kSymWarps * kSymMaxLeaf * 16;  // 62 KB
@@ -211,7 +219,7 @@ __device__ __forceinline__ void rotate_ring(double a0x, double a0y, double a0g, 
     const int from = ((threadIdx.x & 31) + 1) & (R - 1);
     // full rings are the hot loop; partial rings (ragged leaf tails) are kept
     // compact so the six ring instances do not crowd the instruction cache
-#pragma unroll(R == 32 ? 2 : 1)
+#pragma unroll(R == 32 ? kRingUnroll : 1)
     for (int st = 0; st < R; ++st) {
         {
             const double dx = a0x - bx, dy = a0y - by;
@@ -525,7 +533,7 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
     static int minb = 0;
     if (!minb) {
         const char* e = getenv("VFMM_P2P_SYM_MINB");
-        minb = (e && e[0] == '2') ? 2 : 3;
+        minb = (e && e[0] == '3') ? 3 : 2;
     }
     auto* sfn = minb == 3 ? (g ? k_p2p_sym<true, 3> : k_p2p_sym<false, 3>)
                           : (g ? k_p2p_sym<true, 2> : k_p2p_sym<false, 2>);
