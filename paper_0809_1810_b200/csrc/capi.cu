@@ -176,7 +176,9 @@ const Tables* device_tables() {
 }
 
 bool make_layout(int64_t n, int levels, int order, Layout* L) {
-    if (n < 1 || levels < 2 || levels > VFMM_LEVELS_CAP || order < 0 || order > VFMM_ORDER_CAP)
+    // n < 2^30: 32-bit indices, 30-bit look-back counts in the LSD sort
+    if (n < 1 || n >= (1ll << 30) || levels < 2 || levels > VFMM_LEVELS_CAP || order < 0 ||
+        order > VFMM_ORDER_CAP)
         return false;
     std::memset(L, 0, sizeof(Layout));
     L->n = n;
@@ -187,7 +189,7 @@ bool make_layout(int64_t n, int levels, int order, Layout* L) {
     const int bits = 2 * levels;
     L->passes = (bits + 7) / 8;
     L->digit_bits = (bits + L->passes - 1) / L->passes;
-    const int64_t wc = 512;  // elements per radix warp chunk (16 rounds of 32)
+    const int64_t wc = 2048;  // keys per LSD tile (k_onesweep)
     L->wc = (int)wc;
     L->nchunks = (int)((n + wc - 1) / wc);
     const size_t B = (size_t)1 << L->digit_bits;
@@ -204,11 +206,11 @@ bool make_layout(int64_t n, int levels, int order, Layout* L) {
     }
     L->count_off[levels + 1] = cc;
     L->max_tasks = (size_t)((n + 31) / 32) + ((size_t)n < L->nleaves ? (size_t)n : L->nleaves);
-    const size_t hist_elems = B * (size_t)L->nchunks;
-    const size_t t1 = scan_tiles((int64_t)hist_elems), t2 = scan_tiles((int64_t)L->nleaves);
-    L->scan_state_tiles = t1 > t2 ? t1 : t2;
-    // one look-back state per radix pass + one for the task scan
-    L->scan_state_bytes = sizeof(unsigned long long) * (L->scan_state_tiles + 1) * (L->passes + 1);
+    // LSD scratch: global digit histograms, tile tickets, per-pass look-back words
+    L->hist_bytes = sizeof(int) * (L->passes * B + 8 + (size_t)L->passes * L->nchunks * B);
+    L->scan_state_tiles = scan_tiles((int64_t)L->nleaves + 1);
+    // one look-back state per radix pass + the task scan + the leaf-count scan
+    L->scan_state_bytes = sizeof(unsigned long long) * (L->scan_state_tiles + 1) * (L->passes + 2);
 
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -221,7 +223,7 @@ bool make_layout(int64_t n, int levels, int order, Layout* L) {
     L->key_b = take(sizeof(int) * n);
     L->val_a = take(sizeof(int) * n);
     L->val_b = take(sizeof(int) * n);
-    L->hist = take(sizeof(int) * hist_elems * L->passes);
+    L->hist = take(L->hist_bytes);
     L->task_scratch = take(sizeof(int) * L->nleaves);
     L->scan_state = take(L->scan_state_bytes);
     L->src = take(sizeof(Src) * n);

@@ -2,17 +2,33 @@
 //
 // Replaces quadtree.build_tree / grid_indices / Tree.__init__
 // (quadtree.py:39-46, 116-134, 182-201) and the permutation in
-// engine.evaluate (engine.py:355-358).  Kernel sequence (config 2: 9 launches):
-//   k_keys_hist     floor-rule binning with max-edge clamp + domain check + max
-//                   sigma + digit-0 histogram per warp chunk; zeroes scratch
-//   k_scan          single-pass exclusive scan (decoupled look-back)
-//   k_radix_scatter stable LSD scatter; also histograms the next digit per
-//                   output chunk; the last pass gathers x, y, gamma, sigma
-//                   into the sorted Src records (np.argsort(kind="stable"))
+// engine.evaluate (engine.py:355-358): a stable sort of the particles by
+// leaf key (np.argsort(kind="stable")).
+//
+// Counting path (every leaf <= kFastLeafMax particles; config 2: 4 kernels):
+//   k_bin_count     floor-rule binning with max-edge clamp + domain check;
+//                   per-leaf counts (warp-aggregated atomics)
+//   k_scan          counts -> leaf_starts (exclusive, in place)
+//   k_bin_scatter   particle index -> a slot of its leaf (atomic cursor per
+//                   leaf: the order inside a leaf is not yet the stable one);
+//                   flags the LSD path if a leaf is too large
+//   k_leaf_pack     warp per leaf: bitonic sort of the leaf's indices (which
+//                   restores the stable order exactly), then perm, sorted
+//                   keys and the packed Src records
+// LSD radix path (a leaf above kFastLeafMax, decided on the device; the
+// kernels below return at once otherwise):
+//   k_keys_ghist    keys + global digit histograms of every pass
+//   k_onesweep      one stable LSD pass per launch over 4096-key tiles:
+//                   warp match_any ranking, per-digit decoupled look-back,
+//                   coalesced digit-run writes; the last pass moves the
+//                   packed Src records (k_pack_orig)
 //   k_leaf_starts   leaf_starts[4^l + 1] (== concatenate([0], cumsum(bincount)))
+// Then, for both:
 //   k_counts_tasks  per-level occupancy pyramid (Tree.counts) + P2P task counts
-//   k_scan, k_tasks_fill   near-field warp task list
+//   k_scan, k_tasks_fill   near-field warp task list (generic P2P only)
 #include <climits>
+#include <algorithm>
+#include <cstdlib>
 
 #include "vfmm_internal.cuh"
 
@@ -20,71 +36,233 @@ namespace vfmm {
 
 namespace {
 
-constexpr int kWPB = 8;  // warps per block in the radix kernels
 
 __device__ __forceinline__ unsigned long long ordered_bits(double d) {
     unsigned long long b = (unsigned long long)__double_as_longlong(d);
     return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
 }
 
-// Warp chunk c = elements [c*wc, (c+1)*wc).  Also zeroes the scratch words
-// (later histograms, scan look-back state) with a grid-stride loop.
-__global__ void __launch_bounds__(kWPB * 32)
-    k_keys_hist(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
-                double xmin, double ymin, double side,
-                int levels, int bits, int wc, int nchunks, int* __restrict__ key,
-                int* __restrict__ hist0, unsigned* __restrict__ zero, int64_t nzero,
-                Counters* __restrict__ ctr) {
-    extern __shared__ int sh[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int64_t z = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; z < nzero;
-         z += (int64_t)gridDim.x * blockDim.x)
-        zero[z] = 0u;
-    const int B = 1 << bits;
-    int* h = sh + warp * B;
-    for (int d = lane; d < B; d += 32) h[d] = 0;
-    __syncwarp();
+constexpr int kFastLeafMax = 128;  // leaves the counting path sorts with one warp
+// Counters::sort_fallback: 0 counting path, else the LSD radix path because
+// the input looked spatially incoherent (probe) or a leaf is too large.
+constexpr int kSortLsdProbe = 1, kSortLsdBigLeaf = 2;
+
+
+// quadtree.py:44-45: min(int((v - lo) / side * m), m - 1).  The division is
+// replaced by a multiply by 1/side unless the scaled coordinate lies within
+// 1e-9 of a cell edge (the two differ by a few ulps, i.e. < 1e-11 at
+// m <= 8192), where the exact rule decides.
+__device__ __forceinline__ int cell_of(double v, double lo, double side, double inv_side, int m) {
+    const double d = v - lo;
+    const double t = d * inv_side * (double)m;
+    int i = (int)t;
+    const double fr = t - (double)i;
+    if (!(fr > 1e-9 && fr < 1.0 - 1e-9)) i = (int)(d / side * (double)m);
+    return i < m - 1 ? i : m - 1;
+}
+
+// Path choice from a sample of the input order: 64 runs of 32 consecutive
+// particles; many distinct leaves per run (a random order) make the per-leaf
+// atomics and gathers of the counting path scattered, so the LSD sort (whose
+// passes write digit runs) is used instead.
+__global__ void __launch_bounds__(256)
+    k_sort_probe(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                 double xmin, double ymin, double side, int levels, bool force_lsd,
+                 Counters* __restrict__ ctr) {
+    __shared__ int distinct;
+    if (threadIdx.x == 0) distinct = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int m = 1 << levels;
+    const double inv = 1.0 / side;
+    double xs[8], ys[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {  // all loads in flight together
+        const int64_t i = (int64_t)(((double)(warp * 8 + r) / 64.0) * (double)n) + lane;
+        xs[r] = i < n ? x[i] : NAN;
+        ys[r] = i < n ? y[i] : NAN;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {  // 64 runs of 32 spread over [0, n)
+        int k = -1;
+        if (!isnan(xs[r]) && !isnan(ys[r])) {
+            const double xi = fmin(fmax(xs[r], xmin), xmin + side);
+            const double yi = fmin(fmax(ys[r], ymin), ymin + side);
+            k = cell_of(yi, ymin, side, inv, m) * m + cell_of(xi, xmin, side, inv, m);
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, k);
+        if (k >= 0 && lane == __ffs(peers) - 1) atomicAdd(&distinct, 1);
+    }
+    __syncthreads();
+    // more than 8 distinct leaves per 32 consecutive particles on average
+    if (threadIdx.x == 0 && (force_lsd || distinct > 64 * 8)) ctr->sort_fallback = kSortLsdProbe;
+}
+
+// Keys, domain check and per-leaf counts (cnt zeroed; leaf_starts storage).
+__global__ void __launch_bounds__(256)
+    k_bin_count(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                double xmin, double ymin, double side, int levels, int* __restrict__ key,
+                int* __restrict__ cnt, Counters* __restrict__ ctr) {
+    if (ctr->sort_fallback == kSortLsdProbe) return;
+    const int lane = threadIdx.x & 31;
+    const int m = 1 << levels;
+    const double inv = 1.0 / side;
     const double xmax = xmin + side, ymax = ymin + side;  // Domain.xmax (model.py:51-57)
-    const int64_t chunk = (int64_t)blockIdx.x * kWPB + warp;
-    if (chunk < nchunks) {
-        const int64_t beg = chunk * wc;
-        const int64_t end = beg + wc < n ? beg + wc : n;
-        constexpr int R = 8;  // rounds whose loads are issued together
-        for (int64_t b0 = beg; b0 < end; b0 += 32 * R) {
-            double xr[R], yr[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int64_t i = b0 + 32 * r + lane;
-                xr[r] = i < end ? x[i] : 0.0;
-                yr[r] = i < end ? y[i] : 0.0;
+    // grid-stride over whole warps (a capped grid: cheap to skip in LSD mode)
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        int k = -1;
+        if (i < n) {
+            const double xi = x[i], yi = y[i];
+            int ix = 0, iy = 0;
+            if ((xi >= xmin) && (xi <= xmax) && (yi >= ymin) && (yi <= ymax)) {
+                ix = cell_of(xi, xmin, side, inv, m);
+                iy = cell_of(yi, ymin, side, inv, m);
+            } else {
+                atomicAdd(&ctr->bad_count, 1);
+                atomicMax(&ctr->first_bad_neg, INT_MAX - (int)i);
             }
+            k = iy * m + ix;
+            key[i] = k;
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, k);
+        if (k >= 0 && lane == __ffs(peers) - 1) atomicAdd(&cnt[k], __popc(peers));
+    }
+}
+
+// Index i -> a slot of its leaf: one atomic per (warp, leaf) group, lanes
+// ranked in index order inside the group.
+__global__ void __launch_bounds__(256)
+    k_bin_scatter(const int* __restrict__ key, int64_t n, const int* __restrict__ ls,
+                  int* __restrict__ fill, int* __restrict__ slot, Counters* __restrict__ ctr) {
+    if (ctr->sort_fallback == kSortLsdProbe) return;
+    const int lane = threadIdx.x & 31;
+    bool big = false;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        const int k = i < n ? key[i] : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, k);
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (k >= 0 && lane == leader) base = atomicAdd(&fill[k], __popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (k >= 0) {
+            const int lo = ls[k];
+            slot[lo + base + __popc(peers & ((1u << lane) - 1u))] = (int)i;
+            big |= ls[k + 1] - lo > kFastLeafMax;
+        }
+    }
+    if (__any_sync(0xffffffffu, big) && lane == 0) atomicMax(&ctr->sort_fallback, kSortLsdBigLeaf);
+}
+
+// Ascending bitonic sort of 32 E values held as e[k] = element k * 32 + lane.
+template <int E>
+__device__ __forceinline__ void warp_bitonic(int (&e)[E]) {
+    const int lane = threadIdx.x & 31;
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int64_t i = b0 + 32 * r + lane;
-                if (i >= end) continue;
-                const double xi = xr[r], yi = yr[r];
-                const bool inside = (xi >= xmin) && (xi <= xmax) && (yi >= ymin) && (yi <= ymax);
-                int ix = 0, iy = 0;
-                if (inside) {
-                    // quadtree.py:44-45: min(int((x - xmin) / side * m), m - 1)
-                    const double tx = (xi - xmin) / side * (double)m;
-                    const double ty = (yi - ymin) / side * (double)m;
-                    ix = (int)tx;
-                    iy = (int)ty;
-                    ix = ix < m - 1 ? ix : m - 1;
-                    iy = iy < m - 1 ? iy : m - 1;
-                } else {
-                    atomicAdd(&ctr->bad_count, 1);
-                    atomicMax(&ctr->first_bad_neg, INT_MAX - (int)i);
+    for (int size = 2; size <= 32 * E; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride >= 32) {  // partner in the same lane
+                const int ks = stride >> 5;
+#pragma unroll
+                for (int k = 0; k < E; ++k) {
+                    if (k & ks) continue;
+                    const bool up = (((k * 32 + lane) & size) == 0);
+                    const int a = e[k], b = e[k ^ ks];
+                    e[k] = up ? min(a, b) : max(a, b);
+                    e[k ^ ks] = up ? max(a, b) : min(a, b);
                 }
-                const int k = iy * m + ix;
-                key[i] = k;
-                atomicAdd(&h[k & (B - 1)], 1);
+            } else {
+#pragma unroll
+                for (int k = 0; k < E; ++k) {
+                    const int p = k * 32 + lane;
+                    const int o = __shfl_xor_sync(0xffffffffu, e[k], stride);
+                    const bool up = (p & size) == 0, lower = (p & stride) == 0;
+                    e[k] = (up == lower) ? min(e[k], o) : max(e[k], o);
+                }
             }
         }
-        __syncwarp();
-        for (int d = lane; d < B; d += 32) hist0[(int64_t)d * nchunks + chunk] = h[d];
+    }
+}
+
+template <int E>
+__device__ __forceinline__ void leaf_pack(const int* __restrict__ slot, int lo, int c, int leaf,
+                                          const double* __restrict__ x, const double* __restrict__ y,
+                                          const double* __restrict__ g,
+                                          const double* __restrict__ sigma, int* __restrict__ keys,
+                                          int* __restrict__ perm, Src* __restrict__ src,
+                                          unsigned long long& smax, unsigned long long& smin) {
+    const int lane = threadIdx.x & 31;
+    int e[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        const int p = k * 32 + lane;
+        e[k] = p < c ? slot[lo + p] : INT_MAX;
+    }
+    warp_bitonic<E>(e);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        const int p = k * 32 + lane;
+        if (p >= c) continue;
+        const int idx = e[k];
+        const double s = sigma ? sigma[idx] : 1.0;
+        Src r;
+        r.x = x[idx];
+        r.y = y[idx];
+        r.g = g[idx];
+        r.q2 = -1.4426950408889634 / (2.0 * s * s);  // -r^2 / (2 sigma^2) in log2 units
+        src[lo + p] = r;
+        perm[lo + p] = idx;
+        keys[lo + p] = leaf;
+        if (sigma) {
+            const unsigned long long b = ordered_bits(s);
+            smax = b > smax ? b : smax;
+            smin = b < smin ? b : smin;
+        }
+    }
+}
+
+// Warp per leaf: restore the stable order inside the leaf, write the sorted
+// keys, the permutation and the packed records.
+__global__ void __launch_bounds__(256)
+    k_leaf_pack(const int* __restrict__ ls, const int* __restrict__ slot, int nleaves,
+                const double* __restrict__ x, const double* __restrict__ y,
+                const double* __restrict__ g, const double* __restrict__ sigma,
+                int* __restrict__ keys, int* __restrict__ perm, Src* __restrict__ src,
+                Counters* __restrict__ ctr) {
+    if (ctr->sort_fallback) return;
+    __shared__ unsigned long long wmax[8], wmin[8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long smax = 0ull, smin = ~0ull;
+    for (int leaf = blockIdx.x * 8 + warp; leaf < nleaves; leaf += gridDim.x * 8) {
+        const int lo = ls[leaf], c = ls[leaf + 1] - lo;
+        if (c > 64)
+            leaf_pack<4>(slot, lo, c, leaf, x, y, g, sigma, keys, perm, src, smax, smin);
+        else if (c > 32)
+            leaf_pack<2>(slot, lo, c, leaf, x, y, g, sigma, keys, perm, src, smax, smin);
+        else if (c > 0)
+            leaf_pack<1>(slot, lo, c, leaf, x, y, g, sigma, keys, perm, src, smax, smin);
+    }
+    if (!sigma) return;
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, smax, o);
+        smax = t > smax ? t : smax;
+        const unsigned long long u = __shfl_xor_sync(0xffffffffu, smin, o);
+        smin = u < smin ? u : smin;
+    }
+    if (lane == 0) {
+        wmax[warp] = smax;
+        wmin[warp] = smin;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) {
+            smax = wmax[w] > smax ? wmax[w] : smax;
+            smin = wmin[w] < smin ? wmin[w] : smin;
+        }
+        if (smax) atomicMax(&ctr->sigma_max_bits, smax);
+        if (smin != ~0ull) atomicMax(&ctr->sigma_min_neg, ~smin);
     }
 }
 
@@ -95,12 +273,13 @@ __global__ void __launch_bounds__(256)
     k_pack_orig(const double* __restrict__ x, const double* __restrict__ y,
                 const double* __restrict__ g, const double* __restrict__ sigma, int64_t n,
                 Src* __restrict__ out, Counters* __restrict__ ctr) {
+    if (!ctr->sort_fallback) return;
     __shared__ unsigned long long wmax[8], wmin[8];
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long sbits = 0ull, smin = ~0ull;
-    if (i < n) {
+    // grid-stride (a small grid: the launch is cheap when the counting path ran)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
         const double s = sigma ? sigma[i] : 1.0;
-        if (sigma) sbits = smin = ordered_bits(s);
         Src r;
         r.x = x[i];
         r.y = y[i];
@@ -108,6 +287,11 @@ __global__ void __launch_bounds__(256)
         // -r^2 / (2 sigma^2) (engine.py:256) expressed in log2 units
         r.q2 = -1.4426950408889634 / (2.0 * s * s);
         out[i] = r;
+        if (sigma) {
+            const unsigned long long b = ordered_bits(s);
+            sbits = b > sbits ? b : sbits;
+            smin = b < smin ? b : smin;
+        }
     }
     if (!sigma) return;
     for (int o = 16; o > 0; o >>= 1) {
@@ -132,57 +316,212 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-// Stable scatter of one LSD pass: warp chunks are processed in index order,
-// lanes in index order within a round, equal digits ranked by lane
-// (match_any), so the relative order of equal keys is preserved.  Non-final
-// passes histogram the next digit per OUTPUT chunk (integer atomics: the
-// counts are exact); the final pass writes the packed Src records.
-__global__ void __launch_bounds__(kWPB * 32)
-    k_radix_scatter(const int* __restrict__ kin, const int* __restrict__ vin,
-                    int* __restrict__ kout, int* __restrict__ vout, int64_t n, int shift, int bits,
-                    int wc, int nchunks, const int* __restrict__ offs, int* __restrict__ hist_next,
-                    const Src* __restrict__ packed, Src* __restrict__ src) {
-    extern __shared__ int sh[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// ---- LSD radix path: one kernel per pass over tiles of kTile keys ----
+//
+// Tile = 256 threads x 8 keys.  Warp w ranks its 256 consecutive keys in 8
+// rounds of 32 (match_any; lanes and rounds in index order), so ranks are
+// stable.  Per-digit tile counts are chained across tiles by decoupled
+// look-back (tiles numbered by ticket), the keys are staged in shared memory
+// in tile-sorted order and written out digit run by digit run (coalesced).
+constexpr int kTileThreads = 256;
+constexpr int kTileItems = 8;
+constexpr int kTile = kTileThreads * kTileItems;  // 2048
+constexpr unsigned kLbAgg = 1u << 30, kLbIncl = 2u << 30, kLbMask = (1u << 30) - 1;
+
+// Exclusive scan of one value per thread over a 256-thread block.
+__device__ __forceinline__ int block_excl_256(int v, int* wsum) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int add = 0;
+    for (int w = 0; w < warp; ++w) add += wsum[w];
+    return add + incl - v;
+}
+
+// Keys (floor rule, domain check) + the global digit histograms of every pass.
+__global__ void __launch_bounds__(kTileThreads)
+    k_keys_ghist(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                 double xmin, double ymin, double side, int levels, int bits, int passes,
+                 int* __restrict__ key, int* __restrict__ ghist, Counters* __restrict__ ctr) {
+    if (!ctr->sort_fallback) return;  // the counting path built the tree
+    const bool probe_lsd = ctr->sort_fallback == kSortLsdProbe;
+    __shared__ int h[4 * 256];
     const int B = 1 << bits;
-    int* run = sh + warp * B;
-    const int64_t chunk = (int64_t)blockIdx.x * kWPB + warp;
-    if (chunk >= nchunks) return;
-    for (int d = lane; d < B; d += 32) run[d] = offs[(int64_t)d * nchunks + chunk];
-    __syncwarp();
+    for (int i = threadIdx.x; i < passes * B; i += kTileThreads) h[i] = 0;
+    __syncthreads();
+    const int m = 1 << levels;
+    const double inv = 1.0 / side;
+    const double xmax = xmin + side, ymax = ymin + side;  // Domain.xmax (model.py:51-57)
+    const int64_t base = (int64_t)blockIdx.x * kTile;
+#pragma unroll 4
+    for (int it = 0; it < kTileItems; ++it) {
+        const int64_t i = base + it * kTileThreads + threadIdx.x;
+        if (i >= n) break;
+        const double xi = x[i], yi = y[i];
+        int ix = 0, iy = 0;
+        if ((xi >= xmin) && (xi <= xmax) && (yi >= ymin) && (yi <= ymax)) {
+            ix = cell_of(xi, xmin, side, inv, m);
+            iy = cell_of(yi, ymin, side, inv, m);
+        } else if (probe_lsd) {  // otherwise k_bin_count counted them
+            atomicAdd(&ctr->bad_count, 1);
+            atomicMax(&ctr->first_bad_neg, INT_MAX - (int)i);
+        }
+        const int k = iy * m + ix;
+        key[i] = k;
+        for (int p = 0; p < passes; ++p) atomicAdd(&h[p * B + ((k >> (p * bits)) & (B - 1))], 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * B; i += kTileThreads)
+        if (h[i]) atomicAdd(&ghist[i], h[i]);
+}
+
+// One stable LSD pass.  lb: per (tile, digit) look-back words (zeroed),
+// ticket: tile counter (zeroed).  The last pass also moves the packed
+// 32-byte source records (packed[val] -> src[pos]).
+__global__ void __launch_bounds__(kTileThreads)
+    k_onesweep(const int* __restrict__ kin, const int* __restrict__ vin, int* __restrict__ kout,
+               int* __restrict__ vout, int64_t n, int shift, int bits,
+               const int* __restrict__ ghist, unsigned* __restrict__ lb, int* __restrict__ ticket,
+               const Src* __restrict__ packed, Src* __restrict__ src,
+               const Counters* __restrict__ ctr) {
+    if (!ctr->sort_fallback) return;
+    constexpr int W = kTileThreads / 32;
+    __shared__ int wcnt[W][256];   // per-warp digit counts, then per-warp prefixes
+    __shared__ int gbase[256];     // global position of the tile's first key of digit d, minus its local start
+    __shared__ int lstart[256];
+    __shared__ int skey[kTile];
+    __shared__ int sval[kTile];
+    __shared__ int tile_s;
+    const int B = 1 << bits;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) tile_s = atomicAdd(ticket, 1);
+    for (int i = threadIdx.x; i < W * 256; i += kTileThreads) (&wcnt[0][0])[i] = 0;
+    __syncthreads();
+    const int tile = tile_s;
+    const int64_t base = (int64_t)tile * kTile;
+    const int cnt = (int)min((int64_t)kTile, n - base);
+    // ---- rank: warp w owns keys [w*512, (w+1)*512) of the tile ----
+    int kr[kTileItems], vr[kTileItems], rk[kTileItems];
     const unsigned lt = (1u << lane) - 1u;
-    const int64_t beg = chunk * wc;
-    const int64_t end = beg + wc < n ? beg + wc : n;
-    constexpr int R = 8;  // rounds whose loads are issued together
-    for (int64_t base0 = beg; base0 < end; base0 += 32 * R) {
-        int kr[R], vr[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int64_t i = base0 + 32 * r + lane;
-            kr[r] = i < end ? kin[i] : 0;
-            vr[r] = i < end ? (vin ? vin[i] : (int)i) : 0;
+    for (int it = 0; it < kTileItems; ++it) {
+        const int j = warp * 32 * kTileItems + it * 32 + lane;
+        const bool ok = j < cnt;
+        kr[it] = ok ? kin[base + j] : 0;
+        vr[it] = ok ? (vin ? vin[base + j] : (int)(base + j)) : 0;
+    }
+#pragma unroll
+    for (int it = 0; it < kTileItems; ++it) {
+        const int j = warp * 32 * kTileItems + it * 32 + lane;
+        const bool ok = j < cnt;
+        const int d = ok ? (kr[it] >> shift) & (B - 1) : 256 + lane;  // invalid: unique, unranked
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        int pre = 0;
+        if (ok) pre = wcnt[warp][d];
+        rk[it] = pre + __popc(peers & lt);
+        __syncwarp();
+        if (ok && (peers >> lane) == 1u) wcnt[warp][d] = pre + __popc(peers);  // highest lane of the group
+        __syncwarp();
+    }
+    __syncthreads();
+    // ---- per-digit tile counts, warp prefixes, local starts ----
+    const int d = threadIdx.x;  // one thread per digit (B <= 256)
+    int c = 0;
+    if (d < B) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const int t = wcnt[w][d];
+            wcnt[w][d] = c;
+            c += t;
         }
+    }
+    __shared__ int wsum[2][W];
+    lstart[d] = block_excl_256(c, wsum[0]);
+    // global start of digit d: exclusive scan of this pass's global histogram
+    const int gstart = block_excl_256(d < B ? ghist[d] : 0, wsum[1]);
+    // ---- decoupled look-back per digit ----
+    if (d < B) {
+        volatile unsigned* st = lb + (size_t)tile * B;
+        int prefix = 0;
+        // flag and count share one word, so relaxed (volatile) accesses
+        // suffice: no fences, which would also invalidate L1
+        if (tile == 0) {
+            st[d] = kLbIncl | (unsigned)c;
+        } else {
+            st[d] = kLbAgg | (unsigned)c;
+            // walk back 8 predecessors per round (independent loads in flight)
+            for (int j = tile - 1; j >= 0;) {
+                unsigned w[8];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int64_t i = base0 + 32 * r + lane;
-            const bool valid = i < end;
-            const int k = kr[r], v = vr[r];
-            const int d = valid ? (k >> shift) & (B - 1) : B + lane;
-            const unsigned peers = __match_any_sync(0xffffffffu, d);
-            const int rank = __popc(peers & lt);
-            if (valid) {
-                const int pos = run[d] + rank;
-                kout[pos] = k;
-                vout[pos] = v;
-                if (hist_next)
-                    atomicAdd(&hist_next[(int64_t)((k >> (shift + bits)) & (B - 1)) * nchunks + pos / wc], 1);
-                else
-                    src[pos] = packed[v];  // one 32-byte record
+                for (int q = 0; q < 8; ++q)
+                    w[q] = j - q >= 0 ? (unsigned)((volatile unsigned*)(lb + (size_t)(j - q) * B))[d] : 0u + kLbIncl;
+                int q = 0;
+                bool done = false;
+                for (; q < 8; ++q) {
+                    if ((w[q] >> 30) == 0) break;  // not published yet: reload from here
+                    prefix += (int)(w[q] & kLbMask);
+                    if (w[q] & kLbIncl) {
+                        done = true;
+                        break;
+                    }
+                }
+                if (done) break;
+                j -= q;
             }
-            __syncwarp();
-            if (valid && rank == __popc(peers) - 1) run[d] += __popc(peers);
-            __syncwarp();
+            st[d] = kLbIncl | (unsigned)(prefix + c);
         }
+        gbase[d] = gstart + prefix - lstart[d];
+    }
+    __syncthreads();
+    // ---- stage in tile-sorted order ----
+#pragma unroll
+    for (int it = 0; it < kTileItems; ++it) {
+        const int j = warp * 32 * kTileItems + it * 32 + lane;
+        if (j < cnt) {
+            const int dd = (kr[it] >> shift) & (B - 1);
+            const int lp = lstart[dd] + wcnt[warp][dd] + rk[it];
+            skey[lp] = kr[it];
+            sval[lp] = vr[it];
+        }
+    }
+    __syncthreads();
+    // ---- write out digit runs (consecutive j -> consecutive global positions) ----
+    if (!packed) {
+#pragma unroll 4
+        for (int j = threadIdx.x; j < cnt; j += kTileThreads) {
+            const int k = skey[j];
+            const int pos = gbase[(k >> shift) & (B - 1)] + j;
+            kout[pos] = k;
+            vout[pos] = sval[j];
+        }
+        return;
+    }
+    // last pass: also one 32-byte record per key; the random record reads of
+    // a thread's keys are issued together
+#pragma unroll
+    for (int it = 0; it < kTileItems; it += 4) {
+        Src r[4];
+        int pos[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int j = (it + q) * kTileThreads + threadIdx.x;
+            pos[q] = -1;
+            if (j < cnt) {
+                const int k = skey[j], v = sval[j];
+                pos[q] = gbase[(k >> shift) & (B - 1)] + j;
+                kout[pos[q]] = k;
+                vout[pos[q]] = v;
+                r[q] = packed[v];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (pos[q] >= 0) src[pos[q]] = r[q];
     }
 }
 
@@ -226,9 +565,11 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_sums, int* 
 // one look-back per tile keeps the serial chain short (~n / 8192 tiles).
 __global__ void __launch_bounds__(kScanThreads)
     k_scan(int* __restrict__ data, int64_t n, unsigned long long* __restrict__ state,
-           const Counters* __restrict__ sym_skip, bool gauss) {
+           const Counters* __restrict__ sym_skip, bool gauss, const int* __restrict__ skip_flag,
+           int skip_val) {
     // the near-field task list is not needed when the symmetric P2P kernel runs
     if (sym_skip && p2p_symmetric(sym_skip, gauss)) return;
+    if (skip_flag && *skip_flag == skip_val) return;  // leaf-count scan: counting path only
     __shared__ int warp_sums[32];
     __shared__ int total;
     __shared__ int tile_s;
@@ -264,12 +605,11 @@ __global__ void __launch_bounds__(kScanThreads)
     if (threadIdx.x == 0) {
         volatile unsigned long long* st = state + 1;
         long long prefix = 0;
+        // flag and value share one 64-bit word: relaxed (volatile) accesses, no fences
         if (tile == 0) {
-            __threadfence();
             st[0] = kFlagIncl | (unsigned long long)carry;
         } else {
             st[tile] = kFlagAgg | (unsigned long long)carry;
-            __threadfence();
             for (int j = tile - 1; j >= 0;) {
                 const unsigned long long w = st[j];
                 if ((w >> 62) == 0) continue;  // predecessor not published yet
@@ -277,7 +617,6 @@ __global__ void __launch_bounds__(kScanThreads)
                 if (w & kFlagIncl) break;
                 --j;
             }
-            __threadfence();
             st[tile] = kFlagIncl | (unsigned long long)(prefix + carry);
         }
         prefix_s = prefix;
@@ -298,12 +637,14 @@ __global__ void __launch_bounds__(kScanThreads)
 }
 
 __global__ void k_leaf_starts(const int* __restrict__ keys, int64_t n, int nleaves,
-                              int* __restrict__ ls) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i > n) return;
-    const int prev = i > 0 ? keys[i - 1] : -1;
-    const int cur = i < n ? keys[i] : nleaves;
-    for (int k = prev + 1; k <= cur; ++k) ls[k] = (int)i;
+                              int* __restrict__ ls, const Counters* __restrict__ ctr) {
+    if (ctr && !ctr->sort_fallback) return;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int prev = i > 0 ? keys[i - 1] : -1;
+        const int cur = i < n ? keys[i] : nleaves;
+        for (int k = prev + 1; k <= cur; ++k) ls[k] = (int)i;
+    }
 }
 
 // Occupancy of every cell of every level (level 0 first) from leaf_starts
@@ -362,7 +703,21 @@ __global__ void k_tasks_fill(const int* __restrict__ ls, int levels, int chunk, 
 }
 
 
+// VFMM_SORT=lsd forces the LSD radix path (tuning / tests)
+bool force_lsd() {
+    static const bool f = [] {
+        const char* e = getenv("VFMM_SORT");
+        return e && e[0] == 'l';
+    }();
+    return f;
+}
+
 inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
+// grid-stride kernels of the LSD fallback: at most 148 x 4 blocks of 256
+inline unsigned small_grid(int64_t n, unsigned cap = 592u) {
+    const unsigned g = grid_for(n, 256);
+    return g < cap ? g : cap;
+}
 
 }  // namespace
 
@@ -373,9 +728,10 @@ void launch_init_counters(Counters* ctr, cudaStream_t s) {
 size_t scan_tiles(int64_t n) { return (size_t)((n + kScanTile - 1) / kScanTile); }
 
 void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream_t s,
-                     const Counters* sym_skip, bool gauss) {
+                     const Counters* sym_skip, bool gauss, const int* skip_flag, int skip_val) {
     if (n <= 0) return;
-    k_scan<<<(unsigned)scan_tiles(n), kScanThreads, 0, s>>>(data, n, state, sym_skip, gauss);
+    k_scan<<<(unsigned)scan_tiles(n), kScanThreads, 0, s>>>(data, n, state, sym_skip, gauss,
+                                                              skip_flag, skip_val);
     note_launches(1);
 }
 
@@ -387,47 +743,70 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     int* vbuf[2] = {(int*)(ws + L.val_a), (int*)(ws + L.val_b)};
     const int bits = L.digit_bits;
     const int B = 1 << bits;
-    const int64_t hsize = (int64_t)B * L.nchunks;
-    auto hist = [&](int p) { return (int*)(ws + L.hist) + p * hsize; };
     auto state = [&](int i) {
         return (unsigned long long*)(ws + L.scan_state) + (size_t)i * (L.scan_state_tiles + 1);
     };
-    const unsigned blocks = (unsigned)((L.nchunks + kWPB - 1) / kWPB);
-    const size_t shm = (size_t)kWPB * B * sizeof(int);
-    Src* packed = (Src*)(ws + L.near_uv);  // free until the near field runs (9 x 16 B >= 32 B per particle)
-    // scratch zeroed by the first kernel: histograms of passes 1.. and all scan states
-    unsigned* zero = (unsigned*)(ws + L.hist) + hsize;
-    const int64_t nzero_hist = hsize * (L.passes - 1);
-    k_keys_hist<<<blocks, kWPB * 32, shm, s>>>(x, y, L.n, xmin, ymin, side, L.levels, bits,
-                                              L.wc, L.nchunks, kbuf[0], hist(0), zero, nzero_hist,
-                                              ctr);
-    note_launches(1);
+    int* ls = (int*)(ws + L.leaf_starts);
+    int* fkeys = kbuf[L.passes & 1];  // final buffers of either path (vfmm_layout_of)
+    int* fperm = vbuf[L.passes & 1];
+    Src* src = (Src*)(ws + L.src);
     cudaMemsetAsync(ws + L.scan_state, 0, L.scan_state_bytes, s);
+
+    k_sort_probe<<<1, 256, 0, s>>>(x, y, L.n, xmin, ymin, side, L.levels, force_lsd(), ctr);
+    note_launches(1);
+    // ---- counting path (kernels return at once if the probe chose LSD) ----
+    cudaMemsetAsync(ls, 0, sizeof(int) * (L.nleaves + 1), s);
+    k_bin_count<<<small_grid(L.n, 2368), 256, 0, s>>>(x, y, L.n, xmin, ymin, side, L.levels,
+                                                  kbuf[(L.passes + 1) & 1], ls, ctr);
+    note_launches(1);
+    launch_scan_i32(ls, (int64_t)L.nleaves + 1, state(L.passes + 1), s, nullptr, false,
+                    &ctr->sort_fallback, kSortLsdProbe);
+    int* fill = (int*)(ws + L.task_scratch);  // free until the task counts
+    cudaMemsetAsync(fill, 0, sizeof(int) * L.nleaves, s);
+    int* slot = vbuf[(L.passes + 1) & 1];
+    k_bin_scatter<<<small_grid(L.n, 2368), 256, 0, s>>>(kbuf[(L.passes + 1) & 1], L.n, ls, fill,
+                                                    slot, ctr);
+    note_launches(1);
+    // gamma and sigma are first read by the record pack (host mode: their
+    // copies overlap the binning)
+    if (gs_ready) cudaStreamWaitEvent(s, gs_ready, 0);
+    k_leaf_pack<<<std::min(grid_for((int64_t)L.nleaves, 8), 2368u), 256, 0, s>>>(ls, slot, (int)L.nleaves, x, y, g,
+                                                              sigma, fkeys, fperm, src, ctr);
+    note_launches(1);
+
+    // ---- LSD radix path (kernels return at once unless ctr->sort_fallback) ----
+    Src* packed = (Src*)(ws + L.near_uv);  // free until the near field runs (>= 32 B per particle)
+    int* ghist = (int*)(ws + L.hist);     // passes x B global digit counts, tickets, look-back
+    int* tickets = ghist + L.passes * B;
+    unsigned* lbase = (unsigned*)(tickets + 8);
+    const size_t lb_words = (size_t)L.nchunks * B;
+    const unsigned tiles = (unsigned)L.nchunks;
+    cudaMemsetAsync(ghist, 0, L.hist_bytes, s);
+    k_keys_ghist<<<tiles, kTileThreads, 0, s>>>(x, y, L.n, xmin, ymin, side, L.levels, bits,
+                                                L.passes, kbuf[0], ghist, ctr);
+    note_launches(1);
     for (int p = 0; p < L.passes; ++p) {
-        launch_scan_i32(hist(p), hsize, state(p), s, nullptr, false);
         const bool last = p == L.passes - 1;
-        // gamma and sigma are first read by the record pack before the last
-        // pass (host mode: their copies overlap the key / sort work)
         if (last) {
-            if (gs_ready) cudaStreamWaitEvent(s, gs_ready, 0);
-            k_pack_orig<<<grid_for(L.n, 256), 256, 0, s>>>(x, y, g, sigma, L.n, packed, ctr);
+            k_pack_orig<<<small_grid(L.n), 256, 0, s>>>(x, y, g, sigma, L.n, packed, ctr);
             note_launches(1);
         }
-        k_radix_scatter<<<blocks, kWPB * 32, shm, s>>>(
+        k_onesweep<<<tiles, kTileThreads, 0, s>>>(
             kbuf[p & 1], p == 0 ? nullptr : vbuf[p & 1], kbuf[(p + 1) & 1], vbuf[(p + 1) & 1], L.n,
-            p * bits, bits, L.wc, L.nchunks, hist(p), last ? nullptr : hist(p + 1), packed,
-            (Src*)(ws + L.src));
+            p * bits, bits, ghist + p * B, lbase + p * lb_words, tickets + p, last ? packed : nullptr,
+            src, ctr);
         note_launches(1);
     }
-    *keys_out = kbuf[L.passes & 1];
-    *perm_out = vbuf[L.passes & 1];
-    int* ls = (int*)(ws + L.leaf_starts);
-    launch_leaf_starts(*keys_out, L.n, (int)L.nleaves, ls, s);
+    *keys_out = fkeys;
+    *perm_out = fperm;
+    k_leaf_starts<<<small_grid(L.n + 1, 1184), 256, 0, s>>>(fkeys, L.n, (int)L.nleaves, ls, ctr);
+    note_launches(1);
 }
 
 void launch_leaf_starts(const int* sorted_keys, int64_t n, int nleaves, int* leaf_starts,
                         cudaStream_t s) {
-    k_leaf_starts<<<grid_for(n + 1, 256), 256, 0, s>>>(sorted_keys, n, nleaves, leaf_starts);
+    k_leaf_starts<<<grid_for(n + 1, 256), 256, 0, s>>>(sorted_keys, n, nleaves, leaf_starts,
+                                                        nullptr);
     note_launches(1);
 }
 

@@ -48,7 +48,7 @@ struct Counters {
     int ntasks;
     int task_cursor;  // dynamic P2P work distribution
     int max_leaf;     // largest leaf occupancy (owned rows)
-    int pad2;
+    int sort_fallback;  // 1: a leaf exceeds kFastLeafMax, the LSD radix path builds the tree
 };
 
 // Translation tables (device globals, uploaded once per device).
@@ -70,7 +70,7 @@ struct Layout {
     size_t nleaves;
     size_t key_a, key_b, val_a, val_b, hist, task_scratch, scan_state, src, near_uv, leaf_starts,
         counts, mult, loc, leaf_loc, tasks, stage, counters, total;
-    size_t scan_state_tiles, scan_state_bytes;  // per scan instance: 1 ticket + tiles
+    size_t scan_state_tiles, scan_state_bytes, hist_bytes;  // per scan instance: 1 ticket + tiles
     size_t level_cell_off[VFMM_LEVELS_CAP + 2];  // cells before level k (k>=2) in mult/loc
     size_t count_off[VFMM_LEVELS_CAP + 2];       // cells before level k in counts
     size_t max_tasks;
@@ -97,7 +97,8 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
                   Counters* ctr, cudaStream_t s, int** keys_out, int** perm_out,
                   cudaEvent_t gs_ready = nullptr);
 void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream_t s,
-                     const Counters* sym_skip, bool gauss);
+                     const Counters* sym_skip, bool gauss, const int* skip_flag = nullptr,
+                     int skip_val = 0);
 size_t scan_tiles(int64_t n);
 void launch_leaf_starts(const int* sorted_keys, int64_t n, int nleaves, int* leaf_starts,
                         cudaStream_t s);
