@@ -81,6 +81,8 @@ void build_tables(Tables* t) {
     for (int j = 0; j < 2 * kOrderCap + 16; ++j) t->pow2neg[j] = std::ldexp(1.0, -j);
     for (int j = 0; j < kExpTabN; ++j)
         t->exp2tab[j] = (double)exp2l((long double)(j - (kExpTabN - 1)) / (long double)kExpSteps);
+    for (int j = 0; j < kExpTab2N; ++j)
+        t->exp2tab2[j] = (double)exp2l((long double)(j - (kExpTab2N - 1)) / (long double)kExpSteps2);
 }
 
 int current_device_of(const void* p, int* dev) {

@@ -182,8 +182,8 @@ constexpr int kRingUnroll = VFMM_RING_UNROLL;
 #endif
 constexpr bool kRepRing = VFMM_REP_RING;  // replicated-target ring for 33..64-particle leaves  // steps of a full ring per loop iteration
 constexpr int kSymWarps = 8;
-constexpr int kSymExpBytes = (kExpTab * 8 + 15) / 16 * 16;
-constexpr int kSymSmem = kSymExpBytes + 2 * kSymWarps * kSymMaxLeaf * 16;  // 62 KB
+constexpr int kSymExpBytes = (kExpTab2N * 8 + 15) / 16 * 16;
+constexpr int kSymSmem = kSymExpBytes + 2 * kSymWarps * kSymMaxLeaf * 16;  // 92 KB
 
 __device__ __forceinline__ void load_lane(const Src* __restrict__ src, int lo, int cnt, int lane,
                                           double& x, double& y, double& g) {
@@ -194,13 +194,45 @@ __device__ __forceinline__ void load_lane(const Src* __restrict__ src, int lo, i
     g = lane < cnt ? s.g : 0.0;
 }
 
+// Symmetric-kernel pair factor K = (1 - e) / r^2, e = exp(-r^2 / (2 sigma^2)),
+// for the uniform core size of the symmetric mode.  With q = 128 q2
+// (y = r^2 q in units of 1/128 octave) the range reduction reads r^2
+// directly: n = round(r^2 q) by the 1.5*2^52 shifter, s = r^2 q - n by one
+// FMA (|s| <= 1/2), e = T[n] (1 + s P(s)), T[n] = 2^(n/128), P the degree-3
+// minimax fit of (2^(s/128) - 1) / s (relative error of e <= 7.6e-17,
+// 0.68 ulp, before rounding).  y >= -60 octaves is enforced on r^2 with one
+// integer op (r^2 <= r2max, high words); beyond, 1 - e rounds to 1 anyway.
+struct SymExp {
+    double q;      // 128 q2 (< 0)
+    unsigned hi;   // high word of the largest r^2 kept (y128 >= -7680.01)
+};
+__device__ __forceinline__ SymExp sym_exp(double q2) {
+    SymExp e;
+    e.q = 128.0 * q2;
+    e.hi = (unsigned)__double2hiint(7680.0 / -e.q);
+    return e;
+}
+__constant__ double c_exp2_sym[4] = {5.415212348123814e-03, 1.4662262387636998e-05,
+                                     2.6466433582090788e-08, 3.5830355923967645e-11};
+
 template <bool GAUSS>
-__device__ __forceinline__ double pair_kernel(double dx, double dy, double& r2, double q2,
+__device__ __forceinline__ double pair_kernel(double dx, double dy, SymExp x,
                                               const double* __restrict__ tab) {
-    r2 = fma(dy, dy, dx * dx);
+    const double r2 = fma(dy, dy, dx * dx);
     const double inv = rcp_fast(r2);
     if (!GAUSS) return inv;
-    return fma(-inv, exp2_neg(clamp_neg60(r2 * q2), tab), inv);  // (1 - e) / r^2
+    const unsigned hi = min((unsigned)__double2hiint(r2), x.hi);
+    const double r2c = __hiloint2double((int)hi, __double2loint(r2));
+    const double kShift = 6755399441055744.0;  // 1.5 * 2^52
+    const double t = fma(r2c, x.q, kShift);
+    const double s = fma(r2c, x.q, kShift - t);  // r^2 q - n (exact: -n = shift - t)
+    double p = c_exp2_sym[3];
+    p = fma(p, s, c_exp2_sym[2]);
+    p = fma(p, s, c_exp2_sym[1]);
+    p = fma(p, s, c_exp2_sym[0]);
+    const double T = tab[__double2loint(t)];
+    const double e = fma(T, s * p, T);
+    return fma(-inv, e, inv);  // (1 - e) / r^2
 }
 
 // One ring rotation: the B chunk (R sources) is replicated in every R-lane
@@ -213,7 +245,7 @@ __device__ __forceinline__ double pair_kernel(double dx, double dy, double& r2, 
 template <bool GAUSS, int TPL, int R, bool SYM>
 __device__ __forceinline__ void rotate_ring(double a0x, double a0y, double a0g, double a1x,
                                             double a1y, double a1g, double bx, double by, double bg,
-                                            double& ub, double& vb, double q2,
+                                            double& ub, double& vb, SymExp q2,
                                             const double* __restrict__ tab, double& u0, double& v0,
                                             double& u1, double& v1) {
     const int from = ((threadIdx.x & 31) + 1) & (R - 1);
@@ -223,8 +255,7 @@ __device__ __forceinline__ void rotate_ring(double a0x, double a0y, double a0g, 
     for (int st = 0; st < R; ++st) {
         {
             const double dx = a0x - bx, dy = a0y - by;
-            double r2;
-            const double K = pair_kernel<GAUSS>(dx, dy, r2, q2, tab);
+            const double K = pair_kernel<GAUSS>(dx, dy, q2, tab);
             const double ca = bg * K;
             u0 = fma(-ca, dy, u0);
             v0 = fma(ca, dx, v0);
@@ -236,8 +267,7 @@ __device__ __forceinline__ void rotate_ring(double a0x, double a0y, double a0g, 
         }
         if (TPL == 2) {
             const double dx = a1x - bx, dy = a1y - by;
-            double r2;
-            const double K = pair_kernel<GAUSS>(dx, dy, r2, q2, tab);
+            const double K = pair_kernel<GAUSS>(dx, dy, q2, tab);
             const double ca = bg * K;
             u1 = fma(-ca, dy, u1);
             v1 = fma(ca, dx, v1);
@@ -269,7 +299,7 @@ __device__ __forceinline__ void rotate_ring(double a0x, double a0y, double a0g, 
 // written back to `acc` (shared memory, per warp).
 template <bool GAUSS, bool SYM>
 __device__ __forceinline__ void chunk_vs_leaf(const Src* __restrict__ src, int loA, int cntA, int loB,
-                                              int nB, bool first, double2* acc, double q2,
+                                              int nB, bool first, double2* acc, SymExp q2,
                                               const double* __restrict__ tab, double& u0,
                                               double& v0, double& u1, double& v1) {
     const int lane = threadIdx.x & 31;
@@ -331,12 +361,13 @@ __global__ void __launch_bounds__(kSymWarps * 32, MINB)
     double* sexp = reinterpret_cast<double*>(sym_smem);
     double2* accB = reinterpret_cast<double2*>(sym_smem + kSymExpBytes);
     double2* accA = accB + kSymWarps * kSymMaxLeaf;
-    const double* tab = stage_exp_table(sexp, T->exp2tab);
+    for (int i = threadIdx.x; i < kExpTab2N; i += blockDim.x) sexp[i] = T->exp2tab2[i];
+    const double* tab = sexp + (kExpTab2N - 1);  // 2^(n/128) at tab[n], n <= 0
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double2* acc = accB + warp * kSymMaxLeaf;
     double2* accAw = accA + warp * kSymMaxLeaf;
-    const double q2 = GAUSS ? src[0].q2 : 0.0;  // uniform core size
+    const SymExp q2 = sym_exp(GAUSS ? src[0].q2 : -1.0);  // uniform core size
     long long my_pairs = 0;
     // the next item index is fetched one item ahead to hide the atomic's latency
     int next = 0;

@@ -26,6 +26,8 @@ constexpr int kQMax = 2 * kOrderCap + 16;  // H table length (padded for m-chunk
 constexpr int kOffsets = 49;               // 7x7 offset grid (dy+3)*7 + (dx+3)
 constexpr int kExpSteps = 64;              // exp table resolution: 2^(n/64)
 constexpr int kExpTabN = 60 * kExpSteps + 1;  // exp table entries, n = -3840..0
+constexpr int kExpSteps2 = 128;            // symmetric P2P table: 2^(n/128)
+constexpr int kExpTab2N = 60 * kExpSteps2 + 1;  // n = -7680..0 (60 KB)
 constexpr int kNearRows = 3;               // generic P2P: one partial sum per neighbourhood row
 constexpr int kNearSlots = 5;              // symmetric P2P: own blocks + 4 reactions
 constexpr int kSymMaxLeaf = 128;           // symmetric P2P needs leaves of <= 128 particles
@@ -59,6 +61,7 @@ struct Tables {
     double invfact[kOrderCap + 16];
     double pow2neg[2 * kOrderCap + 16];  // 2^-k
     double exp2tab[kExpTabN];        // 2^(n/64), n = -3840..0
+    double exp2tab2[kExpTab2N];      // 2^(n/128), n = -7680..0 (symmetric P2P)
 };
 
 const Tables* device_tables();   // device pointer (uploaded on first use)
