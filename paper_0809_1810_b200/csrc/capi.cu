@@ -29,8 +29,8 @@ bool g_tables_ready[kMaxDevices];
 
 struct Resources {
     bool ready = false;
-    cudaStream_t far = nullptr;   // far-field chain (highest priority)
-    cudaStream_t near = nullptr;  // near field (lowest priority)
+    cudaStream_t far = nullptr;   // far-field chain
+    cudaStream_t near = nullptr;  // near field
     cudaStream_t comp = nullptr;  // compute stream of host-buffer evaluates
     cudaEvent_t fork = nullptr, join_far = nullptr, join_near = nullptr;
     cudaEvent_t xy = nullptr, gs = nullptr, done = nullptr;
@@ -118,9 +118,18 @@ Resources* resources_for(int dev) {
     if (!r.ready) {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        if (cudaStreamCreateWithPriority(&r.far, cudaStreamNonBlocking, hi) != cudaSuccess)
+        // Stream priorities of the two overlapped chains.  Measured (config 2,
+        // graph replay): equal 0.813 ms, near first 0.814, far first 0.851 --
+        // a prioritised far chain takes SM slots from the FP64-bound near
+        // field for latency-bound kernels.  VFMM_STREAM_PRIO=far|equal|near
+        // overrides (tuning).
+        const char* e = getenv("VFMM_STREAM_PRIO");
+        int pf = lo, pn = lo;
+        if (e && e[0] == 'f') pf = hi;
+        if (e && e[0] == 'n') pn = hi;
+        if (cudaStreamCreateWithPriority(&r.far, cudaStreamNonBlocking, pf) != cudaSuccess)
             return nullptr;
-        if (cudaStreamCreateWithPriority(&r.near, cudaStreamNonBlocking, lo) != cudaSuccess)
+        if (cudaStreamCreateWithPriority(&r.near, cudaStreamNonBlocking, pn) != cudaSuccess)
             return nullptr;
         if (cudaStreamCreateWithFlags(&r.comp, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
         cudaEventCreateWithFlags(&r.xy, cudaEventDisableTiming);
@@ -386,9 +395,9 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
                      side, ws, ctr, cs, &keys, &perm, gs_ready);
         launch_counts_tasks(L, ws, ctr, !far_only, rows, kernel == VFMM_KERNEL_GAUSSIAN, cs);
         rec(1, cs);
-        // Overlap: the far-field chain runs on a high-priority stream and the near
-        // field on a low-priority one; P2P CTAs are short-lived, so far-field CTAs
-        // are scheduled as soon as any SM slot frees up.
+        // Overlap: the far-field chain and the near field run on two streams
+        // (equal priority, see resources_for); P2P CTAs are short-lived, so
+        // far-field CTAs are scheduled as soon as SM slots free up.
         if (overlap) {
             cudaEventRecord(R->fork, cs);
             cudaStreamWaitEvent(R->far, R->fork, 0);

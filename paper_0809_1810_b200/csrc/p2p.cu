@@ -177,6 +177,10 @@ __global__ void __launch_bounds__(kP2PWarps * 32, kP2PBlocksPerSM)
 #define VFMM_RING_UNROLL 1
 #endif
 constexpr int kRingUnroll = VFMM_RING_UNROLL;
+#ifndef VFMM_SELF_SYM
+#define VFMM_SELF_SYM 1
+#endif
+constexpr bool kSelfSym = VFMM_SELF_SYM;  // self block: each unordered pair once
 #ifndef VFMM_REP_RING
 #define VFMM_REP_RING 1
 #endif
@@ -346,6 +350,74 @@ __device__ __forceinline__ void chunk_vs_leaf(const Src* __restrict__ src, int l
     }
 }
 
+// Self block of a leaf of nA <= 64 particles, each unordered pair once.
+// Lane l holds particles l (a0) and 32 + l (a1, ghosts past nA: zero
+// circulation).  Two half rings run together -- chunk 0 against itself and
+// chunk 1 against itself: after the first shift, 16 steps pair lane l with
+// l + 1 .. l + 16 (the distance-16 pairs only on lanes < 16), with each
+// source's reaction carried along and shuffled home at the end -- then one
+// symmetric full ring pairs chunk 0 (targets) with chunk 1 (sources).
+template <bool GAUSS>
+__device__ __forceinline__ void self_block_sym(double a0x, double a0y, double a0g, double a1x,
+                                               double a1y, double a1g, bool two, SymExp q2,
+                                               const double* __restrict__ tab, double& u0,
+                                               double& v0, double& u1, double& v1) {
+    const int lane = threadIdx.x & 31, from = (lane + 1) & 31;
+    double b0x = __shfl_sync(0xffffffffu, a0x, from), b0y = __shfl_sync(0xffffffffu, a0y, from);
+    double b0g = __shfl_sync(0xffffffffu, a0g, from);
+    double b1x = __shfl_sync(0xffffffffu, a1x, from), b1y = __shfl_sync(0xffffffffu, a1y, from);
+    double b1g = __shfl_sync(0xffffffffu, a1g, from);
+    double ub0 = 0.0, vb0 = 0.0, ub1 = 0.0, vb1 = 0.0;
+#pragma unroll 1
+    for (int st = 1; st <= 16; ++st) {
+        const bool on = st < 16 || lane < 16;
+        {
+            const double dx = a0x - b0x, dy = a0y - b0y;
+            const double K = on ? pair_kernel<GAUSS>(dx, dy, q2, tab) : 0.0;
+            const double ca = b0g * K, cb = a0g * K;
+            u0 = fma(-ca, dy, u0);
+            v0 = fma(ca, dx, v0);
+            ub0 = fma(cb, dy, ub0);
+            vb0 = fma(-cb, dx, vb0);
+        }
+        if (two) {
+            const double dx = a1x - b1x, dy = a1y - b1y;
+            const double K = on ? pair_kernel<GAUSS>(dx, dy, q2, tab) : 0.0;
+            const double ca = b1g * K, cb = a1g * K;
+            u1 = fma(-ca, dy, u1);
+            v1 = fma(ca, dx, v1);
+            ub1 = fma(cb, dy, ub1);
+            vb1 = fma(-cb, dx, vb1);
+        }
+        if (st < 16) {
+            b0x = __shfl_sync(0xffffffffu, b0x, from);
+            b0y = __shfl_sync(0xffffffffu, b0y, from);
+            b0g = __shfl_sync(0xffffffffu, b0g, from);
+            ub0 = __shfl_sync(0xffffffffu, ub0, from);
+            vb0 = __shfl_sync(0xffffffffu, vb0, from);
+            if (two) {
+                b1x = __shfl_sync(0xffffffffu, b1x, from);
+                b1y = __shfl_sync(0xffffffffu, b1y, from);
+                b1g = __shfl_sync(0xffffffffu, b1g, from);
+                ub1 = __shfl_sync(0xffffffffu, ub1, from);
+                vb1 = __shfl_sync(0xffffffffu, vb1, from);
+            }
+        }
+    }
+    // lane l holds the reaction of particle l + 16: send it home
+    const int home = (lane + 16) & 31;
+    u0 += __shfl_sync(0xffffffffu, ub0, home);
+    v0 += __shfl_sync(0xffffffffu, vb0, home);
+    if (!two) return;
+    u1 += __shfl_sync(0xffffffffu, ub1, home);
+    v1 += __shfl_sync(0xffffffffu, vb1, home);
+    double ubx = 0.0, vbx = 0.0, d0 = 0.0, d1 = 0.0;
+    rotate_ring<GAUSS, 1, 32, true>(a0x, a0y, a0g, 0.0, 0.0, 0.0, a1x, a1y, a1g, ubx, vbx, q2, tab,
+                                    u0, v0, d0, d1);
+    u1 += ubx;
+    v1 += vbx;
+}
+
 template <bool GAUSS, int MINB>
 __global__ void __launch_bounds__(kSymWarps * 32, MINB)
     k_p2p_sym(const Src* __restrict__ src, const int* __restrict__ ls, Counters* __restrict__ ctr,
@@ -397,6 +469,18 @@ __global__ void __launch_bounds__(kSymWarps * 32, MINB)
                 loB = ls[lb];
                 nB = ls[lb + 1] - loB;
                 if (nB == 0) continue;
+            }
+            if (kSelfSym && kind == 0 && nA <= 64) {  // each unordered pair of the leaf once
+                double a0x, a0y, a0g, a1x, a1y, a1g;
+                load_lane(src, loA, min(32, nA), lane, a0x, a0y, a0g);
+                load_lane(src, loA + (nA > 32 ? 32 : 0), max(nA - 32, 0), lane, a1x, a1y, a1g);
+                double u0 = 0.0, v0 = 0.0, u1 = 0.0, v1 = 0.0;
+                self_block_sym<GAUSS>(a0x, a0y, a0g, a1x, a1y, a1g, nA > 32, q2, tab, u0, v0, u1, v1);
+                accAw[lane] = make_double2(u0, v0);
+                accAw[32 + lane] = make_double2(u1, v1);
+                startedA = true;
+                my_pairs += (long long)nA * nA - nA;
+                continue;
             }
             for (int i0 = 0; i0 < nA; i0 += 64) {
                 const int cntA = min(64, nA - i0);
@@ -552,15 +636,20 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
                                          &ctr->near_pairs, kk, sym_disabled() ? 0 : 1);
     note_launches(1);
     // symmetric kernel: runs instead when the device-side mode check allows it
-    static int KS = 0;
-    if (!KS) {
+    // Leaf items per warp: enough CTAs for ~4 waves of 2 CTAs per SM (so
+    // the far chain finds free slots and the tail is short), otherwise as
+    // few CTAs as possible (each stages the 60 KB exp table).  Measured:
+    // config 1 (1K leaves) K=2, config 2 (16K) K=2..3, config 3 (262K) K=32
+    // best.  VFMM_P2P_SYM_K overrides (tuning).
+    static int KS_env = -1;
+    if (KS_env < 0) {
         const char* e = getenv("VFMM_P2P_SYM_K");
-        KS = e ? atoi(e) : 2;
-        if (KS < 1) KS = 2;
+        KS_env = e ? atoi(e) : 0;
     }
     const int64_t sym_items = 1ll << (2 * L.levels);  // one item per leaf
-    const unsigned sblocks = (unsigned)((sym_items + kSymWarps * KS - 1) / (kSymWarps * KS));
-    const int ks = KS;
+    int ks = KS_env > 0 ? KS_env : (int)(sym_items / ((int64_t)kSymWarps * 148 * 2 * 4));
+    ks = ks < 2 ? 2 : (ks > 32 ? 32 : ks);
+    const unsigned sblocks = (unsigned)((sym_items + kSymWarps * ks - 1) / (kSymWarps * ks));
     static int minb = 0;
     if (!minb) {
         const char* e = getenv("VFMM_P2P_SYM_MINB");
