@@ -46,12 +46,14 @@ extern "C" {
 #define VFMM_LEVELS_CAP 13      /* 4^13 leaves; int32 leaf keys */
 
 /* Flags for vfmm_evaluate */
-#define VFMM_FLAG_STATS 1u      /* synchronise the stream at the end and fill *stats (timings, counters) */
+#define VFMM_FLAG_STATS 1u      /* synchronise the stream at the end and fill *stats (counters, t_total) */
 #define VFMM_FLAG_OVERLAP 2u    /* run the near field (P2P) on a side stream concurrently with the
                                    far-field chain; phase timings then overlap */
 #define VFMM_FLAG_FAR_ONLY 4u   /* build the tree and the local expansions only (no near field, no
                                    evaluation at the particles); used before vfmm_evaluate_at */
 #define VFMM_FLAG_PHASE_UP 8u   /* vfmm_evaluate_shard: build + P2M + M2M only */
+#define VFMM_FLAG_PHASE_TIMES 64u /* with VFMM_FLAG_STATS: also time every phase (CUDA events between
+                                   the phases; costs ~0.1 ms per call) */
 #define VFMM_FLAG_UV_PAIRS 32u  /* u is an interleaved (N, 2) array of (u, v) rows -- the reference's
                                    return layout (engine.py:394-398); v is ignored */
 #define VFMM_FLAG_PHASE_DOWN 16u /* vfmm_evaluate_shard: M2L + L2L + P2P + L2P on the workspace of a
@@ -109,8 +111,11 @@ int vfmm_evaluate(const double* x, const double* y, const double* gamma, const d
  * contract, engine.py:335-398): x, y, gamma, sigma and u, v are host arrays
  * (pinned for full speed).  The copies are staged through the workspace and
  * overlapped with the build: positions first (binning / sort need only them),
- * gamma and sigma while the sort runs; u, v are copied back at the end.
- * Synchronous on `stream` only if VFMM_FLAG_STATS is set.                   */
+ * gamma and sigma while the sort runs; u, v are copied back at the end, on
+ * `stream`.  Synchronous on `stream` only if VFMM_FLAG_STATS is set.  Without
+ * it, calls on distinct streams AND distinct workspaces pipeline: the copies
+ * of one call overlap the compute of the previous one (the compute itself is
+ * serialised on the library's internal per-device streams).                 */
 int vfmm_evaluate_host(const double* x, const double* y, const double* gamma, const double* sigma,
                        int64_t n, double xmin, double ymin, double side, int levels, int order,
                        int kernel, double* u, double* v, void* workspace, size_t workspace_bytes,

@@ -12,12 +12,15 @@ from . import errors
 from .engine import (
     FmmConfig,
     FmmRunStats,
+    HostPipeline,
+    PendingEvaluation,
     Workspace,
     evaluate,
     evaluate_arrays,
     evaluate_at,
     evaluate_at_arrays,
     evaluate_host,
+    evaluate_host_async,
 )
 from .kernels import TWO_PI, KernelKind, velocity_direct, velocity_direct_arrays
 from .model import Domain, Particle, enclosing_domain, to_arrays
@@ -30,9 +33,11 @@ __all__ = [
     "errors",
     "FmmConfig",
     "FmmRunStats",
+    "HostPipeline",
     "KernelKind",
     "OutOfDomainError",
     "Particle",
+    "PendingEvaluation",
     "TWO_PI",
     "Workspace",
     "enclosing_domain",
@@ -41,6 +46,7 @@ __all__ = [
     "evaluate_at",
     "evaluate_at_arrays",
     "evaluate_host",
+    "evaluate_host_async",
     "grid_indices",
     "to_arrays",
     "velocity_direct",

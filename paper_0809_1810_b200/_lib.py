@@ -25,6 +25,7 @@ KERNEL_POINT = 0
 KERNEL_GAUSSIAN = 1
 
 FLAG_STATS = 1
+FLAG_PHASE_TIMES = 64
 FLAG_OVERLAP = 2
 FLAG_FAR_ONLY = 4
 FLAG_PHASE_UP = 8

@@ -35,6 +35,7 @@ struct Resources {
     cudaEvent_t fork = nullptr, join_far = nullptr, join_near = nullptr;
     cudaEvent_t xy = nullptr, gs = nullptr, done = nullptr;
     cudaEvent_t ev[9] = {};
+    Counters* hctr = nullptr;  // pinned staging of the device counters (stats)
 };
 Resources g_res[kMaxDevices];
 
@@ -132,6 +133,7 @@ Resources* resources_for(int dev) {
         if (cudaStreamCreateWithPriority(&r.near, cudaStreamNonBlocking, pn) != cudaSuccess)
             return nullptr;
         if (cudaStreamCreateWithFlags(&r.comp, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        if (cudaMallocHost((void**)&r.hctr, sizeof(Counters)) != cudaSuccess) return nullptr;
         cudaEventCreateWithFlags(&r.xy, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&r.gs, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming);
@@ -355,8 +357,10 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
     const bool odd = (L.passes & 1) != 0;
     int* keys = (int*)(ws + (odd ? L.key_b : L.key_a));
     int* perm = (int*)(ws + (odd ? L.val_b : L.val_a));
+    // per-phase events only on request; plain stats time the whole call (ev 0 -> 6)
+    const bool phases = timed && (flags & VFMM_FLAG_PHASE_TIMES) != 0;
     auto rec = [&](int i, cudaStream_t st) {
-        if (timed) cudaEventRecord(R->ev[i], st);
+        if (phases || (timed && (i == 0 || i == 6))) cudaEventRecord(R->ev[i], st);
     };
     for (int i = 0; i < 9; ++i) rec(i, s);  // every event defined even for a single phase
 
@@ -443,25 +447,33 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         }
     }
     if (hio) {
-        const size_t b = sizeof(double) * (size_t)n;
-        if (pairs) {
-            cudaMemcpyAsync(hio->hu, u, 2 * b, cudaMemcpyDeviceToHost, cs);
-        } else {
-            cudaMemcpyAsync(hio->hu, u, b, cudaMemcpyDeviceToHost, cs);
-            cudaMemcpyAsync(hio->hv, v, b, cudaMemcpyDeviceToHost, cs);
-        }
+        // results go back on the CALLER's stream: the internal compute stream
+        // is free for the next call at once (pipelined host-buffer calls on
+        // distinct streams and workspaces overlap D2H(k) and H2D(k+1) with
+        // the compute of k+1)
         cudaEventRecord(R->done, cs);
         cudaStreamWaitEvent(s, R->done, 0);
+        const size_t b = sizeof(double) * (size_t)n;
+        if (pairs) {
+            cudaMemcpyAsync(hio->hu, u, 2 * b, cudaMemcpyDeviceToHost, s);
+        } else {
+            cudaMemcpyAsync(hio->hu, u, b, cudaMemcpyDeviceToHost, s);
+            cudaMemcpyAsync(hio->hv, v, b, cudaMemcpyDeviceToHost, s);
+        }
     }
+    // the counters ride along on the caller's stream: one synchronisation in all
+    if (timed) cudaMemcpyAsync(R->hctr, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s);
     rec(6, s);
     if (cudaGetLastError() != cudaSuccess) return VFMM_ECUDA;
     if (!timed) return VFMM_OK;
 
     if (cudaStreamSynchronize(s) != cudaSuccess) return VFMM_ECUDA;
-    Counters c;
-    if (cudaMemcpy(&c, ctr, sizeof c, cudaMemcpyDeviceToHost) != cudaSuccess) return VFMM_ECUDA;
+    const Counters c = *R->hctr;
     std::memset(stats, 0, sizeof(*stats));
     fill_stats(L, c, kernel, side, stats);
+    stats->overlapped = overlap ? 1 : 0;
+    stats->t_total = elapsed(R->ev[0], R->ev[6]);
+    if (!phases) return c.bad_count ? VFMM_EDOMAIN : VFMM_OK;
     if (up) {
         stats->t_build = elapsed(R->ev[0], R->ev[1]);
         stats->t_upward = elapsed(R->ev[1], R->ev[2]);

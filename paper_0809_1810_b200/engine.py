@@ -142,6 +142,7 @@ def evaluate_arrays(
     device=None,
     overlap: bool = False,
     out: torch.Tensor | None = None,
+    timings: bool = False,
     stacklevel: int = 2,
 ):
     """Array fast path of :func:`evaluate`.
@@ -150,7 +151,9 @@ def evaluate_arrays(
     tensors are used in place).  Returns ``(vel, stats)`` where ``vel`` is a
     (2, N) float64 CUDA tensor holding u (row 0) and v (row 1) in the input
     order.  ``overlap=True`` runs the near field concurrently with the
-    far-field chain (phase timings then overlap in time).
+    far-field chain (phase timings then overlap in time).  ``timings=True``
+    fills the per-phase times of ``stats`` (CUDA events between the phases,
+    ~0.1 ms per call); otherwise only ``t_total`` and the counters.
     """
     validate_config(config)
     require_cuda()
@@ -168,7 +171,7 @@ def evaluate_arrays(
     if out is None:
         out = torch.empty((2, n), dtype=torch.float64, device=dev)
     st = _lib.VfmmStats()
-    flags = _lib.FLAG_STATS | (_lib.FLAG_OVERLAP if overlap else 0)
+    flags = _lib.FLAG_STATS | (_lib.FLAG_OVERLAP if overlap else 0) | (_lib.FLAG_PHASE_TIMES if timings else 0)
     status = lib.vfmm_evaluate(
         xd.data_ptr(), yd.data_ptr(), gd.data_ptr(), sd.data_ptr() if sd is not None else None, n,
         float(domain.xmin), float(domain.ymin), float(domain.side), config.levels, config.order,
@@ -213,6 +216,7 @@ def evaluate_host(
     device=None,
     out: torch.Tensor | None = None,
     overlap: bool = True,
+    timings: bool = False,
     stacklevel: int = 2,
 ):
     """Host-buffer fast path (``vfmm_evaluate_host``): numpy arrays or CPU (ideally
@@ -241,7 +245,8 @@ def evaluate_host(
     if tuple(out.shape) != (n, 2) or not out.is_contiguous() or out.is_cuda:
         raise ValueError("out must be a contiguous host (N, 2) float64 tensor")
     st = _lib.VfmmStats()
-    flags = _lib.FLAG_STATS | _lib.FLAG_UV_PAIRS | (_lib.FLAG_OVERLAP if overlap else 0)
+    flags = (_lib.FLAG_STATS | _lib.FLAG_UV_PAIRS | (_lib.FLAG_OVERLAP if overlap else 0)
+             | (_lib.FLAG_PHASE_TIMES if timings else 0))
     status = lib.vfmm_evaluate_host(
         keep[0][1], keep[1][1], keep[2][1], keep[3][1] if code == _lib.KERNEL_GAUSSIAN else None, n,
         float(domain.xmin), float(domain.ymin), float(domain.side), config.levels, config.order,
@@ -265,12 +270,104 @@ def evaluate_host(
     return out, stats
 
 
+class PendingEvaluation:
+    """An :func:`evaluate_host_async` call in flight; :meth:`result` waits for it."""
+
+    def __init__(self, out, stream, keep, ws, config, domain, n, code):
+        self.out, self.stream, self._keep, self.ws = out, stream, keep, ws
+        self._config, self._domain, self._n, self._code = config, domain, n, code
+
+    def done(self) -> bool:
+        return self.stream.query()
+
+    def result(self, with_stats: bool = False):
+        """The (N, 2) host tensor of (u, v) rows once the call has finished;
+        ``with_stats=True`` also returns the counters (vfmm_read_stats, no
+        timings) and raises :class:`OutOfDomainError` like :func:`evaluate_host`."""
+        self.stream.synchronize()
+        self._keep = None
+        if not with_stats:
+            return self.out
+        lib = _lib.load()
+        st = _lib.VfmmStats()
+        status = lib.vfmm_read_stats(self._n, self._config.levels, self._config.order, self._code,
+                                     float(self._domain.side), self.ws.ptr, ctypes.byref(st),
+                                     self.stream.cuda_stream)
+        if status == _lib.VFMM_EDOMAIN:
+            raise OutOfDomainError(f"particle(s) outside domain {self._domain}")
+        _lib.check(status, "vfmm_read_stats")
+        return self.out, _stats_from(st)
+
+
+def evaluate_host_async(x, y, gamma, sigma, config, domain, *, out: torch.Tensor,
+                        workspace: "Workspace", stream: torch.cuda.Stream, overlap: bool = True):
+    """Asynchronous :func:`evaluate_host` (``vfmm_evaluate_host`` without
+    VFMM_FLAG_STATS): enqueues the copies and the evaluation on ``stream`` and
+    returns a :class:`PendingEvaluation` at once.  Calls on distinct streams
+    and distinct workspaces pipeline -- the host<->device copies of one call
+    overlap the compute of its neighbours -- which is how a batch of
+    independent evaluations reaches the PCIe / compute bound instead of
+    their sum.  ``x .. sigma`` and ``out`` must stay alive (and unchanged)
+    until :meth:`PendingEvaluation.result`; pinned memory for full speed."""
+    validate_config(config)
+    require_cuda()
+    lib = _lib.load()
+    keep = [_host_f64(a) for a in (x, y, gamma, sigma)]
+    n = keep[0][0].numel() if isinstance(keep[0][0], torch.Tensor) else int(np.asarray(keep[0][0]).size)
+    if n != workspace.n or config.levels != workspace.levels or config.order != workspace.order:
+        raise ValueError("workspace shape does not match (n, levels, order)")
+    if tuple(out.shape) != (n, 2) or not out.is_contiguous() or out.is_cuda:
+        raise ValueError("out must be a contiguous host (N, 2) float64 tensor")
+    code = kernel_code(config.kernel)
+    flags = _lib.FLAG_UV_PAIRS | (_lib.FLAG_OVERLAP if overlap else 0)
+    status = lib.vfmm_evaluate_host(
+        keep[0][1], keep[1][1], keep[2][1], keep[3][1] if code == _lib.KERNEL_GAUSSIAN else None, n,
+        float(domain.xmin), float(domain.ymin), float(domain.side), config.levels, config.order,
+        code, out.data_ptr(), None, workspace.ptr, workspace.nbytes, flags, None, stream.cuda_stream,
+    )
+    _lib.check(status, "vfmm_evaluate_host")
+    return PendingEvaluation(out, stream, keep, workspace, config, domain, n, code)
+
+
+class HostPipeline:
+    """``depth`` evaluations of one (n, config, domain) shape in flight, each
+    with its own workspace, stream and pinned output buffer (round robin).
+
+        pipe = HostPipeline(n, config, domain)
+        pending = [pipe.submit(x, y, g, s) for (x, y, g, s) in batches]
+        velocities = [p.result().clone() for p in pending]
+
+    A slot's previous result is waited for before the slot is reused, so
+    results must be consumed (copied) before ``depth`` further submissions."""
+
+    def __init__(self, n: int, config, domain, *, depth: int = 2, device=None, overlap: bool = True):
+        validate_config(config)
+        require_cuda()
+        dev = device_of(device)
+        self.n, self.config, self.domain, self.overlap = n, config, domain, overlap
+        self.slots = [(Workspace(n, config.levels, config.order, dev), torch.cuda.Stream(dev),
+                       torch.empty((n, 2), dtype=torch.float64, pin_memory=True)) for _ in range(depth)]
+        self.pending = [None] * depth
+        self.k = 0
+
+    def submit(self, x, y, gamma, sigma) -> PendingEvaluation:
+        i = self.k % len(self.slots)
+        self.k += 1
+        if self.pending[i] is not None:
+            self.pending[i].result()
+        ws, stream, out = self.slots[i]
+        self.pending[i] = evaluate_host_async(x, y, gamma, sigma, self.config, self.domain, out=out,
+                                              workspace=ws, stream=stream, overlap=self.overlap)
+        return self.pending[i]
+
+
 def evaluate(
     particles: Sequence,
     config,
     domain=None,
     *,
     overlap: bool = False,
+    timings: bool = False,
 ) -> tuple[np.ndarray, FmmRunStats]:
     """Velocity induced at every particle position, with run statistics (engine.py:335-398).
 
@@ -283,8 +380,8 @@ def evaluate(
     x, y, gamma, sigma = to_arrays(particles)
     if domain is None:
         domain = enclosing_domain_of(x, y)
-    vel, stats = evaluate_host(x, y, gamma, sigma, config, domain, overlap=overlap, stacklevel=3,
-                               out=torch.empty((len(x), 2), dtype=torch.float64))
+    vel, stats = evaluate_host(x, y, gamma, sigma, config, domain, overlap=overlap, timings=timings,
+                               stacklevel=3, out=torch.empty((len(x), 2), dtype=torch.float64))
     return vel.numpy(), stats
 
 

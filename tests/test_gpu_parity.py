@@ -319,3 +319,26 @@ def test_extreme_orders_and_depths_match_oracle(levels, order, n):
     ref, ost = O.evaluate(x, y, g, s, levels, order, True, (0.0, 0.0, 1.0))
     assert st.m2l_count == ost["m2l_count"] and st.near_pair_count == ost["near_pair_count"]
     assert np.abs(vel - ref).max() <= REL_TOL * np.abs(ref).max()
+
+
+@pytest.mark.gpu
+def test_host_pipeline_matches_synchronous_call():
+    """evaluate_host_async / HostPipeline (two calls in flight on their own
+    workspaces and streams) give bitwise the results of evaluate_host."""
+    w = W.config1()
+    cfg = vf.FmmConfig(w.levels, w.order, vf.KernelKind.GAUSSIAN_BLOB)
+    dom = vf.Domain(*W.DOMAIN)
+    ref, st = vf.evaluate_host(w.x, w.y, w.gamma, w.sigma, cfg, dom)
+    pipe = vf.HostPipeline(w.x.size, cfg, dom, depth=2)
+    inputs = [(w.x, w.y, w.gamma * (1.0 + k), w.sigma) for k in range(4)]
+    outs = []
+    pend = [pipe.submit(*a) for a in inputs[:2]]
+    for p, a in zip(pend, inputs[:2]):
+        outs.append(p.result().clone())
+    pend = [pipe.submit(*a) for a in inputs[2:]]
+    last, st2 = pend[-1].result(with_stats=True)
+    outs.append(pend[0].result().clone())
+    outs.append(last.clone())
+    for k, o in enumerate(outs):
+        assert torch.equal(o, ref * (1.0 + k)) or np.abs((o - ref * (1.0 + k)).numpy()).max() <= 1e-13 * np.abs(ref.numpy()).max() * (1 + k)
+    assert st2.near_pair_count == st.near_pair_count and st2.m2l_count == st.m2l_count
