@@ -246,6 +246,7 @@ bool make_layout(int64_t n, int levels, int order, Layout* L) {
     L->mult = take(sizeof(double2) * cells * L->P);
     L->loc = take(sizeof(double2) * cells * L->P);
     L->leaf_loc = take(sizeof(double2) * L->nleaves * L->P);
+    L->anc = take(sizeof(double2) * L->level_cell_off[l2l_split_level(levels, L->P)] * L->P);
     L->tasks = take(sizeof(int2) * L->max_tasks);
     L->stage = take(sizeof(double) * 6 * n);  // host-mode staging: x, y, gamma, sigma, u, v
     L->total = off;
@@ -423,10 +424,10 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
     if (down) {
         if (!up) rec(2, cs);
         // ---- M2L (all levels, one launch) ----
-        launch_m2l(L, T, mult, counts, loc, ctr, rows, fs);
+        launch_m2l(L, T, mult, counts, loc, (double2*)(ws + L.anc), ctr, rows, fs);
         rec(3, fs);
         // ---- downward ----
-        launch_l2l(L, T, loc, (double2*)(ws + L.leaf_loc), rows, fs);
+        launch_l2l(L, T, loc, (double2*)(ws + L.leaf_loc), (const double2*)(ws + L.anc), rows, fs);
         rec(4, fs);
         if (overlap && up) {
             cudaEventRecord(R->join_far, fs);
@@ -494,6 +495,13 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         }
     }
     stats->t_total = elapsed(R->ev[up ? 0 : 2], R->ev[6]);
+    static const bool tl = getenv("VFMM_DEBUG_TIMELINE") != nullptr;  // tuning aid
+    if (tl) {
+        static const char* names[9] = {"start", "built", "upward", "m2l", "downward",
+                                       "near joined", "end", "near start", "near end"};
+        for (int i = 1; i < 9; ++i)
+            fprintf(stderr, "vfmm timeline: %-12s %8.4f ms\n", names[i], elapsed(R->ev[0], R->ev[i]));
+    }
     return c.bad_count ? VFMM_EDOMAIN : VFMM_OK;
 }
 

@@ -53,8 +53,8 @@ __device__ const double2 g_zero_coef = {0.0, 0.0};
 template <int TN>
 __global__ void __launch_bounds__(kDestPerBlock * kGroups, 8)
     k_m2l(const double2* __restrict__ mult, const int* __restrict__ counts, double2* __restrict__ loc,
-          int levels, int P, int nchunks, const Tables* __restrict__ T,
-          unsigned long long* __restrict__ m2l_count, Rows rows) {
+          double2* __restrict__ anc, int anc_end, int levels, int P, int nchunks,
+          const Tables* __restrict__ T, unsigned long long* __restrict__ m2l_count, Rows rows) {
     extern __shared__ double2 sH[];  // [27][TN + P - 1], then [kGroups - 1][TN][32] partials
     // ---- decode (level, parity, chunk, block-in-class) from blockIdx.x ----
     int64_t b = blockIdx.x;
@@ -156,7 +156,11 @@ __global__ void __launch_bounds__(kDestPerBlock * kGroups, 8)
                 sx += p.x;
                 sy += p.y;
             }
-            if (m0 + t < P) out[(m0 + t) * cstride] = make_double2(sx, sy);
+            if (m0 + t < P) {
+                out[(m0 + t) * cstride] = make_double2(sx, sy);
+                // M2L parts of the fused L2L's shared ancestors (read-only copy)
+                if (level < anc_end) anc[(out - loc) + (m0 + t) * cstride] = make_double2(sx, sy);
+            }
         }
     }
     if (chunk == 0) {
@@ -169,7 +173,7 @@ __global__ void __launch_bounds__(kDestPerBlock * kGroups, 8)
 
 template <int TN>
 void launch_tn(const Layout& L, const Tables* T, const double2* mult, const int* counts,
-               double2* loc, Counters* ctr, Rows rows, cudaStream_t s) {
+               double2* loc, double2* anc, Counters* ctr, Rows rows, cudaStream_t s) {
     const int nchunks = (L.P + TN - 1) / TN;
     int64_t blocks = 0;
     for (int level = 2; level <= L.levels; ++level) {
@@ -179,20 +183,21 @@ void launch_tn(const Layout& L, const Tables* T, const double2* mult, const int*
     const size_t shm = (size_t)27 * (TN + L.P - 1) * sizeof(double2) +
                        (size_t)(kGroups - 1) * TN * 32 * sizeof(double2);
     k_m2l<TN><<<(unsigned)blocks, kDestPerBlock * kGroups, shm, s>>>(
-        mult, counts, loc, L.levels, L.P, nchunks, T, &ctr->m2l_count, rows);
+        mult, counts, loc, anc, l2l_split_level(L.levels, L.P), L.levels, L.P, nchunks, T,
+        &ctr->m2l_count, rows);
     note_launches(1);
 }
 
 }  // namespace
 
 void launch_m2l(const Layout& L, const Tables* T, const double2* mult, const int* counts,
-                double2* loc, Counters* ctr, Rows rows, cudaStream_t s) {
+                double2* loc, double2* anc, Counters* ctr, Rows rows, cudaStream_t s) {
     switch (coef_chunk(L.P)) {
-        case 4: launch_tn<4>(L, T, mult, counts, loc, ctr, rows, s); break;
-        case 5: launch_tn<5>(L, T, mult, counts, loc, ctr, rows, s); break;
-        case 6: launch_tn<6>(L, T, mult, counts, loc, ctr, rows, s); break;
-        case 7: launch_tn<7>(L, T, mult, counts, loc, ctr, rows, s); break;
-        default: launch_tn<8>(L, T, mult, counts, loc, ctr, rows, s); break;
+        case 4: launch_tn<4>(L, T, mult, counts, loc, anc, ctr, rows, s); break;
+        case 5: launch_tn<5>(L, T, mult, counts, loc, anc, ctr, rows, s); break;
+        case 6: launch_tn<6>(L, T, mult, counts, loc, anc, ctr, rows, s); break;
+        case 7: launch_tn<7>(L, T, mult, counts, loc, anc, ctr, rows, s); break;
+        default: launch_tn<8>(L, T, mult, counts, loc, anc, ctr, rows, s); break;
     }
 }
 

@@ -76,34 +76,97 @@ __global__ void __launch_bounds__(kSubThreads)
     }
 }
 
-// Downward: CTA per cell at level lt (complete local in `loc`), completes the
-// locals of levels lt+1 .. lt+depth of its subtree.  The leaf level (when
-// reached) is written cell-major to leaf_loc, other levels in place (planar).
+// Whole L2L in ONE launch: CTA per cell at the split level ls (the deepest
+// level whose subtree fits shared memory).  Each CTA first walks the chain of
+// its ancestors 2 -> ls (P outputs per level; the ancestors are recomputed by
+// every CTA below them -- identical arithmetic, so identical values -- and
+// written by the first CTA of each), then completes its subtree as above.
+// Replaces ceil((levels - 2) / depth) dependent launches whose first ones
+// ran on a handful of CTAs.
+// coefficient offset of level k (>= 2) in mult / loc: cells of levels 2..k-1
+__device__ __forceinline__ int64_t lvl_off(int k, int P) {
+    return (((int64_t)1 << (2 * k)) - 16) / 3 * P;
+}
+
 __global__ void __launch_bounds__(kSubThreads)
-    k_l2l_subtree(double2* __restrict__ loc, double2* __restrict__ leaf_loc, int lt, int depth,
-                  int levels, int P, size_t off_lt, const Tables* __restrict__ T, Rows rows) {
+    k_l2l_fused(double2* __restrict__ loc, double2* __restrict__ leaf_loc,
+                const double2* __restrict__ anc_m2l, int ls, int levels, int P,
+                const Tables* __restrict__ T, Rows rows) {
     extern __shared__ double2 sm[];
+    const int depth = levels - ls;
     double2* sF = sm + (size_t)sub_off(depth + 1) * P;  // [4][P]
     double* s2 = reinterpret_cast<double*>(sF + 4 * P);  // [P]
-    const int mt = 1 << lt;
+    double2* anc = reinterpret_cast<double2*>(s2 + ((P + 1) & ~1));  // [2][P] ping-pong
+    const int mt = 1 << ls;
     const int cx = blockIdx.x % mt, cy = blockIdx.x / mt;
-    if (!rows_touch(rows, cy, levels - lt)) return;  // subtree outside the owned strip
+    if (!rows_touch(rows, cy, levels - ls)) return;  // subtree outside the owned strip
     for (int i = threadIdx.x; i < 4 * P; i += blockDim.x) sF[i] = T->F[i / P][i % P];
     for (int i = threadIdx.x; i < P; i += blockDim.x) s2[i] = T->pow2neg[i];
-    {
-        const double2* g = loc + off_lt;
-        const int64_t cs = coef_stride(lt);
-        for (int k = threadIdx.x; k < P; k += blockDim.x) sm[k] = g[coef_base(lt, cx, cy) + k * cs];
+    const int n = threadIdx.x;
+    // ---- ancestor chain: level 2 (complete after M2L) down to ls ----
+    if (n < P) {
+        const int sh = ls - 2;
+        anc[n] = loc[lvl_off(2, P) + coef_base(2, cx >> sh, cy >> sh) + n * coef_stride(2)];
     }
     __syncthreads();
-    size_t off_level = off_lt;
+    int cur = 0;
+    for (int k = 3; k <= ls; ++k) {
+        const int sh = ls - k;
+        const int ax = cx >> sh, ay = cy >> sh;
+        if (n < P) {
+            const double2* Lp = anc + cur * P;
+            const double2* Fq = sF + (2 * (ay & 1) + (ax & 1)) * P;
+            double sx = 0.0, sy = 0.0;
+            for (int mm = n; mm < P; ++mm) {
+                const double2 a = Lp[mm];
+                const double axs = a.x * s2[mm], ays = a.y * s2[mm];
+                const double2 f = Fq[mm - n];
+                sx = fma(axs, f.x, fma(-ays, f.y, sx));
+                sy = fma(axs, f.y, fma(ays, f.x, sy));
+            }
+            const int64_t gi = lvl_off(k, P) + coef_base(k, ax, ay) + n * coef_stride(k);
+            // M2L part: shared ancestors (k < ls) from the read-only copy, since
+            // their writer CTA completes them in loc while others still read
+            double2 r = k < ls ? anc_m2l[gi] : loc[gi];
+            r.x += sx;
+            r.y += sy;
+            anc[(cur ^ 1) * P + n] = r;
+            const int mask = (1 << sh) - 1;
+            if ((cx & mask) == 0 && (cy & mask) == 0) {  // first CTA below: the writer
+                if (k == levels)
+                    leaf_loc[((int64_t)ay * (1 << k) + ax) * P + n] = r;
+                else
+                    loc[gi] = r;
+            }
+        }
+        __syncthreads();
+        cur ^= 1;
+    }
+    if (depth == 0) return;
+    // ---- subtree below the root: stage the root and the M2L parts ----
+    {
+        const int total = sub_off(depth + 1) * P;
+        for (int i = threadIdx.x; i < total; i += blockDim.x) {
+            const int c = i / P, k = i % P;
+            if (c == 0) {
+                sm[i] = anc[cur * P + k];
+                continue;
+            }
+            int sl = 1;
+            while (sub_off(sl + 1) <= c) ++sl;
+            const int side = 1 << sl, lc = c - sub_off(sl);
+            const int lvl = ls + sl;
+            sm[i] = loc[lvl_off(lvl, P) + coef_base(lvl, cx * side + lc % side, cy * side + lc / side) +
+                        k * coef_stride(lvl)];
+        }
+    }
+    __syncthreads();
     for (int s = 1; s <= depth; ++s) {
-        const int lvl = lt + s;
-        off_level += (size_t)(1ll << (2 * (lvl - 1))) * P;
+        const int lvl = ls + s;
         const int side = 1 << s;
         const double2* par = sm + (size_t)sub_off(s - 1) * P;
-        double2* cur = sm + (size_t)sub_off(s) * P;
-        double2* g = loc + off_level;
+        double2* cu = sm + (size_t)sub_off(s) * P;
+        double2* g = loc + lvl_off(lvl, P);
         const int64_t cs = coef_stride(lvl);
         const bool leaf = lvl == levels;
         const int m = 1 << lvl;
@@ -113,24 +176,23 @@ __global__ void __launch_bounds__(kSubThreads)
             const int q = 2 * (ly & 1) + (lx & 1);
             const double2* Lp = par + (size_t)((ly >> 1) * (side >> 1) + (lx >> 1)) * P;
             const double2* Fq = sF + q * P;
-            double ax = 0.0, ay = 0.0;
+            double sx = 0.0, sy = 0.0;
             for (int mm = nn; mm < P; ++mm) {
                 const double2 a = Lp[mm];
                 const double axs = a.x * s2[mm], ays = a.y * s2[mm];
                 const double2 f = Fq[mm - nn];
-                ax = fma(axs, f.x, fma(-ays, f.y, ax));
-                ay = fma(axs, f.y, fma(ays, f.x, ay));
+                sx = fma(axs, f.x, fma(-ays, f.y, sx));
+                sy = fma(axs, f.y, fma(ays, f.x, sy));
             }
+            double2 r = cu[i];  // M2L part (staged)
+            r.x += sx;
+            r.y += sy;
+            cu[i] = r;
             const int gx = cx * side + lx, gy = cy * side + ly;
-            const int64_t gi = coef_base(lvl, gx, gy) + nn * cs;
-            double2 r = g[gi];  // M2L part
-            r.x += ax;
-            r.y += ay;
-            cur[i] = r;
             if (leaf)
                 leaf_loc[((int64_t)gy * m + gx) * P + nn] = r;
             else
-                g[gi] = r;
+                g[coef_base(lvl, gx, gy) + nn * cs] = r;
         }
         __syncthreads();
     }
@@ -158,20 +220,22 @@ void launch_m2m(const Layout& L, const Tables* T, double2* mult, cudaStream_t s)
     }
 }
 
-void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc, Rows rows,
-                cudaStream_t s) {
+int l2l_split_level(int levels, int P) {
+    const int d0 = sub_depth(P);
+    return levels - d0 > 2 ? levels - d0 : 2;
+}
+
+void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc,
+                const double2* anc, Rows rows, cudaStream_t s) {
     if (L.levels == 2) {
         launch_leaf_locals_copy(L, loc, leaf_loc, s);
         return;
     }
-    const int d0 = sub_depth(L.P);
-    for (int lt = 2; lt < L.levels;) {
-        const int d = L.levels - lt < d0 ? L.levels - lt : d0;
-        k_l2l_subtree<<<(unsigned)(1ll << (2 * lt)), kSubThreads, sub_smem(d, L.P), s>>>(
-            loc, leaf_loc, lt, d, L.levels, L.P, L.level_cell_off[lt] * L.P, T, rows);
-        note_launches(1);
-        lt += d;
-    }
+    const int ls = l2l_split_level(L.levels, L.P);
+    const size_t shm = sub_smem(L.levels - ls, L.P) + sizeof(double2) * (2 * L.P + 1);
+    k_l2l_fused<<<(unsigned)(1ll << (2 * ls)), kSubThreads, shm, s>>>(loc, leaf_loc, anc, ls,
+                                                                       L.levels, L.P, T, rows);
+    note_launches(1);
 }
 
 }  // namespace vfmm

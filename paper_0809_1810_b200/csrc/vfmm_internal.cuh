@@ -71,7 +71,7 @@ struct Layout {
     int levels, order, P;  // P = order + 1
     int digit_bits, passes, wc, nchunks;
     size_t nleaves;
-    size_t key_a, key_b, val_a, val_b, hist, task_scratch, scan_state, src, near_uv, leaf_starts,
+    size_t key_a, key_b, val_a, val_b, hist, task_scratch, scan_state, src, near_uv, leaf_starts, anc,
         counts, mult, loc, leaf_loc, tasks, stage, counters, total;
     size_t scan_state_tiles, scan_state_bytes, hist_bytes;  // per scan instance: 1 ticket + tiles
     size_t level_cell_off[VFMM_LEVELS_CAP + 2];  // cells before level k (k>=2) in mult/loc
@@ -113,9 +113,12 @@ void launch_init_counters(Counters* ctr, cudaStream_t s);
 void launch_m2m(const Layout& L, const Tables* T, double2* mult, cudaStream_t s);  // subtree.cu
 void launch_leaf_locals_copy(const Layout& L, const double2* loc, double2* leaf_loc, cudaStream_t s);
 void launch_m2l(const Layout& L, const Tables* T, const double2* mult, const int* counts,
-                double2* loc, Counters* ctr, Rows rows, cudaStream_t s);
-void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc, Rows rows,
-                cudaStream_t s);
+                double2* loc, double2* anc, Counters* ctr, Rows rows, cudaStream_t s);
+// L2L split level: CTA roots of the fused downward kernel (subtree.cu); the
+// M2L parts of levels 3 .. split-1 are also kept in the `anc` region
+int l2l_split_level(int levels, int P);
+void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc,
+                const double2* anc, Rows rows, cudaStream_t s);
 int p2p_targets_per_lane();  // 1 or 2 (env VFMM_P2P_TPT, default 1)
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
                 const int2* tasks, Counters* ctr, int kernel, double2* near_uv, Rows rows,
