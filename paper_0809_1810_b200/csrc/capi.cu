@@ -360,6 +360,10 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
     int* perm = (int*)(ws + (odd ? L.val_b : L.val_a));
     // per-phase events only on request; plain stats time the whole call (ev 0 -> 6)
     const bool phases = timed && (flags & VFMM_FLAG_PHASE_TIMES) != 0;
+    auto near_field = [&](cudaStream_t st) {  // P2P, then the per-particle near total
+        launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, rows, st);
+        launch_near_sum(L, keys, near_uv, rows, ls, ctr, kernel, st);
+    };
     auto rec = [&](int i, cudaStream_t st) {
         if (phases || (timed && (i == 0 || i == 6))) cudaEventRecord(R->ev[i], st);
     };
@@ -411,7 +415,7 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         }
         if (overlap && !down) {  // sharded PHASE_UP: start the near field now
             rec(7, R->near);
-            launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, rows, R->near);
+            near_field(R->near);
             rec(8, R->near);
             cudaEventRecord(R->join_near, R->near);
             fs = cs;  // the far chain stays on the caller's stream (the all-reduce follows it)
@@ -432,7 +436,7 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         if (overlap && up) {
             cudaEventRecord(R->join_far, fs);
             rec(7, R->near);
-            launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, rows, R->near);
+            near_field(R->near);
             rec(8, R->near);
             cudaEventRecord(R->join_near, R->near);
             cudaStreamWaitEvent(cs, R->join_far, 0);
@@ -441,10 +445,10 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
             cudaStreamWaitEvent(cs, R->join_near, 0);
         }
         if (!far_only) {
-            if (!overlap) launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, rows, cs);
+            if (!overlap) near_field(cs);
             rec(5, cs);
             launch_l2p_combine(L, T, src, keys, perm, (const double2*)(ws + L.leaf_loc), near_uv,
-                               xmin, ymin, side, u, v, rows, ls, ctr, kernel, cs);
+                               xmin, ymin, side, u, v, rows, cs);
         }
     }
     if (hio) {

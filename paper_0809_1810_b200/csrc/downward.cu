@@ -42,29 +42,23 @@ __device__ __forceinline__ double2 eval_local(const double2* __restrict__ Lh, in
     return make_double2(ax, ay);
 }
 
+// Near-field total per particle, in place in slot 0, right after the near
+// field (on its stream, so it overlaps the far-field chain): symmetric
+// kernel -- slot 0 (the leaf's own blocks) + the reactions of the existing
+// backward neighbours in kind order; generic kernel -- the three
+// neighbourhood-row partial sums in row order.
 __global__ void __launch_bounds__(256)
-    k_l2p_combine(const Src* __restrict__ src, const int* __restrict__ keys,
-                  const int* __restrict__ perm, const double2* __restrict__ loc,
-                  const double2* __restrict__ near_uv, int64_t n, int levels, int P, double xmin,
-                  double ymin, double side, const Tables* __restrict__ T, double* __restrict__ u,
-                  double* __restrict__ v, Rows rows, const int* __restrict__ ls,
-                  const Counters* __restrict__ ctr, bool gauss, int sym_enabled) {
-    __shared__ double sfact[kOrderCap + 16];
-    for (int i = threadIdx.x; i < P; i += blockDim.x) sfact[i] = T->invfact[i];
-    __syncthreads();
+    k_near_sum(const int* __restrict__ keys, double2* __restrict__ near_uv, int64_t n, int levels,
+               Rows rows, const int* __restrict__ ls, const Counters* __restrict__ ctr, bool gauss,
+               int sym_enabled) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int m = 1 << levels;
     const int leaf = keys[i];
     const int ix = leaf % m, iy = leaf / m;
     if (iy < rows.lo || iy >= rows.hi) return;  // halo particle of a sharded run
-    const double r = side / m;
-    const double cx = cell_center(xmin, ix, r), cy = cell_center(ymin, iy, r);
-    const double inv_r = 1.0 / r;
-    double2 nv = make_double2(0.0, 0.0);
+    double2 nv;
     if (sym_enabled && p2p_symmetric(ctr, gauss)) {
-        // symmetric kernel: slot 0 = the leaf's own blocks (self + forward),
-        // slots 1..4 = reactions from the backward neighbours, in kind order
         double2 t[kNearSlots];
 #pragma unroll
         for (int k = 0; k < kNearSlots; ++k) t[k] = near_uv[(int64_t)k * n + i];
@@ -80,10 +74,32 @@ __global__ void __launch_bounds__(256)
             }
         }
     } else {
-        // generic kernel: the three neighbourhood-row partial sums, in row order
         const double2 n0 = near_uv[i], n1 = near_uv[n + i], n2 = near_uv[2 * n + i];
         nv = make_double2((n0.x + n1.x) + n2.x, (n0.y + n1.y) + n2.y);
     }
+    near_uv[i] = nv;
+}
+
+// Far field (L2P) + the near total, un-permuted to the caller's order.
+__global__ void __launch_bounds__(256)
+    k_l2p_combine(const Src* __restrict__ src, const int* __restrict__ keys,
+                  const int* __restrict__ perm, const double2* __restrict__ loc,
+                  const double2* __restrict__ near_uv, int64_t n, int levels, int P, double xmin,
+                  double ymin, double side, const Tables* __restrict__ T, double* __restrict__ u,
+                  double* __restrict__ v, Rows rows) {
+    __shared__ double sfact[kOrderCap + 16];
+    for (int i = threadIdx.x; i < P; i += blockDim.x) sfact[i] = T->invfact[i];
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int m = 1 << levels;
+    const int leaf = keys[i];
+    const int ix = leaf % m, iy = leaf / m;
+    if (iy < rows.lo || iy >= rows.hi) return;  // halo particle of a sharded run
+    const double r = side / m;
+    const double cx = cell_center(xmin, ix, r), cy = cell_center(ymin, iy, r);
+    const double inv_r = 1.0 / r;
+    const double2 nv = near_uv[i];
     const Src s = src[i];
     const double2 f =
         eval_local(loc + (int64_t)leaf * P, 1, P, (s.x - cx) * inv_r, (s.y - cy) * inv_r, sfact);
@@ -157,11 +173,17 @@ void launch_leaf_locals_copy(const Layout& L, const double2* loc, double2* leaf_
 void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const int* keys,
                         const int* perm, const double2* loc, const double2* near_uv, double xmin,
                         double ymin, double side, double* u, double* v, Rows rows,
-                        const int* leaf_starts, const Counters* ctr, int kernel, cudaStream_t s) {
-    const double2* leaf_loc = loc;
+                        cudaStream_t s) {
     k_l2p_combine<<<(unsigned)((L.n + 255) / 256), 256, 0, s>>>(
-        src, keys, perm, leaf_loc, near_uv, L.n, L.levels, L.P, xmin, ymin, side, T, u, v, rows,
-        leaf_starts, ctr, kernel == VFMM_KERNEL_GAUSSIAN, sym_disabled() ? 0 : 1);
+        src, keys, perm, loc, near_uv, L.n, L.levels, L.P, xmin, ymin, side, T, u, v, rows);
+    note_launches(1);
+}
+
+void launch_near_sum(const Layout& L, const int* keys, double2* near_uv, Rows rows,
+                     const int* leaf_starts, const Counters* ctr, int kernel, cudaStream_t s) {
+    k_near_sum<<<(unsigned)((L.n + 255) / 256), 256, 0, s>>>(
+        keys, near_uv, L.n, L.levels, rows, leaf_starts, ctr, kernel == VFMM_KERNEL_GAUSSIAN,
+        sym_disabled() ? 0 : 1);
     note_launches(1);
 }
 

@@ -127,7 +127,10 @@ bool sym_disabled();  // env VFMM_P2P_SYM=0 forces the generic near-field kernel
 void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const int* keys,
                         const int* perm, const double2* loc, const double2* near_uv, double xmin,
                         double ymin, double side, double* u, double* v, Rows rows,
-                        const int* leaf_starts, const Counters* ctr, int kernel, cudaStream_t s);
+                        cudaStream_t s);
+// near-field total per particle into slot 0 (after the near-field kernels)
+void launch_near_sum(const Layout& L, const int* keys, double2* near_uv, Rows rows,
+                     const int* leaf_starts, const Counters* ctr, int kernel, cudaStream_t s);
 void launch_eval_at(const Layout& L, const Tables* T, const double* tx, const double* ty,
                     int64_t m, const Src* src, const int* leaf_starts, const double2* loc,
                     double xmin, double ymin, double side, int kernel, double* u, double* v,

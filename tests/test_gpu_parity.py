@@ -132,24 +132,10 @@ def _symmetric_mode(c, n):
 
 
 def _near_from_slots(ws, c, n):
-    lv = c["levels"]
-    m = 2**lv
-    if not _symmetric_mode(c, n):
-        rows = ws.view("near_uv", torch.float64, 6 * n).cpu().numpy().reshape(3, n, 2)
-        return (rows[0] + rows[1]) + rows[2]
-    slots = ws.view("near_uv", torch.float64, 10 * n).cpu().numpy().reshape(5, n, 2)
-    keys = ws.view("leaf_key", torch.int32, n).cpu().numpy()
-    ls = ws.view("leaf_starts", torch.int32, 4**lv + 1).cpu().numpy()
-    occ = np.diff(ls) > 0
-    iy, ix = keys // m, keys % m
-    # slot 0: the leaf's own blocks; slot k: reaction from the leaf at offset -d_k
-    near = slots[0].copy()
-    for k, (dx, dy) in enumerate([(1, 0), (-1, 1), (0, 1), (1, 1)], start=1):
-        ax, ay = ix - dx, iy - dy
-        ok = (ax >= 0) & (ax < m) & (ay >= 0) & (ay < m)
-        ok[ok] &= occ[(ay * m + ax)[ok]]
-        near[ok] += slots[k][ok]
-    return near
+    """After an evaluate, slot 0 of near_uv holds each particle's complete near
+    field (k_near_sum: own-leaf sums + backward reactions, or the three row
+    partial sums), in sorted order."""
+    return ws.view("near_uv", torch.float64, 2 * n).cpu().numpy().reshape(n, 2).copy()
 
 
 @pytest.mark.parametrize("name", ["config0", "config1", "coincident", "big_leaf_l3", "point_kernel_l5"])
