@@ -354,14 +354,13 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
     double2* mult = (double2*)(ws + L.mult);
     double2* loc = (double2*)(ws + L.loc);
     double2* near_uv = (double2*)(ws + L.near_uv);
-    int2* tasks = (int2*)(ws + L.tasks);
     const bool odd = (L.passes & 1) != 0;
     int* keys = (int*)(ws + (odd ? L.key_b : L.key_a));
     int* perm = (int*)(ws + (odd ? L.val_b : L.val_a));
     // per-phase events only on request; plain stats time the whole call (ev 0 -> 6)
     const bool phases = timed && (flags & VFMM_FLAG_PHASE_TIMES) != 0;
     auto near_field = [&](cudaStream_t st) {  // P2P, then the per-particle near total
-        launch_p2p(L, T, src, ls, tasks, ctr, kernel, near_uv, rows, st);
+        launch_p2p(L, T, src, ls, ws, ctr, kernel, near_uv, rows, st);
         launch_near_sum(L, keys, near_uv, rows, ls, ctr, kernel, st);
     };
     auto rec = [&](int i, cudaStream_t st) {

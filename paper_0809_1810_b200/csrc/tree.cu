@@ -821,7 +821,17 @@ void launch_counts_tasks(const Layout& L, char* ws, Counters* ctr, bool tasks, R
     k_counts_tasks<<<grid_for(total, 256), 256, 0, s>>>(ls, L.levels, total, chunk, rows, counts,
                                                        nt, ctr);
     note_launches(1);
-    if (!tasks) return;
+    (void)tasks;
+    (void)gauss;
+}
+
+// Near-field task list of the generic kernel (launched on the near stream
+// right before it, after the symmetric kernel; both return at once when the
+// symmetric kernel ran).
+void launch_tasks(const Layout& L, char* ws, Counters* ctr, Rows rows, bool gauss, cudaStream_t s) {
+    const int* ls = (const int*)(ws + L.leaf_starts);
+    int* nt = (int*)(ws + L.task_scratch);
+    const int chunk = 32 * p2p_targets_per_lane();
     const int nl = (int)L.nleaves;
     const bool sym = !sym_disabled();
     launch_scan_i32(nt, nl, (unsigned long long*)(ws + L.scan_state) +

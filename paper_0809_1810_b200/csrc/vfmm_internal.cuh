@@ -107,6 +107,7 @@ void launch_leaf_starts(const int* sorted_keys, int64_t n, int nleaves, int* lea
                         cudaStream_t s);
 void launch_counts_tasks(const Layout& L, char* ws, Counters* ctr, bool tasks, Rows rows,
                          bool gauss, cudaStream_t s);
+void launch_tasks(const Layout& L, char* ws, Counters* ctr, Rows rows, bool gauss, cudaStream_t s);
 void launch_p2m(const Layout& L, const Src* src, const int* leaf_starts, double xmin, double ymin,
                 double side, double2* mult_leaf, const Tables* T, Rows rows, cudaStream_t s);
 void launch_init_counters(Counters* ctr, cudaStream_t s);
@@ -121,8 +122,7 @@ void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_lo
                 const double2* anc, Rows rows, cudaStream_t s);
 int p2p_targets_per_lane();  // 1 or 2 (env VFMM_P2P_TPT, default 1)
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
-                const int2* tasks, Counters* ctr, int kernel, double2* near_uv, Rows rows,
-                cudaStream_t s);
+                char* ws, Counters* ctr, int kernel, double2* near_uv, Rows rows, cudaStream_t s);
 bool sym_disabled();  // env VFMM_P2P_SYM=0 forces the generic near-field kernel
 void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const int* keys,
                         const int* perm, const double2* loc, const double2* near_uv, double xmin,
