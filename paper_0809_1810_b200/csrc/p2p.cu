@@ -13,6 +13,7 @@
 // that work on the same leaf, otherwise read as warp-uniform (broadcast)
 // loads through L1.  The 1/(2 pi) factor is applied once per target.
 #include <atomic>
+#include <climits>
 #include <cstdlib>
 
 #include "vfmm_internal.cuh"
@@ -159,35 +160,30 @@ __global__ void __launch_bounds__(kP2PWarps * 32, kP2PBlocksPerSM)
 // Symmetric near field (Newton's third law).  With one core size for every
 // particle the pair kernel K(r) = (1 - exp(-r^2/(2 sigma^2))) / r^2 is shared
 // by (a <- b) and (b <- a): u_a += -G_b K dy, v_a += G_b K dx and
-// u_b += G_a K dy, v_b += -G_a K dx (dx, dy = a - b).  Each leaf A owns its
-// self block (A, A) and the four "forward" blocks (A, A+d),
+// u_b += G_a K dy, v_b += -G_a K dx (dx, dy = a - b).  A work item is a leaf
+// A: its self block (each unordered pair once) and its "forward" neighbours
 // d in {(1,0), (-1,1), (0,1), (1,1)}, so every neighbouring leaf pair is
-// visited once.  One warp evaluates a whole block: lanes hold 32 targets of A,
-// the 32 sources of a B chunk rotate through the lanes by shuffles together
-// with their accumulators, so after 32 steps every (a, b) pair has been seen
-// exactly once and each B accumulator is back in its home lane.  B-chunk
-// accumulators persist in shared memory across A chunks.  A work item is a
-// whole leaf A (self + four forward blocks, in that order): A's own targets
-// accumulate across the five blocks (registers / shared memory) and are
-// written once into slot 0; the reaction on each forward neighbour B goes to
-// B's slot `kind` (1..4).  The combine adds slot 0 and the reaction slots in
-// kind order: deterministic, no atomics, 80 bytes of slots per particle.
-// Work per ordered pair: 12 FP64 instructions (21 in the generic kernel).
+// visited once.  The forward sources form one stream S = R1 ++ R2 (the right
+// neighbour, then the three leaves of the row above -- one contiguous range
+// of the sorted sources), so ragged leaves waste lanes once per item, not
+// once per neighbour.  Rings: lanes keep resident particles (one or two per
+// lane) while a chunk of 32 / 16 / 8 rotating sources moves one lane per step
+// by shuffles together with its accumulators, so after R steps every
+// (resident, rotating) pair has been seen once and each rotating accumulator
+// is back home.  Per item the cheaper layout (counted in lane-pairs) is used:
+// the leaf resident and S rotating, or S resident in passes of 64 and the
+// leaf rotating (its sums in shared memory).  The leaf's own sums go to slot
+// 0, the reaction on a stream particle to its slot `kind` (1..4); the combine
+// adds slot 0 and the reaction slots in kind order: deterministic, no
+// atomics, 80 bytes of slots per particle.  Work per unordered pair: 22 FP64
+// instructions (the one-directional generic kernel: 21 per ordered pair).
 #ifndef VFMM_RING_UNROLL
 #define VFMM_RING_UNROLL 1
 #endif
-constexpr int kRingUnroll = VFMM_RING_UNROLL;
-#ifndef VFMM_SELF_SYM
-#define VFMM_SELF_SYM 1
-#endif
-constexpr bool kSelfSym = VFMM_SELF_SYM;  // self block: each unordered pair once
-#ifndef VFMM_REP_RING
-#define VFMM_REP_RING 1
-#endif
-constexpr bool kRepRing = VFMM_REP_RING;  // replicated-target ring for 33..64-particle leaves  // steps of a full ring per loop iteration
+constexpr int kRingUnroll = VFMM_RING_UNROLL;  // steps of a full ring per loop iteration
 constexpr int kSymWarps = 8;
 constexpr int kSymExpBytes = (kExpTab2N * 8 + 15) / 16 * 16;
-constexpr int kSymSmem = kSymExpBytes + 2 * kSymWarps * kSymMaxLeaf * 16;  // 92 KB
+constexpr int kSymSmem = kSymExpBytes + kSymWarps * kSymMaxLeaf * 16;  // 76 KB
 
 __device__ __forceinline__ void load_lane(const Src* __restrict__ src, int lo, int cnt, int lane,
                                           double& x, double& y, double& g) {
@@ -298,20 +294,17 @@ __device__ __forceinline__ void rotate_ring(double a0x, double a0y, double a0g, 
     }
 }
 
-// One A chunk (cntA <= 64 targets, TPL = 1 or 2 per lane) against all of B in
-// chunks of 32 / 16 / 8 sources.  SYM: B accumulators are read from and
-// written back to `acc` (shared memory, per warp).
-template <bool GAUSS, bool SYM>
-__device__ __forceinline__ void chunk_vs_leaf(const Src* __restrict__ src, int loA, int cntA, int loB,
-                                              int nB, bool first, double2* acc, SymExp q2,
-                                              const double* __restrict__ tab, double& u0,
-                                              double& v0, double& u1, double& v1) {
+// The contiguous sources [loB, loB + nB) rotate through the lanes in rings of
+// 32 / 16 / 8 (ragged tail) while the lanes keep their resident particles
+// (one or two per lane); the rotating sources' sums start from and return to
+// acc[0 .. nB) in shared memory.  Symmetric: both sides accumulate.
+template <bool GAUSS>
+__device__ __forceinline__ void rotate_leaf(const Src* __restrict__ src, double a0x, double a0y,
+                                            double a0g, double a1x, double a1y, double a1g,
+                                            bool two, int loB, int nB, double2* acc, SymExp q2,
+                                            const double* __restrict__ tab, double& u0,
+                                            double& v0, double& u1, double& v1) {
     const int lane = threadIdx.x & 31;
-    double a0x, a0y, a0g, a1x, a1y, a1g;
-    load_lane(src, loA, min(32, cntA), lane, a0x, a0y, a0g);
-    load_lane(src, loA + (cntA > 32 ? 32 : 0), max(cntA - 32, 0), lane, a1x, a1y, a1g);
-    const bool two = cntA > 32;
-    // B chunk data is prefetched one chunk ahead (registers)
     auto ring_of = [](int rem) { return rem > 24 ? 32 : (rem > 8 ? 16 : 8); };
     double nbx, nby, nbg;
     {
@@ -329,34 +322,92 @@ __device__ __forceinline__ void chunk_vs_leaf(const Src* __restrict__ src, int l
             load_lane(src, loB + j0 + R, min(R2, rem - R), lane & (R2 - 1), nbx, nby, nbg);
         }
         double ub = 0.0, vb = 0.0;
-        if (SYM && !first && li < cnt) {
+        if (li < cnt && lane < R) {  // one ring carries the running sums
             const double2 t = acc[j0 + li];
-            if (lane < R) {
-                ub = t.x;
-                vb = t.y;
-            }
+            ub = t.x;
+            vb = t.y;
         }
-#define VFMM_RING(TPLV, RV)                                                                      \
-    rotate_ring<GAUSS, TPLV, RV, SYM>(a0x, a0y, a0g, a1x, a1y, a1g, bx, by, bg, ub, vb, q2, tab, \
-                                      u0, v0, u1, v1)
+#define VFMM_RING(TPLV, RV)                                                                       \
+    rotate_ring<GAUSS, TPLV, RV, true>(a0x, a0y, a0g, a1x, a1y, a1g, bx, by, bg, ub, vb, q2, tab, \
+                                       u0, v0, u1, v1)
         if (two) {
             if (R == 32) VFMM_RING(2, 32); else if (R == 16) VFMM_RING(2, 16); else VFMM_RING(2, 8);
         } else {
             if (R == 32) VFMM_RING(1, 32); else if (R == 16) VFMM_RING(1, 16); else VFMM_RING(1, 8);
         }
 #undef VFMM_RING
-        if (SYM && lane < cnt) acc[j0 + lane] = make_double2(ub, vb);
+        if (lane < cnt) acc[j0 + lane] = make_double2(ub, vb);
         j0 += R;
     }
 }
 
-// Self block of a leaf of nA <= 64 particles, each unordered pair once.
-// Lane l holds particles l (a0) and 32 + l (a1, ghosts past nA: zero
-// circulation).  Two half rings run together -- chunk 0 against itself and
-// chunk 1 against itself: after the first shift, 16 steps pair lane l with
-// l + 1 .. l + 16 (the distance-16 pairs only on lanes < 16), with each
-// source's reaction carried along and shuffled home at the end -- then one
-// symmetric full ring pairs chunk 0 (targets) with chunk 1 (sources).
+// Particle t of the forward stream S = R1 ++ R2 (two contiguous source
+// ranges): its sorted index, or -1 past the end.
+__device__ __forceinline__ int stream_index(int t, int r1, int n1, int r2, int n2) {
+    return t < n1 ? r1 + t : (t < n1 + n2 ? r2 + (t - n1) : -1);
+}
+
+// Ring steps to rotate n sources through (rings of 32 / 16 / 8).
+__device__ __forceinline__ int rot_steps(int n) {
+    const int full = n >> 5, rem = n & 31;
+    return 32 * full + (rem == 0 ? 0 : (rem > 24 ? 32 : (rem > 8 ? 16 : 8)));
+}
+
+// The forward stream S rotates through the lanes (chunks may straddle the
+// R1 / R2 boundary) while the lanes keep up to 64 particles of the leaf; each
+// chunk's reactions are complete when the ring returns home and go straight
+// to the sources' slots.
+template <bool GAUSS>
+__device__ __forceinline__ void rotate_stream(const Src* __restrict__ src, double a0x, double a0y,
+                                              double a0g, double a1x, double a1y, double a1g,
+                                              bool two, int r1, int n1, int r2, int n2, int b3,
+                                              int b4, double2* __restrict__ near5, int64_t n,
+                                              SymExp q2, const double* __restrict__ tab,
+                                              double& u0, double& v0, double& u1, double& v1) {
+    const int lane = threadIdx.x & 31;
+    const int nS = n1 + n2;
+    auto ring_of = [](int rem) { return rem > 24 ? 32 : (rem > 8 ? 16 : 8); };
+    auto load = [&](int j0, int cnt, int li, double& x, double& y, double& g) {
+        const int t = j0 + (li < cnt ? li : 0);
+        const Src& e = src[stream_index(t, r1, n1, r2, n2)];
+        x = e.x;
+        y = e.y;
+        g = li < cnt ? e.g : 0.0;
+    };
+    double nbx, nby, nbg;
+    {
+        const int R = ring_of(nS);
+        load(0, min(R, nS), lane & (R - 1), nbx, nby, nbg);
+    }
+    for (int j0 = 0; j0 < nS;) {
+        const int rem = nS - j0;
+        const int R = ring_of(rem);
+        const int cnt = min(R, rem);
+        double bx = nbx, by = nby, bg = nbg;
+        if (rem > R) {
+            const int R2 = ring_of(rem - R);
+            load(j0 + R, min(R2, rem - R), lane & (R2 - 1), nbx, nby, nbg);
+        }
+        double ub = 0.0, vb = 0.0;
+#define VFMM_RING(TPLV, RV)                                                                       \
+    rotate_ring<GAUSS, TPLV, RV, true>(a0x, a0y, a0g, a1x, a1y, a1g, bx, by, bg, ub, vb, q2, tab, \
+                                       u0, v0, u1, v1)
+        if (two) {
+            if (R == 32) VFMM_RING(2, 32); else if (R == 16) VFMM_RING(2, 16); else VFMM_RING(2, 8);
+        } else {
+            if (R == 32) VFMM_RING(1, 32); else if (R == 16) VFMM_RING(1, 16); else VFMM_RING(1, 8);
+        }
+#undef VFMM_RING
+        if (lane < cnt) {
+            const int t = j0 + lane;
+            const int i = stream_index(t, r1, n1, r2, n2);
+            const int kind = t < n1 ? 1 : (i < b3 ? 2 : (i < b4 ? 3 : 4));
+            near5[(int64_t)kind * n + i] = make_double2(ub * kInv2Pi, vb * kInv2Pi);
+        }
+        j0 += R;
+    }
+}
+
 template <bool GAUSS>
 __device__ __forceinline__ void self_block_sym(double a0x, double a0y, double a0g, double a1x,
                                                double a1y, double a1g, bool two, SymExp q2,
@@ -418,8 +469,13 @@ __device__ __forceinline__ void self_block_sym(double a0x, double a0y, double a0
     v1 += vbx;
 }
 
+#ifdef VFMM_SYM_MAXNREG
+#define VFMM_SYM_BOUNDS __maxnreg__(VFMM_SYM_MAXNREG)
+#else
+#define VFMM_SYM_BOUNDS __launch_bounds__(kSymWarps * 32, MINB)
+#endif
 template <bool GAUSS, int MINB>
-__global__ void __launch_bounds__(kSymWarps * 32, MINB)
+__global__ void VFMM_SYM_BOUNDS
     k_p2p_sym(const Src* __restrict__ src, const int* __restrict__ ls, Counters* __restrict__ ctr,
               int levels, int64_t n, Rows rows, const Tables* __restrict__ T,
               double2* __restrict__ near5, unsigned long long* __restrict__ pairs,
@@ -428,16 +484,14 @@ __global__ void __launch_bounds__(kSymWarps * 32, MINB)
     const int m = 1 << levels;
     const int nitems = 1 << (2 * levels);  // one item per leaf
     if ((int64_t)blockIdx.x * kSymWarps * items_per_warp >= nitems) return;  // spare CTA
-    // dynamic shared memory: exp table | per-warp B accumulators | per-warp A accumulators
+    // dynamic shared memory: exp table | per-warp accumulators of the item's leaf
     extern __shared__ __align__(16) unsigned char sym_smem[];
     double* sexp = reinterpret_cast<double*>(sym_smem);
-    double2* accB = reinterpret_cast<double2*>(sym_smem + kSymExpBytes);
-    double2* accA = accB + kSymWarps * kSymMaxLeaf;
+    double2* accA = reinterpret_cast<double2*>(sym_smem + kSymExpBytes);
     for (int i = threadIdx.x; i < kExpTab2N; i += blockDim.x) sexp[i] = T->exp2tab2[i];
     const double* tab = sexp + (kExpTab2N - 1);  // 2^(n/128) at tab[n], n <= 0
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double2* acc = accB + warp * kSymMaxLeaf;
     double2* accAw = accA + warp * kSymMaxLeaf;
     const SymExp q2 = sym_exp(GAUSS ? src[0].q2 : -1.0);  // uniform core size
     long long my_pairs = 0;
@@ -452,74 +506,109 @@ __global__ void __launch_bounds__(kSymWarps * 32, MINB)
         if (nA == 0) continue;
         const int cx = leaf & (m - 1), cy = leaf >> levels;
         const bool ownA = cy >= rows.lo && cy < rows.hi;
-        bool startedA = false;  // A accumulators hold a partial sum (warp-uniform)
-        for (int kind = 0; kind < 5; ++kind) {
-            int dx_ = 0, dy_ = 0, loB = loA, nB = nA;
-            bool ownB = false;
-            if (kind == 0) {
-                if (!ownA) continue;  // self block: a <- b for all b in A (r^2 == 0 adds exactly 0)
-            } else {
-                dx_ = kind == 2 ? -1 : (kind == 3 ? 0 : 1);
-                dy_ = kind == 1 ? 0 : 1;
-                const int bxc = cx + dx_, byc = cy + dy_;
-                if (bxc < 0 || bxc >= m || byc >= m) continue;
-                ownB = byc >= rows.lo && byc < rows.hi;
-                if (!ownA && !ownB) continue;
-                const int lb = byc * m + bxc;
-                loB = ls[lb];
-                nB = ls[lb + 1] - loB;
-                if (nB == 0) continue;
+        // forward stream S = R1 (leaf (cx+1, cy)) ++ R2 (leaves cx-1..cx+1 of row
+        // cy+1, one contiguous range of the sorted sources)
+        int r1 = 0, n1 = 0, r2 = 0, n2 = 0, b3 = 0, b4 = 0;
+        bool ownR2 = false;
+        if (ownA && cx + 1 < m) {
+            r1 = ls[leaf + 1];
+            n1 = ls[leaf + 2] - r1;
+        }
+        if (cy + 1 < m) {
+            ownR2 = cy + 1 >= rows.lo && cy + 1 < rows.hi;
+            if (ownA || ownR2) {
+                const int row = (cy + 1) * m;
+                const int x0 = cx > 0 ? cx - 1 : 0, x1 = cx + 1 < m ? cx + 1 : m - 1;
+                r2 = ls[row + x0];
+                n2 = ls[row + x1 + 1] - r2;
+                b3 = ls[row + cx];                          // first source of kind 3 (0, 1)
+                b4 = cx + 1 < m ? ls[row + cx + 1] : r2 + n2;  // first source of kind 4 (1, 1)
             }
-            if (kSelfSym && kind == 0 && nA <= 64) {  // each unordered pair of the leaf once
-                double a0x, a0y, a0g, a1x, a1y, a1g;
-                load_lane(src, loA, min(32, nA), lane, a0x, a0y, a0g);
-                load_lane(src, loA + (nA > 32 ? 32 : 0), max(nA - 32, 0), lane, a1x, a1y, a1g);
-                double u0 = 0.0, v0 = 0.0, u1 = 0.0, v1 = 0.0;
-                self_block_sym<GAUSS>(a0x, a0y, a0g, a1x, a1y, a1g, nA > 32, q2, tab, u0, v0, u1, v1);
-                accAw[lane] = make_double2(u0, v0);
-                accAw[32 + lane] = make_double2(u1, v1);
-                startedA = true;
-                my_pairs += (long long)nA * nA - nA;
-                continue;
-            }
-            for (int i0 = 0; i0 < nA; i0 += 64) {
-                const int cntA = min(64, nA - i0);
-                double u0 = 0.0, v0 = 0.0, u1 = 0.0, v1 = 0.0;
-                if (startedA) {
-                    const double2 a0 = accAw[i0 + lane], a1 = accAw[i0 + 32 + lane];
-                    u0 = a0.x; v0 = a0.y; u1 = a1.x; v1 = a1.y;
+        }
+        if (!ownA && n2 == 0) continue;
+        // ---- self block (owned A only): each unordered pair once ----
+        if (ownA && nA <= kSymMaxLeaf) {
+            double a0x, a0y, a0g, a1x, a1y, a1g, a2x, a2y, a2g, a3x, a3y, a3g;
+            load_lane(src, loA, min(32, nA), lane, a0x, a0y, a0g);
+            load_lane(src, loA + (nA > 32 ? 32 : 0), max(nA - 32, 0), lane, a1x, a1y, a1g);
+            double u0 = 0.0, v0 = 0.0, u1 = 0.0, v1 = 0.0;
+            self_block_sym<GAUSS>(a0x, a0y, a0g, a1x, a1y, a1g, nA > 32, q2, tab, u0, v0, u1, v1);
+            if (nA > 64) {
+                load_lane(src, loA + 64, min(32, nA - 64), lane, a2x, a2y, a2g);
+                load_lane(src, loA + (nA > 96 ? 96 : 64), max(nA - 96, 0), lane, a3x, a3y, a3g);
+                double u2 = 0.0, v2 = 0.0, u3 = 0.0, v3 = 0.0;
+                self_block_sym<GAUSS>(a2x, a2y, a2g, a3x, a3y, a3g, nA > 96, q2, tab, u2, v2, u3, v3);
+                // chunks 0, 1 (resident) against chunk 2, then chunk 3 (rotating)
+                double ub = 0.0, vb = 0.0;
+                rotate_ring<GAUSS, 2, 32, true>(a0x, a0y, a0g, a1x, a1y, a1g, a2x, a2y, a2g, ub, vb,
+                                                q2, tab, u0, v0, u1, v1);
+                u2 += ub;
+                v2 += vb;
+                if (nA > 96) {
+                    ub = vb = 0.0;
+                    rotate_ring<GAUSS, 2, 32, true>(a0x, a0y, a0g, a1x, a1y, a1g, a3x, a3y, a3g, ub,
+                                                    vb, q2, tab, u0, v0, u1, v1);
+                    u3 += ub;
+                    v3 += vb;
                 }
-                if (kind == 0)
-                    chunk_vs_leaf<GAUSS, false>(src, loA + i0, cntA, loB, nB, true, acc, q2, tab,
-                                                u0, v0, u1, v1);
-                else
-                    chunk_vs_leaf<GAUSS, true>(src, loA + i0, cntA, loB, nB, i0 == 0, acc, q2,
-                                               tab, u0, v0, u1, v1);
-                accAw[i0 + lane] = make_double2(u0, v0);
-                accAw[i0 + 32 + lane] = make_double2(u1, v1);
+                accAw[64 + lane] = make_double2(u2, v2);
+                accAw[96 + lane] = make_double2(u3, v3);
             }
-            startedA = true;
-            if (kind == 0) {
-                my_pairs += (long long)nA * nA - nA;
-                continue;
-            }
-            // reaction on B: slot `kind` (B's backward neighbour in direction kind)
-            __syncwarp();
-            for (int j = lane; j < nB; j += 32) {
-                const double2 t = acc[j];
-                near5[(int64_t)kind * n + loB + j] = make_double2(t.x * kInv2Pi, t.y * kInv2Pi);
-            }
-            __syncwarp();
-            my_pairs += (long long)nA * nB * ((ownA ? 1 : 0) + (ownB ? 1 : 0));
+            accAw[lane] = make_double2(u0, v0);
+            accAw[32 + lane] = make_double2(u1, v1);
+            my_pairs += (long long)nA * nA - nA;
+        } else {
+            for (int j = lane; j < nA; j += 32) accAw[j] = make_double2(0.0, 0.0);
         }
-        // A's own targets: self + forward blocks, summed in kind order -> slot 0
-        if (startedA) {
-            __syncwarp();
-            for (int j = lane; j < nA; j += 32) {
-                const double2 t = accAw[j];
-                near5[loA + j] = make_double2(t.x * kInv2Pi, t.y * kInv2Pi);
+        __syncwarp();
+        const int nS = n1 + n2;
+        // ---- forward blocks: whichever layout wastes fewer lane-pairs ----
+        // (a) the leaf resident (<= 64: one or two per lane), S rotating;
+        // (b) S resident in passes of 64, the leaf rotating (A's sums in smem).
+        const int slotsA = nA > 32 ? 64 : 32;
+        const int cost_a = nA <= 64 ? slotsA * rot_steps(nS) : INT_MAX;
+        const int cost_b = (nS >> 6) * 64 * rot_steps(nA) + ((nS & 63) == 0 ? 0 : ((nS & 63) > 32 ? 64 : 32) * rot_steps(nA));
+        if (nS > 0 && cost_a <= cost_b) {
+            double a0x, a0y, a0g, a1x, a1y, a1g;
+            load_lane(src, loA, min(32, nA), lane, a0x, a0y, a0g);
+            load_lane(src, loA + (nA > 32 ? 32 : 0), max(nA - 32, 0), lane, a1x, a1y, a1g);
+            const double2 s0 = accAw[lane], s1 = accAw[32 + lane];
+            double u0 = s0.x, v0 = s0.y, u1 = s1.x, v1 = s1.y;
+            rotate_stream<GAUSS>(src, a0x, a0y, a0g, a1x, a1y, a1g, nA > 32, r1, n1, r2, n2, b3, b4,
+                                 near5, n, q2, tab, u0, v0, u1, v1);
+            accAw[lane] = make_double2(u0, v0);
+            accAw[32 + lane] = make_double2(u1, v1);
+        }
+        for (int p0 = 0; cost_a > cost_b && p0 < nS; p0 += 64) {
+            const int cnt = min(64, nS - p0);
+            const int t0 = p0 + lane, t1 = p0 + 32 + lane;
+            const int i0 = stream_index(t0 < p0 + cnt ? t0 : p0, r1, n1, r2, n2);
+            const int i1 = stream_index(t1 < p0 + cnt ? t1 : p0, r1, n1, r2, n2);
+            const Src& s0 = src[i0];
+            const Src& s1 = src[i1];
+            const double a0x = s0.x, a0y = s0.y, a0g = t0 < p0 + cnt ? s0.g : 0.0;
+            const double a1x = s1.x, a1y = s1.y, a1g = t1 < p0 + cnt ? s1.g : 0.0;
+            double u0 = 0.0, v0 = 0.0, u1 = 0.0, v1 = 0.0;
+            rotate_leaf<GAUSS>(src, a0x, a0y, a0g, a1x, a1y, a1g, cnt > 32, loA, nA, accAw, q2, tab,
+                               u0, v0, u1, v1);
+            // reactions on the stream particles -> their slot `kind`
+            if (t0 < p0 + cnt) {
+                const int kind = t0 < n1 ? 1 : (i0 < b3 ? 2 : (i0 < b4 ? 3 : 4));
+                near5[(int64_t)kind * n + i0] = make_double2(u0 * kInv2Pi, v0 * kInv2Pi);
+            }
+            if (t1 < p0 + cnt) {
+                const int kind = t1 < n1 ? 1 : (i1 < b3 ? 2 : (i1 < b4 ? 3 : 4));
+                near5[(int64_t)kind * n + i1] = make_double2(u1 * kInv2Pi, v1 * kInv2Pi);
             }
         }
+        my_pairs += 2ll * nA * n1 + (long long)nA * n2 * ((ownA ? 1 : 0) + (ownR2 ? 1 : 0));
+        // A's own targets: self + forward blocks -> slot 0
+        __syncwarp();
+        for (int j = lane; j < nA; j += 32) {
+            const double2 t = accAw[j];
+            near5[loA + j] = make_double2(t.x * kInv2Pi, t.y * kInv2Pi);
+        }
+        __syncwarp();
     }
     if (lane == 0 && my_pairs) atomicAdd(pairs, (unsigned long long)my_pairs);
 }
