@@ -294,6 +294,83 @@ __device__ __forceinline__ void rotate_ring(double a0x, double a0y, double a0g, 
     }
 }
 
+// Four resident particles per lane (a resident pass of 128): four independent
+// pair chains per step and one rotation of the source (and its sums) per four
+// pairs.  Symmetric only.
+template <bool GAUSS, int R>
+__device__ __forceinline__ void rotate_ring4(const double (&ax)[4], const double (&ay)[4],
+                                             const double (&ag)[4], double bx, double by,
+                                             double bg, double& ub, double& vb, SymExp q2,
+                                             const double* __restrict__ tab, double (&u)[4],
+                                             double (&v)[4]) {
+    const int from = ((threadIdx.x & 31) + 1) & (R - 1);
+#pragma unroll 1
+    for (int st = 0; st < R; ++st) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double dx = ax[k] - bx, dy = ay[k] - by;
+            const double K = pair_kernel<GAUSS>(dx, dy, q2, tab);
+            const double ca = bg * K, cb = ag[k] * K;
+            u[k] = fma(-ca, dy, u[k]);
+            v[k] = fma(ca, dx, v[k]);
+            ub = fma(cb, dy, ub);
+            vb = fma(-cb, dx, vb);
+        }
+        bx = __shfl_sync(0xffffffffu, bx, from, R);
+        by = __shfl_sync(0xffffffffu, by, from, R);
+        bg = __shfl_sync(0xffffffffu, bg, from, R);
+        ub = __shfl_sync(0xffffffffu, ub, from, R);
+        vb = __shfl_sync(0xffffffffu, vb, from, R);
+    }
+#pragma unroll
+    for (int off = R; off < 32; off <<= 1) {
+        ub += __shfl_xor_sync(0xffffffffu, ub, off);
+        vb += __shfl_xor_sync(0xffffffffu, vb, off);
+    }
+}
+
+// The leaf [loB, loB + nB) rotating past four residents per lane; its sums
+// start from and return to acc[] in shared memory.
+template <bool GAUSS>
+__device__ __forceinline__ void rotate_leaf4(const Src* __restrict__ src, const double (&ax)[4],
+                                             const double (&ay)[4], const double (&ag)[4], int loB,
+                                             int nB, double2* acc, SymExp q2,
+                                             const double* __restrict__ tab, double (&u)[4],
+                                             double (&v)[4]) {
+    const int lane = threadIdx.x & 31;
+    auto ring_of = [](int rem) { return rem > 24 ? 32 : (rem > 8 ? 16 : 8); };
+    double nbx, nby, nbg;
+    {
+        const int R = ring_of(nB);
+        load_lane(src, loB, min(R, nB), lane & (R - 1), nbx, nby, nbg);
+    }
+    for (int j0 = 0; j0 < nB;) {
+        const int rem = nB - j0;
+        const int R = ring_of(rem);
+        const int cnt = min(R, rem);
+        const int li = lane & (R - 1);
+        double bx = nbx, by = nby, bg = nbg;
+        if (rem > R) {
+            const int R2 = ring_of(rem - R);
+            load_lane(src, loB + j0 + R, min(R2, rem - R), lane & (R2 - 1), nbx, nby, nbg);
+        }
+        double ub = 0.0, vb = 0.0;
+        if (li < cnt && lane < R) {
+            const double2 t = acc[j0 + li];
+            ub = t.x;
+            vb = t.y;
+        }
+        if (R == 32)
+            rotate_ring4<GAUSS, 32>(ax, ay, ag, bx, by, bg, ub, vb, q2, tab, u, v);
+        else if (R == 16)
+            rotate_ring4<GAUSS, 16>(ax, ay, ag, bx, by, bg, ub, vb, q2, tab, u, v);
+        else
+            rotate_ring4<GAUSS, 8>(ax, ay, ag, bx, by, bg, ub, vb, q2, tab, u, v);
+        if (lane < cnt) acc[j0 + lane] = make_double2(ub, vb);
+        j0 += R;
+    }
+}
+
 // The contiguous sources [loB, loB + nB) rotate through the lanes in rings of
 // 32 / 16 / 8 (ragged tail) while the lanes keep their resident particles
 // (one or two per lane); the rotating sources' sums start from and return to
@@ -346,6 +423,10 @@ __device__ __forceinline__ void rotate_leaf(const Src* __restrict__ src, double 
 __device__ __forceinline__ int stream_index(int t, int r1, int n1, int r2, int n2) {
     return t < n1 ? r1 + t : (t < n1 + n2 ? r2 + (t - n1) : -1);
 }
+
+// Resident slots of the next pass over `rem` stream particles: 128 (four per
+// lane) while more than 96 remain, else 64 or 32.
+__device__ __forceinline__ int pass_slots(int rem) { return rem > 96 ? 128 : (rem > 32 ? 64 : 32); }
 
 // Ring steps to rotate n sources through (rings of 32 / 16 / 8).
 __device__ __forceinline__ int rot_steps(int n) {
@@ -567,8 +648,9 @@ __global__ void VFMM_SYM_BOUNDS
         // (b) S resident in passes of 64, the leaf rotating (A's sums in smem).
         const int slotsA = nA > 32 ? 64 : 32;
         const int cost_a = nA <= 64 ? slotsA * rot_steps(nS) : INT_MAX;
-        const int cost_b = (nS >> 6) * 64 * rot_steps(nA) + ((nS & 63) == 0 ? 0 : ((nS & 63) > 32 ? 64 : 32) * rot_steps(nA));
-        if (nS > 0 && cost_a <= cost_b) {
+        int cost_b = 0;  // resident passes of 128 (4 per lane), 64 or 32
+        for (int r = nS; r > 0; r -= pass_slots(r)) cost_b += pass_slots(r) * rot_steps(nA);
+        if (nS > 0 && cost_a < cost_b) {
             double a0x, a0y, a0g, a1x, a1y, a1g;
             load_lane(src, loA, min(32, nA), lane, a0x, a0y, a0g);
             load_lane(src, loA + (nA > 32 ? 32 : 0), max(nA - 32, 0), lane, a1x, a1y, a1g);
@@ -579,7 +661,33 @@ __global__ void VFMM_SYM_BOUNDS
             accAw[lane] = make_double2(u0, v0);
             accAw[32 + lane] = make_double2(u1, v1);
         }
-        for (int p0 = 0; cost_a > cost_b && p0 < nS; p0 += 64) {
+        for (int p0 = 0; cost_a >= cost_b && p0 < nS;) {
+            if (pass_slots(nS - p0) == 128) {  // four residents per lane
+                double ax[4], ay[4], ag[4], u[4], v[4];
+                int idx[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int t = p0 + 32 * k + lane;
+                    idx[k] = stream_index(t < nS ? t : p0, r1, n1, r2, n2);
+                    const Src& e = src[idx[k]];
+                    ax[k] = e.x;
+                    ay[k] = e.y;
+                    ag[k] = t < nS ? e.g : 0.0;
+                    u[k] = v[k] = 0.0;
+                }
+                rotate_leaf4<GAUSS>(src, ax, ay, ag, loA, nA, accAw, q2, tab, u, v);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int t = p0 + 32 * k + lane;
+                    if (t < nS) {
+                        const int i = idx[k];
+                        const int kind = t < n1 ? 1 : (i < b3 ? 2 : (i < b4 ? 3 : 4));
+                        near5[(int64_t)kind * n + i] = make_double2(u[k] * kInv2Pi, v[k] * kInv2Pi);
+                    }
+                }
+                p0 += 128;
+                continue;
+            }
             const int cnt = min(64, nS - p0);
             const int t0 = p0 + lane, t1 = p0 + 32 + lane;
             const int i0 = stream_index(t0 < p0 + cnt ? t0 : p0, r1, n1, r2, n2);
@@ -600,6 +708,7 @@ __global__ void VFMM_SYM_BOUNDS
                 const int kind = t1 < n1 ? 1 : (i1 < b3 ? 2 : (i1 < b4 ? 3 : 4));
                 near5[(int64_t)kind * n + i1] = make_double2(u1 * kInv2Pi, v1 * kInv2Pi);
             }
+            p0 += 64;
         }
         my_pairs += 2ll * nA * n1 + (long long)nA * n2 * ((ownA ? 1 : 0) + (ownR2 ? 1 : 0));
         // A's own targets: self + forward blocks -> slot 0
