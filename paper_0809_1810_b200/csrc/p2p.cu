@@ -590,11 +590,40 @@ __device__ __forceinline__ void self_block_sym(double a0x, double a0y, double a0
     if (!two) return;
     u1 += __shfl_sync(0xffffffffu, ub1, home);
     v1 += __shfl_sync(0xffffffffu, vb1, home);
-    double ubx = 0.0, vbx = 0.0, d0 = 0.0, d1 = 0.0;
-    rotate_ring<GAUSS, 1, 32, true>(a0x, a0y, a0g, 0.0, 0.0, 0.0, a1x, a1y, a1g, ubx, vbx, q2, tab,
-                                    u0, v0, d0, d1);
-    u1 += ubx;
-    v1 += vbx;
+    // cross ring chunk 0 x chunk 1 as two half-phase copies of chunk 1 (offsets
+    // 0..15 and 16..31) rotating together: two chains per step for 16 steps
+    double pbx = a1x, pby = a1y, pbg = a1g;  // copy P: lane l starts with particle l
+    double qbx = __shfl_sync(0xffffffffu, a1x, home), qby = __shfl_sync(0xffffffffu, a1y, home);
+    double qbg = __shfl_sync(0xffffffffu, a1g, home);  // copy Q: particle l + 16
+    double pu = 0.0, pv = 0.0, qu = 0.0, qv = 0.0;
+#pragma unroll 1
+    for (int st = 0; st < 16; ++st) {
+        const double dx[2] = {a0x - pbx, a0x - qbx}, dy[2] = {a0y - pby, a0y - qby};
+        double K[2];
+        pair_kernels<GAUSS, 2>(dx, dy, K, q2, tab);
+        const double cap = pbg * K[0], caq = qbg * K[1], cbp = a0g * K[0], cbq = a0g * K[1];
+        u0 = fma(-cap, dy[0], u0);
+        v0 = fma(cap, dx[0], v0);
+        u0 = fma(-caq, dy[1], u0);
+        v0 = fma(caq, dx[1], v0);
+        pu = fma(cbp, dy[0], pu);
+        pv = fma(-cbp, dx[0], pv);
+        qu = fma(cbq, dy[1], qu);
+        qv = fma(-cbq, dx[1], qv);
+        pbx = __shfl_sync(0xffffffffu, pbx, from);
+        pby = __shfl_sync(0xffffffffu, pby, from);
+        pbg = __shfl_sync(0xffffffffu, pbg, from);
+        pu = __shfl_sync(0xffffffffu, pu, from);
+        pv = __shfl_sync(0xffffffffu, pv, from);
+        qbx = __shfl_sync(0xffffffffu, qbx, from);
+        qby = __shfl_sync(0xffffffffu, qby, from);
+        qbg = __shfl_sync(0xffffffffu, qbg, from);
+        qu = __shfl_sync(0xffffffffu, qu, from);
+        qv = __shfl_sync(0xffffffffu, qv, from);
+    }
+    // after 16 shifts copy Q is home; copy P holds particle l + 16
+    u1 += __shfl_sync(0xffffffffu, pu, home) + qu;
+    v1 += __shfl_sync(0xffffffffu, pv, home) + qv;
 }
 
 #ifdef VFMM_SYM_MAXNREG
