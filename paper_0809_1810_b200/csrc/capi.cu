@@ -424,15 +424,42 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         launch_m2m(L, T, mult, fs);
         rec(2, fs);
     }
+    bool fuse = false;  // L2P + combine inside the L2L launch (see below)
     if (down) {
         if (!up) rec(2, cs);
         // ---- M2L (all levels, one launch) ----
         launch_m2l(L, T, mult, counts, loc, (double2*)(ws + L.anc), ctr, rows, fs);
         rec(3, fs);
         // ---- downward ----
-        launch_l2l(L, T, loc, (double2*)(ws + L.leaf_loc), (const double2*)(ws + L.anc), rows, fs);
+        // Single-GPU evaluates fuse the L2P + combine into the finest L2L
+        // level (the near-field totals must be complete first): one launch and
+        // one pass over the leaf locals fewer on the critical path.
+        fuse = up && !far_only && levels > 2;
+        FusedOut fo{};
+        if (fuse) {
+            if (overlap) {
+                rec(7, R->near);
+                near_field(R->near);
+                rec(8, R->near);
+                cudaEventRecord(R->join_near, R->near);
+                cudaStreamWaitEvent(fs, R->join_near, 0);
+            } else {
+                rec(7, cs);
+                near_field(cs);
+                rec(8, cs);
+            }
+            fo = FusedOut{src, keys, perm, ls, near_uv, u, v, xmin, ymin, side};
+        }
+        rec(5, fs);
+        launch_l2l(L, T, loc, (double2*)(ws + L.leaf_loc), (const double2*)(ws + L.anc), rows, fo,
+                   fs);
         rec(4, fs);
-        if (overlap && up) {
+        if (fuse) {
+            if (overlap) {
+                cudaEventRecord(R->join_far, fs);
+                cudaStreamWaitEvent(cs, R->join_far, 0);
+            }
+        } else if (overlap && up) {
             cudaEventRecord(R->join_far, fs);
             rec(7, R->near);
             near_field(R->near);
@@ -443,7 +470,7 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         } else if (overlap) {  // sharded PHASE_DOWN: join the near field started in PHASE_UP
             cudaStreamWaitEvent(cs, R->join_near, 0);
         }
-        if (!far_only) {
+        if (!far_only && !fuse) {
             if (!overlap) near_field(cs);
             rec(5, cs);
             launch_l2p_combine(L, T, src, keys, perm, (const double2*)(ws + L.leaf_loc), near_uv,
@@ -485,7 +512,12 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
     if (down) {
         stats->t_m2l = elapsed(R->ev[2], R->ev[3]);
         stats->t_downward = elapsed(R->ev[3], R->ev[4]);
-        if (far_only) {
+        if (fuse) {  // t_downward covers L2L + L2P + combine (after the near field)
+            stats->t_downward = elapsed(R->ev[5], R->ev[4]);
+            stats->t_near = elapsed(R->ev[7], R->ev[8]);
+            stats->t_eval = 0.f;
+            stats->overlapped = overlap ? 1 : 0;
+        } else if (far_only) {
             stats->t_near = 0.f;
             stats->t_eval = 0.f;
         } else if (overlap) {

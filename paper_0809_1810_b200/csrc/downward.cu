@@ -22,26 +22,6 @@ __global__ void k_leaf_locals_copy(const double2* __restrict__ loc2, int P, doub
     out[t] = loc2[n * coef_stride(2) + coef_base(2, cell & 3, cell >> 2)];
 }
 
-// Horner evaluation of the leaf local expansion at z:
-//   f(z) = sum_m Lh_m / m! (-w)^m,  w = (z - c) / r
-__device__ __forceinline__ double2 eval_local(const double2* __restrict__ Lh, int64_t stride, int P,
-                                              double wx, double wy,
-                                              const double* __restrict__ invfact) {
-    const double nx = -wx, ny = -wy;
-    const double2 top = Lh[(P - 1) * stride];
-    double ax = top.x * invfact[P - 1], ay = top.y * invfact[P - 1];
-#pragma unroll 6
-    for (int k = P - 2; k >= 0; --k) {
-        const double2 c = Lh[k * stride];
-        const double f = invfact[k];
-        const double tx = fma(ax, nx, fma(-ay, ny, c.x * f));
-        const double ty = fma(ax, ny, fma(ay, nx, c.y * f));
-        ax = tx;
-        ay = ty;
-    }
-    return make_double2(ax, ay);
-}
-
 // Near-field total per particle, in place in slot 0, right after the near
 // field (on its stream, so it overlaps the far-field chain): symmetric
 // kernel -- slot 0 (the leaf's own blocks) + the reactions of the existing

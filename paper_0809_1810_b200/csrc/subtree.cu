@@ -8,6 +8,8 @@
 //   M2M  P_m  = 2^-(m+1) sum_{k<=m} M_k E_q[m-k]         children in quadrant order
 //   L2L  Lh'_n = M2L_n + sum_{m>=n} (2^-m Lh_m) F_q[m-n]  (M2L part + parent shift)
 // Local cell ids: sub-level s (0 = the CTA's root cell) holds a 2^s x 2^s grid.
+#include <cstdlib>
+
 #include "vfmm_internal.cuh"
 
 namespace vfmm {
@@ -91,17 +93,21 @@ __device__ __forceinline__ int64_t lvl_off(int k, int P) {
 __global__ void __launch_bounds__(kSubThreads)
     k_l2l_fused(double2* __restrict__ loc, double2* __restrict__ leaf_loc,
                 const double2* __restrict__ anc_m2l, int ls, int levels, int P,
-                const Tables* __restrict__ T, Rows rows) {
+                const Tables* __restrict__ T, Rows rows, FusedOut fo) {
     extern __shared__ double2 sm[];
     const int depth = levels - ls;
     double2* sF = sm + (size_t)sub_off(depth + 1) * P;  // [4][P]
     double* s2 = reinterpret_cast<double*>(sF + 4 * P);  // [P]
     double2* anc = reinterpret_cast<double2*>(s2 + ((P + 1) & ~1));  // [2][P] ping-pong
+    double* sfact = reinterpret_cast<double*>(anc + 2 * P);           // [P] 1/k!
     const int mt = 1 << ls;
     const int cx = blockIdx.x % mt, cy = blockIdx.x / mt;
     if (!rows_touch(rows, cy, levels - ls)) return;  // subtree outside the owned strip
     for (int i = threadIdx.x; i < 4 * P; i += blockDim.x) sF[i] = T->F[i / P][i % P];
-    for (int i = threadIdx.x; i < P; i += blockDim.x) s2[i] = T->pow2neg[i];
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        s2[i] = T->pow2neg[i];
+        sfact[i] = T->invfact[i];
+    }
     const int n = threadIdx.x;
     // ---- ancestor chain: level 2 (complete after M2L) down to ls ----
     if (n < P) {
@@ -196,6 +202,37 @@ __global__ void __launch_bounds__(kSubThreads)
         }
         __syncthreads();
     }
+    if (!fo.u) return;
+    // ---- fused L2P + combine over the particles of this CTA's leaves ----
+    // (the leaf locals are in shared memory; one contiguous particle range per
+    // leaf row of the subtree)
+    const int side = 1 << depth, m = 1 << levels;
+    const double r = fo.side / m, inv_r = 1.0 / r;
+    const double2* leafs = sm + (size_t)sub_off(depth) * P;
+    for (int ly = 0; ly < side; ++ly) {
+        const int gy = cy * side + ly;
+        if (gy < rows.lo || gy >= rows.hi) continue;  // halo rows of a sharded run
+        const int row = gy * m + cx * side;
+        const int a0 = fo.ls[row], a1 = fo.ls[row + side];
+        for (int j = a0 + threadIdx.x; j < a1; j += blockDim.x) {
+            const int lx = (fo.keys[j] & (m - 1)) - cx * side;
+            const Src sj = fo.src[j];
+            const double ccx = cell_center(fo.xmin, cx * side + lx, r);
+            const double ccy = cell_center(fo.ymin, gy, r);
+            const double2 f = eval_local(leafs + (size_t)(ly * side + lx) * P, 1, P,
+                                         (sj.x - ccx) * inv_r, (sj.y - ccy) * inv_r, sfact);
+            const double2 nv = fo.near[j];
+            // f_to_velocity: u = Im f / 2pi, v = Re f / 2pi; then far + near
+            const double uo = f.y * kInv2Pi + nv.x, vo = f.x * kInv2Pi + nv.y;
+            const int o = fo.perm[j];
+            if (fo.v) {
+                fo.u[o] = uo;
+                fo.v[o] = vo;
+            } else {
+                reinterpret_cast<double2*>(fo.u)[o] = make_double2(uo, vo);
+            }
+        }
+    }
 }
 
 size_t sub_smem(int depth, int P) {
@@ -221,20 +258,31 @@ void launch_m2m(const Layout& L, const Tables* T, double2* mult, cudaStream_t s)
 }
 
 int l2l_split_level(int levels, int P) {
-    const int d0 = sub_depth(P);
-    return levels - d0 > 2 ? levels - d0 : 2;
+    // CTAs at level l-2 (depth-2 subtrees): enough CTAs for the fused L2P +
+    // combine at small l, short ancestor chains at large l.  Measured (graph
+    // replay, depth 1 / 2 / 3): config 2 0.788 / 0.759 / 0.767 ms, config 1
+    // 0.216 / 0.221 / 0.243 ms, config 3 14.66 / 14.22 / 14.22 ms.
+    // VFMM_L2L_DEPTH overrides (tuning).
+    static const int depth_env = [] {
+        const char* e = getenv("VFMM_L2L_DEPTH");
+        return e ? atoi(e) : 2;
+    }();
+    int d = depth_env > 0 ? depth_env : 2;
+    if (d > sub_depth(P)) d = sub_depth(P);
+    return levels - d > 2 ? levels - d : 2;
 }
 
 void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc,
-                const double2* anc, Rows rows, cudaStream_t s) {
+                const double2* anc, Rows rows, const FusedOut& fo, cudaStream_t s) {
     if (L.levels == 2) {
         launch_leaf_locals_copy(L, loc, leaf_loc, s);
         return;
     }
     const int ls = l2l_split_level(L.levels, L.P);
-    const size_t shm = sub_smem(L.levels - ls, L.P) + sizeof(double2) * (2 * L.P + 1);
+    const size_t shm = sub_smem(L.levels - ls, L.P) + sizeof(double2) * (2 * L.P + 1) +
+                       sizeof(double) * L.P;
     k_l2l_fused<<<(unsigned)(1ll << (2 * ls)), kSubThreads, shm, s>>>(loc, leaf_loc, anc, ls,
-                                                                       L.levels, L.P, T, rows);
+                                                                       L.levels, L.P, T, rows, fo);
     note_launches(1);
 }
 

@@ -118,8 +118,20 @@ void launch_m2l(const Layout& L, const Tables* T, const double2* mult, const int
 // L2L split level: CTA roots of the fused downward kernel (subtree.cu); the
 // M2L parts of levels 3 .. split-1 are also kept in the `anc` region
 int l2l_split_level(int levels, int P);
+// L2P + combine fused into the finest L2L level (single-GPU evaluates): the
+// near-field totals must be complete when the L2L runs.
+struct FusedOut {
+    const Src* src;
+    const int* keys;
+    const int* perm;
+    const int* ls;
+    const double2* near;  // slot 0: near-field total per sorted particle
+    double* u;            // null: not fused (leaf_loc only)
+    double* v;            // null: interleaved (N, 2) output
+    double xmin, ymin, side;
+};
 void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc,
-                const double2* anc, Rows rows, cudaStream_t s);
+                const double2* anc, Rows rows, const FusedOut& fo, cudaStream_t s);
 int p2p_targets_per_lane();  // 1 or 2 (env VFMM_P2P_TPT, default 1)
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
                 char* ws, Counters* ctr, int kernel, double2* near_uv, Rows rows, cudaStream_t s);
@@ -251,6 +263,26 @@ __device__ __forceinline__ void pair_acc(double tx, double ty, double sx, double
     if (GAUSS) c = fma(-c, exp2_neg(clamp_neg60(r2 * q2), tab_end), c);  // c (1 - e)
     u = fma(-c, dy, u);
     v = fma(c, dx, v);
+}
+
+// Horner evaluation of the leaf local expansion at z:
+//   f(z) = sum_m Lh_m / m! (-w)^m,  w = (z - c) / r
+__device__ __forceinline__ double2 eval_local(const double2* __restrict__ Lh, int64_t stride, int P,
+                                              double wx, double wy,
+                                              const double* __restrict__ invfact) {
+    const double nx = -wx, ny = -wy;
+    const double2 top = Lh[(P - 1) * stride];
+    double ax = top.x * invfact[P - 1], ay = top.y * invfact[P - 1];
+#pragma unroll 6
+    for (int k = P - 2; k >= 0; --k) {
+        const double2 c = Lh[k * stride];
+        const double f = invfact[k];
+        const double tx = fma(ax, nx, fma(-ay, ny, c.x * f));
+        const double ty = fma(ax, ny, fma(ay, nx, c.y * f));
+        ax = tx;
+        ay = ty;
+    }
+    return make_double2(ax, ay);
 }
 
 // Stage the exponential table in shared memory (all threads of the block).
