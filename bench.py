@@ -12,9 +12,10 @@ inputs resident in HBM (CUDA graph replay of the C-ABI call; L2 flushed
 between steps by writing a 256 MiB buffer outside the timed events).
 ``e2e`` = the same metric through the public host-buffer API
 (``evaluate_host_async`` -> ``vfmm_evaluate_host``) with pinned HOST buffers:
-every step copies x, y, gamma, sigma in and (u, v) out inside the timed
-region; three independent evaluations are kept in flight (``HostPipeline``), so
-one step's copies overlap its neighbours' compute.  ``e2e.latency_ms`` is one
+every step copies x, y, gamma, sigma in (sigma as one value when all core
+sizes are equal) and (u, v) out inside the timed region; three independent
+evaluations are kept in flight (``HostPipeline``), so one step's copies
+overlap its neighbours' compute.  ``e2e.latency_ms`` is one
 synchronous ``evaluate_host`` call.
 
 ``--impl reference`` times the reference algorithm's CPU implementation (the
@@ -334,6 +335,8 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     e2e = (time.perf_counter() - t0) * 1e3 / k_pipe
     assert torch.equal(pend[-1].out, ref_vel.cpu()), "pipelined result differs"
+    # a uniform sigma array travels as one value (VFMM_FLAG_SIGMA_SCALAR)
+    sigma_uniform = bool((w.sigma.view(np.int64) == w.sigma.view(np.int64)[0]).all())
 
     peak = fp64_peak(lib, torch, dev)
     achieved = P2P_FLOP_PER_PAIR_GAUSS * st.near_pair_count / t_near / 1e12  # t_near in s
@@ -360,7 +363,8 @@ def run_ours(args):
                    "domain": [-1.0, -1.0, 2.0], "l2": "flushed between steps (256 MiB write)",
                    "graph": "CUDA graph replay, near field overlapped with far-field chain",
                    "m2l_count": st.m2l_count, "near_pair_count": st.near_pair_count},
-        "e2e": {"value": n / (e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 4 * 8 * n,
+        "e2e": {"value": n / (e2e * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": 3 * 8 * n + (8 if sigma_uniform else 8 * n),
                 "d2h_bytes_per_step": 2 * 8 * n, "ms_per_step": e2e,
                 "mode": f"evaluate_host_async via HostPipeline(depth={args.e2e_depth}), {k_pipe} steps, "
                         "host wall clock",

@@ -54,6 +54,8 @@ extern "C" {
 #define VFMM_FLAG_PHASE_UP 8u   /* vfmm_evaluate_shard: build + P2M + M2M only */
 #define VFMM_FLAG_PHASE_TIMES 64u /* with VFMM_FLAG_STATS: also time every phase (CUDA events between
                                    the phases; costs ~0.1 ms per call) */
+#define VFMM_FLAG_SIGMA_SCALAR 128u /* vfmm_evaluate_host: sigma points to ONE core size shared by
+                                     all particles (8 bytes copied instead of 8 N) */
 #define VFMM_FLAG_UV_PAIRS 32u  /* u is an interleaved (N, 2) array of (u, v) rows -- the reference's
                                    return layout (engine.py:394-398); v is ignored */
 #define VFMM_FLAG_PHASE_DOWN 16u /* vfmm_evaluate_shard: M2L + L2L + P2P + L2P on the workspace of a

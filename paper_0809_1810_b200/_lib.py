@@ -31,6 +31,7 @@ FLAG_FAR_ONLY = 4
 FLAG_PHASE_UP = 8
 FLAG_PHASE_DOWN = 16
 FLAG_UV_PAIRS = 32
+FLAG_SIGMA_SCALAR = 128
 
 ORDER_CAP = 60
 LEVELS_CAP = 13

@@ -321,6 +321,7 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
                   unsigned flags, Rows rows, vfmm_stats* stats, void* stream,
                   const HostIO* hio = nullptr) {
     const bool timed = (flags & VFMM_FLAG_STATS) != 0;
+    const bool sigma_scalar = (flags & VFMM_FLAG_SIGMA_SCALAR) != 0 && hio != nullptr;
     const bool far_only = (flags & VFMM_FLAG_FAR_ONLY) != 0;
     bool up = (flags & VFMM_FLAG_PHASE_UP) != 0, down = (flags & VFMM_FLAG_PHASE_DOWN) != 0;
     if (!up && !down) up = down = true;
@@ -381,7 +382,9 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         cudaMemcpyAsync(dy, hio->hy, b, cudaMemcpyHostToDevice, s);
         cudaEventRecord(R->xy, s);
         cudaMemcpyAsync(dg, hio->hg, b, cudaMemcpyHostToDevice, s);
-        if (hio->hs) cudaMemcpyAsync(dsg, hio->hs, b, cudaMemcpyHostToDevice, s);
+        // VFMM_FLAG_SIGMA_SCALAR: one core size for all (8 bytes instead of 8 N)
+        if (hio->hs) cudaMemcpyAsync(dsg, hio->hs, sigma_scalar ? sizeof(double) : b,
+                                     cudaMemcpyHostToDevice, s);
         cudaEventRecord(R->gs, s);
         cudaStreamWaitEvent(R->comp, R->xy, 0);
         cs = R->comp;
@@ -400,7 +403,7 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         // ---- build: binning, stable sort, pack, leaf starts, occupancy, tasks ----
         launch_init_counters(ctr, cs);
         launch_build(L, x, y, gamma, kernel == VFMM_KERNEL_GAUSSIAN ? sigma : nullptr, xmin, ymin,
-                     side, ws, ctr, cs, &keys, &perm, gs_ready);
+                     side, ws, ctr, cs, &keys, &perm, gs_ready, sigma_scalar ? 0 : 1);
         launch_counts_tasks(L, ws, ctr, !far_only, rows, kernel == VFMM_KERNEL_GAUSSIAN, cs);
         rec(1, cs);
         // Overlap: the far-field chain and the near field run on two streams

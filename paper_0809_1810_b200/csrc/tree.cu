@@ -190,9 +190,10 @@ template <int E>
 __device__ __forceinline__ void leaf_pack(const int* __restrict__ slot, int lo, int c, int leaf,
                                           const double* __restrict__ x, const double* __restrict__ y,
                                           const double* __restrict__ g,
-                                          const double* __restrict__ sigma, int* __restrict__ keys,
-                                          int* __restrict__ perm, Src* __restrict__ src,
-                                          unsigned long long& smax, unsigned long long& smin) {
+                                          const double* __restrict__ sigma, int sstride,
+                                          int* __restrict__ keys, int* __restrict__ perm,
+                                          Src* __restrict__ src, unsigned long long& smax,
+                                          unsigned long long& smin) {
     const int lane = threadIdx.x & 31;
     int e[E];
 #pragma unroll
@@ -206,7 +207,7 @@ __device__ __forceinline__ void leaf_pack(const int* __restrict__ slot, int lo, 
         const int p = k * 32 + lane;
         if (p >= c) continue;
         const int idx = e[k];
-        const double s = sigma ? sigma[idx] : 1.0;
+        const double s = sigma ? sigma[(int64_t)idx * sstride] : 1.0;
         Src r;
         r.x = x[idx];
         r.y = y[idx];
@@ -228,7 +229,7 @@ __device__ __forceinline__ void leaf_pack(const int* __restrict__ slot, int lo, 
 __global__ void __launch_bounds__(256)
     k_leaf_pack(const int* __restrict__ ls, const int* __restrict__ slot, int nleaves,
                 const double* __restrict__ x, const double* __restrict__ y,
-                const double* __restrict__ g, const double* __restrict__ sigma,
+                const double* __restrict__ g, const double* __restrict__ sigma, int sstride,
                 int* __restrict__ keys, int* __restrict__ perm, Src* __restrict__ src,
                 Counters* __restrict__ ctr) {
     if (ctr->sort_fallback) return;
@@ -238,11 +239,11 @@ __global__ void __launch_bounds__(256)
     for (int leaf = blockIdx.x * 8 + warp; leaf < nleaves; leaf += gridDim.x * 8) {
         const int lo = ls[leaf], c = ls[leaf + 1] - lo;
         if (c > 64)
-            leaf_pack<4>(slot, lo, c, leaf, x, y, g, sigma, keys, perm, src, smax, smin);
+            leaf_pack<4>(slot, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin);
         else if (c > 32)
-            leaf_pack<2>(slot, lo, c, leaf, x, y, g, sigma, keys, perm, src, smax, smin);
+            leaf_pack<2>(slot, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin);
         else if (c > 0)
-            leaf_pack<1>(slot, lo, c, leaf, x, y, g, sigma, keys, perm, src, smax, smin);
+            leaf_pack<1>(slot, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin);
     }
     if (!sigma) return;
     for (int o = 16; o > 0; o >>= 1) {
@@ -271,15 +272,15 @@ __global__ void __launch_bounds__(256)
 // four arrays element by element.
 __global__ void __launch_bounds__(256)
     k_pack_orig(const double* __restrict__ x, const double* __restrict__ y,
-                const double* __restrict__ g, const double* __restrict__ sigma, int64_t n,
-                Src* __restrict__ out, Counters* __restrict__ ctr) {
+                const double* __restrict__ g, const double* __restrict__ sigma, int sstride,
+                int64_t n, Src* __restrict__ out, Counters* __restrict__ ctr) {
     if (!ctr->sort_fallback) return;
     __shared__ unsigned long long wmax[8], wmin[8];
     unsigned long long sbits = 0ull, smin = ~0ull;
     // grid-stride (a small grid: the launch is cheap when the counting path ran)
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const double s = sigma ? sigma[i] : 1.0;
+        const double s = sigma ? sigma[i * sstride] : 1.0;
         Src r;
         r.x = x[i];
         r.y = y[i];
@@ -738,7 +739,7 @@ void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream
 void launch_build(const Layout& L, const double* x, const double* y, const double* g,
                   const double* sigma, double xmin, double ymin, double side, char* ws,
                   Counters* ctr, cudaStream_t s, int** keys_out, int** perm_out,
-                  cudaEvent_t gs_ready) {
+                  cudaEvent_t gs_ready, int sigma_stride) {
     int* kbuf[2] = {(int*)(ws + L.key_a), (int*)(ws + L.key_b)};
     int* vbuf[2] = {(int*)(ws + L.val_a), (int*)(ws + L.val_b)};
     const int bits = L.digit_bits;
@@ -771,7 +772,8 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     // copies overlap the binning)
     if (gs_ready) cudaStreamWaitEvent(s, gs_ready, 0);
     k_leaf_pack<<<std::min(grid_for((int64_t)L.nleaves, 8), 2368u), 256, 0, s>>>(ls, slot, (int)L.nleaves, x, y, g,
-                                                              sigma, fkeys, fperm, src, ctr);
+                                                              sigma, sigma_stride, fkeys, fperm,
+                                                              src, ctr);
     note_launches(1);
 
     // ---- LSD radix path (kernels return at once unless ctr->sort_fallback) ----
@@ -788,7 +790,8 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     for (int p = 0; p < L.passes; ++p) {
         const bool last = p == L.passes - 1;
         if (last) {
-            k_pack_orig<<<small_grid(L.n), 256, 0, s>>>(x, y, g, sigma, L.n, packed, ctr);
+            k_pack_orig<<<small_grid(L.n), 256, 0, s>>>(x, y, g, sigma, sigma_stride, L.n, packed,
+                                                          ctr);
             note_launches(1);
         }
         k_onesweep<<<tiles, kTileThreads, 0, s>>>(

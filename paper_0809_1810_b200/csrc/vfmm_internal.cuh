@@ -98,7 +98,7 @@ void note_launches(int k);
 void launch_build(const Layout& L, const double* x, const double* y, const double* g,
                   const double* sigma, double xmin, double ymin, double side, char* ws,
                   Counters* ctr, cudaStream_t s, int** keys_out, int** perm_out,
-                  cudaEvent_t gs_ready = nullptr);
+                  cudaEvent_t gs_ready = nullptr, int sigma_stride = 1);
 void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream_t s,
                      const Counters* sym_skip, bool gauss, const int* skip_flag = nullptr,
                      int skip_val = 0);

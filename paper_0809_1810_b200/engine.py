@@ -299,8 +299,19 @@ class PendingEvaluation:
         return self.out, _stats_from(st)
 
 
+def _uniform_sigma(keep_entry):
+    """The shared core size when every sigma is bitwise identical, else None."""
+    obj = keep_entry[0]
+    arr = obj.numpy() if isinstance(obj, torch.Tensor) else np.asarray(obj)
+    if arr.size == 0:
+        return None
+    bits = arr.reshape(-1).view(np.int64)
+    return float(arr.reshape(-1)[0]) if bool((bits == bits[0]).all()) else None
+
+
 def evaluate_host_async(x, y, gamma, sigma, config, domain, *, out: torch.Tensor,
-                        workspace: "Workspace", stream: torch.cuda.Stream, overlap: bool = True):
+                        workspace: "Workspace", stream: torch.cuda.Stream, overlap: bool = True,
+                        scalar_sigma: bool = True):
     """Asynchronous :func:`evaluate_host` (``vfmm_evaluate_host`` without
     VFMM_FLAG_STATS): enqueues the copies and the evaluation on ``stream`` and
     returns a :class:`PendingEvaluation` at once.  Calls on distinct streams
@@ -308,7 +319,10 @@ def evaluate_host_async(x, y, gamma, sigma, config, domain, *, out: torch.Tensor
     overlap the compute of its neighbours -- which is how a batch of
     independent evaluations reaches the PCIe / compute bound instead of
     their sum.  ``x .. sigma`` and ``out`` must stay alive (and unchanged)
-    until :meth:`PendingEvaluation.result`; pinned memory for full speed."""
+    until :meth:`PendingEvaluation.result`; pinned memory for full speed.
+    With ``scalar_sigma`` a sigma array whose entries are all bitwise equal
+    is sent as one value (VFMM_FLAG_SIGMA_SCALAR; the host check is hidden
+    behind the previous evaluation's GPU work when calls are pipelined)."""
     validate_config(config)
     require_cuda()
     lib = _lib.load()
@@ -320,8 +334,20 @@ def evaluate_host_async(x, y, gamma, sigma, config, domain, *, out: torch.Tensor
         raise ValueError("out must be a contiguous host (N, 2) float64 tensor")
     code = kernel_code(config.kernel)
     flags = _lib.FLAG_UV_PAIRS | (_lib.FLAG_OVERLAP if overlap else 0)
+    sig_ptr = keep[3][1]
+    if code == _lib.KERNEL_GAUSSIAN and scalar_sigma:
+        one = _uniform_sigma(keep[3])
+        if one is not None:
+            # one pinned value per workspace (its previous call has completed
+            # when the workspace is reused)
+            scalar = getattr(workspace, "_sigma_scalar", None)
+            if scalar is None:
+                scalar = workspace._sigma_scalar = torch.empty(1, dtype=torch.float64).pin_memory()
+            scalar[0] = one
+            sig_ptr = scalar.data_ptr()
+            flags |= _lib.FLAG_SIGMA_SCALAR
     status = lib.vfmm_evaluate_host(
-        keep[0][1], keep[1][1], keep[2][1], keep[3][1] if code == _lib.KERNEL_GAUSSIAN else None, n,
+        keep[0][1], keep[1][1], keep[2][1], sig_ptr if code == _lib.KERNEL_GAUSSIAN else None, n,
         float(domain.xmin), float(domain.ymin), float(domain.side), config.levels, config.order,
         code, out.data_ptr(), None, workspace.ptr, workspace.nbytes, flags, None, stream.cuda_stream,
     )
