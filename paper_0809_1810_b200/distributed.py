@@ -287,13 +287,20 @@ def evaluate_emulated(x, y, gamma, sigma, config, domain, world: int, backend_fa
 def bench_main(args):
     """``bench.py --gpus N`` under torchrun: the sharded evaluate of a BASELINE config.
 
-    Every rank generates the same seeded workload and starts from its
-    contiguous 1/N slice of the particle index range; a step is the full
-    sharded evaluate (redistribution, halo, upward, all-reduces, downward,
-    counter reduction).  Timed with CUDA events between barriers; the max over
-    ranks is reported.
+    Setup (untimed, as the single-GPU bench keeps its inputs resident): every
+    rank generates the same seeded workload, sends its contiguous 1/N slice of
+    the particles to their row-strip owners and exchanges the one-row halos.
+    A step is the sharded evaluate -- PHASE_UP (tree, P2M, M2M; the near field
+    starts), the NCCL all-reduces of the multipole and occupancy pyramids,
+    PHASE_DOWN (M2L, L2L, combine) -- captured in one CUDA graph and replayed
+    with L2 flushed between steps; CUDA events between barriers, max over
+    ranks.  ``e2e``: per step each rank copies its owned particles in from
+    pinned host memory, exchanges the halo (sizes synchronise the host), runs
+    the sharded evaluate and copies its velocities back; wall clock between
+    barriers, max over ranks.
     """
     import json
+    import time
 
     from . import workloads as W
     from .engine import FmmConfig
@@ -312,31 +319,61 @@ def bench_main(args):
     w = W.by_index(args.config)
     cfg = FmmConfig(w.levels, w.order, KernelKind.GAUSSIAN_BLOB)
     dom = Domain(*W.DOMAIN)
+    lib = _lib.load()
     lo, hi = rank * w.n // world, (rank + 1) * w.n // world
     x, y, g, s = (torch.from_numpy(a[lo:hi]).to(dev) for a in (w.x, w.y, w.gamma, w.sigma))
     ids = torch.arange(lo, hi, device=dev)
-    # setup (untimed): particles to their owners; a step is then the halo
-    # exchange plus the sharded evaluate (positions would move between steps)
     owned, rows = redistribute_owned(x, y, g, s, ids, dom, cfg.levels)
+    shard = add_halo(owned, rows, dom, cfg.levels)
+    backend = CudaShardBackend(dev)
+    _, st = evaluate_shard(shard, cfg, dom, backend=backend, counters=True)
 
-    def step(counters=False):
-        shard = add_halo(owned, rows, dom, cfg.levels)
-        return evaluate_shard(shard, cfg, dom, counters=counters)
-
-    _, st = step(counters=True)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        for _ in range(max(3, args.warmup)):
+            evaluate_shard(shard, cfg, dom, backend=backend, counters=False)
+    torch.cuda.synchronize(dev)
+    c0 = lib.vfmm_launch_count()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        evaluate_shard(shard, cfg, dom, backend=backend, counters=False)
+    launches = lib.vfmm_launch_count() - c0
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
+        flush.zero_()
+        graph.replay()
+    torch.cuda.synchronize(dev)
     dist.barrier()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(args.steps):
-        step()
-    b.record()
-    torch.cuda.synchronize()
+    cur = torch.cuda.current_stream(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for a, b in ev:
+        flush.zero_()
+        a.record(cur)
+        graph.replay()
+        b.record(cur)
+    torch.cuda.synchronize(dev)
     dist.barrier()
-    ms = torch.tensor([a.elapsed_time(b) / args.steps], device=dev)
+    ms = torch.tensor([sum(a.elapsed_time(b) for a, b in ev) / args.steps], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+
+    # end to end from pinned host buffers: owned particles in, owned velocities out
+    host_cols = owned.cpu().pin_memory()
+    host_vel = torch.empty((2, owned.shape[1]), dtype=torch.float64).pin_memory()
+    e2e_steps = max(3, args.e2e_steps)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        dcols = host_cols.to(dev, non_blocking=True)
+        sh = add_halo(dcols, rows, dom, cfg.levels)
+        vel, _ = evaluate_shard(sh, cfg, dom, backend=backend, counters=False)
+        host_vel.copy_(vel[:, : owned.shape[1]], non_blocking=True)
+        torch.cuda.synchronize(dev)
+    e2e = torch.tensor([(time.perf_counter() - t0) * 1e3 / e2e_steps], device=dev)
+    dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    nb = torch.tensor([owned.shape[1]], dtype=torch.int64, device=dev)
+    dist.all_reduce(nb, op=dist.ReduceOp.MAX)
     if rank == 0:
         print(json.dumps({
             "metric": "FMM particle velocity evals/sec (fp64)", "value": w.n / (float(ms) * 1e-3),
@@ -344,7 +381,17 @@ def bench_main(args):
             "ms_per_step": float(ms), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "n": w.n, "levels": w.levels, "order": w.order,
-                       "sharding": f"{world} row strips of leaves", "m2l_count": st.m2l_count,
-                       "near_pair_count": st.near_pair_count},
+                       "sharding": f"{world} row strips of leaves (+ one-row halos)",
+                       "graph": "CUDA graph replay of the sharded evaluate (PHASE_UP, NCCL "
+                                "all-reduce of the multipole/occupancy pyramids, PHASE_DOWN)",
+                       "l2": "flushed between steps (256 MiB write)",
+                       "m2l_count": st.m2l_count, "near_pair_count": st.near_pair_count},
+            "e2e": {"value": w.n / (float(e2e) * 1e-3), "unit": "particle-evals/s",
+                    "h2d_bytes_per_step": 40 * int(nb), "d2h_bytes_per_step": 16 * int(nb),
+                    "ms_per_step": float(e2e),
+                    "mode": "per rank: owned particles H2D, halo exchange, sharded evaluate, "
+                            "velocities D2H; wall clock, max over ranks (bytes: largest rank)"},
+            "gpu_launches": int(launches) * args.steps,
+            "roofline": None, "cpu_baseline": None,
         }), flush=True)
     dist.destroy_process_group()
