@@ -60,6 +60,11 @@ extern "C" {
                                    return layout (engine.py:394-398); v is ignored */
 #define VFMM_FLAG_PHASE_DOWN 16u /* vfmm_evaluate_shard: M2L + L2L + P2P + L2P on the workspace of a
                                     previous PHASE_UP call (after the caller reduced the multipoles) */
+#define VFMM_FLAG_GRAPH 256u    /* vfmm_evaluate_host: run the device part as a CUDA graph, captured
+                                   on first use and cached per (device, workspace, n, levels, order,
+                                   kernel, domain, flags); the copies stay plain async copies on
+                                   `stream` around the graph launch.  Not with VFMM_FLAG_PHASE_TIMES
+                                   (falls back to stream launches), nor while `stream` is capturing */
 
 /* engine.FmmRunStats (engine.py:58-74).  Times in milliseconds (CUDA events). */
 typedef struct vfmm_stats {
@@ -117,7 +122,10 @@ int vfmm_evaluate(const double* x, const double* y, const double* gamma, const d
  * `stream`.  Synchronous on `stream` only if VFMM_FLAG_STATS is set.  Without
  * it, calls on distinct streams AND distinct workspaces pipeline: the copies
  * of one call overlap the compute of the previous one (the compute itself is
- * serialised on the library's internal per-device streams).                 */
+ * serialised on the library's internal per-device streams).  With
+ * VFMM_FLAG_GRAPH the compute is one cached CUDA-graph launch on `stream`
+ * after all input copies (no launch gaps; graphs of distinct workspaces may
+ * run concurrently).                                                        */
 int vfmm_evaluate_host(const double* x, const double* y, const double* gamma, const double* sigma,
                        int64_t n, double xmin, double ymin, double side, int levels, int order,
                        int kernel, double* u, double* v, void* workspace, size_t workspace_bytes,

@@ -32,6 +32,7 @@ FLAG_PHASE_UP = 8
 FLAG_PHASE_DOWN = 16
 FLAG_UV_PAIRS = 32
 FLAG_SIGMA_SCALAR = 128
+FLAG_GRAPH = 256
 
 ORDER_CAP = 60
 LEVELS_CAP = 13

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <atomic>
 #include <mutex>
+#include <vector>
 
 #include "vfmm_internal.cuh"
 
@@ -319,9 +320,11 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
                   int64_t n, double xmin, double ymin, double side, int levels, int order,
                   int kernel, double* u, double* v, void* workspace, size_t workspace_bytes,
                   unsigned flags, Rows rows, vfmm_stats* stats, void* stream,
-                  const HostIO* hio = nullptr) {
+                  const HostIO* hio = nullptr, bool sigma_one = false) {
     const bool timed = (flags & VFMM_FLAG_STATS) != 0;
-    const bool sigma_scalar = (flags & VFMM_FLAG_SIGMA_SCALAR) != 0 && hio != nullptr;
+    // one core size for all particles: host mode (VFMM_FLAG_SIGMA_SCALAR) or
+    // the device part of a graph-replayed host call (sigma_one)
+    const bool sigma_scalar = ((flags & VFMM_FLAG_SIGMA_SCALAR) != 0 && hio != nullptr) || sigma_one;
     const bool far_only = (flags & VFMM_FLAG_FAR_ONLY) != 0;
     bool up = (flags & VFMM_FLAG_PHASE_UP) != 0, down = (flags & VFMM_FLAG_PHASE_DOWN) != 0;
     if (!up && !down) up = down = true;
@@ -555,6 +558,144 @@ int vfmm_evaluate(const double* x, const double* y, const double* gamma, const d
                          Rows{0, 1 << levels}, stats, stream);
 }
 
+namespace {
+
+// Cached CUDA graphs of the device part of vfmm_evaluate_host
+// (VFMM_FLAG_GRAPH): staged inputs -> staged (u, v).  Everything a graph
+// bakes in is part of the key; the graph reads / writes only the workspace.
+struct HostGraph {
+    int dev;
+    const void* ws;
+    int64_t n;
+    int levels, order, kernel;
+    unsigned flags;
+    double xmin, ymin, side;
+    cudaGraphExec_t exec;
+    long long launches;  // kernels per replay
+    unsigned long long used;
+};
+std::mutex g_graph_mu;
+std::vector<HostGraph> g_graphs;
+unsigned long long g_graph_tick = 0;
+constexpr size_t kMaxGraphs = 32;
+
+// Returns VFMM_OK after enqueueing copies + graph + copies on `s`, or -1 when
+// the graph path does not apply (the caller falls back to stream launches).
+int evaluate_host_graph(const HostIO& io, int64_t n, double xmin, double ymin, double side,
+                        int levels, int order, int kernel, void* workspace,
+                        size_t workspace_bytes, unsigned flags, vfmm_stats* stats, void* stream) {
+    const bool timed = (flags & VFMM_FLAG_STATS) != 0;
+    if (flags & (VFMM_FLAG_PHASE_TIMES | VFMM_FLAG_PHASE_UP | VFMM_FLAG_PHASE_DOWN |
+                 VFMM_FLAG_FAR_ONLY))
+        return -1;
+    if (!args_ok(n, levels, order, side, kernel) || !std::isfinite(xmin) || !std::isfinite(ymin))
+        return VFMM_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cst) != cudaSuccess || cst != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return -1;
+    }
+    Layout L;
+    make_layout(n, levels, order, &L);
+    if (!workspace || workspace_bytes < L.total) return VFMM_EWORKSPACE;
+    int dev = 0;
+    if (current_device_of(workspace, &dev) != 0) return VFMM_ECUDA;
+    Resources* R = resources_for(dev);
+    if (!R || !tables_for(dev)) return VFMM_ECUDA;
+    char* ws = (char*)workspace;
+    double* st = (double*)(ws + L.stage);
+    double *dx = st, *dy = st + n, *dg = st + 2 * n, *dsg = st + 3 * n, *du = st + 4 * n,
+           *dv = st + 5 * n;
+    const bool gauss = kernel == VFMM_KERNEL_GAUSSIAN;
+    const bool one = gauss && (flags & VFMM_FLAG_SIGMA_SCALAR) != 0;
+    const bool pairs = (flags & VFMM_FLAG_UV_PAIRS) != 0;
+    // flags of the captured device evaluate (no stats: counters are read after the replay)
+    const unsigned dflags = flags & (VFMM_FLAG_OVERLAP | VFMM_FLAG_UV_PAIRS);
+    const unsigned kflags = dflags | (one ? VFMM_FLAG_SIGMA_SCALAR : 0u);
+
+    cudaGraphExec_t exec = nullptr;
+    long long nl = 0;
+    {
+        std::lock_guard<std::mutex> lk(g_graph_mu);
+        for (auto& g : g_graphs)
+            if (g.dev == dev && g.ws == workspace && g.n == n && g.levels == levels &&
+                g.order == order && g.kernel == kernel && g.flags == kflags && g.xmin == xmin &&
+                g.ymin == ymin && g.side == side) {
+                g.used = ++g_graph_tick;
+                exec = g.exec;
+                nl = g.launches;
+                break;
+            }
+        if (!exec) {
+            // capture on the library's compute stream (thread-local mode: other
+            // threads' unrelated CUDA calls do not invalidate the capture)
+            cudaStream_t cap = R->comp;
+            const long long before = g_launches.load();
+            if (cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+                cudaGetLastError();
+                return -1;
+            }
+            const int rc = evaluate_impl(dx, dy, dg, gauss ? dsg : nullptr, n, xmin, ymin, side,
+                                         levels, order, kernel, du, pairs ? nullptr : dv, workspace,
+                                         workspace_bytes, dflags, Rows{0, 1 << levels}, nullptr,
+                                         cap, nullptr, one);
+            cudaGraph_t graph = nullptr;
+            const cudaError_t ec = cudaStreamEndCapture(cap, &graph);
+            nl = g_launches.load() - before;
+            g_launches.fetch_sub(nl);  // counted per replay instead
+            if (rc != VFMM_OK || ec != cudaSuccess || !graph) {
+                if (graph) cudaGraphDestroy(graph);
+                cudaGetLastError();
+                return rc != VFMM_OK ? rc : -1;
+            }
+            const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (ei != cudaSuccess) {
+                cudaGetLastError();
+                return -1;
+            }
+            if (g_graphs.size() >= kMaxGraphs) {  // evict the least recently used
+                size_t lru = 0;
+                for (size_t i = 1; i < g_graphs.size(); ++i)
+                    if (g_graphs[i].used < g_graphs[lru].used) lru = i;
+                cudaGraphExecDestroy(g_graphs[lru].exec);
+                g_graphs.erase(g_graphs.begin() + (long)lru);
+            }
+            g_graphs.push_back(HostGraph{dev, workspace, n, levels, order, kernel, kflags, xmin,
+                                         ymin, side, exec, nl, ++g_graph_tick});
+        }
+    }
+    if (timed) cudaEventRecord(R->ev[0], s);
+    const size_t b = sizeof(double) * (size_t)n;
+    cudaMemcpyAsync(dx, io.hx, b, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(dy, io.hy, b, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(dg, io.hg, b, cudaMemcpyHostToDevice, s);
+    if (gauss) cudaMemcpyAsync(dsg, io.hs, one ? sizeof(double) : b, cudaMemcpyHostToDevice, s);
+    if (cudaGraphLaunch(exec, s) != cudaSuccess) return VFMM_ECUDA;
+    note_launches((int)nl);
+    if (pairs) {
+        cudaMemcpyAsync(io.hu, du, 2 * b, cudaMemcpyDeviceToHost, s);
+    } else {
+        cudaMemcpyAsync(io.hu, du, b, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(io.hv, dv, b, cudaMemcpyDeviceToHost, s);
+    }
+    if (!timed) return cudaGetLastError() == cudaSuccess ? VFMM_OK : VFMM_ECUDA;
+    if (!stats) return VFMM_EINVAL;
+    Counters* ctr = (Counters*)(ws + L.counters);
+    cudaMemcpyAsync(R->hctr, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s);
+    cudaEventRecord(R->ev[6], s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return VFMM_ECUDA;
+    const Counters c = *R->hctr;
+    std::memset(stats, 0, sizeof(*stats));
+    fill_stats(L, c, kernel, side, stats);
+    stats->overlapped = (dflags & VFMM_FLAG_OVERLAP) ? 1 : 0;
+    stats->t_total = elapsed(R->ev[0], R->ev[6]);
+    return c.bad_count ? VFMM_EDOMAIN : VFMM_OK;
+}
+
+}  // namespace
+
 int vfmm_evaluate_host(const double* x, const double* y, const double* gamma, const double* sigma,
                        int64_t n, double xmin, double ymin, double side, int levels, int order,
                        int kernel, double* u, double* v, void* workspace, size_t workspace_bytes,
@@ -564,6 +705,11 @@ int vfmm_evaluate_host(const double* x, const double* y, const double* gamma, co
         (kernel == VFMM_KERNEL_GAUSSIAN && !sigma))
         return VFMM_EINVAL;
     const HostIO io{x, y, gamma, kernel == VFMM_KERNEL_GAUSSIAN ? sigma : nullptr, u, v};
+    if (flags & VFMM_FLAG_GRAPH) {
+        const int rc = evaluate_host_graph(io, n, xmin, ymin, side, levels, order, kernel,
+                                           workspace, workspace_bytes, flags, stats, stream);
+        if (rc >= 0) return rc;
+    }
     // staging pointers are substituted inside; pass the host ones for the argument checks
     return evaluate_impl(x, y, gamma, sigma, n, xmin, ymin, side, levels, order, kernel, u, v,
                          workspace, workspace_bytes,

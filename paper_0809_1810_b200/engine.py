@@ -217,6 +217,7 @@ def evaluate_host(
     out: torch.Tensor | None = None,
     overlap: bool = True,
     timings: bool = False,
+    graph: bool = False,
     stacklevel: int = 2,
 ):
     """Host-buffer fast path (``vfmm_evaluate_host``): numpy arrays or CPU (ideally
@@ -246,7 +247,7 @@ def evaluate_host(
         raise ValueError("out must be a contiguous host (N, 2) float64 tensor")
     st = _lib.VfmmStats()
     flags = (_lib.FLAG_STATS | _lib.FLAG_UV_PAIRS | (_lib.FLAG_OVERLAP if overlap else 0)
-             | (_lib.FLAG_PHASE_TIMES if timings else 0))
+             | (_lib.FLAG_PHASE_TIMES if timings else 0) | (_lib.FLAG_GRAPH if graph else 0))
     status = lib.vfmm_evaluate_host(
         keep[0][1], keep[1][1], keep[2][1], keep[3][1] if code == _lib.KERNEL_GAUSSIAN else None, n,
         float(domain.xmin), float(domain.ymin), float(domain.side), config.levels, config.order,
@@ -311,7 +312,7 @@ def _uniform_sigma(keep_entry):
 
 def evaluate_host_async(x, y, gamma, sigma, config, domain, *, out: torch.Tensor,
                         workspace: "Workspace", stream: torch.cuda.Stream, overlap: bool = True,
-                        scalar_sigma: bool = True):
+                        scalar_sigma: bool = True, graph: bool = True):
     """Asynchronous :func:`evaluate_host` (``vfmm_evaluate_host`` without
     VFMM_FLAG_STATS): enqueues the copies and the evaluation on ``stream`` and
     returns a :class:`PendingEvaluation` at once.  Calls on distinct streams
@@ -322,7 +323,10 @@ def evaluate_host_async(x, y, gamma, sigma, config, domain, *, out: torch.Tensor
     until :meth:`PendingEvaluation.result`; pinned memory for full speed.
     With ``scalar_sigma`` a sigma array whose entries are all bitwise equal
     is sent as one value (VFMM_FLAG_SIGMA_SCALAR; the host check is hidden
-    behind the previous evaluation's GPU work when calls are pipelined)."""
+    behind the previous evaluation's GPU work when calls are pipelined).
+    With ``graph`` (default) the device part is one cached CUDA-graph launch
+    per call (VFMM_FLAG_GRAPH; captured on the first call of each
+    workspace / shape / domain)."""
     validate_config(config)
     require_cuda()
     lib = _lib.load()
@@ -333,7 +337,7 @@ def evaluate_host_async(x, y, gamma, sigma, config, domain, *, out: torch.Tensor
     if tuple(out.shape) != (n, 2) or not out.is_contiguous() or out.is_cuda:
         raise ValueError("out must be a contiguous host (N, 2) float64 tensor")
     code = kernel_code(config.kernel)
-    flags = _lib.FLAG_UV_PAIRS | (_lib.FLAG_OVERLAP if overlap else 0)
+    flags = _lib.FLAG_UV_PAIRS | (_lib.FLAG_OVERLAP if overlap else 0) | (_lib.FLAG_GRAPH if graph else 0)
     sig_ptr = keep[3][1]
     if code == _lib.KERNEL_GAUSSIAN and scalar_sigma:
         one = _uniform_sigma(keep[3])
@@ -366,11 +370,12 @@ class HostPipeline:
     A slot's previous result is waited for before the slot is reused, so
     results must be consumed (copied) before ``depth`` further submissions."""
 
-    def __init__(self, n: int, config, domain, *, depth: int = 2, device=None, overlap: bool = True):
+    def __init__(self, n: int, config, domain, *, depth: int = 2, device=None, overlap: bool = True,
+                 graph: bool = True):
         validate_config(config)
         require_cuda()
         dev = device_of(device)
-        self.n, self.config, self.domain, self.overlap = n, config, domain, overlap
+        self.n, self.config, self.domain, self.overlap, self.graph = n, config, domain, overlap, graph
         self.slots = [(Workspace(n, config.levels, config.order, dev), torch.cuda.Stream(dev),
                        torch.empty((n, 2), dtype=torch.float64, pin_memory=True)) for _ in range(depth)]
         self.pending = [None] * depth
@@ -383,7 +388,8 @@ class HostPipeline:
             self.pending[i].result()
         ws, stream, out = self.slots[i]
         self.pending[i] = evaluate_host_async(x, y, gamma, sigma, self.config, self.domain, out=out,
-                                              workspace=ws, stream=stream, overlap=self.overlap)
+                                              workspace=ws, stream=stream, overlap=self.overlap,
+                                              graph=self.graph)
         return self.pending[i]
 
 

@@ -328,3 +328,43 @@ def test_host_pipeline_matches_synchronous_call():
     for k, o in enumerate(outs):
         assert torch.equal(o, ref * (1.0 + k)) or np.abs((o - ref * (1.0 + k)).numpy()).max() <= 1e-13 * np.abs(ref.numpy()).max() * (1 + k)
     assert st2.near_pair_count == st.near_pair_count and st2.m2l_count == st.m2l_count
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["lattice", "random_order", "mixed_sigma"])
+def test_host_graph_path_matches_stream_launches(case):
+    """VFMM_FLAG_GRAPH (cached CUDA graph of the device part) gives bitwise the
+    stream-launched results: a coherent input (counting sort, symmetric P2P),
+    a random-order one (LSD radix path chosen on the device inside the graph)
+    and per-particle core sizes (generic P2P); replays reuse the cached graph
+    with new input values, a different domain gets its own graph."""
+    from paper_0809_1810_b200 import _lib
+
+    rng = np.random.default_rng(7)
+    if case == "lattice":
+        w = W.config1()
+        x, y, g, s = w.x, w.y, w.gamma, w.sigma
+        levels, order = w.levels, w.order
+    else:
+        n = 20000
+        x, y = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+        g = rng.standard_normal(n) * 1e-4
+        s = np.full(n, 0.01) if case == "random_order" else rng.uniform(0.005, 0.01, n)
+        levels, order = 5, 12
+    cfg = vf.FmmConfig(levels, order, vf.KernelKind.GAUSSIAN_BLOB)
+    pinned = tuple(torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (x, y, g, s))
+    for dom in (vf.Domain(*W.DOMAIN), vf.Domain(-1.5, -1.5, 3.0)):
+        ref, st = vf.evaluate_host(*pinned, cfg, dom, graph=False)
+        for scale in (1.0, -2.5):  # first call captures, the second replays the cached graph
+            gin = pinned[2] * scale
+            want = ref * scale if scale == 1.0 else vf.evaluate_host(pinned[0], pinned[1], gin, pinned[3],
+                                                                      cfg, dom, graph=False)[0]
+            before = _lib.load().vfmm_launch_count()
+            got, st2 = vf.evaluate_host(pinned[0], pinned[1], gin, pinned[3], cfg, dom, graph=True)
+            assert _lib.load().vfmm_launch_count() > before
+            assert torch.equal(got, want)
+            assert st2.m2l_count == st.m2l_count and st2.near_pair_count == st.near_pair_count
+        pipe = vf.HostPipeline(x.size, cfg, dom, depth=2, graph=True)
+        pend = [pipe.submit(*pinned) for _ in range(2)]
+        for p in pend:
+            assert torch.equal(p.result(), ref)
