@@ -37,21 +37,25 @@ __device__ __forceinline__ void il_offset(int px, int py, int o, int& dx, int& d
 }
 
 // Block = 32 destinations j of one parity plane x one chunk of TN outputs, as
-// kGroups warps: warp g accumulates the offsets [9g, 9g + 9) of the parity
+// kGroups warps: warp g accumulates the offsets [27g/G, 27(g+1)/G) of the parity
 // class (row-major order, engine.py:166-185) and the partial sums are added
 // in group order through shared memory (deterministic).  With the planar
 // layout the source of offset (dx, dy) for consecutive destinations is a run
 // of consecutive cells of one source plane, so each multipole coefficient
 // load is coalesced; the Hankel rows are block-uniform smem broadcasts.
-constexpr int kGroups = 3;
+// G = 3 offset groups (8 CTAs of 3 warps per SM) for large grids; G = 9
+// (3 CTAs of 9 warps) when the 3-group grid is under ~4 waves: each warp has a
+// third of the work, so the last partial wave is short.  Measured (median
+// t_m2l): config 1 0.0215 -> 0.0155 ms, config 2 0.0911 -> 0.0891 ms with
+// G = 9; config 3 1.50 ms (G = 3) vs 1.61 ms (G = 9).
 constexpr int kDestPerBlock = 32;
 
 // Multipole source for destinations whose source is empty / outside the grid:
 // a zero coefficient read with stride 0 (no per-coefficient select).
 __device__ const double2 g_zero_coef = {0.0, 0.0};
 
-template <int TN>
-__global__ void __launch_bounds__(kDestPerBlock * kGroups, 8)
+template <int TN, int kGroups>
+__global__ void __launch_bounds__(kDestPerBlock * kGroups, kGroups == 3 ? 8 : 3)
     k_m2l(const double2* __restrict__ mult, const int* __restrict__ counts, double2* __restrict__ loc,
           double2* __restrict__ anc, int anc_end, int levels, int P, int nchunks,
           const Tables* __restrict__ T, unsigned long long* __restrict__ m2l_count, Rows rows) {
@@ -114,7 +118,8 @@ __global__ void __launch_bounds__(kDestPerBlock * kGroups, 8)
 #pragma unroll
     for (int t = 0; t < TN; ++t) ax[t] = ay[t] = 0.0;
     int ntrans = 0;
-    for (int o = 9 * group; o < 9 * group + 9; ++o) {
+    constexpr int kOffPerGroup = 27 / kGroups;
+    for (int o = kOffPerGroup * group; o < kOffPerGroup * (group + 1); ++o) {
         const int2 d = soff[o];
         const int sx = ix + d.x, sy = iy + d.y;
         const bool inr = active && sx >= 0 && sx < mk && sy >= 0 && sy < mk;
@@ -180,11 +185,18 @@ void launch_tn(const Layout& L, const Tables* T, const double2* mult, const int*
         const int64_t dests = 1ll << (2 * (level - 1));
         blocks += (dests + kDestPerBlock - 1) / kDestPerBlock * 4 * nchunks;
     }
-    const size_t shm = (size_t)27 * (TN + L.P - 1) * sizeof(double2) +
-                       (size_t)(kGroups - 1) * TN * 32 * sizeof(double2);
-    k_m2l<TN><<<(unsigned)blocks, kDestPerBlock * kGroups, shm, s>>>(
-        mult, counts, loc, anc, l2l_split_level(L.levels, L.P), L.levels, L.P, nchunks, T,
-        &ctr->m2l_count, rows);
+    auto shm_of = [&](int groups) {
+        return (size_t)27 * (TN + L.P - 1) * sizeof(double2) +
+               (size_t)(groups - 1) * TN * 32 * sizeof(double2);
+    };
+    const int anc_end = l2l_split_level(L.levels, L.P);
+    if (blocks < 4 * 148 * 8 && shm_of(9) <= 48 * 1024) {
+        k_m2l<TN, 9><<<(unsigned)blocks, kDestPerBlock * 9, shm_of(9), s>>>(
+            mult, counts, loc, anc, anc_end, L.levels, L.P, nchunks, T, &ctr->m2l_count, rows);
+    } else {
+        k_m2l<TN, 3><<<(unsigned)blocks, kDestPerBlock * 3, shm_of(3), s>>>(
+            mult, counts, loc, anc, anc_end, L.levels, L.P, nchunks, T, &ctr->m2l_count, rows);
+    }
     note_launches(1);
 }
 
