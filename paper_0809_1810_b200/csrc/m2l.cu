@@ -15,6 +15,8 @@
 // TN complex FMAs.  Per destination, offsets apply in row-major source order
 // (the accumulation order of engine.py:166-185); empty sources are skipped
 // when a whole warp's sources are empty and multiply as exact zeros otherwise.
+#include <cstdlib>
+
 #include "vfmm_internal.cuh"
 
 namespace vfmm {
@@ -50,12 +52,107 @@ __device__ __forceinline__ void il_offset(int px, int py, int o, int& dx, int& d
 // G = 9; config 3 1.50 ms (G = 3) vs 1.61 ms (G = 9).
 constexpr int kDestPerBlock = 32;
 
+// Opposite offsets o and -o of one interaction list share their Hankel row up
+// to signs: tau_{-o} = -tau_o, so H_{-o}[q] = (-1)^(q+1) H_o[q], and the two
+// translations of a destination collapse into ONE Hankel product,
+//   Lh_m += sum_n H_o[m+n] X_n,  X_n = M1_n - M2_n if m+n is even,
+//                                      M1_n + M2_n if m+n is odd,
+// (M1 from the source at +o, M2 from the source at -o).  16 of the 27 offsets
+// of every parity class (those in the 5x5 ring) pair up, so a destination
+// needs 19 products instead of 27.  Units in row-major order of their first
+// offset; o2 = -1 for an unpaired offset.
+constexpr int kUnits = 19;
+struct UnitTab {
+    int8_t o1[4][kUnits], o2[4][kUnits];
+};
+constexpr UnitTab make_units() {
+    UnitTab t{};
+    for (int par = 0; par < 4; ++par) {
+        const int px = par & 1, py = par >> 1;
+        int dxs[27] = {}, dys[27] = {};
+        int idx = 0;
+        for (int yy = -2 - py; yy < 4 - py; ++yy)
+            for (int xx = -2 - px; xx < 4 - px; ++xx) {
+                const int ax = xx < 0 ? -xx : xx, ay = yy < 0 ? -yy : yy;
+                if ((ax > ay ? ax : ay) >= 2) {
+                    dxs[idx] = xx;
+                    dys[idx] = yy;
+                    ++idx;
+                }
+            }
+        int nu = 0;
+        for (int o = 0; o < 27; ++o) {
+            int partner = -1;
+            for (int q = 0; q < 27; ++q)
+                if (dxs[q] == -dxs[o] && dys[q] == -dys[o]) partner = q;
+            if (partner >= 0 && partner < o) continue;  // already in the unit of its partner
+            t.o1[par][nu] = (int8_t)o;
+            t.o2[par][nu] = (int8_t)partner;
+            ++nu;
+        }
+    }
+    return t;
+}
+__constant__ UnitTab c_units = make_units();
+
 // Multipole source for destinations whose source is empty / outside the grid:
 // a zero coefficient read with stride 0 (no per-coefficient select).
 __device__ const double2 g_zero_coef = {0.0, 0.0};
 
+// One paired unit: the Hankel row h (= H_o[m0 ..]) applied to X_n (see the
+// unit table); MP = parity of m0, so D / S per (t, n) is a compile-time choice.
+template <int TN, int MP>
+__device__ __forceinline__ void m2l_pair(const double2* M1, int64_t st1, const double2* M2,
+                                         int64_t st2, const double2* h, int P, double (&ax)[TN],
+                                         double (&ay)[TN]) {
+    int n = 0;
+#ifndef VFMM_M2L_PUNR
+#define VFMM_M2L_PUNR 1
+#endif
+    constexpr int kPUnr = VFMM_M2L_PUNR;
+#pragma unroll kPUnr
+    for (; n + 1 < P; n += 2) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const double2 a1 = M1[k * st1], a2 = M2[k * st2];
+            const double sx_ = a1.x + a2.x, sy_ = a1.y + a2.y;
+            const double dx_ = a1.x - a2.x, dy_ = a1.y - a2.y;
+#pragma unroll
+            for (int t = 0; t < TN; ++t) {
+                const bool odd = ((MP + t + k) & 1) != 0;  // parity of m0 + t + n
+                const double xr = odd ? sx_ : dx_, xi = odd ? sy_ : dy_;
+                const double2 hh = h[t + n + k];
+                ax[t] = fma(hh.x, xr, fma(-hh.y, xi, ax[t]));
+                ay[t] = fma(hh.x, xi, fma(hh.y, xr, ay[t]));
+            }
+        }
+        M1 += 2 * st1;
+        M2 += 2 * st2;
+    }
+    if (n < P) {
+        const double2 a1 = *M1, a2 = *M2;
+        const double sx_ = a1.x + a2.x, sy_ = a1.y + a2.y;
+        const double dx_ = a1.x - a2.x, dy_ = a1.y - a2.y;
+        const int np = n & 1;
+#pragma unroll
+        for (int t = 0; t < TN; ++t) {
+            const bool odd = ((MP + t + np) & 1) != 0;
+            const double xr = odd ? sx_ : dx_, xi = odd ? sy_ : dy_;
+            const double2 hh = h[t + n];
+            ax[t] = fma(hh.x, xr, fma(-hh.y, xi, ax[t]));
+            ay[t] = fma(hh.x, xi, fma(hh.y, xr, ay[t]));
+        }
+    }
+}
+
 template <int TN, int kGroups>
-__global__ void __launch_bounds__(kDestPerBlock * kGroups, kGroups == 3 ? 8 : 3)
+#ifndef VFMM_M2L_MB3
+#define VFMM_M2L_MB3 8
+#endif
+#ifndef VFMM_M2L_MB9
+#define VFMM_M2L_MB9 3
+#endif
+__global__ void __launch_bounds__(kDestPerBlock * kGroups, kGroups == 3 ? VFMM_M2L_MB3 : VFMM_M2L_MB9)
     k_m2l(const double2* __restrict__ mult, const int* __restrict__ counts, double2* __restrict__ loc,
           double2* __restrict__ anc, int anc_end, int levels, int P, int nchunks,
           const Tables* __restrict__ T, unsigned long long* __restrict__ m2l_count, Rows rows) {
@@ -118,31 +215,51 @@ __global__ void __launch_bounds__(kDestPerBlock * kGroups, kGroups == 3 ? 8 : 3)
 #pragma unroll
     for (int t = 0; t < TN; ++t) ax[t] = ay[t] = 0.0;
     int ntrans = 0;
-    constexpr int kOffPerGroup = 27 / kGroups;
-    for (int o = kOffPerGroup * group; o < kOffPerGroup * (group + 1); ++o) {
-        const int2 d = soff[o];
+    // this warp's units: [kUnits g / G, kUnits (g + 1) / G)
+    const int u_end = kUnits * (group + 1) / kGroups;
+    for (int u = kUnits * group / kGroups; u < u_end; ++u) {
+        const int o1 = c_units.o1[parity][u], o2 = c_units.o2[parity][u];
+        const int2 d = soff[o1];
         const int sx = ix + d.x, sy = iy + d.y;
         const bool inr = active && sx >= 0 && sx < mk && sy >= 0 && sy < mk;
         const bool live = inr && cnt[(int64_t)sy * mk + sx] > 0;
         ntrans += (live && counts_here) ? 1 : 0;
-        if (!__any_sync(0xffffffffu, live)) continue;
-        const double2* h = sH + o * HL;
         // source plane / index (floor division of the shifted coordinates)
-        const int sp = ((sy & 1) << 1) | (sx & 1);
-        const double2* Ms =
-            live ? M + sp * psz + (int64_t)(sy >> 1) * half + (sx >> 1) : &g_zero_coef;
+        const double2* Ms = live ? M + (((sy & 1) << 1) | (sx & 1)) * psz +
+                                       (int64_t)(sy >> 1) * half + (sx >> 1)
+                                 : &g_zero_coef;
         const int64_t step = live ? cstride : 0;
+        const double2* h = sH + o1 * HL;
+        if (o2 < 0) {
+            if (!__any_sync(0xffffffffu, live)) continue;
 #pragma unroll 3
-        for (int n = 0; n < P; ++n) {
-            const double2 a = *Ms;
-            Ms += step;
+            for (int n = 0; n < P; ++n) {
+                const double2 a = *Ms;
+                Ms += step;
 #pragma unroll
-            for (int t = 0; t < TN; ++t) {
-                const double2 hh = h[t + n];
-                ax[t] = fma(hh.x, a.x, fma(-hh.y, a.y, ax[t]));
-                ay[t] = fma(hh.x, a.y, fma(hh.y, a.x, ay[t]));
+                for (int t = 0; t < TN; ++t) {
+                    const double2 hh = h[t + n];
+                    ax[t] = fma(hh.x, a.x, fma(-hh.y, a.y, ax[t]));
+                    ay[t] = fma(hh.x, a.y, fma(hh.y, a.x, ay[t]));
+                }
             }
+            continue;
         }
+        // the opposite source (offset -o1)
+        const int tx = ix - d.x, ty = iy - d.y;
+        const bool inr2 = active && tx >= 0 && tx < mk && ty >= 0 && ty < mk;
+        const bool live2 = inr2 && cnt[(int64_t)ty * mk + tx] > 0;
+        ntrans += (live2 && counts_here) ? 1 : 0;
+        if (!__any_sync(0xffffffffu, live || live2)) continue;
+        const double2* Ms2 = live2 ? M + (((ty & 1) << 1) | (tx & 1)) * psz +
+                                         (int64_t)(ty >> 1) * half + (tx >> 1)
+                                   : &g_zero_coef;
+        const int64_t step2 = live2 ? cstride : 0;
+        // X_n = D = M1 - M2 where q = m0 + t + n is even, S = M1 + M2 where odd
+        if (m0 & 1)
+            m2l_pair<TN, 1>(Ms, step, Ms2, step2, h, P, ax, ay);
+        else
+            m2l_pair<TN, 0>(Ms, step, Ms2, step2, h, P, ax, ay);
     }
     // ---- combine the group partials in group order ----
     double2* part = sH + 27 * HL;
@@ -190,7 +307,9 @@ void launch_tn(const Layout& L, const Tables* T, const double2* mult, const int*
                (size_t)(groups - 1) * TN * 32 * sizeof(double2);
     };
     const int anc_end = l2l_split_level(L.levels, L.P);
-    if (blocks < 4 * 148 * 8 && shm_of(9) <= 48 * 1024) {
+    static const int g_env = getenv("VFMM_M2L_G") ? atoi(getenv("VFMM_M2L_G")) : 0;  // tuning
+    const bool nine = g_env ? g_env == 9 : blocks < 4 * 148 * 8;
+    if (nine && shm_of(9) <= 48 * 1024) {
         k_m2l<TN, 9><<<(unsigned)blocks, kDestPerBlock * 9, shm_of(9), s>>>(
             mult, counts, loc, anc, anc_end, L.levels, L.P, nchunks, T, &ctr->m2l_count, rows);
     } else {
