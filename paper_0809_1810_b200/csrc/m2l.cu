@@ -52,18 +52,27 @@ __device__ __forceinline__ void il_offset(int px, int py, int o, int& dx, int& d
 // G = 9; config 3 1.50 ms (G = 3) vs 1.61 ms (G = 9).
 constexpr int kDestPerBlock = 32;
 
-// Opposite offsets o and -o of one interaction list share their Hankel row up
-// to signs: tau_{-o} = -tau_o, so H_{-o}[q] = (-1)^(q+1) H_o[q], and the two
-// translations of a destination collapse into ONE Hankel product,
-//   Lh_m += sum_n H_o[m+n] X_n,  X_n = M1_n - M2_n if m+n is even,
-//                                      M1_n + M2_n if m+n is odd,
-// (M1 from the source at +o, M2 from the source at -o).  16 of the 27 offsets
-// of every parity class (those in the 5x5 ring) pair up, so a destination
-// needs 19 products instead of 27.  Units in row-major order of their first
-// offset; o2 = -1 for an unpaired offset.
-constexpr int kUnits = 19;
+// Symmetric offsets share their Hankel row up to conjugation and signs
+// (tau_o = -(dx + i dy)):
+//   -o        : tau -> -tau        H[q] -> (-1)^(q+1) H[q]        (kind 1)
+//   (dx, -dy) : tau -> conj(tau)   H[q] -> conj(H[q])             (kind 2)
+//   (-dx, dy) : tau -> -conj(tau)  H[q] -> (-1)^(q+1) conj(H[q])  (kind 3)
+// so the translations of a destination from a source M1 at o and a source M2
+// at the partner offset collapse into ONE product with the row h = H_o:
+//   kind 1:   Lh_m += sum_n h[m+n] X_n,  X = M1 - M2 (m+n even), M1 + M2 (odd)
+//   kind 2/3: Lh_m += sum_n (Re h[m+n] X_n + i Im h[m+n] Y_n), S = M1 + M2,
+//             D = M1 - M2; kind 2: X = S, Y = D; kind 3: (X, Y) = (D, S) for
+//             m+n even, (S, D) for m+n odd
+// (H M1 + conj(H) B = Re H (M1 + B) + i Im H (M1 - B)).  Each costs 4 real
+// FMA per (m, n), like one plain translation.  Of the 27 offsets of a parity
+// class the 16 of the 5x5 ring pair as +-o (kind 1), the outer column and row
+// give two mirror pairs each (kinds 2 and 3) and 3 stay single: 15 products
+// per destination instead of 27.  Units in row-major order of their first
+// offset; o2 = -1 for a single offset.
+constexpr int kUnits = 15;
 struct UnitTab {
-    int8_t o1[4][kUnits], o2[4][kUnits];
+    int8_t o1[4][kUnits], o2[4][kUnits], kind[4][kUnits];
+    int count[4];
 };
 constexpr UnitTab make_units() {
     UnitTab t{};
@@ -80,68 +89,86 @@ constexpr UnitTab make_units() {
                     ++idx;
                 }
             }
+        bool used[27] = {};
         int nu = 0;
         for (int o = 0; o < 27; ++o) {
-            int partner = -1;
-            for (int q = 0; q < 27; ++q)
-                if (dxs[q] == -dxs[o] && dys[q] == -dys[o]) partner = q;
-            if (partner >= 0 && partner < o) continue;  // already in the unit of its partner
-            t.o1[par][nu] = (int8_t)o;
-            t.o2[par][nu] = (int8_t)partner;
+            if (used[o]) continue;
+            used[o] = true;
+            int partner = -1, kind = 0;
+            for (int k = 0; k < 3 && partner < 0; ++k) {
+                if ((k == 1 && dys[o] == 0) || (k == 2 && dxs[o] == 0)) continue;
+                const int wx = k == 1 ? dxs[o] : -dxs[o], wy = k == 2 ? dys[o] : -dys[o];
+                for (int q = 0; q < 27; ++q)
+                    if (!used[q] && dxs[q] == wx && dys[q] == wy) {
+                        partner = q;
+                        kind = k + 1;
+                    }
+            }
+            if (partner >= 0) used[partner] = true;
+            if (nu < kUnits) {
+                t.o1[par][nu] = (int8_t)o;
+                t.o2[par][nu] = (int8_t)partner;
+                t.kind[par][nu] = (int8_t)kind;
+            }
             ++nu;
         }
+        t.count[par] = nu;
     }
     return t;
 }
-__constant__ UnitTab c_units = make_units();
+constexpr UnitTab kUnitTab = make_units();
+static_assert(kUnitTab.count[0] == kUnits && kUnitTab.count[1] == kUnits &&
+                  kUnitTab.count[2] == kUnits && kUnitTab.count[3] == kUnits,
+              "15 units per parity class");
+__constant__ UnitTab c_units = kUnitTab;
 
 // Multipole source for destinations whose source is empty / outside the grid:
 // a zero coefficient read with stride 0 (no per-coefficient select).
 __device__ const double2 g_zero_coef = {0.0, 0.0};
 
-// One paired unit: the Hankel row h (= H_o[m0 ..]) applied to X_n (see the
-// unit table); MP = parity of m0, so D / S per (t, n) is a compile-time choice.
-template <int TN, int MP>
+// One paired unit (see the unit table) for outputs m0 .. m0+TN-1; MP = parity
+// of m0, so the per-(t, n) choices of X / Y are compile-time.
+template <int TN, int KIND, int MP>
+__device__ __forceinline__ void m2l_pair_step(double2 a1, double2 a2, const double2* h, int np,
+                                              double (&ax)[TN], double (&ay)[TN]) {
+    const double sr = a1.x + a2.x, si = a1.y + a2.y;
+    const double dr = a1.x - a2.x, di = a1.y - a2.y;
+#pragma unroll
+    for (int t = 0; t < TN; ++t) {
+        const bool odd = ((MP + t + np) & 1) != 0;  // parity of m + n
+        const bool swap = KIND != 2 && odd;          // kinds 1, 3: S where m + n is odd
+        const double xr = swap ? sr : dr, xi = swap ? si : di;
+        const double2 hh = h[t];
+        if (KIND == 1) {  // h * X, X = D (m+n even) / S (odd)
+            ax[t] = fma(hh.x, xr, fma(-hh.y, xi, ax[t]));
+            ay[t] = fma(hh.x, xi, fma(hh.y, xr, ay[t]));
+        } else {  // Re h * X + i Im h * Y
+            const bool xs = KIND == 2 || odd;  // X = S (kind 2, or kind 3 at odd m+n)
+            const double Xr = xs ? sr : dr, Xi = xs ? si : di;
+            const double Yr = xs ? dr : sr, Yi = xs ? di : si;
+            ax[t] = fma(hh.x, Xr, fma(-hh.y, Yi, ax[t]));
+            ay[t] = fma(hh.x, Xi, fma(hh.y, Yr, ay[t]));
+        }
+    }
+}
+template <int TN, int KIND, int MP>
 __device__ __forceinline__ void m2l_pair(const double2* M1, int64_t st1, const double2* M2,
                                          int64_t st2, const double2* h, int P, double (&ax)[TN],
                                          double (&ay)[TN]) {
     int n = 0;
-#ifndef VFMM_M2L_PUNR
-#define VFMM_M2L_PUNR 1
-#endif
-    constexpr int kPUnr = VFMM_M2L_PUNR;
-#pragma unroll kPUnr
+#pragma unroll 1
     for (; n + 1 < P; n += 2) {
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const double2 a1 = M1[k * st1], a2 = M2[k * st2];
-            const double sx_ = a1.x + a2.x, sy_ = a1.y + a2.y;
-            const double dx_ = a1.x - a2.x, dy_ = a1.y - a2.y;
-#pragma unroll
-            for (int t = 0; t < TN; ++t) {
-                const bool odd = ((MP + t + k) & 1) != 0;  // parity of m0 + t + n
-                const double xr = odd ? sx_ : dx_, xi = odd ? sy_ : dy_;
-                const double2 hh = h[t + n + k];
-                ax[t] = fma(hh.x, xr, fma(-hh.y, xi, ax[t]));
-                ay[t] = fma(hh.x, xi, fma(hh.y, xr, ay[t]));
-            }
-        }
+        const double2 a1 = M1[0], a2 = M2[0], b1 = M1[st1], b2 = M2[st2];
+        m2l_pair_step<TN, KIND, MP>(a1, a2, h + n, 0, ax, ay);
+        m2l_pair_step<TN, KIND, MP>(b1, b2, h + n + 1, 1, ax, ay);
         M1 += 2 * st1;
         M2 += 2 * st2;
     }
     if (n < P) {
-        const double2 a1 = *M1, a2 = *M2;
-        const double sx_ = a1.x + a2.x, sy_ = a1.y + a2.y;
-        const double dx_ = a1.x - a2.x, dy_ = a1.y - a2.y;
-        const int np = n & 1;
-#pragma unroll
-        for (int t = 0; t < TN; ++t) {
-            const bool odd = ((MP + t + np) & 1) != 0;
-            const double xr = odd ? sx_ : dx_, xi = odd ? sy_ : dy_;
-            const double2 hh = h[t + n];
-            ax[t] = fma(hh.x, xr, fma(-hh.y, xi, ax[t]));
-            ay[t] = fma(hh.x, xi, fma(hh.y, xr, ay[t]));
-        }
+        if (n & 1)
+            m2l_pair_step<TN, KIND, MP>(*M1, *M2, h + n, 1, ax, ay);
+        else
+            m2l_pair_step<TN, KIND, MP>(*M1, *M2, h + n, 0, ax, ay);
     }
 }
 
@@ -219,6 +246,7 @@ __global__ void __launch_bounds__(kDestPerBlock * kGroups, kGroups == 3 ? VFMM_M
     const int u_end = kUnits * (group + 1) / kGroups;
     for (int u = kUnits * group / kGroups; u < u_end; ++u) {
         const int o1 = c_units.o1[parity][u], o2 = c_units.o2[parity][u];
+        const int kind = c_units.kind[parity][u];
         const int2 d = soff[o1];
         const int sx = ix + d.x, sy = iy + d.y;
         const bool inr = active && sx >= 0 && sx < mk && sy >= 0 && sy < mk;
@@ -245,8 +273,9 @@ __global__ void __launch_bounds__(kDestPerBlock * kGroups, kGroups == 3 ? VFMM_M
             }
             continue;
         }
-        // the opposite source (offset -o1)
-        const int tx = ix - d.x, ty = iy - d.y;
+        // the partner source (offset -o1, or its y / x mirror)
+        const int2 d2 = soff[o2];
+        const int tx = ix + d2.x, ty = iy + d2.y;
         const bool inr2 = active && tx >= 0 && tx < mk && ty >= 0 && ty < mk;
         const bool live2 = inr2 && cnt[(int64_t)ty * mk + tx] > 0;
         ntrans += (live2 && counts_here) ? 1 : 0;
@@ -255,11 +284,16 @@ __global__ void __launch_bounds__(kDestPerBlock * kGroups, kGroups == 3 ? VFMM_M
                                          (int64_t)(ty >> 1) * half + (tx >> 1)
                                    : &g_zero_coef;
         const int64_t step2 = live2 ? cstride : 0;
-        // X_n = D = M1 - M2 where q = m0 + t + n is even, S = M1 + M2 where odd
-        if (m0 & 1)
-            m2l_pair<TN, 1>(Ms, step, Ms2, step2, h, P, ax, ay);
-        else
-            m2l_pair<TN, 0>(Ms, step, Ms2, step2, h, P, ax, ay);
+        const bool mo = (m0 & 1) != 0;
+        if (kind == 1) {
+            if (mo) m2l_pair<TN, 1, 1>(Ms, step, Ms2, step2, h, P, ax, ay);
+            else m2l_pair<TN, 1, 0>(Ms, step, Ms2, step2, h, P, ax, ay);
+        } else if (kind == 2) {
+            m2l_pair<TN, 2, 0>(Ms, step, Ms2, step2, h, P, ax, ay);
+        } else {
+            if (mo) m2l_pair<TN, 3, 1>(Ms, step, Ms2, step2, h, P, ax, ay);
+            else m2l_pair<TN, 3, 0>(Ms, step, Ms2, step2, h, P, ax, ay);
+        }
     }
     // ---- combine the group partials in group order ----
     double2* part = sH + 27 * HL;
