@@ -45,11 +45,12 @@ __device__ __forceinline__ void il_offset(int px, int py, int o, int& dx, int& d
 // layout the source of offset (dx, dy) for consecutive destinations is a run
 // of consecutive cells of one source plane, so each multipole coefficient
 // load is coalesced; the Hankel rows are block-uniform smem broadcasts.
-// G = 3 offset groups (8 CTAs of 3 warps per SM) for large grids; G = 9
-// (3 CTAs of 9 warps) when the 3-group grid is under ~4 waves: each warp has a
-// third of the work, so the last partial wave is short.  Measured (median
-// t_m2l): config 1 0.0215 -> 0.0155 ms, config 2 0.0911 -> 0.0891 ms with
-// G = 9; config 3 1.50 ms (G = 3) vs 1.61 ms (G = 9).
+// G offset-unit groups (warps) per CTA, one CTA = 32 destinations: G = 3 (8
+// CTAs of 3 warps per SM) for large grids; for grids under ~4 waves of
+// 3-warp CTAs G = 15 (one unit per warp: no barrier imbalance) and for tiny
+// grids (< 600 CTAs) G = 9.  Measured (median t_m2l, 15-unit kernel):
+// config 2 0.0778 (G 9) / 0.0727 (G 5) / 0.0706 ms (G 15); config 1 0.0143
+// (G 9) / 0.0225 ms (G 15); config 3 1.20 ms (G 3).
 constexpr int kDestPerBlock = 32;
 
 // Symmetric offsets share their Hankel row up to conjugation and signs
@@ -179,7 +180,12 @@ template <int TN, int kGroups>
 #ifndef VFMM_M2L_MB9
 #define VFMM_M2L_MB9 3
 #endif
-__global__ void __launch_bounds__(kDestPerBlock * kGroups, kGroups == 3 ? VFMM_M2L_MB3 : VFMM_M2L_MB9)
+#ifndef VFMM_M2L_MB15
+#define VFMM_M2L_MB15 2
+#endif
+__global__ void __launch_bounds__(kDestPerBlock * kGroups,
+                                  kGroups == 3 ? VFMM_M2L_MB3
+                                               : (kGroups == 9 ? VFMM_M2L_MB9 : VFMM_M2L_MB15))
     k_m2l(const double2* __restrict__ mult, const int* __restrict__ counts, double2* __restrict__ loc,
           double2* __restrict__ anc, int anc_end, int levels, int P, int nchunks,
           const Tables* __restrict__ T, unsigned long long* __restrict__ m2l_count, Rows rows) {
@@ -341,15 +347,21 @@ void launch_tn(const Layout& L, const Tables* T, const double2* mult, const int*
                (size_t)(groups - 1) * TN * 32 * sizeof(double2);
     };
     const int anc_end = l2l_split_level(L.levels, L.P);
-    static const int g_env = getenv("VFMM_M2L_G") ? atoi(getenv("VFMM_M2L_G")) : 0;  // tuning
-    const bool nine = g_env ? g_env == 9 : blocks < 4 * 148 * 8;
-    if (nine && shm_of(9) <= 48 * 1024) {
+    // offset groups (warps) per CTA by grid size, see the kernel comment;
+    // VFMM_M2L_G = 3 / 9 / 15 overrides (tuning)
+    static const int g_env = getenv("VFMM_M2L_G") ? atoi(getenv("VFMM_M2L_G")) : 0;
+    int g = blocks < 600 ? 9 : (blocks < 4 * 148 * 8 ? 15 : 3);
+    if (g_env == 3 || g_env == 9 || g_env == 15) g = g_env;
+    if (g != 3 && shm_of(g) > 48 * 1024) g = 3;
+    if (g == 9)
         k_m2l<TN, 9><<<(unsigned)blocks, kDestPerBlock * 9, shm_of(9), s>>>(
             mult, counts, loc, anc, anc_end, L.levels, L.P, nchunks, T, &ctr->m2l_count, rows);
-    } else {
+    else if (g == 15)
+        k_m2l<TN, 15><<<(unsigned)blocks, kDestPerBlock * 15, shm_of(15), s>>>(
+            mult, counts, loc, anc, anc_end, L.levels, L.P, nchunks, T, &ctr->m2l_count, rows);
+    else
         k_m2l<TN, 3><<<(unsigned)blocks, kDestPerBlock * 3, shm_of(3), s>>>(
             mult, counts, loc, anc, anc_end, L.levels, L.P, nchunks, T, &ctr->m2l_count, rows);
-    }
     note_launches(1);
 }
 
