@@ -21,6 +21,10 @@ __device__ Tables g_tables;
 
 static std::atomic<long long> g_launches{0};
 void note_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+bool pdl_enabled() {
+    static const bool on = !(getenv("VFMM_PDL") && getenv("VFMM_PDL")[0] == '0');
+    return on;
+}
 
 namespace {
 
@@ -259,6 +263,7 @@ bool make_layout(int64_t n, int levels, int order, Layout* L) {
 namespace vfmm {
 
 __global__ void k_fp64_probe(double* sink, int iters) {
+    pdl_enter();
     double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-3, a2 = a0 + 2e-3, a3 = a0 + 3e-3;
     double a4 = a0 + 4e-3, a5 = a0 + 5e-3, a6 = a0 + 6e-3, a7 = a0 + 7e-3;
     const double b = 0.999999, c = 1e-7;
@@ -826,7 +831,7 @@ int vfmm_fp64_probe(double* sink, int blocks, int iters, double* flops, void* st
     if (!sink || blocks < 1 || iters < 1) return VFMM_EINVAL;
     int dev = 0;
     if (current_device_of(sink, &dev) != 0) return VFMM_ECUDA;
-    k_fp64_probe<<<blocks, 256, 0, (cudaStream_t)stream>>>(sink, iters);
+    launch_k(k_fp64_probe, blocks, 256, 0, (cudaStream_t)stream, sink, iters);
     note_launches(1);
     if (flops) *flops = (double)blocks * 256.0 * (double)iters * 32.0 * 2.0;
     return cudaGetLastError() == cudaSuccess ? VFMM_OK : VFMM_ECUDA;

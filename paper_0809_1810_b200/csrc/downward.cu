@@ -16,6 +16,7 @@ namespace {
 
 // levels == 2 has no L2L: copy the level-2 planar locals to the cell-major leaf array
 __global__ void k_leaf_locals_copy(const double2* __restrict__ loc2, int P, double2* __restrict__ out) {
+    pdl_enter();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= 16 * P) return;
     const int cell = t / P, n = t % P;
@@ -31,6 +32,7 @@ __global__ void __launch_bounds__(256)
     k_near_sum(const int* __restrict__ keys, double2* __restrict__ near_uv, int64_t n, int levels,
                Rows rows, const int* __restrict__ ls, const Counters* __restrict__ ctr, bool gauss,
                int sym_enabled) {
+    pdl_enter();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int m = 1 << levels;
@@ -67,6 +69,7 @@ __global__ void __launch_bounds__(256)
                   const double2* __restrict__ near_uv, int64_t n, int levels, int P, double xmin,
                   double ymin, double side, const Tables* __restrict__ T, double* __restrict__ u,
                   double* __restrict__ v, Rows rows) {
+    pdl_enter();
     __shared__ double sfact[kOrderCap + 16];
     for (int i = threadIdx.x; i < P; i += blockDim.x) sfact[i] = T->invfact[i];
     __syncthreads();
@@ -103,6 +106,7 @@ __global__ void __launch_bounds__(256)
               const double2* __restrict__ loc, int levels, int P, double xmin, double ymin,
               double side, const Tables* __restrict__ T, double* __restrict__ u,
               double* __restrict__ v, Counters* ctr) {
+    pdl_enter();
     __shared__ double sfact[kOrderCap + 16];
     __shared__ double sexp[kExpTab];
     for (int i = threadIdx.x; i < P; i += blockDim.x) sfact[i] = T->invfact[i];
@@ -146,7 +150,7 @@ __global__ void __launch_bounds__(256)
 }  // namespace
 
 void launch_leaf_locals_copy(const Layout& L, const double2* loc, double2* leaf_loc, cudaStream_t s) {
-    k_leaf_locals_copy<<<(16 * L.P + 127) / 128, 128, 0, s>>>(loc, L.P, leaf_loc);
+    launch_k(k_leaf_locals_copy, (16 * L.P + 127) / 128, 128, 0, s, loc, L.P, leaf_loc);
     note_launches(1);
 }
 
@@ -154,14 +158,14 @@ void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const 
                         const int* perm, const double2* loc, const double2* near_uv, double xmin,
                         double ymin, double side, double* u, double* v, Rows rows,
                         cudaStream_t s) {
-    k_l2p_combine<<<(unsigned)((L.n + 255) / 256), 256, 0, s>>>(
+    launch_k(k_l2p_combine, (unsigned)((L.n + 255) / 256), 256, 0, s, 
         src, keys, perm, loc, near_uv, L.n, L.levels, L.P, xmin, ymin, side, T, u, v, rows);
     note_launches(1);
 }
 
 void launch_near_sum(const Layout& L, const int* keys, double2* near_uv, Rows rows,
                      const int* leaf_starts, const Counters* ctr, int kernel, cudaStream_t s) {
-    k_near_sum<<<(unsigned)((L.n + 255) / 256), 256, 0, s>>>(
+    launch_k(k_near_sum, (unsigned)((L.n + 255) / 256), 256, 0, s, 
         keys, near_uv, L.n, L.levels, rows, leaf_starts, ctr, kernel == VFMM_KERNEL_GAUSSIAN,
         sym_disabled() ? 0 : 1);
     note_launches(1);
@@ -174,10 +178,10 @@ void launch_eval_at(const Layout& L, const Tables* T, const double* tx, const do
     const double2* leaf_loc = loc;
     const unsigned g = (unsigned)((m + 255) / 256);
     if (kernel == VFMM_KERNEL_GAUSSIAN)
-        k_eval_at<true><<<g, 256, 0, s>>>(tx, ty, m, src, leaf_starts, leaf_loc, L.levels, L.P,
+        launch_k(k_eval_at<true>, g, 256, 0, s, tx, ty, m, src, leaf_starts, leaf_loc, L.levels, L.P,
                                           xmin, ymin, side, T, u, v, ctr);
     else
-        k_eval_at<false><<<g, 256, 0, s>>>(tx, ty, m, src, leaf_starts, leaf_loc, L.levels, L.P,
+        launch_k(k_eval_at<false>, g, 256, 0, s, tx, ty, m, src, leaf_starts, leaf_loc, L.levels, L.P,
                                            xmin, ymin, side, T, u, v, ctr);
     note_launches(1);
 }

@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(kDestPerBlock * kGroups,
     k_m2l(const double2* __restrict__ mult, const int* __restrict__ counts, double2* __restrict__ loc,
           double2* __restrict__ anc, int anc_end, int levels, int P, int nchunks,
           const Tables* __restrict__ T, unsigned long long* __restrict__ m2l_count, Rows rows) {
+    pdl_enter();
     extern __shared__ double2 sH[];  // [27][TN + P - 1], then [kGroups - 1][TN][32] partials
     // ---- decode (level, parity, chunk, block-in-class) from blockIdx.x ----
     int64_t b = blockIdx.x;
@@ -354,13 +355,13 @@ void launch_tn(const Layout& L, const Tables* T, const double2* mult, const int*
     if (g_env == 3 || g_env == 9 || g_env == 15) g = g_env;
     if (g != 3 && shm_of(g) > 48 * 1024) g = 3;
     if (g == 9)
-        k_m2l<TN, 9><<<(unsigned)blocks, kDestPerBlock * 9, shm_of(9), s>>>(
+        launch_k(k_m2l<TN, 9>, (unsigned)blocks, kDestPerBlock * 9, shm_of(9), s, 
             mult, counts, loc, anc, anc_end, L.levels, L.P, nchunks, T, &ctr->m2l_count, rows);
     else if (g == 15)
-        k_m2l<TN, 15><<<(unsigned)blocks, kDestPerBlock * 15, shm_of(15), s>>>(
+        launch_k(k_m2l<TN, 15>, (unsigned)blocks, kDestPerBlock * 15, shm_of(15), s, 
             mult, counts, loc, anc, anc_end, L.levels, L.P, nchunks, T, &ctr->m2l_count, rows);
     else
-        k_m2l<TN, 3><<<(unsigned)blocks, kDestPerBlock * 3, shm_of(3), s>>>(
+        launch_k(k_m2l<TN, 3>, (unsigned)blocks, kDestPerBlock * 3, shm_of(3), s, 
             mult, counts, loc, anc, anc_end, L.levels, L.P, nchunks, T, &ctr->m2l_count, rows);
     note_launches(1);
 }

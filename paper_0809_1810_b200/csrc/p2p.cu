@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(kP2PWarps * 32, kP2PBlocksPerSM)
           Counters* __restrict__ ctr, int levels, int64_t n, const Tables* __restrict__ T,
           double2* __restrict__ near_uv, unsigned long long* __restrict__ pairs, int items_per_warp,
           int sym_enabled) {
+    pdl_enter();
     if (sym_enabled && p2p_symmetric(ctr, GAUSS)) return;  // the symmetric kernel handles it
     const int nitems = ctr->ntasks * kNearRows;
     if ((int64_t)blockIdx.x * kP2PWarps * items_per_warp >= nitems) return;  // spare CTA
@@ -637,6 +638,7 @@ __global__ void VFMM_SYM_BOUNDS
               int levels, int64_t n, Rows rows, const Tables* __restrict__ T,
               double2* __restrict__ near5, unsigned long long* __restrict__ pairs,
               int items_per_warp) {
+    pdl_enter();
     if (!p2p_symmetric(ctr, GAUSS)) return;  // the generic kernel handles it
     const int m = 1 << levels;
     const int nitems = 1 << (2 * levels);  // one item per leaf
@@ -811,6 +813,7 @@ __global__ void __launch_bounds__(kDirThreads)
              const double* __restrict__ g, const double* __restrict__ sigma, int64_t n,
              int64_t slice_len, const Tables* __restrict__ T, double* __restrict__ pu,
              double* __restrict__ pv) {
+    pdl_enter();
     __shared__ Src tile[kDirThreads];
     __shared__ double sexp[kExpTab];
     const double* stab = stage_exp_table(sexp, T->exp2tab);
@@ -857,6 +860,7 @@ __global__ void __launch_bounds__(kDirThreads)
 __global__ void k_direct_reduce(const double* __restrict__ pu, const double* __restrict__ pv,
                                 int64_t mt, int nsplit, double* __restrict__ u,
                                 double* __restrict__ v) {
+    pdl_enter();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= mt) return;
     double a = 0.0, b = 0.0;
@@ -933,7 +937,7 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
         attr_set.fetch_or(1ull << dev);
     }
     if (!sym_disabled()) {
-        sfn<<<sblocks, kSymWarps * 32, kSymSmem, s>>>(src, leaf_starts, ctr, L.levels, L.n, rows, T,
+        launch_k(sfn, sblocks, kSymWarps * 32, kSymSmem, s, src, leaf_starts, ctr, L.levels, L.n, rows, T,
                                                       near_uv, &ctr->near_pairs, ks);
         note_launches(1);
     }
@@ -959,7 +963,7 @@ static void launch_p2p_generic(const Layout& L, const Tables* T, const Src* src,
                                            : (g ? k_p2p<true, 1> : k_p2p<false, 1>);
     launch_tasks(L, ws, ctr, rows, kernel == VFMM_KERNEL_GAUSSIAN, s);
     const int2* tasks = (const int2*)(ws + L.tasks);
-    fn<<<blocks, kP2PWarps * 32, 0, s>>>(src, leaf_starts, tasks, ctr, L.levels, L.n, T, near_uv,
+    launch_k(fn, blocks, kP2PWarps * 32, 0, s, src, leaf_starts, tasks, ctr, L.levels, L.n, T, near_uv,
                                          &ctr->near_pairs, kk, sym_disabled() ? 0 : 1);
     note_launches(1);
 }
@@ -982,11 +986,11 @@ void launch_direct(const double* tx, const double* ty, int64_t m, const double* 
     slice = (slice + kDirThreads - 1) / kDirThreads * kDirThreads;
     dim3 grid((unsigned)((m + kDirThreads - 1) / kDirThreads), (unsigned)nsplit);
     if (kernel == VFMM_KERNEL_GAUSSIAN)
-        k_direct<true><<<grid, kDirThreads, 0, s>>>(tx, ty, m, x, y, g, sigma, n, slice, T, pu, pv);
+        launch_k(k_direct<true>, grid, kDirThreads, 0, s, tx, ty, m, x, y, g, sigma, n, slice, T, pu, pv);
     else
-        k_direct<false><<<grid, kDirThreads, 0, s>>>(tx, ty, m, x, y, g, sigma, n, slice, T, pu, pv);
+        launch_k(k_direct<false>, grid, kDirThreads, 0, s, tx, ty, m, x, y, g, sigma, n, slice, T, pu, pv);
     note_launches(1);
-    k_direct_reduce<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(pu, pv, m, nsplit, u, v);
+    launch_k(k_direct_reduce, (unsigned)((m + 255) / 256), 256, 0, s, pu, pv, m, nsplit, u, v);
     note_launches(1);
 }
 

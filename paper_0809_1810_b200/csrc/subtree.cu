@@ -25,6 +25,7 @@ __device__ __forceinline__ int sub_off(int s) { return ((1 << (2 * s)) - 1) / 3;
 __global__ void __launch_bounds__(kSubThreads)
     k_m2m_subtree(double2* __restrict__ mult, int lf, int depth, int P, size_t off_lf,
                   const Tables* __restrict__ T) {
+    pdl_enter();
     extern __shared__ double2 sm[];  // [sub_off(depth+1)][P] cells + tables
     double2* sE = sm + (size_t)sub_off(depth + 1) * P;  // [4][P]
     double* s2 = reinterpret_cast<double*>(sE + 4 * P);  // [P + 1]
@@ -94,6 +95,7 @@ __global__ void __launch_bounds__(kSubThreads)
     k_l2l_fused(double2* __restrict__ loc, double2* __restrict__ leaf_loc,
                 const double2* __restrict__ anc_m2l, int ls, int levels, int P,
                 const Tables* __restrict__ T, Rows rows, FusedOut fo) {
+    pdl_enter();
     extern __shared__ double2 sm[];
     const int depth = levels - ls;
     double2* sF = sm + (size_t)sub_off(depth + 1) * P;  // [4][P]
@@ -250,7 +252,7 @@ void launch_m2m(const Layout& L, const Tables* T, double2* mult, cudaStream_t s)
         const int d = lf - 2 < d0 ? lf - 2 : d0;
         const int lt = lf - d;
         const size_t off_lf = L.level_cell_off[lf] * L.P;
-        k_m2m_subtree<<<(unsigned)(1ll << (2 * lt)), kSubThreads, sub_smem(d, L.P), s>>>(
+        launch_k(k_m2m_subtree, (unsigned)(1ll << (2 * lt)), kSubThreads, sub_smem(d, L.P), s, 
             mult, lf, d, L.P, off_lf, T);
         note_launches(1);
         lf = lt;
@@ -281,7 +283,7 @@ void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_lo
     const int ls = l2l_split_level(L.levels, L.P);
     const size_t shm = sub_smem(L.levels - ls, L.P) + sizeof(double2) * (2 * L.P + 1) +
                        sizeof(double) * L.P;
-    k_l2l_fused<<<(unsigned)(1ll << (2 * ls)), kSubThreads, shm, s>>>(loc, leaf_loc, anc, ls,
+    launch_k(k_l2l_fused, (unsigned)(1ll << (2 * ls)), kSubThreads, shm, s, loc, leaf_loc, anc, ls,
                                                                        L.levels, L.P, T, rows, fo);
     note_launches(1);
 }

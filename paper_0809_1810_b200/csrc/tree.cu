@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(256)
     k_sort_probe(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                  double xmin, double ymin, double side, int levels, bool force_lsd,
                  Counters* __restrict__ ctr) {
+    pdl_enter();
     __shared__ int distinct;
     if (threadIdx.x == 0) distinct = 0;
     __syncthreads();
@@ -103,6 +104,7 @@ __global__ void __launch_bounds__(256)
     k_bin_count(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                 double xmin, double ymin, double side, int levels, int* __restrict__ key,
                 int* __restrict__ cnt, Counters* __restrict__ ctr) {
+    pdl_enter();
     if (ctr->sort_fallback == kSortLsdProbe) return;
     const int lane = threadIdx.x & 31;
     const int m = 1 << levels;
@@ -135,6 +137,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     k_bin_scatter(const int* __restrict__ key, int64_t n, const int* __restrict__ ls,
                   int* __restrict__ fill, int* __restrict__ slot, Counters* __restrict__ ctr) {
+    pdl_enter();
     if (ctr->sort_fallback == kSortLsdProbe) return;
     const int lane = threadIdx.x & 31;
     bool big = false;
@@ -232,6 +235,7 @@ __global__ void __launch_bounds__(256)
                 const double* __restrict__ g, const double* __restrict__ sigma, int sstride,
                 int* __restrict__ keys, int* __restrict__ perm, Src* __restrict__ src,
                 Counters* __restrict__ ctr) {
+    pdl_enter();
     if (ctr->sort_fallback) return;
     __shared__ unsigned long long wmax[8], wmin[8];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -274,6 +278,7 @@ __global__ void __launch_bounds__(256)
     k_pack_orig(const double* __restrict__ x, const double* __restrict__ y,
                 const double* __restrict__ g, const double* __restrict__ sigma, int sstride,
                 int64_t n, Src* __restrict__ out, Counters* __restrict__ ctr) {
+    pdl_enter();
     if (!ctr->sort_fallback) return;
     __shared__ unsigned long long wmax[8], wmin[8];
     unsigned long long sbits = 0ull, smin = ~0ull;
@@ -349,6 +354,7 @@ __global__ void __launch_bounds__(kTileThreads)
     k_keys_ghist(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                  double xmin, double ymin, double side, int levels, int bits, int passes,
                  int* __restrict__ key, int* __restrict__ ghist, Counters* __restrict__ ctr) {
+    pdl_enter();
     if (!ctr->sort_fallback) return;  // the counting path built the tree
     const bool probe_lsd = ctr->sort_fallback == kSortLsdProbe;
     __shared__ int h[4 * 256];
@@ -390,6 +396,7 @@ __global__ void __launch_bounds__(kTileThreads)
                const int* __restrict__ ghist, unsigned* __restrict__ lb, int* __restrict__ ticket,
                const Src* __restrict__ packed, Src* __restrict__ src,
                const Counters* __restrict__ ctr) {
+    pdl_enter();
     if (!ctr->sort_fallback) return;
     constexpr int W = kTileThreads / 32;
     __shared__ int wcnt[W][256];   // per-warp digit counts, then per-warp prefixes
@@ -568,6 +575,7 @@ __global__ void __launch_bounds__(kScanThreads)
     k_scan(int* __restrict__ data, int64_t n, unsigned long long* __restrict__ state,
            const Counters* __restrict__ sym_skip, bool gauss, const int* __restrict__ skip_flag,
            int skip_val) {
+    pdl_enter();
     // the near-field task list is not needed when the symmetric P2P kernel runs
     if (sym_skip && p2p_symmetric(sym_skip, gauss)) return;
     if (skip_flag && *skip_flag == skip_val) return;  // leaf-count scan: counting path only
@@ -639,6 +647,7 @@ __global__ void __launch_bounds__(kScanThreads)
 
 __global__ void k_leaf_starts(const int* __restrict__ keys, int64_t n, int nleaves,
                               int* __restrict__ ls, const Counters* __restrict__ ctr) {
+    pdl_enter();
     if (ctr && !ctr->sort_fallback) return;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -655,6 +664,7 @@ __global__ void k_leaf_starts(const int* __restrict__ keys, int64_t n, int nleav
 __global__ void k_counts_tasks(const int* __restrict__ ls, int levels, int64_t total_cells,
                                int chunk, Rows rows, int* __restrict__ counts,
                                int* __restrict__ ntask, Counters* __restrict__ ctr) {
+    pdl_enter();
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= total_cells) return;
     int k = 0;
@@ -691,6 +701,7 @@ __global__ void k_counts_tasks(const int* __restrict__ ls, int levels, int64_t t
 __global__ void k_tasks_fill(const int* __restrict__ ls, int levels, int chunk, Rows rows,
                              const int* __restrict__ off, int2* __restrict__ tasks, Counters* ctr,
                              bool gauss, bool sym_enabled) {
+    pdl_enter();
     if (sym_enabled && p2p_symmetric(ctr, gauss)) return;  // symmetric P2P: no task list
     const int nleaves = 1 << (2 * levels);
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -731,7 +742,7 @@ size_t scan_tiles(int64_t n) { return (size_t)((n + kScanTile - 1) / kScanTile);
 void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream_t s,
                      const Counters* sym_skip, bool gauss, const int* skip_flag, int skip_val) {
     if (n <= 0) return;
-    k_scan<<<(unsigned)scan_tiles(n), kScanThreads, 0, s>>>(data, n, state, sym_skip, gauss,
+    launch_k(k_scan, (unsigned)scan_tiles(n), kScanThreads, 0, s, data, n, state, sym_skip, gauss,
                                                               skip_flag, skip_val);
     note_launches(1);
 }
@@ -753,11 +764,11 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     Src* src = (Src*)(ws + L.src);
     cudaMemsetAsync(ws + L.scan_state, 0, L.scan_state_bytes, s);
 
-    k_sort_probe<<<1, 256, 0, s>>>(x, y, L.n, xmin, ymin, side, L.levels, force_lsd(), ctr);
+    launch_k(k_sort_probe, 1, 256, 0, s, x, y, L.n, xmin, ymin, side, L.levels, force_lsd(), ctr);
     note_launches(1);
     // ---- counting path (kernels return at once if the probe chose LSD) ----
     cudaMemsetAsync(ls, 0, sizeof(int) * (L.nleaves + 1), s);
-    k_bin_count<<<small_grid(L.n, 2368), 256, 0, s>>>(x, y, L.n, xmin, ymin, side, L.levels,
+    launch_k(k_bin_count, small_grid(L.n, 2368), 256, 0, s, x, y, L.n, xmin, ymin, side, L.levels,
                                                   kbuf[(L.passes + 1) & 1], ls, ctr);
     note_launches(1);
     launch_scan_i32(ls, (int64_t)L.nleaves + 1, state(L.passes + 1), s, nullptr, false,
@@ -765,13 +776,13 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     int* fill = (int*)(ws + L.task_scratch);  // free until the task counts
     cudaMemsetAsync(fill, 0, sizeof(int) * L.nleaves, s);
     int* slot = vbuf[(L.passes + 1) & 1];
-    k_bin_scatter<<<small_grid(L.n, 2368), 256, 0, s>>>(kbuf[(L.passes + 1) & 1], L.n, ls, fill,
+    launch_k(k_bin_scatter, small_grid(L.n, 2368), 256, 0, s, kbuf[(L.passes + 1) & 1], L.n, ls, fill,
                                                     slot, ctr);
     note_launches(1);
     // gamma and sigma are first read by the record pack (host mode: their
     // copies overlap the binning)
     if (gs_ready) cudaStreamWaitEvent(s, gs_ready, 0);
-    k_leaf_pack<<<std::min(grid_for((int64_t)L.nleaves, 8), 2368u), 256, 0, s>>>(ls, slot, (int)L.nleaves, x, y, g,
+    launch_k(k_leaf_pack, std::min(grid_for((int64_t)L.nleaves, 8), 2368u), 256, 0, s, ls, slot, (int)L.nleaves, x, y, g,
                                                               sigma, sigma_stride, fkeys, fperm,
                                                               src, ctr);
     note_launches(1);
@@ -784,17 +795,17 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     const size_t lb_words = (size_t)L.nchunks * B;
     const unsigned tiles = (unsigned)L.nchunks;
     cudaMemsetAsync(ghist, 0, L.hist_bytes, s);
-    k_keys_ghist<<<tiles, kTileThreads, 0, s>>>(x, y, L.n, xmin, ymin, side, L.levels, bits,
+    launch_k(k_keys_ghist, tiles, kTileThreads, 0, s, x, y, L.n, xmin, ymin, side, L.levels, bits,
                                                 L.passes, kbuf[0], ghist, ctr);
     note_launches(1);
     for (int p = 0; p < L.passes; ++p) {
         const bool last = p == L.passes - 1;
         if (last) {
-            k_pack_orig<<<small_grid(L.n), 256, 0, s>>>(x, y, g, sigma, sigma_stride, L.n, packed,
+            launch_k(k_pack_orig, small_grid(L.n), 256, 0, s, x, y, g, sigma, sigma_stride, L.n, packed,
                                                           ctr);
             note_launches(1);
         }
-        k_onesweep<<<tiles, kTileThreads, 0, s>>>(
+        launch_k(k_onesweep, tiles, kTileThreads, 0, s, 
             kbuf[p & 1], p == 0 ? nullptr : vbuf[p & 1], kbuf[(p + 1) & 1], vbuf[(p + 1) & 1], L.n,
             p * bits, bits, ghist + p * B, lbase + p * lb_words, tickets + p, last ? packed : nullptr,
             src, ctr);
@@ -802,13 +813,13 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     }
     *keys_out = fkeys;
     *perm_out = fperm;
-    k_leaf_starts<<<small_grid(L.n + 1, 1184), 256, 0, s>>>(fkeys, L.n, (int)L.nleaves, ls, ctr);
+    launch_k(k_leaf_starts, small_grid(L.n + 1, 1184), 256, 0, s, fkeys, L.n, (int)L.nleaves, ls, ctr);
     note_launches(1);
 }
 
 void launch_leaf_starts(const int* sorted_keys, int64_t n, int nleaves, int* leaf_starts,
                         cudaStream_t s) {
-    k_leaf_starts<<<grid_for(n + 1, 256), 256, 0, s>>>(sorted_keys, n, nleaves, leaf_starts,
+    launch_k(k_leaf_starts, grid_for(n + 1, 256), 256, 0, s, sorted_keys, n, nleaves, leaf_starts,
                                                         nullptr);
     note_launches(1);
 }
@@ -821,7 +832,7 @@ void launch_counts_tasks(const Layout& L, char* ws, Counters* ctr, bool tasks, R
     int64_t total = 0;
     for (int k = 0; k <= L.levels; ++k) total += 1ll << (2 * k);
     const int chunk = 32 * p2p_targets_per_lane();
-    k_counts_tasks<<<grid_for(total, 256), 256, 0, s>>>(ls, L.levels, total, chunk, rows, counts,
+    launch_k(k_counts_tasks, grid_for(total, 256), 256, 0, s, ls, L.levels, total, chunk, rows, counts,
                                                        nt, ctr);
     note_launches(1);
     (void)tasks;
@@ -840,7 +851,7 @@ void launch_tasks(const Layout& L, char* ws, Counters* ctr, Rows rows, bool gaus
     launch_scan_i32(nt, nl, (unsigned long long*)(ws + L.scan_state) +
                                 (size_t)L.passes * (L.scan_state_tiles + 1), s,
                     sym ? ctr : nullptr, gauss);
-    k_tasks_fill<<<grid_for(nl, 256), 256, 0, s>>>(ls, L.levels, chunk, rows, nt,
+    launch_k(k_tasks_fill, grid_for(nl, 256), 256, 0, s, ls, L.levels, chunk, rows, nt,
                                                  (int2*)(ws + L.tasks), ctr, gauss, sym);
     note_launches(1);
 }

@@ -21,6 +21,7 @@ __global__ void __launch_bounds__(kP2MWarps * 32)
     k_p2m(const Src* __restrict__ src, const int* __restrict__ ls, int levels, int P, double xmin,
           double ymin, double side, const Tables* __restrict__ T, Rows rows,
           double2* __restrict__ mult) {
+    pdl_enter();
     __shared__ double2 buf[kP2MWarps][32][33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m = 1 << levels;
@@ -94,6 +95,7 @@ __global__ void __launch_bounds__(128)
     k_p2m_grp(const Src* __restrict__ src, const int* __restrict__ ls, int levels, int P,
               double xmin, double ymin, double side, const Tables* __restrict__ T, Rows rows,
               double2* __restrict__ mult) {
+    pdl_enter();
     const int sub = threadIdx.x & (G - 1);
     const int m = 1 << levels;
     const int64_t leaf = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
@@ -165,16 +167,16 @@ void launch_p2m(const Layout& L, const Src* src, const int* leaf_starts, double 
         constexpr int G = 8;
         const unsigned blocks = (unsigned)((nl * G + 127) / 128);
         if (L.P <= 16)
-            k_p2m_grp<G, 16><<<blocks, 128, 0, s>>>(src, leaf_starts, L.levels, L.P, xmin, ymin,
+            launch_k(k_p2m_grp<G, 16>, blocks, 128, 0, s, src, leaf_starts, L.levels, L.P, xmin, ymin,
                                                     side, T, rows, mult_leaf);
         else if (L.P <= 24)
-            k_p2m_grp<G, 24><<<blocks, 128, 0, s>>>(src, leaf_starts, L.levels, L.P, xmin, ymin,
+            launch_k(k_p2m_grp<G, 24>, blocks, 128, 0, s, src, leaf_starts, L.levels, L.P, xmin, ymin,
                                                     side, T, rows, mult_leaf);
         else
-            k_p2m_grp<G, 32><<<blocks, 128, 0, s>>>(src, leaf_starts, L.levels, L.P, xmin, ymin,
+            launch_k(k_p2m_grp<G, 32>, blocks, 128, 0, s, src, leaf_starts, L.levels, L.P, xmin, ymin,
                                                     side, T, rows, mult_leaf);
     } else {
-        k_p2m<<<(unsigned)((nl + kP2MWarps - 1) / kP2MWarps), kP2MWarps * 32, 0, s>>>(
+        launch_k(k_p2m, (unsigned)((nl + kP2MWarps - 1) / kP2MWarps), kP2MWarps * 32, 0, s, 
             src, leaf_starts, L.levels, L.P, xmin, ymin, side, T, rows, mult_leaf);
     }
     note_launches(1);

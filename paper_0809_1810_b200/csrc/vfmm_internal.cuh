@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/vfmm.h"
 
 namespace vfmm {
@@ -93,6 +95,37 @@ __host__ __device__ __forceinline__ bool rows_touch(Rows r, int level_row, int s
 
 // Host-side count of kernel launches issued by the library (bench evidence).
 void note_launches(int k);
+
+// Programmatic dependent launch (PDL).  Every library kernel starts with
+// pdl_enter(): griddepcontrol.wait blocks until the preceding kernel of the
+// stream has completed and its memory is visible (a no-op without a
+// programmatic dependency), then launch_dependents lets the NEXT kernel's
+// CTAs be scheduled as soon as every CTA of this grid has started.  Kernels
+// are launched with launch_k (cudaLaunchAttributeProgrammaticStreamSerialization),
+// so the launch latency and ramp of a kernel overlap the tail of its
+// predecessor instead of adding to the chain (CUDA graphs keep the
+// programmatic edges).  Because every kernel waits before touching memory,
+// stream order semantics are unchanged.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_enabled();  // VFMM_PDL=0 disables the attribute (A/B measurement)
+template <typename... K, typename... A>
+inline void launch_k(void (*kern)(K...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     A&&... args) {
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+}
 
 // ---- kernels launchers (each enqueues on `s`) ----
 void launch_build(const Layout& L, const double* x, const double* y, const double* g,
