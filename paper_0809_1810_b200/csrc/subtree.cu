@@ -91,7 +91,10 @@ __device__ __forceinline__ int64_t lvl_off(int k, int P) {
     return (((int64_t)1 << (2 * k)) - 16) / 3 * P;
 }
 
-__global__ void __launch_bounds__(kSubThreads)
+#ifndef VFMM_L2L_MINB
+#define VFMM_L2L_MINB 4
+#endif
+__global__ void __launch_bounds__(kSubThreads, VFMM_L2L_MINB)
     k_l2l_fused(double2* __restrict__ loc, double2* __restrict__ leaf_loc,
                 const double2* __restrict__ anc_m2l, int ls, int levels, int P,
                 const Tables* __restrict__ T, Rows rows, FusedOut fo) {
@@ -110,41 +113,55 @@ __global__ void __launch_bounds__(kSubThreads)
         s2[i] = T->pow2neg[i];
         sfact[i] = T->invfact[i];
     }
-    const int n = threadIdx.x;
     // ---- ancestor chain: level 2 (complete after M2L) down to ls ----
-    if (n < P) {
-        const int sh = ls - 2;
+    // output n of a level is summed by 8 lanes (terms mm = n + lane8, step 8)
+    // and reduced by xor shuffles: P x 8 threads instead of P serial sums
+    if (threadIdx.x < P) {
+        const int n = threadIdx.x, sh = ls - 2;
         anc[n] = loc[lvl_off(2, P) + coef_base(2, cx >> sh, cy >> sh) + n * coef_stride(2)];
     }
     __syncthreads();
     int cur = 0;
+    const int l8 = threadIdx.x & 7;
     for (int k = 3; k <= ls; ++k) {
         const int sh = ls - k;
         const int ax = cx >> sh, ay = cy >> sh;
-        if (n < P) {
-            const double2* Lp = anc + cur * P;
-            const double2* Fq = sF + (2 * (ay & 1) + (ax & 1)) * P;
+        const double2* Lp = anc + cur * P;
+        const double2* Fq = sF + (2 * (ay & 1) + (ax & 1)) * P;
+        for (int n0 = 0; n0 < P; n0 += kSubThreads / 8) {  // block-uniform trip count
+            const int n = n0 + (threadIdx.x >> 3);
+            const bool nact = n < P;
             double sx = 0.0, sy = 0.0;
-            for (int mm = n; mm < P; ++mm) {
-                const double2 a = Lp[mm];
-                const double axs = a.x * s2[mm], ays = a.y * s2[mm];
-                const double2 f = Fq[mm - n];
-                sx = fma(axs, f.x, fma(-ays, f.y, sx));
-                sy = fma(axs, f.y, fma(ays, f.x, sy));
+            if (nact) {
+                for (int mm = n + l8; mm < P; mm += 8) {
+                    const double2 a = Lp[mm];
+                    const double axs = a.x * s2[mm], ays = a.y * s2[mm];
+                    const double2 f = Fq[mm - n];
+                    sx = fma(axs, f.x, fma(-ays, f.y, sx));
+                    sy = fma(axs, f.y, fma(ays, f.x, sy));
+                }
             }
-            const int64_t gi = lvl_off(k, P) + coef_base(k, ax, ay) + n * coef_stride(k);
-            // M2L part: shared ancestors (k < ls) from the read-only copy, since
-            // their writer CTA completes them in loc while others still read
-            double2 r = k < ls ? anc_m2l[gi] : loc[gi];
-            r.x += sx;
-            r.y += sy;
-            anc[(cur ^ 1) * P + n] = r;
-            const int mask = (1 << sh) - 1;
-            if ((cx & mask) == 0 && (cy & mask) == 0) {  // first CTA below: the writer
-                if (k == levels)
-                    leaf_loc[((int64_t)ay * (1 << k) + ax) * P + n] = r;
-                else
-                    loc[gi] = r;
+            // 8-lane groups are aligned within a warp; every lane takes part
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) {
+                sx += __shfl_xor_sync(0xffffffffu, sx, o);
+                sy += __shfl_xor_sync(0xffffffffu, sy, o);
+            }
+            if (nact && l8 == 0) {
+                const int64_t gi = lvl_off(k, P) + coef_base(k, ax, ay) + n * coef_stride(k);
+                // M2L part: shared ancestors (k < ls) from the read-only copy, since
+                // their writer CTA completes them in loc while others still read
+                double2 r = k < ls ? anc_m2l[gi] : loc[gi];
+                r.x += sx;
+                r.y += sy;
+                anc[(cur ^ 1) * P + n] = r;
+                const int mask = (1 << sh) - 1;
+                if ((cx & mask) == 0 && (cy & mask) == 0) {  // first CTA below: the writer
+                    if (k == levels)
+                        leaf_loc[((int64_t)ay * (1 << k) + ax) * P + n] = r;
+                    else
+                        loc[gi] = r;
+                }
             }
         }
         __syncthreads();
@@ -211,27 +228,63 @@ __global__ void __launch_bounds__(kSubThreads)
     const int side = 1 << depth, m = 1 << levels;
     const double r = fo.side / m, inv_r = 1.0 / r;
     const double2* leafs = sm + (size_t)sub_off(depth) * P;
-    for (int ly = 0; ly < side; ++ly) {
-        const int gy = cy * side + ly;
-        if (gy < rows.lo || gy >= rows.hi) continue;  // halo rows of a sharded run
-        const int row = gy * m + cx * side;
-        const int a0 = fo.ls[row], a1 = fo.ls[row + side];
-        for (int j = a0 + threadIdx.x; j < a1; j += blockDim.x) {
-            const int lx = (fo.keys[j] & (m - 1)) - cx * side;
-            const Src sj = fo.src[j];
+    // the particles of the subtree's leaf rows (one contiguous sorted range per
+    // row) as one flat index space, so each thread batches kB particles' loads
+    __shared__ int rb[16], rp[17];
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int ly = 0; ly < side; ++ly) {
+            const int gy = cy * side + ly;
+            rb[ly] = 0;
+            rp[ly] = acc;
+            if (gy < rows.lo || gy >= rows.hi) continue;  // halo rows of a sharded run
+            const int row = gy * m + cx * side;
+            const int a0 = fo.ls[row], a1 = fo.ls[row + side];
+            rb[ly] = a0;
+            acc += a1 - a0;
+        }
+        rp[side] = acc;
+    }
+    __syncthreads();
+    const int total = rp[side];
+    constexpr int kB = 4;
+    for (int base = threadIdx.x; base < total; base += kB * kSubThreads) {
+        int jj[kB], lyy[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            const int idx = base + u * kSubThreads;
+            int ly = 0;
+            while (ly + 1 < side && rp[ly + 1] <= idx) ++ly;
+            lyy[u] = ly;
+            jj[u] = idx < total ? rb[ly] + idx - rp[ly] : -1;
+        }
+        int key[kB], o[kB];
+        Src sj[kB];
+        double2 nv[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            const int j = jj[u] < 0 ? 0 : jj[u];
+            key[u] = fo.keys[j];
+            sj[u] = fo.src[j];
+            nv[u] = fo.near[j];
+            o[u] = fo.perm[j];
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            if (jj[u] < 0) continue;
+            const int ly = lyy[u], gy = cy * side + ly;
+            const int lx = (key[u] & (m - 1)) - cx * side;
             const double ccx = cell_center(fo.xmin, cx * side + lx, r);
             const double ccy = cell_center(fo.ymin, gy, r);
             const double2 f = eval_local(leafs + (size_t)(ly * side + lx) * P, 1, P,
-                                         (sj.x - ccx) * inv_r, (sj.y - ccy) * inv_r, sfact);
-            const double2 nv = fo.near[j];
+                                         (sj[u].x - ccx) * inv_r, (sj[u].y - ccy) * inv_r, sfact);
             // f_to_velocity: u = Im f / 2pi, v = Re f / 2pi; then far + near
-            const double uo = f.y * kInv2Pi + nv.x, vo = f.x * kInv2Pi + nv.y;
-            const int o = fo.perm[j];
+            const double uo = f.y * kInv2Pi + nv[u].x, vo = f.x * kInv2Pi + nv[u].y;
             if (fo.v) {
-                fo.u[o] = uo;
-                fo.v[o] = vo;
+                fo.u[o[u]] = uo;
+                fo.v[o[u]] = vo;
             } else {
-                reinterpret_cast<double2*>(fo.u)[o] = make_double2(uo, vo);
+                reinterpret_cast<double2*>(fo.u)[o[u]] = make_double2(uo, vo);
             }
         }
     }

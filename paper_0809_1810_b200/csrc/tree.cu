@@ -661,19 +661,29 @@ __global__ void k_leaf_starts(const int* __restrict__ keys, int64_t n, int nleav
 // (Tree.counts, quadtree.py:126-134):
 // a level-k cell covers 2^(l-k) leaf rows, each a contiguous leaf range.
 // Leaf cells also emit their P2P task count ceil(count / chunk).
-__global__ void k_counts_tasks(const int* __restrict__ ls, int levels, int64_t total_cells,
+__global__ void k_counts_tasks(const int* __restrict__ ls, int levels, int64_t total_threads,
                                int chunk, Rows rows, int* __restrict__ counts,
                                int* __restrict__ ntask, Counters* __restrict__ ctr) {
     pdl_enter();
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= total_cells) return;
-    int k = 0;
-    int64_t off = 0;
-    while (off + (1ll << (2 * k)) <= t) {
-        off += 1ll << (2 * k);
+    // A cell of level k spans s = 2^(levels-k) leaf rows; g = min(32, s)
+    // lanes split its rows and add their partial counts by xor shuffles (the
+    // coarse cells were serial 32..128-row loops).  Thread ranges per level:
+    // 4^k g_k threads, each level's range aligned to its g.
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int k = 0, g = 1;
+    int64_t off = 0, cell_off = 0;
+    for (;;) {
+        const int s = 1 << (levels - k);
+        g = s < 32 ? s : 32;
+        const int64_t nt = (1ll << (2 * k)) * g;
+        if (t < off + nt || k == levels) break;
+        off += nt;
+        cell_off += 1ll << (2 * k);
         ++k;
     }
-    const int64_t cell = t - off;
+    const bool valid = t < total_threads;
+    const int64_t cell = valid ? (t - off) / g : 0;
+    const int sub = valid ? (int)((t - off) % g) : 0;
     const int mk = 1 << k;
     const int ix = (int)(cell % mk), iy = (int)(cell / mk);
     const int m = 1 << levels;
@@ -682,20 +692,29 @@ __global__ void k_counts_tasks(const int* __restrict__ ls, int levels, int64_t t
     // are disjoint and their sum is the global occupancy
     const int r0 = max(iy * s, rows.lo), r1 = min((iy + 1) * s, rows.hi);
     int c = 0;
-    for (int r = r0; r < r1; ++r) {
-        const int64_t row = (int64_t)r * m;
-        c += ls[row + (int64_t)(ix + 1) * s] - ls[row + (int64_t)ix * s];
+    if (valid)
+        for (int r = r0 + sub; r < r1; r += g) {
+            const int64_t row = (int64_t)r * m;
+            c += ls[row + (int64_t)(ix + 1) * s] - ls[row + (int64_t)ix * s];
+        }
+    // every lane runs the same shuffles; a lane adds only within its g-group
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const int v = __shfl_xor_sync(0xffffffffu, c, o);
+        if (o < g) c += v;
     }
-    counts[t] = c;
-    // only leaves of the owned row strip get near-field tasks
     int full = 0;
-    if (k == levels) {
-        ntask[cell] = (iy >= rows.lo && iy < rows.hi) ? (c + chunk - 1) / chunk : 0;
-        full = ls[cell + 1] - ls[cell];  // owned and halo rows (the symmetric P2P touches both)
+    if (valid && sub == 0) {
+        counts[cell_off + cell] = c;
+        // only leaves of the owned row strip get near-field tasks
+        if (k == levels) {
+            ntask[cell] = (iy >= rows.lo && iy < rows.hi) ? (c + chunk - 1) / chunk : 0;
+            full = ls[cell + 1] - ls[cell];  // owned and halo rows (the symmetric P2P touches both)
+        }
     }
     // largest leaf: one atomic per warp
-    full = __reduce_max_sync(__activemask(), full);
-    if ((threadIdx.x & 31) == (__ffs(__activemask()) - 1) && full > 0) atomicMax(&ctr->max_leaf, full);
+    full = __reduce_max_sync(0xffffffffu, full);
+    if ((threadIdx.x & 31) == 0 && full > 0) atomicMax(&ctr->max_leaf, full);
 }
 
 __global__ void k_tasks_fill(const int* __restrict__ ls, int levels, int chunk, Rows rows,
@@ -829,8 +848,11 @@ void launch_counts_tasks(const Layout& L, char* ws, Counters* ctr, bool tasks, R
     const int* ls = (const int*)(ws + L.leaf_starts);
     int* counts = (int*)(ws + L.counts);
     int* nt = (int*)(ws + L.task_scratch);
-    int64_t total = 0;
-    for (int k = 0; k <= L.levels; ++k) total += 1ll << (2 * k);
+    int64_t total = 0;  // threads: 4^k cells x min(32, 2^(levels-k)) lanes per level
+    for (int k = 0; k <= L.levels; ++k) {
+        const int64_t rows_k = 1ll << (L.levels - k);
+        total += (1ll << (2 * k)) * (rows_k < 32 ? rows_k : 32);
+    }
     const int chunk = 32 * p2p_targets_per_lane();
     launch_k(k_counts_tasks, grid_for(total, 256), 256, 0, s, ls, L.levels, total, chunk, rows, counts,
                                                        nt, ctr);
