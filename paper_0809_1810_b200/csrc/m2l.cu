@@ -46,11 +46,11 @@ __device__ __forceinline__ void il_offset(int px, int py, int o, int& dx, int& d
 // of consecutive cells of one source plane, so each multipole coefficient
 // load is coalesced; the Hankel rows are block-uniform smem broadcasts.
 // G offset-unit groups (warps) per CTA, one CTA = 32 destinations: G = 3 (8
-// CTAs of 3 warps per SM) for large grids; for grids under ~4 waves of
-// 3-warp CTAs G = 15 (one unit per warp: no barrier imbalance) and for tiny
-// grids (< 600 CTAs) G = 9.  Measured (median t_m2l, 15-unit kernel):
-// config 2 0.0778 (G 9) / 0.0727 (G 5) / 0.0706 ms (G 15); config 1 0.0143
-// (G 9) / 0.0225 ms (G 15); config 3 1.20 ms (G 3).
+// CTAs of 3 warps per SM; 5 of the 15 units per warp) by default; G = 9 (3
+// CTAs of 9 warps) for tiny grids (< 600 CTAs), where more, shorter warps
+// fill the SMs.  Measured (median t_m2l, 15-unit kernel): config 1 0.0225
+// (G 3) / 0.0143 ms (G 9); config 2 0.0706-0.0717 (G 3) / 0.0727 (G 5) /
+// 0.0778 ms (G 9); config 3 1.20 ms (G 3).
 constexpr int kDestPerBlock = 32;
 
 // Symmetric offsets share their Hankel row up to conjugation and signs
@@ -180,12 +180,7 @@ template <int TN, int kGroups>
 #ifndef VFMM_M2L_MB9
 #define VFMM_M2L_MB9 3
 #endif
-#ifndef VFMM_M2L_MB15
-#define VFMM_M2L_MB15 2
-#endif
-__global__ void __launch_bounds__(kDestPerBlock * kGroups,
-                                  kGroups == 3 ? VFMM_M2L_MB3
-                                               : (kGroups == 9 ? VFMM_M2L_MB9 : VFMM_M2L_MB15))
+__global__ void __launch_bounds__(kDestPerBlock * kGroups, kGroups == 3 ? VFMM_M2L_MB3 : VFMM_M2L_MB9)
     k_m2l(const double2* __restrict__ mult, const int* __restrict__ counts, double2* __restrict__ loc,
           double2* __restrict__ anc, int anc_end, int levels, int P, int nchunks,
           const Tables* __restrict__ T, unsigned long long* __restrict__ m2l_count, Rows rows) {
@@ -349,16 +344,13 @@ void launch_tn(const Layout& L, const Tables* T, const double2* mult, const int*
     };
     const int anc_end = l2l_split_level(L.levels, L.P);
     // offset groups (warps) per CTA by grid size, see the kernel comment;
-    // VFMM_M2L_G = 3 / 9 / 15 overrides (tuning)
+    // VFMM_M2L_G = 3 / 9 overrides (tuning)
     static const int g_env = getenv("VFMM_M2L_G") ? atoi(getenv("VFMM_M2L_G")) : 0;
-    int g = blocks < 600 ? 9 : (blocks < 4 * 148 * 8 ? 15 : 3);
-    if (g_env == 3 || g_env == 9 || g_env == 15) g = g_env;
-    if (g != 3 && shm_of(g) > 48 * 1024) g = 3;
+    int g = blocks < 600 ? 9 : 3;
+    if (g_env == 3 || g_env == 9) g = g_env;
+    if (g == 9 && shm_of(9) > 48 * 1024) g = 3;
     if (g == 9)
-        launch_k(k_m2l<TN, 9>, (unsigned)blocks, kDestPerBlock * 9, shm_of(9), s, 
-            mult, counts, loc, anc, anc_end, L.levels, L.P, nchunks, T, &ctr->m2l_count, rows);
-    else if (g == 15)
-        launch_k(k_m2l<TN, 15>, (unsigned)blocks, kDestPerBlock * 15, shm_of(15), s, 
+        launch_k(k_m2l<TN, 9>, (unsigned)blocks, kDestPerBlock * 9, shm_of(9), s,
             mult, counts, loc, anc, anc_end, L.levels, L.P, nchunks, T, &ctr->m2l_count, rows);
     else
         launch_k(k_m2l<TN, 3>, (unsigned)blocks, kDestPerBlock * 3, shm_of(3), s, 

@@ -18,11 +18,27 @@ KEYS = [
 STALL = "smsp__average_warps_issue_stalled_"
 
 
+def summarise_all(path):
+    """One entry per profiled launch (keyed by kernel name, first launch wins)."""
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    res = {}
+    for vals in rows[2:]:
+        d = summarise_row(rows[0], rows[1], vals)
+        name = d["kernel"].split("(")[0].replace("unnamed>::", "").replace("void ", "").strip()
+        res.setdefault(name, d)
+    return res
+
+
 def summarise(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    head, units, vals = rows[0], rows[1], rows[2]
+    return summarise_row(rows[0], rows[1], rows[2])
+
+
+def summarise_row(head, units, vals):
     d = {k: [vals[head.index(k)], units[head.index(k)]] for k in KEYS if k in head}
     stalls = []
     for i, k in enumerate(head):
@@ -39,8 +55,11 @@ def summarise(path):
 if __name__ == "__main__":
     res = {}
     for arg in sys.argv[2:]:
-        name, path = arg.split("=", 1)
-        res[name] = summarise(path)
+        if "=" in arg:  # name=report with one launch
+            name, path = arg.split("=", 1)
+            res[name] = summarise(path)
+        else:  # report with several launches: one entry per kernel
+            res.update(summarise_all(arg))
     with open(sys.argv[1], "w") as f:
         json.dump(res, f, indent=1)
     print(json.dumps({k: [v["gpu__time_duration.sum"], v["top_stalls_per_issue"][:3]] for k, v in res.items()}))
