@@ -18,6 +18,7 @@ namespace {
 
 constexpr int kSubThreads = 256;
 
+
 __device__ __forceinline__ int sub_off(int s) { return ((1 << (2 * s)) - 1) / 3; }  // cells before sub-level s
 
 // Upward: CTA per cell at level lt = lf - depth; reads the 4^depth cells at
@@ -91,10 +92,11 @@ __device__ __forceinline__ int64_t lvl_off(int k, int P) {
     return (((int64_t)1 << (2 * k)) - 16) / 3 * P;
 }
 
-#ifndef VFMM_L2L_MINB
-#define VFMM_L2L_MINB 4
-#endif
-__global__ void __launch_bounds__(kSubThreads, VFMM_L2L_MINB)
+// CTA size: 128 threads (8 CTAs/SM: config 2's 1,024 CTAs in one wave;
+// downward 0.050 -> 0.043 ms, config 3 1.69 -> 1.47 ms) unless the grid is
+// small (config 1: 64 CTAs, where 256 threads per CTA are faster).
+template <int kL2LThreads>
+__global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
     k_l2l_fused(double2* __restrict__ loc, double2* __restrict__ leaf_loc,
                 const double2* __restrict__ anc_m2l, int ls, int levels, int P,
                 const Tables* __restrict__ T, Rows rows, FusedOut fo) {
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(kSubThreads, VFMM_L2L_MINB)
         const int ax = cx >> sh, ay = cy >> sh;
         const double2* Lp = anc + cur * P;
         const double2* Fq = sF + (2 * (ay & 1) + (ax & 1)) * P;
-        for (int n0 = 0; n0 < P; n0 += kSubThreads / 8) {  // block-uniform trip count
+        for (int n0 = 0; n0 < P; n0 += kL2LThreads / 8) {  // block-uniform trip count
             const int n = n0 + (threadIdx.x >> 3);
             const bool nact = n < P;
             double sx = 0.0, sy = 0.0;
@@ -248,11 +250,11 @@ __global__ void __launch_bounds__(kSubThreads, VFMM_L2L_MINB)
     __syncthreads();
     const int total = rp[side];
     constexpr int kB = 4;
-    for (int base = threadIdx.x; base < total; base += kB * kSubThreads) {
+    for (int base = threadIdx.x; base < total; base += kB * kL2LThreads) {
         int jj[kB], lyy[kB];
 #pragma unroll
         for (int u = 0; u < kB; ++u) {
-            const int idx = base + u * kSubThreads;
+            const int idx = base + u * kL2LThreads;
             int ly = 0;
             while (ly + 1 < side && rp[ly + 1] <= idx) ++ly;
             lyy[u] = ly;
@@ -336,8 +338,11 @@ void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_lo
     const int ls = l2l_split_level(L.levels, L.P);
     const size_t shm = sub_smem(L.levels - ls, L.P) + sizeof(double2) * (2 * L.P + 1) +
                        sizeof(double) * L.P;
-    launch_k(k_l2l_fused, (unsigned)(1ll << (2 * ls)), kSubThreads, shm, s, loc, leaf_loc, anc, ls,
-                                                                       L.levels, L.P, T, rows, fo);
+    const unsigned ctas = (unsigned)(1ll << (2 * ls));
+    if (ctas >= 148 * 4)
+        launch_k(k_l2l_fused<128>, ctas, 128, shm, s, loc, leaf_loc, anc, ls, L.levels, L.P, T, rows, fo);
+    else
+        launch_k(k_l2l_fused<256>, ctas, 256, shm, s, loc, leaf_loc, anc, ls, L.levels, L.P, T, rows, fo);
     note_launches(1);
 }
 
