@@ -432,7 +432,7 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         }
         // ---- upward ----
         launch_p2m(L, src, ls, xmin, ymin, side, mult + L.level_cell_off[levels] * L.P, T, rows, fs);
-        launch_m2m(L, T, mult, fs);
+        launch_m2m(L, T, mult, rows, fs);
         rec(2, fs);
     }
     bool fuse = false;  // L2P + combine inside the L2L launch (see below)

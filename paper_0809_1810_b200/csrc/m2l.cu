@@ -210,6 +210,16 @@ __global__ void __launch_bounds__(kDestPerBlock * kGroups, kGroups == 3 ? VFMM_M
     const int HL = TN + P - 1;
     const int group = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+    // sharded runs: CTAs whose 32 destinations all lie outside the owned row
+    // strip exit before staging the tables
+    {
+        const int half0 = 1 << (level - 1);
+        const int64_t psz0 = (int64_t)half0 * half0;
+        const int64_t j0 = blk * kDestPerBlock + lane;
+        const int iy0 = 2 * (j0 < psz0 ? (int)(j0 / half0) : 0) + py;
+        const bool act0 = j0 < psz0 && rows_touch(rows, iy0, levels - level);
+        if (!__syncthreads_or(act0)) return;
+    }
     // ---- stage the 27 offsets and their H rows of this parity class ----
     __shared__ int2 soff[27];
     if (threadIdx.x < 27) {

@@ -637,11 +637,13 @@ __global__ void VFMM_SYM_BOUNDS
     k_p2p_sym(const Src* __restrict__ src, const int* __restrict__ ls, Counters* __restrict__ ctr,
               int levels, int64_t n, Rows rows, const Tables* __restrict__ T,
               double2* __restrict__ near5, unsigned long long* __restrict__ pairs,
-              int items_per_warp) {
+              int items_per_warp, int item_base, int nitems) {
     pdl_enter();
     if (!p2p_symmetric(ctr, GAUSS)) return;  // the generic kernel handles it
     const int m = 1 << levels;
-    const int nitems = 1 << (2 * levels);  // one item per leaf
+    // one item per leaf of rows [rows.lo - 1, rows.hi) (all leaves when not
+    // sharded; the row below the strip pairs its halo leaves with the owned
+    // row above); leaf = item_base + item
     if ((int64_t)blockIdx.x * kSymWarps * items_per_warp >= nitems) return;  // spare CTA
     // dynamic shared memory: exp table | per-warp accumulators of the item's leaf
     extern __shared__ __align__(16) unsigned char sym_smem[];
@@ -658,8 +660,9 @@ __global__ void VFMM_SYM_BOUNDS
     int next = 0;
     if (lane == 0) next = atomicAdd(&ctr->task_cursor, 1);
     for (int it = 0; it < items_per_warp; ++it) {
-        const int leaf = __shfl_sync(0xffffffffu, next, 0);
-        if (leaf >= nitems) break;
+        const int item = __shfl_sync(0xffffffffu, next, 0);
+        if (item >= nitems) break;
+        const int leaf = item_base + item;
         if (lane == 0 && it + 1 < items_per_warp) next = atomicAdd(&ctr->task_cursor, 1);
         const int loA = ls[leaf], nA = ls[leaf + 1] - loA;
         if (nA == 0) continue;
@@ -916,7 +919,11 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
         const char* e = getenv("VFMM_P2P_SYM_K");
         KS_env = e ? atoi(e) : 0;
     }
-    const int64_t sym_items = 1ll << (2 * L.levels);  // one item per leaf
+    // one item per leaf of the rows the strip needs: [rows.lo - 1, rows.hi)
+    const int mrow = 1 << L.levels;
+    const int row0 = rows.lo > 0 ? rows.lo - 1 : 0, row1 = rows.hi < mrow ? rows.hi : mrow;
+    const int item_base = row0 * mrow;
+    const int64_t sym_items = (int64_t)(row1 > row0 ? row1 - row0 : 0) * mrow;
     int ks = KS_env > 0 ? KS_env : (int)(sym_items / ((int64_t)kSymWarps * 148 * 2 * 4));
     ks = ks < 2 ? 2 : (ks > 32 ? 32 : ks);
     const unsigned sblocks = (unsigned)((sym_items + kSymWarps * ks - 1) / (kSymWarps * ks));
@@ -936,9 +943,10 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
             cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
         attr_set.fetch_or(1ull << dev);
     }
-    if (!sym_disabled()) {
+    if (!sym_disabled() && sblocks > 0) {
         launch_k(sfn, sblocks, kSymWarps * 32, kSymSmem, s, src, leaf_starts, ctr, L.levels, L.n, rows, T,
-                                                      near_uv, &ctr->near_pairs, ks);
+                                                      near_uv, &ctr->near_pairs, ks, item_base,
+                 (int)sym_items);
         note_launches(1);
     }
 }

@@ -25,8 +25,28 @@ __device__ __forceinline__ int sub_off(int s) { return ((1 << (2 * s)) - 1) / 3;
 // level lf (global, planar), writes levels lf-1 .. lt.
 __global__ void __launch_bounds__(kSubThreads)
     k_m2m_subtree(double2* __restrict__ mult, int lf, int depth, int P, size_t off_lf,
-                  const Tables* __restrict__ T) {
+                  const Tables* __restrict__ T, int levels, Rows rows) {
     pdl_enter();
+    {
+        // sharded runs: a subtree outside the owned row strip has no local
+        // sources (P2M wrote zeros there) -- write its zero multipoles directly
+        const int lt0 = lf - depth, mt0 = 1 << lt0;
+        const int cx0 = blockIdx.x % mt0, cy0 = blockIdx.x / mt0;
+        if (!rows_touch(rows, cy0, levels - lt0)) {
+            size_t off = off_lf;
+            for (int s = depth - 1; s >= 0; --s) {
+                const int lvl = lt0 + s, side = 1 << s;
+                off -= (size_t)(1ll << (2 * lvl)) * P;
+                const int64_t cs = coef_stride(lvl);
+                for (int i = threadIdx.x; i < side * side * P; i += blockDim.x) {
+                    const int c = i / P, mm = i % P;
+                    mult[off + coef_base(lvl, cx0 * side + c % side, cy0 * side + c / side) +
+                         mm * cs] = make_double2(0.0, 0.0);
+                }
+            }
+            return;
+        }
+    }
     extern __shared__ double2 sm[];  // [sub_off(depth+1)][P] cells + tables
     double2* sE = sm + (size_t)sub_off(depth + 1) * P;  // [4][P]
     double* s2 = reinterpret_cast<double*>(sE + 4 * P);  // [P + 1]
@@ -301,14 +321,14 @@ int sub_depth(int P) { return sub_smem(3, P) <= 48 * 1024 ? 3 : 2; }
 
 }  // namespace
 
-void launch_m2m(const Layout& L, const Tables* T, double2* mult, cudaStream_t s) {
+void launch_m2m(const Layout& L, const Tables* T, double2* mult, Rows rows, cudaStream_t s) {
     const int d0 = sub_depth(L.P);
     for (int lf = L.levels; lf > 2;) {
         const int d = lf - 2 < d0 ? lf - 2 : d0;
         const int lt = lf - d;
         const size_t off_lf = L.level_cell_off[lf] * L.P;
         launch_k(k_m2m_subtree, (unsigned)(1ll << (2 * lt)), kSubThreads, sub_smem(d, L.P), s, 
-            mult, lf, d, L.P, off_lf, T);
+            mult, lf, d, L.P, off_lf, T, L.levels, rows);
         note_launches(1);
         lf = lt;
     }

@@ -144,7 +144,7 @@ void launch_tasks(const Layout& L, char* ws, Counters* ctr, Rows rows, bool gaus
 void launch_p2m(const Layout& L, const Src* src, const int* leaf_starts, double xmin, double ymin,
                 double side, double2* mult_leaf, const Tables* T, Rows rows, cudaStream_t s);
 void launch_init_counters(Counters* ctr, cudaStream_t s);
-void launch_m2m(const Layout& L, const Tables* T, double2* mult, cudaStream_t s);  // subtree.cu
+void launch_m2m(const Layout& L, const Tables* T, double2* mult, Rows rows, cudaStream_t s);  // subtree.cu
 void launch_leaf_locals_copy(const Layout& L, const double2* loc, double2* leaf_loc, cudaStream_t s);
 void launch_m2l(const Layout& L, const Tables* T, const double2* mult, const int* counts,
                 double2* loc, double2* anc, Counters* ctr, Rows rows, cudaStream_t s);
