@@ -963,9 +963,18 @@ static void launch_p2p_generic(const Layout& L, const Tables* T, const Src* src,
         K = e ? atoi(e) : 2;
         if (K < 1) K = 2;
     }
-    const size_t per_block = (size_t)kP2PWarps * K;
-    const unsigned blocks = (unsigned)((L.max_tasks * kNearRows + per_block - 1) / per_block);
-    const int kk = K;
+    // The grid covers the upper bound of work items; capped at kGenericCap
+    // CTAs (items per warp raised to match), so that in symmetric mode --
+    // where every CTA exits at once -- the idle launch stays cheap (config 3:
+    // 147K idle CTAs cost ~65 us).  VFMM_P2P_GRID_CAP overrides (tuning).
+    static const size_t cap = getenv("VFMM_P2P_GRID_CAP") ? (size_t)atol(getenv("VFMM_P2P_GRID_CAP"))
+                                                          : (size_t)148 * 2 * 8;
+    const size_t max_items = L.max_tasks * kNearRows;
+    size_t per_block = (size_t)kP2PWarps * K;
+    if ((max_items + per_block - 1) / per_block > cap && cap > 0)
+        per_block = ((max_items + cap - 1) / cap + kP2PWarps - 1) / kP2PWarps * kP2PWarps;
+    const unsigned blocks = (unsigned)((max_items + per_block - 1) / per_block);
+    const int kk = (int)(per_block / kP2PWarps);
     const bool g = kernel == VFMM_KERNEL_GAUSSIAN;
     auto* fn = p2p_targets_per_lane() == 2 ? (g ? k_p2p<true, 2> : k_p2p<false, 2>)
                                            : (g ? k_p2p<true, 1> : k_p2p<false, 1>);

@@ -649,11 +649,19 @@ __global__ void k_leaf_starts(const int* __restrict__ keys, int64_t n, int nleav
                               int* __restrict__ ls, const Counters* __restrict__ ctr) {
     pdl_enter();
     if (ctr && !ctr->sort_fallback) return;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int prev = i > 0 ? keys[i - 1] : -1;
-        const int cur = i < n ? keys[i] : nleaves;
-        for (int k = prev + 1; k <= cur; ++k) ls[k] = (int)i;
+    // leaf-parallel lower_bound in the sorted keys: ls[k] = first i with
+    // keys[i] >= k.  (A particle-parallel fill of the gaps between consecutive
+    // keys left one thread filling every empty leaf of a long gap -- the
+    // leaves outside a rank's row strip: 0.8 ms at config 3 on 8 ranks.)
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k <= nleaves;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (keys[mid] < k) lo = mid + 1;
+            else hi = mid;
+        }
+        ls[k] = (int)lo;
     }
 }
 
@@ -832,13 +840,14 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     }
     *keys_out = fkeys;
     *perm_out = fperm;
-    launch_k(k_leaf_starts, small_grid(L.n + 1, 1184), 256, 0, s, fkeys, L.n, (int)L.nleaves, ls, ctr);
+    launch_k(k_leaf_starts, small_grid((int64_t)L.nleaves + 1, 2368), 256, 0, s, fkeys, L.n,
+             (int)L.nleaves, ls, ctr);
     note_launches(1);
 }
 
 void launch_leaf_starts(const int* sorted_keys, int64_t n, int nleaves, int* leaf_starts,
                         cudaStream_t s) {
-    launch_k(k_leaf_starts, grid_for(n + 1, 256), 256, 0, s, sorted_keys, n, nleaves, leaf_starts,
+    launch_k(k_leaf_starts, grid_for((int64_t)nleaves + 1, 256), 256, 0, s, sorted_keys, n, nleaves, leaf_starts,
                                                         nullptr);
     note_launches(1);
 }
