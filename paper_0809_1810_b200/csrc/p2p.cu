@@ -913,7 +913,7 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
     // the far chain finds free slots and the tail is short), otherwise as
     // few CTAs as possible (each stages the 60 KB exp table).  Measured:
     // config 1 (1K leaves) K=2, config 2 (16K) K=2..3, config 3 (262K) K=32
-    // best.  VFMM_P2P_SYM_K overrides (tuning).
+    // best (before the one-item rule below).  VFMM_P2P_SYM_K overrides (tuning).
     static int KS_env = -1;
     if (KS_env < 0) {
         const char* e = getenv("VFMM_P2P_SYM_K");
@@ -924,8 +924,13 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
     const int row0 = rows.lo > 0 ? rows.lo - 1 : 0, row1 = rows.hi < mrow ? rows.hi : mrow;
     const int item_base = row0 * mrow;
     const int64_t sym_items = (int64_t)(row1 > row0 ? row1 - row0 : 0) * mrow;
+    // at least 2 items per warp, except when even that leaves fewer than ~4
+    // waves of 2 CTAs per SM: one item per warp then (config 1: 1,024 leaves,
+    // P2P 0.144 -> 0.086 ms; a rank of an 8-way config-2 run: 0.266 -> 0.218
+    // ms per step; config 2 itself keeps 2: 0.7257 vs 0.7297 ms with 1)
+    const int kSymKMin = sym_items < (int64_t)kSymWarps * 2 * 148 * 2 * 4 ? 1 : 2;
     int ks = KS_env > 0 ? KS_env : (int)(sym_items / ((int64_t)kSymWarps * 148 * 2 * 4));
-    ks = ks < 2 ? 2 : (ks > 32 ? 32 : ks);
+    ks = ks < kSymKMin ? kSymKMin : (ks > 32 ? 32 : ks);
     const unsigned sblocks = (unsigned)((sym_items + kSymWarps * ks - 1) / (kSymWarps * ks));
     static int minb = 0;
     if (!minb) {
