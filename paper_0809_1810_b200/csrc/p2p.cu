@@ -968,12 +968,12 @@ static void launch_p2p_generic(const Layout& L, const Tables* T, const Src* src,
         K = e ? atoi(e) : 2;
         if (K < 1) K = 2;
     }
-    // The grid covers the upper bound of work items; capped at kGenericCap
-    // CTAs (items per warp raised to match), so that in symmetric mode --
-    // where every CTA exits at once -- the idle launch stays cheap (config 3:
-    // 147K idle CTAs cost ~65 us).  VFMM_P2P_GRID_CAP overrides (tuning).
+    // The grid covers the upper bound of work items (VFMM_P2P_GRID_CAP caps it,
+    // raising the items per warp -- tuning only: in symmetric mode the idle
+    // CTAs of this kernel give the far chain a head start before P2P fills
+    // the GPU, and capping them cost config 3 3.6%: 14.23 -> 14.75 ms).
     static const size_t cap = getenv("VFMM_P2P_GRID_CAP") ? (size_t)atol(getenv("VFMM_P2P_GRID_CAP"))
-                                                          : (size_t)148 * 2 * 8;
+                                                          : (size_t)0;
     const size_t max_items = L.max_tasks * kNearRows;
     size_t per_block = (size_t)kP2PWarps * K;
     if ((max_items + per_block - 1) / per_block > cap && cap > 0)
