@@ -37,6 +37,8 @@ struct Resources {
     cudaStream_t far = nullptr;   // far-field chain
     cudaStream_t near = nullptr;  // near field
     cudaStream_t comp = nullptr;  // compute stream of host-buffer evaluates
+    cudaStream_t lsd = nullptr;   // LSD radix branch of the tree build
+    cudaEvent_t lsd_fork = nullptr, lsd_join = nullptr;
     cudaEvent_t fork = nullptr, join_far = nullptr, join_near = nullptr;
     cudaEvent_t xy = nullptr, gs = nullptr, done = nullptr;
     cudaEvent_t ev[9] = {};
@@ -138,6 +140,9 @@ Resources* resources_for(int dev) {
         if (cudaStreamCreateWithPriority(&r.near, cudaStreamNonBlocking, pn) != cudaSuccess)
             return nullptr;
         if (cudaStreamCreateWithFlags(&r.comp, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        if (cudaStreamCreateWithFlags(&r.lsd, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        cudaEventCreateWithFlags(&r.lsd_fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&r.lsd_join, cudaEventDisableTiming);
         if (cudaMallocHost((void**)&r.hctr, sizeof(Counters)) != cudaSuccess) return nullptr;
         cudaEventCreateWithFlags(&r.xy, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&r.gs, cudaEventDisableTiming);
@@ -406,12 +411,16 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
     }
 
     cudaStream_t fs = cs;
+    // VFMM_LSD_BRANCH=1: the LSD radix kernels as a parallel branch of the build
+    // (off by default: measured no gain -- config 2 0.7313 vs 0.7317 ms in line)
+    static const bool lsd_branch = getenv("VFMM_LSD_BRANCH") && getenv("VFMM_LSD_BRANCH")[0] == '1';
     if (up) {
         if (!hio) rec(0, cs);
         // ---- build: binning, stable sort, pack, leaf starts, occupancy, tasks ----
         launch_init_counters(ctr, cs);
         launch_build(L, x, y, gamma, kernel == VFMM_KERNEL_GAUSSIAN ? sigma : nullptr, xmin, ymin,
-                     side, ws, ctr, cs, &keys, &perm, gs_ready, sigma_scalar ? 0 : 1);
+                     side, ws, ctr, cs, &keys, &perm, gs_ready, sigma_scalar ? 0 : 1,
+                     lsd_branch ? R->lsd : nullptr, R->lsd_fork, R->lsd_join);
         launch_counts_tasks(L, ws, ctr, !far_only, rows, kernel == VFMM_KERNEL_GAUSSIAN, cs);
         rec(1, cs);
         // Overlap: the far-field chain and the near field run on two streams

@@ -774,10 +774,27 @@ void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream
     note_launches(1);
 }
 
+// Zero up to four scratch regions in one launch (the build's look-back
+// states, leaf counts, slot fills and LSD histograms; memset nodes would break
+// the programmatic-launch chain).
+struct ZeroRegions {
+    int* p[4];
+    int64_t n[4];  // ints
+};
+__global__ void k_zero_regions(ZeroRegions z) {
+    pdl_enter();
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+        for (int64_t i = t0; i < z.n[r]; i += stride) z.p[r][i] = 0;
+}
+
 void launch_build(const Layout& L, const double* x, const double* y, const double* g,
                   const double* sigma, double xmin, double ymin, double side, char* ws,
                   Counters* ctr, cudaStream_t s, int** keys_out, int** perm_out,
-                  cudaEvent_t gs_ready, int sigma_stride) {
+                  cudaEvent_t gs_ready, int sigma_stride, cudaStream_t lsd_stream,
+                  cudaEvent_t lsd_fork, cudaEvent_t lsd_join) {
     int* kbuf[2] = {(int*)(ws + L.key_a), (int*)(ws + L.key_b)};
     int* vbuf[2] = {(int*)(ws + L.val_a), (int*)(ws + L.val_b)};
     const int bits = L.digit_bits;
@@ -789,23 +806,38 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     int* fkeys = kbuf[L.passes & 1];  // final buffers of either path (vfmm_layout_of)
     int* fperm = vbuf[L.passes & 1];
     Src* src = (Src*)(ws + L.src);
-    cudaMemsetAsync(ws + L.scan_state, 0, L.scan_state_bytes, s);
+    int* fill = (int*)(ws + L.task_scratch);  // free until the task counts
+    int* ghist = (int*)(ws + L.hist);         // LSD: passes x B global digit counts, tickets, look-back
+    {
+        ZeroRegions z{{(int*)(ws + L.scan_state), ls, fill, ghist},
+                      {(int64_t)(L.scan_state_bytes / sizeof(int)), (int64_t)L.nleaves + 1,
+                       (int64_t)L.nleaves, (int64_t)(L.hist_bytes / sizeof(int))}};
+        launch_k(k_zero_regions, 296, 256, 0, s, z);
+        note_launches(1);
+    }
 
     launch_k(k_sort_probe, 1, 256, 0, s, x, y, L.n, xmin, ymin, side, L.levels, force_lsd(), ctr);
     note_launches(1);
     // ---- counting path (kernels return at once if the probe chose LSD) ----
-    cudaMemsetAsync(ls, 0, sizeof(int) * (L.nleaves + 1), s);
     launch_k(k_bin_count, small_grid(L.n, 2368), 256, 0, s, x, y, L.n, xmin, ymin, side, L.levels,
                                                   kbuf[(L.passes + 1) & 1], ls, ctr);
     note_launches(1);
     launch_scan_i32(ls, (int64_t)L.nleaves + 1, state(L.passes + 1), s, nullptr, false,
                     &ctr->sort_fallback, kSortLsdProbe);
-    int* fill = (int*)(ws + L.task_scratch);  // free until the task counts
-    cudaMemsetAsync(fill, 0, sizeof(int) * L.nleaves, s);
     int* slot = vbuf[(L.passes + 1) & 1];
     launch_k(k_bin_scatter, small_grid(L.n, 2368), 256, 0, s, kbuf[(L.passes + 1) & 1], L.n, ls, fill,
                                                     slot, ctr);
     note_launches(1);
+    // The path choice is final after k_bin_scatter (a leaf > 128 switches to
+    // LSD there).  With a side stream the LSD kernels -- which return at once
+    // on the counting path -- run as a parallel branch joined after
+    // k_leaf_pack, off the counting path's critical chain (and vice versa).
+    const bool branch = lsd_stream && lsd_fork && lsd_join;
+    cudaStream_t ls_s = branch ? lsd_stream : s;
+    if (branch) {
+        cudaEventRecord(lsd_fork, s);
+        cudaStreamWaitEvent(lsd_stream, lsd_fork, 0);
+    }
     // gamma and sigma are first read by the record pack (host mode: their
     // copies overlap the binning)
     if (gs_ready) cudaStreamWaitEvent(s, gs_ready, 0);
@@ -816,23 +848,22 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
 
     // ---- LSD radix path (kernels return at once unless ctr->sort_fallback) ----
     Src* packed = (Src*)(ws + L.near_uv);  // free until the near field runs (>= 32 B per particle)
-    int* ghist = (int*)(ws + L.hist);     // passes x B global digit counts, tickets, look-back
     int* tickets = ghist + L.passes * B;
     unsigned* lbase = (unsigned*)(tickets + 8);
     const size_t lb_words = (size_t)L.nchunks * B;
     const unsigned tiles = (unsigned)L.nchunks;
-    cudaMemsetAsync(ghist, 0, L.hist_bytes, s);
-    launch_k(k_keys_ghist, tiles, kTileThreads, 0, s, x, y, L.n, xmin, ymin, side, L.levels, bits,
+    launch_k(k_keys_ghist, tiles, kTileThreads, 0, ls_s, x, y, L.n, xmin, ymin, side, L.levels, bits,
                                                 L.passes, kbuf[0], ghist, ctr);
     note_launches(1);
     for (int p = 0; p < L.passes; ++p) {
         const bool last = p == L.passes - 1;
         if (last) {
-            launch_k(k_pack_orig, small_grid(L.n), 256, 0, s, x, y, g, sigma, sigma_stride, L.n, packed,
+            if (branch && gs_ready) cudaStreamWaitEvent(ls_s, gs_ready, 0);
+            launch_k(k_pack_orig, small_grid(L.n), 256, 0, ls_s, x, y, g, sigma, sigma_stride, L.n, packed,
                                                           ctr);
             note_launches(1);
         }
-        launch_k(k_onesweep, tiles, kTileThreads, 0, s, 
+        launch_k(k_onesweep, tiles, kTileThreads, 0, ls_s, 
             kbuf[p & 1], p == 0 ? nullptr : vbuf[p & 1], kbuf[(p + 1) & 1], vbuf[(p + 1) & 1], L.n,
             p * bits, bits, ghist + p * B, lbase + p * lb_words, tickets + p, last ? packed : nullptr,
             src, ctr);
@@ -840,9 +871,13 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     }
     *keys_out = fkeys;
     *perm_out = fperm;
-    launch_k(k_leaf_starts, small_grid((int64_t)L.nleaves + 1, 2368), 256, 0, s, fkeys, L.n,
+    launch_k(k_leaf_starts, small_grid((int64_t)L.nleaves + 1, 2368), 256, 0, ls_s, fkeys, L.n,
              (int)L.nleaves, ls, ctr);
     note_launches(1);
+    if (branch) {
+        cudaEventRecord(lsd_join, lsd_stream);
+        cudaStreamWaitEvent(s, lsd_join, 0);
+    }
 }
 
 void launch_leaf_starts(const int* sorted_keys, int64_t n, int nleaves, int* leaf_starts,

@@ -131,7 +131,10 @@ inline void launch_k(void (*kern)(K...), dim3 grid, dim3 block, size_t smem, cud
 void launch_build(const Layout& L, const double* x, const double* y, const double* g,
                   const double* sigma, double xmin, double ymin, double side, char* ws,
                   Counters* ctr, cudaStream_t s, int** keys_out, int** perm_out,
-                  cudaEvent_t gs_ready = nullptr, int sigma_stride = 1);
+                  cudaEvent_t gs_ready = nullptr, int sigma_stride = 1,
+                  // optional: the LSD radix kernels as a parallel branch (fork / join events)
+                  cudaStream_t lsd_stream = nullptr, cudaEvent_t lsd_fork = nullptr,
+                  cudaEvent_t lsd_join = nullptr);
 void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream_t s,
                      const Counters* sym_skip, bool gauss, const int* skip_flag = nullptr,
                      int skip_val = 0);
