@@ -62,10 +62,15 @@ __global__ void __launch_bounds__(kSubThreads)
         const double2* src = mult + off_lf;
         const int64_t cs = coef_stride(lf);
         double2* dst = sm + (size_t)sub_off(depth) * P;
+        // coefficient-major order with the subtree's cells of one parity plane
+        // row consecutive: runs of side/2 cells are contiguous in the planar
+        // layout (the cell-major order read 16 B per coefficient stride)
+        const int hs = side >> 1;  // cells per plane row of the subtree (side >= 2)
         for (int i = threadIdx.x; i < ncell * P; i += blockDim.x) {
-            const int c = i / P, k = i % P;
-            const int gx = cx * side + (c % side), gy = cy * side + (c / side);
-            dst[i] = src[coef_base(lf, gx, gy) + k * cs];
+            const int k = i / ncell, r = i % ncell;
+            const int plane = r / (hs * hs), hy = (r / hs) % hs, hx = r % hs;
+            const int lx = 2 * hx + (plane & 1), ly = 2 * hy + (plane >> 1);
+            dst[(ly * side + lx) * P + k] = src[coef_base(lf, cx * side + lx, cy * side + ly) + k * cs];
         }
     }
     __syncthreads();
@@ -79,22 +84,39 @@ __global__ void __launch_bounds__(kSubThreads)
         double2* par = sm + (size_t)sub_off(s) * P;
         double2* gout = mult + off_level;
         const int64_t cs = coef_stride(lvl);
-        for (int i = threadIdx.x; i < side * side * P; i += blockDim.x) {
-            const int c = i / P, mm = i % P;
+        // 8 lanes per output coefficient: lane l8 sums the terms (q, k) with
+        // 4k + q = l8 mod 8 of the 4 (mm+1) terms, then an xor-shuffle
+        // reduction (the serial chains were up to 72 terms long, on 18 of 256
+        // threads at the subtree root)
+        const int nitem = side * side * P;
+        const int l8 = threadIdx.x & 7;
+        for (int i0 = 0; i0 < nitem; i0 += kSubThreads / 8) {  // block-uniform trip count
+            const int i = i0 + (threadIdx.x >> 3);
+            const bool act = i < nitem;
+            // coefficient-major: consecutive groups write consecutive cells
+            const int c = act ? i % (side * side) : 0, mm = act ? i / (side * side) : 0;
             const int px = c % side, py = c / side;
             double ax = 0.0, ay = 0.0;
-            for (int q = 0; q < 4; ++q) {
-                const int chx = 2 * px + (q & 1), chy = 2 * py + (q >> 1);
-                const double2* M = child + (size_t)(chy * 2 * side + chx) * P;
-                for (int k = 0; k <= mm; ++k) {
-                    const double2 a = M[k], e = sE[q * P + mm - k];
+            if (act) {
+                for (int t = l8; t < 4 * (mm + 1); t += 8) {
+                    const int q = t & 3, k = t >> 2;
+                    const int chx = 2 * px + (q & 1), chy = 2 * py + (q >> 1);
+                    const double2 a = child[(size_t)(chy * 2 * side + chx) * P + k];
+                    const double2 e = sE[q * P + mm - k];
                     ax = fma(a.x, e.x, fma(-a.y, e.y, ax));
                     ay = fma(a.x, e.y, fma(a.y, e.x, ay));
                 }
             }
-            const double2 r = make_double2(ax * s2[mm + 1], ay * s2[mm + 1]);
-            par[i] = r;
-            gout[coef_base(lvl, cx * side + px, cy * side + py) + mm * cs] = r;
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) {
+                ax += __shfl_xor_sync(0xffffffffu, ax, o);
+                ay += __shfl_xor_sync(0xffffffffu, ay, o);
+            }
+            if (act && l8 == 0) {
+                const double2 r = make_double2(ax * s2[mm + 1], ay * s2[mm + 1]);
+                par[c * P + mm] = r;
+                gout[coef_base(lvl, cx * side + px, cy * side + py) + mm * cs] = r;
+            }
         }
         __syncthreads();
     }
