@@ -368,3 +368,30 @@ def test_host_graph_path_matches_stream_launches(case):
         pend = [pipe.submit(*pinned) for _ in range(2)]
         for p in pend:
             assert torch.equal(p.result(), ref)
+
+
+@pytest.mark.gpu
+def test_programmatic_launch_off_is_bitwise_identical(tmp_path):
+    """Programmatic dependent launch changes only when kernels are scheduled:
+    an evaluate with the attribute disabled (VFMM_PDL=0, read at library load,
+    so in a child process) gives bitwise the same velocities and counters."""
+    import subprocess
+    import sys
+
+    w = W.config1()
+    cfg = vf.FmmConfig(w.levels, w.order, vf.KernelKind.GAUSSIAN_BLOB)
+    vel, st = vf.evaluate_arrays(w.x, w.y, w.gamma, w.sigma, cfg, vf.Domain(*W.DOMAIN), overlap=True)
+    out = tmp_path / "pdl_off.npy"
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_0809_1810_b200 as vf\n"
+        "from paper_0809_1810_b200 import workloads as W\n"
+        "w = W.config1(); cfg = vf.FmmConfig(w.levels, w.order, vf.KernelKind.GAUSSIAN_BLOB)\n"
+        "v, st = vf.evaluate_arrays(w.x, w.y, w.gamma, w.sigma, cfg, vf.Domain(*W.DOMAIN), overlap=True)\n"
+        "np.save(%r, np.concatenate([v.cpu().numpy().ravel(), [st.m2l_count, st.near_pair_count]]))\n"
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), str(out))
+    env = dict(os.environ, VFMM_PDL="0")
+    subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=600)
+    other = np.load(out)
+    mine = np.concatenate([vel.cpu().numpy().ravel(), [st.m2l_count, st.near_pair_count]])
+    assert np.array_equal(mine, other)
