@@ -237,6 +237,7 @@ def run_ours(args):
     if world > 1 or args.sharded:
         from paper_0809_1810_b200 import distributed
 
+        args.clock_sampler = ClockSampler  # clocks sampled on each rank's GPU in the timed region
         return distributed.bench_main(args)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)

@@ -347,12 +347,18 @@ def bench_main(args):
     cur = torch.cuda.current_stream(dev)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
+    sampler = getattr(args, "clock_sampler", None)
+    clk = sampler(local) if sampler is not None else None
+    if clk is not None:
+        clk.__enter__()
     for a, b in ev:
         flush.zero_()
         a.record(cur)
         graph.replay()
         b.record(cur)
     torch.cuda.synchronize(dev)
+    if clk is not None:
+        clk.__exit__(None, None, None)
     dist.barrier()
     ms = torch.tensor([sum(a.elapsed_time(b) for a, b in ev) / args.steps], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
@@ -393,5 +399,6 @@ def bench_main(args):
                             "velocities D2H; wall clock, max over ranks (bytes: largest rank)"},
             "gpu_launches": int(launches) * args.steps,
             "roofline": None, "cpu_baseline": None,
+            "clocks": clk.summary() if clk is not None else None,
         }), flush=True)
     dist.destroy_process_group()
