@@ -238,6 +238,7 @@ def run_ours(args):
         from paper_0809_1810_b200 import distributed
 
         args.clock_sampler = ClockSampler  # clocks sampled on each rank's GPU in the timed region
+        args.fp64_peak = fp64_peak          # roofline denominator, measured live per rank
         return distributed.bench_main(args)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)

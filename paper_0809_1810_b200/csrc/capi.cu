@@ -528,6 +528,10 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
     if (up) {
         stats->t_build = elapsed(R->ev[0], R->ev[1]);
         stats->t_upward = elapsed(R->ev[1], R->ev[2]);
+        if (!down && overlap) {  // sharded PHASE_UP: the near field it started
+            cudaEventSynchronize(R->ev[8]);
+            stats->t_near = elapsed(R->ev[7], R->ev[8]);
+        }
     }
     if (down) {
         stats->t_m2l = elapsed(R->ev[2], R->ev[3]);

@@ -380,6 +380,39 @@ def bench_main(args):
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
     nb = torch.tensor([owned.shape[1]], dtype=torch.int64, device=dev)
     dist.all_reduce(nb, op=dist.ReduceOp.MAX)
+
+    # roofline of the dominant kernel (P2P) per rank: one extra sharded evaluate
+    # in stats mode (phase events), achieved = 42 flop x this rank's near pairs /
+    # its near-field time; the line reports the slowest rank
+    roof = None
+    peak_fn = getattr(args, "fp64_peak", None)
+    if peak_fn is not None:
+        import ctypes
+
+        sh_vel = torch.zeros((2, shard.cols.shape[1]), dtype=torch.float64, device=dev)
+        backend.up(shard, cfg, dom)
+        backend.down(shard, cfg, dom, counters=False)
+        torch.cuda.synchronize(dev)
+        st_up, st_dn = _lib.VfmmStats(), _lib.VfmmStats()
+        for ph, st_ in ((_lib.FLAG_PHASE_UP, st_up), (_lib.FLAG_PHASE_DOWN, st_dn)):
+            rc = lib.vfmm_evaluate_shard(*backend._args(shard, cfg, dom), sh_vel[0].data_ptr(),
+                                         sh_vel[1].data_ptr(), backend.ws.ptr, backend.ws.nbytes,
+                                         ph | _lib.FLAG_OVERLAP | _lib.FLAG_STATS | _lib.FLAG_PHASE_TIMES,
+                                         ctypes.byref(st_), stream_ptr(dev))
+            _lib.check(rc, "vfmm_evaluate_shard(stats)")
+        t_near = float(st_up.t_near) * 1e-3  # s (the near field runs in PHASE_UP)
+        pairs = float(st_dn.near_pair_count)
+        ach = 42.0 * pairs / t_near / 1e12 if t_near > 0 else 0.0
+        peak = float(peak_fn(lib, torch, dev))
+        rr = torch.tensor([ach, peak, t_near * 1e3], dtype=torch.float64, device=dev)
+        gathered = [torch.zeros_like(rr) for _ in range(world)]
+        dist.all_gather(gathered, rr)
+        slow = min(gathered, key=lambda t: float(t[0]))
+        roof = {"bound": "fp64", "kernel": "k_p2p (near field), slowest rank",
+                "achieved": float(slow[0]), "peak": float(slow[1]), "unit": "TFLOP/s",
+                "frac": float(slow[0] / slow[1]) if float(slow[1]) > 0 else None,
+                "peak_source": "measured live: DFMA probe (vfmm_fp64_probe), per rank",
+                "traffic": None, "p2p_ms": float(slow[2]), "flop_per_pair": 42}
     if rank == 0:
         print(json.dumps({
             "metric": "FMM particle velocity evals/sec (fp64)", "value": w.n / (float(ms) * 1e-3),
@@ -398,7 +431,7 @@ def bench_main(args):
                     "mode": "per rank: owned particles H2D, halo exchange, sharded evaluate, "
                             "velocities D2H; wall clock, max over ranks (bytes: largest rank)"},
             "gpu_launches": int(launches) * args.steps,
-            "roofline": None, "cpu_baseline": None,
+            "roofline": roof, "cpu_baseline": None,
             "clocks": clk.summary() if clk is not None else None,
         }), flush=True)
     dist.destroy_process_group()
