@@ -21,6 +21,17 @@
  *                           by upward_pass / translate_pass (engine.py:114-187)
  *   vfmm_stats           <- engine.FmmRunStats         engine.py:58-74
  *
+ * Threading: every entry point may be called from any host thread.  Calls on
+ * one device serialise their enqueue (the library's internal per-device
+ * streams, events and pinned counter staging are shared); a call with
+ * VFMM_FLAG_STATS also holds the device until it has synchronised and read
+ * its counters.  Concurrent calls must use distinct workspaces (a workspace
+ * holds the whole state of one evaluate); the Python layer keys its cached
+ * workspaces by thread.  The caller's current device is restored on return.
+ *
+ * Sizes: 1 <= n < 2^30 (32-bit sorted indices), 2 <= levels <= 13,
+ * 0 <= order <= 60.
+ *
  * Status codes (return value of every function):
  */
 #ifndef VFMM_H
@@ -51,7 +62,9 @@ extern "C" {
                                    far-field chain; phase timings then overlap */
 #define VFMM_FLAG_FAR_ONLY 4u   /* build the tree and the local expansions only (no near field, no
                                    evaluation at the particles); used before vfmm_evaluate_at */
-#define VFMM_FLAG_PHASE_UP 8u   /* vfmm_evaluate_shard: build + P2M + M2M only */
+#define VFMM_FLAG_PHASE_UP 8u   /* vfmm_evaluate_shard: build + P2M + M2M (+ the near field when
+                                   VFMM_FLAG_OVERLAP is also set: it then runs on an internal stream
+                                   and hides the caller's exchange) */
 #define VFMM_FLAG_PHASE_TIMES 64u /* with VFMM_FLAG_STATS: also time every phase (CUDA events between
                                    the phases; costs ~0.1 ms per call) */
 #define VFMM_FLAG_SIGMA_SCALAR 128u /* vfmm_evaluate_host: sigma points to ONE core size shared by
@@ -59,7 +72,10 @@ extern "C" {
 #define VFMM_FLAG_UV_PAIRS 32u  /* u is an interleaved (N, 2) array of (u, v) rows -- the reference's
                                    return layout (engine.py:394-398); v is ignored */
 #define VFMM_FLAG_PHASE_DOWN 16u /* vfmm_evaluate_shard: M2L + L2L + P2P + L2P on the workspace of a
-                                    previous PHASE_UP call (after the caller reduced the multipoles) */
+                                    previous PHASE_UP call (after the caller exchanged the multipoles).
+                                    Whether the near field still has to run is taken from what that
+                                    PHASE_UP recorded for the workspace, not from this call's
+                                    VFMM_FLAG_OVERLAP; PHASE_DOWN without a PHASE_UP -> VFMM_EINVAL */
 #define VFMM_FLAG_GRAPH 256u    /* vfmm_evaluate_host: run the device part as a CUDA graph, captured
                                    on first use and cached per (device, workspace, n, levels, order,
                                    kernel, domain, flags); the copies stay plain async copies on
@@ -161,6 +177,14 @@ int vfmm_counts_region(int64_t n, int levels, int order, size_t* offset, size_t*
  * (synchronises `stream`).  Timings are left at 0.                          */
 int vfmm_read_stats(int64_t n, int levels, int order, int kernel, double side,
                     const void* workspace, vfmm_stats* stats, void* stream);
+
+/* Enqueue on `stream` a copy of the out-of-domain particle count of the last
+ * evaluate on `workspace` into *host_dst (pinned host memory; valid once the
+ * stream has reached this point).  The asynchronous host path uses it so that
+ * every result is domain-checked like engine.evaluate (quadtree.py:191-198)
+ * without an extra synchronisation.                                         */
+int vfmm_bad_count_async(int64_t n, int levels, int order, const void* workspace,
+                         int32_t* host_dst, void* stream);
 
 /* engine.evaluate_at (engine.py:401-460): velocity at m arbitrary in-domain
  * targets (tx, ty) from the particle set already processed by the LAST

@@ -47,6 +47,7 @@ EXPORTED_SYMBOLS = (
     "vfmm_mult_region",
     "vfmm_counts_region",
     "vfmm_read_stats",
+    "vfmm_bad_count_async",
     "vfmm_evaluate_at",
     "vfmm_direct_workspace_size",
     "vfmm_direct",
@@ -126,6 +127,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.vfmm_mult_region.argtypes = [_I64, _I, _I, ctypes.POINTER(_SZ), ctypes.POINTER(_SZ)]
         lib.vfmm_counts_region.argtypes = [_I64, _I, _I, ctypes.POINTER(_SZ), ctypes.POINTER(_SZ)]
         lib.vfmm_read_stats.argtypes = [_I64, _I, _I, _I, _D, _P, ctypes.POINTER(VfmmStats), _P]
+        lib.vfmm_bad_count_async.argtypes = [_I64, _I, _I, _P, _P, _P]
         lib.vfmm_evaluate_at.argtypes = [_P, _P, _I64, _I64, _D, _D, _D, _I, _I, _I, _P, _P, _P,
                                          ctypes.POINTER(_I64), _P]
         lib.vfmm_direct_workspace_size.argtypes = [_I64, _I64, ctypes.POINTER(_SZ)]

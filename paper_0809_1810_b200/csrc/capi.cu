@@ -43,6 +43,13 @@ struct Resources {
     cudaEvent_t xy = nullptr, gs = nullptr, done = nullptr;
     cudaEvent_t ev[9] = {};
     Counters* hctr = nullptr;  // pinned staging of the device counters (stats)
+    // Serialises the calls on this device: the internal streams, events and
+    // the pinned counter staging above are shared, so one call enqueues (and,
+    // with VFMM_FLAG_STATS, synchronises and reads its counters) at a time.
+    // Recursive: a graph capture (evaluate_host_graph) holds it around the
+    // evaluate_impl it captures, so no other call touches the shared streams
+    // while they are part of the capture.
+    std::recursive_mutex mu;
 };
 Resources g_res[kMaxDevices];
 
@@ -93,15 +100,32 @@ void build_tables(Tables* t) {
         t->exp2tab2[j] = (double)exp2l((long double)(j - (kExpTab2N - 1)) / (long double)kExpSteps2);
 }
 
-int current_device_of(const void* p, int* dev) {
-    cudaPointerAttributes a;
-    if (p && cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeDevice) {
-        *dev = a.device;
-        return cudaSetDevice(a.device) == cudaSuccess ? 0 : -1;
+// Makes the device that owns `p` current for the duration of one C-ABI call
+// and restores the caller's current device when the call returns (the
+// reference has no device state; a call must not move torch's current
+// device).  A host / null pointer keeps the current device.
+struct DeviceGuard {
+    int prev = -1;
+    bool switched = false;
+    int bind(const void* p, int* dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) return -1;
+        *dev = prev;
+        cudaPointerAttributes a;
+        if (p && cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeDevice) {
+            *dev = a.device;
+            if (a.device != prev) {
+                if (cudaSetDevice(a.device) != cudaSuccess) return -1;
+                switched = true;
+            }
+            return 0;
+        }
+        cudaGetLastError();
+        return 0;
     }
-    cudaGetLastError();
-    return cudaGetDevice(dev) == cudaSuccess ? 0 : -1;
-}
+    ~DeviceGuard() {
+        if (switched) cudaSetDevice(prev);
+    }
+};
 
 const Tables* tables_for(int dev) {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -171,7 +195,7 @@ double decode_sigma(unsigned long long b) {
 }
 
 bool args_ok(int64_t n, int levels, int order, double side, int kernel) {
-    return n >= 1 && n < (int64_t)1 << 31 && levels >= 2 && levels <= VFMM_LEVELS_CAP &&
+    return n >= 1 && n < (int64_t)1 << 30 && levels >= 2 && levels <= VFMM_LEVELS_CAP &&
            order >= 0 && order <= VFMM_ORDER_CAP && side > 0.0 && std::isfinite(side) &&
            (kernel == VFMM_KERNEL_POINT || kernel == VFMM_KERNEL_GAUSSIAN);
 }
@@ -325,6 +349,28 @@ struct HostIO {
     double *hu, *hv;
 };
 
+// What PHASE_UP did on a workspace, read by the PHASE_DOWN that follows it.
+struct PhaseRecord {
+    bool up_done = false;       // a PHASE_UP ran and its PHASE_DOWN has not
+    bool near_started = false;  // that PHASE_UP launched the near field (OVERLAP)
+    cudaEvent_t join_near = nullptr;
+};
+std::mutex g_phase_mu;
+std::vector<std::pair<const void*, PhaseRecord*>> g_phase;
+
+PhaseRecord* phase_record(const void* ws) {
+    std::lock_guard<std::mutex> lk(g_phase_mu);
+    for (auto& e : g_phase)
+        if (e.first == ws) return e.second;
+    PhaseRecord* r = new PhaseRecord;
+    if (cudaEventCreateWithFlags(&r->join_near, cudaEventDisableTiming) != cudaSuccess) {
+        delete r;
+        return nullptr;
+    }
+    g_phase.emplace_back(ws, r);
+    return r;
+}
+
 // One evaluate (or one phase of a sharded evaluate) over leaf rows [row_lo, row_hi).
 int evaluate_impl(const double* x, const double* y, const double* gamma, const double* sigma,
                   int64_t n, double xmin, double ymin, double side, int levels, int order,
@@ -342,7 +388,7 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
     // far-field chain.  In a sharded run (separate phases) the near field is
     // launched at the end of PHASE_UP -- it needs only the local tree -- so it
     // also hides the caller's multipole all-reduce; PHASE_DOWN joins it.
-    const bool overlap = (flags & VFMM_FLAG_OVERLAP) != 0 && !far_only;
+    bool overlap = (flags & VFMM_FLAG_OVERLAP) != 0 && !far_only;
     const bool pairs = (flags & VFMM_FLAG_UV_PAIRS) != 0;
     if (pairs) v = nullptr;  // u is an interleaved (N, 2) array
     if (!x || !y || !gamma || (down && !far_only && (!u || (!pairs && !v)))) return VFMM_EINVAL;
@@ -352,13 +398,25 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         return VFMM_EINVAL;
     if (rows.lo < 0 || rows.hi > (1 << levels) || rows.lo > rows.hi) return VFMM_EINVAL;
     Layout L;
-    make_layout(n, levels, order, &L);
+    if (!make_layout(n, levels, order, &L)) return VFMM_EINVAL;
     if (!workspace || workspace_bytes < L.total) return VFMM_EWORKSPACE;
     int dev = 0;
-    if (current_device_of(hio ? workspace : (const void*)x, &dev) != 0) return VFMM_ECUDA;
+    DeviceGuard dg;
+    if (dg.bind(hio ? workspace : (const void*)x, &dev) != 0) return VFMM_ECUDA;
     const Tables* T = tables_for(dev);
     Resources* R = resources_for(dev);
     if (!T || !R) return VFMM_ECUDA;
+    std::lock_guard<std::recursive_mutex> call_lock(R->mu);
+    // Sharded phases: PHASE_DOWN joins the near field only if PHASE_UP on
+    // this workspace started it (recorded per workspace), whatever its own
+    // OVERLAP flag says; PHASE_DOWN without a preceding PHASE_UP is invalid.
+    PhaseRecord* rec_up = nullptr;
+    if (up != down) {
+        rec_up = phase_record(workspace);
+        if (!rec_up) return VFMM_ECUDA;
+        if (down && !rec_up->up_done) return VFMM_EINVAL;
+        if (down) overlap = rec_up->near_started;
+    }
     cudaStream_t s = (cudaStream_t)stream;
     char* ws = (char*)workspace;
     Counters* ctr = (Counters*)(ws + L.counters);
@@ -436,8 +494,12 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
             rec(7, R->near);
             near_field(R->near);
             rec(8, R->near);
-            cudaEventRecord(R->join_near, R->near);
+            cudaEventRecord(rec_up->join_near, R->near);
             fs = cs;  // the far chain stays on the caller's stream (the all-reduce follows it)
+        }
+        if (rec_up) {
+            rec_up->up_done = true;
+            rec_up->near_started = overlap;
         }
         // ---- upward ----
         launch_p2m(L, src, ls, xmin, ymin, side, mult + L.level_cell_off[levels] * L.P, T, rows, fs);
@@ -488,8 +550,9 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
             cudaStreamWaitEvent(cs, R->join_far, 0);
             cudaStreamWaitEvent(cs, R->join_near, 0);
         } else if (overlap) {  // sharded PHASE_DOWN: join the near field started in PHASE_UP
-            cudaStreamWaitEvent(cs, R->join_near, 0);
+            cudaStreamWaitEvent(cs, rec_up->join_near, 0);
         }
+        if (rec_up) rec_up->up_done = false;  // one PHASE_DOWN per PHASE_UP
         if (!far_only && !fuse) {
             if (!overlap) near_field(cs);
             rec(5, cs);
@@ -615,12 +678,14 @@ int evaluate_host_graph(const HostIO& io, int64_t n, double xmin, double ymin, d
         return -1;
     }
     Layout L;
-    make_layout(n, levels, order, &L);
+    if (!make_layout(n, levels, order, &L)) return VFMM_EINVAL;
     if (!workspace || workspace_bytes < L.total) return VFMM_EWORKSPACE;
     int dev = 0;
-    if (current_device_of(workspace, &dev) != 0) return VFMM_ECUDA;
+    DeviceGuard guard;
+    if (guard.bind(workspace, &dev) != 0) return VFMM_ECUDA;
     Resources* R = resources_for(dev);
     if (!R || !tables_for(dev)) return VFMM_ECUDA;
+    std::lock_guard<std::recursive_mutex> call_lock(R->mu);  // capture, ev[], hctr
     char* ws = (char*)workspace;
     double* st = (double*)(ws + L.stage);
     double *dx = st, *dy = st + n, *dg = st + 2 * n, *dsg = st + 3 * n, *du = st + 4 * n,
@@ -765,7 +830,8 @@ int vfmm_read_stats(int64_t n, int levels, int order, int kernel, double side,
     Layout L;
     if (!stats || !workspace || !make_layout(n, levels, order, &L)) return VFMM_EINVAL;
     int dev = 0;
-    current_device_of(workspace, &dev);
+    DeviceGuard dg;
+    if (dg.bind(workspace, &dev) != 0) return VFMM_ECUDA;
     if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return VFMM_ECUDA;
     Counters c;
     if (cudaMemcpy(&c, (const char*)workspace + L.counters, sizeof c, cudaMemcpyDeviceToHost) !=
@@ -774,6 +840,19 @@ int vfmm_read_stats(int64_t n, int levels, int order, int kernel, double side,
     std::memset(stats, 0, sizeof(*stats));
     fill_stats(L, c, kernel, side, stats);
     return c.bad_count ? VFMM_EDOMAIN : VFMM_OK;
+}
+
+int vfmm_bad_count_async(int64_t n, int levels, int order, const void* workspace,
+                         int32_t* host_dst, void* stream) {
+    Layout L;
+    if (!workspace || !host_dst || !make_layout(n, levels, order, &L)) return VFMM_EINVAL;
+    int dev = 0;
+    DeviceGuard dg;
+    if (dg.bind(workspace, &dev) != 0) return VFMM_ECUDA;
+    const Counters* ctr = (const Counters*)((const char*)workspace + L.counters);
+    cudaMemcpyAsync(host_dst, &ctr->bad_count, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                    (cudaStream_t)stream);
+    return cudaGetLastError() == cudaSuccess ? VFMM_OK : VFMM_ECUDA;
 }
 
 int vfmm_evaluate_at(const double* tx, const double* ty, int64_t m, int64_t n, double xmin,
@@ -786,9 +865,10 @@ int vfmm_evaluate_at(const double* tx, const double* ty, int64_t m, int64_t n, d
         return VFMM_OK;
     }
     Layout L;
-    make_layout(n, levels, order, &L);
+    if (!make_layout(n, levels, order, &L)) return VFMM_EINVAL;
     int dev = 0;
-    if (current_device_of(tx, &dev) != 0) return VFMM_ECUDA;
+    DeviceGuard dg;
+    if (dg.bind(tx, &dev) != 0) return VFMM_ECUDA;
     const Tables* T = tables_for(dev);
     if (!T) return VFMM_ECUDA;
     cudaStream_t s = (cudaStream_t)stream;
@@ -827,7 +907,8 @@ int vfmm_direct(const double* tx, const double* ty, int64_t m, const double* x, 
     vfmm_direct_workspace_size(m, n, &need);
     if (!workspace || workspace_bytes < need) return VFMM_EWORKSPACE;
     int dev = 0;
-    if (current_device_of(tx, &dev) != 0) return VFMM_ECUDA;
+    DeviceGuard dg;
+    if (dg.bind(tx, &dev) != 0) return VFMM_ECUDA;
     const Tables* T = tables_for(dev);
     if (!T) return VFMM_ECUDA;
     const int ns = direct_nsplit(m, n);
@@ -843,7 +924,8 @@ int64_t vfmm_launch_count(void) { return (int64_t)g_launches.load(); }
 int vfmm_fp64_probe(double* sink, int blocks, int iters, double* flops, void* stream) {
     if (!sink || blocks < 1 || iters < 1) return VFMM_EINVAL;
     int dev = 0;
-    if (current_device_of(sink, &dev) != 0) return VFMM_ECUDA;
+    DeviceGuard dg;
+    if (dg.bind(sink, &dev) != 0) return VFMM_ECUDA;
     launch_k(k_fp64_probe, blocks, 256, 0, (cudaStream_t)stream, sink, iters);
     note_launches(1);
     if (flops) *flops = (double)blocks * 256.0 * (double)iters * 32.0 * 2.0;

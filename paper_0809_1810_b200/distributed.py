@@ -117,10 +117,12 @@ def redistribute(x, y, gamma, sigma, ids, domain, levels: int, group=None) -> Sh
 class CudaShardBackend:
     """PHASE_UP / PHASE_DOWN of ``vfmm_evaluate_shard`` on this rank's GPU."""
 
-    def __init__(self, device: torch.device, private_workspace: bool = False):
+    def __init__(self, device: torch.device, private_workspace: bool = False,
+                 up_flags: int = _lib.FLAG_OVERLAP, down_flags: int = _lib.FLAG_OVERLAP):
         require_cuda()
         self.device = device
         self.private = private_workspace
+        self.up_flags, self.down_flags = up_flags, down_flags
         self.lib = _lib.load()
         self.ws = None
 
@@ -148,7 +150,7 @@ class CudaShardBackend:
         # asynchronous; OVERLAP starts the near field here (it needs only the local tree)
         rc = self.lib.vfmm_evaluate_shard(*self._args(shard, config, domain), None, None,
                                           self.ws.ptr, self.ws.nbytes,
-                                          _lib.FLAG_PHASE_UP | _lib.FLAG_OVERLAP, None,
+                                          _lib.FLAG_PHASE_UP | self.up_flags, None,
                                           stream_ptr(self.device))
         _lib.check(rc, "vfmm_evaluate_shard(up)")
         buf = self.ws.buffer
@@ -163,7 +165,7 @@ class CudaShardBackend:
             return vel, 0, 0
         rc = self.lib.vfmm_evaluate_shard(*self._args(shard, config, domain), vel[0].data_ptr(),
                                           vel[1].data_ptr(), self.ws.ptr, self.ws.nbytes,
-                                          _lib.FLAG_PHASE_DOWN | _lib.FLAG_OVERLAP, None,
+                                          _lib.FLAG_PHASE_DOWN | self.down_flags, None,
                                           stream_ptr(self.device))
         _lib.check(rc, "vfmm_evaluate_shard(down)")
         if not counters:

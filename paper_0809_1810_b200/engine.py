@@ -14,6 +14,7 @@ device workspace and maps status codes to the reference's exceptions.
 from __future__ import annotations
 
 import ctypes
+import threading
 import warnings
 from dataclasses import dataclass
 from typing import Sequence
@@ -74,9 +75,14 @@ class FmmRunStats:
 
 
 class Workspace:
-    """Device scratch for one (n, levels, order) shape, reused across calls."""
+    """Device scratch for one (n, levels, order) shape, reused across calls.
+
+    The cache is keyed by host thread as well: a workspace holds the whole
+    state of one evaluate, so two threads evaluating at once never share one
+    (the library serialises their enqueue, include/vfmm.h "Threading")."""
 
     _cache: dict = {}
+    _cache_lock = threading.Lock()
 
     def __init__(self, n: int, levels: int, order: int, device: torch.device):
         self.n, self.levels, self.order, self.device = n, levels, order, device
@@ -90,14 +96,15 @@ class Workspace:
 
     @classmethod
     def get(cls, n: int, levels: int, order: int, device: torch.device) -> "Workspace":
-        key = (device.index, n, levels, order)
-        ws = cls._cache.get(key)
-        if ws is None:
-            if len(cls._cache) >= 2:
-                cls._cache.pop(next(iter(cls._cache)))
-            ws = cls(n, levels, order, device)
-            cls._cache[key] = ws
-        return ws
+        key = (threading.get_ident(), device.index, n, levels, order)
+        with cls._cache_lock:
+            ws = cls._cache.get(key)
+            if ws is None:
+                if len(cls._cache) >= 4:
+                    cls._cache.pop(next(iter(cls._cache)))
+                ws = cls(n, levels, order, device)
+                cls._cache[key] = ws
+            return ws
 
     # ---- typed views of the internal arrays (parity tests / debugging) ----
     def view(self, name: str, dtype: torch.dtype, count: int) -> torch.Tensor:
@@ -274,19 +281,29 @@ def evaluate_host(
 class PendingEvaluation:
     """An :func:`evaluate_host_async` call in flight; :meth:`result` waits for it."""
 
-    def __init__(self, out, stream, keep, ws, config, domain, n, code):
+    def __init__(self, out, stream, keep, ws, config, domain, n, code, bad):
         self.out, self.stream, self._keep, self.ws = out, stream, keep, ws
         self._config, self._domain, self._n, self._code = config, domain, n, code
+        self._bad = bad  # pinned int32: out-of-domain count, copied on the stream
 
     def done(self) -> bool:
         return self.stream.query()
 
     def result(self, with_stats: bool = False):
-        """The (N, 2) host tensor of (u, v) rows once the call has finished;
-        ``with_stats=True`` also returns the counters (vfmm_read_stats, no
-        timings) and raises :class:`OutOfDomainError` like :func:`evaluate_host`."""
+        """The (N, 2) host tensor of (u, v) rows once the call has finished.
+        Raises :class:`OutOfDomainError` like :func:`evaluate_host` when a
+        particle lay outside the domain (quadtree.py:191-198; the count rides
+        along on the stream, no extra synchronisation).  ``with_stats=True``
+        also returns the counters (vfmm_read_stats, no timings)."""
         self.stream.synchronize()
-        self._keep = None
+        keep, self._keep = self._keep, None
+        nbad = int(self._bad[0])
+        if nbad:
+            xs, ys = (k[0].numpy() if isinstance(k[0], torch.Tensor) else k[0] for k in keep[:2])
+            bad = _bad_indices(xs, ys, self._domain)
+            raise OutOfDomainError(
+                f"{nbad} particle(s) outside domain {self._domain}, first indices {bad[:5].tolist()}"
+            )
         if not with_stats:
             return self.out
         lib = _lib.load()
@@ -356,7 +373,12 @@ def evaluate_host_async(x, y, gamma, sigma, config, domain, *, out: torch.Tensor
         code, out.data_ptr(), None, workspace.ptr, workspace.nbytes, flags, None, stream.cuda_stream,
     )
     _lib.check(status, "vfmm_evaluate_host")
-    return PendingEvaluation(out, stream, keep, workspace, config, domain, n, code)
+    bad = getattr(workspace, "_bad_count", None)
+    if bad is None:
+        bad = workspace._bad_count = torch.zeros(1, dtype=torch.int32).pin_memory()
+    _lib.check(lib.vfmm_bad_count_async(n, config.levels, config.order, workspace.ptr, bad.data_ptr(),
+                                        stream.cuda_stream), "vfmm_bad_count_async")
+    return PendingEvaluation(out, stream, keep, workspace, config, domain, n, code, bad)
 
 
 class HostPipeline:
@@ -384,8 +406,8 @@ class HostPipeline:
     def submit(self, x, y, gamma, sigma) -> PendingEvaluation:
         i = self.k % len(self.slots)
         self.k += 1
-        if self.pending[i] is not None:
-            self.pending[i].result()
+        if self.pending[i] is not None:  # the slot's buffers must be free
+            self.pending[i].stream.synchronize()
         ws, stream, out = self.slots[i]
         self.pending[i] = evaluate_host_async(x, y, gamma, sigma, self.config, self.domain, out=out,
                                               workspace=ws, stream=stream, overlap=self.overlap,

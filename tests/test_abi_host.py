@@ -61,6 +61,22 @@ def test_invalid_arguments_rejected_without_touching_the_gpu():
     rc = lib.vfmm_evaluate(None, None, None, None, 10, 0.0, 0.0, 1.0, 3, 4, 0, None, None, None, 0,
                            _lib.FLAG_STATS, ctypes.byref(st), None)
     assert rc == _lib.VFMM_EINVAL
+    # n >= 2^30 (32-bit sorted indices): rejected by the size query AND by the
+    # evaluate entry points before any layout / CUDA work (fake non-null pointers)
+    big = 1 << 30
+    assert lib.vfmm_workspace_size(big, 3, 4, ctypes.byref(sz)) == _lib.VFMM_EINVAL
+    assert lib.vfmm_workspace_size(big - 1, 3, 4, ctypes.byref(sz)) == _lib.VFMM_OK
+    fake = ctypes.c_void_p(256)
+    for fn in (lib.vfmm_evaluate, lib.vfmm_evaluate_host):
+        rc = fn(fake, fake, fake, fake, big, 0.0, 0.0, 1.0, 3, 4, 1, fake, fake, fake, 1 << 40,
+                _lib.FLAG_STATS, ctypes.byref(st), None)
+        assert rc == _lib.VFMM_EINVAL
+    rc = lib.vfmm_evaluate_shard(fake, fake, fake, fake, big, 0.0, 0.0, 1.0, 3, 4, 1, 0, 8, fake, fake,
+                                 fake, 1 << 40, _lib.FLAG_PHASE_UP, ctypes.byref(st), None)
+    assert rc == _lib.VFMM_EINVAL
+    nbad = ctypes.c_int64()
+    assert lib.vfmm_evaluate_at(fake, fake, 4, big, 0.0, 0.0, 1.0, 3, 4, 1, fake, fake, fake,
+                                ctypes.byref(nbad), None) == _lib.VFMM_EINVAL
 
 
 def test_config_validation_matches_reference():

@@ -1,0 +1,173 @@
+"""Full-size parity against the REFERENCE FMM itself (north_star: "within 1e-12
+of the reference FMM at every config").
+
+``tests/golden/golden_large.npz`` was written by ``make_golden_large.py``,
+which runs the reference ``vortexfmm.engine.evaluate`` (engine.py:335-398) on
+the full BASELINE config 2 (N = 2^20, l = 7, p = 17) and config 3 (N = 2^24,
+l = 9, p = 20), and the config-4 error study at N = 2^16 (reference FMM vs
+reference ``velocity_direct``, exact maps, errors.py:46-120) and at N = 2^18 /
+2^20 (reference FMM and reference direct sum at the harness's sampled
+targets, harness.py:235-245).  Bar: max |v_gpu - v_ref| / max|v_ref| <= 1e-12
+(the reference's global normalisation, errors.py:64-73), exact counters,
+per-bin map differences <= 1e-12 * max|v_direct| (absolute: high-p maps are
+round-off noise)."""
+import os
+import warnings
+
+import numpy as np
+import pytest
+
+from _golden import digest
+from oracle import fmm_oracle as O
+from paper_0809_1810_b200 import errors, workloads as W
+from paper_0809_1810_b200.model import Domain
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GL = dict(np.load(os.path.join(HERE, "golden", "golden_large.npz"), allow_pickle=False))
+MAP16 = [str(c) for c in GL["meta/map16_cases"]]
+SAMPLED = [str(c) for c in GL["meta/sampled_cases"]]
+BOX = Domain(-1.0, -1.0, 2.0)
+REL_TOL = 1e-12
+
+
+def _full(idx):
+    pre = f"full/config{idx}/"
+    w = W.by_index(idx)
+    assert digest(w.x, w.y, w.gamma, w.sigma) == str(GL[pre + "digest"]), "input generator drifted"
+    return w, pre
+
+
+def _check_full(vel, m2l, near, pre):
+    """vel: (N, 2) in the input order."""
+    assert (m2l, near) == tuple(int(v) for v in GL[pre + "counts"][:2])
+    vmax = float(GL[pre + "vmax"])
+    err = float(np.abs(vel[GL[pre + "sample"]] - GL[pre + "vel"]).max() / vmax)
+    assert err <= REL_TOL, f"max rel err {err:.3e} at the {GL[pre + 'sample'].size} sampled particles"
+    assert abs(float(np.abs(vel).max()) - vmax) <= REL_TOL * vmax
+    n = vel.shape[0]
+    assert np.all(np.abs(vel.sum(axis=0) - GL[pre + "colsum"]) <= REL_TOL * vmax * n)
+    return err
+
+
+# ------------------------------------------------------------------ CPU: the oracle port
+def test_oracle_port_matches_reference_config2():
+    """The numpy restatement (test infrastructure) against the reference at full config 2."""
+    w, pre = _full(2)
+    vel, st = O.evaluate(w.x, w.y, w.gamma, w.sigma, w.levels, w.order, True, W.DOMAIN)
+    _check_full(vel, st["m2l_count"], st["near_pair_count"], pre)
+
+
+@pytest.mark.parametrize("case", ["4_10", "5_15", "8_10"])
+def test_oracle_port_error_maps_match_reference_n65536(case):
+    """Oracle FMM + the host error pipeline reproduce the reference maps at N = 2^16
+    (the reference direct sum is stored, so no O(N^2) work here)."""
+    lv, p = (int(v) for v in case.split("_"))
+    w = W.config4(256, lv, p)
+    vel, st = O.evaluate(w.x, w.y, w.gamma, w.sigma, lv, p, True, W.DOMAIN)
+    _check_map16(case, vel, st["m2l_count"], st["near_pair_count"], GL["map16/direct"], w)
+
+
+def _check_map16(case, vel, m2l, near, direct, w, check_violations=True):
+    pre = f"map16/{case}/"
+    lv, p = (int(v) for v in case.split("_"))
+    assert (m2l, near) == tuple(int(v) for v in GL[pre + "counts"][:2])
+    ref_direct = GL["map16/direct"]
+    vmax = float(np.hypot(ref_direct[:, 0], ref_direct[:, 1]).max())
+    tol = REL_TOL * vmax
+    assert np.abs(direct - ref_direct).max() <= tol
+    assert np.abs(vel[::97] - GL[pre + "vel_sample"]).max() <= REL_TOL * np.abs(GL[pre + "vel_sample"]).max() * 4
+    pos = np.stack((w.x, w.y), axis=1)
+    bud = errors.bound_budgets(w.x, w.y, w.gamma, lv, p, BOX)
+    rep = errors.compare(vel, direct, pos, bud)
+    s = GL[pre + "scalars"]
+    assert abs(rep.max_abs - s[0]) <= tol and abs(rep.rms_abs - s[2]) <= tol
+    for g in (8, 32):
+        emap = errors.spatial_map(rep, BOX, g)
+        assert np.array_equal(emap.counts, GL[pre + f"map{g}_counts"])
+        for key, got in (("max", emap.max_err), ("mean", emap.mean_err)):
+            ref = GL[pre + f"map{g}_{key}"]
+            assert np.array_equal(np.isnan(got), np.isnan(ref))
+            ok = ~np.isnan(ref)
+            d = np.abs(got[ok] - ref[ok]).max()
+            assert d <= tol, f"{case} g={g} {key}: per-bin diff {d:.3e} > {tol:.3e}"
+    if check_violations:
+        assert len(errors.bound_check(rep)) == int(GL[pre + "violations"])
+
+
+# ------------------------------------------------------------------ GPU: the product path
+@pytest.mark.gpu
+@pytest.mark.parametrize("idx", [2, 3])
+def test_full_config_matches_reference_fmm(idx):
+    import torch
+
+    import paper_0809_1810_b200 as vf
+
+    w, pre = _full(idx)
+    cfg = vf.FmmConfig(w.levels, w.order, vf.KernelKind.GAUSSIAN_BLOB)
+    t = [torch.from_numpy(a).cuda() for a in (w.x, w.y, w.gamma, w.sigma)]
+    for overlap in (False, True):
+        vel, st = vf.evaluate_arrays(*t, cfg, vf.Domain(*W.DOMAIN), overlap=overlap)
+        err = _check_full(vel.cpu().numpy().T, st.m2l_count, st.near_pair_count, pre)
+        assert st.sigma_guard_ok == bool(GL[pre + "counts"][2])
+        print(f"config {idx} overlap={overlap}: max rel err vs reference {err:.2e}")
+    del t, vel
+    torch.cuda.empty_cache()
+
+
+_DIRECT16 = {}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", MAP16)
+def test_gpu_error_maps_match_reference_n65536(case):
+    """GPU FMM + GPU direct sum (K10) + the host error pipeline at N = 2^16 against
+    the reference FMM / reference velocity_direct maps, bin by bin."""
+    import torch
+
+    import paper_0809_1810_b200 as vf
+
+    lv, p = (int(v) for v in case.split("_"))
+    w = W.config4(256, lv, p)
+    t = [torch.from_numpy(a).cuda() for a in (w.x, w.y, w.gamma, w.sigma)]
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")  # the sigma guard is violated by design at l >= 6
+        vel, st = vf.evaluate_arrays(*t, vf.FmmConfig(lv, p, vf.KernelKind.GAUSSIAN_BLOB),
+                                     vf.Domain(*W.DOMAIN))
+    if "d" not in _DIRECT16:  # the particle set depends on m only
+        u, v = vf.velocity_direct_arrays(t[0], t[1], *t, vf.KernelKind.GAUSSIAN_BLOB)
+        _DIRECT16["d"] = torch.stack((u, v), dim=1).cpu().numpy()
+    _check_map16(case, vel.cpu().numpy().T, st.m2l_count, st.near_pair_count, _DIRECT16["d"], w)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", SAMPLED)
+def test_gpu_sampled_error_study_matches_reference(case):
+    """N = 2^18 / 2^20: GPU FMM vs the reference FMM and GPU direct vs the reference
+    direct sum at the harness's sampled targets; then the sampled report."""
+    import torch
+
+    import paper_0809_1810_b200 as vf
+
+    pre = f"samp/{case}/"
+    m, lv, p = (int(v) for v in case.split("_"))
+    w = W.config4(m, lv, p)
+    t = [torch.from_numpy(a).cuda() for a in (w.x, w.y, w.gamma, w.sigma)]
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        vel, st = vf.evaluate_arrays(*t, vf.FmmConfig(lv, p, vf.KernelKind.GAUSSIAN_BLOB), vf.Domain(*W.DOMAIN))
+    assert (st.m2l_count, st.near_pair_count) == tuple(int(v) for v in GL[pre + "counts"][:2])
+    sample = GL[pre + "sample"]
+    got = vel.cpu().numpy().T[sample]
+    err = np.abs(got - GL[pre + "fmm"]).max() / float(GL[pre + "vmax_fmm"])
+    assert err <= REL_TOL, f"{case}: FMM max rel err {err:.3e}"
+    idx = torch.from_numpy(sample).cuda()
+    u, v = vf.velocity_direct_arrays(t[0][idx], t[1][idx], *t, vf.KernelKind.GAUSSIAN_BLOB)
+    direct = torch.stack((u, v), dim=1).cpu().numpy()
+    ref_direct = GL[pre + "direct"]
+    dmax = float(np.hypot(ref_direct[:, 0], ref_direct[:, 1]).max())
+    assert np.abs(direct - ref_direct).max() <= REL_TOL * dmax
+    pos = np.stack((w.x, w.y), axis=1)[sample]
+    rep = errors.compare(got, direct, pos)
+    ref = errors.compare(GL[pre + "fmm"], ref_direct, pos)
+    assert abs(rep.max_abs - ref.max_abs) <= REL_TOL * dmax
+    assert abs(rep.rms_abs - ref.rms_abs) <= REL_TOL * dmax
