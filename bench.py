@@ -19,8 +19,9 @@ overlap its neighbours' compute.  ``e2e.latency_ms`` is one
 synchronous ``evaluate_host`` call.
 
 ``--impl reference`` times the reference algorithm's CPU implementation (the
-numpy oracle port in oracle/, the reference being pure Python) on a bounded
-config-2-shaped sample on the host cores.
+numpy oracle port in oracle/, the reference being pure Python and absent on
+the GPU box) on the SAME workload: one full config-2 evaluate per worker
+process per step, one worker per host core.
 """
 
 from __future__ import annotations
@@ -53,6 +54,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2, choices=[0, 1, 2, 3])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-workers", type=int, default=0, help="reference arm: worker processes (0 = auto)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-depth", type=int, default=3, help="evaluations in flight in the e2e pipeline")
     ap.add_argument("--sharded", action="store_true",
@@ -71,22 +73,43 @@ def workload(idx):
     return W.by_index(idx)
 
 
-def cpu_sample_workload():
-    """Bounded CPU sample with config 2's shape: lattice Lamb-Oseen pair, 64 particles
-    per leaf, p = 17, at 1/16 of the particle count (m = 256, l = 5)."""
-    from paper_0809_1810_b200 import workloads as W
+def host_info():
+    """nproc, CPU model and memory of the host the CPU arms run on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    mem_gb = None
+    try:
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemAvailable"):
+                    mem_gb = int(line.split()[1]) / 2**20
+    except OSError:
+        pass
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:
+        cores = os.cpu_count() or 1
+    return {"nproc": cores, "cpu_model": model, "mem_available_gb": mem_gb,
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS", "unset")}
 
-    x, y, h = W.lattice(256)
-    g = (W.lamb_oseen(x, y, 0.0, 0.0) - W.lamb_oseen(x, y, 0.5, 0.0)) * h * h
-    return W.Workload("config2_shape_m256_l5_p17", x, y, g, np.full(x.size, h / 0.8), 5, 17)
 
-
-def time_oracle(w, repeats=1):
+def time_oracle(w, repeats=1, blas_threads=1):
+    """t_total of the numpy oracle port (the reference algorithm restated,
+    oracle/fmm_oracle.py) on this host; ``blas_threads=None`` leaves the BLAS
+    pool at its default (all cores), as the reference runs when
+    OPENBLAS_NUM_THREADS is unset."""
     from threadpoolctl import threadpool_limits
 
     from oracle import fmm_oracle as O
 
-    with threadpool_limits(limits=1):
+    with threadpool_limits(limits=blas_threads):
         times = []
         for _ in range(repeats):
             _, st = O.evaluate(w.x, w.y, w.gamma, w.sigma, w.levels, w.order, True, (-1.0, -1.0, 2.0))
@@ -97,6 +120,7 @@ def time_oracle(w, repeats=1):
 # ----------------------------------------------------------------- reference arm
 _REF_W = None
 _REF_LIMIT = None
+REF_RSS_GB = {0: 0.3, 1: 0.5, 2: 1.5, 3: 24.0}  # measured peak RSS of one port evaluate (+ margin)
 
 
 def _ref_init():
@@ -116,22 +140,27 @@ def _ref_step(_):
 
 
 def run_reference(args):
-    """The reference algorithm's CPU path (the numpy oracle port; the reference
-    is pure Python) on ALL host cores: one worker process per core, each
-    evaluating its own copy of the bounded config-2-shaped sample; a step is
-    one sample per worker, value = workers x N / step wall time."""
+    """The reference algorithm's CPU path on ALL host cores, on exactly our arm's
+    workload: the reference is pure Python + numpy and cannot travel to the GPU
+    box, so its restatement (the numpy oracle port, oracle/fmm_oracle.py, pinned
+    to the reference at 1e-12 on the full config 2 by tests/test_large_parity.py)
+    runs one worker process per core (one BLAS thread each: the reference is
+    single-threaded apart from zgemm threads, which slow it down).
+    A step is one FULL evaluate of the configuration per worker (N = 1,048,576,
+    l = 7, p = 17 for config 2); value = workers x N / step wall time."""
     import multiprocessing as mp
 
     global _REF_W
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    _REF_W = w = cpu_sample_workload()
-    try:
-        cores = len(os.sched_getaffinity(0))
-    except AttributeError:
-        cores = os.cpu_count() or 1
-    workers = max(1, min(cores, 64))
+    _REF_W = w = workload(args.config)
+    host = host_info()
+    workers = max(1, min(host["nproc"], 64))
+    if host["mem_available_gb"]:
+        workers = max(1, min(workers, int(0.6 * host["mem_available_gb"] / REF_RSS_GB[args.config])))
+    if args.ref_workers:
+        workers = args.ref_workers
     t = []
     with mp.get_context("fork").Pool(workers, initializer=_ref_init) as pool:
         for _ in range(args.warmup):
@@ -142,14 +171,17 @@ def run_reference(args):
             t.append(time.perf_counter() - t0)
     mean = statistics.fmean(t)
     value = workers * w.n / mean
-    sample = (f"{w.name}: N={w.n} per worker per step, {workers} worker processes "
-              f"(config 2 is N=1048576, l=7)")
+    sample = (f"one full {w.name} evaluate (N={w.n}, l={w.levels}, p={w.order}) per worker per step, "
+              f"{workers} worker processes x 1 BLAS thread")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": "config2 shape (bounded CPU sample)", "sample": sample},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": w.name, "n": w.n, "levels": w.levels, "order": w.order, "kernel": "gaussian",
+                   "domain": [-1.0, -1.0, 2.0], "same_config": True},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample,
+                         "host": host},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -354,12 +386,14 @@ def run_ours(args):
     cpu = None
     if not args.no_cpu_baseline:
         tt = time_oracle(w)[0]
+        t_all = time_oracle(w, blas_threads=None)[0]
         cpu = {"value": n / tt, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"one full {w.name} evaluate (N={n}) by the numpy oracle port, 1 BLAS thread"}
+               "sample": f"one full {w.name} evaluate (N={n}) by the numpy oracle port, 1 BLAS thread",
+               "blas_default_value": n / t_all, "host": host_info()}
 
     line = {
         "metric": METRIC, "value": n / (ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "n": n, "levels": w.levels, "order": w.order, "kernel": "gaussian",
                    "domain": [-1.0, -1.0, 2.0], "l2": "flushed between steps (256 MiB write)",
