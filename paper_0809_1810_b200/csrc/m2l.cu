@@ -15,7 +15,13 @@
 // TN complex FMAs.  Per destination, offsets apply in row-major source order
 // (the accumulation order of engine.py:166-185); empty sources are skipped
 // when a whole warp's sources are empty and multiply as exact zeros otherwise.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "vfmm_internal.cuh"
 
@@ -339,6 +345,402 @@ __global__ void __launch_bounds__(kDestPerBlock * kGroups, kGroups == 3 ? VFMM_M
     }
 }
 
+
+// ============================================================================
+// Tiled M2L (P <= kTileMaxP): a CTA owns a tile of 8 x 4 destination PARENTS
+// of one level -- 128 destination cells, one warp per parity class -- and one
+// chunk of TN output coefficients.  Every source its 128 destinations need
+// lies in the children of the tile's parents grown by one parent on each side
+// (dx in [-2-px, 3-px] -> source parent jx-1 .. jx+1), i.e. a window of
+// 10 x 6 parents = 4 planes x 6 rows x 10 cells, which is ONE box of the
+// planar layout [P][4 planes][half][half]: a single TMA (cp.async.bulk.tensor,
+// 4-D, out-of-grid cells zero-filled by the copy engine) stages all P
+// coefficients of the window in shared memory, and every source coefficient
+// is then read from shared memory by all the destinations that use it (27
+// per cell) instead of from L2 once per (destination, offset, chunk).
+// L2 -> SM traffic per CTA: 240 cells x P x 16 B for 128 destinations (1.9x
+// the destination data) plus the Hankel rows of the chunk.  Small levels
+// (half < 10 parents per side) fill the window with bounds-checked loads.
+// The arithmetic per destination is the 15-unit symmetric-offset schedule of
+// k_m2l (same units, same order), with the Hankel values of two consecutive
+// n held in registers (TN + 1 loads per two n instead of 2 TN).
+constexpr int kTPX = 8, kTPY = 4;                 // destination parents per tile
+constexpr int kWX = kTPX + 2, kWY = kTPY + 2;     // window parents (one-parent halo)
+constexpr int kWinCells = 4 * kWY * kWX;          // window cells per coefficient (240)
+constexpr int kTileMaxP = 26;                     // window <= 100 KB of shared memory
+
+struct M2LMaps {
+    CUtensorMap map[VFMM_LEVELS_CAP + 1];  // per level (levels with half >= kWX)
+};
+
+// (dx, dy) of offset o of parity class par, engine._il_offsets order
+struct OffTab {
+    int8_t dx[4][27], dy[4][27];
+};
+constexpr OffTab make_offtab() {
+    OffTab t{};
+    for (int par = 0; par < 4; ++par) {
+        const int px = par & 1, py = par >> 1;
+        int idx = 0;
+        for (int yy = -2 - py; yy < 4 - py; ++yy)
+            for (int xx = -2 - px; xx < 4 - px; ++xx) {
+                const int ax = xx < 0 ? -xx : xx, ay = yy < 0 ? -yy : yy;
+                if ((ax > ay ? ax : ay) >= 2) {
+                    t.dx[par][idx] = (int8_t)xx;
+                    t.dy[par][idx] = (int8_t)yy;
+                    ++idx;
+                }
+            }
+    }
+    return t;
+}
+__constant__ OffTab c_off = make_offtab();
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+
+// Accumulators: the real and imaginary parts of every output are split in
+// two partial sums (acc[0][t] += hr xr, acc[1][t] -= hi xi; acc[2][t] += hr xi,
+// acc[3][t] += hi xr), so the four FMAs of a complex product are independent
+// and one coefficient step has no dependent DFMA pair (ncu: "wait" was the top
+// stall of the nested form); the halves are added once at the end.
+template <int TN>
+struct TileAcc {
+    double a[4][TN];
+};
+
+// one complex product h * X (X = (xr, xi)) into output t
+template <int TN>
+__device__ __forceinline__ void cmac(TileAcc<TN>& A, int t, double2 h, double xr, double xi) {
+    A.a[0][t] = fma(h.x, xr, A.a[0][t]);
+    A.a[1][t] = fma(-h.y, xi, A.a[1][t]);
+    A.a[2][t] = fma(h.x, xi, A.a[2][t]);
+    A.a[3][t] = fma(h.y, xr, A.a[3][t]);
+}
+// Re h * X + i Im h * Y into output t
+template <int TN>
+__device__ __forceinline__ void rmac(TileAcc<TN>& A, int t, double2 h, double Xr, double Xi, double Yr,
+                                     double Yi) {
+    A.a[0][t] = fma(h.x, Xr, A.a[0][t]);
+    A.a[1][t] = fma(-h.y, Yi, A.a[1][t]);
+    A.a[2][t] = fma(h.x, Xi, A.a[2][t]);
+    A.a[3][t] = fma(h.y, Yr, A.a[3][t]);
+}
+
+template <int TN, int KIND, int MP>
+__device__ __forceinline__ void tile_pair_step(double2 a1, double2 a2, const double2* hv, int np,
+                                               TileAcc<TN>& A) {
+    const double sr = a1.x + a2.x, si = a1.y + a2.y;
+    const double dr = a1.x - a2.x, di = a1.y - a2.y;
+#pragma unroll
+    for (int t = 0; t < TN; ++t) {
+        const bool odd = ((MP + t + np) & 1) != 0;  // parity of m + n
+        if (KIND == 1) {  // h * X, X = D (m+n even) / S (odd)
+            cmac(A, t, hv[t], odd ? sr : dr, odd ? si : di);
+        } else {  // Re h * X + i Im h * Y; X = S for kind 2, or kind 3 at odd m+n
+            const bool xs = KIND == 2 || odd;
+            rmac(A, t, hv[t], xs ? sr : dr, xs ? si : di, xs ? dr : sr, xs ? di : si);
+        }
+    }
+}
+
+template <int TN>
+__device__ __forceinline__ void tile_plain(const double2* __restrict__ s1, const double2* __restrict__ h,
+                                           int P, TileAcc<TN>& A) {
+    int n = 0;
+#pragma unroll 1
+    for (; n + 1 < P; n += 2) {
+        double2 hv[TN + 1];
+#pragma unroll
+        for (int t = 0; t <= TN; ++t) hv[t] = h[n + t];
+        const double2 a = s1[n * kWinCells], b = s1[(n + 1) * kWinCells];
+#pragma unroll
+        for (int t = 0; t < TN; ++t) cmac(A, t, hv[t], a.x, a.y);
+#pragma unroll
+        for (int t = 0; t < TN; ++t) cmac(A, t, hv[t + 1], b.x, b.y);
+    }
+    if (n < P) {
+        const double2 a = s1[n * kWinCells];
+#pragma unroll
+        for (int t = 0; t < TN; ++t) cmac(A, t, h[n + t], a.x, a.y);
+    }
+}
+
+template <int TN, int KIND, int MP>
+__device__ __forceinline__ void tile_pair(const double2* __restrict__ s1, const double2* __restrict__ s2,
+                                          const double2* __restrict__ h, int P, TileAcc<TN>& A) {
+    int n = 0;
+#pragma unroll 1
+    for (; n + 1 < P; n += 2) {
+        double2 hv[TN + 1];
+#pragma unroll
+        for (int t = 0; t <= TN; ++t) hv[t] = h[n + t];
+        const double2 a1 = s1[n * kWinCells], a2 = s2[n * kWinCells];
+        const double2 b1 = s1[(n + 1) * kWinCells], b2 = s2[(n + 1) * kWinCells];
+        tile_pair_step<TN, KIND, MP>(a1, a2, hv, 0, A);
+        tile_pair_step<TN, KIND, MP>(b1, b2, hv + 1, 1, A);
+    }
+    if (n < P) {  // n even
+        double2 hv[TN];
+#pragma unroll
+        for (int t = 0; t < TN; ++t) hv[t] = h[n + t];
+        tile_pair_step<TN, KIND, MP>(s1[n * kWinCells], s2[n * kWinCells], hv, 0, A);
+    }
+}
+
+template <int TN, int CW>
+__global__ void __launch_bounds__(128 * CW, CW == 1 ? 2 : 1)
+    k_m2l_tile(const __grid_constant__ M2LMaps maps, const double2* __restrict__ mult,
+               const int* __restrict__ counts, double2* __restrict__ loc, double2* __restrict__ anc,
+               int anc_end, int levels, int P, int nchunks, const Tables* __restrict__ T,
+               unsigned long long* __restrict__ m2l_count, Rows rows) {
+    pdl_enter();
+    extern __shared__ __align__(1024) unsigned char m2l_smem[];
+    double2* win = reinterpret_cast<double2*>(m2l_smem);  // [P][4][kWY][kWX]
+    double2* sH = win + (size_t)P * kWinCells;            // [49][HL]
+    __shared__ int scnt[kWinCells];                       // occupancy of the window cells
+    __shared__ __align__(8) unsigned long long bar;
+    // ---- decode (level, tile, chunk) ----
+    int64_t b = blockIdx.x;
+    int level = 2;
+    size_t cell_off = 0, cnt_off = 5;
+    int half = 2, tiles_x = 1;
+    for (;;) {
+        half = 1 << (level - 1);
+        tiles_x = (half + kTPX - 1) / kTPX;
+        const int tiles_y = (half + kTPY - 1) / kTPY;
+        const int64_t nb = (int64_t)tiles_x * tiles_y * ((nchunks + CW - 1) / CW);
+        if (b < nb || level == levels) break;
+        b -= nb;
+        cell_off += (size_t)1 << (2 * level);
+        cnt_off += (size_t)1 << (2 * level);
+        ++level;
+    }
+    const int ngroups = (nchunks + CW - 1) / CW;  // chunk groups of CW chunks (one per warp quad)
+    const int chunk = (int)(b % ngroups) * CW + (int)(threadIdx.x >> 7);
+    const int64_t tile = b / ngroups;
+    const int jx0 = (int)(tile % tiles_x) * kTPX, jy0 = (int)(tile / tiles_x) * kTPY;
+    const int parity = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
+    const int px = parity & 1, py = parity >> 1;
+    const int jx = jx0 + (lane & 7), jy = jy0 + (lane >> 3);
+    const int ix = 2 * jx + px, iy = 2 * jy + py;
+    const int shift = levels - level;
+    const bool active = chunk < nchunks && jx < half && jy < half && rows_touch(rows, iy, shift);
+    if (!__syncthreads_or(active)) return;  // sharded runs: tile outside the strip
+
+    const int mk = 1 << level;
+    const int64_t psz = (int64_t)half * half, cstride = 4 * psz;
+    const double2* M = mult + cell_off * P;
+    const bool tma = half >= kWX;
+    if (tma && threadIdx.x == 0) {
+        const unsigned ba = smem_u32(&bar);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ba));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const unsigned bytes = (unsigned)(P * kWinCells * sizeof(double2));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ba), "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(win)),
+            "l"(reinterpret_cast<unsigned long long>(&maps.map[level])), "r"(2 * (jx0 - 1)),
+            "r"(jy0 - 1), "r"(0), "r"(0), "r"(ba)
+            : "memory");
+    }
+    if (!tma) {  // small levels: bounds-checked cooperative fill
+        for (int i = threadIdx.x; i < P * kWinCells; i += blockDim.x) {
+            const int n = i / kWinCells, r = i % kWinCells;
+            const int plane = r / (kWX * kWY), rr = r % (kWX * kWY);
+            const int gy = jy0 - 1 + rr / kWX, gx = jx0 - 1 + rr % kWX;
+            win[i] = (gx >= 0 && gx < half && gy >= 0 && gy < half)
+                         ? M[n * cstride + plane * psz + (int64_t)gy * half + gx]
+                         : make_double2(0.0, 0.0);
+        }
+    }
+    // occupancy of the window cells (the reference skips empty sources and
+    // counts the (destination, nonempty source) pairs, engine.py:173-180)
+    for (int r = threadIdx.x; r < kWinCells; r += blockDim.x) {
+        const int plane = r / (kWX * kWY), rr = r % (kWX * kWY);
+        const int sx = 2 * (jx0 - 1 + rr % kWX) + (plane & 1);
+        const int sy = 2 * (jy0 - 1 + rr / kWX) + (plane >> 1);
+        scnt[r] = (sx >= 0 && sx < mk && sy >= 0 && sy < mk) ? counts[cnt_off + (int64_t)sy * mk + sx] : 0;
+    }
+    // Hankel rows of this chunk group for the 7 x 7 offset grid: entries
+    // mg .. mg + CW TN + P - 1 (one pad for the two-coefficient loop)
+    const int mg = (chunk / CW) * CW * TN, m0 = chunk * TN;
+    const int HL = CW * TN + P;
+    for (int i = threadIdx.x; i < kOffsets * HL; i += blockDim.x) {
+        const int o = i / HL, q = i % HL;
+        sH[i] = T->H[o][mg + q];
+    }
+    __syncthreads();
+    if (tma) {
+        const unsigned ba = smem_u32(&bar);
+        asm volatile(
+            "{\n .reg .pred p;\n WAIT_%=:\n"
+            " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+            " @!p bra WAIT_%=;\n}" ::"r"(ba)
+            : "memory");
+    }
+
+    // destination's own parent sits at window (lane & 7) + 1, (lane >> 3) + 1
+    const int counts_here = active && (iy << shift) >= rows.lo;
+    TileAcc<TN> A;
+#pragma unroll
+    for (int t = 0; t < TN; ++t) A.a[0][t] = A.a[1][t] = A.a[2][t] = A.a[3][t] = 0.0;
+    int ntrans = 0;
+    const bool mo = (m0 & 1) != 0;
+    auto src_of = [&](int o, bool& live) {
+        const int sx = ix + c_off.dx[parity][o], sy = iy + c_off.dy[parity][o];
+        const int r = (((sy & 1) << 1) | (sx & 1)) * (kWX * kWY) + ((sy >> 1) - jy0 + 1) * kWX +
+                      ((sx >> 1) - jx0 + 1);
+        live = active && scnt[r] > 0;
+        return r;
+    };
+#pragma unroll 1
+    for (int u = 0; u < kUnits; ++u) {
+        const int o1 = c_units.o1[parity][u], o2 = c_units.o2[parity][u];
+        const int kind = c_units.kind[parity][u];
+        bool live1, live2 = false;
+        const int r1 = src_of(o1, live1);
+        const int r2 = o2 >= 0 ? src_of(o2, live2) : r1;
+        ntrans += (counts_here && live1 ? 1 : 0) + (counts_here && live2 ? 1 : 0);
+        if (!__any_sync(0xffffffffu, live1 || live2)) continue;
+        // empty sources hold zero multipoles: they multiply as exact zeros
+        const double2* h =
+            sH + ((c_off.dy[parity][o1] + 3) * 7 + (c_off.dx[parity][o1] + 3)) * HL + (m0 - mg);
+        const double2* s1 = win + r1;
+        if (o2 < 0) {
+            tile_plain<TN>(s1, h, P, A);
+            continue;
+        }
+        const double2* s2 = win + r2;
+        if (kind == 1) {
+            if (mo) tile_pair<TN, 1, 1>(s1, s2, h, P, A);
+            else tile_pair<TN, 1, 0>(s1, s2, h, P, A);
+        } else if (kind == 2) {
+            tile_pair<TN, 2, 0>(s1, s2, h, P, A);
+        } else {
+            if (mo) tile_pair<TN, 3, 1>(s1, s2, h, P, A);
+            else tile_pair<TN, 3, 0>(s1, s2, h, P, A);
+        }
+    }
+    if (active) {
+        double2* out = loc + cell_off * P + parity * psz + (int64_t)jy * half + jx;
+#pragma unroll
+        for (int t = 0; t < TN; ++t) {
+            if (m0 + t < P) {
+                const double2 r = make_double2(A.a[0][t] + A.a[1][t], A.a[2][t] + A.a[3][t]);
+                out[(m0 + t) * cstride] = r;
+                if (level < anc_end) anc[(out - loc) + (m0 + t) * cstride] = r;
+            }
+        }
+    }
+    if (chunk == 0) {  // warp-uniform
+        for (int sft = 16; sft > 0; sft >>= 1) ntrans += __shfl_xor_sync(0xffffffffu, ntrans, sft);
+        if (lane == 0 && ntrans) atomicAdd(m2l_count, (unsigned long long)ntrans);
+    }
+}
+
+// Tensor maps of the multipole levels (driver entry point; no -lcuda), cached
+// per (multipole base, levels, P): encoding is host work, reused by every call
+// on the same workspace.
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+
+bool m2l_maps(const Layout& L, const double2* mult, M2LMaps* out) {
+    struct Entry {
+        const double2* mult;
+        int levels, P;
+        M2LMaps maps;
+    };
+    static std::mutex mu;
+    static std::vector<Entry> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto& e : cache)
+        if (e.mult == mult && e.levels == L.levels && e.P == L.P) {
+            *out = e.maps;
+            return true;
+        }
+    auto enc = encode_fn();
+    if (!enc) return false;
+    Entry e{mult, L.levels, L.P, {}};
+    std::memset(&e.maps, 0, sizeof(e.maps));
+    for (int k = 2; k <= L.levels; ++k) {
+        const uint64_t half = 1ull << (k - 1);
+        if (half < (uint64_t)kWX) continue;
+        const cuuint64_t dims[4] = {2 * half, half, 4, (cuuint64_t)L.P};
+        const cuuint64_t strides[3] = {half * 16, half * half * 16, 4 * half * half * 16};
+        const cuuint32_t box[4] = {2 * kWX, kWY, 4, (cuuint32_t)L.P};
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        void* base = (void*)(mult + L.level_cell_off[k] * L.P);
+        if (enc(&e.maps.map[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    if (cache.size() >= 64) cache.erase(cache.begin());
+    cache.push_back(e);
+    *out = e.maps;
+    return true;
+}
+
+template <int TN, int CW>
+void launch_tile_cw(const Layout& L, const M2LMaps& maps, const Tables* T, const double2* mult,
+                    const int* counts, double2* loc, double2* anc, Counters* ctr, Rows rows,
+                    int64_t tiles, int nchunks, cudaStream_t s) {
+    const int64_t blocks = tiles * ((nchunks + CW - 1) / CW);
+    const size_t smem = (size_t)L.P * kWinCells * sizeof(double2) +
+                        (size_t)kOffsets * (CW * TN + L.P) * sizeof(double2);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_m2l_tile<TN, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_set = true;
+    }
+    launch_k(k_m2l_tile<TN, CW>, (unsigned)blocks, 128 * CW, smem, s, maps, mult, counts, loc, anc,
+             l2l_split_level(L.levels, L.P), L.levels, L.P, nchunks, T, &ctr->m2l_count, rows);
+    note_launches(1);
+}
+
+// Tile kernel when the grid fills the GPU (>= 2 CTAs per SM); the direct-load
+// kernel (k_m2l, many small CTAs) below that.  All chunks of a tile share one
+// CTA (CW = nchunks <= 3, one window per 4 CW warps) once the grid is >= 8
+// waves of single-chunk CTAs, one chunk per CTA otherwise (balance: config 2
+// has 516 single-chunk CTAs).  VFMM_M2L_CW=1|3 overrides (tuning).
+template <int TN>
+bool launch_tile_tn(const Layout& L, const Tables* T, const double2* mult, const int* counts,
+                    double2* loc, double2* anc, Counters* ctr, Rows rows, cudaStream_t s) {
+    const int nchunks = (L.P + TN - 1) / TN;
+    int64_t tiles = 0;
+    for (int level = 2; level <= L.levels; ++level) {
+        const int half = 1 << (level - 1);
+        tiles += (int64_t)((half + kTPX - 1) / kTPX) * ((half + kTPY - 1) / kTPY);
+    }
+    if (tiles * nchunks < 2 * 148) return false;
+    M2LMaps maps;
+    if (!m2l_maps(L, mult, &maps)) return false;
+    static const int cw_env = getenv("VFMM_M2L_CW") ? atoi(getenv("VFMM_M2L_CW")) : 0;
+    int cw = (tiles * nchunks >= 8 * 2 * 148 && nchunks <= 3) ? nchunks : 1;
+    if (cw_env >= 1 && cw_env <= 3) cw = cw_env;
+    if (cw == 1)
+        launch_tile_cw<TN, 1>(L, maps, T, mult, counts, loc, anc, ctr, rows, tiles, nchunks, s);
+    else if (cw == 2)
+        launch_tile_cw<TN, 2>(L, maps, T, mult, counts, loc, anc, ctr, rows, tiles, nchunks, s);
+    else
+        launch_tile_cw<TN, 3>(L, maps, T, mult, counts, loc, anc, ctr, rows, tiles, nchunks, s);
+    return true;
+}
+
 template <int TN>
 void launch_tn(const Layout& L, const Tables* T, const double2* mult, const int* counts,
                double2* loc, double2* anc, Counters* ctr, Rows rows, cudaStream_t s) {
@@ -372,6 +774,20 @@ void launch_tn(const Layout& L, const Tables* T, const double2* mult, const int*
 
 void launch_m2l(const Layout& L, const Tables* T, const double2* mult, const int* counts,
                 double2* loc, double2* anc, Counters* ctr, Rows rows, cudaStream_t s) {
+    // the shared-memory window kernel (TMA) for P <= 26; VFMM_M2L_TILE=0 keeps
+    // the direct-load kernel (A/B measurement)
+    static const bool tile_on = !(getenv("VFMM_M2L_TILE") && getenv("VFMM_M2L_TILE")[0] == '0');
+    if (tile_on && L.P <= kTileMaxP) {
+        bool ok = false;
+        switch (coef_chunk(L.P)) {
+            case 4: ok = launch_tile_tn<4>(L, T, mult, counts, loc, anc, ctr, rows, s); break;
+            case 5: ok = launch_tile_tn<5>(L, T, mult, counts, loc, anc, ctr, rows, s); break;
+            case 6: ok = launch_tile_tn<6>(L, T, mult, counts, loc, anc, ctr, rows, s); break;
+            case 7: ok = launch_tile_tn<7>(L, T, mult, counts, loc, anc, ctr, rows, s); break;
+            default: ok = launch_tile_tn<8>(L, T, mult, counts, loc, anc, ctr, rows, s); break;
+        }
+        if (ok) return;
+    }
     switch (coef_chunk(L.P)) {
         case 4: launch_tn<4>(L, T, mult, counts, loc, anc, ctr, rows, s); break;
         case 5: launch_tn<5>(L, T, mult, counts, loc, anc, ctr, rows, s); break;

@@ -1,6 +1,8 @@
-"""M2L variant probe: median t_m2l (stats mode, serialised phases) of the
-factored kernel vs the Hankel-row kernel (VFMM_M2L_HANKEL=1) on one BASELINE
-config, and the max relative velocity difference between the two."""
+"""M2L probe: median t_m2l (stats mode, serialised phases) on one BASELINE config,
+its algorithmic TFLOP/s (8 (p+1)^2 flop per translation) and a
+checksum of the velocities.  Run once per variant (the library reads its A/B
+switches once per process), e.g. VFMM_M2L_TILE=0 for the direct-load kernel.
+Usage: m2l_probe.py [config] [reps]"""
 import os
 import statistics
 import sys
@@ -18,24 +20,13 @@ w = W.by_index(cfg_idx)
 dev = torch.device("cuda", 0)
 xd, yd, gd, sd = (torch.from_numpy(a).to(dev) for a in (w.x, w.y, w.gamma, w.sigma))
 cfg = vf.FmmConfig(w.levels, w.order, vf.KernelKind.GAUSSIAN_BLOB)
-
-
-def run(hankel):
-    if hankel:
-        os.environ["VFMM_M2L_HANKEL"] = "1"
-    else:
-        os.environ.pop("VFMM_M2L_HANKEL", None)
-    ts = []
-    for _ in range(reps):
-        vel, st = vf.evaluate_arrays(xd, yd, gd, sd, cfg, vf.Domain(*W.DOMAIN), timings=True)
-        ts.append(st.t_m2l * 1e3)
-    torch.cuda.synchronize()
-    return vel.cpu().numpy(), statistics.median(ts[2:]), st
-
-
-vh, th, sh = run(True)
-vfac, tf, sf = run(False)
-err = float(np.abs(vfac - vh).max() / np.abs(vh).max())
-flop = 8 * (w.order + 1) ** 2 * sf.m2l_count
-print(f"{os.environ.get('VFMM_LIB', 'default')} {w.name}: m2l hankel {th:.4f} ms, factored {tf:.4f} ms "
-      f"({flop / tf / 1e9:.2f} TF/s algorithmic), max rel diff {err:.2e}, counts {sh.m2l_count} {sf.m2l_count}")
+ts = []
+for _ in range(reps):
+    vel, st = vf.evaluate_arrays(xd, yd, gd, sd, cfg, vf.Domain(*W.DOMAIN), timings=True)
+    ts.append(st.t_m2l * 1e3)
+t = statistics.median(ts[2:])
+flop = 8 * (w.order + 1) ** 2 * st.m2l_count
+v = vel.cpu().numpy()
+tag = "tile" if os.environ.get("VFMM_M2L_TILE", "1") != "0" else "direct"
+print(f"{tag} {w.name}: m2l {t:.4f} ms ({flop / t / 1e9:.2f} TF/s algorithmic), m2l_count {st.m2l_count}, "
+      f"checksum {np.abs(v).sum():.15e}")
