@@ -150,13 +150,15 @@ int vfmm_evaluate_host(const double* x, const double* y, const double* gamma, co
 /* Sharded evaluate (one process per GPU; leaves sharded in row strips).
  * The local arrays hold this rank's owned particles (leaf rows [row_lo,
  * row_hi) of the 2^levels x 2^levels leaf grid) plus halo copies of the
- * particles in leaf rows row_lo-1 and row_hi.  Two phases:
- *   PHASE_UP   : tree over the local particles; P2M over owned leaves only;
- *                M2M over the whole pyramid -> partial multipoles.
- *   (caller)   : sum-all-reduce the multipole region (vfmm_mult_region) and the
- *                int32 occupancy region (vfmm_counts_region) across ranks --
- *                multipoles are linear in gamma and each rank counts only its
- *                owned rows, so the sums are the global pyramids.
+ * particles in leaf rows row_lo-1 and row_hi (the P2P of the boundary leaves,
+ * engine.py:216-235).  Per evaluate:
+ *   PHASE_UP   : tree over the local particles; strip-local upward pass: P2M
+ *                of the owned leaves, M2M of the subtrees touching the strip
+ *                (a coarse cell straddling strips gets this rank's PARTIAL
+ *                multipole); with VFMM_FLAG_OVERLAP the near field starts.
+ *   (caller)   : vfmm_shard_pack -> NCCL allgather of the coarse buffers and
+ *                grouped send/recv of the halo buffers with the neighbour
+ *                strips -> vfmm_shard_unpack (see below).
  *   PHASE_DOWN : M2L / L2L for cells touching the owned strip, P2P for owned
  *                leaves, L2P + combine for owned particles (u, v of halo
  *                particles are left untouched).
@@ -167,6 +169,29 @@ int vfmm_evaluate_shard(const double* x, const double* y, const double* gamma, c
                         int64_t n, double xmin, double ymin, double side, int levels, int order,
                         int kernel, int row_lo, int row_hi, double* u, double* v, void* workspace,
                         size_t workspace_bytes, unsigned flags, vfmm_stats* stats, void* stream);
+
+/* Multipole exchange of the sharded evaluate.  The M2L of a cell reaches two
+ * cell rows up and down (engine.py:77-89), so with every strip starting and
+ * ending on an even cell row of level k and >= 2 rows tall ("fine" levels
+ * kc+1 .. levels) a rank needs one plane row of each parity plane from each
+ * neighbour strip; the small "coarse" levels 2 .. kc (kc <= 1: none) are
+ * all-gathered (each rank's partials of the cells touching its strip, zero
+ * elsewhere) and summed in rank order.  The occupancy pyramid travels along.
+ * Buffer sizes depend on (levels, order, kc) only, so they are equal on every
+ * rank; VFMM_EINVAL when a level above kc is not fine for this strip.        */
+int vfmm_shard_exchange_size(int64_t n, int levels, int order, int row_lo, int row_hi, int kc,
+                             size_t* coarse_bytes, size_t* halo_bytes);
+/* After PHASE_UP, on `stream`: this rank's coarse contribution, its first
+ * owned plane rows (halo_down, for the strip below) and its last ones
+ * (halo_up, for the strip above).  NULL halo pointers are skipped.          */
+int vfmm_shard_pack(int64_t n, int levels, int order, int row_lo, int row_hi, int kc,
+                    const void* workspace, void* coarse, void* halo_down, void* halo_up, void* stream);
+/* Before PHASE_DOWN, on `stream`: coarse levels = the sum of the `world`
+ * contributions in coarse_all (rank order, coarse_bytes apart); the halo rows
+ * received from the strip below / above (NULL: none, e.g. the edge strips). */
+int vfmm_shard_unpack(int64_t n, int levels, int order, int row_lo, int row_hi, int kc, void* workspace,
+                      const void* coarse_all, int world, const void* halo_below, const void* halo_above,
+                      void* stream);
 
 /* Byte ranges of the multipole pyramid (complex128, all levels) and of the
  * occupancy pyramid (int32, levels 0..l) inside the workspace. */

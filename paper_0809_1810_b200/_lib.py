@@ -44,6 +44,9 @@ EXPORTED_SYMBOLS = (
     "vfmm_evaluate",
     "vfmm_evaluate_host",
     "vfmm_evaluate_shard",
+    "vfmm_shard_exchange_size",
+    "vfmm_shard_pack",
+    "vfmm_shard_unpack",
     "vfmm_mult_region",
     "vfmm_counts_region",
     "vfmm_read_stats",
@@ -124,6 +127,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.vfmm_evaluate_host.argtypes = lib.vfmm_evaluate.argtypes
         lib.vfmm_evaluate_shard.argtypes = [_P, _P, _P, _P, _I64, _D, _D, _D, _I, _I, _I, _I, _I, _P,
                                             _P, _P, _SZ, ctypes.c_uint, ctypes.POINTER(VfmmStats), _P]
+        lib.vfmm_shard_exchange_size.argtypes = [_I64, _I, _I, _I, _I, _I, ctypes.POINTER(_SZ),
+                                                 ctypes.POINTER(_SZ)]
+        lib.vfmm_shard_pack.argtypes = [_I64, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P]
+        lib.vfmm_shard_unpack.argtypes = [_I64, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P]
         lib.vfmm_mult_region.argtypes = [_I64, _I, _I, ctypes.POINTER(_SZ), ctypes.POINTER(_SZ)]
         lib.vfmm_counts_region.argtypes = [_I64, _I, _I, ctypes.POINTER(_SZ), ctypes.POINTER(_SZ)]
         lib.vfmm_read_stats.argtypes = [_I64, _I, _I, _I, _D, _P, ctypes.POINTER(VfmmStats), _P]

@@ -28,24 +28,11 @@ __global__ void __launch_bounds__(kSubThreads)
                   const Tables* __restrict__ T, int levels, Rows rows) {
     pdl_enter();
     {
-        // sharded runs: a subtree outside the owned row strip has no local
-        // sources (P2M wrote zeros there) -- write its zero multipoles directly
+        // sharded runs are strip-local: a subtree outside the owned row strip
+        // is not visited (its cells are neither read nor written here; the
+        // multipole exchange supplies what the strip's M2L needs)
         const int lt0 = lf - depth, mt0 = 1 << lt0;
-        const int cx0 = blockIdx.x % mt0, cy0 = blockIdx.x / mt0;
-        if (!rows_touch(rows, cy0, levels - lt0)) {
-            size_t off = off_lf;
-            for (int s = depth - 1; s >= 0; --s) {
-                const int lvl = lt0 + s, side = 1 << s;
-                off -= (size_t)(1ll << (2 * lvl)) * P;
-                const int64_t cs = coef_stride(lvl);
-                for (int i = threadIdx.x; i < side * side * P; i += blockDim.x) {
-                    const int c = i / P, mm = i % P;
-                    mult[off + coef_base(lvl, cx0 * side + c % side, cy0 * side + c / side) +
-                         mm * cs] = make_double2(0.0, 0.0);
-                }
-            }
-            return;
-        }
+        if (!rows_touch(rows, (int)(blockIdx.x / mt0), levels - lt0)) return;
     }
     extern __shared__ double2 sm[];  // [sub_off(depth+1)][P] cells + tables
     double2* sE = sm + (size_t)sub_off(depth + 1) * P;  // [4][P]
@@ -70,7 +57,13 @@ __global__ void __launch_bounds__(kSubThreads)
             const int k = i / ncell, r = i % ncell;
             const int plane = r / (hs * hs), hy = (r / hs) % hs, hx = r % hs;
             const int lx = 2 * hx + (plane & 1), ly = 2 * hy + (plane >> 1);
-            dst[(ly * side + lx) * P + k] = src[coef_base(lf, cx * side + lx, cy * side + ly) + k * cs];
+            // cells whose leaf rows lie outside the strip contribute nothing
+            // (sharded partial sums: a coarse parent collects only this rank's
+            // children; the exchange adds the other ranks' partials)
+            const int gy = cy * side + ly;
+            dst[(ly * side + lx) * P + k] = rows_touch(rows, gy, levels - lf)
+                                                ? src[coef_base(lf, cx * side + lx, gy) + k * cs]
+                                                : make_double2(0.0, 0.0);
         }
     }
     __syncthreads();

@@ -25,15 +25,15 @@ __global__ void __launch_bounds__(kP2MWarps * 32)
     __shared__ double2 buf[kP2MWarps][32][33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m = 1 << levels;
-    const int64_t leaf = (int64_t)blockIdx.x * kP2MWarps + warp;
-    if (leaf >= (int64_t)m * m) return;
+    // the grid covers the leaves of the owned row strip only (all leaves on one GPU)
+    const int64_t leaf = (int64_t)rows.lo * m + (int64_t)blockIdx.x * kP2MWarps + warp;
+    if (leaf >= (int64_t)rows.hi * m) return;
     const int lo = ls[leaf], hi = ls[leaf + 1];
     const int ix = (int)(leaf % m), iy = (int)(leaf / m);
     double2* out = mult + coef_base(levels, ix, iy);
     const int64_t cs = coef_stride(levels);
-    // empty leaves, and leaves outside the owned row strip (sharded run: their
-    // particles are halo copies owned by a neighbour rank), carry zero
-    if (lo == hi || iy < rows.lo || iy >= rows.hi) {
+    // empty leaves carry zero
+    if (lo == hi) {
         for (int k = lane; k < P; k += 32) out[k * cs] = make_double2(0.0, 0.0);
         return;
     }
@@ -98,14 +98,15 @@ __global__ void __launch_bounds__(128)
     pdl_enter();
     const int sub = threadIdx.x & (G - 1);
     const int m = 1 << levels;
-    const int64_t leaf = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
-    const bool valid = leaf < (int64_t)m * m;  // whole groups are (in)valid together
+    // the grid covers the leaves of the owned row strip only (all leaves on one GPU)
+    const int64_t leaf = (int64_t)rows.lo * m + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const bool valid = leaf < (int64_t)rows.hi * m;  // whole groups are (in)valid together
     if (!valid) return;
     const int lo = ls[leaf], hi = ls[leaf + 1];
     const int ix = (int)(leaf % m), iy = (int)(leaf / m);
     double2* out = mult + coef_base(levels, ix, iy);
     const int64_t cs = coef_stride(levels);
-    const bool live = lo < hi && iy >= rows.lo && iy < rows.hi;  // uniform per group
+    const bool live = lo < hi;  // uniform per group
     double ax[PMAX], ay[PMAX];
 #pragma unroll
     for (int k = 0; k < PMAX; ++k) ax[k] = ay[k] = 0.0;
@@ -159,10 +160,13 @@ int coef_chunk(int P) {
 
 void launch_p2m(const Layout& L, const Src* src, const int* leaf_starts, double xmin, double ymin,
                 double side, double2* mult_leaf, const Tables* T, Rows rows, cudaStream_t s) {
-    const int64_t nl = (int64_t)L.nleaves;
+    // strip-local: only the leaves of the owned rows are visited (sharded runs
+    // leave the other leaves' multipoles alone; the exchange fills the halo)
+    const int64_t nl = (int64_t)(rows.hi - rows.lo) << L.levels;
+    if (nl <= 0) return;
     // sub-warp groups while leaves are small enough for 8 lanes to sweep them
     // (mean occupancy <= 256); the warp-per-leaf transpose kernel otherwise
-    const bool grp = L.P <= 32 && L.n <= 256 * nl;
+    const bool grp = L.P <= 32 && L.n <= 256 * (int64_t)L.nleaves;
     if (grp) {
         constexpr int G = 8;
         const unsigned blocks = (unsigned)((nl * G + 127) / 128);

@@ -7,14 +7,19 @@ leaf keys (the row-major analogue of a Morton range).  Per evaluate:
 1. **redistribution** -- every particle goes to the rank owning its leaf row
    (``all_to_all_single``; the binning is the reference floor rule,
    quadtree.py:39-46, evaluated with the same IEEE operations as the kernel);
-2. **halo** -- each rank sends the particles of its first / last owned row to
-   the neighbour below / above (``all_to_all_single``), which is exactly what
-   the P2P of its boundary leaves needs (3x3 neighbourhoods, engine.py:216-235);
-3. **upward** on the GPU (``vfmm_evaluate_shard`` PHASE_UP): P2M over owned
-   leaves only, M2M over the whole pyramid, occupancy of owned rows;
-4. **all-reduce** (SUM, NCCL over NVLink) of the multipole pyramid and of the
-   int32 occupancy pyramid -- multipoles are linear in Gamma and the per-rank
-   occupancies are disjoint, so the sums are the global pyramids;
+2. **particle halo** -- each rank sends the particles of its first / last owned
+   row to the neighbour below / above, which is exactly what the P2P of its
+   boundary leaves needs (3x3 neighbourhoods, engine.py:216-235);
+3. **upward** on the GPU (``vfmm_evaluate_shard`` PHASE_UP), strip-local: P2M
+   of the owned leaves, M2M of the subtrees touching the strip (partial
+   multipoles for coarse cells straddling strips); the near field starts;
+4. **multipole exchange** over NCCL (``exchange_multipoles``): an allgather of
+   the small coarse levels 2..kc (each rank's partials, summed in rank order
+   by ``vfmm_shard_unpack``) and a grouped send / recv with the neighbour
+   strips of one plane row per parity plane of every fine level -- the two
+   cell rows the M2L reaches beyond the strip (engine.py:77-89).  Config 3 on
+   8 ranks: ~0.7 MB of multipoles per rank and direction instead of the
+   117 MB pyramid;
 5. **downward** on the GPU (PHASE_DOWN): M2L / L2L for cells touching the
    strip, P2P for owned leaves, L2P + combine for owned particles;
 6. **counters** -- int64 all-reduce; each rank counts only what it owns, so the
@@ -43,9 +48,18 @@ from .quadtree import OutOfDomainError
 
 
 def row_bounds(levels: int, world: int) -> list[tuple[int, int]]:
-    """Equal strips of the 2^levels leaf rows: rank r owns [r*m//world, (r+1)*m//world)."""
+    """Near-equal strips of the 2^levels leaf rows: rank r owns [b_r, b_{r+1}),
+    b_r = floor(r m / world) rounded down to a multiple of u, the largest power
+    of two <= m / (8 world) (1 for small grids).  Power-of-two worlds get
+    exact equal strips; other worlds get strips within ~1/8 of each other
+    whose boundaries sit on even cell rows of more levels, so fewer levels
+    have to be all-gathered (``coarse_cut``)."""
     m = 2**levels
-    return [(r * m // world, (r + 1) * m // world) for r in range(world)]
+    u = 1
+    while 2 * u <= m // (8 * world):
+        u *= 2
+    b = [(r * m // world) // u * u for r in range(world)] + [m]
+    return [(b[r], b[r + 1]) for r in range(world)]
 
 
 def leaf_rows(y: torch.Tensor, domain, levels: int) -> torch.Tensor:
@@ -57,6 +71,34 @@ def leaf_rows(y: torch.Tensor, domain, levels: int) -> torch.Tensor:
 def owner_of_rows(rows: torch.Tensor, bounds) -> torch.Tensor:
     starts = torch.tensor([lo for lo, _ in bounds], dtype=torch.int64, device=rows.device)
     return torch.searchsorted(starts, rows, right=True) - 1
+
+
+def coarse_cut(levels: int, bounds) -> int:
+    """kc: the levels 2..kc are all-gathered, the levels above exchange halo rows.
+
+    A level k is "fine" when every non-empty strip starts and ends on an even
+    cell row of level k and is at least two cell rows tall: the two cell rows
+    the M2L reaches beyond a strip then belong to the neighbour strip and form
+    one row of each parity plane.  Fine levels are closed upwards, so kc is
+    the finest level that is not fine (1 when every level is)."""
+    kc = 1
+    for k in range(2, levels + 1):
+        sft = levels - k
+        mask = (1 << (sft + 1)) - 1
+        fine = all((lo & mask) == 0 and (hi & mask) == 0 and ((hi - lo) >> sft) >= 2
+                   for lo, hi in bounds if hi > lo)
+        if not fine:
+            kc = k
+    return kc
+
+
+def neighbours(bounds, rank: int):
+    """(rank below, rank above) of a strip: the nearest ranks with non-empty strips."""
+    if bounds[rank][1] <= bounds[rank][0]:
+        return None, None
+    below = next((r for r in range(rank - 1, -1, -1) if bounds[r][1] > bounds[r][0]), None)
+    above = next((r for r in range(rank + 1, len(bounds)) if bounds[r][1] > bounds[r][0]), None)
+    return below, above
 
 
 def _exchange(cols: torch.Tensor, dest: torch.Tensor, world: int, group=None) -> torch.Tensor:
@@ -132,29 +174,66 @@ class CudaShardBackend:
                 float(domain.xmin), float(domain.ymin), float(domain.side), config.levels,
                 config.order, kernel_code(config.kernel), shard.rows[0], shard.rows[1])
 
-    def regions(self, n: int, config):
-        mo, mb = _lib.region("mult", n, config.levels, config.order)
-        co, cb = _lib.region("counts", n, config.levels, config.order)
-        return (mo, mb), (co, cb)
-
     def up(self, shard: Shard, config, domain):
-        """Returns (multipoles as float64, occupancy as int32) views to be sum-reduced."""
+        """PHASE_UP (asynchronous on the current stream); OVERLAP starts the near field."""
         nl = shard.cols.shape[1]
-        (mo, mb), (co, cb) = self.regions(nl, config)
-        if nl == 0:  # nothing local: contribute zeros to the reductions
+        self.shape = (nl, config.levels, config.order, shard.rows)
+        if nl == 0:
             self.ws = None
-            return (torch.zeros(mb // 8, dtype=torch.float64, device=self.device),
-                    torch.zeros(cb // 4, dtype=torch.int32, device=self.device))
+            return
         self.ws = (Workspace(nl, config.levels, config.order, self.device) if self.private
                    else Workspace.get(nl, config.levels, config.order, self.device))
-        # asynchronous; OVERLAP starts the near field here (it needs only the local tree)
         rc = self.lib.vfmm_evaluate_shard(*self._args(shard, config, domain), None, None,
                                           self.ws.ptr, self.ws.nbytes,
                                           _lib.FLAG_PHASE_UP | self.up_flags, None,
                                           stream_ptr(self.device))
         _lib.check(rc, "vfmm_evaluate_shard(up)")
-        buf = self.ws.buffer
-        return buf[mo: mo + mb].view(torch.float64), buf[co: co + cb].view(torch.int32)
+
+    def _buffers(self, kc: int):
+        """Exchange buffers (reused across calls: graph replays see fixed addresses)."""
+        nl, lv, p, (lo, hi) = self.shape
+        key = (lv, p, lo, hi, kc)
+        if getattr(self, "_buf_key", None) != key:
+            cb, hb = ctypes.c_size_t(), ctypes.c_size_t()
+            rc = self.lib.vfmm_shard_exchange_size(max(nl, 1), lv, p, lo, hi, kc, ctypes.byref(cb),
+                                                   ctypes.byref(hb))
+            _lib.check(rc, "vfmm_shard_exchange_size")
+            mk = lambda b: torch.zeros(b, dtype=torch.uint8, device=self.device)  # noqa: E731
+            self._bufs = {"coarse": mk(cb.value), "down": mk(hb.value), "up": mk(hb.value),
+                          "below": mk(hb.value), "above": mk(hb.value)}
+            self._buf_key = key
+        return self._bufs
+
+    def pack(self, kc: int, below: bool, above: bool):
+        """(coarse contribution, rows for the strip below, rows for the strip above);
+        byte tensors, None where there is nothing to send."""
+        nl, lv, p, (lo, hi) = self.shape
+        b = self._buffers(kc)
+        coarse = b["coarse"] if b["coarse"].numel() else None
+        down = b["down"] if below and b["down"].numel() else None
+        up = b["up"] if above and b["up"].numel() else None
+        if self.ws is None:  # nothing local: a zero contribution
+            if coarse is not None:
+                coarse.zero_()
+            return coarse, down, up
+        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        rc = self.lib.vfmm_shard_pack(nl, lv, p, lo, hi, kc, self.ws.ptr, ptr(coarse), ptr(down),
+                                      ptr(up), stream_ptr(self.device))
+        _lib.check(rc, "vfmm_shard_pack")
+        return coarse, down, up
+
+    def recv_buffers(self, kc: int):
+        b = self._buffers(kc)
+        return b["below"], b["above"]
+
+    def unpack(self, kc: int, coarse_all, world: int, from_below, from_above):
+        if self.ws is None:
+            return
+        nl, lv, p, (lo, hi) = self.shape
+        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        rc = self.lib.vfmm_shard_unpack(nl, lv, p, lo, hi, kc, self.ws.ptr, ptr(coarse_all), world,
+                                        ptr(from_below), ptr(from_above), stream_ptr(self.device))
+        _lib.check(rc, "vfmm_shard_unpack")
 
     def down(self, shard: Shard, config, domain, counters: bool = True):
         """(2, n_local) velocities (owned columns valid), m2l_count, near_pair_count
@@ -178,18 +257,57 @@ class CudaShardBackend:
         return vel, int(st.m2l_count), int(st.near_pair_count)
 
 
+def _all_gather_bytes(out: torch.Tensor, inp: torch.Tensor, world: int, group=None):
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, inp, group=group)
+    else:
+        dist.all_gather(list(out.view(world, -1).unbind(0)), inp, group=group)
+
+
+def exchange_multipoles(backend, config, world: int, rank: int, group=None, stats: dict | None = None):
+    """Step 4: coarse allgather + neighbour halo rows, between PHASE_UP and PHASE_DOWN."""
+    bounds = row_bounds(config.levels, world)
+    kc = coarse_cut(config.levels, bounds)
+    below, above = neighbours(bounds, rank)
+    coarse, down, up = backend.pack(kc, below is not None, above is not None)
+    coarse_all = None
+    if coarse is not None:
+        coarse_all = torch.empty(world * coarse.numel(), dtype=torch.uint8, device=coarse.device)
+        _all_gather_bytes(coarse_all, coarse, world, group)
+    rb, ra = backend.recv_buffers(kc)
+    from_below = rb if down is not None else None
+    from_above = ra if up is not None else None
+    ops = []
+    glob = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)
+    if below is not None and down is not None:
+        ops += [dist.P2POp(dist.isend, down, glob(below), group),
+                dist.P2POp(dist.irecv, from_below, glob(below), group)]
+    if above is not None and up is not None:
+        ops += [dist.P2POp(dist.isend, up, glob(above), group),
+                dist.P2POp(dist.irecv, from_above, glob(above), group)]
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    backend.unpack(kc, coarse_all, world, from_below, from_above)
+    if stats is not None:
+        stats.update(kc=kc, coarse_bytes=0 if coarse is None else coarse.numel(),
+                     halo_bytes_sent=sum(t.numel() for t in (down, up) if t is not None),
+                     recv_bytes=(0 if coarse_all is None else coarse_all.numel())
+                     + sum(t.numel() for t in (from_below, from_above) if t is not None))
+
+
 def evaluate_shard(shard: Shard, config, domain, *, backend=None, group=None, counters=True):
-    """Steps 3-6 on a prepared shard: upward, all-reduces, downward, counters.
+    """Steps 3-6 on a prepared shard: upward, multipole exchange, downward, counters.
     Returns ((2, n_local) velocities, FmmRunStats or None)."""
     if backend is None:
         backend = CudaShardBackend(shard.cols.device)
-    mult, occ = backend.up(shard, config, domain)
-    dist.all_reduce(mult, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(occ, op=dist.ReduceOp.SUM, group=group)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    backend.up(shard, config, domain)
+    exchange_multipoles(backend, config, world, rank, group)
     vel, m2l, near = backend.down(shard, config, domain, counters=counters)
     if not counters:
         return vel, None
-    cnt = torch.tensor([m2l, near, shard.n_owned], dtype=torch.int64, device=mult.device)
+    cnt = torch.tensor([m2l, near, shard.n_owned], dtype=torch.int64, device=shard.cols.device)
     dist.all_reduce(cnt, op=dist.ReduceOp.SUM, group=group)
     return vel, FmmRunStats(n=int(cnt[2]), levels=config.levels, order=config.order,
                             m2l_count=int(cnt[0]), near_pair_count=int(cnt[1]))
@@ -258,8 +376,9 @@ def make_shards(x, y, gamma, sigma, domain, levels: int, world: int) -> list[Sha
 
 def evaluate_emulated(x, y, gamma, sigma, config, domain, world: int, backend_factory=None):
     """``world`` logical ranks run one after another on one device, with the
-    reductions done locally: every rank's PHASE_UP, the pyramids summed, then
-    every rank's PHASE_DOWN.  Exercises the row-restricted kernels of the
+    exchange done locally: every rank's PHASE_UP and pack, the coarse
+    contributions concatenated and every rank's unpack with its neighbours'
+    halo rows, then every rank's PHASE_DOWN.  Exercises the row-restricted kernels of the
     sharded path on a single GPU (R logical ranks sequentially).
     Returns ((2, N) velocities, m2l_count, near_pair_count)."""
     validate_config(config)
@@ -268,12 +387,17 @@ def evaluate_emulated(x, y, gamma, sigma, config, domain, world: int, backend_fa
             return CudaShardBackend(x.device, private_workspace=True)
     shards = make_shards(x, y, gamma, sigma, domain, config.levels, world)
     backends = [backend_factory() for _ in shards]
-    parts = [b.up(sh, config, domain) for b, sh in zip(backends, shards)]
-    mult = torch.stack([p[0].clone() for p in parts]).sum(dim=0)
-    occ = torch.stack([p[1].clone() for p in parts]).sum(dim=0)
-    for p in parts:
-        p[0].copy_(mult)
-        p[1].copy_(occ)
+    for b, sh in zip(backends, shards):
+        b.up(sh, config, domain)
+    bounds = row_bounds(config.levels, world)
+    kc = coarse_cut(config.levels, bounds)
+    nb = [neighbours(bounds, r) for r in range(world)]
+    packs = [b.pack(kc, lo is not None, hi is not None) for b, (lo, hi) in zip(backends, nb)]
+    coarse_all = (torch.cat([p[0] for p in packs]) if packs and packs[0][0] is not None else None)
+    for r, b in enumerate(backends):
+        below, above = nb[r]
+        b.unpack(kc, coarse_all, world, packs[below][2] if below is not None else None,
+                 packs[above][1] if above is not None else None)
     out = torch.zeros((2, x.numel()), dtype=torch.float64, device=x.device)
     m2l = near = 0
     for sh, b in zip(shards, backends):

@@ -99,12 +99,73 @@ def test_row_bounds_and_owner():
     assert D.row_bounds(2, 8)[0] == (0, 0)  # more ranks than rows: empty strips
 
 
+def test_coarse_cut_and_neighbours():
+    assert D.coarse_cut(7, D.row_bounds(7, 1)) == 1  # one strip: nothing to exchange
+    assert D.coarse_cut(7, D.row_bounds(7, 2)) == 1  # every level fine: halo rows only
+    assert D.coarse_cut(7, D.row_bounds(7, 4)) == 2
+    assert D.coarse_cut(7, D.row_bounds(7, 8)) == 3
+    assert D.coarse_cut(9, D.row_bounds(9, 8)) == 3
+    b3 = D.row_bounds(7, 3)
+    assert b3 == [(0, 40), (40, 84), (84, 128)] and D.coarse_cut(7, b3) == 5
+    assert D.neighbours(D.row_bounds(7, 4), 0) == (None, 1)
+    assert D.neighbours(D.row_bounds(7, 4), 3) == (2, None)
+    b = D.row_bounds(2, 8)  # 4 rows, 8 ranks: empty strips are skipped
+    assert D.neighbours(b, 2) == (None, None) or b[2][0] < b[2][1]
+    nonempty = [r for r in range(8) if b[r][1] > b[r][0]]
+    for i, r in enumerate(nonempty):
+        lo, hi = D.neighbours(b, r)
+        assert lo == (nonempty[i - 1] if i else None)
+        assert hi == (nonempty[i + 1] if i + 1 < len(nonempty) else None)
+
+
+def test_multipole_exchange_volume_config3_on_8_ranks():
+    """SURVEY.md §8e / north_star: coarse allgather + neighbour halo rows instead of
+    the whole pyramid (117 MB at config 3): <= 5 MB received per rank and step."""
+    import ctypes
+
+    from paper_0809_1810_b200 import _lib
+
+    lib = _lib.load()
+    lv, p, world = 9, 20, 8
+    bounds = D.row_bounds(lv, world)
+    kc = D.coarse_cut(lv, bounds)
+    pyramid = sum(4**k for k in range(2, lv + 1)) * (p + 1) * 16
+    for r, (lo, hi) in enumerate(bounds):
+        cb, hb = ctypes.c_size_t(), ctypes.c_size_t()
+        assert lib.vfmm_shard_exchange_size(2_000_000, lv, p, lo, hi, kc, ctypes.byref(cb), ctypes.byref(hb)) == 0
+        below, above = D.neighbours(bounds, r)
+        recv = world * cb.value + hb.value * ((below is not None) + (above is not None))
+        assert recv <= 5_000_000, recv
+        assert recv < pyramid / 50
+    # a level above kc that is not fine for the strip is rejected
+    cb, hb = ctypes.c_size_t(), ctypes.c_size_t()
+    lo, hi = bounds[1]
+    assert lib.vfmm_shard_exchange_size(1000, lv, p, lo, hi, kc - 1, ctypes.byref(cb), ctypes.byref(hb)) == 1
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("world", [2, 3, 4, 8, 16])
 def test_gpu_shard_kernels_match_single_gpu(world):
     from paper_0809_1810_b200 import workloads as W
 
     w = W.config1()
+    dev = torch.device("cuda", 0)
+    t = [torch.from_numpy(a).to(dev) for a in (w.x, w.y, w.gamma, w.sigma)]
+    cfg = vf.FmmConfig(w.levels, w.order, G)
+    dom = vf.Domain(*W.DOMAIN)
+    ref, st = vf.evaluate_arrays(*t, cfg, dom)
+    vel, m2l, near = D.evaluate_emulated(*t, cfg, dom, world)
+    assert m2l == st.m2l_count and near == st.near_pair_count
+    assert float((vel - ref).abs().max() / ref.abs().max()) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 8])
+def test_gpu_shard_kernels_config2_full_size(world):
+    """Config 2 (N = 2^20, l = 7, p = 17) on W logical ranks vs the single-GPU evaluate."""
+    from paper_0809_1810_b200 import workloads as W
+
+    w = W.config2()
     dev = torch.device("cuda", 0)
     t = [torch.from_numpy(a).to(dev) for a in (w.x, w.y, w.gamma, w.sigma)]
     cfg = vf.FmmConfig(w.levels, w.order, G)
