@@ -513,12 +513,22 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         launch_m2l(L, T, mult, counts, loc, (double2*)(ws + L.anc), ctr, rows, fs);
         rec(3, fs);
         // ---- downward ----
-        // Single-GPU evaluates fuse the L2P + combine into the finest L2L
-        // level (the near-field totals must be complete first): one launch and
-        // one pass over the leaf locals fewer on the critical path.
-        fuse = up && !far_only && levels > 2;
+        // The L2P + combine is fused into the finest L2L level (the
+        // near-field totals must be complete first): one launch and one pass
+        // over the leaf locals fewer on the critical path.  A sharded
+        // PHASE_DOWN joins the near field PHASE_UP started (or runs it now).
+        fuse = !far_only && levels > 2;
         FusedOut fo{};
-        if (fuse) {
+        if (fuse && !up) {
+            if (overlap) {
+                cudaStreamWaitEvent(fs, rec_up->join_near, 0);
+            } else {
+                rec(7, cs);
+                near_field(cs);
+                rec(8, cs);
+            }
+            fo = FusedOut{src, keys, perm, ls, near_uv, u, v, xmin, ymin, side};
+        } else if (fuse) {
             if (overlap) {
                 rec(7, R->near);
                 near_field(R->near);
@@ -537,7 +547,7 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
                    fs);
         rec(4, fs);
         if (fuse) {
-            if (overlap) {
+            if (overlap && up) {
                 cudaEventRecord(R->join_far, fs);
                 cudaStreamWaitEvent(cs, R->join_far, 0);
             }

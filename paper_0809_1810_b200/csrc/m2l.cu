@@ -489,8 +489,12 @@ __device__ __forceinline__ void tile_pair(const double2* __restrict__ s1, const 
     }
 }
 
-template <int TN, int CW>
-__global__ void __launch_bounds__(128 * CW, CW == 1 ? 2 : 1)
+// Warps: 4 parity classes x CW chunks x G unit groups.  G > 1 (small or
+// strip-restricted grids) splits the 15 units of a destination over G warps,
+// whose partial sums are added in group order through shared memory
+// (deterministic); CW > 1 (large grids) shares the window between chunks.
+template <int TN, int CW, int G>
+__global__ void __launch_bounds__(128 * CW * G, CW * G == 1 ? 2 : 1)
     k_m2l_tile(const __grid_constant__ M2LMaps maps, const double2* __restrict__ mult,
                const int* __restrict__ counts, double2* __restrict__ loc, double2* __restrict__ anc,
                int anc_end, int levels, int P, int nchunks, const Tables* __restrict__ T,
@@ -518,7 +522,9 @@ __global__ void __launch_bounds__(128 * CW, CW == 1 ? 2 : 1)
         ++level;
     }
     const int ngroups = (nchunks + CW - 1) / CW;  // chunk groups of CW chunks (one per warp quad)
-    const int chunk = (int)(b % ngroups) * CW + (int)(threadIdx.x >> 7);
+    const int warp_id = threadIdx.x >> 5;
+    const int chunk = (int)(b % ngroups) * CW + (warp_id >> 2) % CW;
+    const int group = (warp_id >> 2) / CW;  // unit group
     const int64_t tile = b / ngroups;
     const int jx0 = (int)(tile % tiles_x) * kTPX, jy0 = (int)(tile / tiles_x) * kTPY;
     const int parity = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
@@ -598,8 +604,9 @@ __global__ void __launch_bounds__(128 * CW, CW == 1 ? 2 : 1)
         live = active && scnt[r] > 0;
         return r;
     };
+    const int u_end = kUnits * (group + 1) / G;
 #pragma unroll 1
-    for (int u = 0; u < kUnits; ++u) {
+    for (int u = kUnits * group / G; u < u_end; ++u) {
         const int o1 = c_units.o1[parity][u], o2 = c_units.o2[parity][u];
         const int kind = c_units.kind[parity][u];
         bool live1, live2 = false;
@@ -626,14 +633,36 @@ __global__ void __launch_bounds__(128 * CW, CW == 1 ? 2 : 1)
             else tile_pair<TN, 3, 0>(s1, s2, h, P, A);
         }
     }
-    if (active) {
+    double2 res[TN];
+#pragma unroll
+    for (int t = 0; t < TN; ++t) res[t] = make_double2(A.a[0][t] + A.a[1][t], A.a[2][t] + A.a[3][t]);
+    if (G > 1) {  // groups 1.. hand their partials to group 0 through the (now free) window
+        __syncthreads();
+        double2* part = win;  // [G - 1][CW][4][TN][32]
+        const int slot = ((warp_id >> 2) % CW) * 4 + parity;
+        if (group > 0) {
+#pragma unroll
+            for (int t = 0; t < TN; ++t) part[(((group - 1) * CW * 4 + slot) * TN + t) * 32 + lane] = res[t];
+        }
+        __syncthreads();
+        if (group == 0) {
+            for (int gg = 1; gg < G; ++gg) {
+#pragma unroll
+                for (int t = 0; t < TN; ++t) {
+                    const double2 q = part[(((gg - 1) * CW * 4 + slot) * TN + t) * 32 + lane];
+                    res[t].x += q.x;
+                    res[t].y += q.y;
+                }
+            }
+        }
+    }
+    if (active && group == 0) {
         double2* out = loc + cell_off * P + parity * psz + (int64_t)jy * half + jx;
 #pragma unroll
         for (int t = 0; t < TN; ++t) {
             if (m0 + t < P) {
-                const double2 r = make_double2(A.a[0][t] + A.a[1][t], A.a[2][t] + A.a[3][t]);
-                out[(m0 + t) * cstride] = r;
-                if (level < anc_end) anc[(out - loc) + (m0 + t) * cstride] = r;
+                out[(m0 + t) * cstride] = res[t];
+                if (level < anc_end) anc[(out - loc) + (m0 + t) * cstride] = res[t];
             }
         }
     }
@@ -695,19 +724,21 @@ bool m2l_maps(const Layout& L, const double2* mult, M2LMaps* out) {
     return true;
 }
 
-template <int TN, int CW>
+template <int TN, int CW, int G>
 void launch_tile_cw(const Layout& L, const M2LMaps& maps, const Tables* T, const double2* mult,
                     const int* counts, double2* loc, double2* anc, Counters* ctr, Rows rows,
                     int64_t tiles, int nchunks, cudaStream_t s) {
     const int64_t blocks = tiles * ((nchunks + CW - 1) / CW);
-    const size_t smem = (size_t)L.P * kWinCells * sizeof(double2) +
-                        (size_t)kOffsets * (CW * TN + L.P) * sizeof(double2);
+    size_t smem = (size_t)L.P * kWinCells * sizeof(double2) +
+                  (size_t)kOffsets * (CW * TN + L.P) * sizeof(double2);
+    const size_t parts = (size_t)(G - 1) * CW * 4 * TN * 32 * sizeof(double2);  // reuses the window
+    if (parts > smem) smem = parts;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_m2l_tile<TN, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_m2l_tile<TN, CW, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = true;
     }
-    launch_k(k_m2l_tile<TN, CW>, (unsigned)blocks, 128 * CW, smem, s, maps, mult, counts, loc, anc,
+    launch_k(k_m2l_tile<TN, CW, G>, (unsigned)blocks, 128 * CW * G, smem, s, maps, mult, counts, loc, anc,
              l2l_split_level(L.levels, L.P), L.levels, L.P, nchunks, T, &ctr->m2l_count, rows);
     note_launches(1);
 }
@@ -721,23 +752,35 @@ template <int TN>
 bool launch_tile_tn(const Layout& L, const Tables* T, const double2* mult, const int* counts,
                     double2* loc, double2* anc, Counters* ctr, Rows rows, cudaStream_t s) {
     const int nchunks = (L.P + TN - 1) / TN;
-    int64_t tiles = 0;
+    int64_t tiles = 0, active = 0;  // active: tiles touching the owned strip (sharded runs)
     for (int level = 2; level <= L.levels; ++level) {
         const int half = 1 << (level - 1);
-        tiles += (int64_t)((half + kTPX - 1) / kTPX) * ((half + kTPY - 1) / kTPY);
+        const int ty = (half + kTPY - 1) / kTPY, tx = (half + kTPX - 1) / kTPX;
+        tiles += (int64_t)tx * ty;
+        for (int t = 0; t < ty; ++t) {  // tile t covers cell rows [8 t, 8 t + 8) of the level
+            const int s = L.levels - level;
+            if (((8 * t) << s) < rows.hi && ((8 * t + 8) << s) > rows.lo) active += tx;
+        }
     }
-    if (tiles * nchunks < 2 * 148) return false;
+    if (active * nchunks < 32) return false;
     M2LMaps maps;
     if (!m2l_maps(L, mult, &maps)) return false;
     static const int cw_env = getenv("VFMM_M2L_CW") ? atoi(getenv("VFMM_M2L_CW")) : 0;
-    int cw = (tiles * nchunks >= 8 * 2 * 148 && nchunks <= 3) ? nchunks : 1;
+    static const int g_env = getenv("VFMM_M2L_TG") ? atoi(getenv("VFMM_M2L_TG")) : 0;
+    const int64_t work = active * nchunks;  // single-chunk CTAs that do work
+    int cw = (work >= 8 * 2 * 148 && nchunks <= 3) ? nchunks : 1;
+    int g = work < 2 * 148 ? 3 : 1;  // sparse grids: shorter warps, more of them
     if (cw_env >= 1 && cw_env <= 3) cw = cw_env;
-    if (cw == 1)
-        launch_tile_cw<TN, 1>(L, maps, T, mult, counts, loc, anc, ctr, rows, tiles, nchunks, s);
+    if (g_env == 1 || g_env == 3) g = g_env;
+    if (g == 3) cw = 1;
+    if (cw == 1 && g == 1)
+        launch_tile_cw<TN, 1, 1>(L, maps, T, mult, counts, loc, anc, ctr, rows, tiles, nchunks, s);
+    else if (g == 3)
+        launch_tile_cw<TN, 1, 3>(L, maps, T, mult, counts, loc, anc, ctr, rows, tiles, nchunks, s);
     else if (cw == 2)
-        launch_tile_cw<TN, 2>(L, maps, T, mult, counts, loc, anc, ctr, rows, tiles, nchunks, s);
+        launch_tile_cw<TN, 2, 1>(L, maps, T, mult, counts, loc, anc, ctr, rows, tiles, nchunks, s);
     else
-        launch_tile_cw<TN, 3>(L, maps, T, mult, counts, loc, anc, ctr, rows, tiles, nchunks, s);
+        launch_tile_cw<TN, 3, 1>(L, maps, T, mult, counts, loc, anc, ctr, rows, tiles, nchunks, s);
     return true;
 }
 

@@ -1,5 +1,5 @@
-python -m pytest tests/test_distributed.py tests/test_gpu_api.py -m gpu -x -q > gpurun_out/shard_tests.log 2>&1; echo rc=$? >> gpurun_out/shard_tests.log
-tail -5 gpurun_out/shard_tests.log
-python tools/shard_probe.py 2 1 2 4 8 > gpurun_out/shard_probe.log 2>&1
-python tools/shard_probe.py 3 8 >> gpurun_out/shard_probe.log 2>&1
-cat gpurun_out/shard_probe.log
+python -m pytest tests/test_distributed.py tests/test_gpu_api.py tests/test_gpu_parity.py -m gpu -x -q 2>&1 | tail -2
+PHASES=1 python tools/shard_probe.py 2 1 8 2>&1 | tail -8
+for c in 1 2 3; do python tools/m2l_probe.py $c; done
+VFMM_M2L_TG=3 python tools/m2l_probe.py 2
+VFMM_M2L_TG=3 python tools/m2l_probe.py 1
