@@ -667,6 +667,9 @@ struct HostGraph {
 };
 std::mutex g_graph_mu;
 std::vector<HostGraph> g_graphs;
+// Keys seen once: a graph is captured on the SECOND call of a key, so one-off
+// shapes (parameter sweeps) do not pay the capture + instantiation (~1 ms).
+std::vector<HostGraph> g_graph_seen;
 unsigned long long g_graph_tick = 0;
 constexpr size_t kMaxGraphs = 32;
 
@@ -720,6 +723,20 @@ int evaluate_host_graph(const HostIO& io, int64_t n, double xmin, double ymin, d
                 nl = g.launches;
                 break;
             }
+        if (!exec) {
+            bool seen = false;
+            for (auto& g : g_graph_seen)
+                if (g.dev == dev && g.ws == workspace && g.n == n && g.levels == levels &&
+                    g.order == order && g.kernel == kernel && g.flags == kflags && g.xmin == xmin &&
+                    g.ymin == ymin && g.side == side)
+                    seen = true;
+            if (!seen) {
+                if (g_graph_seen.size() >= 64) g_graph_seen.erase(g_graph_seen.begin());
+                g_graph_seen.push_back(HostGraph{dev, workspace, n, levels, order, kernel, kflags, xmin,
+                                                 ymin, side, nullptr, 0, 0});
+                return -1;  // stream launches this time
+            }
+        }
         if (!exec) {
             // capture on the library's compute stream (thread-local mode: other
             // threads' unrelated CUDA calls do not invalidate the capture)

@@ -53,6 +53,9 @@ __global__ void __launch_bounds__(kSubThreads)
         // row consecutive: runs of side/2 cells are contiguous in the planar
         // layout (the cell-major order read 16 B per coefficient stride)
         const int hs = side >> 1;  // cells per plane row of the subtree (side >= 2)
+        // the whole subtree inside the strip (always on one GPU): no masking
+        const bool inside = ((cy * side) << (levels - lf)) >= rows.lo &&
+                            ((cy * side + side) << (levels - lf)) <= rows.hi;
         for (int i = threadIdx.x; i < ncell * P; i += blockDim.x) {
             const int k = i / ncell, r = i % ncell;
             const int plane = r / (hs * hs), hy = (r / hs) % hs, hx = r % hs;
@@ -61,7 +64,7 @@ __global__ void __launch_bounds__(kSubThreads)
             // (sharded partial sums: a coarse parent collects only this rank's
             // children; the exchange adds the other ranks' partials)
             const int gy = cy * side + ly;
-            dst[(ly * side + lx) * P + k] = rows_touch(rows, gy, levels - lf)
+            dst[(ly * side + lx) * P + k] = (inside || rows_touch(rows, gy, levels - lf))
                                                 ? src[coef_base(lf, cx * side + lx, gy) + k * cs]
                                                 : make_double2(0.0, 0.0);
         }

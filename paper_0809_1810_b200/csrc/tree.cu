@@ -65,11 +65,9 @@ __device__ __forceinline__ int cell_of(double v, double lo, double side, double 
 // particles; many distinct leaves per run (a random order) make the per-leaf
 // atomics and gathers of the counting path scattered, so the LSD sort (whose
 // passes write digit runs) is used instead.
-__global__ void __launch_bounds__(256)
-    k_sort_probe(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
-                 double xmin, double ymin, double side, int levels, bool force_lsd,
-                 Counters* __restrict__ ctr) {
-    pdl_enter();
+__device__ void sort_probe_impl(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                                double xmin, double ymin, double side, int levels, bool force_lsd,
+                                Counters* __restrict__ ctr) {
     __shared__ int distinct;
     if (threadIdx.x == 0) distinct = 0;
     __syncthreads();
@@ -645,6 +643,39 @@ __global__ void __launch_bounds__(kScanThreads)
     }
 }
 
+// One CTA of 1024 threads for short arrays (the leaf counts of l <= 8: at
+// most 65,537 ints): sub-tiles of 4096 ints scanned in turn with a running
+// carry -- no tile tickets and no look-back chain across CTAs (config 2's
+// 16,385 leaf counts: 3 chained tiles took ~10 us).
+constexpr int kScanOneThreads = 1024;
+constexpr int64_t kScanOneMax = 65537;
+__global__ void __launch_bounds__(kScanOneThreads)
+    k_scan_one(int* __restrict__ data, int64_t n, const int* __restrict__ skip_flag, int skip_val) {
+    pdl_enter();
+    if (skip_flag && *skip_flag == skip_val) return;  // leaf-count scan: counting path only
+    __shared__ int warp_sums[32];
+    __shared__ int total;
+    int carry = 0;
+    for (int64_t base = 0; base < n; base += (int64_t)kScanOneThreads * kScanItems) {
+        const int64_t i0 = base + (int64_t)threadIdx.x * kScanItems;
+        int v[kScanItems];
+        int sum = 0;
+#pragma unroll
+        for (int j = 0; j < kScanItems; ++j) {
+            v[j] = i0 + j < n ? data[i0 + j] : 0;
+            sum += v[j];
+        }
+        int r = carry + block_exclusive_scan(sum, warp_sums, &total);
+#pragma unroll
+        for (int j = 0; j < kScanItems; ++j) {
+            if (i0 + j < n) data[i0 + j] = r;
+            r += v[j];
+        }
+        carry += total;
+        __syncthreads();
+    }
+}
+
 __global__ void k_leaf_starts(const int* __restrict__ keys, int64_t n, int nleaves,
                               int* __restrict__ ls, const Counters* __restrict__ ctr) {
     pdl_enter();
@@ -769,6 +800,11 @@ size_t scan_tiles(int64_t n) { return (size_t)((n + kScanTile - 1) / kScanTile);
 void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream_t s,
                      const Counters* sym_skip, bool gauss, const int* skip_flag, int skip_val) {
     if (n <= 0) return;
+    if (!sym_skip && n <= kScanOneMax) {
+        launch_k(k_scan_one, 1, kScanOneThreads, 0, s, data, n, skip_flag, skip_val);
+        note_launches(1);
+        return;
+    }
     launch_k(k_scan, (unsigned)scan_tiles(n), kScanThreads, 0, s, data, n, state, sym_skip, gauss,
                                                               skip_flag, skip_val);
     note_launches(1);
@@ -781,10 +817,27 @@ struct ZeroRegions {
     int* p[4];
     int64_t n[4];  // ints
 };
-__global__ void k_zero_regions(ZeroRegions z) {
+struct ProbeArgs {
+    const double *x, *y;
+    int64_t n;
+    double xmin, ymin, side;
+    int levels;
+    bool force_lsd;
+};
+__device__ void sort_probe(const ProbeArgs& a, Counters* ctr) {
+    sort_probe_impl(a.x, a.y, a.n, a.xmin, a.ymin, a.side, a.levels, a.force_lsd, ctr);
+}
+// The build's first kernel: zero the scratch regions, and CTA 0 also runs the
+// sort-path probe (one launch instead of two; the counters are zeroed by the
+// memset that precedes it).
+__global__ void k_zero_regions(ZeroRegions z, ProbeArgs pa, Counters* ctr) {
     pdl_enter();
-    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if (blockIdx.x == 0) {
+        sort_probe(pa, ctr);
+        return;
+    }
+    const int64_t t0 = (int64_t)(blockIdx.x - 1) * blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)(gridDim.x - 1) * blockDim.x;
 #pragma unroll
     for (int r = 0; r < 4; ++r)
         for (int64_t i = t0; i < z.n[r]; i += stride) z.p[r][i] = 0;
@@ -812,12 +865,10 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
         ZeroRegions z{{(int*)(ws + L.scan_state), ls, fill, ghist},
                       {(int64_t)(L.scan_state_bytes / sizeof(int)), (int64_t)L.nleaves + 1,
                        (int64_t)L.nleaves, (int64_t)(L.hist_bytes / sizeof(int))}};
-        launch_k(k_zero_regions, 296, 256, 0, s, z);
+        const ProbeArgs pa{x, y, L.n, xmin, ymin, side, L.levels, force_lsd()};
+        launch_k(k_zero_regions, 297, 256, 0, s, z, pa, ctr);
         note_launches(1);
     }
-
-    launch_k(k_sort_probe, 1, 256, 0, s, x, y, L.n, xmin, ymin, side, L.levels, force_lsd(), ctr);
-    note_launches(1);
     // ---- counting path (kernels return at once if the probe chose LSD) ----
     launch_k(k_bin_count, small_grid(L.n, 2368), 256, 0, s, x, y, L.n, xmin, ymin, side, L.levels,
                                                   kbuf[(L.passes + 1) & 1], ls, ctr);
