@@ -312,8 +312,11 @@ def run_ours(args):
     launches_per_step = lib.vfmm_launch_count() - c0
 
     graph = torch.cuda.CUDAGraph()
+    c1 = lib.vfmm_launch_count()
     with torch.cuda.graph(graph, stream=stream):
         call(torch.cuda.current_stream(dev))
+    # kernels a replay launches (the untaken paths sit in conditional nodes)
+    graph_launches = lib.vfmm_launch_count() - c1
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(max(3, args.warmup)):
         flush.zero_()
@@ -406,7 +409,8 @@ def run_ours(args):
                         "host wall clock",
                 "latency_ms": e2e_latency,
                 "latency_mode": "one synchronous evaluate_host call (stats on; copies overlapped with the build), CUDA events"},
-        "gpu_launches": int(launches_per_step) * args.steps,
+        "gpu_launches": int(graph_launches) * args.steps,
+        "launches_per_step": {"graph_replay": int(graph_launches), "stream_call": int(launches_per_step)},
         "roofline": {"bound": "fp64", "kernel": "k_p2p (near field)", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "peak_source": "measured live: DFMA probe (vfmm_fp64_probe), 148x8 CTAs",

@@ -232,7 +232,10 @@ int vfmm_direct(const double* tx, const double* ty, int64_t m,
 int vfmm_fp64_probe(double* sink, int blocks, int iters, double* flops, void* stream);
 
 /* Total kernel launches issued by this library in this process (host-side
- * counter; CUDA-graph replays are not counted).                           */
+ * counter; CUDA-graph replays are not counted).  While a call is captured
+ * into a CUDA graph, the untaken path of a device-side choice (the LSD sort,
+ * the generic near field) is put in the body of an IF conditional node that
+ * a kernel of the taken path sets; those body launches are not counted.    */
 int64_t vfmm_launch_count(void);
 
 /* Version / build string. */

@@ -637,8 +637,11 @@ __global__ void VFMM_SYM_BOUNDS
     k_p2p_sym(const Src* __restrict__ src, const int* __restrict__ ls, Counters* __restrict__ ctr,
               int levels, int64_t n, Rows rows, const Tables* __restrict__ T,
               double2* __restrict__ near5, unsigned long long* __restrict__ pairs,
-              int items_per_warp, int item_base, int nitems) {
+              int items_per_warp, int item_base, int nitems, GraphCond generic_cond) {
     pdl_enter();
+    // a captured graph runs the generic near-field chain (an IF node after
+    // this kernel) only when the symmetric mode does not apply
+    graph_cond_set(generic_cond, p2p_symmetric(ctr, GAUSS) ? 0u : 1u);
     if (!p2p_symmetric(ctr, GAUSS)) return;  // the generic kernel handles it
     const int m = 1 << levels;
     // one item per leaf of rows [rows.lo - 1, rows.hi) (all leaves when not
@@ -902,12 +905,17 @@ static void launch_p2p_generic(const Layout& L, const Tables* T, const Src* src,
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
                 char* ws, Counters* ctr, int kernel, double2* near_uv, Rows rows, cudaStream_t s) {
     const bool g = kernel == VFMM_KERNEL_GAUSSIAN;
-    // The generic kernel and its task list go first: in symmetric mode they
-    // return at once, and that ~10 us head start lets P2M (far stream) take
-    // its first wave of SM slots before the near field fills the GPU --
-    // measured 0.790 vs 0.799 ms per config-2 evaluate (graph replay) with
-    // them launched after the symmetric kernel.
-    launch_p2p_generic(L, T, src, leaf_starts, ws, ctr, kernel, near_uv, rows, s);
+    // Stream launches: the generic kernel and its task list go first: in
+    // symmetric mode they return at once, and that ~10 us head start lets P2M
+    // (far stream) take its first wave of SM slots before the near field
+    // fills the GPU -- measured 0.790 vs 0.799 ms per config-2 evaluate with
+    // them launched after the symmetric kernel.  Graph capture: the symmetric
+    // kernel first, the generic chain in an IF node it sets (not launched at
+    // all when the symmetric kernel ran).
+    // VFMM_GRAPH_COND=2: the conditional node for the sort path only (A/B)
+    static const bool cond_near = !(getenv("VFMM_GRAPH_COND") && getenv("VFMM_GRAPH_COND")[0] == '2');
+    const GraphCond gc = (sym_disabled() || !cond_near) ? GraphCond{} : graph_cond_create(s);
+    if (!gc.on) launch_p2p_generic(L, T, src, leaf_starts, ws, ctr, kernel, near_uv, rows, s);
     // symmetric kernel: runs instead when the device-side mode check allows it
     // Leaf items per warp: enough CTAs for ~4 waves of 2 CTAs per SM (so
     // the far chain finds free slots and the tail is short), otherwise as
@@ -951,8 +959,17 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
     if (!sym_disabled() && sblocks > 0) {
         launch_k(sfn, sblocks, kSymWarps * 32, kSymSmem, s, src, leaf_starts, ctr, L.levels, L.n, rows, T,
                                                       near_uv, &ctr->near_pairs, ks, item_base,
-                 (int)sym_items);
+                 (int)sym_items, gc);
         note_launches(1);
+    } else if (gc.on) {  // no symmetric kernel to set the condition: run the chain
+        launch_p2p_generic(L, T, src, leaf_starts, ws, ctr, kernel, near_uv, rows, s);
+        return;
+    }
+    if (gc.on) {
+        cudaGraphNode_t node = nullptr;
+        cudaStream_t bs = graph_cond_begin(s, gc, &node);
+        launch_p2p_generic(L, T, src, leaf_starts, ws, ctr, kernel, near_uv, rows, bs);
+        graph_cond_end(s, bs, node);
     }
 }
 

@@ -232,8 +232,11 @@ __global__ void __launch_bounds__(256)
                 const double* __restrict__ x, const double* __restrict__ y,
                 const double* __restrict__ g, const double* __restrict__ sigma, int sstride,
                 int* __restrict__ keys, int* __restrict__ perm, Src* __restrict__ src,
-                Counters* __restrict__ ctr) {
+                Counters* __restrict__ ctr, GraphCond lsd_cond) {
     pdl_enter();
+    // the path choice is final here (k_bin_scatter): a captured graph runs the
+    // LSD kernels (an IF node after this kernel) only when it is taken
+    graph_cond_set(lsd_cond, ctr->sort_fallback != 0 ? 1u : 0u);
     if (ctr->sort_fallback) return;
     __shared__ unsigned long long wmax[8], wmin[8];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -883,7 +886,9 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     // LSD there).  With a side stream the LSD kernels -- which return at once
     // on the counting path -- run as a parallel branch joined after
     // k_leaf_pack, off the counting path's critical chain (and vice versa).
-    const bool branch = lsd_stream && lsd_fork && lsd_join;
+    // graph capture: the LSD kernels go into an IF node set by k_leaf_pack
+    const GraphCond lsd_cond = gs_ready ? GraphCond{} : graph_cond_create(s);
+    const bool branch = lsd_stream && lsd_fork && lsd_join && !lsd_cond.on;
     cudaStream_t ls_s = branch ? lsd_stream : s;
     if (branch) {
         cudaEventRecord(lsd_fork, s);
@@ -894,8 +899,10 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     if (gs_ready) cudaStreamWaitEvent(s, gs_ready, 0);
     launch_k(k_leaf_pack, std::min(grid_for((int64_t)L.nleaves, 8), 2368u), 256, 0, s, ls, slot, (int)L.nleaves, x, y, g,
                                                               sigma, sigma_stride, fkeys, fperm,
-                                                              src, ctr);
+                                                              src, ctr, lsd_cond);
     note_launches(1);
+    cudaGraphNode_t lsd_node = nullptr;
+    if (lsd_cond.on) ls_s = graph_cond_begin(s, lsd_cond, &lsd_node);
 
     // ---- LSD radix path (kernels return at once unless ctr->sort_fallback) ----
     Src* packed = (Src*)(ws + L.near_uv);  // free until the near field runs (>= 32 B per particle)
@@ -925,6 +932,7 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     launch_k(k_leaf_starts, small_grid((int64_t)L.nleaves + 1, 2368), 256, 0, ls_s, fkeys, L.n,
              (int)L.nleaves, ls, ctr);
     note_launches(1);
+    if (lsd_cond.on) graph_cond_end(s, ls_s, lsd_node);
     if (branch) {
         cudaEventRecord(lsd_join, lsd_stream);
         cudaStreamWaitEvent(s, lsd_join, 0);

@@ -127,6 +127,29 @@ inline void launch_k(void (*kern)(K...), dim3 grid, dim3 block, size_t smem, cud
     cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
 }
 
+// ---- CUDA-graph conditional nodes (device-side path choice) ----
+// The build picks its sort path and the near field its kernel on the device
+// (k_bin_scatter / k_counts_tasks decide, no host sync).  Stream launches run
+// the untaken path's kernels, which return at once; when the call is being
+// CAPTURED into a graph, the untaken path is instead put in the body of an IF
+// conditional node whose condition a kernel of the taken path sets with
+// cudaGraphSetConditional, so a replay launches only the kernels it needs.
+struct GraphCond {
+    bool on = false;                       // capturing, handle valid
+    cudaGraphConditionalHandle h = 0;
+};
+// A handle on the graph being captured on s (on = false when s is not capturing).
+GraphCond graph_cond_create(cudaStream_t s);
+bool graph_cond_enabled();  // VFMM_GRAPH_COND=0 disables (A/B)
+// Append an IF node on `h` to the capture of s and start capturing its body on
+// the library's body stream (returned); graph_cond_end closes the body and
+// makes the node the capture dependency of s.
+cudaStream_t graph_cond_begin(cudaStream_t s, const GraphCond& c, cudaGraphNode_t* node);
+void graph_cond_end(cudaStream_t s, cudaStream_t body, cudaGraphNode_t node);
+__device__ __forceinline__ void graph_cond_set(const GraphCond& c, unsigned value) {
+    if (c.on && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(c.h, value);
+}
+
 // ---- kernels launchers (each enqueues on `s`) ----
 void launch_build(const Layout& L, const double* x, const double* y, const double* g,
                   const double* sigma, double xmin, double ymin, double side, char* ws,
