@@ -340,7 +340,7 @@ bool make_layout(int64_t n, int levels, int order, Layout* L) {
     L->task_scratch = take(sizeof(int) * L->nleaves);
     L->scan_state = take(L->scan_state_bytes);
     L->src = take(sizeof(Src) * n);
-    L->near_uv = take(sizeof(double2) * n * kNearSlots);
+    L->near_uv = take(sizeof(double2) * n * kNearSlotsAlloc);
     L->leaf_starts = take(sizeof(int) * (L->nleaves + 1));
     L->counts = take(sizeof(int) * cc);
     L->mult = take(sizeof(double2) * cells * L->P);
@@ -609,7 +609,8 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         // near-field totals must be complete first): one launch and one pass
         // over the leaf locals fewer on the critical path.  A sharded
         // PHASE_DOWN joins the near field PHASE_UP started (or runs it now).
-        fuse = !far_only && levels > 2;
+        static const bool fuse_env = !(getenv("VFMM_FUSE_L2P") && getenv("VFMM_FUSE_L2P")[0] == '0');
+        fuse = fuse_env && !far_only && levels > 2;
         FusedOut fo{};
         if (fuse && !up) {
             if (overlap) {

@@ -31,7 +31,7 @@ __global__ void k_leaf_locals_copy(const double2* __restrict__ loc2, int P, doub
 __global__ void __launch_bounds__(256)
     k_near_sum(const int* __restrict__ keys, double2* __restrict__ near_uv, int64_t n, int levels,
                Rows rows, const int* __restrict__ ls, const Counters* __restrict__ ctr, bool gauss,
-               int sym_enabled) {
+               int sym_enabled, int split) {
     pdl_enter();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -45,6 +45,11 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int k = 0; k < kNearSlots; ++k) t[k] = near_uv[(int64_t)k * n + i];
         nv = t[0];
+        if (split == 2) {  // the leaf's second item (forward stream part 2)
+            const double2 t5 = near_uv[(int64_t)kSplitSlot * n + i];
+            nv.x += t5.x;
+            nv.y += t5.y;
+        }
 #pragma unroll
         for (int k = 1; k < kNearSlots; ++k) {
             // the item of leaf (ix, iy) - d_k wrote slot k; d = (1,0), (-1,1), (0,1), (1,1)
@@ -167,7 +172,7 @@ void launch_near_sum(const Layout& L, const int* keys, double2* near_uv, Rows ro
                      const int* leaf_starts, const Counters* ctr, int kernel, cudaStream_t s) {
     launch_k(k_near_sum, (unsigned)((L.n + 255) / 256), 256, 0, s, 
         keys, near_uv, L.n, L.levels, rows, leaf_starts, ctr, kernel == VFMM_KERNEL_GAUSSIAN,
-        sym_disabled() ? 0 : 1);
+        sym_disabled() ? 0 : 1, p2p_sym_split(L, rows));
     note_launches(1);
 }
 

@@ -637,7 +637,7 @@ __global__ void VFMM_SYM_BOUNDS
     k_p2p_sym(const Src* __restrict__ src, const int* __restrict__ ls, Counters* __restrict__ ctr,
               int levels, int64_t n, Rows rows, const Tables* __restrict__ T,
               double2* __restrict__ near5, unsigned long long* __restrict__ pairs,
-              int items_per_warp, int item_base, int nitems, GraphCond generic_cond) {
+              int items_per_warp, int item_base, int nitems, int split, GraphCond generic_cond) {
     pdl_enter();
     // a captured graph runs the generic near-field chain (an IF node after
     // this kernel) only when the symmetric mode does not apply
@@ -665,7 +665,9 @@ __global__ void VFMM_SYM_BOUNDS
     for (int it = 0; it < items_per_warp; ++it) {
         const int item = __shfl_sync(0xffffffffu, next, 0);
         if (item >= nitems) break;
-        const int leaf = item_base + item;
+        // split == 2: part 0 = self block + R1 + the left leaf of R2, part 1 =
+        // the other two leaves of R2 (the leaf's sums go to kSplitSlot)
+        const int leaf = item_base + item / split, part = item % split;
         if (lane == 0 && it + 1 < items_per_warp) next = atomicAdd(&ctr->task_cursor, 1);
         const int loA = ls[leaf], nA = ls[leaf + 1] - loA;
         if (nA == 0) continue;
@@ -675,7 +677,7 @@ __global__ void VFMM_SYM_BOUNDS
         // cy+1, one contiguous range of the sorted sources)
         int r1 = 0, n1 = 0, r2 = 0, n2 = 0, b3 = 0, b4 = 0;
         bool ownR2 = false;
-        if (ownA && cx + 1 < m) {
+        if (ownA && cx + 1 < m && part == 0) {
             r1 = ls[leaf + 1];
             n1 = ls[leaf + 2] - r1;
         }
@@ -684,15 +686,17 @@ __global__ void VFMM_SYM_BOUNDS
             if (ownA || ownR2) {
                 const int row = (cy + 1) * m;
                 const int x0 = cx > 0 ? cx - 1 : 0, x1 = cx + 1 < m ? cx + 1 : m - 1;
-                r2 = ls[row + x0];
-                n2 = ls[row + x1 + 1] - r2;
                 b3 = ls[row + cx];                          // first source of kind 3 (0, 1)
-                b4 = cx + 1 < m ? ls[row + cx + 1] : r2 + n2;  // first source of kind 4 (1, 1)
+                b4 = cx + 1 < m ? ls[row + cx + 1] : ls[row + x1 + 1];  // first source of kind 4 (1, 1)
+                const int s0 = split == 1 || part == 1 ? (split == 1 ? x0 : cx) : x0;
+                const int e0 = split == 1 || part == 1 ? x1 + 1 : cx;  // leaves [s0, e0) of row cy + 1
+                r2 = ls[row + s0];
+                n2 = ls[row + e0] - r2;
             }
         }
         if (!ownA && n2 == 0) continue;
         // ---- self block (owned A only): each unordered pair once ----
-        if (ownA && nA <= kSymMaxLeaf) {
+        if (part == 0 && ownA && nA <= kSymMaxLeaf) {
             double a0x, a0y, a0g, a1x, a1y, a1g, a2x, a2y, a2g, a3x, a3y, a3g;
             load_lane(src, loA, min(32, nA), lane, a0x, a0y, a0g);
             load_lane(src, loA + (nA > 32 ? 32 : 0), max(nA - 32, 0), lane, a1x, a1y, a1g);
@@ -795,11 +799,12 @@ __global__ void VFMM_SYM_BOUNDS
             p0 += 64;
         }
         my_pairs += 2ll * nA * n1 + (long long)nA * n2 * ((ownA ? 1 : 0) + (ownR2 ? 1 : 0));
-        // A's own targets: self + forward blocks -> slot 0
+        // A's own targets: self + forward blocks -> slot 0 (kSplitSlot: part 1)
         __syncwarp();
+        double2* own = near5 + (part == 0 ? 0 : (int64_t)kSplitSlot * n);
         for (int j = lane; j < nA; j += 32) {
             const double2 t = accAw[j];
-            near5[loA + j] = make_double2(t.x * kInv2Pi, t.y * kInv2Pi);
+            own[loA + j] = make_double2(t.x * kInv2Pi, t.y * kInv2Pi);
         }
         __syncwarp();
     }
@@ -902,6 +907,20 @@ static void launch_p2p_generic(const Layout& L, const Tables* T, const Src* src,
                                const int* leaf_starts, char* ws, Counters* ctr, int kernel,
                                double2* near_uv, Rows rows, cudaStream_t s);
 
+// Split when two items per leaf still fit one wave of warps (2 CTAs of 8
+// warps per SM): the per-item latency, not the SM throughput, then bounds the
+// near field (config 1, 1,024 leaves: 0.131 -> 0.093 ms).  A rank of an 8-way
+// config-2 run (2,176 leaves, one wave unsplit) got slower split.
+// VFMM_P2P_SPLIT=0|1 forces it off / on (A/B).
+int p2p_sym_split(const Layout& L, Rows rows) {
+    static const int env = getenv("VFMM_P2P_SPLIT") ? atoi(getenv("VFMM_P2P_SPLIT")) : -1;
+    if (env == 0 || env == 1) return env ? 2 : 1;
+    const int mrow = 1 << L.levels;
+    const int row0 = rows.lo > 0 ? rows.lo - 1 : 0, row1 = rows.hi < mrow ? rows.hi : mrow;
+    const int64_t leaves = (int64_t)(row1 > row0 ? row1 - row0 : 0) * mrow;
+    return 2 * leaves <= (int64_t)kSymWarps * 2 * 148 ? 2 : 1;  // two items per leaf fit one wave
+}
+
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
                 char* ws, Counters* ctr, int kernel, double2* near_uv, Rows rows, cudaStream_t s) {
     const bool g = kernel == VFMM_KERNEL_GAUSSIAN;
@@ -927,11 +946,12 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
         const char* e = getenv("VFMM_P2P_SYM_K");
         KS_env = e ? atoi(e) : 0;
     }
-    // one item per leaf of the rows the strip needs: [rows.lo - 1, rows.hi)
+    // one item (two when split) per leaf of the rows the strip needs: [rows.lo - 1, rows.hi)
     const int mrow = 1 << L.levels;
     const int row0 = rows.lo > 0 ? rows.lo - 1 : 0, row1 = rows.hi < mrow ? rows.hi : mrow;
     const int item_base = row0 * mrow;
-    const int64_t sym_items = (int64_t)(row1 > row0 ? row1 - row0 : 0) * mrow;
+    const int split = p2p_sym_split(L, rows);
+    const int64_t sym_items = (int64_t)(row1 > row0 ? row1 - row0 : 0) * mrow * split;
     // at least 2 items per warp, except when even that leaves fewer than ~4
     // waves of 2 CTAs per SM: one item per warp then (config 1: 1,024 leaves,
     // P2P 0.144 -> 0.086 ms; a rank of an 8-way config-2 run: 0.266 -> 0.218
@@ -959,7 +979,7 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
     if (!sym_disabled() && sblocks > 0) {
         launch_k(sfn, sblocks, kSymWarps * 32, kSymSmem, s, src, leaf_starts, ctr, L.levels, L.n, rows, T,
                                                       near_uv, &ctr->near_pairs, ks, item_base,
-                 (int)sym_items, gc);
+                 (int)sym_items, split, gc);
         note_launches(1);
     } else if (gc.on) {  // no symmetric kernel to set the condition: run the chain
         launch_p2p_generic(L, T, src, leaf_starts, ws, ctr, kernel, near_uv, rows, s);

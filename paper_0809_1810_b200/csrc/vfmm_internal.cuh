@@ -32,6 +32,8 @@ constexpr int kExpSteps2 = 128;            // symmetric P2P table: 2^(n/128)
 constexpr int kExpTab2N = 60 * kExpSteps2 + 1;  // n = -7680..0 (60 KB)
 constexpr int kNearRows = 3;               // generic P2P: one partial sum per neighbourhood row
 constexpr int kNearSlots = 5;              // symmetric P2P: own blocks + 4 reactions
+constexpr int kSplitSlot = 5;              // split items: the leaf's sums from its second item
+constexpr int kNearSlotsAlloc = 6;         // near_uv slots allocated per particle
 constexpr int kSymMaxLeaf = 128;           // symmetric P2P needs leaves of <= 128 particles
 
 // Packed per-particle source record in leaf-sorted order: x, y, gamma and
@@ -195,6 +197,10 @@ int p2p_targets_per_lane();  // 1 or 2 (env VFMM_P2P_TPT, default 1)
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
                 char* ws, Counters* ctr, int kernel, double2* near_uv, Rows rows, cudaStream_t s);
 bool sym_disabled();  // env VFMM_P2P_SYM=0 forces the generic near-field kernel
+// symmetric P2P work items per leaf: 2 (the forward stream split in two
+// items, the leaf's own sums of the second in slot kSplitSlot) when the
+// leaves alone would not fill the GPU, else 1 (same choice in k_near_sum)
+int p2p_sym_split(const Layout& L, Rows rows);
 void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const int* keys,
                         const int* perm, const double2* loc, const double2* near_uv, double xmin,
                         double ymin, double side, double* u, double* v, Rows rows,
