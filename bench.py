@@ -377,14 +377,33 @@ def run_ours(args):
 
     peak = fp64_peak(lib, torch, dev)
     achieved = P2P_FLOP_PER_PAIR_GAUSS * st.near_pair_count / t_near / 1e12  # t_near in s
+    # traffic and the executed FP64-pipe fraction of the dominant kernel: from
+    # the committed `ncu --set full` capture of the same kernel and config
+    # (profiles/p2p_traffic_config<c>.json, written by tools/ncu_summary.py);
+    # a bench run cannot profile itself
     traffic = None
+    ncu = {}
     prof = os.path.join(REPO, "profiles", f"p2p_traffic_config{args.config}.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            ncu = json.load(open(prof))
+            traffic = ncu.get("dram_bytes_per_launch")
         except Exception:
-            traffic = None
+            traffic, ncu = None, {}
     m2l_flops = 8 * (w.order + 1) ** 2 * st.m2l_count
+    hbm = None
+    try:
+        hbm = float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        hbm = 6457.7  # this pool's measured copy bandwidth (round 1 MEASURED_PEAKS.json)
+    t_build = statistics.fmean(p.t_build for p in phase)
+    build_bytes = 80 * n  # read x, y, Gamma, sigma; write the sorted copy; perm / keys
+    # whole-pipeline roofline: FP64 work at the FP64 peak + the tree build's bytes at HBM
+    # (T_roof = sum(FP64 flops) / F64_peak + tree_bytes / HBM)
+    fp64_flops = (P2P_FLOP_PER_PAIR_GAUSS * st.near_pair_count + m2l_flops
+                  + (8 * w.order + 4) * n + (8 * w.order + 6) * n
+                  + 2 * 4 * (w.order + 1) * (w.order + 2) * sum(4**k for k in range(3, w.levels + 1)))
+    t_roof = fp64_flops / (peak * 1e12) + build_bytes / (hbm * 1e9)
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -417,8 +436,17 @@ def run_ours(args):
                      "nominal_peak": NOMINAL_FP64_TFLOPS,
                      "traffic": traffic, "p2p_ms": t_near * 1e3,
                      "flop_per_pair": P2P_FLOP_PER_PAIR_GAUSS,
+                     "fp64_pipe_executed_pct": ncu.get("fp64_pipe_active_pct"),
+                     "ncu_source": ncu.get("source"),
                      "m2l": {"achieved": m2l_flops / t_m2l / 1e12, "ms": t_m2l * 1e3,
-                             "flop_per_translation": 8 * (w.order + 1) ** 2}},
+                             "frac": m2l_flops / t_m2l / 1e12 / peak,
+                             "flop_per_translation": 8 * (w.order + 1) ** 2},
+                     "build": {"bound": "hbm", "achieved": build_bytes / t_build / 1e9, "ms": t_build * 1e3,
+                               "peak": hbm, "unit": "GB/s", "frac": build_bytes / t_build / 1e9 / hbm,
+                               "bytes_per_particle": 80},
+                     "step": {"t_roof_ms": t_roof * 1e3, "frac": t_roof / (ms * 1e-3),
+                              "note": "sum of FP64 work at the live FP64 peak + build bytes at measured HBM, "
+                                      "over the measured step"}},
         "phases_ms": {k: statistics.fmean(getattr(p, k) for p in phase) * 1e3 for k in
                       ("t_build", "t_upward", "t_m2l", "t_downward", "t_eval", "t_near", "t_total")},
         "clocks": clk.summary(),

@@ -601,6 +601,7 @@ __global__ void __launch_bounds__(128 * CW * G, CW * G == 1 ? 2 : 1)
         const int sx = ix + c_off.dx[parity][o], sy = iy + c_off.dy[parity][o];
         const int r = (((sy & 1) << 1) | (sx & 1)) * (kWX * kWY) + ((sy >> 1) - jy0 + 1) * kWX +
                       ((sx >> 1) - jx0 + 1);
+        VCHECK(!active || (r >= 0 && r < kWinCells));
         live = active && scnt[r] > 0;
         return r;
     };
@@ -618,6 +619,8 @@ __global__ void __launch_bounds__(128 * CW * G, CW * G == 1 ? 2 : 1)
         const double2* h =
             sH + ((c_off.dy[parity][o1] + 3) * 7 + (c_off.dx[parity][o1] + 3)) * HL + (m0 - mg);
         const double2* s1 = win + r1;
+        VCHECK(m0 - mg + TN + P <= HL + TN);
+        VJITTER();
         if (o2 < 0) {
             tile_plain<TN>(s1, h, P, A);
             continue;

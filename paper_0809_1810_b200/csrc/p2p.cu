@@ -190,6 +190,7 @@ constexpr int kSymSmem = kSymExpBytes + kSymWarps * kSymMaxLeaf * 16;  // 76 KB
 __device__ __forceinline__ void load_lane(const Src* __restrict__ src, int lo, int cnt, int lane,
                                           double& x, double& y, double& g) {
     // ghosts (lane >= cnt) sit on the chunk's first particle with zero circulation
+    VCHECK(cnt <= 0 || lo >= 0);
     const Src& s = src[lo + (lane < cnt ? lane : 0)];
     x = s.x;
     y = s.y;
@@ -232,6 +233,7 @@ __device__ __forceinline__ double pair_kernel(double dx, double dy, SymExp x,
     p = fma(p, s, c_exp2_sym[2]);
     p = fma(p, s, c_exp2_sym[1]);
     p = fma(p, s, c_exp2_sym[0]);
+    VCHECK(__double2loint(t) <= 0 && __double2loint(t) >= -(kExpTab2N - 1));
     const double T = tab[__double2loint(t)];
     const double e = fma(T, s * p, T);
     return fma(-inv, e, inv);  // (1 - e) / r^2
@@ -271,6 +273,7 @@ __device__ __forceinline__ void pair_kernels(const double (&dx)[N], const double
     for (int k = 0; k < N; ++k) pp[k] = fma(pp[k], sr[k], c_exp2_sym[0]);
 #pragma unroll
     for (int k = 0; k < N; ++k) {
+        VCHECK(ti[k] <= 0 && ti[k] >= -(kExpTab2N - 1));
         const double T = tab[ti[k]];
         const double e = fma(T, sr[k] * pp[k], T);
         K[k] = fma(-K[k], e, K[k]);  // (1 - e) / r^2
@@ -534,6 +537,7 @@ __device__ __forceinline__ void rotate_stream(const Src* __restrict__ src, doubl
             const int t = j0 + lane;
             const int i = stream_index(t, r1, n1, r2, n2);
             const int kind = t < n1 ? 1 : (i < b3 ? 2 : (i < b4 ? 3 : 4));
+            VCHECK(i >= 0 && i < n && kind >= 1 && kind <= 4);
             near5[(int64_t)kind * n + i] = make_double2(ub * kInv2Pi, vb * kInv2Pi);
         }
         j0 += R;
@@ -670,6 +674,8 @@ __global__ void VFMM_SYM_BOUNDS
         const int leaf = item_base + item / split, part = item % split;
         if (lane == 0 && it + 1 < items_per_warp) next = atomicAdd(&ctr->task_cursor, 1);
         const int loA = ls[leaf], nA = ls[leaf + 1] - loA;
+        VCHECK(loA >= 0 && nA >= 0 && (int64_t)loA + nA <= n && nA <= kSymMaxLeaf);
+        VJITTER();
         if (nA == 0) continue;
         const int cx = leaf & (m - 1), cy = leaf >> levels;
         const bool ownA = cy >= rows.lo && cy < rows.hi;
@@ -770,6 +776,7 @@ __global__ void VFMM_SYM_BOUNDS
                     if (t < nS) {
                         const int i = idx[k];
                         const int kind = t < n1 ? 1 : (i < b3 ? 2 : (i < b4 ? 3 : 4));
+                        VCHECK(i >= 0 && i < n && kind >= 1 && kind <= 4);
                         near5[(int64_t)kind * n + i] = make_double2(u[k] * kInv2Pi, v[k] * kInv2Pi);
                     }
                 }
@@ -790,10 +797,12 @@ __global__ void VFMM_SYM_BOUNDS
             // reactions on the stream particles -> their slot `kind`
             if (t0 < p0 + cnt) {
                 const int kind = t0 < n1 ? 1 : (i0 < b3 ? 2 : (i0 < b4 ? 3 : 4));
+                VCHECK(i0 >= 0 && i0 < n && kind >= 1 && kind <= 4);
                 near5[(int64_t)kind * n + i0] = make_double2(u0 * kInv2Pi, v0 * kInv2Pi);
             }
             if (t1 < p0 + cnt) {
                 const int kind = t1 < n1 ? 1 : (i1 < b3 ? 2 : (i1 < b4 ? 3 : 4));
+                VCHECK(i1 >= 0 && i1 < n && kind >= 1 && kind <= 4);
                 near5[(int64_t)kind * n + i1] = make_double2(u1 * kInv2Pi, v1 * kInv2Pi);
             }
             p0 += 64;
@@ -801,6 +810,7 @@ __global__ void VFMM_SYM_BOUNDS
         my_pairs += 2ll * nA * n1 + (long long)nA * n2 * ((ownA ? 1 : 0) + (ownR2 ? 1 : 0));
         // A's own targets: self + forward blocks -> slot 0 (kSplitSlot: part 1)
         __syncwarp();
+        VCHECK(part == 0 || split == 2);
         double2* own = near5 + (part == 0 ? 0 : (int64_t)kSplitSlot * n);
         for (int j = lane; j < nA; j += 32) {
             const double2 t = accAw[j];

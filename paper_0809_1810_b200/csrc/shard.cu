@@ -129,6 +129,7 @@ __device__ __forceinline__ int64_t halo_mult_elem(const ExchangePlan& p, int64_t
     const int s = p.levels - k;
     const int lo2 = (p.lo >> s) >> 1, hi2 = (p.hi >> s) >> 1;  // plane rows of the strip
     const int jy = dir == 0 ? (pack ? lo2 : lo2 - 1) : (pack ? hi2 - 1 : hi2);
+    VCHECK(jy >= 0 && jy < half && coef < p.P);
     const int64_t psz = (int64_t)half * half;
     return (int64_t)p.mult_off[k] * p.P + coef * 4 * psz + plane * psz + (int64_t)jy * half + jx;
 }
@@ -140,6 +141,7 @@ __device__ __forceinline__ int64_t halo_cnt_elem(const ExchangePlan& p, int64_t 
     const int s = p.levels - k;
     const int lo = p.lo >> s, hi = p.hi >> s;
     const int iy = dir == 0 ? (pack ? lo : lo - 2) + row : (pack ? hi - 2 : hi) + row;
+    VCHECK(iy >= 0 && iy < mk && row < 2);
     return (int64_t)p.count_off[k] + (int64_t)iy * mk + ix;
 }
 

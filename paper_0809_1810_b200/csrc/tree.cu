@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(256)
         base = __shfl_sync(0xffffffffu, base, leader);
         if (k >= 0) {
             const int lo = ls[k];
+            VCHECK(lo >= 0 && lo + base + __popc(peers & ((1u << lane) - 1u)) < ls[k + 1]);
             slot[lo + base + __popc(peers & ((1u << lane) - 1u))] = (int)i;
             big |= ls[k + 1] - lo > kFastLeafMax;
         }

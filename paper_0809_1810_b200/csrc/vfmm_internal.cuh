@@ -108,9 +108,39 @@ void note_launches(int k);
 // predecessor instead of adding to the chain (CUDA graphs keep the
 // programmatic edges).  Because every kernel waits before touching memory,
 // stream order semantics are unchanged.
+// Checked / jittered builds (compute-sanitizer is closed on this pool; the
+// substitutes, tools/build_variant.sh + tests/test_checked_build.py):
+//   -DVFMM_CHECKED  VCHECK(cond) traps on a failed bounds / invariant check
+//                   at the kernels' indexing points (a memcheck substitute);
+//   -DVFMM_JITTER   every warp sleeps a pseudo-random 0..2 us at kernel entry
+//                   and at VJITTER() points inside the work loops, reshuffling
+//                   the warp interleaving (a racecheck / synccheck substitute:
+//                   results must stay bitwise identical to the plain build).
+#ifdef VFMM_CHECKED
+#define VCHECK(cond)         \
+    do {                     \
+        if (!(cond)) __trap(); \
+    } while (0)
+#else
+#define VCHECK(cond) \
+    do {             \
+    } while (0)
+#endif
+__device__ __forceinline__ void vjitter_impl() {
+#ifdef VFMM_JITTER
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    unsigned h = (unsigned)(t ^ (t >> 17)) * 2654435761u ^ (blockIdx.x * 40503u + (threadIdx.x >> 5) * 977u);
+    h ^= h >> 13;
+    __nanosleep(h & 2047u);
+#endif
+}
+#define VJITTER() vjitter_impl()
+
 __device__ __forceinline__ void pdl_enter() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    vjitter_impl();
 }
 bool pdl_enabled();  // VFMM_PDL=0 disables the attribute (A/B measurement)
 template <typename... K, typename... A>

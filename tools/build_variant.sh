@@ -9,7 +9,7 @@ out=$root/build/$name
 mkdir -p "$out"
 src=$root/paper_0809_1810_b200/csrc
 objs=()
-for f in capi tree upward subtree m2l downward p2p; do
+for f in capi tree upward subtree m2l downward p2p shard; do
   /usr/local/cuda/bin/nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
     -Xcompiler -fPIC --expt-relaxed-constexpr -Xptxas -v "$@" -c "$src/$f.cu" -o "$out/$f.o" \
     2> "$out/$f.ptxas.log" &
