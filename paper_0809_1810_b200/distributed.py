@@ -136,18 +136,48 @@ def redistribute_owned(x, y, gamma, sigma, ids, domain, levels: int, group=None)
 
 
 def add_halo(owned: torch.Tensor, rows, domain, levels: int, group=None) -> Shard:
-    """Step 2: my first owned leaf row goes to rank-1, my last to rank+1."""
+    """Step 2: my first owned leaf row goes to the strip below, my last to the
+    strip above (grouped NCCL send / recv with the two neighbours).  One host
+    synchronisation: the four message sizes, read together, size the receive
+    buffers; the compaction uses ``nonzero_static`` (no further syncs)."""
     rank, world = dist.get_rank(group), dist.get_world_size(group)
+    bounds = row_bounds(levels, world)
     lo, hi = rows
+    below, above = neighbours(bounds, rank)
+    glob = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)
     r = leaf_rows(owned[1], domain, levels)
-    none = torch.zeros_like(r, dtype=torch.bool)
-    down = (r == lo) & (rank > 0) if hi > lo else none
-    up = (r == hi - 1) & (rank < world - 1) if hi > lo else none
-    idx = torch.cat([torch.nonzero(down).flatten(), torch.nonzero(up).flatten()])
-    dest = torch.cat([torch.full((int(down.sum()),), rank - 1, dtype=torch.int64, device=r.device),
-                      torch.full((int(up.sum()),), rank + 1, dtype=torch.int64, device=r.device)])
-    halo = _exchange(owned[:, idx], dest, world, group)
-    return Shard(torch.cat([owned, halo], dim=1), owned.shape[1], (lo, hi))
+    dev = owned.device
+    m_down = (r == lo) if below is not None else torch.zeros_like(r, dtype=torch.bool)
+    m_up = (r == hi - 1) if above is not None else torch.zeros_like(r, dtype=torch.bool)
+    sizes = torch.stack([m_down.sum(), m_up.sum()]).to(torch.int64)
+    recv_sizes = torch.zeros(2, dtype=torch.int64, device=dev)  # from below, from above
+    ops = []
+    if below is not None:
+        ops += [dist.P2POp(dist.isend, sizes[0:1].contiguous(), glob(below), group),
+                dist.P2POp(dist.irecv, recv_sizes[0:1], glob(below), group)]
+    if above is not None:
+        ops += [dist.P2POp(dist.isend, sizes[1:2].contiguous(), glob(above), group),
+                dist.P2POp(dist.irecv, recv_sizes[1:2], glob(above), group)]
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    n_down, n_up, n_below, n_above = torch.cat([sizes, recv_sizes]).tolist()  # the one sync
+    k = owned.shape[0]
+    send_down = owned[:, torch.nonzero_static(m_down, size=n_down).flatten()].contiguous()
+    send_up = owned[:, torch.nonzero_static(m_up, size=n_up).flatten()].contiguous()
+    from_below = torch.empty((k, n_below), dtype=owned.dtype, device=dev)
+    from_above = torch.empty((k, n_above), dtype=owned.dtype, device=dev)
+    ops = []
+    if below is not None:
+        ops += [dist.P2POp(dist.isend, send_down, glob(below), group),
+                dist.P2POp(dist.irecv, from_below, glob(below), group)]
+    if above is not None:
+        ops += [dist.P2POp(dist.isend, send_up, glob(above), group),
+                dist.P2POp(dist.irecv, from_above, glob(above), group)]
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return Shard(torch.cat([owned, from_below, from_above], dim=1), owned.shape[1], (lo, hi))
 
 
 def redistribute(x, y, gamma, sigma, ids, domain, levels: int, group=None) -> Shard:
@@ -416,14 +446,16 @@ def bench_main(args):
     Setup (untimed, as the single-GPU bench keeps its inputs resident): every
     rank generates the same seeded workload, sends its contiguous 1/N slice of
     the particles to their row-strip owners and exchanges the one-row halos.
-    A step is the sharded evaluate -- PHASE_UP (tree, P2M, M2M; the near field
-    starts), the NCCL all-reduces of the multipole and occupancy pyramids,
-    PHASE_DOWN (M2L, L2L, combine) -- captured in one CUDA graph and replayed
-    with L2 flushed between steps; CUDA events between barriers, max over
-    ranks.  ``e2e``: per step each rank copies its owned particles in from
-    pinned host memory, exchanges the halo (sizes synchronise the host), runs
-    the sharded evaluate and copies its velocities back; wall clock between
-    barriers, max over ranks.
+    A step is the sharded evaluate -- PHASE_UP (tree, strip-local P2M / M2M;
+    the near field starts), the multipole exchange (NCCL allgather of the
+    coarse levels + grouped send / recv of the neighbours' halo rows),
+    PHASE_DOWN (M2L, L2L, L2P + combine) -- captured in one CUDA graph and
+    replayed with L2 flushed between steps; CUDA events between barriers, max
+    over ranks.  ``e2e``: per step each rank copies its owned particles in
+    from pinned host memory, exchanges the particle halo with its neighbours
+    (one host synchronisation for the message sizes), runs the sharded
+    evaluate and copies its velocities back; wall clock between barriers, max
+    over ranks.
     """
     import json
     import time
@@ -453,6 +485,15 @@ def bench_main(args):
     shard = add_halo(owned, rows, dom, cfg.levels)
     backend = CudaShardBackend(dev)
     _, st = evaluate_shard(shard, cfg, dom, backend=backend, counters=True)
+    xstat = {}
+    backend.up(shard, cfg, dom)  # one more step, recording the exchange sizes
+    exchange_multipoles(backend, cfg, world, rank, stats=xstat)
+    backend.down(shard, cfg, dom, counters=False)
+    xs = torch.tensor([xstat.get("recv_bytes", 0), xstat.get("halo_bytes_sent", 0)], dtype=torch.int64,
+                      device=dev)
+    dist.all_reduce(xs, op=dist.ReduceOp.MAX)
+    xstat = {"coarse_levels": f"2..{xstat.get('kc', 1)}" if xstat.get("kc", 1) >= 2 else "none",
+             "max_recv_bytes_per_rank": int(xs[0]), "max_halo_bytes_sent_per_rank": int(xs[1])}
 
     stream = torch.cuda.Stream(dev)
     with torch.cuda.stream(stream):
@@ -546,9 +587,11 @@ def bench_main(args):
             "ms_per_step": float(ms), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "n": w.n, "levels": w.levels, "order": w.order,
-                       "sharding": f"{world} row strips of leaves (+ one-row halos)",
+                       "sharding": f"{world} row strips of leaves (+ one-row particle halos)",
                        "graph": "CUDA graph replay of the sharded evaluate (PHASE_UP, NCCL "
-                                "all-reduce of the multipole/occupancy pyramids, PHASE_DOWN)",
+                                "coarse-level allgather + neighbour halo-row send/recv of the "
+                                "multipoles, PHASE_DOWN)",
+                       "exchange": xstat,
                        "l2": "flushed between steps (256 MiB write)",
                        "m2l_count": st.m2l_count, "near_pair_count": st.near_pair_count},
             "e2e": {"value": w.n / (float(e2e) * 1e-3), "unit": "particle-evals/s",
