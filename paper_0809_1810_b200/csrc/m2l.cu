@@ -494,7 +494,7 @@ __device__ __forceinline__ void tile_pair(const double2* __restrict__ s1, const 
 // whose partial sums are added in group order through shared memory
 // (deterministic); CW > 1 (large grids) shares the window between chunks.
 template <int TN, int CW, int G>
-__global__ void __launch_bounds__(128 * CW * G, CW * G == 1 ? 2 : 1)
+__global__ void __launch_bounds__(128 * CW * G, CW * G <= 2 ? 2 : 1)
     k_m2l_tile(const __grid_constant__ M2LMaps maps, const double2* __restrict__ mult,
                const int* __restrict__ counts, double2* __restrict__ loc, double2* __restrict__ anc,
                int anc_end, int levels, int P, int nchunks, const Tables* __restrict__ T,
@@ -771,13 +771,19 @@ bool launch_tile_tn(const Layout& L, const Tables* T, const double2* mult, const
     static const int cw_env = getenv("VFMM_M2L_CW") ? atoi(getenv("VFMM_M2L_CW")) : 0;
     static const int g_env = getenv("VFMM_M2L_TG") ? atoi(getenv("VFMM_M2L_TG")) : 0;
     const int64_t work = active * nchunks;  // single-chunk CTAs that do work
-    int cw = (work >= 8 * 2 * 148 && nchunks <= 3) ? nchunks : 1;
-    int g = work < 2 * 148 ? 3 : 1;  // sparse grids: shorter warps, more of them
+    // Measured (median t_m2l): config 2 G = 1 / 2 / 3: 0.0686 / 0.0604 / 0.0666 ms;
+    // config 3 G = 2: 0.912 ms, all chunks per CTA (CW = 3): 0.953, G = 1: 0.993.
+    // Two unit groups per tile (8 warps, 2 CTAs / SM = 16 warps / SM at <= 128
+    // registers) by default; three for sparse grids (a rank's strip).
+    int cw = 1;
+    int g = work < 2 * 148 ? 3 : 2;
     if (cw_env >= 1 && cw_env <= 3) cw = cw_env;
-    if (g_env == 1 || g_env == 3) g = g_env;
-    if (g == 3) cw = 1;
+    if (g_env >= 1 && g_env <= 3) g = g_env;
+    if (g > 1) cw = 1;
     if (cw == 1 && g == 1)
         launch_tile_cw<TN, 1, 1>(L, maps, T, mult, counts, loc, anc, ctr, rows, tiles, nchunks, s);
+    else if (g == 2)
+        launch_tile_cw<TN, 1, 2>(L, maps, T, mult, counts, loc, anc, ctr, rows, tiles, nchunks, s);
     else if (g == 3)
         launch_tile_cw<TN, 1, 3>(L, maps, T, mult, counts, loc, anc, ctr, rows, tiles, nchunks, s);
     else if (cw == 2)
