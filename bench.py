@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-workers", type=int, default=0, help="reference arm: worker processes (0 = auto)")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--e2e-depth", type=int, default=3, help="evaluations in flight in the e2e pipeline")
+    ap.add_argument("--e2e-depth", type=int, default=4, help="evaluations in flight in the e2e pipeline")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU sharded path even for one rank (path check)")
     return ap.parse_args()
