@@ -40,6 +40,7 @@ bool g_tables_ready[kMaxDevices];
 struct Resources {
     bool ready = false;
     cudaStream_t far = nullptr;   // far-field chain
+    cudaStream_t far_hi = nullptr;  // high-priority stream (VFMM_PRIO_M2L A/B)
     cudaStream_t near = nullptr;  // near field
     cudaStream_t comp = nullptr;  // compute stream of host-buffer evaluates
     cudaStream_t lsd = nullptr;   // LSD radix branch of the tree build
@@ -164,6 +165,8 @@ Resources* resources_for(int dev) {
         int pf = lo, pn = lo;
         if (e && e[0] == 'f') pf = hi;
         if (e && e[0] == 'n') pn = hi;
+        if (cudaStreamCreateWithPriority(&r.far_hi, cudaStreamNonBlocking, hi) != cudaSuccess)
+            return nullptr;
         if (cudaStreamCreateWithPriority(&r.far, cudaStreamNonBlocking, pf) != cudaSuccess)
             return nullptr;
         if (cudaStreamCreateWithPriority(&r.near, cudaStreamNonBlocking, pn) != cudaSuccess)
@@ -599,6 +602,16 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         rec(2, fs);
     }
     bool fuse = false;  // L2P + combine inside the L2L launch (see below)
+    // VFMM_PRIO_M2L=1 (A/B): M2L and L2L on a high-priority stream, so they
+    // take SM slots as soon as near-field CTAs retire and finish before the
+    // near field; the L2P + combine then runs alone after the join
+    static const bool prio_m2l = getenv("VFMM_PRIO_M2L") && getenv("VFMM_PRIO_M2L")[0] == '1';
+    const bool hp = prio_m2l && overlap && up && down && !far_only;
+    if (hp) {
+        cudaEventRecord(R->lsd_join, fs);
+        cudaStreamWaitEvent(R->far_hi, R->lsd_join, 0);
+        fs = R->far_hi;
+    }
     if (down) {
         if (!up) rec(2, cs);
         // ---- M2L (all levels, one launch) ----
@@ -610,7 +623,7 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         // over the leaf locals fewer on the critical path.  A sharded
         // PHASE_DOWN joins the near field PHASE_UP started (or runs it now).
         static const bool fuse_env = !(getenv("VFMM_FUSE_L2P") && getenv("VFMM_FUSE_L2P")[0] == '0');
-        fuse = fuse_env && !far_only && levels > 2;
+        fuse = fuse_env && !hp && !far_only && levels > 2;
         FusedOut fo{};
         if (fuse && !up) {
             if (overlap) {

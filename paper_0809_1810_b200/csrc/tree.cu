@@ -647,36 +647,35 @@ __global__ void __launch_bounds__(kScanThreads)
     }
 }
 
-// One CTA of 1024 threads for short arrays (the leaf counts of l <= 8: at
-// most 65,537 ints): sub-tiles of 4096 ints scanned in turn with a running
-// carry -- no tile tickets and no look-back chain across CTAs (config 2's
-// 16,385 leaf counts: 3 chained tiles took ~10 us).
+// One CTA of 1024 threads for short arrays (up to 24,576 ints: the leaf
+// counts of l <= 7): every thread loads its contiguous run of c = ceil(n /
+// 1024) <= 24 ints at once (all loads in flight together), one block scan of
+// the run sums, then the writes -- one global round trip instead of one per
+// 4,096-int sub-tile (config 2's 16,385 leaf counts: 3 chained look-back tiles
+// took ~10 us, a sub-tile loop ~13 us under ncu).
 constexpr int kScanOneThreads = 1024;
-constexpr int64_t kScanOneMax = 65537;
+constexpr int kScanOneRun = 24;
+constexpr int64_t kScanOneMax = (int64_t)kScanOneThreads * kScanOneRun;
 __global__ void __launch_bounds__(kScanOneThreads)
     k_scan_one(int* __restrict__ data, int64_t n, const int* __restrict__ skip_flag, int skip_val) {
     pdl_enter();
     if (skip_flag && *skip_flag == skip_val) return;  // leaf-count scan: counting path only
     __shared__ int warp_sums[32];
     __shared__ int total;
-    int carry = 0;
-    for (int64_t base = 0; base < n; base += (int64_t)kScanOneThreads * kScanItems) {
-        const int64_t i0 = base + (int64_t)threadIdx.x * kScanItems;
-        int v[kScanItems];
-        int sum = 0;
+    const int c = (int)((n + kScanOneThreads - 1) / kScanOneThreads);
+    const int64_t i0 = (int64_t)threadIdx.x * c;
+    int v[kScanOneRun];
+    int sum = 0;
 #pragma unroll
-        for (int j = 0; j < kScanItems; ++j) {
-            v[j] = i0 + j < n ? data[i0 + j] : 0;
-            sum += v[j];
-        }
-        int r = carry + block_exclusive_scan(sum, warp_sums, &total);
+    for (int j = 0; j < kScanOneRun; ++j) {
+        v[j] = (j < c && i0 + j < n) ? data[i0 + j] : 0;
+        sum += v[j];
+    }
+    int r = block_exclusive_scan(sum, warp_sums, &total);
 #pragma unroll
-        for (int j = 0; j < kScanItems; ++j) {
-            if (i0 + j < n) data[i0 + j] = r;
-            r += v[j];
-        }
-        carry += total;
-        __syncthreads();
+    for (int j = 0; j < kScanOneRun; ++j) {
+        if (j < c && i0 + j < n) data[i0 + j] = r;
+        r += v[j];
     }
 }
 

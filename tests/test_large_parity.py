@@ -171,3 +171,37 @@ def test_gpu_sampled_error_study_matches_reference(case):
     ref = errors.compare(GL[pre + "fmm"], ref_direct, pos)
     assert abs(rep.max_abs - ref.max_abs) <= REL_TOL * dmax
     assert abs(rep.rms_abs - ref.rms_abs) <= REL_TOL * dmax
+
+
+# ------------------------------------------------------------------ GPU: every path at full size
+VARIANTS = [
+    (2, {"VFMM_SORT": "lsd"}, "device"),          # LSD radix sort path at 2^20
+    (2, {"VFMM_P2P_SYM": "0"}, "device"),         # generic (one-directional) near field
+    (2, {"VFMM_M2L_TILE": "0"}, "device"),        # direct-load M2L kernel
+    (2, {"VFMM_GRAPH_COND": "0"}, "host_graph"),  # public host API, cached graph, no conditionals
+    (2, {}, "host_graph"),                        # public host API, graph with conditional nodes
+    (2, {}, "sharded8"),                          # 8 logical ranks: strip-local upward + exchange
+    (3, {}, "sharded8"),                          # the multi-GPU configuration on 8 logical ranks
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("idx,env,mode", VARIANTS,
+                         ids=[f"config{i}-{m}-{'-'.join(f'{k}={v}' for k, v in e.items()) or 'default'}"
+                              for i, e, m in VARIANTS])
+def test_full_size_paths_match_reference_fmm(idx, env, mode, tmp_path):
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(HERE)
+    out = tmp_path / "v.npz"
+    r = subprocess.run([sys.executable, os.path.join(repo, "tools", "eval_sample.py"), str(idx), str(out), mode],
+                       cwd=repo, env=dict(os.environ, **env), capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    d = np.load(out)
+    pre = f"full/config{idx}/"
+    assert tuple(int(v) for v in d["counts"]) == tuple(int(v) for v in GL[pre + "counts"][:2])
+    vmax = float(GL[pre + "vmax"])
+    err = float(np.abs(d["vel"] - GL[pre + "vel"]).max() / vmax)
+    assert err <= REL_TOL, f"max rel err {err:.3e}"
+    assert abs(float(d["vmax"]) - vmax) <= REL_TOL * vmax
