@@ -354,6 +354,19 @@ def run_ours(args):
             e2e_ms.append(a.elapsed_time(b))
     assert torch.equal(host_out, ref_vel.cpu())
     e2e_latency = statistics.fmean(e2e_ms)
+    # the reference's own signature: evaluate(list[Particle], FmmConfig, Domain)
+    # -> (numpy (N, 2), FmmRunStats), list -> arrays conversion and the numpy
+    # result included (SURVEY.md §8d asks for it beside the array paths)
+    parts = [vf.Particle(float(a), float(b), float(c), float(d))
+             for a, b, c, d in zip(w.x, w.y, w.gamma, w.sigma)]
+    sig_ms = []
+    for i in range(3):
+        t0 = time.perf_counter()
+        vnp, _ = vf.evaluate(parts, cfg, dom)
+        sig_ms.append((time.perf_counter() - t0) * 1e3)
+    assert np.array_equal(vnp, ref_vel.cpu().numpy()) or np.abs(vnp - ref_vel.cpu().numpy()).max() <= 1e-12 * np.abs(vnp).max()
+    sig_ms = statistics.fmean(sig_ms[1:])
+    del parts
     # throughput of a batch of independent evaluations through the async API:
     # HostPipeline keeps --e2e-depth calls in flight (own workspace, stream, pinned
     # output), so step k's H2D / D2H overlap the compute of its neighbours;
@@ -427,7 +440,10 @@ def run_ours(args):
                 "mode": f"evaluate_host_async via HostPipeline(depth={args.e2e_depth}, cached CUDA graph per slot), {k_pipe} steps, "
                         "host wall clock",
                 "latency_ms": e2e_latency,
-                "latency_mode": "one synchronous evaluate_host call (stats on; copies overlapped with the build), CUDA events"},
+                "latency_mode": "one synchronous evaluate_host call (stats on; copies overlapped with the build), CUDA events",
+                "reference_signature_ms": sig_ms,
+                "reference_signature_mode": "evaluate(list[Particle], FmmConfig, Domain) -> (numpy (N, 2), stats): "
+                                            "list -> arrays conversion, copies, evaluate, numpy result; host wall clock"},
         "gpu_launches": int(graph_launches) * args.steps,
         "launches_per_step": {"graph_replay": int(graph_launches), "stream_call": int(launches_per_step)},
         "roofline": {"bound": "fp64", "kernel": "k_p2p (near field)", "achieved": achieved,

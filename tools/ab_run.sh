@@ -1,5 +1,6 @@
-run() { env $1 python bench.py --no-cpu-baseline --e2e-steps 2 > gpurun_out/ab.json 2>gpurun_out/ab.err; python -c "import json; d=json.load(open('gpurun_out/ab.json')); print('$1', round(d['ms_per_step'],4), d['launches_per_step'])" || tail -3 gpurun_out/ab.err; }
-run X=1
-run VFMM_PRIO_M2L=1
-run "VFMM_PRIO_M2L=1 VFMM_NEAR_AFTER=none"
-run X=1
+for v in "X=1" "VFMM_P2P_SPLIT=1" "VFMM_P2P_SPLIT=1 VFMM_P2P_SYM_K=2" "VFMM_P2P_SPLIT=1 VFMM_P2P_SYM_K=3"; do
+  echo "$v: $(env $v python tools/shard_probe.py 2 8 2>&1 | tail -1 | cut -c1-120)"
+done
+for v in "X=1" "VFMM_P2P_SYM_K=2" "VFMM_P2P_SPLIT=1 VFMM_P2P_SYM_K=2"; do
+  echo "$v: $(env $v python tools/phase_probe.py 1 2>&1 | tail -1)"
+done
