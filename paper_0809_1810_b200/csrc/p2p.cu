@@ -182,6 +182,17 @@ __global__ void __launch_bounds__(kP2PWarps * 32, kP2PBlocksPerSM)
 #define VFMM_RING_UNROLL 1
 #endif
 constexpr int kRingUnroll = VFMM_RING_UNROLL;  // steps of a full ring per loop iteration
+#ifndef VFMM_RING4_UNROLL
+#define VFMM_RING4_UNROLL 2
+#endif
+// the same for four residents per lane: two steps per iteration let the
+// scheduler overlap a step's tail with the next one's head (config 2 near
+// field 0.578 -> 0.565 ms, step 0.7335 -> 0.7222 ms; 4: no further gain)
+constexpr int kRing4Unroll = VFMM_RING4_UNROLL;
+#ifndef VFMM_SELF_UNROLL
+#define VFMM_SELF_UNROLL 1
+#endif
+constexpr int kSelfUnroll = VFMM_SELF_UNROLL;  // self-block ring steps per iteration
 
 constexpr int kSymWarps = 8;
 constexpr int kSymExpBytes = (kExpTab2N * 8 + 15) / 16 * 16;
@@ -353,7 +364,7 @@ __device__ __forceinline__ void rotate_ring4(const double (&ax)[4], const double
                                              const double* __restrict__ tab, double (&u)[4],
                                              double (&v)[4]) {
     const int from = ((threadIdx.x & 31) + 1) & (R - 1);
-#pragma unroll 1
+#pragma unroll(kRing4Unroll)
     for (int st = 0; st < R; ++st) {
         double dx[4], dy[4], K[4];
 #pragma unroll
@@ -555,7 +566,7 @@ __device__ __forceinline__ void self_block_sym(double a0x, double a0y, double a0
     double b1x = __shfl_sync(0xffffffffu, a1x, from), b1y = __shfl_sync(0xffffffffu, a1y, from);
     double b1g = __shfl_sync(0xffffffffu, a1g, from);
     double ub0 = 0.0, vb0 = 0.0, ub1 = 0.0, vb1 = 0.0;
-#pragma unroll 1
+#pragma unroll(kSelfUnroll)
     for (int st = 1; st <= 16; ++st) {
         const bool on = st < 16 || lane < 16;
         {  // both chunks' chains together (the second is all ghosts when !two)
@@ -601,7 +612,7 @@ __device__ __forceinline__ void self_block_sym(double a0x, double a0y, double a0
     double qbx = __shfl_sync(0xffffffffu, a1x, home), qby = __shfl_sync(0xffffffffu, a1y, home);
     double qbg = __shfl_sync(0xffffffffu, a1g, home);  // copy Q: particle l + 16
     double pu = 0.0, pv = 0.0, qu = 0.0, qv = 0.0;
-#pragma unroll 1
+#pragma unroll(kSelfUnroll)
     for (int st = 0; st < 16; ++st) {
         const double dx[2] = {a0x - pbx, a0x - qbx}, dy[2] = {a0y - pby, a0y - qby};
         double K[2];

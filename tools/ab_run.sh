@@ -1,6 +1,8 @@
-for v in "X=1" "VFMM_P2P_SPLIT=1" "VFMM_P2P_SPLIT=1 VFMM_P2P_SYM_K=2" "VFMM_P2P_SPLIT=1 VFMM_P2P_SYM_K=3"; do
-  echo "$v: $(env $v python tools/shard_probe.py 2 8 2>&1 | tail -1 | cut -c1-120)"
+for rep in 1 2; do
+for lib in default build/s2/libvfmm.so build/s2r2/libvfmm.so; do
+  if [ "$lib" = default ]; then e=""; else e="VFMM_LIB=$lib"; fi
+  echo "$lib: $(env $e X=1 python tools/phase_probe.py 2 2>&1 | tail -1 | cut -c1-150)"
 done
-for v in "X=1" "VFMM_P2P_SYM_K=2" "VFMM_P2P_SPLIT=1 VFMM_P2P_SYM_K=2"; do
-  echo "$v: $(env $v python tools/phase_probe.py 1 2>&1 | tail -1)"
 done
+echo "c1 default $(python tools/phase_probe.py 1 | tail -1)"
+echo "c1 s2 $(VFMM_LIB=build/s2/libvfmm.so python tools/phase_probe.py 1 | tail -1)"
