@@ -341,6 +341,7 @@ bool make_layout(int64_t n, int levels, int order, Layout* L) {
     L->val_b = take(sizeof(int) * n);
     L->hist = take(L->hist_bytes);
     L->task_scratch = take(sizeof(int) * L->nleaves);
+    L->near_done = take(sizeof(int) * L->nleaves);  // symmetric P2P: writers done per leaf
     L->scan_state = take(L->scan_state_bytes);
     L->src = take(sizeof(Src) * n);
     L->near_uv = take(sizeof(double2) * n * kNearSlotsAlloc);
@@ -501,8 +502,7 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
     // per-phase events only on request; plain stats time the whole call (ev 0 -> 6)
     const bool phases = timed && (flags & VFMM_FLAG_PHASE_TIMES) != 0;
     auto near_field = [&](cudaStream_t st) {  // P2P, then the per-particle near total
-        launch_p2p(L, T, src, ls, ws, ctr, kernel, near_uv, rows, st);
-        launch_near_sum(L, keys, near_uv, rows, ls, ctr, kernel, st);
+        launch_p2p(L, T, src, ls, ws, ctr, kernel, near_uv, rows, keys, st);
     };
     auto rec = [&](int i, cudaStream_t st) {
         if (phases || (timed && (i == 0 || i == 6))) cudaEventRecord(R->ev[i], st);

@@ -31,7 +31,7 @@ __global__ void k_leaf_locals_copy(const double2* __restrict__ loc2, int P, doub
 __global__ void __launch_bounds__(256)
     k_near_sum(const int* __restrict__ keys, double2* __restrict__ near_uv, int64_t n, int levels,
                Rows rows, const int* __restrict__ ls, const Counters* __restrict__ ctr, bool gauss,
-               int sym_enabled, int split) {
+               int sym_enabled, int split, int sym_fused) {
     pdl_enter();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -40,7 +40,9 @@ __global__ void __launch_bounds__(256)
     const int ix = leaf % m, iy = leaf / m;
     if (iy < rows.lo || iy >= rows.hi) return;  // halo particle of a sharded run
     double2 nv;
-    if (sym_enabled && p2p_symmetric(ctr, gauss)) {
+    const bool sym = sym_enabled && p2p_symmetric(ctr, gauss);
+    if (sym && sym_fused) return;  // k_p2p_sym's last writers summed the slots
+    if (sym) {
         double2 t[kNearSlots];
 #pragma unroll
         for (int k = 0; k < kNearSlots; ++k) t[k] = near_uv[(int64_t)k * n + i];
@@ -169,10 +171,11 @@ void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const 
 }
 
 void launch_near_sum(const Layout& L, const int* keys, double2* near_uv, Rows rows,
-                     const int* leaf_starts, const Counters* ctr, int kernel, cudaStream_t s) {
+                     const int* leaf_starts, const Counters* ctr, int kernel, bool sym_fused,
+                     cudaStream_t s) {
     launch_k(k_near_sum, (unsigned)((L.n + 255) / 256), 256, 0, s, 
         keys, near_uv, L.n, L.levels, rows, leaf_starts, ctr, kernel == VFMM_KERNEL_GAUSSIAN,
-        sym_disabled() ? 0 : 1, p2p_sym_split(L, rows));
+        sym_disabled() ? 0 : 1, p2p_sym_split(L, rows), sym_fused ? 1 : 0);
     note_launches(1);
 }
 

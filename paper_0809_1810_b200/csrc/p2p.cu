@@ -642,6 +642,48 @@ __device__ __forceinline__ void self_block_sym(double a0x, double a0y, double a0
     v1 += __shfl_sync(0xffffffffu, pv, home) + qv;
 }
 
+// One write event on owned leaf `lf` (all its writes fenced before): the last
+// of the expected events sums the leaf's near-field slots into slot 0 in
+// k_near_sum's order -- own item(s) (slot 0, slot kSplitSlot), then the
+// reactions of the backward neighbours d_k = (1,0), (-1,1), (0,1), (1,1)
+// (slots 1..4) that exist and hold particles.  The sums read L2 (just written
+// by other SMs: __ldcg).
+__device__ __noinline__ void leaf_written(int lf, int m, int levels, int64_t n, int split,
+                                          const int* __restrict__ ls, double2* near5, int* done) {
+    const int lane = threadIdx.x & 31;
+    const int ix = lf & (m - 1), iy = lf >> levels;
+    bool ok[5];
+    int expected = split;  // own items
+#pragma unroll
+    for (int k = 1; k < 5; ++k) {
+        const int ax = ix - (k == 2 ? -1 : (k == 3 ? 0 : 1)), ay = iy - (k == 1 ? 0 : 1);
+        ok[k] = ax >= 0 && ax < m && ay >= 0 && ls[ay * m + ax + 1] != ls[ay * m + ax];
+        expected += ok[k] ? 1 : 0;
+    }
+    int old = 0;
+    if (lane == 0) old = atomicAdd(&done[lf], 1);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old != expected - 1) return;
+    __threadfence();
+    const int lo = ls[lf], hi = ls[lf + 1];
+    for (int i = lo + lane; i < hi; i += 32) {
+        double2 nv = __ldcg(&near5[i]);
+        if (split == 2) {
+            const double2 t5 = __ldcg(&near5[(int64_t)kSplitSlot * n + i]);
+            nv.x += t5.x;
+            nv.y += t5.y;
+        }
+#pragma unroll
+        for (int k = 1; k < 5; ++k)
+            if (ok[k]) {
+                const double2 t = __ldcg(&near5[(int64_t)k * n + i]);
+                nv.x += t.x;
+                nv.y += t.y;
+            }
+        near5[i] = nv;
+    }
+}
+
 #ifdef VFMM_SYM_MAXNREG
 #define VFMM_SYM_BOUNDS __maxnreg__(VFMM_SYM_MAXNREG)
 #else
@@ -652,7 +694,8 @@ __global__ void VFMM_SYM_BOUNDS
     k_p2p_sym(const Src* __restrict__ src, const int* __restrict__ ls, Counters* __restrict__ ctr,
               int levels, int64_t n, Rows rows, const Tables* __restrict__ T,
               double2* __restrict__ near5, unsigned long long* __restrict__ pairs,
-              int items_per_warp, int item_base, int nitems, int split, GraphCond generic_cond) {
+              int items_per_warp, int item_base, int nitems, int split, GraphCond generic_cond,
+              int* __restrict__ done) {
     pdl_enter();
     // a captured graph runs the generic near-field chain (an IF node after
     // this kernel) only when the symmetric mode does not apply
@@ -693,6 +736,7 @@ __global__ void VFMM_SYM_BOUNDS
         // forward stream S = R1 (leaf (cx+1, cy)) ++ R2 (leaves cx-1..cx+1 of row
         // cy+1, one contiguous range of the sorted sources)
         int r1 = 0, n1 = 0, r2 = 0, n2 = 0, b3 = 0, b4 = 0;
+        int x2lo = 0, x2hi = 0;  // leaves [x2lo, x2hi) of row cy + 1 in the stream
         bool ownR2 = false;
         if (ownA && cx + 1 < m && part == 0) {
             r1 = ls[leaf + 1];
@@ -709,6 +753,8 @@ __global__ void VFMM_SYM_BOUNDS
                 const int e0 = split == 1 || part == 1 ? x1 + 1 : cx;  // leaves [s0, e0) of row cy + 1
                 r2 = ls[row + s0];
                 n2 = ls[row + e0] - r2;
+                x2lo = s0;
+                x2hi = e0;
             }
         }
         if (!ownA && n2 == 0) continue;
@@ -828,6 +874,20 @@ __global__ void VFMM_SYM_BOUNDS
             own[loA + j] = make_double2(t.x * kInv2Pi, t.y * kInv2Pi);
         }
         __syncwarp();
+        if (done) {
+            // The last writer of an owned leaf adds its slots (the order of
+            // k_near_sum, which then has nothing to do): every leaf this item
+            // wrote into counts one write event; the expected number is the
+            // leaf's own items plus its existing non-empty backward neighbours.
+            __threadfence();
+            if (ownA) leaf_written(leaf, m, levels, n, split, ls, near5, done);
+            if (n1 > 0) leaf_written(leaf + 1, m, levels, n, split, ls, near5, done);
+            if (ownR2 && n2 > 0)
+                for (int x = x2lo; x < x2hi; ++x) {
+                    const int lf = (cy + 1) * m + x;
+                    if (ls[lf + 1] > ls[lf]) leaf_written(lf, m, levels, n, split, ls, near5, done);
+                }
+        }
     }
     if (lane == 0 && my_pairs) atomicAdd(pairs, (unsigned long long)my_pairs);
 }
@@ -943,7 +1003,21 @@ int p2p_sym_split(const Layout& L, Rows rows) {
 }
 
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
-                char* ws, Counters* ctr, int kernel, double2* near_uv, Rows rows, cudaStream_t s) {
+                char* ws, Counters* ctr, int kernel, double2* near_uv, Rows rows, const int* keys,
+                cudaStream_t s) {
+    // VFMM_SYM_FUSED_SUM=1 (A/B): the symmetric kernel's last writers sum each
+    // leaf's slots instead of k_near_sum.  Measured slower (config 2 step
+    // 0.7222 -> 0.7355 ms: the fences, counters and per-leaf sums at item
+    // ends cost the near field more than the separate 20 us pass).
+    static const bool fused_env = getenv("VFMM_SYM_FUSED_SUM") && getenv("VFMM_SYM_FUSED_SUM")[0] == '1';
+    const bool fused = fused_env && !sym_disabled();
+    int* done = fused ? (int*)(ws + L.near_done) : nullptr;
+    auto generic_chain = [&](cudaStream_t st) {
+        launch_p2p_generic(L, T, src, leaf_starts, ws, ctr, kernel, near_uv, rows, st);
+    };
+    auto near_sum = [&](cudaStream_t st) {
+        launch_near_sum(L, keys, near_uv, rows, leaf_starts, ctr, kernel, fused, st);
+    };
     const bool g = kernel == VFMM_KERNEL_GAUSSIAN;
     // Stream launches: the generic kernel and its task list go first: in
     // symmetric mode they return at once, and that ~10 us head start lets P2M
@@ -955,7 +1029,7 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
     // VFMM_GRAPH_COND=2: the conditional node for the sort path only (A/B)
     static const bool cond_near = !(getenv("VFMM_GRAPH_COND") && getenv("VFMM_GRAPH_COND")[0] == '2');
     const GraphCond gc = (sym_disabled() || !cond_near) ? GraphCond{} : graph_cond_create(s);
-    if (!gc.on) launch_p2p_generic(L, T, src, leaf_starts, ws, ctr, kernel, near_uv, rows, s);
+    if (!gc.on) generic_chain(s);
     // symmetric kernel: runs instead when the device-side mode check allows it
     // Leaf items per warp: enough CTAs for ~4 waves of 2 CTAs per SM (so
     // the far chain finds free slots and the tail is short), otherwise as
@@ -1000,17 +1074,22 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
     if (!sym_disabled() && sblocks > 0) {
         launch_k(sfn, sblocks, kSymWarps * 32, kSymSmem, s, src, leaf_starts, ctr, L.levels, L.n, rows, T,
                                                       near_uv, &ctr->near_pairs, ks, item_base,
-                 (int)sym_items, split, gc);
+                 (int)sym_items, split, gc, done);
         note_launches(1);
     } else if (gc.on) {  // no symmetric kernel to set the condition: run the chain
-        launch_p2p_generic(L, T, src, leaf_starts, ws, ctr, kernel, near_uv, rows, s);
+        generic_chain(s);
+        near_sum(s);
         return;
     }
-    if (gc.on) {
+    if (gc.on) {  // the generic chain only when the symmetric mode does not apply
         cudaGraphNode_t node = nullptr;
         cudaStream_t bs = graph_cond_begin(s, gc, &node);
-        launch_p2p_generic(L, T, src, leaf_starts, ws, ctr, kernel, near_uv, rows, bs);
+        generic_chain(bs);
+        if (fused) near_sum(bs);  // (the symmetric kernel summed its own slots)
         graph_cond_end(s, bs, node);
+        if (!fused) near_sum(s);
+    } else {
+        near_sum(s);
     }
 }
 

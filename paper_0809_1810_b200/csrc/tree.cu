@@ -817,8 +817,8 @@ void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream
 // states, leaf counts, slot fills and LSD histograms; memset nodes would break
 // the programmatic-launch chain).
 struct ZeroRegions {
-    int* p[4];
-    int64_t n[4];  // ints
+    int* p[5];
+    int64_t n[5];  // ints
 };
 struct ProbeArgs {
     const double *x, *y;
@@ -842,7 +842,7 @@ __global__ void k_zero_regions(ZeroRegions z, ProbeArgs pa, Counters* ctr) {
     const int64_t t0 = (int64_t)(blockIdx.x - 1) * blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)(gridDim.x - 1) * blockDim.x;
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < 5; ++r)
         for (int64_t i = t0; i < z.n[r]; i += stride) z.p[r][i] = 0;
 }
 
@@ -865,9 +865,9 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     int* fill = (int*)(ws + L.task_scratch);  // free until the task counts
     int* ghist = (int*)(ws + L.hist);         // LSD: passes x B global digit counts, tickets, look-back
     {
-        ZeroRegions z{{(int*)(ws + L.scan_state), ls, fill, ghist},
+        ZeroRegions z{{(int*)(ws + L.scan_state), ls, fill, ghist, (int*)(ws + L.near_done)},
                       {(int64_t)(L.scan_state_bytes / sizeof(int)), (int64_t)L.nleaves + 1,
-                       (int64_t)L.nleaves, (int64_t)(L.hist_bytes / sizeof(int))}};
+                       (int64_t)L.nleaves, (int64_t)(L.hist_bytes / sizeof(int)), (int64_t)L.nleaves}};
         const ProbeArgs pa{x, y, L.n, xmin, ymin, side, L.levels, force_lsd()};
         launch_k(k_zero_regions, 297, 256, 0, s, z, pa, ctr);
         note_launches(1);

@@ -75,7 +75,7 @@ struct Layout {
     int levels, order, P;  // P = order + 1
     int digit_bits, passes, wc, nchunks;
     size_t nleaves;
-    size_t key_a, key_b, val_a, val_b, hist, task_scratch, scan_state, src, near_uv, leaf_starts, anc,
+    size_t key_a, key_b, val_a, val_b, hist, task_scratch, near_done, scan_state, src, near_uv, leaf_starts, anc,
         counts, mult, loc, leaf_loc, tasks, stage, counters, total;
     size_t scan_state_tiles, scan_state_bytes, hist_bytes;  // per scan instance: 1 ticket + tiles
     size_t level_cell_off[VFMM_LEVELS_CAP + 2];  // cells before level k (k>=2) in mult/loc
@@ -224,8 +224,10 @@ struct FusedOut {
 void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc,
                 const double2* anc, Rows rows, const FusedOut& fo, cudaStream_t s);
 int p2p_targets_per_lane();  // 1 or 2 (env VFMM_P2P_TPT, default 1)
+// the near field: P2P kernels and the per-particle near-field totals (slot 0)
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
-                char* ws, Counters* ctr, int kernel, double2* near_uv, Rows rows, cudaStream_t s);
+                char* ws, Counters* ctr, int kernel, double2* near_uv, Rows rows, const int* keys,
+                cudaStream_t s);
 bool sym_disabled();  // env VFMM_P2P_SYM=0 forces the generic near-field kernel
 // symmetric P2P work items per leaf: 2 (the forward stream split in two
 // items, the leaf's own sums of the second in slot kSplitSlot) when the
@@ -236,8 +238,11 @@ void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const 
                         double ymin, double side, double* u, double* v, Rows rows,
                         cudaStream_t s);
 // near-field total per particle into slot 0 (after the near-field kernels)
+// sym_fused: the symmetric kernel sums its slots itself (k_near_sum then
+// only serves the generic kernel)
 void launch_near_sum(const Layout& L, const int* keys, double2* near_uv, Rows rows,
-                     const int* leaf_starts, const Counters* ctr, int kernel, cudaStream_t s);
+                     const int* leaf_starts, const Counters* ctr, int kernel, bool sym_fused,
+                     cudaStream_t s);
 void launch_eval_at(const Layout& L, const Tables* T, const double* tx, const double* ty,
                     int64_t m, const Src* src, const int* leaf_starts, const double2* loc,
                     double xmin, double ymin, double side, int kernel, double* u, double* v,
