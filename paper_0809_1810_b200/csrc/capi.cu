@@ -341,6 +341,7 @@ bool make_layout(int64_t n, int levels, int order, Layout* L) {
     L->val_b = take(sizeof(int) * n);
     L->hist = take(L->hist_bytes);
     L->task_scratch = take(sizeof(int) * L->nleaves);
+    L->fill = take(sizeof(int) * L->nleaves);
     L->near_done = take(sizeof(int) * L->nleaves);  // symmetric P2P: writers done per leaf
     L->scan_state = take(L->scan_state_bytes);
     L->src = take(sizeof(Src) * n);
@@ -546,9 +547,8 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
         // ---- build: binning, stable sort, pack, leaf starts, occupancy, tasks ----
         launch_init_counters(ctr, cs);
         launch_build(L, x, y, gamma, kernel == VFMM_KERNEL_GAUSSIAN ? sigma : nullptr, xmin, ymin,
-                     side, ws, ctr, cs, &keys, &perm, gs_ready, sigma_scalar ? 0 : 1,
+                     side, ws, ctr, cs, &keys, &perm, gs_ready, sigma_scalar ? 0 : 1, rows,
                      lsd_branch ? R->lsd : nullptr, R->lsd_fork, R->lsd_join);
-        launch_counts_tasks(L, ws, ctr, !far_only, rows, kernel == VFMM_KERNEL_GAUSSIAN, cs);
         rec(1, cs);
         // Overlap: the far-field chain and the near field run on two streams
         // (equal priority, see resources_for); P2P CTAs are short-lived, so

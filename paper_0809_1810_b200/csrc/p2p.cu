@@ -195,7 +195,13 @@ constexpr int kRing4Unroll = VFMM_RING4_UNROLL;
 constexpr int kSelfUnroll = VFMM_SELF_UNROLL;  // self-block ring steps per iteration
 
 constexpr int kSymWarps = 8;
+// VFMM_SYM_TAB_GLOBAL: the exp table is read from global memory through L1
+// (no per-CTA staging; one L1 copy per SM shared by every CTA it runs)
+#ifdef VFMM_SYM_TAB_GLOBAL
+constexpr int kSymExpBytes = 0;
+#else
 constexpr int kSymExpBytes = (kExpTab2N * 8 + 15) / 16 * 16;
+#endif
 constexpr int kSymSmem = kSymExpBytes + kSymWarps * kSymMaxLeaf * 16;  // 76 KB
 
 __device__ __forceinline__ void load_lane(const Src* __restrict__ src, int lo, int cnt, int lane,
@@ -708,11 +714,15 @@ __global__ void VFMM_SYM_BOUNDS
     if ((int64_t)blockIdx.x * kSymWarps * items_per_warp >= nitems) return;  // spare CTA
     // dynamic shared memory: exp table | per-warp accumulators of the item's leaf
     extern __shared__ __align__(16) unsigned char sym_smem[];
-    double* sexp = reinterpret_cast<double*>(sym_smem);
     double2* accA = reinterpret_cast<double2*>(sym_smem + kSymExpBytes);
+#ifdef VFMM_SYM_TAB_GLOBAL
+    const double* tab = T->exp2tab2 + (kExpTab2N - 1);
+#else
+    double* sexp = reinterpret_cast<double*>(sym_smem);
     for (int i = threadIdx.x; i < kExpTab2N; i += blockDim.x) sexp[i] = T->exp2tab2[i];
     const double* tab = sexp + (kExpTab2N - 1);  // 2^(n/128) at tab[n], n <= 0
     __syncthreads();
+#endif
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double2* accAw = accA + warp * kSymMaxLeaf;
     const SymExp q2 = sym_exp(GAUSS ? src[0].q2 : -1.0);  // uniform core size

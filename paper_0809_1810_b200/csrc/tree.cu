@@ -130,16 +130,104 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Occupancy of every cell of every level (level 0 first) from leaf_starts
+// (Tree.counts, quadtree.py:126-134):
+// a level-k cell covers 2^(l-k) leaf rows, each a contiguous leaf range.
+// Leaf cells also emit their P2P task count ceil(count / chunk).
+struct CountsArgs {
+    int ctas;  // CTAs of 256 threads doing this work (k_bin_scatter's first CTAs)
+    int levels;
+    int64_t total_threads;
+    int chunk;
+    Rows rows;
+    int* counts;
+    int* ntask;
+};
+__device__ __forceinline__ void counts_tasks_body(int64_t t, const int* __restrict__ ls,
+                                                  const CountsArgs& a, Counters* __restrict__ ctr) {
+    // A cell of level k spans s = 2^(levels-k) leaf rows; g = min(32, s)
+    // lanes split its rows and add their partial counts by xor shuffles (the
+    // coarse cells were serial 32..128-row loops).  Thread ranges per level:
+    // 4^k g_k threads, each level's range aligned to its g.
+    const int levels = a.levels;
+    const Rows rows = a.rows;
+    int k = 0, g = 1;
+    int64_t off = 0, cell_off = 0;
+    for (;;) {
+        const int s = 1 << (levels - k);
+        g = s < 32 ? s : 32;
+        const int64_t nt = (1ll << (2 * k)) * g;
+        if (t < off + nt || k == levels) break;
+        off += nt;
+        cell_off += 1ll << (2 * k);
+        ++k;
+    }
+    const bool valid = t < a.total_threads;
+    const int64_t cell = valid ? (t - off) / g : 0;
+    const int sub = valid ? (int)((t - off) % g) : 0;
+    const int mk = 1 << k;
+    const int ix = (int)(cell % mk), iy = (int)(cell / mk);
+    const int m = 1 << levels;
+    const int s = 1 << (levels - k);
+    // only owned leaf rows are counted, so per-rank pyramids of a sharded run
+    // are disjoint and their sum is the global occupancy
+    const int r0 = max(iy * s, rows.lo), r1 = min((iy + 1) * s, rows.hi);
+    int c = 0;
+    if (valid)
+        for (int r = r0 + sub; r < r1; r += g) {
+            const int64_t row = (int64_t)r * m;
+            c += ls[row + (int64_t)(ix + 1) * s] - ls[row + (int64_t)ix * s];
+        }
+    // every lane runs the same shuffles; a lane adds only within its g-group
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const int v = __shfl_xor_sync(0xffffffffu, c, o);
+        if (o < g) c += v;
+    }
+    int full = 0;
+    if (valid && sub == 0) {
+        a.counts[cell_off + cell] = c;
+        // only leaves of the owned row strip get near-field tasks
+        if (k == levels) {
+            a.ntask[cell] = (iy >= rows.lo && iy < rows.hi) ? (c + a.chunk - 1) / a.chunk : 0;
+            full = ls[cell + 1] - ls[cell];  // owned and halo rows (the symmetric P2P touches both)
+        }
+    }
+    // largest leaf: one atomic per warp
+    full = __reduce_max_sync(0xffffffffu, full);
+    if ((threadIdx.x & 31) == 0 && full > 0) atomicMax(&ctr->max_leaf, full);
+}
+
+// The same after the LSD radix path (k_bin_scatter did it on the counting
+// path; a big-leaf fallback recomputes identical values).
+__global__ void __launch_bounds__(256)
+    k_counts_tasks(const int* __restrict__ ls, CountsArgs a, Counters* __restrict__ ctr) {
+    pdl_enter();
+    if (!ctr->sort_fallback) return;
+    counts_tasks_body((int64_t)blockIdx.x * blockDim.x + threadIdx.x, ls, a, ctr);
+}
+
 // Index i -> a slot of its leaf: one atomic per (warp, leaf) group, lanes
 // ranked in index order inside the group.
+//
+// The first ca.ctas CTAs instead compute the occupancy pyramid and task
+// counts (counts_tasks_body): leaf_starts is final once the scan ran, so the
+// counts leave the critical chain (they were a separate launch after the
+// record pack).
 __global__ void __launch_bounds__(256)
     k_bin_scatter(const int* __restrict__ key, int64_t n, const int* __restrict__ ls,
-                  int* __restrict__ fill, int* __restrict__ slot, Counters* __restrict__ ctr) {
+                  int* __restrict__ fill, int* __restrict__ slot, Counters* __restrict__ ctr,
+                  CountsArgs ca) {
     pdl_enter();
     if (ctr->sort_fallback == kSortLsdProbe) return;
+    if ((int)blockIdx.x < ca.ctas) {
+        counts_tasks_body((int64_t)blockIdx.x * blockDim.x + threadIdx.x, ls, ca, ctr);
+        return;
+    }
     const int lane = threadIdx.x & 31;
     bool big = false;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned nb = gridDim.x - ca.ctas;
+    for (int64_t i0 = (int64_t)(blockIdx.x - ca.ctas) * blockDim.x; i0 < n; i0 += (int64_t)nb * blockDim.x) {
         const int64_t i = i0 + threadIdx.x;
         const int k = i < n ? key[i] : -1;
         const unsigned peers = __match_any_sync(0xffffffffu, k);
@@ -648,34 +736,88 @@ __global__ void __launch_bounds__(kScanThreads)
 }
 
 // One CTA of 1024 threads for short arrays (up to 24,576 ints: the leaf
-// counts of l <= 7): every thread loads its contiguous run of c = ceil(n /
-// 1024) <= 24 ints at once (all loads in flight together), one block scan of
-// the run sums, then the writes -- one global round trip instead of one per
-// 4,096-int sub-tile (config 2's 16,385 leaf counts: 3 chained look-back tiles
-// took ~10 us, a sub-tile loop ~13 us under ncu).
+// counts of l <= 7).  The array is read as J <= 6 stripes of 1,024 int4
+// (thread t holds int4 t of every stripe: every warp load is 512 contiguous
+// bytes, all loads in flight together), the J stripe scans run together
+// (one shuffle ladder over J values), and the results go back to the same
+// int4 slots.  One global round trip, fully coalesced (the previous
+// contiguous-run-per-thread layout made every load a 32-sector request:
+// 11.3 us for config 2's 16,385 leaf counts under ncu, lg_throttle stalls).
 constexpr int kScanOneThreads = 1024;
-constexpr int kScanOneRun = 24;
-constexpr int64_t kScanOneMax = (int64_t)kScanOneThreads * kScanOneRun;
+constexpr int kScanOneJ = 6;
+constexpr int64_t kScanOneMax = (int64_t)kScanOneThreads * 4 * kScanOneJ;
 __global__ void __launch_bounds__(kScanOneThreads)
     k_scan_one(int* __restrict__ data, int64_t n, const int* __restrict__ skip_flag, int skip_val) {
     pdl_enter();
     if (skip_flag && *skip_flag == skip_val) return;  // leaf-count scan: counting path only
-    __shared__ int warp_sums[32];
-    __shared__ int total;
-    const int c = (int)((n + kScanOneThreads - 1) / kScanOneThreads);
-    const int64_t i0 = (int64_t)threadIdx.x * c;
-    int v[kScanOneRun];
-    int sum = 0;
+    __shared__ int wsum[kScanOneJ][32];
+    __shared__ int stripe_base[kScanOneJ];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int64_t n4 = (n + 3) >> 2;
+    const bool vec = (reinterpret_cast<uintptr_t>(data) & 15) == 0;
+    int4 q[kScanOneJ];
+    int s[kScanOneJ], incl[kScanOneJ];
 #pragma unroll
-    for (int j = 0; j < kScanOneRun; ++j) {
-        v[j] = (j < c && i0 + j < n) ? data[i0 + j] : 0;
-        sum += v[j];
+    for (int j = 0; j < kScanOneJ; ++j) {
+        const int64_t i4 = (int64_t)j * kScanOneThreads + t;
+        const int64_t e = i4 * 4;
+        if (vec && e + 4 <= n) {
+            q[j] = __ldcg(reinterpret_cast<const int4*>(data) + i4);
+        } else {
+            q[j].x = e < n ? __ldcg(data + e) : 0;
+            q[j].y = e + 1 < n ? __ldcg(data + e + 1) : 0;
+            q[j].z = e + 2 < n ? __ldcg(data + e + 2) : 0;
+            q[j].w = e + 3 < n ? __ldcg(data + e + 3) : 0;
+        }
+        s[j] = q[j].x + q[j].y + q[j].z + q[j].w;
+        incl[j] = s[j];
     }
-    int r = block_exclusive_scan(sum, warp_sums, &total);
 #pragma unroll
-    for (int j = 0; j < kScanOneRun; ++j) {
-        if (j < c && i0 + j < n) data[i0 + j] = r;
-        r += v[j];
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+        for (int j = 0; j < kScanOneJ; ++j) {
+            const int u = __shfl_up_sync(0xffffffffu, incl[j], o);
+            if (lane >= o) incl[j] += u;
+        }
+    }
+    if (lane == 31)
+#pragma unroll
+        for (int j = 0; j < kScanOneJ; ++j) wsum[j][warp] = incl[j];
+    __syncthreads();
+    if (warp < kScanOneJ) {  // warp j scans stripe j's 32 warp sums
+        const int w = wsum[warp][lane];
+        int wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += u;
+        }
+        wsum[warp][lane] = wi - w;
+        if (lane == 31) stripe_base[warp] = wi;  // stripe total (made a prefix below)
+    }
+    __syncthreads();
+    int base = 0;
+#pragma unroll
+    for (int j = 0; j < kScanOneJ; ++j) {
+        const int tot = stripe_base[j];
+        const int64_t i4 = (int64_t)j * kScanOneThreads + t;
+        const int64_t e = i4 * 4;
+        if (i4 < n4) {
+            int4 r;
+            r.x = base + wsum[j][warp] + incl[j] - s[j];
+            r.y = r.x + q[j].x;
+            r.z = r.y + q[j].y;
+            r.w = r.z + q[j].z;
+            if (vec && e + 4 <= n) {
+                reinterpret_cast<int4*>(data)[i4] = r;
+            } else {
+                if (e < n) data[e] = r.x;
+                if (e + 1 < n) data[e + 1] = r.y;
+                if (e + 2 < n) data[e + 2] = r.z;
+                if (e + 3 < n) data[e + 3] = r.w;
+            }
+        }
+        base += tot;
     }
 }
 
@@ -697,66 +839,6 @@ __global__ void k_leaf_starts(const int* __restrict__ keys, int64_t n, int nleav
         }
         ls[k] = (int)lo;
     }
-}
-
-// Occupancy of every cell of every level (level 0 first) from leaf_starts
-// (Tree.counts, quadtree.py:126-134):
-// a level-k cell covers 2^(l-k) leaf rows, each a contiguous leaf range.
-// Leaf cells also emit their P2P task count ceil(count / chunk).
-__global__ void k_counts_tasks(const int* __restrict__ ls, int levels, int64_t total_threads,
-                               int chunk, Rows rows, int* __restrict__ counts,
-                               int* __restrict__ ntask, Counters* __restrict__ ctr) {
-    pdl_enter();
-    // A cell of level k spans s = 2^(levels-k) leaf rows; g = min(32, s)
-    // lanes split its rows and add their partial counts by xor shuffles (the
-    // coarse cells were serial 32..128-row loops).  Thread ranges per level:
-    // 4^k g_k threads, each level's range aligned to its g.
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int k = 0, g = 1;
-    int64_t off = 0, cell_off = 0;
-    for (;;) {
-        const int s = 1 << (levels - k);
-        g = s < 32 ? s : 32;
-        const int64_t nt = (1ll << (2 * k)) * g;
-        if (t < off + nt || k == levels) break;
-        off += nt;
-        cell_off += 1ll << (2 * k);
-        ++k;
-    }
-    const bool valid = t < total_threads;
-    const int64_t cell = valid ? (t - off) / g : 0;
-    const int sub = valid ? (int)((t - off) % g) : 0;
-    const int mk = 1 << k;
-    const int ix = (int)(cell % mk), iy = (int)(cell / mk);
-    const int m = 1 << levels;
-    const int s = 1 << (levels - k);
-    // only owned leaf rows are counted, so per-rank pyramids of a sharded run
-    // are disjoint and their sum is the global occupancy
-    const int r0 = max(iy * s, rows.lo), r1 = min((iy + 1) * s, rows.hi);
-    int c = 0;
-    if (valid)
-        for (int r = r0 + sub; r < r1; r += g) {
-            const int64_t row = (int64_t)r * m;
-            c += ls[row + (int64_t)(ix + 1) * s] - ls[row + (int64_t)ix * s];
-        }
-    // every lane runs the same shuffles; a lane adds only within its g-group
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const int v = __shfl_xor_sync(0xffffffffu, c, o);
-        if (o < g) c += v;
-    }
-    int full = 0;
-    if (valid && sub == 0) {
-        counts[cell_off + cell] = c;
-        // only leaves of the owned row strip get near-field tasks
-        if (k == levels) {
-            ntask[cell] = (iy >= rows.lo && iy < rows.hi) ? (c + chunk - 1) / chunk : 0;
-            full = ls[cell + 1] - ls[cell];  // owned and halo rows (the symmetric P2P touches both)
-        }
-    }
-    // largest leaf: one atomic per warp
-    full = __reduce_max_sync(0xffffffffu, full);
-    if ((threadIdx.x & 31) == 0 && full > 0) atomicMax(&ctr->max_leaf, full);
 }
 
 __global__ void k_tasks_fill(const int* __restrict__ ls, int levels, int chunk, Rows rows,
@@ -846,11 +928,30 @@ __global__ void k_zero_regions(ZeroRegions z, ProbeArgs pa, Counters* ctr) {
         for (int64_t i = t0; i < z.n[r]; i += stride) z.p[r][i] = 0;
 }
 
+// Occupancy pyramid + task counts: 4^k cells x min(32, 2^(levels-k)) lanes per level.
+CountsArgs counts_args(const Layout& L, char* ws, Rows rows) {
+    int64_t total = 0;
+    for (int k = 0; k <= L.levels; ++k) {
+        const int64_t rows_k = 1ll << (L.levels - k);
+        total += (1ll << (2 * k)) * (rows_k < 32 ? rows_k : 32);
+    }
+    CountsArgs a;
+    a.ctas = (int)grid_for(total, 256);
+    a.levels = L.levels;
+    a.total_threads = total;
+    a.chunk = 32 * p2p_targets_per_lane();
+    a.rows = rows;
+    a.counts = (int*)(ws + L.counts);
+    a.ntask = (int*)(ws + L.task_scratch);
+    return a;
+}
+
 void launch_build(const Layout& L, const double* x, const double* y, const double* g,
                   const double* sigma, double xmin, double ymin, double side, char* ws,
                   Counters* ctr, cudaStream_t s, int** keys_out, int** perm_out,
-                  cudaEvent_t gs_ready, int sigma_stride, cudaStream_t lsd_stream,
+                  cudaEvent_t gs_ready, int sigma_stride, Rows rows, cudaStream_t lsd_stream,
                   cudaEvent_t lsd_fork, cudaEvent_t lsd_join) {
+    const CountsArgs ca = counts_args(L, ws, rows);
     int* kbuf[2] = {(int*)(ws + L.key_a), (int*)(ws + L.key_b)};
     int* vbuf[2] = {(int*)(ws + L.val_a), (int*)(ws + L.val_b)};
     const int bits = L.digit_bits;
@@ -862,7 +963,7 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     int* fkeys = kbuf[L.passes & 1];  // final buffers of either path (vfmm_layout_of)
     int* fperm = vbuf[L.passes & 1];
     Src* src = (Src*)(ws + L.src);
-    int* fill = (int*)(ws + L.task_scratch);  // free until the task counts
+    int* fill = (int*)(ws + L.fill);          // per-leaf slot cursors of k_bin_scatter
     int* ghist = (int*)(ws + L.hist);         // LSD: passes x B global digit counts, tickets, look-back
     {
         ZeroRegions z{{(int*)(ws + L.scan_state), ls, fill, ghist, (int*)(ws + L.near_done)},
@@ -879,8 +980,8 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     launch_scan_i32(ls, (int64_t)L.nleaves + 1, state(L.passes + 1), s, nullptr, false,
                     &ctr->sort_fallback, kSortLsdProbe);
     int* slot = vbuf[(L.passes + 1) & 1];
-    launch_k(k_bin_scatter, small_grid(L.n, 2368), 256, 0, s, kbuf[(L.passes + 1) & 1], L.n, ls, fill,
-                                                    slot, ctr);
+    launch_k(k_bin_scatter, small_grid(L.n, 2368) + ca.ctas, 256, 0, s, kbuf[(L.passes + 1) & 1], L.n,
+             ls, fill, slot, ctr, ca);
     note_launches(1);
     // The path choice is final after k_bin_scatter (a leaf > 128 switches to
     // LSD there).  With a side stream the LSD kernels -- which return at once
@@ -932,6 +1033,8 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     launch_k(k_leaf_starts, small_grid((int64_t)L.nleaves + 1, 2368), 256, 0, ls_s, fkeys, L.n,
              (int)L.nleaves, ls, ctr);
     note_launches(1);
+    launch_k(k_counts_tasks, (unsigned)ca.ctas, 256, 0, ls_s, (const int*)ls, ca, ctr);
+    note_launches(1);
     if (lsd_cond.on) graph_cond_end(s, ls_s, lsd_node);
     if (branch) {
         cudaEventRecord(lsd_join, lsd_stream);
@@ -944,24 +1047,6 @@ void launch_leaf_starts(const int* sorted_keys, int64_t n, int nleaves, int* lea
     launch_k(k_leaf_starts, grid_for((int64_t)nleaves + 1, 256), 256, 0, s, sorted_keys, n, nleaves, leaf_starts,
                                                         nullptr);
     note_launches(1);
-}
-
-void launch_counts_tasks(const Layout& L, char* ws, Counters* ctr, bool tasks, Rows rows,
-                         bool gauss, cudaStream_t s) {
-    const int* ls = (const int*)(ws + L.leaf_starts);
-    int* counts = (int*)(ws + L.counts);
-    int* nt = (int*)(ws + L.task_scratch);
-    int64_t total = 0;  // threads: 4^k cells x min(32, 2^(levels-k)) lanes per level
-    for (int k = 0; k <= L.levels; ++k) {
-        const int64_t rows_k = 1ll << (L.levels - k);
-        total += (1ll << (2 * k)) * (rows_k < 32 ? rows_k : 32);
-    }
-    const int chunk = 32 * p2p_targets_per_lane();
-    launch_k(k_counts_tasks, grid_for(total, 256), 256, 0, s, ls, L.levels, total, chunk, rows, counts,
-                                                       nt, ctr);
-    note_launches(1);
-    (void)tasks;
-    (void)gauss;
 }
 
 // Near-field task list of the generic kernel (launched on the near stream

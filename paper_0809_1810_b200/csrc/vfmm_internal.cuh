@@ -75,7 +75,7 @@ struct Layout {
     int levels, order, P;  // P = order + 1
     int digit_bits, passes, wc, nchunks;
     size_t nleaves;
-    size_t key_a, key_b, val_a, val_b, hist, task_scratch, near_done, scan_state, src, near_uv, leaf_starts, anc,
+    size_t key_a, key_b, val_a, val_b, hist, task_scratch, fill, near_done, scan_state, src, near_uv, leaf_starts, anc,
         counts, mult, loc, leaf_loc, tasks, stage, counters, total;
     size_t scan_state_tiles, scan_state_bytes, hist_bytes;  // per scan instance: 1 ticket + tiles
     size_t level_cell_off[VFMM_LEVELS_CAP + 2];  // cells before level k (k>=2) in mult/loc
@@ -187,6 +187,8 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
                   const double* sigma, double xmin, double ymin, double side, char* ws,
                   Counters* ctr, cudaStream_t s, int** keys_out, int** perm_out,
                   cudaEvent_t gs_ready = nullptr, int sigma_stride = 1,
+                  // leaf rows owned (occupancy pyramid and task counts, computed in the build)
+                  Rows rows = Rows{0, 1 << 30},
                   // optional: the LSD radix kernels as a parallel branch (fork / join events)
                   cudaStream_t lsd_stream = nullptr, cudaEvent_t lsd_fork = nullptr,
                   cudaEvent_t lsd_join = nullptr);
@@ -196,8 +198,6 @@ void launch_scan_i32(int* data, int64_t n, unsigned long long* state, cudaStream
 size_t scan_tiles(int64_t n);
 void launch_leaf_starts(const int* sorted_keys, int64_t n, int nleaves, int* leaf_starts,
                         cudaStream_t s);
-void launch_counts_tasks(const Layout& L, char* ws, Counters* ctr, bool tasks, Rows rows,
-                         bool gauss, cudaStream_t s);
 void launch_tasks(const Layout& L, char* ws, Counters* ctr, Rows rows, bool gauss, cudaStream_t s);
 void launch_p2m(const Layout& L, const Src* src, const int* leaf_starts, double xmin, double ymin,
                 double side, double2* mult_leaf, const Tables* T, Rows rows, cudaStream_t s);

@@ -1,3 +1,4 @@
-python -m pytest tests/test_gpu_parity.py tests/test_large_parity.py -m gpu -x -q 2>&1 | tail -1
-run() { env $1 python bench.py --no-cpu-baseline --e2e-steps 2 > gpurun_out/ab.json 2>gpurun_out/ab.err; python -c "import json; d=json.load(open('gpurun_out/ab.json')); print('$1', round(d['ms_per_step'],4), round(d['roofline']['p2p_ms'],4), d['launches_per_step'])" 2>/dev/null || tail -1 gpurun_out/ab.err; }
-for r in 1 2; do run X=1; run VFMM_SYM_FUSED_SUM=1; done
+# A/B of environment settings / library variants on the default bench (config 2):
+#   bash tools/ab_run.sh "X=1" "VFMM_P2P_SYM_K=2" "VFMM_LIB=build/tabg/libvfmm.so" ...
+run() { env $1 python bench.py --no-cpu-baseline --e2e-steps 2 > gpurun_out/ab.json 2>gpurun_out/ab.err; python -c "import json; d=json.load(open('gpurun_out/ab.json')); print('$1', round(d['ms_per_step'],4), 'p2p', round(d['roofline']['p2p_ms'],4), 'build', round(d['roofline']['build']['ms'],4), d['launches_per_step'])" 2>/dev/null || tail -1 gpurun_out/ab.err; }
+for r in 1 2; do for a in "$@"; do run "$a"; done; done
