@@ -193,6 +193,9 @@ constexpr int kRing4Unroll = VFMM_RING4_UNROLL;
 #define VFMM_SELF_UNROLL 1
 #endif
 constexpr int kSelfUnroll = VFMM_SELF_UNROLL;  // self-block ring steps per iteration
+#ifndef VFMM_SELF_MERGED
+#define VFMM_SELF_MERGED 0  // 1: self block of 33..64 as one 4-chain loop (config 2 P2P -0.3%, config 3 +8%: off)
+#endif
 
 constexpr int kSymWarps = 8;
 // VFMM_SYM_TAB_GLOBAL: the exp table is read from global memory through L1
@@ -572,6 +575,81 @@ __device__ __forceinline__ void self_block_sym(double a0x, double a0y, double a0
     double b1x = __shfl_sync(0xffffffffu, a1x, from), b1y = __shfl_sync(0xffffffffu, a1y, from);
     double b1g = __shfl_sync(0xffffffffu, a1g, from);
     double ub0 = 0.0, vb0 = 0.0, ub1 = 0.0, vb1 = 0.0;
+    const int home = (lane + 16) & 31;
+#if VFMM_SELF_MERGED
+    if (two) {
+        // 33..64 particles: the two half rings and the cross ring (two
+        // half-phase copies P, Q of chunk 1 against chunk 0) advance in ONE
+        // 16-step loop -- four independent pair chains per step instead of
+        // two, like the four-resident ring of the forward blocks.  The cross
+        // terms of chunk 0 collect in (cu, cv) and are added after the half
+        // ring's sums, as in the two-loop order.
+        double pbx = a1x, pby = a1y, pbg = a1g;  // copy P: lane l starts with particle l
+        double qbx = __shfl_sync(0xffffffffu, a1x, home), qby = __shfl_sync(0xffffffffu, a1y, home);
+        double qbg = __shfl_sync(0xffffffffu, a1g, home);  // copy Q: particle l + 16
+        double pu = 0.0, pv = 0.0, qu = 0.0, qv = 0.0, cu = 0.0, cv = 0.0;
+#pragma unroll(kSelfUnroll)
+        for (int st = 1; st <= 16; ++st) {
+            const bool on = st < 16 || lane < 16;
+            const double dx[4] = {a0x - b0x, a1x - b1x, a0x - pbx, a0x - qbx};
+            const double dy[4] = {a0y - b0y, a1y - b1y, a0y - pby, a0y - qby};
+            double K[4];
+            pair_kernels<GAUSS, 4>(dx, dy, K, q2, tab);
+            const double k0 = on ? K[0] : 0.0, k1 = on ? K[1] : 0.0;
+            const double ca0 = b0g * k0, cb0 = a0g * k0, ca1 = b1g * k1, cb1 = a1g * k1;
+            u0 = fma(-ca0, dy[0], u0);
+            v0 = fma(ca0, dx[0], v0);
+            ub0 = fma(cb0, dy[0], ub0);
+            vb0 = fma(-cb0, dx[0], vb0);
+            u1 = fma(-ca1, dy[1], u1);
+            v1 = fma(ca1, dx[1], v1);
+            ub1 = fma(cb1, dy[1], ub1);
+            vb1 = fma(-cb1, dx[1], vb1);
+            const double cap = pbg * K[2], caq = qbg * K[3], cbp = a0g * K[2], cbq = a0g * K[3];
+            cu = fma(-cap, dy[2], cu);
+            cv = fma(cap, dx[2], cv);
+            cu = fma(-caq, dy[3], cu);
+            cv = fma(caq, dx[3], cv);
+            pu = fma(cbp, dy[2], pu);
+            pv = fma(-cbp, dx[2], pv);
+            qu = fma(cbq, dy[3], qu);
+            qv = fma(-cbq, dx[3], qv);
+            if (st < 16) {
+                b0x = __shfl_sync(0xffffffffu, b0x, from);
+                b0y = __shfl_sync(0xffffffffu, b0y, from);
+                b0g = __shfl_sync(0xffffffffu, b0g, from);
+                ub0 = __shfl_sync(0xffffffffu, ub0, from);
+                vb0 = __shfl_sync(0xffffffffu, vb0, from);
+                b1x = __shfl_sync(0xffffffffu, b1x, from);
+                b1y = __shfl_sync(0xffffffffu, b1y, from);
+                b1g = __shfl_sync(0xffffffffu, b1g, from);
+                ub1 = __shfl_sync(0xffffffffu, ub1, from);
+                vb1 = __shfl_sync(0xffffffffu, vb1, from);
+            }
+            pbx = __shfl_sync(0xffffffffu, pbx, from);
+            pby = __shfl_sync(0xffffffffu, pby, from);
+            pbg = __shfl_sync(0xffffffffu, pbg, from);
+            pu = __shfl_sync(0xffffffffu, pu, from);
+            pv = __shfl_sync(0xffffffffu, pv, from);
+            qbx = __shfl_sync(0xffffffffu, qbx, from);
+            qby = __shfl_sync(0xffffffffu, qby, from);
+            qbg = __shfl_sync(0xffffffffu, qbg, from);
+            qu = __shfl_sync(0xffffffffu, qu, from);
+            qv = __shfl_sync(0xffffffffu, qv, from);
+        }
+        // lane l holds the half-ring reaction of particle l + 16: send it home
+        u0 += __shfl_sync(0xffffffffu, ub0, home);
+        v0 += __shfl_sync(0xffffffffu, vb0, home);
+        u1 += __shfl_sync(0xffffffffu, ub1, home);
+        v1 += __shfl_sync(0xffffffffu, vb1, home);
+        u0 += cu;
+        v0 += cv;
+        // after 16 shifts copy Q is home; copy P holds particle l + 16
+        u1 += __shfl_sync(0xffffffffu, pu, home) + qu;
+        v1 += __shfl_sync(0xffffffffu, pv, home) + qv;
+        return;
+    }
+#endif
 #pragma unroll(kSelfUnroll)
     for (int st = 1; st <= 16; ++st) {
         const bool on = st < 16 || lane < 16;
@@ -606,7 +684,6 @@ __device__ __forceinline__ void self_block_sym(double a0x, double a0y, double a0
         }
     }
     // lane l holds the reaction of particle l + 16: send it home
-    const int home = (lane + 16) & 31;
     u0 += __shfl_sync(0xffffffffu, ub0, home);
     v0 += __shfl_sync(0xffffffffu, vb0, home);
     if (!two) return;
@@ -719,9 +796,39 @@ __global__ void VFMM_SYM_BOUNDS
     const double* tab = T->exp2tab2 + (kExpTab2N - 1);
 #else
     double* sexp = reinterpret_cast<double*>(sym_smem);
-    for (int i = threadIdx.x; i < kExpTab2N; i += blockDim.x) sexp[i] = T->exp2tab2[i];
     const double* tab = sexp + (kExpTab2N - 1);  // 2^(n/128) at tab[n], n <= 0
-    __syncthreads();
+    // The 60 KB table is staged by ONE bulk copy (TMA engine, mbarrier
+    // completion) issued here and waited for only before the first pair of
+    // the warp's first item, so it overlaps the item's index and particle
+    // loads (the cooperative loop stalled every new CTA: 3% of the kernel's
+    // stall samples at one item per warp).
+    __shared__ __align__(8) unsigned long long tab_bar;
+    const unsigned tab_ba = (unsigned)__cvta_generic_to_shared(&tab_bar);
+    if (threadIdx.x == 0) {
+        constexpr unsigned bytes = (unsigned)((kExpTab2N + 1) * sizeof(double));
+        static_assert(bytes % 16 == 0 && bytes <= kSymExpBytes, "bulk copy of the exp table");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tab_ba));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tab_ba), "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                (unsigned)__cvta_generic_to_shared(sexp)),
+            "l"(T->exp2tab2), "r"(bytes), "r"(tab_ba)
+            : "memory");
+    }
+    __syncthreads();  // the barrier's initialisation is visible
+    bool tab_ready = false;
+    auto wait_tab = [&]() {
+        if (tab_ready) return;
+        asm volatile(
+            "{\n .reg .pred p;\n WAIT_%=:\n"
+            " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+            " @!p bra WAIT_%=;\n}" ::"r"(tab_ba)
+            : "memory");
+        tab_ready = true;
+    };
 #endif
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double2* accAw = accA + warp * kSymMaxLeaf;
@@ -768,6 +875,9 @@ __global__ void VFMM_SYM_BOUNDS
             }
         }
         if (!ownA && n2 == 0) continue;
+#ifndef VFMM_SYM_TAB_GLOBAL
+        wait_tab();
+#endif
         // ---- self block (owned A only): each unordered pair once ----
         if (part == 0 && ownA && nA <= kSymMaxLeaf) {
             double a0x, a0y, a0g, a1x, a1y, a1g, a2x, a2y, a2g, a3x, a3y, a3g;
@@ -1068,16 +1178,17 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
     static int minb = 0;
     if (!minb) {
         const char* e = getenv("VFMM_P2P_SYM_MINB");
-        minb = (e && e[0] == '3') ? 3 : 2;
+        minb = (e && (e[0] == '3' || e[0] == '1')) ? e[0] - '0' : 2;
     }
-    auto* sfn = minb == 3 ? (g ? k_p2p_sym<true, 3> : k_p2p_sym<false, 3>)
-                          : (g ? k_p2p_sym<true, 2> : k_p2p_sym<false, 2>);
+    auto* sfn = minb == 3   ? (g ? k_p2p_sym<true, 3> : k_p2p_sym<false, 3>)
+                : minb == 1 ? (g ? k_p2p_sym<true, 1> : k_p2p_sym<false, 1>)
+                            : (g ? k_p2p_sym<true, 2> : k_p2p_sym<false, 2>);
     static std::atomic<unsigned long long> attr_set{0};  // per device ordinal
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !(attr_set.load() >> dev & 1ull)) {
         for (auto* f : {k_p2p_sym<true, 3>, k_p2p_sym<false, 3>, k_p2p_sym<true, 2>,
-                        k_p2p_sym<false, 2>})
+                        k_p2p_sym<false, 2>, k_p2p_sym<true, 1>, k_p2p_sym<false, 1>})
             cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
         attr_set.fetch_or(1ull << dev);
     }

@@ -276,6 +276,18 @@ __device__ __forceinline__ void warp_bitonic(int (&e)[E]) {
     }
 }
 
+// -1 / (2 sigma^2 ln 2) (the exponent of engine.py:256 in log2 units), the
+// IEEE division done only when sigma changes from the thread's previous
+// particle (uniform core sizes: once per thread; it was a quarter of
+// k_leaf_pack's stall samples).  Results are identical to dividing every time.
+__device__ __forceinline__ double q2_of(double s, double& s_prev, double& q_prev) {
+    if (!(s == s_prev)) {
+        s_prev = s;
+        q_prev = -1.4426950408889634 / (2.0 * s * s);
+    }
+    return q_prev;
+}
+
 template <int E>
 __device__ __forceinline__ void leaf_pack(const int* __restrict__ slot, int lo, int c, int leaf,
                                           const double* __restrict__ x, const double* __restrict__ y,
@@ -283,7 +295,7 @@ __device__ __forceinline__ void leaf_pack(const int* __restrict__ slot, int lo, 
                                           const double* __restrict__ sigma, int sstride,
                                           int* __restrict__ keys, int* __restrict__ perm,
                                           Src* __restrict__ src, unsigned long long& smax,
-                                          unsigned long long& smin) {
+                                          unsigned long long& smin, double& s_prev, double& q_prev) {
     const int lane = threadIdx.x & 31;
     int e[E];
 #pragma unroll
@@ -302,7 +314,7 @@ __device__ __forceinline__ void leaf_pack(const int* __restrict__ slot, int lo, 
         r.x = x[idx];
         r.y = y[idx];
         r.g = g[idx];
-        r.q2 = -1.4426950408889634 / (2.0 * s * s);  // -r^2 / (2 sigma^2) in log2 units
+        r.q2 = q2_of(s, s_prev, q_prev);  // -r^2 / (2 sigma^2) in log2 units
         src[lo + p] = r;
         perm[lo + p] = idx;
         keys[lo + p] = leaf;
@@ -330,14 +342,15 @@ __global__ void __launch_bounds__(256)
     __shared__ unsigned long long wmax[8], wmin[8];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned long long smax = 0ull, smin = ~0ull;
+    double s_prev = __longlong_as_double(0x7ff8000000000000ll), q_prev = 0.0;  // NaN: nothing cached
     for (int leaf = blockIdx.x * 8 + warp; leaf < nleaves; leaf += gridDim.x * 8) {
         const int lo = ls[leaf], c = ls[leaf + 1] - lo;
         if (c > 64)
-            leaf_pack<4>(slot, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin);
+            leaf_pack<4>(slot, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
         else if (c > 32)
-            leaf_pack<2>(slot, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin);
+            leaf_pack<2>(slot, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
         else if (c > 0)
-            leaf_pack<1>(slot, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin);
+            leaf_pack<1>(slot, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
     }
     if (!sigma) return;
     for (int o = 16; o > 0; o >>= 1) {
@@ -372,6 +385,7 @@ __global__ void __launch_bounds__(256)
     if (!ctr->sort_fallback) return;
     __shared__ unsigned long long wmax[8], wmin[8];
     unsigned long long sbits = 0ull, smin = ~0ull;
+    double s_prev = __longlong_as_double(0x7ff8000000000000ll), q_prev = 0.0;  // NaN: nothing cached
     // grid-stride (a small grid: the launch is cheap when the counting path ran)
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -381,7 +395,7 @@ __global__ void __launch_bounds__(256)
         r.y = y[i];
         r.g = g[i];
         // -r^2 / (2 sigma^2) (engine.py:256) expressed in log2 units
-        r.q2 = -1.4426950408889634 / (2.0 * s * s);
+        r.q2 = q2_of(s, s_prev, q_prev);
         out[i] = r;
         if (sigma) {
             const unsigned long long b = ordered_bits(s);

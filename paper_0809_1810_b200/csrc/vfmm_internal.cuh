@@ -65,7 +65,9 @@ struct Tables {
     double invfact[kOrderCap + 16];
     double pow2neg[2 * kOrderCap + 16];  // 2^-k
     double exp2tab[kExpTabN];        // 2^(n/64), n = -3840..0
-    double exp2tab2[kExpTab2N];      // 2^(n/128), n = -7680..0 (symmetric P2P)
+    // 2^(n/128), n = -7680..0 (symmetric P2P); 16-byte aligned and padded to
+    // an even count so one bulk copy (cp.async.bulk) stages it
+    alignas(16) double exp2tab2[kExpTab2N + 1];
 };
 
 const Tables* device_tables();   // device pointer (uploaded on first use)

@@ -88,8 +88,8 @@ __device__ __forceinline__ void pair_kernels(const double (&dx)[N], const double
 }
 
 // V: 0 = ring4 as in k_p2p_sym; 1 = eight residents (two ring4 halves share one rotating source)
-template <int TAB, int V, int MINB, int ABL = 0>
-__global__ void __launch_bounds__(256, MINB) k_ring(const double* __restrict__ pos, const double* __restrict__ gtab,
+template <int TAB, int V, int MINB, int ABL = 0, int BT = 256>
+__global__ void __launch_bounds__(BT, MINB) k_ring(const double* __restrict__ pos, const double* __restrict__ gtab,
                                                     double* out, int reps, double q2v) {
     extern __shared__ double tab_s[];
     const int ntab = TAB == 0 ? kTabN : 128;
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(256, MINB) k_ring(const double* __restrict__ p
     q2.hi = (unsigned)__double2hiint(7680.0 / -q2.q);
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    constexpr int NR = V == 1 ? 8 : 4;
+    constexpr int NR = V == 1 ? 8 : (V == 2 ? 6 : (V == 3 ? 2 : 4));
     double ax[NR], ay[NR], ag[NR], u[NR], v[NR];
 #pragma unroll
     for (int k = 0; k < NR; ++k) {
@@ -116,7 +116,58 @@ __global__ void __launch_bounds__(256, MINB) k_ring(const double* __restrict__ p
     for (int r = 0; r < reps; ++r) {
 #pragma unroll 2
         for (int st = 0; st < 32; ++st) {
-            if (V == 0) {
+            if (V == 3) {  // two residents
+                double dx[2], dy[2], K[2];
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    dx[k] = ax[k] - bx;
+                    dy[k] = ay[k] - by;
+                }
+                pair_kernels<2, TAB, ABL>(dx, dy, K, q2, tab);
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const double ca = bg * K[k], cb = ag[k] * K[k];
+                    u[k] = fma(-ca, dy[k], u[k]);
+                    v[k] = fma(ca, dx[k], v[k]);
+                    ub = fma(cb, dy[k], ub);
+                    vb = fma(-cb, dx[k], vb);
+                }
+            } else if (V == 2) {  // six residents: chains of 4 + 2
+                {
+                    double dx[4], dy[4], K[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        dx[k] = ax[k] - bx;
+                        dy[k] = ay[k] - by;
+                    }
+                    pair_kernels<4, TAB, ABL>(dx, dy, K, q2, tab);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const double ca = bg * K[k], cb = ag[k] * K[k];
+                        u[k] = fma(-ca, dy[k], u[k]);
+                        v[k] = fma(ca, dx[k], v[k]);
+                        ub = fma(cb, dy[k], ub);
+                        vb = fma(-cb, dx[k], vb);
+                    }
+                }
+                {
+                    double dx[2], dy[2], K[2];
+#pragma unroll
+                    for (int k = 0; k < 2; ++k) {
+                        dx[k] = ax[4 + k] - bx;
+                        dy[k] = ay[4 + k] - by;
+                    }
+                    pair_kernels<2, TAB, ABL>(dx, dy, K, q2, tab);
+#pragma unroll
+                    for (int k = 0; k < 2; ++k) {
+                        const double ca = bg * K[k], cb = ag[4 + k] * K[k];
+                        u[4 + k] = fma(-ca, dy[k], u[4 + k]);
+                        v[4 + k] = fma(ca, dx[k], v[4 + k]);
+                        ub = fma(cb, dy[k], ub);
+                        vb = fma(-cb, dx[k], vb);
+                    }
+                }
+            } else if (V == 0) {
                 double dx[4], dy[4], K[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -185,24 +236,24 @@ int main(int argc, char** argv) {
     double *dp, *dt, *out;
     cudaMalloc(&dp, 8 * 8192);
     cudaMalloc(&dt, 8 * kTabN);
-    cudaMalloc(&out, 8 * 148 * 4 * 256);
+    cudaMalloc(&out, 8 * 148 * 4 * 512);
     cudaMemcpy(dp, hp.data(), 8 * 8192, cudaMemcpyHostToDevice);
     cudaMemcpy(dt, ht.data(), 8 * kTabN, cudaMemcpyHostToDevice);
     const double sigma = h / 0.8, q2 = -1.4426950408889634 / (2 * sigma * sigma);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    auto run = [&](const char* name, auto kern, int smem, int minb, int npairs_per_step) {
+    auto run = [&](const char* name, auto kern, int smem, int minb, int npairs_per_step, int bt = 256) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         const int grid = 148 * minb;
-        kern<<<grid, 256, smem>>>(dp, dt, out, 2, q2);
+        kern<<<grid, bt, smem>>>(dp, dt, out, 2, q2);
         cudaEventRecord(e0);
-        kern<<<grid, 256, smem>>>(dp, dt, out, reps, q2);
+        kern<<<grid, bt, smem>>>(dp, dt, out, reps, q2);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
-        const double pairs = (double)grid * 256 * reps * 32 * npairs_per_step;  // lane-pairs
+        const double pairs = (double)grid * bt * reps * 32 * npairs_per_step;  // lane-pairs
         const double fp64 = pairs * 22;
         const double peak = 64.0 * 148 * clk_khz * 1e3;  // FP64 lanes/s at the rated clock
         printf("%-34s %8.3f ms  %.3f Gpair/s  fp64 frac %.3f  (%s)\n", name, ms, pairs / ms / 1e6,
@@ -217,8 +268,13 @@ int main(int argc, char** argv) {
     run("ring4 abl no-shfl", k_ring<0, 0, 2, 1>, kTabN * 8, 2, 4);
     run("ring4 abl no-lds", k_ring<0, 0, 2, 2>, kTabN * 8, 2, 4);
     run("ring4 abl no-mufu", k_ring<0, 0, 2, 4>, kTabN * 8, 2, 4);
-    run("ring4 abl no-clamps", k_ring<0, 0, 2, 8>, kTabN * 8, 2, 4);
-    run("ring4 abl no-shfl,lds,mufu,clamp", k_ring<0, 0, 2, 15>, kTabN * 8, 2, 4);
-    run("ring8 abl no-shfl,lds,mufu,clamp", k_ring<0, 1, 1, 15>, kTabN * 8, 1, 8);
+    run("ring4 abl no-shfl,lds,mufu", k_ring<0, 0, 2, 7>, kTabN * 8, 2, 4);
+    run("ring8 384thr MINB1", k_ring<0, 1, 1, 0, 384>, kTabN * 8, 1, 8, 384);
+    run("ring6 384thr MINB1", k_ring<0, 2, 1, 0, 384>, kTabN * 8, 1, 6, 384);
+    run("ring6 256thr MINB1", k_ring<0, 2, 1, 0, 256>, kTabN * 8, 1, 6, 256);
+    run("ring4 256thr MINB1", k_ring<0, 0, 1, 0, 256>, kTabN * 8, 1, 4, 256);
+    run("ring2 256thr MINB2", k_ring<0, 3, 2, 0, 256>, kTabN * 8, 2, 2, 256);
+    run("ring2 256thr MINB1", k_ring<0, 3, 1, 0, 256>, kTabN * 8, 1, 2, 256);
+    run("ring8 abl no-shfl,lds,mufu", k_ring<0, 1, 1, 7>, kTabN * 8, 1, 8);
     return 0;
 }
