@@ -197,7 +197,10 @@ constexpr int kSelfUnroll = VFMM_SELF_UNROLL;  // self-block ring steps per iter
 #define VFMM_SELF_MERGED 0  // 1: self block of 33..64 as one 4-chain loop (config 2 P2P -0.3%, config 3 +8%: off)
 #endif
 
-constexpr int kSymWarps = 8;
+#ifndef VFMM_SYM_WARPS
+#define VFMM_SYM_WARPS 8
+#endif
+constexpr int kSymWarps = VFMM_SYM_WARPS;  // warps per CTA of the symmetric kernel
 // VFMM_SYM_TAB_GLOBAL: the exp table is read from global memory through L1
 // (no per-CTA staging; one L1 copy per SM shared by every CTA it runs)
 #ifdef VFMM_SYM_TAB_GLOBAL

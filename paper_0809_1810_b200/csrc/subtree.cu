@@ -209,20 +209,18 @@ __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
     }
     if (depth == 0) return;
     // ---- subtree below the root: stage the root and the M2L parts ----
-    {
-        const int total = sub_off(depth + 1) * P;
-        for (int i = threadIdx.x; i < total; i += blockDim.x) {
-            const int c = i / P, k = i % P;
-            if (c == 0) {
-                sm[i] = anc[cur * P + k];
-                continue;
-            }
-            int sl = 1;
-            while (sub_off(sl + 1) <= c) ++sl;
-            const int side = 1 << sl, lc = c - sub_off(sl);
-            const int lvl = ls + sl;
-            sm[i] = loc[lvl_off(lvl, P) + coef_base(lvl, cx * side + lc % side, cy * side + lc / side) +
-                        k * coef_stride(lvl)];
+    // (level by level: the level offsets hoisted, the cell / coefficient
+    // split by a multiply-high instead of a division by the runtime P)
+    const unsigned pmag = (unsigned)((0x100000000ull + P - 1) / P);  // i / P = umulhi(i, pmag), i < 2^16
+    for (int k = threadIdx.x; k < P; k += blockDim.x) sm[k] = anc[cur * P + k];
+    for (int sl = 1; sl <= depth; ++sl) {
+        const int side = 1 << sl, lvl = ls + sl;
+        const double2* g = loc + lvl_off(lvl, P);
+        const int64_t cs = coef_stride(lvl);
+        double2* dst = sm + (size_t)sub_off(sl) * P;
+        for (int i = threadIdx.x; i < side * side * P; i += blockDim.x) {
+            const int lc = (int)__umulhi((unsigned)i, pmag), k = i - lc * P;
+            dst[i] = g[coef_base(lvl, cx * side + (lc & (side - 1)), cy * side + (lc >> sl)) + k * cs];
         }
     }
     __syncthreads();
@@ -236,8 +234,8 @@ __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
         const bool leaf = lvl == levels;
         const int m = 1 << lvl;
         for (int i = threadIdx.x; i < side * side * P; i += blockDim.x) {
-            const int c = i / P, nn = i % P;
-            const int lx = c % side, ly = c / side;
+            const int c = (int)__umulhi((unsigned)i, pmag), nn = i - c * P;
+            const int lx = c & (side - 1), ly = c >> s;
             const int q = 2 * (ly & 1) + (lx & 1);
             const double2* Lp = par + (size_t)((ly >> 1) * (side >> 1) + (lx >> 1)) * P;
             const double2* Fq = sF + q * P;
@@ -252,7 +250,9 @@ __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
             double2 r = cu[i];  // M2L part (staged)
             r.x += sx;
             r.y += sy;
-            cu[i] = r;
+            // the leaf level keeps Lh_n / n! for the fused L2P (eval_local's
+            // per-particle products, formed once per leaf)
+            cu[i] = leaf && fo.u ? make_double2(r.x * sfact[nn], r.y * sfact[nn]) : r;
             const int gx = cx * side + lx, gy = cy * side + ly;
             if (leaf)
                 leaf_loc[((int64_t)gy * m + gx) * P + nn] = r;
@@ -299,25 +299,35 @@ __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
             jj[u] = idx < total ? rb[ly] + idx - rp[ly] : -1;
         }
         int key[kB], o[kB];
-        Src sj[kB];
+        double2 sj[kB];
         double2 nv[kB];
 #pragma unroll
         for (int u = 0; u < kB; ++u) {
             const int j = jj[u] < 0 ? 0 : jj[u];
             key[u] = fo.keys[j];
-            sj[u] = fo.src[j];
+            sj[u] = *reinterpret_cast<const double2*>(&fo.src[j]);  // x, y of the record
             nv[u] = fo.near[j];
             o[u] = fo.perm[j];
         }
+        // the kB particles' Horner chains advance together (ILP)
+        const double2* lp[kB];
+        double wx[kB], wy[kB];
+        double2 ff[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            const int ly = lyy[u], gy = cy * side + ly;
+            const int lx = jj[u] < 0 ? 0 : (key[u] & (m - 1)) - cx * side;
+            const double ccx = cell_center(fo.xmin, cx * side + lx, r);
+            const double ccy = cell_center(fo.ymin, gy, r);
+            lp[u] = leafs + (size_t)(ly * side + lx) * P;
+            wx[u] = (sj[u].x - ccx) * inv_r;
+            wy[u] = (sj[u].y - ccy) * inv_r;
+        }
+        eval_local_multi<kB>(lp, P, wx, wy, ff);
 #pragma unroll
         for (int u = 0; u < kB; ++u) {
             if (jj[u] < 0) continue;
-            const int ly = lyy[u], gy = cy * side + ly;
-            const int lx = (key[u] & (m - 1)) - cx * side;
-            const double ccx = cell_center(fo.xmin, cx * side + lx, r);
-            const double ccy = cell_center(fo.ymin, gy, r);
-            const double2 f = eval_local(leafs + (size_t)(ly * side + lx) * P, 1, P,
-                                         (sj[u].x - ccx) * inv_r, (sj[u].y - ccy) * inv_r, sfact);
+            const double2 f = ff[u];
             // f_to_velocity: u = Im f / 2pi, v = Re f / 2pi; then far + near
             const double uo = f.y * kInv2Pi + nv[u].x, vo = f.x * kInv2Pi + nv[u].y;
             if (fo.v) {

@@ -387,6 +387,38 @@ __device__ __forceinline__ double2 eval_local(const double2* __restrict__ Lh, in
     return make_double2(ax, ay);
 }
 
+// NB independent evaluations of eval_local advanced together (coefficient
+// k of every particle, then k - 1, ...): NB Horner chains in flight instead of
+// one; each particle's arithmetic and order are eval_local's exactly.
+// Lh here holds the coefficients already multiplied by 1/k! (the products
+// eval_local forms per particle, formed once per leaf: same values).
+template <int NB>
+__device__ __forceinline__ void eval_local_multi(const double2* const (&Lh)[NB], int P,
+                                                 const double (&wx)[NB], const double (&wy)[NB],
+                                                 double2 (&out)[NB]) {
+    double ax[NB], ay[NB];
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+        const double2 top = Lh[u][P - 1];
+        ax[u] = top.x;
+        ay[u] = top.y;
+    }
+#pragma unroll 2
+    for (int k = P - 2; k >= 0; --k) {
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            const double2 c = Lh[u][k];
+            const double nx = -wx[u], ny = -wy[u];
+            const double tx = fma(ax[u], nx, fma(-ay[u], ny, c.x));
+            const double ty = fma(ax[u], ny, fma(ay[u], nx, c.y));
+            ax[u] = tx;
+            ay[u] = ty;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < NB; ++u) out[u] = make_double2(ax[u], ay[u]);
+}
+
 // Stage the exponential table in shared memory (all threads of the block).
 __device__ __forceinline__ const double* stage_exp_table(double* smem, const double* __restrict__ g) {
     for (int i = threadIdx.x; i < kExpTab; i += blockDim.x) smem[i] = g[i];
