@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
     double* s2 = reinterpret_cast<double*>(sF + 4 * P);  // [P]
     double2* anc = reinterpret_cast<double2*>(s2 + ((P + 1) & ~1));  // [2][P] ping-pong
     double* sfact = reinterpret_cast<double*>(anc + 2 * P);           // [P] 1/k!
+    double2* apart = reinterpret_cast<double2*>(sfact + ((P + 1) & ~1));  // [ls - 2][P] M2L parts
     const int mt = 1 << ls;
     const int cx = blockIdx.x % mt, cy = blockIdx.x / mt;
     if (!rows_touch(rows, cy, levels - ls)) return;  // subtree outside the owned strip
@@ -153,14 +154,37 @@ __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
         s2[i] = T->pow2neg[i];
         sfact[i] = T->invfact[i];
     }
-    // ---- ancestor chain: level 2 (complete after M2L) down to ls ----
-    // output n of a level is summed by 8 lanes (terms mm = n + lane8, step 8)
-    // and reduced by xor shuffles: P x 8 threads instead of P serial sums
+    // ---- every global read of the chain and the subtree, issued at once ----
+    // (level 2, the ancestors' M2L parts, the subtree's M2L parts: none depends
+    // on the chain, so one memory latency instead of one per level)
     if (threadIdx.x < P) {
         const int n = threadIdx.x, sh = ls - 2;
         anc[n] = loc[lvl_off(2, P) + coef_base(2, cx >> sh, cy >> sh) + n * coef_stride(2)];
     }
+    for (int i = threadIdx.x; i < (ls - 2) * P; i += blockDim.x) {
+        const int k = 3 + i / P, n = i % P, sh = ls - k;
+        const int64_t gi = lvl_off(k, P) + coef_base(k, cx >> sh, cy >> sh) + n * coef_stride(k);
+        // M2L part: shared ancestors (k < ls) from the read-only copy, since
+        // their writer CTA completes them in loc while others still read
+        apart[i] = k < ls ? anc_m2l[gi] : loc[gi];
+    }
+    // subtree levels 1..depth (level by level: offsets hoisted, the cell /
+    // coefficient split by a multiply-high instead of a division by P)
+    const unsigned pmag = (unsigned)((0x100000000ull + P - 1) / P);  // i / P = umulhi(i, pmag), i < 2^16
+    for (int sl = 1; sl <= depth; ++sl) {
+        const int side = 1 << sl, lvl = ls + sl;
+        const double2* g = loc + lvl_off(lvl, P);
+        const int64_t cs = coef_stride(lvl);
+        double2* dst = sm + (size_t)sub_off(sl) * P;
+        for (int i = threadIdx.x; i < side * side * P; i += blockDim.x) {
+            const int lc = (int)__umulhi((unsigned)i, pmag), k = i - lc * P;
+            dst[i] = g[coef_base(lvl, cx * side + (lc & (side - 1)), cy * side + (lc >> sl)) + k * cs];
+        }
+    }
     __syncthreads();
+    // ---- ancestor chain: level 2 (complete after M2L) down to ls ----
+    // output n of a level is summed by 8 lanes (terms mm = n + lane8, step 8)
+    // and reduced by xor shuffles: P x 8 threads instead of P serial sums
     int cur = 0;
     const int l8 = threadIdx.x & 7;
     for (int k = 3; k <= ls; ++k) {
@@ -189,9 +213,7 @@ __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
             }
             if (nact && l8 == 0) {
                 const int64_t gi = lvl_off(k, P) + coef_base(k, ax, ay) + n * coef_stride(k);
-                // M2L part: shared ancestors (k < ls) from the read-only copy, since
-                // their writer CTA completes them in loc while others still read
-                double2 r = k < ls ? anc_m2l[gi] : loc[gi];
+                double2 r = apart[(k - 3) * P + n];
                 r.x += sx;
                 r.y += sy;
                 anc[(cur ^ 1) * P + n] = r;
@@ -208,20 +230,12 @@ __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
         cur ^= 1;
     }
     if (depth == 0) return;
-    // ---- subtree below the root: stage the root and the M2L parts ----
-    // (level by level: the level offsets hoisted, the cell / coefficient
-    // split by a multiply-high instead of a division by the runtime P)
-    const unsigned pmag = (unsigned)((0x100000000ull + P - 1) / P);  // i / P = umulhi(i, pmag), i < 2^16
-    for (int k = threadIdx.x; k < P; k += blockDim.x) sm[k] = anc[cur * P + k];
-    for (int sl = 1; sl <= depth; ++sl) {
-        const int side = 1 << sl, lvl = ls + sl;
-        const double2* g = loc + lvl_off(lvl, P);
-        const int64_t cs = coef_stride(lvl);
-        double2* dst = sm + (size_t)sub_off(sl) * P;
-        for (int i = threadIdx.x; i < side * side * P; i += blockDim.x) {
-            const int lc = (int)__umulhi((unsigned)i, pmag), k = i - lc * P;
-            dst[i] = g[coef_base(lvl, cx * side + (lc & (side - 1)), cy * side + (lc >> sl)) + k * cs];
-        }
+    // ---- subtree below the root ----
+    // parents are kept in shared memory pre-multiplied by 2^-m (exact: a
+    // power of two), the factor the shift applies to every term
+    for (int k = threadIdx.x; k < P; k += blockDim.x) {
+        const double2 a = anc[cur * P + k];
+        sm[k] = make_double2(a.x * s2[k], a.y * s2[k]);
     }
     __syncthreads();
     for (int s = 1; s <= depth; ++s) {
@@ -241,18 +255,19 @@ __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
             const double2* Fq = sF + q * P;
             double sx = 0.0, sy = 0.0;
             for (int mm = nn; mm < P; ++mm) {
-                const double2 a = Lp[mm];
-                const double axs = a.x * s2[mm], ays = a.y * s2[mm];
+                const double2 a = Lp[mm];  // 2^-mm Lh_mm
                 const double2 f = Fq[mm - nn];
-                sx = fma(axs, f.x, fma(-ays, f.y, sx));
-                sy = fma(axs, f.y, fma(ays, f.x, sy));
+                sx = fma(a.x, f.x, fma(-a.y, f.y, sx));
+                sy = fma(a.x, f.y, fma(a.y, f.x, sy));
             }
             double2 r = cu[i];  // M2L part (staged)
             r.x += sx;
             r.y += sy;
-            // the leaf level keeps Lh_n / n! for the fused L2P (eval_local's
-            // per-particle products, formed once per leaf)
-            cu[i] = leaf && fo.u ? make_double2(r.x * sfact[nn], r.y * sfact[nn]) : r;
+            // next level's parents: 2^-n Lh_n; the leaf level keeps Lh_n / n!
+            // for the fused L2P (eval_local's per-particle products, formed
+            // once per leaf)
+            const double sc = leaf ? sfact[nn] : s2[nn];
+            cu[i] = leaf && !fo.u ? r : make_double2(r.x * sc, r.y * sc);
             const int gx = cx * side + lx, gy = cy * side + ly;
             if (leaf)
                 leaf_loc[((int64_t)gy * m + gx) * P + nn] = r;
@@ -385,7 +400,7 @@ void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_lo
     }
     const int ls = l2l_split_level(L.levels, L.P);
     const size_t shm = sub_smem(L.levels - ls, L.P) + sizeof(double2) * (2 * L.P + 1) +
-                       sizeof(double) * L.P;
+                       sizeof(double) * (L.P + 1) + sizeof(double2) * (ls - 2) * L.P;
     const unsigned ctas = (unsigned)(1ll << (2 * ls));
     if (ctas >= 148 * 4)
         launch_k(k_l2l_fused<128>, ctas, 128, shm, s, loc, leaf_loc, anc, ls, L.levels, L.P, T, rows, fo);
