@@ -6,6 +6,7 @@
 // (engine.py:205-213), expansions.f_to_velocity (expansions.py:217-225), the
 // combine in engine.evaluate (engine.py:394-396) and the far + near parts of
 // engine.evaluate_at (engine.py:434-459).
+#include <algorithm>
 #include <climits>
 
 #include "vfmm_internal.cuh"
@@ -27,46 +28,66 @@ __global__ void k_leaf_locals_copy(const double2* __restrict__ loc2, int P, doub
 // field (on its stream, so it overlaps the far-field chain): symmetric
 // kernel -- slot 0 (the leaf's own blocks) + the reactions of the existing
 // backward neighbours in kind order; generic kernel -- the three
-// neighbourhood-row partial sums in row order.
+// neighbourhood-row partial sums in row order.  Symmetric mode: one warp per
+// leaf, the neighbour test made once per leaf and the leaf's particles (one
+// contiguous sorted range) summed with coalesced slot loads; generic mode
+// (leaves of any size): one thread per particle.
 __global__ void __launch_bounds__(256)
-    k_near_sum(const int* __restrict__ keys, double2* __restrict__ near_uv, int64_t n, int levels,
-               Rows rows, const int* __restrict__ ls, const Counters* __restrict__ ctr, bool gauss,
+    k_near_sum(const int* __restrict__ keys, double2* __restrict__ near_uv, int64_t n, int levels, Rows rows,
+               const int* __restrict__ ls, const Counters* __restrict__ ctr, bool gauss,
                int sym_enabled, int split, int sym_fused) {
     pdl_enter();
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
     const int m = 1 << levels;
-    const int leaf = keys[i];
-    const int ix = leaf % m, iy = leaf / m;
-    if (iy < rows.lo || iy >= rows.hi) return;  // halo particle of a sharded run
-    double2 nv;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool sym = sym_enabled && p2p_symmetric(ctr, gauss);
     if (sym && sym_fused) return;  // k_p2p_sym's last writers summed the slots
-    if (sym) {
-        double2 t[kNearSlots];
-#pragma unroll
-        for (int k = 0; k < kNearSlots; ++k) t[k] = near_uv[(int64_t)k * n + i];
-        nv = t[0];
-        if (split == 2) {  // the leaf's second item (forward stream part 2)
-            const double2 t5 = near_uv[(int64_t)kSplitSlot * n + i];
-            nv.x += t5.x;
-            nv.y += t5.y;
-        }
+    if (!sym) {  // generic kernel (leaves of any size): thread per particle
+        if (t >= n) return;
+        const int64_t i = t;
+        const int lf = keys[i];
+        if ((lf >> levels) < rows.lo || (lf >> levels) >= rows.hi) return;  // halo particle
+        const double2 n0 = near_uv[i], n1 = near_uv[n + i], n2 = near_uv[2 * n + i];
+        near_uv[i] = make_double2((n0.x + n1.x) + n2.x, (n0.y + n1.y) + n2.y);
+        return;
+    }
+    // symmetric kernel (leaves of <= 128 particles): warp per leaf
+    const int leaf = (int)(t >> 5);
+    const int lane = threadIdx.x & 31;
+    if (leaf >= m * m) return;
+    const int ix = leaf & (m - 1), iy = leaf >> levels;
+    if (iy < rows.lo || iy >= rows.hi) return;  // halo leaves of a sharded run
+    const int lo = ls[leaf], hi = ls[leaf + 1];
+    bool ok[kNearSlots];
+    {
 #pragma unroll
         for (int k = 1; k < kNearSlots; ++k) {
             // the item of leaf (ix, iy) - d_k wrote slot k; d = (1,0), (-1,1), (0,1), (1,1)
             const int ax = ix - (k == 2 ? -1 : (k == 3 ? 0 : 1)), ay = iy - (k == 1 ? 0 : 1);
-            const bool ok = ax >= 0 && ax < m && ay >= 0 && ls[ay * m + ax + 1] != ls[ay * m + ax];
-            if (ok) {
-                nv.x += t[k].x;
-                nv.y += t[k].y;
+            ok[k] = ax >= 0 && ax < m && ay >= 0 && ls[ay * m + ax + 1] != ls[ay * m + ax];
+        }
+    }
+    for (int i = lo + lane; i < hi; i += 32) {
+        double2 nv;
+        {
+            double2 t[kNearSlots];
+#pragma unroll
+            for (int k = 0; k < kNearSlots; ++k) t[k] = near_uv[(int64_t)k * n + i];
+            nv = t[0];
+            if (split == 2) {  // the leaf's second item (forward stream part 2)
+                const double2 t5 = near_uv[(int64_t)kSplitSlot * n + i];
+                nv.x += t5.x;
+                nv.y += t5.y;
+            }
+#pragma unroll
+            for (int k = 1; k < kNearSlots; ++k) {
+                if (ok[k]) {
+                    nv.x += t[k].x;
+                    nv.y += t[k].y;
+                }
             }
         }
-    } else {
-        const double2 n0 = near_uv[i], n1 = near_uv[n + i], n2 = near_uv[2 * n + i];
-        nv = make_double2((n0.x + n1.x) + n2.x, (n0.y + n1.y) + n2.y);
+        near_uv[i] = nv;
     }
-    near_uv[i] = nv;
 }
 
 // Far field (L2P) + the near total, un-permuted to the caller's order.
@@ -173,9 +194,10 @@ void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const 
 void launch_near_sum(const Layout& L, const int* keys, double2* near_uv, Rows rows,
                      const int* leaf_starts, const Counters* ctr, int kernel, bool sym_fused,
                      cudaStream_t s) {
-    launch_k(k_near_sum, (unsigned)((L.n + 255) / 256), 256, 0, s, 
-        keys, near_uv, L.n, L.levels, rows, leaf_starts, ctr, kernel == VFMM_KERNEL_GAUSSIAN,
-        sym_disabled() ? 0 : 1, p2p_sym_split(L, rows), sym_fused ? 1 : 0);
+    const int64_t threads = std::max<int64_t>((int64_t)L.nleaves * 32, L.n);  // sym: warp per leaf; generic: thread per particle
+    launch_k(k_near_sum, (unsigned)((threads + 255) / 256), 256, 0, s, keys, near_uv, L.n, L.levels,
+             rows, leaf_starts, ctr, kernel == VFMM_KERNEL_GAUSSIAN, sym_disabled() ? 0 : 1,
+             p2p_sym_split(L, rows), sym_fused ? 1 : 0);
     note_launches(1);
 }
 
