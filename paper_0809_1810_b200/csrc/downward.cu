@@ -35,7 +35,7 @@ __global__ void k_leaf_locals_copy(const double2* __restrict__ loc2, int P, doub
 __global__ void __launch_bounds__(256)
     k_near_sum(const int* __restrict__ keys, double2* __restrict__ near_uv, int64_t n, int levels, Rows rows,
                const int* __restrict__ ls, const Counters* __restrict__ ctr, bool gauss,
-               int sym_enabled, int split, int sym_fused) {
+               int sym_enabled, int split_from, int item_base, int sym_fused) {
     pdl_enter();
     const int m = 1 << levels;
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
             for (int k = 0; k < kNearSlots; ++k) t[k] = near_uv[(int64_t)k * n + i];
             nv = t[0];
-            if (split == 2) {  // the leaf's second item (forward stream part 2)
+            if (sym_leaf_split(leaf, item_base, split_from) == 2) {  // the leaf's second item
                 const double2 t5 = near_uv[(int64_t)kSplitSlot * n + i];
                 nv.x += t5.x;
                 nv.y += t5.y;
@@ -197,7 +197,7 @@ void launch_near_sum(const Layout& L, const int* keys, double2* near_uv, Rows ro
     const int64_t threads = std::max<int64_t>((int64_t)L.nleaves * 32, L.n);  // sym: warp per leaf; generic: thread per particle
     launch_k(k_near_sum, (unsigned)((threads + 255) / 256), 256, 0, s, keys, near_uv, L.n, L.levels,
              rows, leaf_starts, ctr, kernel == VFMM_KERNEL_GAUSSIAN, sym_disabled() ? 0 : 1,
-             p2p_sym_split(L, rows), sym_fused ? 1 : 0);
+             p2p_sym_split_from(L, rows), (rows.lo > 0 ? rows.lo - 1 : 0) << L.levels, sym_fused ? 1 : 0);
     note_launches(1);
 }
 

@@ -734,9 +734,11 @@ __device__ __forceinline__ void self_block_sym(double a0x, double a0y, double a0
 // reactions of the backward neighbours d_k = (1,0), (-1,1), (0,1), (1,1)
 // (slots 1..4) that exist and hold particles.  The sums read L2 (just written
 // by other SMs: __ldcg).
-__device__ __noinline__ void leaf_written(int lf, int m, int levels, int64_t n, int split,
-                                          const int* __restrict__ ls, double2* near5, int* done) {
+__device__ __noinline__ void leaf_written(int lf, int m, int levels, int64_t n, int split_from,
+                                          int item_base, const int* __restrict__ ls, double2* near5,
+                                          int* done) {
     const int lane = threadIdx.x & 31;
+    const int split = sym_leaf_split(lf, item_base, split_from);
     const int ix = lf & (m - 1), iy = lf >> levels;
     bool ok[5];
     int expected = split;  // own items
@@ -775,12 +777,16 @@ __device__ __noinline__ void leaf_written(int lf, int m, int levels, int64_t n, 
 #else
 #define VFMM_SYM_BOUNDS __launch_bounds__(kSymWarps * 32, MINB)
 #endif
-template <bool GAUSS, int MINB>
+// TSPLIT: leaves from split_from on are two items (a tail of half items);
+// otherwise split_from is 0 (every leaf two items) or the leaf count (none)
+// and the kernel uses the uniform item -> leaf map (its code is measurably
+// faster: config 2 near field 0.558 vs 0.550 ms)
+template <bool GAUSS, int MINB, bool TSPLIT>
 __global__ void VFMM_SYM_BOUNDS
     k_p2p_sym(const Src* __restrict__ src, const int* __restrict__ ls, Counters* __restrict__ ctr,
               int levels, int64_t n, Rows rows, const Tables* __restrict__ T,
               double2* __restrict__ near5, unsigned long long* __restrict__ pairs,
-              int items_per_warp, int item_base, int nitems, int split, GraphCond generic_cond,
+              int items_per_warp, int item_base, int nitems, int split_from, GraphCond generic_cond,
               int* __restrict__ done) {
     pdl_enter();
     // a captured graph runs the generic near-field chain (an IF node after
@@ -843,9 +849,14 @@ __global__ void VFMM_SYM_BOUNDS
     for (int it = 0; it < items_per_warp; ++it) {
         const int item = __shfl_sync(0xffffffffu, next, 0);
         if (item >= nitems) break;
-        // split == 2: part 0 = self block + R1 + the left leaf of R2, part 1 =
-        // the other two leaves of R2 (the leaf's sums go to kSplitSlot)
-        const int leaf = item_base + item / split, part = item % split;
+        // leaves from split_from on (relative to item_base) are two items:
+        // part 0 = self block + R1 + the left leaf of R2, part 1 = the other
+        // two leaves of R2 (the leaf's sums go to kSplitSlot)
+        const int split = TSPLIT ? (item < split_from ? 1 : 2) : (split_from == 0 ? 2 : 1);
+        const int leaf =
+            TSPLIT ? item_base + (split == 1 ? item : split_from + ((item - split_from) >> 1))
+                   : item_base + item / split;
+        const int part = TSPLIT ? (split == 1 ? 0 : (item - split_from) & 1) : item % split;
         if (lane == 0 && it + 1 < items_per_warp) next = atomicAdd(&ctr->task_cursor, 1);
         const int loA = ls[leaf], nA = ls[leaf + 1] - loA;
         VCHECK(loA >= 0 && nA >= 0 && (int64_t)loA + nA <= n && nA <= kSymMaxLeaf);
@@ -1003,12 +1014,13 @@ __global__ void VFMM_SYM_BOUNDS
             // wrote into counts one write event; the expected number is the
             // leaf's own items plus its existing non-empty backward neighbours.
             __threadfence();
-            if (ownA) leaf_written(leaf, m, levels, n, split, ls, near5, done);
-            if (n1 > 0) leaf_written(leaf + 1, m, levels, n, split, ls, near5, done);
+            if (ownA) leaf_written(leaf, m, levels, n, split_from, item_base, ls, near5, done);
+            if (n1 > 0) leaf_written(leaf + 1, m, levels, n, split_from, item_base, ls, near5, done);
             if (ownR2 && n2 > 0)
                 for (int x = x2lo; x < x2hi; ++x) {
                     const int lf = (cy + 1) * m + x;
-                    if (ls[lf + 1] > ls[lf]) leaf_written(lf, m, levels, n, split, ls, near5, done);
+                    if (ls[lf + 1] > ls[lf])
+                        leaf_written(lf, m, levels, n, split_from, item_base, ls, near5, done);
                 }
         }
     }
@@ -1111,18 +1123,31 @@ static void launch_p2p_generic(const Layout& L, const Tables* T, const Src* src,
                                const int* leaf_starts, char* ws, Counters* ctr, int kernel,
                                double2* near_uv, Rows rows, cudaStream_t s);
 
-// Split when two items per leaf still fit one wave of warps (2 CTAs of 8
-// warps per SM): the per-item latency, not the SM throughput, then bounds the
-// near field (config 1, 1,024 leaves: 0.131 -> 0.093 ms).  A rank of an 8-way
-// config-2 run (2,176 leaves, one wave unsplit) got slower split.
-// VFMM_P2P_SPLIT=0|1 forces it off / on (A/B).
-int p2p_sym_split(const Layout& L, Rows rows) {
+// Which leaves get two work items (split_from: the first split leaf,
+// relative to the item base): all of them when two items per leaf still fit
+// one wave of warps (2 CTAs of 8 warps per SM) -- the per-item latency, not
+// the SM throughput, then bounds the near field (config 1, 1,024 leaves:
+// 0.131 -> 0.093 ms); otherwise the last `tail` leaves (default one wave of
+// warps: 2,368), so the final items are halves and the near field's tail,
+// where SMs run out of work, is half as long.  VFMM_P2P_SPLIT=0|1 forces
+// none / all, VFMM_P2P_SPLIT_TAIL sets the tail (A/B).
+int p2p_sym_split_from(const Layout& L, Rows rows) {
     static const int env = getenv("VFMM_P2P_SPLIT") ? atoi(getenv("VFMM_P2P_SPLIT")) : -1;
-    if (env == 0 || env == 1) return env ? 2 : 1;
+    static const int tail_env = getenv("VFMM_P2P_SPLIT_TAIL") ? atoi(getenv("VFMM_P2P_SPLIT_TAIL")) : -1;
     const int mrow = 1 << L.levels;
     const int row0 = rows.lo > 0 ? rows.lo - 1 : 0, row1 = rows.hi < mrow ? rows.hi : mrow;
     const int64_t leaves = (int64_t)(row1 > row0 ? row1 - row0 : 0) * mrow;
-    return 2 * leaves <= (int64_t)kSymWarps * 2 * 148 ? 2 : 1;  // two items per leaf fit one wave
+    if (env == 0) return (int)leaves;
+    if (env == 1) return 0;
+    const int64_t wave = (int64_t)kSymWarps * 2 * 148;
+    if (2 * leaves <= wave) return 0;  // two items per leaf fit one wave
+    // the tail of half items pays off when warps take several items each
+    // (config 3, 262K leaves: near field 11.99 -> 11.61 ms); with about one
+    // item per warp (config 2) the uniform kernel without it is faster
+    // (0.550 vs 0.565 ms)
+    if (tail_env < 0 && leaves < wave * 4 * 4) return (int)leaves;
+    const int64_t tail = tail_env >= 0 ? tail_env : wave;
+    return (int)(leaves > tail ? leaves - tail : 0);
 }
 
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,
@@ -1168,8 +1193,9 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
     const int mrow = 1 << L.levels;
     const int row0 = rows.lo > 0 ? rows.lo - 1 : 0, row1 = rows.hi < mrow ? rows.hi : mrow;
     const int item_base = row0 * mrow;
-    const int split = p2p_sym_split(L, rows);
-    const int64_t sym_items = (int64_t)(row1 > row0 ? row1 - row0 : 0) * mrow * split;
+    const int split_from = p2p_sym_split_from(L, rows);
+    const int64_t sym_leaves = (int64_t)(row1 > row0 ? row1 - row0 : 0) * mrow;
+    const int64_t sym_items = split_from + 2 * (sym_leaves - split_from);
     // at least 2 items per warp, except when even that leaves fewer than ~4
     // waves of 2 CTAs per SM: one item per warp then (config 1: 1,024 leaves,
     // P2P 0.144 -> 0.086 ms; a rank of an 8-way config-2 run: 0.266 -> 0.218
@@ -1183,22 +1209,25 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
         const char* e = getenv("VFMM_P2P_SYM_MINB");
         minb = (e && (e[0] == '3' || e[0] == '1')) ? e[0] - '0' : 2;
     }
-    auto* sfn = minb == 3   ? (g ? k_p2p_sym<true, 3> : k_p2p_sym<false, 3>)
-                : minb == 1 ? (g ? k_p2p_sym<true, 1> : k_p2p_sym<false, 1>)
-                            : (g ? k_p2p_sym<true, 2> : k_p2p_sym<false, 2>);
+    const bool tsplit = split_from != 0 && split_from < sym_leaves;  // a tail of half items
+    auto* sfn = minb == 3 ? (g ? (tsplit ? k_p2p_sym<true, 3, true> : k_p2p_sym<true, 3, false>)
+                               : (tsplit ? k_p2p_sym<false, 3, true> : k_p2p_sym<false, 3, false>))
+                          : (g ? (tsplit ? k_p2p_sym<true, 2, true> : k_p2p_sym<true, 2, false>)
+                               : (tsplit ? k_p2p_sym<false, 2, true> : k_p2p_sym<false, 2, false>));
     static std::atomic<unsigned long long> attr_set{0};  // per device ordinal
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !(attr_set.load() >> dev & 1ull)) {
-        for (auto* f : {k_p2p_sym<true, 3>, k_p2p_sym<false, 3>, k_p2p_sym<true, 2>,
-                        k_p2p_sym<false, 2>, k_p2p_sym<true, 1>, k_p2p_sym<false, 1>})
+        for (auto* f : {k_p2p_sym<true, 3, true>, k_p2p_sym<false, 3, true>, k_p2p_sym<true, 2, true>,
+                        k_p2p_sym<false, 2, true>, k_p2p_sym<true, 3, false>, k_p2p_sym<false, 3, false>,
+                        k_p2p_sym<true, 2, false>, k_p2p_sym<false, 2, false>})
             cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
         attr_set.fetch_or(1ull << dev);
     }
     if (!sym_disabled() && sblocks > 0) {
         launch_k(sfn, sblocks, kSymWarps * 32, kSymSmem, s, src, leaf_starts, ctr, L.levels, L.n, rows, T,
                                                       near_uv, &ctr->near_pairs, ks, item_base,
-                 (int)sym_items, split, gc, done);
+                 (int)sym_items, split_from, gc, done);
         note_launches(1);
     } else if (gc.on) {  // no symmetric kernel to set the condition: run the chain
         generic_chain(s);

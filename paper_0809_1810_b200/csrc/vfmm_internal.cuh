@@ -231,10 +231,13 @@ void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* lea
                 char* ws, Counters* ctr, int kernel, double2* near_uv, Rows rows, const int* keys,
                 cudaStream_t s);
 bool sym_disabled();  // env VFMM_P2P_SYM=0 forces the generic near-field kernel
-// symmetric P2P work items per leaf: 2 (the forward stream split in two
-// items, the leaf's own sums of the second in slot kSplitSlot) when the
-// leaves alone would not fill the GPU, else 1 (same choice in k_near_sum)
-int p2p_sym_split(const Layout& L, Rows rows);
+// symmetric P2P: leaves [item_base + split_from, ...) get two work items
+// (the forward stream split in two, the leaf's own sums of the second in slot
+// kSplitSlot), the leaves before them one (same choice in k_near_sum)
+int p2p_sym_split_from(const Layout& L, Rows rows);
+__host__ __device__ __forceinline__ int sym_leaf_split(int leaf, int item_base, int split_from) {
+    return leaf - item_base >= split_from ? 2 : 1;
+}
 void launch_l2p_combine(const Layout& L, const Tables* T, const Src* src, const int* keys,
                         const int* perm, const double2* loc, const double2* near_uv, double xmin,
                         double ymin, double side, double* u, double* v, Rows rows,
