@@ -114,19 +114,26 @@ __global__ void __launch_bounds__(128)
     const double cx = cell_center(xmin, ix, r), cy = cell_center(ymin, iy, r);
     const double inv_r = 1.0 / r;
     if (live) {
-        for (int j = lo + sub; j < hi; j += G) {
-            const Src s = src[j];
-            const double wx = (s.x - cx) * inv_r, wy = (s.y - cy) * inv_r;
-            double tx = s.g, ty = 0.0;
+        // the next particle's record is loaded while the current one's powers
+        // are summed (the load had stalled every iteration: long_scoreboard);
+        // the power loop leaves at k = P (uniform) instead of predicating
+        // PMAX - P idle steps
+        int j = lo + sub;
+        double3 nxt = make_double3(0.0, 0.0, 0.0);
+        if (j < hi) nxt = make_double3(src[j].x, src[j].y, src[j].g);
+        for (; j < hi; j += G) {
+            const double3 sj = nxt;
+            if (j + G < hi) nxt = make_double3(src[j + G].x, src[j + G].y, src[j + G].g);
+            const double wx = (sj.x - cx) * inv_r, wy = (sj.y - cy) * inv_r;
+            double tx = sj.z, ty = 0.0;
 #pragma unroll
             for (int k = 0; k < PMAX; ++k) {
-                if (k < P) {
-                    ax[k] += tx;
-                    ay[k] += ty;
-                    const double nx = tx * wx - ty * wy;
-                    ty = tx * wy + ty * wx;
-                    tx = nx;
-                }
+                if (k >= P) break;
+                ax[k] += tx;
+                ay[k] += ty;
+                const double nx = tx * wx - ty * wy;
+                ty = tx * wy + ty * wx;
+                tx = nx;
             }
         }
     }

@@ -102,6 +102,13 @@ __global__ void __launch_bounds__(BT, MINB) k_ring(const double* __restrict__ po
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     constexpr int NR = V == 1 ? 8 : (V == 2 ? 6 : (V == 3 ? 2 : 4));
+    __shared__ double4 rot[8][32];  // V == 4: the rotating chunk's (x, y, g) per warp
+    if (V == 4) {
+        rot[threadIdx.x >> 5][lane] = make_double4(pos[(gw * 64 + 200 + lane) % 4096 * 2],
+                                                   pos[(gw * 64 + 200 + lane) % 4096 * 2 + 1], 0.5, 0.0);
+        __syncwarp();
+    }
+    const double4* rw = rot[threadIdx.x >> 5];
     double ax[NR], ay[NR], ag[NR], u[NR], v[NR];
 #pragma unroll
     for (int k = 0; k < NR; ++k) {
@@ -167,6 +174,23 @@ __global__ void __launch_bounds__(BT, MINB) k_ring(const double* __restrict__ po
                         vb = fma(-cb, dx[k], vb);
                     }
                 }
+            } else if (V == 4) {
+                const double4 b = rw[(lane + st) & 31];
+                double dx[4], dy[4], K[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    dx[k] = ax[k] - b.x;
+                    dy[k] = ay[k] - b.y;
+                }
+                pair_kernels<4, TAB, ABL>(dx, dy, K, q2, tab);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const double ca = b.z * K[k], cb = ag[k] * K[k];
+                    u[k] = fma(-ca, dy[k], u[k]);
+                    v[k] = fma(ca, dx[k], v[k]);
+                    ub = fma(cb, dy[k], ub);
+                    vb = fma(-cb, dx[k], vb);
+                }
             } else if (V == 0) {
                 double dx[4], dy[4], K[4];
 #pragma unroll
@@ -203,7 +227,10 @@ __global__ void __launch_bounds__(BT, MINB) k_ring(const double* __restrict__ po
                     }
                 }
             }
-            if (ABL & 1) {
+            if (V == 4) {
+                ub = __shfl_sync(0xffffffffu, ub, from);
+                vb = __shfl_sync(0xffffffffu, vb, from);
+            } else if (ABL & 1) {
                 bx += 1e-9;
                 by -= 1e-9;
             } else {
@@ -273,6 +300,7 @@ int main(int argc, char** argv) {
     run("ring6 384thr MINB1", k_ring<0, 2, 1, 0, 384>, kTabN * 8, 1, 6, 384);
     run("ring6 256thr MINB1", k_ring<0, 2, 1, 0, 256>, kTabN * 8, 1, 6, 256);
     run("ring4 256thr MINB1", k_ring<0, 0, 1, 0, 256>, kTabN * 8, 1, 4, 256);
+    run("ring4 smem-positions MINB2", k_ring<0, 4, 2, 0, 256>, kTabN * 8, 2, 4, 256);
     run("ring2 256thr MINB2", k_ring<0, 3, 2, 0, 256>, kTabN * 8, 2, 2, 256);
     run("ring2 256thr MINB1", k_ring<0, 3, 1, 0, 256>, kTabN * 8, 1, 2, 256);
     run("ring8 abl no-shfl,lds,mufu", k_ring<0, 1, 1, 7>, kTabN * 8, 1, 8);
