@@ -57,8 +57,9 @@ __global__ void __launch_bounds__(kSubThreads)
         const bool inside = ((cy * side) << (levels - lf)) >= rows.lo &&
                             ((cy * side + side) << (levels - lf)) <= rows.hi;
         for (int i = threadIdx.x; i < ncell * P; i += blockDim.x) {
-            const int k = i / ncell, r = i % ncell;
-            const int plane = r / (hs * hs), hy = (r / hs) % hs, hx = r % hs;
+            // (powers of two: shifts and masks instead of runtime divisions)
+            const int k = i >> (2 * depth), r = i & (ncell - 1);
+            const int plane = r >> (2 * depth - 2), hy = (r >> (depth - 1)) & (hs - 1), hx = r & (hs - 1);
             const int lx = 2 * hx + (plane & 1), ly = 2 * hy + (plane >> 1);
             // cells whose leaf rows lie outside the strip contribute nothing
             // (sharded partial sums: a coarse parent collects only this rank's
@@ -90,8 +91,8 @@ __global__ void __launch_bounds__(kSubThreads)
             const int i = i0 + (threadIdx.x >> 3);
             const bool act = i < nitem;
             // coefficient-major: consecutive groups write consecutive cells
-            const int c = act ? i % (side * side) : 0, mm = act ? i / (side * side) : 0;
-            const int px = c % side, py = c / side;
+            const int c = act ? i & (side * side - 1) : 0, mm = act ? i >> (2 * s) : 0;
+            const int px = c & (side - 1), py = c >> s;
             double ax = 0.0, ay = 0.0;
             if (act) {
                 for (int t = l8; t < 4 * (mm + 1); t += 8) {

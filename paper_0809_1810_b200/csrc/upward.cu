@@ -6,6 +6,9 @@
 // M_n = a_n / (r^{n+1} n!) (vfmm_internal.cuh), which makes the shift
 // operator level independent:  P_m = 2^{-(m+1)} sum_{k<=m} M_k E_q[m-k],
 // in the planar coefficient layout (coef_base / coef_stride).
+#include <cstdlib>
+#include <type_traits>
+
 #include "vfmm_internal.cuh"
 
 namespace vfmm {
@@ -175,17 +178,38 @@ void launch_p2m(const Layout& L, const Src* src, const int* leaf_starts, double 
     // (mean occupancy <= 256); the warp-per-leaf transpose kernel otherwise
     const bool grp = L.P <= 32 && L.n <= 256 * (int64_t)L.nleaves;
     if (grp) {
-        constexpr int G = 8;
-        const unsigned blocks = (unsigned)((nl * G + 127) / 128);
-        if (L.P <= 16)
-            launch_k(k_p2m_grp<G, 16>, blocks, 128, 0, s, src, leaf_starts, L.levels, L.P, xmin, ymin,
-                                                    side, T, rows, mult_leaf);
-        else if (L.P <= 24)
-            launch_k(k_p2m_grp<G, 24>, blocks, 128, 0, s, src, leaf_starts, L.levels, L.P, xmin, ymin,
-                                                    side, T, rows, mult_leaf);
+        // Lanes per leaf: the fewest of 2 / 4 / 8 that still give ~12 warps
+        // per SM (fewer lanes: longer per-lane sums, a shorter butterfly).
+        // Measured upward pass (P2M + M2M), G = 8 / 4 / 2: config 2 54.2 /
+        // 52.3 / 55.6 us, config 3 0.562 / 0.507 / 0.486 ms, config 1 21.5 /
+        // 25.6 / 33.8 us.  VFMM_P2M_G=2|4|8|16 overrides (A/B).
+        static const int genv = getenv("VFMM_P2M_G") ? atoi(getenv("VFMM_P2M_G")) : 0;
+        int gsel = genv;
+        if (gsel <= 0) {
+            const int64_t want = 148 * 384;  // threads
+            gsel = nl * 2 >= want ? 2 : (nl * 4 >= want ? 4 : 8);
+        }
+        auto go = [&](auto g_tag) {
+            constexpr int G = decltype(g_tag)::value;
+            const unsigned blocks = (unsigned)((nl * G + 127) / 128);
+            if (L.P <= 16)
+                launch_k(k_p2m_grp<G, 16>, blocks, 128, 0, s, src, leaf_starts, L.levels, L.P, xmin,
+                         ymin, side, T, rows, mult_leaf);
+            else if (L.P <= 24)
+                launch_k(k_p2m_grp<G, 24>, blocks, 128, 0, s, src, leaf_starts, L.levels, L.P, xmin,
+                         ymin, side, T, rows, mult_leaf);
+            else
+                launch_k(k_p2m_grp<G, 32>, blocks, 128, 0, s, src, leaf_starts, L.levels, L.P, xmin,
+                         ymin, side, T, rows, mult_leaf);
+        };
+        if (gsel == 2)
+            go(std::integral_constant<int, 2>{});
+        else if (gsel == 4)
+            go(std::integral_constant<int, 4>{});
+        else if (gsel == 16)
+            go(std::integral_constant<int, 16>{});
         else
-            launch_k(k_p2m_grp<G, 32>, blocks, 128, 0, s, src, leaf_starts, L.levels, L.P, xmin, ymin,
-                                                    side, T, rows, mult_leaf);
+            go(std::integral_constant<int, 8>{});
     } else {
         launch_k(k_p2m, (unsigned)((nl + kP2MWarps - 1) / kP2MWarps), kP2MWarps * 32, 0, s, 
             src, leaf_starts, L.levels, L.P, xmin, ymin, side, T, rows, mult_leaf);
