@@ -545,7 +545,7 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
     if (up) {
         if (!hio) rec(0, cs);
         // ---- build: binning, stable sort, pack, leaf starts, occupancy, tasks ----
-        launch_init_counters(ctr, cs);
+        // (the counters are zeroed by the build's first kernel)
         launch_build(L, x, y, gamma, kernel == VFMM_KERNEL_GAUSSIAN ? sigma : nullptr, xmin, ymin,
                      side, ws, ctr, cs, &keys, &perm, gs_ready, sigma_scalar ? 0 : 1, rows,
                      lsd_branch ? R->lsd : nullptr, R->lsd_fork, R->lsd_join);

@@ -457,9 +457,14 @@ __device__ __forceinline__ int block_excl_256(int v, int* wsum) {
 __global__ void __launch_bounds__(kTileThreads)
     k_keys_ghist(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                  double xmin, double ymin, double side, int levels, int bits, int passes,
-                 int* __restrict__ key, int* __restrict__ ghist, Counters* __restrict__ ctr) {
+                 int* __restrict__ key, int* __restrict__ ghist, unsigned* __restrict__ lb,
+                 int64_t lb_words, Counters* __restrict__ ctr) {
     pdl_enter();
     if (!ctr->sort_fallback) return;  // the counting path built the tree
+    // this tile's decoupled look-back words of every pass (zeroed here, on
+    // the LSD path only, instead of in the build's first kernel)
+    for (int i = threadIdx.x; i < passes << bits; i += kTileThreads)
+        lb[(int64_t)(i >> bits) * lb_words + ((int64_t)blockIdx.x << bits) + (i & ((1 << bits) - 1))] = 0u;
     const bool probe_lsd = ctr->sort_fallback == kSortLsdProbe;
     __shared__ int h[4 * 256];
     const int B = 1 << bits;
@@ -932,6 +937,11 @@ __device__ void sort_probe(const ProbeArgs& a, Counters* ctr) {
 __global__ void k_zero_regions(ZeroRegions z, ProbeArgs pa, Counters* ctr) {
     pdl_enter();
     if (blockIdx.x == 0) {
+        // the counters first (instead of a memset node, which would break
+        // the programmatic-launch chain), then the probe that sets one of them
+        for (int i = threadIdx.x; i < (int)(sizeof(Counters) / sizeof(int)); i += blockDim.x)
+            reinterpret_cast<int*>(ctr)[i] = 0;
+        __syncthreads();
         sort_probe(pa, ctr);
         return;
     }
@@ -982,7 +992,7 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     {
         ZeroRegions z{{(int*)(ws + L.scan_state), ls, fill, ghist, (int*)(ws + L.near_done)},
                       {(int64_t)(L.scan_state_bytes / sizeof(int)), (int64_t)L.nleaves + 1,
-                       (int64_t)L.nleaves, (int64_t)(L.hist_bytes / sizeof(int)), (int64_t)L.nleaves}};
+                       (int64_t)L.nleaves, (int64_t)L.passes * B + 8, (int64_t)L.nleaves}};
         const ProbeArgs pa{x, y, L.n, xmin, ymin, side, L.levels, force_lsd()};
         launch_k(k_zero_regions, 297, 256, 0, s, z, pa, ctr);
         note_launches(1);
@@ -1026,7 +1036,7 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     const size_t lb_words = (size_t)L.nchunks * B;
     const unsigned tiles = (unsigned)L.nchunks;
     launch_k(k_keys_ghist, tiles, kTileThreads, 0, ls_s, x, y, L.n, xmin, ymin, side, L.levels, bits,
-                                                L.passes, kbuf[0], ghist, ctr);
+             L.passes, kbuf[0], ghist, lbase, (int64_t)lb_words, ctr);
     note_launches(1);
     for (int p = 0; p < L.passes; ++p) {
         const bool last = p == L.passes - 1;
