@@ -76,6 +76,11 @@ extern "C" {
                                     Whether the near field still has to run is taken from what that
                                     PHASE_UP recorded for the workspace, not from this call's
                                     VFMM_FLAG_OVERLAP; PHASE_DOWN without a PHASE_UP -> VFMM_EINVAL */
+#define VFMM_FLAG_GRAPH_PHASES 512u /* while the call is captured into a CUDA graph (and without
+                                   VFMM_FLAG_STATS): its phase events become event-record nodes of
+                                   the graph; after a replay vfmm_graph_phase_times() reads the
+                                   phase times as the graph ran them (benchmarks; one such graph per
+                                   device at a time) */
 #define VFMM_FLAG_GRAPH 256u    /* vfmm_evaluate_host: run the device part as a CUDA graph, captured
                                    on first use and cached per (device, workspace, n, levels, order,
                                    kernel, domain, flags); the copies stay plain async copies on
@@ -237,6 +242,12 @@ int vfmm_fp64_probe(double* sink, int blocks, int iters, double* flops, void* st
  * the generic near field) is put in the body of an IF conditional node that
  * a kernel of the taken path sets; those body launches are not counted.    */
 int64_t vfmm_launch_count(void);
+
+/* Phase times of the last replay of a graph captured with
+ * VFMM_FLAG_GRAPH_PHASES on `device`: ms[0..7] = elapsed from the call's
+ * start to: built, upward, m2l, downward, near joined, end, near start, near
+ * end (-1 for an event the call did not record).  Synchronise first.       */
+int vfmm_graph_phase_times(int device, float* ms);
 
 /* Version / build string. */
 const char* vfmm_version(void);

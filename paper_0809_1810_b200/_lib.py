@@ -33,6 +33,7 @@ FLAG_PHASE_DOWN = 16
 FLAG_UV_PAIRS = 32
 FLAG_SIGMA_SCALAR = 128
 FLAG_GRAPH = 256
+FLAG_GRAPH_PHASES = 512
 
 ORDER_CAP = 60
 LEVELS_CAP = 13
@@ -56,6 +57,7 @@ EXPORTED_SYMBOLS = (
     "vfmm_direct",
     "vfmm_fp64_probe",
     "vfmm_launch_count",
+    "vfmm_graph_phase_times",
     "vfmm_version",
 )
 
@@ -142,6 +144,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.vfmm_fp64_probe.argtypes = [_P, _I, _I, ctypes.POINTER(_D), _P]
         lib.vfmm_version.restype = ctypes.c_char_p
         lib.vfmm_launch_count.argtypes = []
+        lib.vfmm_graph_phase_times.argtypes = [_I, ctypes.POINTER(ctypes.c_float)]
         for name in EXPORTED_SYMBOLS:
             if name not in ("vfmm_version", "vfmm_launch_count"):
                 getattr(lib, name).restype = _I

@@ -48,6 +48,7 @@ struct Resources {
     cudaEvent_t fork = nullptr, join_far = nullptr, join_near = nullptr;
     cudaEvent_t xy = nullptr, gs = nullptr, done = nullptr;
     cudaEvent_t ev[9] = {};
+    cudaEvent_t gev[9] = {};  // VFMM_FLAG_GRAPH_PHASES: event-record nodes of a captured call
     Counters* hctr = nullptr;  // pinned staging of the device counters (stats)
     // Serialises the calls on this device: the internal streams, events and
     // the pinned counter staging above are shared, so one call enqueues (and,
@@ -183,6 +184,7 @@ Resources* resources_for(int dev) {
         cudaEventCreateWithFlags(&r.join_far, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&r.join_near, cudaEventDisableTiming);
         for (auto& e : r.ev) cudaEventCreate(&e);
+        for (auto& e : r.gev) cudaEventCreate(&e);
         r.ready = true;
     }
     return &r;
@@ -505,8 +507,21 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
     auto near_field = [&](cudaStream_t st) {  // P2P, then the per-particle near total
         launch_p2p(L, T, src, ls, ws, ctr, kernel, near_uv, rows, keys, st);
     };
+    // VFMM_FLAG_GRAPH_PHASES while captured: the phase events become
+    // event-record nodes of the graph (read after a replay by
+    // vfmm_graph_phase_times), so the phases are timed as the graph runs them
+    bool gphases = false;
+    if ((flags & VFMM_FLAG_GRAPH_PHASES) && !timed) {
+        cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+        gphases = cudaStreamIsCapturing((cudaStream_t)stream, &cst) == cudaSuccess &&
+                  cst == cudaStreamCaptureStatusActive;
+        cudaGetLastError();
+    }
     auto rec = [&](int i, cudaStream_t st) {
-        if (phases || (timed && (i == 0 || i == 6))) cudaEventRecord(R->ev[i], st);
+        if (gphases)
+            cudaEventRecordWithFlags(R->gev[i], st, cudaEventRecordExternal);
+        else if (phases || (timed && (i == 0 || i == 6)))
+            cudaEventRecord(R->ev[i], st);
     };
     for (int i = 0; i < 9; ++i) rec(i, s);  // every event defined even for a single phase
 
@@ -1053,6 +1068,22 @@ int vfmm_direct(const double* tx, const double* ty, int64_t m, const double* x, 
 }
 
 int64_t vfmm_launch_count(void) { return (int64_t)g_launches.load(); }
+
+int vfmm_graph_phase_times(int device, float* ms) {
+    if (!ms || device < 0 || device >= kMaxDevices) return VFMM_EINVAL;
+    Resources* R = &g_res[device];
+    if (!R->ready) return VFMM_EINVAL;
+    std::lock_guard<std::recursive_mutex> lk(R->mu);
+    for (int i = 1; i < 9; ++i) {
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, R->gev[0], R->gev[i]) != cudaSuccess) {
+            cudaGetLastError();
+            t = -1.f;  // not recorded by the captured call (e.g. a phase it did not run)
+        }
+        ms[i - 1] = t;
+    }
+    return VFMM_OK;
+}
 
 int vfmm_fp64_probe(double* sink, int blocks, int iters, double* flops, void* stream) {
     if (!sink || blocks < 1 || iters < 1) return VFMM_EINVAL;
