@@ -43,6 +43,7 @@ __device__ __forceinline__ unsigned long long ordered_bits(double d) {
 }
 
 constexpr int kFastLeafMax = 128;  // leaves the counting path sorts with one warp
+constexpr int kBinILP = 4;         // particles per thread in flight in the binning kernels
 // Counters::sort_fallback: 0 counting path, else the LSD radix path because
 // the input looked spatially incoherent (probe) or a leaf is too large.
 constexpr int kSortLsdProbe = 1, kSortLsdBigLeaf = 2;
@@ -108,25 +109,39 @@ __global__ void __launch_bounds__(256)
     const int m = 1 << levels;
     const double inv = 1.0 / side;
     const double xmax = xmin + side, ymax = ymin + side;  // Domain.xmax (model.py:51-57)
-    // grid-stride over whole warps (a capped grid: cheap to skip in LSD mode)
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = i0 + threadIdx.x;
-        int k = -1;
-        if (i < n) {
-            const double xi = x[i], yi = y[i];
-            int ix = 0, iy = 0;
-            if ((xi >= xmin) && (xi <= xmax) && (yi >= ymin) && (yi <= ymax)) {
-                ix = cell_of(xi, xmin, side, inv, m);
-                iy = cell_of(yi, ymin, side, inv, m);
-            } else {
-                atomicAdd(&ctr->bad_count, 1);
-                atomicMax(&ctr->first_bad_neg, INT_MAX - (int)i);
-            }
-            k = iy * m + ix;
-            key[i] = k;
+    // grid-stride over tiles of kBinILP x 256 particles; a thread's kBinILP
+    // positions are loaded together (the single load per thread had every
+    // warp waiting on memory: 1.5 TB/s), then binned one 256-slice at a time
+    // (warp-aggregated atomics per slice)
+    const int64_t tile = (int64_t)kBinILP * blockDim.x;
+    for (int64_t t0 = (int64_t)blockIdx.x * tile; t0 < n; t0 += (int64_t)gridDim.x * tile) {
+        double xs[kBinILP], ys[kBinILP];
+#pragma unroll
+        for (int u = 0; u < kBinILP; ++u) {
+            const int64_t i = t0 + u * blockDim.x + threadIdx.x;
+            xs[u] = i < n ? x[i] : 0.0;
+            ys[u] = i < n ? y[i] : 0.0;
         }
-        const unsigned peers = __match_any_sync(0xffffffffu, k);
-        if (k >= 0 && lane == __ffs(peers) - 1) atomicAdd(&cnt[k], __popc(peers));
+#pragma unroll
+        for (int u = 0; u < kBinILP; ++u) {
+            const int64_t i = t0 + u * blockDim.x + threadIdx.x;
+            int k = -1;
+            if (i < n) {
+                const double xi = xs[u], yi = ys[u];
+                int ix = 0, iy = 0;
+                if ((xi >= xmin) && (xi <= xmax) && (yi >= ymin) && (yi <= ymax)) {
+                    ix = cell_of(xi, xmin, side, inv, m);
+                    iy = cell_of(yi, ymin, side, inv, m);
+                } else {
+                    atomicAdd(&ctr->bad_count, 1);
+                    atomicMax(&ctr->first_bad_neg, INT_MAX - (int)i);
+                }
+                k = iy * m + ix;
+                key[i] = k;
+            }
+            const unsigned peers = __match_any_sync(0xffffffffu, k);
+            if (k >= 0 && lane == __ffs(peers) - 1) atomicAdd(&cnt[k], __popc(peers));
+        }
     }
 }
 
@@ -227,19 +242,36 @@ __global__ void __launch_bounds__(256)
     const int lane = threadIdx.x & 31;
     bool big = false;
     const unsigned nb = gridDim.x - ca.ctas;
-    for (int64_t i0 = (int64_t)(blockIdx.x - ca.ctas) * blockDim.x; i0 < n; i0 += (int64_t)nb * blockDim.x) {
-        const int64_t i = i0 + threadIdx.x;
-        const int k = i < n ? key[i] : -1;
-        const unsigned peers = __match_any_sync(0xffffffffu, k);
-        const int leader = __ffs(peers) - 1;
-        int base = 0;
-        if (k >= 0 && lane == leader) base = atomicAdd(&fill[k], __popc(peers));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        if (k >= 0) {
-            const int lo = ls[k];
-            VCHECK(lo >= 0 && lo + base + __popc(peers & ((1u << lane) - 1u)) < ls[k + 1]);
-            slot[lo + base + __popc(peers & ((1u << lane) - 1u))] = (int)i;
-            big |= ls[k + 1] - lo > kFastLeafMax;
+    // tiles of kBinILP x 256 particles: the keys, then their leaf ranges, are
+    // loaded together before the slots are claimed one 256-slice at a time
+    const int64_t tile = (int64_t)kBinILP * blockDim.x;
+    for (int64_t t0 = (int64_t)(blockIdx.x - ca.ctas) * tile; t0 < n; t0 += (int64_t)nb * tile) {
+        int ks[kBinILP], lo[kBinILP], hi[kBinILP];
+#pragma unroll
+        for (int u = 0; u < kBinILP; ++u) {
+            const int64_t i = t0 + u * blockDim.x + threadIdx.x;
+            ks[u] = i < n ? key[i] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < kBinILP; ++u) {
+            lo[u] = ks[u] >= 0 ? ls[ks[u]] : 0;
+            hi[u] = ks[u] >= 0 ? ls[ks[u] + 1] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kBinILP; ++u) {
+            const int64_t i = t0 + u * blockDim.x + threadIdx.x;
+            const int k = ks[u];
+            const unsigned peers = __match_any_sync(0xffffffffu, k);
+            const int leader = __ffs(peers) - 1;
+            int base = 0;
+            if (k >= 0 && lane == leader) base = atomicAdd(&fill[k], __popc(peers));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (k >= 0) {
+                const int pos = lo[u] + base + __popc(peers & ((1u << lane) - 1u));
+                VCHECK(lo[u] >= 0 && pos < hi[u]);
+                slot[pos] = (int)i;
+                big |= hi[u] - lo[u] > kFastLeafMax;
+            }
         }
     }
     if (__any_sync(0xffffffffu, big) && lane == 0) atomicMax(&ctr->sort_fallback, kSortLsdBigLeaf);
@@ -998,13 +1030,13 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
         note_launches(1);
     }
     // ---- counting path (kernels return at once if the probe chose LSD) ----
-    launch_k(k_bin_count, small_grid(L.n, 2368), 256, 0, s, x, y, L.n, xmin, ymin, side, L.levels,
+    launch_k(k_bin_count, small_grid((L.n + kBinILP - 1) / kBinILP, 2368), 256, 0, s, x, y, L.n, xmin, ymin, side, L.levels,
                                                   kbuf[(L.passes + 1) & 1], ls, ctr);
     note_launches(1);
     launch_scan_i32(ls, (int64_t)L.nleaves + 1, state(L.passes + 1), s, nullptr, false,
                     &ctr->sort_fallback, kSortLsdProbe);
     int* slot = vbuf[(L.passes + 1) & 1];
-    launch_k(k_bin_scatter, small_grid(L.n, 2368) + ca.ctas, 256, 0, s, kbuf[(L.passes + 1) & 1], L.n,
+    launch_k(k_bin_scatter, small_grid((L.n + kBinILP - 1) / kBinILP, 2368) + ca.ctas, 256, 0, s, kbuf[(L.passes + 1) & 1], L.n,
              ls, fill, slot, ctr, ca);
     note_launches(1);
     // The path choice is final after k_bin_scatter (a leaf > 128 switches to
