@@ -189,6 +189,9 @@ constexpr int kRingUnroll = VFMM_RING_UNROLL;  // steps of a full ring per loop 
 // scheduler overlap a step's tail with the next one's head (config 2 near
 // field 0.578 -> 0.565 ms, step 0.7335 -> 0.7222 ms; 4: no further gain)
 constexpr int kRing4Unroll = VFMM_RING4_UNROLL;
+#ifndef VFMM_RING4_UNROLL_RAGGED
+#define VFMM_RING4_UNROLL_RAGGED 1
+#endif
 #ifndef VFMM_SELF_UNROLL
 #define VFMM_SELF_UNROLL 1
 #endif
@@ -369,14 +372,14 @@ __device__ __forceinline__ void rotate_ring(double a0x, double a0y, double a0g, 
 // Four resident particles per lane (a resident pass of 128): four independent
 // pair chains per step and one rotation of the source (and its sums) per four
 // pairs.  Symmetric only.
-template <bool GAUSS, int R>
+template <bool GAUSS, int R, int UNR = kRing4Unroll>
 __device__ __forceinline__ void rotate_ring4(const double (&ax)[4], const double (&ay)[4],
                                              const double (&ag)[4], double bx, double by,
                                              double bg, double& ub, double& vb, SymExp q2,
                                              const double* __restrict__ tab, double (&u)[4],
                                              double (&v)[4]) {
     const int from = ((threadIdx.x & 31) + 1) & (R - 1);
-#pragma unroll(kRing4Unroll)
+#pragma unroll(UNR)
     for (int st = 0; st < R; ++st) {
         double dx[4], dy[4], K[4];
 #pragma unroll
@@ -408,7 +411,7 @@ __device__ __forceinline__ void rotate_ring4(const double (&ax)[4], const double
 
 // The leaf [loB, loB + nB) rotating past four residents per lane; its sums
 // start from and return to acc[] in shared memory.
-template <bool GAUSS>
+template <bool GAUSS, int UNR = kRing4Unroll>
 __device__ __forceinline__ void rotate_leaf4(const Src* __restrict__ src, const double (&ax)[4],
                                              const double (&ay)[4], const double (&ag)[4], int loB,
                                              int nB, double2* acc, SymExp q2,
@@ -438,11 +441,11 @@ __device__ __forceinline__ void rotate_leaf4(const Src* __restrict__ src, const 
             vb = t.y;
         }
         if (R == 32)
-            rotate_ring4<GAUSS, 32>(ax, ay, ag, bx, by, bg, ub, vb, q2, tab, u, v);
+            rotate_ring4<GAUSS, 32, UNR>(ax, ay, ag, bx, by, bg, ub, vb, q2, tab, u, v);
         else if (R == 16)
-            rotate_ring4<GAUSS, 16>(ax, ay, ag, bx, by, bg, ub, vb, q2, tab, u, v);
+            rotate_ring4<GAUSS, 16, UNR>(ax, ay, ag, bx, by, bg, ub, vb, q2, tab, u, v);
         else
-            rotate_ring4<GAUSS, 8>(ax, ay, ag, bx, by, bg, ub, vb, q2, tab, u, v);
+            rotate_ring4<GAUSS, 8, UNR>(ax, ay, ag, bx, by, bg, ub, vb, q2, tab, u, v);
         if (lane < cnt) acc[j0 + lane] = make_double2(ub, vb);
         j0 += R;
     }
@@ -960,7 +963,11 @@ __global__ void VFMM_SYM_BOUNDS
                     ag[k] = t < nS ? e.g : 0.0;
                     u[k] = v[k] = 0.0;
                 }
-                rotate_leaf4<GAUSS>(src, ax, ay, ag, loA, nA, accAw, q2, tab, u, v);
+                // ragged leaves (the tail-split instance: large random-order
+                // grids) take many code paths per SM; the ring is not unrolled
+                // there (instruction-fetch stalls, config 3)
+                rotate_leaf4<GAUSS, TSPLIT ? VFMM_RING4_UNROLL_RAGGED : kRing4Unroll>(src, ax, ay, ag, loA, nA,
+                                                                                       accAw, q2, tab, u, v);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const int t = p0 + 32 * k + lane;
