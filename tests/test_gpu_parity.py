@@ -395,3 +395,45 @@ def test_programmatic_launch_off_is_bitwise_identical(tmp_path):
     other = np.load(out)
     mine = np.concatenate([vel.cpu().numpy().ravel(), [st.m2l_count, st.near_pair_count]])
     assert np.array_equal(mine, other)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", ["VFMM_P2P_SPLIT=0", "VFMM_P2P_SPLIT=1", "VFMM_P2P_SPLIT_TAIL=1000",
+                                 "VFMM_P2P_SPLIT_TAIL=0"])
+def test_near_field_item_splits_agree(env, tmp_path):
+    """The symmetric near field's work-item layouts -- one item per leaf, two
+    per leaf, and a tail of two-item leaves (the TSPLIT kernel instance large
+    random grids use, forced here on a 4,096-leaf grid) -- sum the same pairs
+    in different orders: velocities agree to 1e-13 of max|v| (and with the
+    oracle to 1e-12), counters exactly.  The layout is read from the
+    environment at library load, so each runs in a child process."""
+    import subprocess
+    import sys
+
+    rng = np.random.default_rng(11)
+    n, levels, order = 40000, 6, 8
+    x, y = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    g = rng.normal(size=n)
+    s = np.full(n, 0.004)
+    src = tmp_path / "in.npz"
+    np.savez(src, x=x, y=y, g=g, s=s)
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_0809_1810_b200 as vf\n"
+        "d = np.load(%r); cfg = vf.FmmConfig(%d, %d, vf.KernelKind.GAUSSIAN_BLOB)\n"
+        "v, st = vf.evaluate_arrays(d['x'], d['y'], d['g'], d['s'], cfg, vf.Domain(-1.0, -1.0, 2.0), overlap=True)\n"
+        "np.save(sys.argv[1], np.concatenate([v.cpu().numpy().ravel(), [st.m2l_count, st.near_pair_count]]))\n"
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), str(src), levels, order)
+    outs = {}
+    for tag, e in (("default", {}), ("variant", dict([env.split("=")]))):
+        out = tmp_path / f"{tag}.npy"
+        subprocess.run([sys.executable, "-c", code, str(out)], env=dict(os.environ, **e), check=True,
+                       timeout=600)
+        outs[tag] = np.load(out)
+    a, b = outs["default"], outs["variant"]
+    assert np.array_equal(a[-2:], b[-2:]), (a[-2:], b[-2:])
+    va, vb = a[:-2], b[:-2]
+    assert np.abs(va - vb).max() <= 1e-13 * np.abs(va).max()
+    ref, _ = O.evaluate(x, y, g, s, levels, order, True, (-1.0, -1.0, 2.0))
+    got = vb.reshape(2, n).T
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
