@@ -473,7 +473,20 @@ def bench_main(args):
     os.environ.setdefault("WORLD_SIZE", str(world))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    # rank 0 prints ONE JSON line on stdout: NCCL's version banner (printed
+    # when the first communicator comes up) goes to stderr instead
+    import sys as _sys
+    _sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+    finally:
+        _sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
     w = W.by_index(args.config)
     cfg = FmmConfig(w.levels, w.order, KernelKind.GAUSSIAN_BLOB)
     dom = Domain(*W.DOMAIN)
@@ -540,19 +553,47 @@ def bench_main(args):
     ms = torch.tensor([sum(a.elapsed_time(b) for a, b in ev) / args.steps], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
 
-    # end to end from pinned host buffers: owned particles in, owned velocities out
+    # end to end from pinned host buffers: owned particles in, owned velocities
+    # out, every step.  Two steps in flight: step k+1's inputs are copied in on
+    # a copy stream while step k computes, and step k's velocities are copied
+    # out on it while step k+1 computes (the particle-halo size exchange is
+    # the one host synchronisation per step)
     host_cols = owned.cpu().pin_memory()
-    host_vel = torch.empty((2, owned.shape[1]), dtype=torch.float64).pin_memory()
+    k_own = owned.shape[1]
+    host_vel = [torch.empty((2, k_own), dtype=torch.float64).pin_memory() for _ in range(2)]
+    dcols = [torch.empty_like(owned) for _ in range(2)]
+    copy = torch.cuda.Stream(dev)
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_used = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]
     e2e_steps = max(3, args.e2e_steps)
     torch.cuda.synchronize(dev)
     dist.barrier()
+    main = torch.cuda.current_stream(dev)
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        dcols = host_cols.to(dev, non_blocking=True)
-        sh = add_halo(dcols, rows, dom, cfg.levels)
+    with torch.cuda.stream(copy):
+        dcols[0].copy_(host_cols, non_blocking=True)
+        ev_in[0].record(copy)
+    for k in range(e2e_steps):
+        b = k & 1
+        main.wait_event(ev_in[b])
+        if k + 1 < e2e_steps:  # prefetch the next step's inputs into the other buffer
+            if k >= 1:
+                copy.wait_event(ev_used[b ^ 1])
+            with torch.cuda.stream(copy):
+                dcols[b ^ 1].copy_(host_cols, non_blocking=True)
+                ev_in[b ^ 1].record(copy)
+        sh = add_halo(dcols[b], rows, dom, cfg.levels)
         vel, _ = evaluate_shard(sh, cfg, dom, backend=backend, counters=False)
-        host_vel.copy_(vel[:, : owned.shape[1]], non_blocking=True)
-        torch.cuda.synchronize(dev)
+        ev_used[b].record(main)
+        copy.wait_event(ev_used[b])
+        if k >= 2:
+            ev_done[b].synchronize()  # the host buffer of step k - 2 is free
+        vel.record_stream(copy)
+        with torch.cuda.stream(copy):
+            host_vel[b].copy_(vel[:, :k_own], non_blocking=True)
+            ev_done[b].record(copy)
+    torch.cuda.synchronize(dev)
     e2e = torch.tensor([(time.perf_counter() - t0) * 1e3 / e2e_steps], device=dev)
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
     nb = torch.tensor([owned.shape[1]], dtype=torch.int64, device=dev)
@@ -608,7 +649,8 @@ def bench_main(args):
                     "h2d_bytes_per_step": 40 * int(nb), "d2h_bytes_per_step": 16 * int(nb),
                     "ms_per_step": float(e2e),
                     "mode": "per rank: owned particles H2D, halo exchange, sharded evaluate, "
-                            "velocities D2H; wall clock, max over ranks (bytes: largest rank)"},
+                            "velocities D2H, two steps in flight (copies on a copy stream); "
+                            "wall clock, max over ranks (bytes: largest rank)"},
             "gpu_launches": int(launches) * args.steps,
             "roofline": roof, "cpu_baseline": None,
             "clocks": clk.summary() if clk is not None else None,
