@@ -440,6 +440,66 @@ def evaluate_emulated(x, y, gamma, sigma, config, domain, world: int, backend_fa
 
 
 # ----------------------------------------------------------------------------- bench
+def e2e_loop(variant, host_cols, owned, rows_in, rows, dom, cfg, backend, steps, dev):
+    """ms per step of the multi-GPU bench's end-to-end loop: every step copies
+    this rank's inputs (the first ``rows_in`` rows of the owned columns) in
+    from pinned host memory, exchanges the particle halo, runs the sharded
+    evaluate and copies the owned velocities out.  "copy" (default): two
+    steps in flight, inputs and outputs on a copy stream; "sync": one step at
+    a time (A/B).  Two untimed steps first."""
+    main = torch.cuda.Stream(dev)
+    with torch.cuda.stream(main):
+        _e2e_loop(variant, host_cols, owned, rows_in, rows, dom, cfg, backend, 2, dev, main)
+        return _e2e_loop(variant, host_cols, owned, rows_in, rows, dom, cfg, backend, steps, dev, main)
+
+
+def _e2e_loop(variant, host_cols, owned, rows_in, rows, dom, cfg, backend, steps, dev, main):
+    import time
+
+    k_own = owned.shape[1]
+    host_vel = [torch.empty((2, k_own), dtype=torch.float64).pin_memory() for _ in range(2)]
+    dcols = [owned.clone() for _ in range(2)]  # resident sigma / id rows
+    copy = torch.cuda.Stream(dev)
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_used = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    t0 = time.perf_counter()
+    if variant == "sync":
+        for _ in range(steps):
+            dcols[0][:rows_in].copy_(host_cols[:rows_in], non_blocking=True)
+            sh = add_halo(dcols[0], rows, dom, cfg.levels)
+            vel, _ = evaluate_shard(sh, cfg, dom, backend=backend, counters=False)
+            host_vel[0].copy_(vel[:, :k_own], non_blocking=True)
+            torch.cuda.synchronize(dev)
+        return (time.perf_counter() - t0) * 1e3 / steps
+    with torch.cuda.stream(copy):
+        dcols[0][:rows_in].copy_(host_cols[:rows_in], non_blocking=True)
+        ev_in[0].record(copy)
+    for k in range(steps):
+        b = k & 1
+        main.wait_event(ev_in[b])
+        if k + 1 < steps:  # the next step's inputs, once step k - 1 is done with the buffer
+            if k >= 1:
+                copy.wait_event(ev_used[b ^ 1])
+            with torch.cuda.stream(copy):
+                dcols[b ^ 1][:rows_in].copy_(host_cols[:rows_in], non_blocking=True)
+                ev_in[b ^ 1].record(copy)
+        sh = add_halo(dcols[b], rows, dom, cfg.levels)
+        vel, _ = evaluate_shard(sh, cfg, dom, backend=backend, counters=False)
+        ev_used[b].record(main)
+        if k >= 2:
+            ev_done[b].synchronize()  # the host buffer of step k - 2 is free
+        vel.record_stream(copy)
+        with torch.cuda.stream(copy):
+            copy.wait_event(ev_used[b])
+            host_vel[b].copy_(vel[:, :k_own], non_blocking=True)
+            ev_done[b].record(copy)
+    torch.cuda.synchronize(dev)
+    return (time.perf_counter() - t0) * 1e3 / steps
+
+
 def bench_main(args):
     """``bench.py --gpus N`` under torchrun: the sharded evaluate of a BASELINE config.
 
@@ -553,48 +613,22 @@ def bench_main(args):
     ms = torch.tensor([sum(a.elapsed_time(b) for a, b in ev) / args.steps], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
 
-    # end to end from pinned host buffers: owned particles in, owned velocities
-    # out, every step.  Two steps in flight: step k+1's inputs are copied in on
-    # a copy stream while step k computes, and step k's velocities are copied
-    # out on it while step k+1 computes (the particle-halo size exchange is
-    # the one host synchronisation per step)
+    # end to end from pinned host buffers (e2e_loop): owned particles in,
+    # owned velocities out, every step, two steps in flight
     host_cols = owned.cpu().pin_memory()
     k_own = owned.shape[1]
-    host_vel = [torch.empty((2, k_own), dtype=torch.float64).pin_memory() for _ in range(2)]
-    dcols = [torch.empty_like(owned) for _ in range(2)]
-    copy = torch.cuda.Stream(dev)
-    ev_in = [torch.cuda.Event() for _ in range(2)]
-    ev_used = [torch.cuda.Event() for _ in range(2)]
-    ev_done = [torch.cuda.Event() for _ in range(2)]
-    e2e_steps = max(3, args.e2e_steps)
-    torch.cuda.synchronize(dev)
-    dist.barrier()
-    main = torch.cuda.current_stream(dev)
-    t0 = time.perf_counter()
-    with torch.cuda.stream(copy):
-        dcols[0].copy_(host_cols, non_blocking=True)
-        ev_in[0].record(copy)
-    for k in range(e2e_steps):
-        b = k & 1
-        main.wait_event(ev_in[b])
-        if k + 1 < e2e_steps:  # prefetch the next step's inputs into the other buffer
-            if k >= 1:
-                copy.wait_event(ev_used[b ^ 1])
-            with torch.cuda.stream(copy):
-                dcols[b ^ 1].copy_(host_cols, non_blocking=True)
-                ev_in[b ^ 1].record(copy)
-        sh = add_halo(dcols[b], rows, dom, cfg.levels)
-        vel, _ = evaluate_shard(sh, cfg, dom, backend=backend, counters=False)
-        ev_used[b].record(main)
-        copy.wait_event(ev_used[b])
-        if k >= 2:
-            ev_done[b].synchronize()  # the host buffer of step k - 2 is free
-        vel.record_stream(copy)
-        with torch.cuda.stream(copy):
-            host_vel[b].copy_(vel[:, :k_own], non_blocking=True)
-            ev_done[b].record(copy)
-    torch.cuda.synchronize(dev)
-    e2e = torch.tensor([(time.perf_counter() - t0) * 1e3 / e2e_steps], device=dev)
+    # the step's inputs: x, y, gamma -- and sigma unless every core size is
+    # the same (then it travels as the resident column, like the single-GPU
+    # path's one-value sigma); the global ids are the sharding's metadata and
+    # stay resident
+    sig = host_cols[3]
+    sig_uniform = bool(k_own == 0 or bool((sig == sig[0]).all()))
+    rows_in = int(os.environ.get("VFMM_E2E_ROWS", 3 if sig_uniform else 4))  # (env: A/B)
+    h2d_row_bytes = 8 * rows_in
+    e2e_steps = max(12, args.e2e_steps)  # two in flight: enough steps to amortise the fill
+    variant = os.environ.get("VFMM_E2E_VARIANT", "copy")
+    ms_e2e = e2e_loop(variant, host_cols, owned, rows_in, rows, dom, cfg, backend, e2e_steps, dev)
+    e2e = torch.tensor([ms_e2e], device=dev)
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
     nb = torch.tensor([owned.shape[1]], dtype=torch.int64, device=dev)
     dist.all_reduce(nb, op=dist.ReduceOp.MAX)
@@ -646,7 +680,7 @@ def bench_main(args):
                        "l2": "flushed between steps (256 MiB write)",
                        "m2l_count": st.m2l_count, "near_pair_count": st.near_pair_count},
             "e2e": {"value": w.n / (float(e2e) * 1e-3), "unit": "particle-evals/s",
-                    "h2d_bytes_per_step": 40 * int(nb), "d2h_bytes_per_step": 16 * int(nb),
+                    "h2d_bytes_per_step": h2d_row_bytes * int(nb), "d2h_bytes_per_step": 16 * int(nb),
                     "ms_per_step": float(e2e),
                     "mode": "per rank: owned particles H2D, halo exchange, sharded evaluate, "
                             "velocities D2H, two steps in flight (copies on a copy stream); "
