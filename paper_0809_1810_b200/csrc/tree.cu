@@ -5,27 +5,35 @@
 // engine.evaluate (engine.py:355-358): a stable sort of the particles by
 // leaf key (np.argsort(kind="stable")).
 //
-// Counting path (every leaf <= kFastLeafMax particles; config 2: 4 kernels):
+// k_zero_regions    the counters and the scratch regions; CTA 0 samples the
+//                   input order and picks the sort path (probe)
+// Counting path (coherent input order, every leaf <= kFastLeafMax particles;
+// config 2: 5 kernels in all):
 //   k_bin_count     floor-rule binning with max-edge clamp + domain check;
-//                   per-leaf counts (warp-aggregated atomics)
-//   k_scan          counts -> leaf_starts (exclusive, in place)
+//                   per-leaf counts (warp-aggregated atomics), four
+//                   particles per thread in flight
+//   k_scan_one      counts -> leaf_starts (exclusive, in place; one CTA,
+//                   striped int4 accesses; k_scan for long arrays)
 //   k_bin_scatter   particle index -> a slot of its leaf (atomic cursor per
 //                   leaf: the order inside a leaf is not yet the stable one);
-//                   flags the LSD path if a leaf is too large
+//                   flags the LSD path if a leaf is too large; its first
+//                   CTAs compute the occupancy pyramid (Tree.counts) and the
+//                   P2P task counts
 //   k_leaf_pack     warp per leaf: bitonic sort of the leaf's indices (which
 //                   restores the stable order exactly), then perm, sorted
 //                   keys and the packed Src records
-// LSD radix path (a leaf above kFastLeafMax, decided on the device; the
-// kernels below return at once otherwise):
-//   k_keys_ghist    keys + global digit histograms of every pass
-//   k_onesweep      one stable LSD pass per launch over 4096-key tiles:
+// LSD radix path (random input order, or a leaf above kFastLeafMax; decided
+// on the device -- the kernels return at once otherwise, and a captured graph
+// puts them in an IF conditional node):
+//   k_keys_ghist    keys + global digit histograms of every pass (and zeroes
+//                   its tile's look-back words)
+//   k_onesweep      one stable LSD pass per launch over 2048-key tiles:
 //                   warp match_any ranking, per-digit decoupled look-back,
 //                   coalesced digit-run writes; the last pass moves the
 //                   packed Src records (k_pack_orig)
 //   k_leaf_starts   leaf_starts[4^l + 1] (== concatenate([0], cumsum(bincount)))
-// Then, for both:
-//   k_counts_tasks  per-level occupancy pyramid (Tree.counts) + P2P task counts
-//   k_scan, k_tasks_fill   near-field warp task list (generic P2P only)
+//   k_counts_tasks  the occupancy pyramid + task counts of this path
+// Generic near field only: k_scan, k_tasks_fill (the warp task list).
 #include <climits>
 #include <algorithm>
 #include <cstdlib>
