@@ -31,12 +31,25 @@ struct SymExp {
 // TAB: 0 = 60 KB table 2^(n/128); 1 = 1 KB table 2^(j/128), exponent added as an integer
 // ABL (ablations, wrong numerics, cost probes only): 1 no shuffles, 2 no table
 // load, 4 no MUFU (seed from an FMA), 8 no integer clamps
-template <int N, int TAB, int ABL = 0>
+template <int N, int TAB, int ABL = 0, int ORD = 0>
 __device__ __forceinline__ void pair_kernels(const double (&dx)[N], const double (&dy)[N], double (&K)[N],
                                              SymExp q2, const double* __restrict__ tab) {
     double r2[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) r2[k] = fma(dy[k], dy[k], dx[k] * dx[k]);
+    const double kShift0 = 6755399441055744.0;
+    double sr0[N];
+    int ti0[N];
+    if (ORD == 1) {  // exp range reduction before the reciprocal
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            const unsigned hi = min((unsigned)__double2hiint(r2[k]), q2.hi);
+            const double r2c = __hiloint2double((int)hi, __double2loint(r2[k]));
+            const double t = fma(r2c, q2.q, kShift0);
+            ti0[k] = __double2loint(t);
+            sr0[k] = fma(r2c, q2.q, kShift0 - t);
+        }
+    }
 #pragma unroll
     for (int k = 0; k < N; ++k) {
         if (ABL & 4) {
@@ -57,13 +70,21 @@ __device__ __forceinline__ void pair_kernels(const double (&dx)[N], const double
     const double kShift = 6755399441055744.0;
     double sr[N], pp[N];
     int ti[N];
+    if (ORD == 1) {
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-        const unsigned hi = (ABL & 8) ? 0u : min((unsigned)__double2hiint(r2[k]), q2.hi);
-        const double r2c = (ABL & 8) ? r2[k] : __hiloint2double((int)hi, __double2loint(r2[k]));
-        const double t = fma(r2c, q2.q, kShift);
-        ti[k] = __double2loint(t);
-        sr[k] = fma(r2c, q2.q, kShift - t);
+        for (int k = 0; k < N; ++k) {
+            sr[k] = sr0[k];
+            ti[k] = ti0[k];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            const unsigned hi = (ABL & 8) ? 0u : min((unsigned)__double2hiint(r2[k]), q2.hi);
+            const double r2c = (ABL & 8) ? r2[k] : __hiloint2double((int)hi, __double2loint(r2[k]));
+            const double t = fma(r2c, q2.q, kShift);
+            ti[k] = __double2loint(t);
+            sr[k] = fma(r2c, q2.q, kShift - t);
+        }
     }
 #pragma unroll
     for (int k = 0; k < N; ++k) pp[k] = fma(c_p[3], sr[k], c_p[2]);
@@ -88,7 +109,7 @@ __device__ __forceinline__ void pair_kernels(const double (&dx)[N], const double
 }
 
 // V: 0 = ring4 as in k_p2p_sym; 1 = eight residents (two ring4 halves share one rotating source)
-template <int TAB, int V, int MINB, int ABL = 0, int BT = 256>
+template <int TAB, int V, int MINB, int ABL = 0, int BT = 256, int UNR = 2, int ORD = 0>
 __global__ void __launch_bounds__(BT, MINB) k_ring(const double* __restrict__ pos, const double* __restrict__ gtab,
                                                     double* out, int reps, double q2v) {
     extern __shared__ double tab_s[];
@@ -121,7 +142,7 @@ __global__ void __launch_bounds__(BT, MINB) k_ring(const double* __restrict__ po
     double bg = 0.5, ub = 0.0, vb = 0.0;
     const int from = (lane + 1) & 31;
     for (int r = 0; r < reps; ++r) {
-#pragma unroll 2
+#pragma unroll(UNR)
         for (int st = 0; st < 32; ++st) {
             if (V == 3) {  // two residents
                 double dx[2], dy[2], K[2];
@@ -147,7 +168,7 @@ __global__ void __launch_bounds__(BT, MINB) k_ring(const double* __restrict__ po
                         dx[k] = ax[k] - bx;
                         dy[k] = ay[k] - by;
                     }
-                    pair_kernels<4, TAB, ABL>(dx, dy, K, q2, tab);
+                    pair_kernels<4, TAB, ABL, ORD>(dx, dy, K, q2, tab);
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         const double ca = bg * K[k], cb = ag[k] * K[k];
@@ -182,7 +203,7 @@ __global__ void __launch_bounds__(BT, MINB) k_ring(const double* __restrict__ po
                     dx[k] = ax[k] - b.x;
                     dy[k] = ay[k] - b.y;
                 }
-                pair_kernels<4, TAB, ABL>(dx, dy, K, q2, tab);
+                pair_kernels<4, TAB, ABL, ORD>(dx, dy, K, q2, tab);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const double ca = b.z * K[k], cb = ag[k] * K[k];
@@ -198,7 +219,7 @@ __global__ void __launch_bounds__(BT, MINB) k_ring(const double* __restrict__ po
                     dx[k] = ax[k] - bx;
                     dy[k] = ay[k] - by;
                 }
-                pair_kernels<4, TAB, ABL>(dx, dy, K, q2, tab);
+                pair_kernels<4, TAB, ABL, ORD>(dx, dy, K, q2, tab);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const double ca = bg * K[k], cb = ag[k] * K[k];
@@ -216,7 +237,7 @@ __global__ void __launch_bounds__(BT, MINB) k_ring(const double* __restrict__ po
                         dx[k] = ax[4 * h + k] - bx;
                         dy[k] = ay[4 * h + k] - by;
                     }
-                    pair_kernels<4, TAB, ABL>(dx, dy, K, q2, tab);
+                    pair_kernels<4, TAB, ABL, ORD>(dx, dy, K, q2, tab);
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         const double ca = bg * K[k], cb = ag[4 * h + k] * K[k];
@@ -301,6 +322,10 @@ int main(int argc, char** argv) {
     run("ring6 256thr MINB1", k_ring<0, 2, 1, 0, 256>, kTabN * 8, 1, 6, 256);
     run("ring4 256thr MINB1", k_ring<0, 0, 1, 0, 256>, kTabN * 8, 1, 4, 256);
     run("ring4 smem-positions MINB2", k_ring<0, 4, 2, 0, 256>, kTabN * 8, 2, 4, 256);
+    run("ring4 MINB2 unroll1", k_ring<0, 0, 2, 0, 256, 1>, kTabN * 8, 2, 4, 256);
+    run("ring4 MINB2 unroll4", k_ring<0, 0, 2, 0, 256, 4>, kTabN * 8, 2, 4, 256);
+    run("ring4 MINB2 exp-first", k_ring<0, 0, 2, 0, 256, 2, 1>, kTabN * 8, 2, 4, 256);
+    run("ring4 MINB2 exp-first unroll1", k_ring<0, 0, 2, 0, 256, 1, 1>, kTabN * 8, 2, 4, 256);
     run("ring2 256thr MINB2", k_ring<0, 3, 2, 0, 256>, kTabN * 8, 2, 2, 256);
     run("ring2 256thr MINB1", k_ring<0, 3, 1, 0, 256>, kTabN * 8, 1, 2, 256);
     run("ring8 abl no-shfl,lds,mufu", k_ring<0, 1, 1, 7>, kTabN * 8, 1, 8);
