@@ -396,6 +396,86 @@ constexpr OffTab make_offtab() {
 }
 __constant__ OffTab c_off = make_offtab();
 
+// Units of the tiled kernel: as the unit table above, but offsets whose
+// four-member orbit {o, -o, o', -o'} (o' = (dx, -dy)) lies in the class share
+// ONE product (kind 4): with s = (-1)^(m+n+1), A = M(o) + s M(-o) and
+// B = M(o') + s M(-o'), H_o A + conj(H_o) B = Re H_o (A + B) + i Im H_o (A - B)
+// -- four real FMA per (m, n) for four translations, after 16 adds per n
+// shared by the chunk's outputs.  The 5 x 5 ring gives three orbits and two
+// axis pairs, the outer row / column two mirror pairs each, three offsets stay
+// single: 12 products per destination (15 with pairs only).
+#ifndef VFMM_M2L_QUADS
+#define VFMM_M2L_QUADS 1
+#endif
+constexpr int kQUnits = 12;
+struct QuadTab {
+    int8_t o[4][kQUnits][4], kind[4][kQUnits];
+    int count[4];
+};
+constexpr QuadTab make_quads() {
+    QuadTab t{};
+    for (int par = 0; par < 4; ++par) {
+        const int px = par & 1, py = par >> 1;
+        int dxs[27] = {}, dys[27] = {};
+        int idx = 0;
+        for (int yy = -2 - py; yy < 4 - py; ++yy)
+            for (int xx = -2 - px; xx < 4 - px; ++xx) {
+                const int ax = xx < 0 ? -xx : xx, ay = yy < 0 ? -yy : yy;
+                if ((ax > ay ? ax : ay) >= 2) {
+                    dxs[idx] = xx;
+                    dys[idx] = yy;
+                    ++idx;
+                }
+            }
+        auto find = [&](int wx, int wy, const bool* used) {
+            for (int q = 0; q < 27; ++q)
+                if (!used[q] && dxs[q] == wx && dys[q] == wy) return q;
+            return -1;
+        };
+        bool used[27] = {};
+        int nu = 0;
+        for (int o = 0; o < 27; ++o) {
+            if (used[o]) continue;
+            used[o] = true;
+            int mem[4] = {o, -1, -1, -1};
+            int kind = 0;
+            if (dxs[o] != 0 && dys[o] != 0) {
+                const int a = find(-dxs[o], -dys[o], used), b = find(dxs[o], -dys[o], used),
+                          c = find(-dxs[o], dys[o], used);
+                if (a >= 0 && b >= 0 && c >= 0) {
+                    mem[1] = a;
+                    mem[2] = b;
+                    mem[3] = c;
+                    used[a] = used[b] = used[c] = true;
+                    kind = 4;
+                }
+            }
+            for (int k = 0; k < 3 && kind == 0; ++k) {
+                if ((k == 1 && dys[o] == 0) || (k == 2 && dxs[o] == 0)) continue;
+                const int wx = k == 1 ? dxs[o] : -dxs[o], wy = k == 2 ? dys[o] : -dys[o];
+                const int q = find(wx, wy, used);
+                if (q >= 0) {
+                    mem[1] = q;
+                    used[q] = true;
+                    kind = k + 1;
+                }
+            }
+            if (nu < kQUnits) {
+                for (int j = 0; j < 4; ++j) t.o[par][nu][j] = (int8_t)mem[j];
+                t.kind[par][nu] = (int8_t)kind;
+            }
+            ++nu;
+        }
+        t.count[par] = nu;
+    }
+    return t;
+}
+constexpr QuadTab kQuadTab = make_quads();
+static_assert(kQuadTab.count[0] == kQUnits && kQuadTab.count[1] == kQUnits &&
+                  kQuadTab.count[2] == kQUnits && kQuadTab.count[3] == kQUnits,
+              "12 units per parity class");
+__constant__ QuadTab c_quads = kQuadTab;
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return (unsigned)__cvta_generic_to_shared(p);
 }
@@ -486,6 +566,46 @@ __device__ __forceinline__ void tile_pair(const double2* __restrict__ s1, const 
 #pragma unroll
         for (int t = 0; t < TN; ++t) hv[t] = h[n + t];
         tile_pair_step<TN, KIND, MP>(s1[n * kWinCells], s2[n * kWinCells], hv, 0, A);
+    }
+}
+
+// One four-member orbit unit (kind 4) for outputs m0 .. m0+TN-1 (MP =
+// parity of m0): X = A + B, Y = A - B with A = M1 + s M2, B = M3 + s M4,
+// s = (-1)^(m+n+1) (m + n odd: s = +1).
+template <int TN, int MP>
+__device__ __forceinline__ void tile_quad_step(double2 a1, double2 a2, double2 a3, double2 a4,
+                                               const double2* hv, int np, TileAcc<TN>& A) {
+    const double apr = a1.x + a2.x, api = a1.y + a2.y, amr = a1.x - a2.x, ami = a1.y - a2.y;
+    const double bpr = a3.x + a4.x, bpi = a3.y + a4.y, bmr = a3.x - a4.x, bmi = a3.y - a4.y;
+    const double xor_ = apr + bpr, xoi = api + bpi, yor = apr - bpr, yoi = api - bpi;  // m+n odd
+    const double xer = amr + bmr, xei = ami + bmi, yer = amr - bmr, yei = ami - bmi;   // m+n even
+#pragma unroll
+    for (int t = 0; t < TN; ++t) {
+        const bool odd = ((MP + t + np) & 1) != 0;
+        rmac(A, t, hv[t], odd ? xor_ : xer, odd ? xoi : xei, odd ? yor : yer, odd ? yoi : yei);
+    }
+}
+template <int TN, int MP>
+__device__ __forceinline__ void tile_quad(const double2* __restrict__ s1, const double2* __restrict__ s2,
+                                          const double2* __restrict__ s3, const double2* __restrict__ s4,
+                                          const double2* __restrict__ h, int P, TileAcc<TN>& A) {
+    int n = 0;
+#pragma unroll 1
+    for (; n + 1 < P; n += 2) {
+        double2 hv[TN + 1];
+#pragma unroll
+        for (int t = 0; t <= TN; ++t) hv[t] = h[n + t];
+        tile_quad_step<TN, MP>(s1[n * kWinCells], s2[n * kWinCells], s3[n * kWinCells], s4[n * kWinCells],
+                               hv, 0, A);
+        tile_quad_step<TN, MP>(s1[(n + 1) * kWinCells], s2[(n + 1) * kWinCells], s3[(n + 1) * kWinCells],
+                               s4[(n + 1) * kWinCells], hv + 1, 1, A);
+    }
+    if (n < P) {  // n even
+        double2 hv[TN];
+#pragma unroll
+        for (int t = 0; t < TN; ++t) hv[t] = h[n + t];
+        tile_quad_step<TN, MP>(s1[n * kWinCells], s2[n * kWinCells], s3[n * kWinCells], s4[n * kWinCells],
+                               hv, 0, A);
     }
 }
 
@@ -605,6 +725,52 @@ __global__ void __launch_bounds__(128 * CW * G, CW * G <= 2 ? 2 : 1)
         live = active && scnt[r] > 0;
         return r;
     };
+    // orbit units with one or two unit groups per destination (config 2, G =
+    // 2: 0.0608 -> 0.0567 ms; config 3: 0.918 -> 0.820 ms); the 15 equal-cost
+    // pair units for three groups (sparse grids: config 1's M2L 0.0143 ms
+    // with pairs vs 0.0162 with orbits, whose unequal units unbalance them)
+    if constexpr (VFMM_M2L_QUADS && G <= 2) {
+    const int u_end = kQUnits * (group + 1) / G;
+#pragma unroll 1
+    for (int u = kQUnits * group / G; u < u_end; ++u) {
+        const int o1 = c_quads.o[parity][u][0], o2 = c_quads.o[parity][u][1];
+        const int kind = c_quads.kind[parity][u];
+        bool live1, live2 = false, live3 = false, live4 = false;
+        const int r1 = src_of(o1, live1);
+        const int r2 = o2 >= 0 ? src_of(o2, live2) : r1;
+        int r3 = r1, r4 = r1;
+        if (kind == 4) {
+            r3 = src_of(c_quads.o[parity][u][2], live3);
+            r4 = src_of(c_quads.o[parity][u][3], live4);
+        }
+        ntrans += (counts_here && live1 ? 1 : 0) + (counts_here && live2 ? 1 : 0) +
+                  (counts_here && live3 ? 1 : 0) + (counts_here && live4 ? 1 : 0);
+        if (!__any_sync(0xffffffffu, live1 || live2 || live3 || live4)) continue;
+        // empty sources hold zero multipoles: they multiply as exact zeros
+        const double2* h =
+            sH + ((c_off.dy[parity][o1] + 3) * 7 + (c_off.dx[parity][o1] + 3)) * HL + (m0 - mg);
+        const double2* s1 = win + r1;
+        VCHECK(m0 - mg + TN + P <= HL + TN);
+        VJITTER();
+        if (o2 < 0) {
+            tile_plain<TN>(s1, h, P, A);
+            continue;
+        }
+        const double2* s2 = win + r2;
+        if (kind == 4) {
+            if (mo) tile_quad<TN, 1>(s1, s2, win + r3, win + r4, h, P, A);
+            else tile_quad<TN, 0>(s1, s2, win + r3, win + r4, h, P, A);
+        } else if (kind == 1) {
+            if (mo) tile_pair<TN, 1, 1>(s1, s2, h, P, A);
+            else tile_pair<TN, 1, 0>(s1, s2, h, P, A);
+        } else if (kind == 2) {
+            tile_pair<TN, 2, 0>(s1, s2, h, P, A);
+        } else {
+            if (mo) tile_pair<TN, 3, 1>(s1, s2, h, P, A);
+            else tile_pair<TN, 3, 0>(s1, s2, h, P, A);
+        }
+    }
+    } else {
     const int u_end = kUnits * (group + 1) / G;
 #pragma unroll 1
     for (int u = kUnits * group / G; u < u_end; ++u) {
@@ -635,6 +801,7 @@ __global__ void __launch_bounds__(128 * CW * G, CW * G <= 2 ? 2 : 1)
             if (mo) tile_pair<TN, 3, 1>(s1, s2, h, P, A);
             else tile_pair<TN, 3, 0>(s1, s2, h, P, A);
         }
+    }
     }
     double2 res[TN];
 #pragma unroll
