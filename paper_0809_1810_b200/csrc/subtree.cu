@@ -8,6 +8,7 @@
 //   M2M  P_m  = 2^-(m+1) sum_{k<=m} M_k E_q[m-k]         children in quadrant order
 //   L2L  Lh'_n = M2L_n + sum_{m>=n} (2^-m Lh_m) F_q[m-n]  (M2L part + parent shift)
 // Local cell ids: sub-level s (0 = the CTA's root cell) holds a 2^s x 2^s grid.
+#include <cstdio>
 #include <cstdlib>
 
 #include "vfmm_internal.cuh"
@@ -139,7 +140,16 @@ __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
     k_l2l_fused(double2* __restrict__ loc, double2* __restrict__ leaf_loc,
                 const double2* __restrict__ anc_m2l, int ls, int levels, int P,
                 const Tables* __restrict__ T, Rows rows, FusedOut fo) {
+#ifdef VFMM_L2L_TRACE
+    unsigned long long tr[8];
+    int ntr = 0;
+    auto mark = [&]() { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr[ntr])); ++ntr; };
+    mark();
+#else
+    auto mark = [&]() {};
+#endif
     pdl_enter();
+    mark();
     extern __shared__ double2 sm[];
     const int depth = levels - ls;
     double2* sF = sm + (size_t)sub_off(depth + 1) * P;  // [4][P]
@@ -150,39 +160,65 @@ __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
     const int mt = 1 << ls;
     const int cx = blockIdx.x % mt, cy = blockIdx.x / mt;
     if (!rows_touch(rows, cy, levels - ls)) return;  // subtree outside the owned strip
-    for (int i = threadIdx.x; i < 4 * P; i += blockDim.x) sF[i] = T->F[i / P][i % P];
+    // ---- every global read of the tables, the chain and the subtree, issued
+    // together: element e of one flat index space [F tables 4P | level 2 P |
+    // ancestors' M2L parts (ls-2)P | subtree levels 1..depth] is fetched into
+    // registers by thread e mod blockDim in round e / blockDim, all rounds'
+    // loads before any shared-memory store (the level-by-level loops had
+    // waited one memory latency per loop and round: ~5 us of the CTA's life).
+    // The chain's M2L parts of shared ancestors (k < ls) come from the
+    // read-only copy, since their writer CTA completes them in loc while
+    // others still read.
+    const unsigned pmag = (unsigned)((0x100000000ull + P - 1) / P);  // i / P = umulhi(i, pmag), i < 2^16
+    const int nA = (4 + 1 + (ls - 2)) * P, nAll = nA + sub_off(depth + 1) * P - P;
+    auto fetch = [&](int e, double2*& dst) -> double2 {
+        if (e < 4 * P) {  // L2L quadrant tables
+            const int q = (int)__umulhi((unsigned)e, pmag);
+            dst = sF + e;
+            return T->F[q][e - q * P];
+        }
+        if (e < 5 * P) {  // level 2 ancestor
+            const int n = e - 4 * P, sh = ls - 2;
+            dst = anc + n;
+            return loc[lvl_off(2, P) + coef_base(2, cx >> sh, cy >> sh) + n * coef_stride(2)];
+        }
+        if (e < nA) {  // M2L parts of the ancestors 3..ls
+            const int i = e - 5 * P;
+            const int kk = (int)__umulhi((unsigned)i, pmag), n = i - kk * P, k = 3 + kk, sh = ls - k;
+            const int64_t gi = lvl_off(k, P) + coef_base(k, cx >> sh, cy >> sh) + n * coef_stride(k);
+            dst = apart + i;
+            return k < ls ? anc_m2l[gi] : loc[gi];
+        }
+        // subtree: cell c >= 1 (sub-level sl) coefficient k
+        const int i = e - nA + P;  // index into sm (cells from 1)
+        const int c = (int)__umulhi((unsigned)i, pmag), k = i - c * P;
+        int sl = 1;
+        while (sub_off(sl + 1) <= c) ++sl;
+        const int side = 1 << sl, lc = c - sub_off(sl), lvl = ls + sl;
+        dst = sm + i;
+        return loc[lvl_off(lvl, P) + coef_base(lvl, cx * side + (lc & (side - 1)), cy * side + (lc >> sl)) +
+                   k * coef_stride(lvl)];
+    };
+    constexpr int kPre = 8;
+    for (int e0 = 0; e0 < nAll; e0 += kPre * kL2LThreads) {
+        double2 v[kPre];
+        double2* d[kPre];
+#pragma unroll
+        for (int j = 0; j < kPre; ++j) {
+            const int e = e0 + j * kL2LThreads + threadIdx.x;
+            d[j] = nullptr;
+            if (e < nAll) v[j] = fetch(e, d[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < kPre; ++j)
+            if (d[j]) *d[j] = v[j];
+    }
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
         s2[i] = T->pow2neg[i];
         sfact[i] = T->invfact[i];
     }
-    // ---- every global read of the chain and the subtree, issued at once ----
-    // (level 2, the ancestors' M2L parts, the subtree's M2L parts: none depends
-    // on the chain, so one memory latency instead of one per level)
-    if (threadIdx.x < P) {
-        const int n = threadIdx.x, sh = ls - 2;
-        anc[n] = loc[lvl_off(2, P) + coef_base(2, cx >> sh, cy >> sh) + n * coef_stride(2)];
-    }
-    for (int i = threadIdx.x; i < (ls - 2) * P; i += blockDim.x) {
-        const int k = 3 + i / P, n = i % P, sh = ls - k;
-        const int64_t gi = lvl_off(k, P) + coef_base(k, cx >> sh, cy >> sh) + n * coef_stride(k);
-        // M2L part: shared ancestors (k < ls) from the read-only copy, since
-        // their writer CTA completes them in loc while others still read
-        apart[i] = k < ls ? anc_m2l[gi] : loc[gi];
-    }
-    // subtree levels 1..depth (level by level: offsets hoisted, the cell /
-    // coefficient split by a multiply-high instead of a division by P)
-    const unsigned pmag = (unsigned)((0x100000000ull + P - 1) / P);  // i / P = umulhi(i, pmag), i < 2^16
-    for (int sl = 1; sl <= depth; ++sl) {
-        const int side = 1 << sl, lvl = ls + sl;
-        const double2* g = loc + lvl_off(lvl, P);
-        const int64_t cs = coef_stride(lvl);
-        double2* dst = sm + (size_t)sub_off(sl) * P;
-        for (int i = threadIdx.x; i < side * side * P; i += blockDim.x) {
-            const int lc = (int)__umulhi((unsigned)i, pmag), k = i - lc * P;
-            dst[i] = g[coef_base(lvl, cx * side + (lc & (side - 1)), cy * side + (lc >> sl)) + k * cs];
-        }
-    }
     __syncthreads();
+    mark();
     // ---- ancestor chain: level 2 (complete after M2L) down to ls ----
     // output n of a level is summed by 8 lanes (terms mm = n + lane8, step 8)
     // and reduced by xor shuffles: P x 8 threads instead of P serial sums
@@ -230,6 +266,7 @@ __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
         __syncthreads();
         cur ^= 1;
     }
+    mark();
     if (depth == 0) return;
     // ---- subtree below the root ----
     // parents are kept in shared memory pre-multiplied by 2^-m (exact: a
@@ -277,6 +314,7 @@ __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
         }
         __syncthreads();
     }
+    mark();
     if (!fo.u) return;
     // ---- fused L2P + combine over the particles of this CTA's leaves ----
     // (the leaf locals are in shared memory; one contiguous particle range per
@@ -354,6 +392,14 @@ __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
             }
         }
     }
+#ifdef VFMM_L2L_TRACE
+    __syncthreads();
+    mark();
+    if (threadIdx.x == 0 && (blockIdx.x % 97) == 0)
+        printf("l2l cta %d: wait %.2f prefetch %.2f anc %.2f subtree %.2f l2p %.2f us\n", blockIdx.x,
+               (tr[1] - tr[0]) * 1e-3, (tr[2] - tr[1]) * 1e-3, (tr[3] - tr[2]) * 1e-3, (tr[4] - tr[3]) * 1e-3,
+               (tr[5] - tr[4]) * 1e-3);
+#endif
 }
 
 size_t sub_smem(int depth, int P) {
