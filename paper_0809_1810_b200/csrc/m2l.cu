@@ -407,6 +407,9 @@ __constant__ OffTab c_off = make_offtab();
 #ifndef VFMM_M2L_QUADS
 #define VFMM_M2L_QUADS 1
 #endif
+#ifndef VFMM_M2L_QUADS_GMAX
+#define VFMM_M2L_QUADS_GMAX 3
+#endif
 constexpr int kQUnits = 12;
 struct QuadTab {
     int8_t o[4][kQUnits][4], kind[4][kQUnits];
@@ -467,6 +470,34 @@ constexpr QuadTab make_quads() {
             ++nu;
         }
         t.count[par] = nu;
+        // Balanced order: (orbit, pair, pair, single) x 3, so every third of
+        // the units costs the same (per coefficient 16 adds + 4 TN FMA for an
+        // orbit, 4 adds + 4 TN for a pair, 4 TN for a single) and three unit
+        // groups (sparse grids) stay balanced.
+        if (nu == kQUnits) {
+            int8_t oo[kQUnits][4] = {}, kk[kQUnits] = {};
+            int qi = 0, pi = 0, si = 0, w = 0;
+            int q[kQUnits] = {}, pr[kQUnits] = {}, sg[kQUnits] = {};
+            for (int u = 0; u < kQUnits; ++u) {
+                if (t.kind[par][u] == 4) q[qi++] = u;
+                else if (t.kind[par][u] == 0) sg[si++] = u;
+                else pr[pi++] = u;
+            }
+            int a = 0, b = 0, c = 0;
+            const bool ok = qi == 3 && pi == 6 && si == 3;
+            for (int g = 0; ok && g < 3; ++g) {
+                const int us[4] = {q[a++], pr[b++], pr[b++], sg[c++]};
+                for (int j = 0; j < 4; ++j, ++w) {
+                    for (int m = 0; m < 4; ++m) oo[w][m] = t.o[par][us[j]][m];
+                    kk[w] = t.kind[par][us[j]];
+                }
+            }
+            if (ok)
+                for (int u = 0; u < kQUnits; ++u) {
+                    for (int m = 0; m < 4; ++m) t.o[par][u][m] = oo[u][m];
+                    t.kind[par][u] = kk[u];
+                }
+        }
     }
     return t;
 }
@@ -725,11 +756,10 @@ __global__ void __launch_bounds__(128 * CW * G, CW * G <= 2 ? 2 : 1)
         live = active && scnt[r] > 0;
         return r;
     };
-    // orbit units with one or two unit groups per destination (config 2, G =
-    // 2: 0.0608 -> 0.0567 ms; config 3: 0.918 -> 0.820 ms); the 15 equal-cost
-    // pair units for three groups (sparse grids: config 1's M2L 0.0143 ms
-    // with pairs vs 0.0162 with orbits, whose unequal units unbalance them)
-    if constexpr (VFMM_M2L_QUADS && G <= 2) {
+    // orbit units (config 2, G = 2: 0.0608 -> 0.0567 ms; config 3: 0.918 ->
+    // 0.812 ms); their balanced order keeps three unit groups (sparse grids)
+    // even; VFMM_M2L_QUADS=0 / _GMAX restrict them (A/B)
+    if constexpr (VFMM_M2L_QUADS && G <= VFMM_M2L_QUADS_GMAX) {
     const int u_end = kQUnits * (group + 1) / G;
 #pragma unroll 1
     for (int u = kQUnits * group / G; u < u_end; ++u) {
