@@ -1149,10 +1149,11 @@ int p2p_sym_split_from(const Layout& L, Rows rows) {
     const int64_t wave = (int64_t)kSymWarps * 2 * 148;
     if (2 * leaves <= wave) return 0;  // two items per leaf fit one wave
     // the tail of half items pays off when warps take several items each
-    // (config 3, 262K leaves: near field 11.99 -> 11.61 ms); with about one
-    // item per warp (config 2) the uniform kernel without it is faster
-    // (0.550 vs 0.565 ms)
-    if (tail_env < 0 && leaves < wave * 4 * 4) return (int)leaves;
+    // (config 3, 262K leaves: near field 11.99 -> 11.61 ms; a rank of an
+    // 8-way config-3 run, 33K leaves: 1.952 -> 1.935 ms per step); with about
+    // one item per warp (config 2, 16K leaves) the uniform kernel without it
+    // is faster (0.550 vs 0.565 ms)
+    if (tail_env < 0 && leaves < wave * 8) return (int)leaves;
     const int64_t tail = tail_env >= 0 ? tail_env : wave;
     return (int)(leaves > tail ? leaves - tail : 0);
 }
