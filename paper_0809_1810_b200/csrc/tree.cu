@@ -55,6 +55,7 @@ constexpr int kBinILP = 4;         // particles per thread in flight in the binn
 // Counters::sort_fallback: 0 counting path, else the LSD radix path because
 // the input looked spatially incoherent (probe) or a leaf is too large.
 constexpr int kSortLsdProbe = 1, kSortLsdBigLeaf = 2;
+constexpr int64_t kLsdMinN = 3ll << 20;  // random order below this: the counting path
 
 
 // quadtree.py:44-45: min(int((v - lo) / side * m), m - 1).  The division is
@@ -75,7 +76,7 @@ __device__ __forceinline__ int cell_of(double v, double lo, double side, double 
 // atomics and gathers of the counting path scattered, so the LSD sort (whose
 // passes write digit runs) is used instead.
 __device__ void sort_probe_impl(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
-                                double xmin, double ymin, double side, int levels, bool force_lsd,
+                                double xmin, double ymin, double side, int levels, int probe_mode,
                                 Counters* __restrict__ ctr) {
     __shared__ int distinct;
     if (threadIdx.x == 0) distinct = 0;
@@ -103,7 +104,14 @@ __device__ void sort_probe_impl(const double* __restrict__ x, const double* __re
     }
     __syncthreads();
     // more than 8 distinct leaves per 32 consecutive particles on average
-    if (threadIdx.x == 0 && (force_lsd || distinct > 64 * 8)) ctr->sort_fallback = kSortLsdProbe;
+    // and enough particles that the counting path's scattered accesses miss L2
+    // (random order, build ms counting / LSD: N = 2^20 0.093 / 0.113, a rank
+    // of an 8-way config-3 run (2.1M, 64 per leaf) counting 45 us faster, N =
+    // 2^22 0.342 / 0.321, 2^24 1.90 / 1.17; tools/sort_probe.py)
+    // (probe_mode: 0 auto, 1 force LSD, 2 never LSD by the probe -- A/B)
+    if (threadIdx.x == 0 &&
+        (probe_mode == 1 || (probe_mode == 0 && distinct > 64 * 8 && n > kLsdMinN)))
+        ctr->sort_fallback = kSortLsdProbe;
 }
 
 // Keys, domain check and per-leaf counts (cnt zeroed; leaf_starts storage).
@@ -917,11 +925,12 @@ __global__ void k_tasks_fill(const int* __restrict__ ls, int levels, int chunk, 
 }
 
 
-// VFMM_SORT=lsd forces the LSD radix path (tuning / tests)
-bool force_lsd() {
-    static const bool f = [] {
+// VFMM_SORT=lsd forces the LSD radix path, VFMM_SORT=count keeps the probe
+// from choosing it (a leaf above kFastLeafMax still does) -- tuning / tests
+int sort_probe_mode() {
+    static const int f = [] {
         const char* e = getenv("VFMM_SORT");
-        return e && e[0] == 'l';
+        return e ? (e[0] == 'l' ? 1 : (e[0] == 'c' ? 2 : 0)) : 0;
     }();
     return f;
 }
@@ -966,10 +975,10 @@ struct ProbeArgs {
     int64_t n;
     double xmin, ymin, side;
     int levels;
-    bool force_lsd;
+    int probe_mode;
 };
 __device__ void sort_probe(const ProbeArgs& a, Counters* ctr) {
-    sort_probe_impl(a.x, a.y, a.n, a.xmin, a.ymin, a.side, a.levels, a.force_lsd, ctr);
+    sort_probe_impl(a.x, a.y, a.n, a.xmin, a.ymin, a.side, a.levels, a.probe_mode, ctr);
 }
 // The build's first kernel: zero the scratch regions, and CTA 0 also runs the
 // sort-path probe (one launch instead of two; the counters are zeroed by the
@@ -1033,7 +1042,7 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
         ZeroRegions z{{(int*)(ws + L.scan_state), ls, fill, ghist, (int*)(ws + L.near_done)},
                       {(int64_t)(L.scan_state_bytes / sizeof(int)), (int64_t)L.nleaves + 1,
                        (int64_t)L.nleaves, (int64_t)L.passes * B + 8, (int64_t)L.nleaves}};
-        const ProbeArgs pa{x, y, L.n, xmin, ymin, side, L.levels, force_lsd()};
+        const ProbeArgs pa{x, y, L.n, xmin, ymin, side, L.levels, sort_probe_mode()};
         launch_k(k_zero_regions, 297, 256, 0, s, z, pa, ctr);
         note_launches(1);
     }

@@ -331,13 +331,15 @@ def test_host_pipeline_matches_synchronous_call():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["lattice", "random_order", "mixed_sigma"])
+@pytest.mark.parametrize("case", ["lattice", "random_order", "random_order_big_leaf", "mixed_sigma"])
 def test_host_graph_path_matches_stream_launches(case):
     """VFMM_FLAG_GRAPH (cached CUDA graph of the device part) gives bitwise the
     stream-launched results: a coherent input (counting sort, symmetric P2P),
-    a random-order one (LSD radix path chosen on the device inside the graph)
-    and per-particle core sizes (generic P2P); replays reuse the cached graph
-    with new input values, a different domain gets its own graph."""
+    a random-order one (counting sort below the LSD size threshold), a random
+    one with a leaf of > 128 particles (LSD radix path chosen on the device
+    inside the graph, generic P2P) and per-particle core sizes (generic P2P);
+    replays reuse the cached graph with new input values, a different domain
+    gets its own graph."""
     from paper_0809_1810_b200 import _lib
 
     rng = np.random.default_rng(7)
@@ -348,8 +350,11 @@ def test_host_graph_path_matches_stream_launches(case):
     else:
         n = 20000
         x, y = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+        if case == "random_order_big_leaf":  # 300 particles in one leaf: the LSD path
+            x[:300] = rng.uniform(0.50, 0.53, 300)
+            y[:300] = rng.uniform(0.50, 0.53, 300)
         g = rng.standard_normal(n) * 1e-4
-        s = np.full(n, 0.01) if case == "random_order" else rng.uniform(0.005, 0.01, n)
+        s = np.full(n, 0.01) if case.startswith("random_order") else rng.uniform(0.005, 0.01, n)
         levels, order = 5, 12
     cfg = vf.FmmConfig(levels, order, vf.KernelKind.GAUSSIAN_BLOB)
     pinned = tuple(torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (x, y, g, s))
