@@ -18,10 +18,11 @@ evaluations are kept in flight (``HostPipeline``), so one step's copies
 overlap its neighbours' compute.  ``e2e.latency_ms`` is one
 synchronous ``evaluate_host`` call.
 
-``--impl reference`` times the reference algorithm's CPU implementation (the
-numpy oracle port in oracle/, the reference being pure Python and absent on
-the GPU box) on the SAME workload: one full config-2 evaluate per worker
-process per step, one worker per host core.
+``--impl reference`` times the reference's CPU implementation on the SAME
+workload: the unmodified ``vortexfmm`` package from its offline install under
+baseline/_ref/ when present (it travels with the snapshot), else the numpy
+oracle port in oracle/; one full config-2 evaluate per worker process per
+step, one worker per host core.
 """
 
 from __future__ import annotations
@@ -123,29 +124,65 @@ _REF_LIMIT = None
 REF_RSS_GB = {0: 0.3, 1: 0.5, 2: 1.5, 3: 24.0}  # measured peak RSS of one port evaluate (+ margin)
 
 
+def _ref_package():
+    """The UNMODIFIED reference package when its one offline install is present
+    (tools/install_reference.sh -> git-ignored baseline/_ref/, which travels to
+    the GPU box with the snapshot), else None (the numpy oracle port stands in)."""
+    path = os.path.join(REPO, "baseline", "_ref")
+    if os.environ.get("VFMM_REF_ARM") == "port" or not os.path.isdir(os.path.join(path, "vortexfmm")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import vortexfmm.engine as eng
+        import vortexfmm.model as mod
+    except Exception:  # a broken install: fall back to the port, and say so in `kind`
+        return None
+    return eng, mod
+
+
+_REF_CALL = None
+
+
 def _ref_init():
-    global _REF_LIMIT
+    """Per worker: one BLAS thread; with the reference installed, the particle
+    list its public API takes (built once, outside the timed steps: it is the
+    caller's input, not part of evaluate)."""
+    global _REF_LIMIT, _REF_CALL
     from threadpoolctl import threadpool_limits
 
     _REF_LIMIT = threadpool_limits(limits=1)  # one BLAS thread per worker process
+    w = _REF_W
+    pkg = _ref_package()
+    if pkg is not None:
+        eng, mod = pkg
+        ps = [mod.Particle(*t) for t in zip(w.x.tolist(), w.y.tolist(), w.gamma.tolist(), w.sigma.tolist())]
+        cfg = eng.FmmConfig(w.levels, w.order, eng.KernelKind.GAUSSIAN_BLOB)
+        dom = mod.Domain(-1.0, -1.0, 2.0)
+        _REF_CALL = lambda: eng.evaluate(ps, cfg, dom)  # noqa: E731
+    else:
+        from oracle import fmm_oracle as O
+
+        _REF_CALL = lambda: O.evaluate(w.x, w.y, w.gamma, w.sigma, w.levels, w.order, True,  # noqa: E731
+                                       (-1.0, -1.0, 2.0))
 
 
 def _ref_step(_):
-    from oracle import fmm_oracle as O
-
-    w = _REF_W
     t0 = time.perf_counter()
-    O.evaluate(w.x, w.y, w.gamma, w.sigma, w.levels, w.order, True, (-1.0, -1.0, 2.0))
+    _REF_CALL()
     return time.perf_counter() - t0
 
 
 def run_reference(args):
-    """The reference algorithm's CPU path on ALL host cores, on exactly our arm's
-    workload: the reference is pure Python + numpy and cannot travel to the GPU
-    box, so its restatement (the numpy oracle port, oracle/fmm_oracle.py, pinned
-    to the reference at 1e-12 on the full config 2 by tests/test_large_parity.py)
-    runs one worker process per core (one BLAS thread each: the reference is
-    single-threaded apart from zgemm threads, which slow it down).
+    """The reference's own CPU path on ALL host cores, on exactly our arm's
+    workload.  With the reference's offline install present (baseline/_ref/,
+    written by tools/install_reference.sh; `kind` = "reference") every worker
+    calls the UNMODIFIED ``vortexfmm.engine.evaluate(list[Particle], FmmConfig,
+    Domain)``; without it (`kind` = "port") the numpy oracle port runs instead
+    (oracle/fmm_oracle.py, pinned to the reference at 1e-12 on the full config 2
+    by tests/test_large_parity.py; ~1.7x faster than the reference itself).
+    One worker process per core, one BLAS thread each: the reference is
+    single-threaded apart from zgemm threads, which slow it down.
     A step is one FULL evaluate of the configuration per worker (N = 1,048,576,
     l = 7, p = 17 for config 2); value = workers x N / step wall time."""
     import multiprocessing as mp
@@ -171,7 +208,10 @@ def run_reference(args):
             t.append(time.perf_counter() - t0)
     mean = statistics.fmean(t)
     value = workers * w.n / mean
-    sample = (f"one full {w.name} evaluate (N={w.n}, l={w.levels}, p={w.order}) per worker per step, "
+    kind = "reference" if _ref_package() is not None else "port"
+    what = ("the unmodified vortexfmm.engine.evaluate (baseline/_ref)" if kind == "reference"
+            else "the numpy oracle port")
+    sample = (f"one full {w.name} evaluate (N={w.n}, l={w.levels}, p={w.order}) by {what} per worker per step, "
               f"{workers} worker processes x 1 BLAS thread")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -180,7 +220,7 @@ def run_reference(args):
         "data": "synthetic",
         "config": {"workload": w.name, "n": w.n, "levels": w.levels, "order": w.order, "kernel": "gaussian",
                    "domain": [-1.0, -1.0, 2.0], "same_config": True},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": kind, "sample": sample,
                          "host": host},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
