@@ -152,6 +152,26 @@ int vfmm_evaluate_host(const double* x, const double* y, const double* gamma, co
                        int kernel, double* u, double* v, void* workspace, size_t workspace_bytes,
                        unsigned flags, vfmm_stats* stats, void* stream);
 
+/* vfmm_evaluate_host for a batch of INDEPENDENT evaluations kept in flight
+ * (the reference runs them one after another, harness.py:211-267): the same
+ * host-buffer contract (engine.py:335-398), with the three stages of a call
+ * on three streams of the caller -- the input copies on `h2d_stream`, the
+ * cached CUDA graph of the device part on `compute_stream` (VFMM_FLAG_GRAPH is
+ * implied), the copy of (u, v) back on `d2h_stream` -- ordered by events
+ * inside the library.  The copy streams are meant to be shared by every call
+ * of the batch (copies are serialised by the two copy engines anyway) and the
+ * compute streams to be few (evaluations on distinct compute streams share
+ * the SMs), so input copies run ahead of the compute and results drain behind
+ * it, whatever the number of buffers in flight.  The call has completed when
+ * `d2h_stream` reaches the point of the call's return (record an event there);
+ * ONE call per workspace may be in flight.  No VFMM_FLAG_STATS / phase flags
+ * (VFMM_EINVAL); the three streams must be distinct, the copy streams non-NULL. */
+int vfmm_evaluate_host_streams(const double* x, const double* y, const double* gamma,
+                               const double* sigma, int64_t n, double xmin, double ymin, double side,
+                               int levels, int order, int kernel, double* u, double* v,
+                               void* workspace, size_t workspace_bytes, unsigned flags,
+                               void* compute_stream, void* h2d_stream, void* d2h_stream);
+
 /* Sharded evaluate (one process per GPU; leaves sharded in row strips).
  * The local arrays hold this rank's owned particles (leaf rows [row_lo,
  * row_hi) of the 2^levels x 2^levels leaf grid) plus halo copies of the

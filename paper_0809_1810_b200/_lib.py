@@ -44,6 +44,7 @@ EXPORTED_SYMBOLS = (
     "vfmm_layout_of",
     "vfmm_evaluate",
     "vfmm_evaluate_host",
+    "vfmm_evaluate_host_streams",
     "vfmm_evaluate_shard",
     "vfmm_shard_exchange_size",
     "vfmm_shard_pack",
@@ -127,6 +128,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.vfmm_evaluate.argtypes = [_P, _P, _P, _P, _I64, _D, _D, _D, _I, _I, _I, _P, _P, _P, _SZ,
                                       ctypes.c_uint, ctypes.POINTER(VfmmStats), _P]
         lib.vfmm_evaluate_host.argtypes = lib.vfmm_evaluate.argtypes
+        lib.vfmm_evaluate_host_streams.argtypes = [_P, _P, _P, _P, _I64, _D, _D, _D, _I, _I, _I, _P, _P,
+                                                   _P, _SZ, ctypes.c_uint, _P, _P, _P]
         lib.vfmm_evaluate_shard.argtypes = [_P, _P, _P, _P, _I64, _D, _D, _D, _I, _I, _I, _I, _I, _P,
                                             _P, _P, _SZ, ctypes.c_uint, ctypes.POINTER(VfmmStats), _P]
         lib.vfmm_shard_exchange_size.argtypes = [_I64, _I, _I, _I, _I, _I, ctypes.POINTER(_SZ),

@@ -785,6 +785,9 @@ struct HostGraph {
     cudaGraphExec_t exec;
     long long launches;  // kernels per replay
     unsigned long long used;
+    // vfmm_evaluate_host_streams: inputs staged (copy stream -> compute stream) and
+    // velocities ready (compute stream -> copy stream); one call per workspace in flight
+    cudaEvent_t ev_in = nullptr, ev_done = nullptr;
 };
 std::mutex g_graph_mu;
 std::vector<HostGraph> g_graphs;
@@ -798,7 +801,8 @@ constexpr size_t kMaxGraphs = 32;
 // the graph path does not apply (the caller falls back to stream launches).
 int evaluate_host_graph(const HostIO& io, int64_t n, double xmin, double ymin, double side,
                         int levels, int order, int kernel, void* workspace,
-                        size_t workspace_bytes, unsigned flags, vfmm_stats* stats, void* stream) {
+                        size_t workspace_bytes, unsigned flags, vfmm_stats* stats, void* stream,
+                        void* h2d_stream = nullptr, void* d2h_stream = nullptr) {
     const bool timed = (flags & VFMM_FLAG_STATS) != 0;
     if (flags & (VFMM_FLAG_PHASE_TIMES | VFMM_FLAG_PHASE_UP | VFMM_FLAG_PHASE_DOWN |
                  VFMM_FLAG_FAR_ONLY))
@@ -832,6 +836,7 @@ int evaluate_host_graph(const HostIO& io, int64_t n, double xmin, double ymin, d
     const unsigned kflags = dflags | (one ? VFMM_FLAG_SIGMA_SCALAR : 0u);
 
     cudaGraphExec_t exec = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_done = nullptr;
     long long nl = 0;
     {
         std::lock_guard<std::mutex> lk(g_graph_mu);
@@ -842,6 +847,8 @@ int evaluate_host_graph(const HostIO& io, int64_t n, double xmin, double ymin, d
                 g.used = ++g_graph_tick;
                 exec = g.exec;
                 nl = g.launches;
+                ev_in = g.ev_in;
+                ev_done = g.ev_done;
                 break;
             }
         if (!exec) {
@@ -891,25 +898,47 @@ int evaluate_host_graph(const HostIO& io, int64_t n, double xmin, double ymin, d
                 for (size_t i = 1; i < g_graphs.size(); ++i)
                     if (g_graphs[i].used < g_graphs[lru].used) lru = i;
                 cudaGraphExecDestroy(g_graphs[lru].exec);
+                if (g_graphs[lru].ev_in) cudaEventDestroy(g_graphs[lru].ev_in);
+                if (g_graphs[lru].ev_done) cudaEventDestroy(g_graphs[lru].ev_done);
                 g_graphs.erase(g_graphs.begin() + (long)lru);
             }
-            g_graphs.push_back(HostGraph{dev, workspace, n, levels, order, kernel, kflags, xmin,
-                                         ymin, side, exec, nl, ++g_graph_tick});
+            if (cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming) != cudaSuccess) {
+                cudaGetLastError();
+                cudaGraphExecDestroy(exec);
+                return -1;
+            }
+            HostGraph hg{dev, workspace, n, levels, order, kernel, kflags, xmin, ymin, side, exec, nl,
+                         ++g_graph_tick};
+            hg.ev_in = ev_in;
+            hg.ev_done = ev_done;
+            g_graphs.push_back(hg);
         }
     }
+    // copies on the caller's copy streams when given (vfmm_evaluate_host_streams)
+    cudaStream_t sin = h2d_stream ? (cudaStream_t)h2d_stream : s;
+    cudaStream_t sout = d2h_stream ? (cudaStream_t)d2h_stream : s;
     if (timed) cudaEventRecord(R->ev[0], s);
     const size_t b = sizeof(double) * (size_t)n;
-    cudaMemcpyAsync(dx, io.hx, b, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(dy, io.hy, b, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(dg, io.hg, b, cudaMemcpyHostToDevice, s);
-    if (gauss) cudaMemcpyAsync(dsg, io.hs, one ? sizeof(double) : b, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(dx, io.hx, b, cudaMemcpyHostToDevice, sin);
+    cudaMemcpyAsync(dy, io.hy, b, cudaMemcpyHostToDevice, sin);
+    cudaMemcpyAsync(dg, io.hg, b, cudaMemcpyHostToDevice, sin);
+    if (gauss) cudaMemcpyAsync(dsg, io.hs, one ? sizeof(double) : b, cudaMemcpyHostToDevice, sin);
+    if (sin != s) {
+        cudaEventRecord(ev_in, sin);
+        cudaStreamWaitEvent(s, ev_in, 0);
+    }
     if (cudaGraphLaunch(exec, s) != cudaSuccess) return VFMM_ECUDA;
     note_launches((int)nl);
+    if (sout != s) {
+        cudaEventRecord(ev_done, s);
+        cudaStreamWaitEvent(sout, ev_done, 0);
+    }
     if (pairs) {
-        cudaMemcpyAsync(io.hu, du, 2 * b, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(io.hu, du, 2 * b, cudaMemcpyDeviceToHost, sout);
     } else {
-        cudaMemcpyAsync(io.hu, du, b, cudaMemcpyDeviceToHost, s);
-        cudaMemcpyAsync(io.hv, dv, b, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(io.hu, du, b, cudaMemcpyDeviceToHost, sout);
+        cudaMemcpyAsync(io.hv, dv, b, cudaMemcpyDeviceToHost, sout);
     }
     if (!timed) return cudaGetLastError() == cudaSuccess ? VFMM_OK : VFMM_ECUDA;
     if (!stats) return VFMM_EINVAL;
@@ -946,6 +975,47 @@ int vfmm_evaluate_host(const double* x, const double* y, const double* gamma, co
                          workspace, workspace_bytes,
                          flags & ~(VFMM_FLAG_PHASE_UP | VFMM_FLAG_PHASE_DOWN | VFMM_FLAG_FAR_ONLY),
                          Rows{0, 1 << levels}, stats, stream, &io);
+}
+
+int vfmm_evaluate_host_streams(const double* x, const double* y, const double* gamma,
+                               const double* sigma, int64_t n, double xmin, double ymin, double side,
+                               int levels, int order, int kernel, double* u, double* v,
+                               void* workspace, size_t workspace_bytes, unsigned flags,
+                               void* compute_stream, void* h2d_stream, void* d2h_stream) {
+    if (levels < 2 || levels > VFMM_LEVELS_CAP) return VFMM_EINVAL;
+    if (!x || !y || !gamma || !u || (!v && !(flags & VFMM_FLAG_UV_PAIRS)) ||
+        (kernel == VFMM_KERNEL_GAUSSIAN && !sigma))
+        return VFMM_EINVAL;
+    if ((flags & (VFMM_FLAG_STATS | VFMM_FLAG_PHASE_TIMES | VFMM_FLAG_PHASE_UP | VFMM_FLAG_PHASE_DOWN |
+                  VFMM_FLAG_FAR_ONLY)) ||
+        !h2d_stream || !d2h_stream || h2d_stream == compute_stream || d2h_stream == compute_stream)
+        return VFMM_EINVAL;
+    const HostIO io{x, y, gamma, kernel == VFMM_KERNEL_GAUSSIAN ? sigma : nullptr, u, v};
+    const int rc = evaluate_host_graph(io, n, xmin, ymin, side, levels, order, kernel, workspace,
+                                       workspace_bytes, flags | VFMM_FLAG_GRAPH, nullptr,
+                                       compute_stream, h2d_stream, d2h_stream);
+    if (rc >= 0) return rc;
+    // no graph for this key yet (first sighting) or capture unavailable: the whole call on
+    // the compute stream, in stream order with what the copy streams hold; the caller's
+    // "complete when d2h_stream reaches this point" still holds
+    cudaStream_t cs = (cudaStream_t)compute_stream;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (cudaEventCreateWithFlags(&e0, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) != cudaSuccess) {
+        if (e0) cudaEventDestroy(e0);
+        cudaGetLastError();
+        return VFMM_ECUDA;
+    }
+    cudaEventRecord(e0, (cudaStream_t)h2d_stream);
+    cudaStreamWaitEvent(cs, e0, 0);
+    const int rs = evaluate_impl(x, y, gamma, sigma, n, xmin, ymin, side, levels, order, kernel, u, v,
+                                 workspace, workspace_bytes, flags & ~VFMM_FLAG_GRAPH,
+                                 Rows{0, 1 << levels}, nullptr, compute_stream, &io);
+    cudaEventRecord(e1, cs);
+    cudaStreamWaitEvent((cudaStream_t)d2h_stream, e1, 0);
+    cudaEventDestroy(e0);  // released by the runtime once the recorded work has completed
+    cudaEventDestroy(e1);
+    return rs;
 }
 
 int vfmm_evaluate_shard(const double* x, const double* y, const double* gamma, const double* sigma,

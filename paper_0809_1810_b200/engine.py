@@ -291,13 +291,23 @@ def evaluate_host(
 class PendingEvaluation:
     """An :func:`evaluate_host_async` call in flight; :meth:`result` waits for it."""
 
-    def __init__(self, out, stream, keep, ws, config, domain, n, code, bad):
+    def __init__(self, out, stream, keep, ws, config, domain, n, code, bad, event=None):
         self.out, self.stream, self._keep, self.ws = out, stream, keep, ws
         self._config, self._domain, self._n, self._code = config, domain, n, code
         self._bad = bad  # pinned int32: out-of-domain count, copied on the stream
+        # three-stream calls: recorded on the D2H copy stream (shared by the batch) after
+        # this call's last copy; `stream` is then that copy stream
+        self._event = event
 
     def done(self) -> bool:
-        return self.stream.query()
+        return self._event.query() if self._event is not None else self.stream.query()
+
+    def wait(self) -> None:
+        """Block the host until this call's result is in ``out``."""
+        if self._event is not None:
+            self._event.synchronize()
+        else:
+            self.stream.synchronize()
 
     def result(self, with_stats: bool = False):
         """The (N, 2) host tensor of (u, v) rows once the call has finished.
@@ -305,7 +315,7 @@ class PendingEvaluation:
         particle lay outside the domain (quadtree.py:191-198; the count rides
         along on the stream, no extra synchronisation).  ``with_stats=True``
         also returns the counters (vfmm_read_stats, no timings)."""
-        self.stream.synchronize()
+        self.wait()
         keep, self._keep = self._keep, None
         nbad = int(self._bad[0])
         if nbad:
@@ -340,7 +350,7 @@ def _uniform_sigma(keep_entry):
 
 def evaluate_host_async(x, y, gamma, sigma, config, domain, *, out: torch.Tensor,
                         workspace: "Workspace", stream: torch.cuda.Stream, overlap: bool = True,
-                        scalar_sigma: bool = True, graph: bool = True):
+                        scalar_sigma: bool = True, graph: bool = True, copy_streams=None):
     """Asynchronous :func:`evaluate_host` (``vfmm_evaluate_host`` without
     VFMM_FLAG_STATS): enqueues the copies and the evaluation on ``stream`` and
     returns a :class:`PendingEvaluation` at once.  Calls on distinct streams
@@ -354,7 +364,10 @@ def evaluate_host_async(x, y, gamma, sigma, config, domain, *, out: torch.Tensor
     behind the previous evaluation's GPU work when calls are pipelined).
     With ``graph`` (default) the device part is one cached CUDA-graph launch
     per call (VFMM_FLAG_GRAPH; captured on the first call of each
-    workspace / shape / domain)."""
+    workspace / shape / domain).  ``copy_streams=(h2d, d2h)`` puts the input
+    copies and the result copy on those two streams (shared by a batch) and
+    only the graph on ``stream`` (``vfmm_evaluate_host_streams``): inputs
+    then run ahead of the compute and results drain behind it."""
     validate_config(config)
     require_cuda()
     lib = _lib.load()
@@ -378,15 +391,31 @@ def evaluate_host_async(x, y, gamma, sigma, config, domain, *, out: torch.Tensor
             scalar[0] = one
             sig_ptr = scalar.data_ptr()
             flags |= _lib.FLAG_SIGMA_SCALAR
+    sig_arg = sig_ptr if code == _lib.KERNEL_GAUSSIAN else None
+    bad = getattr(workspace, "_bad_count", None)
+    if bad is None:
+        bad = workspace._bad_count = torch.zeros(1, dtype=torch.int32).pin_memory()
+    if copy_streams is not None:
+        h2d, d2h = copy_streams
+        status = lib.vfmm_evaluate_host_streams(
+            keep[0][1], keep[1][1], keep[2][1], sig_arg, n, float(domain.xmin), float(domain.ymin),
+            float(domain.side), config.levels, config.order, code, out.data_ptr(), None, workspace.ptr,
+            workspace.nbytes, flags, stream.cuda_stream, h2d.cuda_stream, d2h.cuda_stream,
+        )
+        _lib.check(status, "vfmm_evaluate_host_streams")
+        _lib.check(lib.vfmm_bad_count_async(n, config.levels, config.order, workspace.ptr, bad.data_ptr(),
+                                            d2h.cuda_stream), "vfmm_bad_count_async")
+        event = getattr(workspace, "_done_event", None)
+        if event is None:  # one call per workspace in flight: the event is reused
+            event = workspace._done_event = torch.cuda.Event()
+        event.record(d2h)
+        return PendingEvaluation(out, d2h, keep, workspace, config, domain, n, code, bad, event)
     status = lib.vfmm_evaluate_host(
-        keep[0][1], keep[1][1], keep[2][1], sig_ptr if code == _lib.KERNEL_GAUSSIAN else None, n,
+        keep[0][1], keep[1][1], keep[2][1], sig_arg, n,
         float(domain.xmin), float(domain.ymin), float(domain.side), config.levels, config.order,
         code, out.data_ptr(), None, workspace.ptr, workspace.nbytes, flags, None, stream.cuda_stream,
     )
     _lib.check(status, "vfmm_evaluate_host")
-    bad = getattr(workspace, "_bad_count", None)
-    if bad is None:
-        bad = workspace._bad_count = torch.zeros(1, dtype=torch.int32).pin_memory()
     _lib.check(lib.vfmm_bad_count_async(n, config.levels, config.order, workspace.ptr, bad.data_ptr(),
                                         stream.cuda_stream), "vfmm_bad_count_async")
     return PendingEvaluation(out, stream, keep, workspace, config, domain, n, code, bad)
@@ -394,21 +423,36 @@ def evaluate_host_async(x, y, gamma, sigma, config, domain, *, out: torch.Tensor
 
 class HostPipeline:
     """``depth`` evaluations of one (n, config, domain) shape in flight, each
-    with its own workspace, stream and pinned output buffer (round robin).
+    with its own workspace and pinned output buffer (round robin).
 
         pipe = HostPipeline(n, config, domain)
         pending = [pipe.submit(x, y, g, s) for (x, y, g, s) in batches]
         velocities = [p.result().clone() for p in pending]
 
-    A slot's previous result is waited for before the slot is reused, so
-    results must be consumed (copied) before ``depth`` further submissions."""
+    Three stages on three kinds of stream (``vfmm_evaluate_host_streams``):
+    every call's input copies on ONE H2D stream, its cached CUDA graph on one
+    of ``compute_streams`` streams (round robin: that many evaluations share
+    the SMs, so the latency-bound head and tail of one hide behind the near
+    field of another), its result copy on ONE D2H stream.  Input copies run
+    ahead of the compute and results drain behind it: a batch runs at the
+    slower of the PCIe copies and the overlapped compute.  With
+    ``compute_streams=0`` every slot uses one stream for all three stages
+    (the round-2 layout; A/B).  A slot's previous result is waited for before
+    the slot is reused, so results must be consumed (copied) before ``depth``
+    further submissions."""
 
     def __init__(self, n: int, config, domain, *, depth: int = 2, device=None, overlap: bool = True,
-                 graph: bool = True):
+                 graph: bool = True, compute_streams: int | None = None):
         validate_config(config)
         require_cuda()
         dev = device_of(device)
         self.n, self.config, self.domain, self.overlap, self.graph = n, config, domain, overlap, graph
+        if compute_streams is None:
+            compute_streams = min(depth, 4) if graph else 0
+        if compute_streams and not graph:
+            raise ValueError("the three-stream pipeline replays CUDA graphs (graph=True)")
+        self.copy_streams = (torch.cuda.Stream(dev), torch.cuda.Stream(dev)) if compute_streams else None
+        self.compute = [torch.cuda.Stream(dev) for _ in range(compute_streams)]
         self.slots = [(Workspace(n, config.levels, config.order, dev), torch.cuda.Stream(dev),
                        torch.empty((n, 2), dtype=torch.float64, pin_memory=True)) for _ in range(depth)]
         self.pending = [None] * depth
@@ -416,13 +460,15 @@ class HostPipeline:
 
     def submit(self, x, y, gamma, sigma) -> PendingEvaluation:
         i = self.k % len(self.slots)
-        self.k += 1
         if self.pending[i] is not None:  # the slot's buffers must be free
-            self.pending[i].stream.synchronize()
+            self.pending[i].wait()
         ws, stream, out = self.slots[i]
+        if self.compute:
+            stream = self.compute[self.k % len(self.compute)]
+        self.k += 1
         self.pending[i] = evaluate_host_async(x, y, gamma, sigma, self.config, self.domain, out=out,
                                               workspace=ws, stream=stream, overlap=self.overlap,
-                                              graph=self.graph)
+                                              graph=self.graph, copy_streams=self.copy_streams)
         return self.pending[i]
 
 

@@ -98,6 +98,69 @@ def test_async_host_path_raises_out_of_domain():
     assert np.isfinite(ok.numpy()).all()
 
 
+@pytest.mark.parametrize("depth,compute_streams", [(2, 0), (3, 1), (5, 2), (6, 4)])
+def test_host_pipeline_layouts_are_bitwise_equal(depth, compute_streams):
+    """The three-stream pipeline (vfmm_evaluate_host_streams: copies on shared
+    copy streams, graphs on a few compute streams) and the one-stream-per-slot
+    layout return, for every batch of a sequence, exactly what a synchronous
+    evaluate_host returns -- also on the first submissions of each slot (stream
+    launches, then the graph capture, then replays)."""
+    cfg = vf.FmmConfig(4, 11, G)
+    cases = [_case(s) for s in (3, 4, 5)]
+    want = [vf.evaluate_host(*c, cfg, DOM)[0].clone() for c in cases]
+    pipe = vf.HostPipeline(20000, cfg, DOM, depth=depth, compute_streams=compute_streams)
+    pinned = [[torch.from_numpy(a).pin_memory() for a in c] for c in cases]
+    pend = []
+    for k in range(4 * depth + 3):
+        p = pipe.submit(*pinned[k % 3])
+        pend.append((k % 3, p))
+        if len(pend) >= depth:  # consume before the slot comes round again
+            j, q = pend.pop(0)
+            assert torch.equal(q.result(), want[j])
+    for j, q in pend:
+        assert torch.equal(q.result(), want[j])
+        assert q.done()
+
+
+def test_host_streams_entry_rejects_bad_arguments():
+    lib = _lib.load()
+    w = W.config0()
+    cfg = vf.FmmConfig(w.levels, w.order, G)
+    pipe = vf.HostPipeline(w.n, cfg, DOM, depth=1, compute_streams=1)
+    ws, _, out = pipe.slots[0]
+    h = [torch.from_numpy(a).pin_memory() for a in (w.x, w.y, w.gamma, w.sigma)]
+    h2d, d2h = pipe.copy_streams
+    cs = pipe.compute[0]
+
+    def call(flags, a, b, c):
+        return lib.vfmm_evaluate_host_streams(
+            h[0].data_ptr(), h[1].data_ptr(), h[2].data_ptr(), h[3].data_ptr(), w.n, DOM.xmin, DOM.ymin,
+            DOM.side, w.levels, w.order, _lib.KERNEL_GAUSSIAN, out.data_ptr(), None, ws.ptr, ws.nbytes,
+            flags, a, b, c)
+
+    ok = _lib.FLAG_UV_PAIRS | _lib.FLAG_OVERLAP
+    assert call(ok | _lib.FLAG_STATS, cs.cuda_stream, h2d.cuda_stream, d2h.cuda_stream) == _lib.VFMM_EINVAL
+    assert call(ok, cs.cuda_stream, None, d2h.cuda_stream) == _lib.VFMM_EINVAL
+    assert call(ok, cs.cuda_stream, cs.cuda_stream, d2h.cuda_stream) == _lib.VFMM_EINVAL
+    assert call(ok, cs.cuda_stream, h2d.cuda_stream, d2h.cuda_stream) == _lib.VFMM_OK
+    torch.cuda.synchronize()
+    want = vf.evaluate_host(w.x, w.y, w.gamma, w.sigma, cfg, DOM)[0]
+    assert torch.equal(out, want)
+
+
+def test_async_three_stream_path_raises_out_of_domain():
+    w = W.config0()
+    x = w.x.copy()
+    x[23] = -1.25
+    cfg = vf.FmmConfig(w.levels, w.order, G)
+    pipe = vf.HostPipeline(w.n, cfg, DOM, depth=3, compute_streams=2)
+    for _ in range(4):  # through the stream-launch, capture and replay calls of a slot
+        assert np.isfinite(pipe.submit(w.x, w.y, w.gamma, w.sigma).result().numpy()).all()
+    with pytest.raises(vf.OutOfDomainError, match=r"first indices \[23\]"):
+        pipe.submit(x, w.y, w.gamma, w.sigma).result()
+    assert np.isfinite(pipe.submit(w.x, w.y, w.gamma, w.sigma).result().numpy()).all()
+
+
 def test_current_device_left_alone():
     before = torch.cuda.current_device()
     w = W.config0()
