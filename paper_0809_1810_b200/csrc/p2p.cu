@@ -270,6 +270,9 @@ __device__ __forceinline__ double pair_kernel(double dx, double dy, SymExp x,
 // interleaved: with N = 4 the ring step is 3% faster than four calls of
 // pair_kernel (the compiler's own interleaving stops short under the
 // 128-register cap).
+#ifndef VFMM_SYM_I2F
+#define VFMM_SYM_I2F 0
+#endif
 template <bool GAUSS, int N>
 __device__ __forceinline__ void pair_kernels(const double (&dx)[N], const double (&dy)[N],
                                              double (&K)[N], SymExp q2,
@@ -289,7 +292,12 @@ __device__ __forceinline__ void pair_kernels(const double (&dx)[N], const double
         const double r2c = __hiloint2double((int)hi, __double2loint(r2[k]));
         const double t = fma(r2c, q2.q, kShift);
         ti[k] = __double2loint(t);
+#if VFMM_SYM_I2F
+        // -n from the integer (I2F on the conversion pipe) instead of kShift - t (a DADD)
+        sr[k] = fma(r2c, q2.q, -(double)ti[k]);
+#else
         sr[k] = fma(r2c, q2.q, kShift - t);
+#endif
     }
 #pragma unroll
     for (int k = 0; k < N; ++k) pp[k] = fma(c_exp2_sym[3], sr[k], c_exp2_sym[2]);
