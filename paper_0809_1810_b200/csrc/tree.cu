@@ -8,7 +8,8 @@
 // k_zero_regions    the counters and the scratch regions; CTA 0 samples the
 //                   input order and picks the sort path (probe)
 // Counting path (coherent input order, every leaf <= kFastLeafMax particles;
-// config 2: 5 kernels in all):
+// config 2: 4 kernels in all -- bucket mode, see k_bin_count; 5 when the
+// buckets do not fit the near-field slots, i.e. below ~5 particles per leaf):
 //   k_bin_count     floor-rule binning with max-edge clamp + domain check;
 //                   per-leaf counts (warp-aggregated atomics), four
 //                   particles per thread in flight
@@ -115,13 +116,21 @@ __device__ void sort_probe_impl(const double* __restrict__ x, const double* __re
 }
 
 // Keys, domain check and per-leaf counts (cnt zeroed; leaf_starts storage).
+//
+// Bucket mode (bucket != nullptr; launch_build picks it when the buckets fit
+// the idle near-field slots): the count's atomic also claims the particle's
+// slot in its leaf's fixed bucket of kFastLeafMax indices, so k_bin_scatter
+// (a second pass over the keys with a second atomic per group) is not
+// launched and the keys are not stored; a leaf above kFastLeafMax flags the
+// LSD path, as k_bin_scatter would.
 __global__ void __launch_bounds__(256)
     k_bin_count(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                 double xmin, double ymin, double side, int levels, int* __restrict__ key,
-                int* __restrict__ cnt, Counters* __restrict__ ctr) {
+                int* __restrict__ cnt, Counters* __restrict__ ctr, int* __restrict__ bucket) {
     pdl_enter();
     if (ctr->sort_fallback == kSortLsdProbe) return;
     const int lane = threadIdx.x & 31;
+    bool big = false;
     const int m = 1 << levels;
     const double inv = 1.0 / side;
     const double xmax = xmin + side, ymax = ymin + side;  // Domain.xmax (model.py:51-57)
@@ -138,6 +147,8 @@ __global__ void __launch_bounds__(256)
             xs[u] = i < n ? x[i] : 0.0;
             ys[u] = i < n ? y[i] : 0.0;
         }
+        int ks[kBinILP], base[kBinILP];
+        unsigned pe[kBinILP];
 #pragma unroll
         for (int u = 0; u < kBinILP; ++u) {
             const int64_t i = t0 + u * blockDim.x + threadIdx.x;
@@ -153,12 +164,33 @@ __global__ void __launch_bounds__(256)
                     atomicMax(&ctr->first_bad_neg, INT_MAX - (int)i);
                 }
                 k = iy * m + ix;
-                key[i] = k;
+                if (!bucket) key[i] = k;
             }
             const unsigned peers = __match_any_sync(0xffffffffu, k);
-            if (k >= 0 && lane == __ffs(peers) - 1) atomicAdd(&cnt[k], __popc(peers));
+            ks[u] = k;
+            pe[u] = peers;
+            base[u] = 0;
+            // the group's atomics of the kBinILP slices are all in flight before
+            // the first returned base is used
+            if (k >= 0 && lane == __ffs(peers) - 1) base[u] = atomicAdd(&cnt[k], __popc(peers));
+        }
+        if (bucket) {
+#pragma unroll
+            for (int u = 0; u < kBinILP; ++u) {
+                const int64_t i = t0 + u * blockDim.x + threadIdx.x;
+                const int b = __shfl_sync(0xffffffffu, base[u], __ffs(pe[u]) - 1);
+                if (ks[u] >= 0) {
+                    const int pos = b + __popc(pe[u] & ((1u << lane) - 1u));
+                    if (pos < kFastLeafMax)
+                        bucket[(int64_t)ks[u] * kFastLeafMax + pos] = (int)i;
+                    else
+                        big = true;
+                }
+            }
         }
     }
+    if (bucket && __any_sync(0xffffffffu, big) && lane == 0)
+        atomicMax(&ctr->sort_fallback, kSortLsdBigLeaf);
 }
 
 // Occupancy of every cell of every level (level 0 first) from leaf_starts
@@ -337,7 +369,7 @@ __device__ __forceinline__ double q2_of(double s, double& s_prev, double& q_prev
 }
 
 template <int E>
-__device__ __forceinline__ void leaf_pack(const int* __restrict__ slot, int lo, int c, int leaf,
+__device__ __forceinline__ void leaf_pack(const int* __restrict__ sl, int lo, int c, int leaf,
                                           const double* __restrict__ x, const double* __restrict__ y,
                                           const double* __restrict__ g,
                                           const double* __restrict__ sigma, int sstride,
@@ -349,7 +381,7 @@ __device__ __forceinline__ void leaf_pack(const int* __restrict__ slot, int lo, 
 #pragma unroll
     for (int k = 0; k < E; ++k) {
         const int p = k * 32 + lane;
-        e[k] = p < c ? slot[lo + p] : INT_MAX;
+        e[k] = p < c ? sl[p] : INT_MAX;
     }
     warp_bitonic<E>(e);
 #pragma unroll
@@ -381,24 +413,34 @@ __global__ void __launch_bounds__(256)
                 const double* __restrict__ x, const double* __restrict__ y,
                 const double* __restrict__ g, const double* __restrict__ sigma, int sstride,
                 int* __restrict__ keys, int* __restrict__ perm, Src* __restrict__ src,
-                Counters* __restrict__ ctr, GraphCond lsd_cond) {
+                Counters* __restrict__ ctr, GraphCond lsd_cond, int bucket_stride, CountsArgs ca) {
     pdl_enter();
-    // the path choice is final here (k_bin_scatter): a captured graph runs the
-    // LSD kernels (an IF node after this kernel) only when it is taken
+    // the path choice is final here (k_bin_scatter / k_bin_count's buckets): a
+    // captured graph runs the LSD kernels (an IF node after this kernel) only
+    // when it is taken
     graph_cond_set(lsd_cond, ctr->sort_fallback != 0 ? 1u : 0u);
     if (ctr->sort_fallback) return;
+    // bucket mode: the first ca.ctas CTAs compute the occupancy pyramid and the
+    // task counts (k_bin_scatter's first CTAs do otherwise)
+    if ((int)blockIdx.x < ca.ctas) {
+        counts_tasks_body((int64_t)blockIdx.x * blockDim.x + threadIdx.x, ls, ca, ctr);
+        return;
+    }
     __shared__ unsigned long long wmax[8], wmin[8];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned long long smax = 0ull, smin = ~0ull;
     double s_prev = __longlong_as_double(0x7ff8000000000000ll), q_prev = 0.0;  // NaN: nothing cached
-    for (int leaf = blockIdx.x * 8 + warp; leaf < nleaves; leaf += gridDim.x * 8) {
+    const int nb = gridDim.x - ca.ctas;
+    for (int leaf = (blockIdx.x - ca.ctas) * 8 + warp; leaf < nleaves; leaf += nb * 8) {
         const int lo = ls[leaf], c = ls[leaf + 1] - lo;
+        // the leaf's indices: its bucket, or its range of the scattered slots
+        const int* sl = bucket_stride ? slot + (int64_t)leaf * bucket_stride : slot + lo;
         if (c > 64)
-            leaf_pack<4>(slot, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
+            leaf_pack<4>(sl, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
         else if (c > 32)
-            leaf_pack<2>(slot, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
+            leaf_pack<2>(sl, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
         else if (c > 0)
-            leaf_pack<1>(slot, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
+            leaf_pack<1>(sl, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
     }
     if (!sigma) return;
     for (int o = 16; o > 0; o >>= 1) {
@@ -1047,15 +1089,26 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
         note_launches(1);
     }
     // ---- counting path (kernels return at once if the probe chose LSD) ----
+    // Bucket mode: fixed buckets of kFastLeafMax indices per leaf in the
+    // near-field slots (idle until the near field runs; the LSD path's packed
+    // records use the same region later) when they fit: the count claims the
+    // slots and k_bin_scatter is not launched.  VFMM_BUILD_BUCKET=0: A/B.
+    static const bool bucket_env = !(getenv("VFMM_BUILD_BUCKET") && getenv("VFMM_BUILD_BUCKET")[0] == '0');
+    const bool bucket = bucket_env && (size_t)L.nleaves * kFastLeafMax * sizeof(int) <=
+                                          sizeof(double2) * (size_t)L.n * kNearSlotsAlloc;
+    int* slot = bucket ? (int*)(ws + L.near_uv) : vbuf[(L.passes + 1) & 1];
     launch_k(k_bin_count, small_grid((L.n + kBinILP - 1) / kBinILP, 2368), 256, 0, s, x, y, L.n, xmin, ymin, side, L.levels,
-                                                  kbuf[(L.passes + 1) & 1], ls, ctr);
+                                                  kbuf[(L.passes + 1) & 1], ls, ctr, bucket ? slot : nullptr);
     note_launches(1);
     launch_scan_i32(ls, (int64_t)L.nleaves + 1, state(L.passes + 1), s, nullptr, false,
                     &ctr->sort_fallback, kSortLsdProbe);
-    int* slot = vbuf[(L.passes + 1) & 1];
-    launch_k(k_bin_scatter, small_grid((L.n + kBinILP - 1) / kBinILP, 2368) + ca.ctas, 256, 0, s, kbuf[(L.passes + 1) & 1], L.n,
-             ls, fill, slot, ctr, ca);
-    note_launches(1);
+    if (!bucket) {
+        launch_k(k_bin_scatter, small_grid((L.n + kBinILP - 1) / kBinILP, 2368) + ca.ctas, 256, 0, s, kbuf[(L.passes + 1) & 1], L.n,
+                 ls, fill, slot, ctr, ca);
+        note_launches(1);
+    }
+    CountsArgs ca_pack = ca;
+    if (!bucket) ca_pack.ctas = 0;
     // The path choice is final after k_bin_scatter (a leaf > 128 switches to
     // LSD there).  With a side stream the LSD kernels -- which return at once
     // on the counting path -- run as a parallel branch joined after
@@ -1071,9 +1124,10 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     // gamma and sigma are first read by the record pack (host mode: their
     // copies overlap the binning)
     if (gs_ready) cudaStreamWaitEvent(s, gs_ready, 0);
-    launch_k(k_leaf_pack, std::min(grid_for((int64_t)L.nleaves, 8), 2368u), 256, 0, s, ls, slot, (int)L.nleaves, x, y, g,
+    launch_k(k_leaf_pack, std::min(grid_for((int64_t)L.nleaves, 8), 2368u) + (unsigned)ca_pack.ctas, 256, 0, s, ls, slot,
+                                                              (int)L.nleaves, x, y, g,
                                                               sigma, sigma_stride, fkeys, fperm,
-                                                              src, ctr, lsd_cond);
+                                                              src, ctr, lsd_cond, bucket ? kFastLeafMax : 0, ca_pack);
     note_launches(1);
     cudaGraphNode_t lsd_node = nullptr;
     if (lsd_cond.on) ls_s = graph_cond_begin(s, lsd_cond, &lsd_node);
