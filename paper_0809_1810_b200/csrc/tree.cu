@@ -384,24 +384,41 @@ __device__ __forceinline__ void leaf_pack(const int* __restrict__ sl, int lo, in
         e[k] = p < c ? sl[p] : INT_MAX;
     }
     warp_bitonic<E>(e);
+    // the gathers of two rounds in flight before the first record is packed (the
+    // sigma-dependent branch of q2_of otherwise serialises the rounds of loads)
+    constexpr int H = E < 2 ? E : 2;
 #pragma unroll
-    for (int k = 0; k < E; ++k) {
-        const int p = k * 32 + lane;
-        if (p >= c) continue;
-        const int idx = e[k];
-        const double s = sigma ? sigma[(int64_t)idx * sstride] : 1.0;
-        Src r;
-        r.x = x[idx];
-        r.y = y[idx];
-        r.g = g[idx];
-        r.q2 = q2_of(s, s_prev, q_prev);  // -r^2 / (2 sigma^2) in log2 units
-        src[lo + p] = r;
-        perm[lo + p] = idx;
-        keys[lo + p] = leaf;
-        if (sigma) {
-            const unsigned long long b = ordered_bits(s);
-            smax = b > smax ? b : smax;
-            smin = b < smin ? b : smin;
+    for (int k0 = 0; k0 < E; k0 += H) {
+        double gx[H], gy[H], gg[H], gs[H];
+#pragma unroll
+        for (int j = 0; j < H; ++j) {
+            const bool ok = (k0 + j) * 32 + lane < c;
+            const int idx = ok ? e[k0 + j] : 0;
+            gs[j] = (ok && sigma) ? sigma[(int64_t)idx * sstride] : 1.0;
+            gx[j] = ok ? x[idx] : 0.0;
+            gy[j] = ok ? y[idx] : 0.0;
+            gg[j] = ok ? g[idx] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < H; ++j) {
+            const int k = k0 + j;
+            const int p = k * 32 + lane;
+            if (p >= c) continue;
+            const int idx = e[k];
+            const double s = gs[j];
+            Src r;
+            r.x = gx[j];
+            r.y = gy[j];
+            r.g = gg[j];
+            r.q2 = q2_of(s, s_prev, q_prev);  // -r^2 / (2 sigma^2) in log2 units
+            src[lo + p] = r;
+            perm[lo + p] = idx;
+            keys[lo + p] = leaf;
+            if (sigma) {
+                const unsigned long long b = ordered_bits(s);
+                smax = b > smax ? b : smax;
+                smin = b < smin ? b : smin;
+            }
         }
     }
 }
