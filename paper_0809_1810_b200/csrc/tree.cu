@@ -1037,6 +1037,13 @@ struct ProbeArgs {
     int probe_mode;
 };
 __device__ void sort_probe(const ProbeArgs& a, Counters* ctr) {
+    // below kLsdMinN the sample cannot choose the LSD path: skip its loads (the
+    // probe was the longest dependency chain of the build's first kernel)
+    if (a.probe_mode == 1) {
+        if (threadIdx.x == 0) ctr->sort_fallback = kSortLsdProbe;
+        return;
+    }
+    if (a.probe_mode != 0 || a.n <= kLsdMinN) return;
     sort_probe_impl(a.x, a.y, a.n, a.xmin, a.ymin, a.side, a.levels, a.probe_mode, ctr);
 }
 // The build's first kernel: zero the scratch regions, and CTA 0 also runs the
