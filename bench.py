@@ -497,12 +497,18 @@ def run_ours(args):
     for p in pipe.pending:
         p.result()
     torch.cuda.synchronize(dev)
-    t0 = time.perf_counter()
-    pend = [pipe.submit(hx, hy, hg, hs) for _ in range(k_pipe)]
-    for p in pipe.pending:
-        p.result()
-    torch.cuda.synchronize(dev)
-    e2e = (time.perf_counter() - t0) * 1e3 / k_pipe
+    # three batches of k_pipe steps, each timed on its own; the median is reported
+    # (and all three kept in the line): PCIe-bound, a batch now and then reads ~7%
+    # slower on this pool's hosts
+    e2e_batches = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        pend = [pipe.submit(hx, hy, hg, hs) for _ in range(k_pipe)]
+        for p in pipe.pending:
+            p.result()
+        torch.cuda.synchronize(dev)
+        e2e_batches.append((time.perf_counter() - t0) * 1e3 / k_pipe)
+    e2e = statistics.median(e2e_batches)
     assert torch.equal(pend[-1].out, ref_vel.cpu()), "pipelined result differs"
     # a uniform sigma array travels as one value (VFMM_FLAG_SIGMA_SCALAR)
     sigma_uniform = bool((w.sigma.view(np.int64) == w.sigma.view(np.int64)[0]).all())
@@ -558,10 +564,10 @@ def run_ours(args):
                    "m2l_count": st.m2l_count, "near_pair_count": st.near_pair_count},
         "e2e": {"value": n / (e2e * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": 3 * 8 * n + (8 if sigma_uniform else 8 * n),
-                "d2h_bytes_per_step": 2 * 8 * n, "ms_per_step": e2e,
+                "d2h_bytes_per_step": 2 * 8 * n, "ms_per_step": e2e, "batches_ms_per_step": e2e_batches,
                 "mode": f"evaluate_host_async via HostPipeline(depth={args.e2e_depth}, compute_streams="
                         f"{args.e2e_compute_streams}: input copies on one H2D stream, cached CUDA graph per slot "
-                        f"on the compute streams, results on one D2H stream), {k_pipe} steps, host wall clock",
+                        f"on the compute streams, results on one D2H stream), median of 3 batches of {k_pipe} steps, host wall clock",
                 "latency_ms": e2e_latency,
                 "latency_mode": "one synchronous evaluate_host call (stats on; copies overlapped with the build), CUDA events",
                 "reference_signature_ms": sig_ms,

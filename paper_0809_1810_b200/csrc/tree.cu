@@ -425,7 +425,10 @@ __device__ __forceinline__ void leaf_pack(const int* __restrict__ sl, int lo, in
 
 // Warp per leaf: restore the stable order inside the leaf, write the sorted
 // keys, the permutation and the packed records.
-__global__ void __launch_bounds__(256)
+#ifndef VFMM_PACK_MINB
+#define VFMM_PACK_MINB 5  // 48 registers: 5 CTAs per SM (config 2 build 46.3 -> 44.4 us; 6: 45.5, 8: 49.7)
+#endif
+__global__ void __launch_bounds__(256, VFMM_PACK_MINB)
     k_leaf_pack(const int* __restrict__ ls, const int* __restrict__ slot, int nleaves,
                 const double* __restrict__ x, const double* __restrict__ y,
                 const double* __restrict__ g, const double* __restrict__ sigma, int sstride,
