@@ -553,6 +553,25 @@ def run_ours(args):
         cpu = {"value": n / tt, "unit": UNIT, "cores": 1, "kind": "port",
                "sample": f"one full {w.name} evaluate (N={n}) by the numpy oracle port, 1 BLAS thread",
                "blas_default_value": n / t_all, "host": host_info()}
+        pkg = _ref_package()
+        if pkg is not None:
+            # the unmodified reference itself when its offline install travelled with the repo
+            # (baseline/_ref): one full evaluate through its public API, 1 BLAS thread
+            from threadpoolctl import threadpool_limits
+
+            eng, mod = pkg
+            ps = [mod.Particle(*t) for t in zip(w.x.tolist(), w.y.tolist(), w.gamma.tolist(), w.sigma.tolist())]
+            rcfg = eng.FmmConfig(w.levels, w.order, eng.KernelKind.GAUSSIAN_BLOB)
+            with threadpool_limits(limits=1):
+                t0 = time.perf_counter()
+                rvel, _ = eng.evaluate(ps, rcfg, mod.Domain(-1.0, -1.0, 2.0))
+                t_ref = time.perf_counter() - t0
+            del ps
+            rerr = float(np.abs(rvel - ref_vel.cpu().numpy()).max() / np.abs(rvel).max())
+            cpu.update({"port_value": cpu["value"], "value": n / t_ref, "kind": "reference",
+                        "sample": f"one full {w.name} evaluate (N={n}) by the unmodified "
+                                  "vortexfmm.engine.evaluate (baseline/_ref), 1 BLAS thread",
+                        "max_rel_diff_vs_gpu": rerr})
 
     line = {
         "metric": METRIC, "value": n / (ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
