@@ -8,8 +8,9 @@
 // k_zero_regions    the counters and the scratch regions; CTA 0 samples the
 //                   input order and picks the sort path (probe)
 // Counting path (coherent input order, every leaf <= kFastLeafMax particles;
-// config 2: 4 kernels in all -- bucket mode, see k_bin_count; 5 when the
-// buckets do not fit the near-field slots, i.e. below ~5 particles per leaf):
+// config 2: 3 kernels in all -- bucket mode with the scan fused into the pack,
+// see k_bin_count / k_leaf_pack; 4 at l >= 8; 5 when the buckets do not fit
+// the near-field slots, i.e. below ~5 particles per leaf):
 //   k_bin_count     floor-rule binning with max-edge clamp + domain check;
 //                   per-leaf counts (warp-aggregated atomics), four
 //                   particles per thread in flight
@@ -206,6 +207,10 @@ struct CountsArgs {
     int* counts;
     int* ntask;
 };
+// FROM_CNT: `ls` holds the raw per-leaf counts instead of leaf_starts (the
+// fused-scan build, where leaf_starts is being written by the same kernel):
+// a cell's rows are summed leaf by leaf (int4 loads).
+template <bool FROM_CNT = false>
 __device__ __forceinline__ void counts_tasks_body(int64_t t, const int* __restrict__ ls,
                                                   const CountsArgs& a, Counters* __restrict__ ctr) {
     // A cell of level k spans s = 2^(levels-k) leaf rows; g = min(32, s)
@@ -239,7 +244,20 @@ __device__ __forceinline__ void counts_tasks_body(int64_t t, const int* __restri
     if (valid)
         for (int r = r0 + sub; r < r1; r += g) {
             const int64_t row = (int64_t)r * m;
-            c += ls[row + (int64_t)(ix + 1) * s] - ls[row + (int64_t)ix * s];
+            if (!FROM_CNT) {
+                c += ls[row + (int64_t)(ix + 1) * s] - ls[row + (int64_t)ix * s];
+            } else if (s >= 4) {
+                const int4* p4 = reinterpret_cast<const int4*>(ls + row + (int64_t)ix * s);
+                int c4[4] = {0, 0, 0, 0};
+#pragma unroll 4
+                for (int j = 0; j < (s >> 2); ++j) {
+                    const int4 q = p4[j];
+                    c4[j & 3] += (q.x + q.y) + (q.z + q.w);
+                }
+                c += (c4[0] + c4[1]) + (c4[2] + c4[3]);
+            } else {
+                for (int j = 0; j < s; ++j) c += ls[row + (int64_t)ix * s + j];
+            }
         }
     // every lane runs the same shuffles; a lane adds only within its g-group
 #pragma unroll
@@ -253,7 +271,8 @@ __device__ __forceinline__ void counts_tasks_body(int64_t t, const int* __restri
         // only leaves of the owned row strip get near-field tasks
         if (k == levels) {
             a.ntask[cell] = (iy >= rows.lo && iy < rows.hi) ? (c + a.chunk - 1) / a.chunk : 0;
-            full = ls[cell + 1] - ls[cell];  // owned and halo rows (the symmetric P2P touches both)
+            // owned and halo rows (the symmetric P2P touches both)
+            full = FROM_CNT ? ls[cell] : ls[cell + 1] - ls[cell];
         }
     }
     // largest leaf: one atomic per warp
@@ -428,12 +447,21 @@ __device__ __forceinline__ void leaf_pack(const int* __restrict__ sl, int lo, in
 #ifndef VFMM_PACK_MINB
 #define VFMM_PACK_MINB 5  // 48 registers: 5 CTAs per SM (config 2 build 46.3 -> 44.4 us; 6: 45.5, 8: 49.7)
 #endif
+constexpr int kPackFusedMaxLeaves = 1 << 14;  // fused-scan mode: l <= 7
+constexpr int kPackFusedGrid = 148 * VFMM_PACK_MINB;
+// Fused-scan mode (cnt != nullptr; bucket mode at l <= 7): `cnt` holds the raw
+// per-leaf counts and this kernel also produces leaf_starts, so the scan
+// launch between the count and the pack drops out.  A CTA owns a contiguous
+// run of L <= 32 leaves: it sums the counts below its run (striped int4
+// loads, one round trip; the whole array is 64 KB in L2), scans its own L
+// counts in one warp, writes its part of leaf_starts and packs its leaves.
 __global__ void __launch_bounds__(256, VFMM_PACK_MINB)
-    k_leaf_pack(const int* __restrict__ ls, const int* __restrict__ slot, int nleaves,
+    k_leaf_pack(int* __restrict__ ls, const int* __restrict__ slot, int nleaves,
                 const double* __restrict__ x, const double* __restrict__ y,
                 const double* __restrict__ g, const double* __restrict__ sigma, int sstride,
                 int* __restrict__ keys, int* __restrict__ perm, Src* __restrict__ src,
-                Counters* __restrict__ ctr, GraphCond lsd_cond, int bucket_stride, CountsArgs ca) {
+                Counters* __restrict__ ctr, GraphCond lsd_cond, int bucket_stride, CountsArgs ca,
+                const int* __restrict__ cnt) {
     pdl_enter();
     // the path choice is final here (k_bin_scatter / k_bin_count's buckets): a
     // captured graph runs the LSD kernels (an IF node after this kernel) only
@@ -443,24 +471,77 @@ __global__ void __launch_bounds__(256, VFMM_PACK_MINB)
     // bucket mode: the first ca.ctas CTAs compute the occupancy pyramid and the
     // task counts (k_bin_scatter's first CTAs do otherwise)
     if ((int)blockIdx.x < ca.ctas) {
-        counts_tasks_body((int64_t)blockIdx.x * blockDim.x + threadIdx.x, ls, ca, ctr);
+        if (cnt)
+            counts_tasks_body<true>((int64_t)blockIdx.x * blockDim.x + threadIdx.x, cnt, ca, ctr);
+        else
+            counts_tasks_body((int64_t)blockIdx.x * blockDim.x + threadIdx.x, ls, ca, ctr);
         return;
     }
     __shared__ unsigned long long wmax[8], wmin[8];
+    __shared__ int s_part[8], s_lo[32], s_c[32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned long long smax = 0ull, smin = ~0ull;
     double s_prev = __longlong_as_double(0x7ff8000000000000ll), q_prev = 0.0;  // NaN: nothing cached
     const int nb = gridDim.x - ca.ctas;
-    for (int leaf = (blockIdx.x - ca.ctas) * 8 + warp; leaf < nleaves; leaf += nb * 8) {
-        const int lo = ls[leaf], c = ls[leaf + 1] - lo;
-        // the leaf's indices: its bucket, or its range of the scattered slots
-        const int* sl = bucket_stride ? slot + (int64_t)leaf * bucket_stride : slot + lo;
-        if (c > 64)
-            leaf_pack<4>(sl, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
-        else if (c > 32)
-            leaf_pack<2>(sl, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
-        else if (c > 0)
-            leaf_pack<1>(sl, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
+    if (cnt) {
+        const int L = (nleaves + nb - 1) / nb;  // <= 32 (launch_build)
+        const int first = (blockIdx.x - ca.ctas) * L;
+        if (first >= nleaves) return;
+        // the counts below the run
+        int part = 0;
+        const int4* c4 = reinterpret_cast<const int4*>(cnt);
+        for (int i4 = threadIdx.x; i4 * 4 < first; i4 += 256) {
+            const int4 q = c4[i4];
+            const int e = i4 * 4;
+            part += q.x + (e + 1 < first ? q.y : 0) + (e + 2 < first ? q.z : 0) + (e + 3 < first ? q.w : 0);
+        }
+        // the run's own counts (warp 0), meanwhile
+        int cj = 0;
+        if (warp == 0 && lane < L && first + lane < nleaves) cj = cnt[first + lane];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) s_part[warp] = part;
+        __syncthreads();
+        if (warp == 0) {
+            int base = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) base += s_part[w];
+            int incl = cj;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            s_lo[lane] = base + incl - cj;
+            s_c[lane] = cj;
+            if (lane < L && first + lane < nleaves) {
+                ls[first + lane] = base + incl - cj;
+                if (first + lane == nleaves - 1) ls[nleaves] = base + incl;
+            }
+        }
+        __syncthreads();
+        for (int j = warp; j < L && first + j < nleaves; j += 8) {
+            const int leaf = first + j, lo = s_lo[j], c = s_c[j];
+            const int* sl = slot + (int64_t)leaf * bucket_stride;
+            if (c > 64)
+                leaf_pack<4>(sl, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
+            else if (c > 32)
+                leaf_pack<2>(sl, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
+            else if (c > 0)
+                leaf_pack<1>(sl, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
+        }
+    } else {
+        for (int leaf = (blockIdx.x - ca.ctas) * 8 + warp; leaf < nleaves; leaf += nb * 8) {
+            const int lo = ls[leaf], c = ls[leaf + 1] - lo;
+            // the leaf's indices: its bucket, or its range of the scattered slots
+            const int* sl = bucket_stride ? slot + (int64_t)leaf * bucket_stride : slot + lo;
+            if (c > 64)
+                leaf_pack<4>(sl, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
+            else if (c > 32)
+                leaf_pack<2>(sl, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
+            else if (c > 0)
+                leaf_pack<1>(sl, lo, c, leaf, x, y, g, sigma, sstride, keys, perm, src, smax, smin, s_prev, q_prev);
+        }
     }
     if (!sigma) return;
     for (int o = 16; o > 0; o >>= 1) {
@@ -1124,11 +1205,18 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     const bool bucket = bucket_env && (size_t)L.nleaves * kFastLeafMax * sizeof(int) <=
                                           sizeof(double2) * (size_t)L.n * kNearSlotsAlloc;
     int* slot = bucket ? (int*)(ws + L.near_uv) : vbuf[(L.passes + 1) & 1];
+    // Fused scan (bucket mode, l <= 7): the counts go to the (zeroed, otherwise
+    // unused) slot-cursor array and k_leaf_pack derives leaf_starts from them;
+    // no scan launch.  VFMM_BUILD_FUSED_SCAN=0: A/B.
+    static const bool fused_env = !(getenv("VFMM_BUILD_FUSED_SCAN") && getenv("VFMM_BUILD_FUSED_SCAN")[0] == '0');
+    const bool fused = bucket && fused_env && L.nleaves <= kPackFusedMaxLeaves;
+    int* cnt = fused ? fill : ls;
     launch_k(k_bin_count, small_grid((L.n + kBinILP - 1) / kBinILP, 2368), 256, 0, s, x, y, L.n, xmin, ymin, side, L.levels,
-                                                  kbuf[(L.passes + 1) & 1], ls, ctr, bucket ? slot : nullptr);
+                                                  kbuf[(L.passes + 1) & 1], cnt, ctr, bucket ? slot : nullptr);
     note_launches(1);
-    launch_scan_i32(ls, (int64_t)L.nleaves + 1, state(L.passes + 1), s, nullptr, false,
-                    &ctr->sort_fallback, kSortLsdProbe);
+    if (!fused)
+        launch_scan_i32(ls, (int64_t)L.nleaves + 1, state(L.passes + 1), s, nullptr, false,
+                        &ctr->sort_fallback, kSortLsdProbe);
     if (!bucket) {
         launch_k(k_bin_scatter, small_grid((L.n + kBinILP - 1) / kBinILP, 2368) + ca.ctas, 256, 0, s, kbuf[(L.passes + 1) & 1], L.n,
                  ls, fill, slot, ctr, ca);
@@ -1151,10 +1239,13 @@ void launch_build(const Layout& L, const double* x, const double* y, const doubl
     // gamma and sigma are first read by the record pack (host mode: their
     // copies overlap the binning)
     if (gs_ready) cudaStreamWaitEvent(s, gs_ready, 0);
-    launch_k(k_leaf_pack, std::min(grid_for((int64_t)L.nleaves, 8), 2368u) + (unsigned)ca_pack.ctas, 256, 0, s, ls, slot,
+    const unsigned pack_grid = fused ? std::min(grid_for((int64_t)L.nleaves, 8), (unsigned)kPackFusedGrid)
+                                     : std::min(grid_for((int64_t)L.nleaves, 8), 2368u);
+    launch_k(k_leaf_pack, pack_grid + (unsigned)ca_pack.ctas, 256, 0, s, ls, slot,
                                                               (int)L.nleaves, x, y, g,
                                                               sigma, sigma_stride, fkeys, fperm,
-                                                              src, ctr, lsd_cond, bucket ? kFastLeafMax : 0, ca_pack);
+                                                              src, ctr, lsd_cond, bucket ? kFastLeafMax : 0, ca_pack,
+                                                              fused ? (const int*)cnt : (const int*)nullptr);
     note_launches(1);
     cudaGraphNode_t lsd_node = nullptr;
     if (lsd_cond.on) ls_s = graph_cond_begin(s, lsd_cond, &lsd_node);
