@@ -74,6 +74,63 @@ def test_tree_structure_exact(name):
         off += 4**k
 
 
+def _fuzz_case(seed):
+    """Random (n, levels, distribution) across the build's mode boundaries: buckets with the
+    scan fused into the pack (l <= 7, >= ~5 particles per leaf), buckets with the scan launch
+    (l = 8), the scatter path (sparse leaves), a leaf above 128 (LSD fallback), tiny inputs."""
+    rng = np.random.default_rng(1000 + seed)
+    lv = int(rng.integers(2, 9))
+    occ = [0.3, 2.0, 7.0, 30.0, 70.0][seed % 5]
+    n = int(max(1, min(400_000, occ * 4**lv * rng.uniform(0.7, 1.3))))
+    kind = seed % 4
+    if kind == 0:  # uniform
+        x, y = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    elif kind == 1:  # clustered: some leaves far above the mean
+        c = rng.uniform(-0.8, 0.8, (4, 2))
+        w = rng.integers(0, 4, n)
+        x = np.clip(c[w, 0] + 0.05 * rng.standard_normal(n), -1, 1)
+        y = np.clip(c[w, 1] + 0.05 * rng.standard_normal(n), -1, 1)
+    elif kind == 2:  # lattice, row-major (coherent order), with points on cell edges
+        m = max(1, int(np.sqrt(n)))
+        gx, gy = np.meshgrid(np.linspace(-1, 1, m), np.linspace(-1, 1, m))
+        x, y = gx.ravel().copy(), gy.ravel().copy()
+    else:  # uniform, a few duplicates and domain corners
+        x, y = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+        x[: min(n, 4)] = [-1.0, 1.0, -1.0, 1.0][: min(n, 4)]
+        y[: min(n, 4)] = [-1.0, -1.0, 1.0, 1.0][: min(n, 4)]
+        if n > 10:
+            x[5:10] = x[4]
+            y[5:10] = y[4]
+    n = x.size
+    return x, y, rng.standard_normal(n) * 1e-3, np.full(n, 0.02), lv
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_tree_structure_exact_randomised(seed):
+    """The build's outputs equal the oracle bit for bit and the velocities match it, across the
+    mode boundaries of the counting path (see _fuzz_case)."""
+    x, y, g, s, lv = _fuzz_case(seed)
+    dom = (-1.0, -1.0, 2.0)
+    order = 6
+    vel, st, _ = run(x, y, g, s, lv, order, True, dom, overlap=bool(seed & 1))
+    n = x.size
+    ws = Workspace.get(n, lv, order, torch.device("cuda", torch.cuda.current_device()))
+    tree = O.Tree(O.leaf_keys(x, y, lv, *dom), lv, *dom)
+    assert np.array_equal(ws.view("perm", torch.int32, n).cpu().numpy(), tree.order)
+    assert np.array_equal(ws.view("leaf_key", torch.int32, n).cpu().numpy(), tree.sorted_leaf)
+    assert np.array_equal(ws.view("leaf_starts", torch.int32, 4**lv + 1).cpu().numpy(), tree.leaf_starts)
+    counts = ws.view("counts", torch.int32, sum(4**k for k in range(lv + 1))).cpu().numpy()
+    off = 0
+    for k in range(lv + 1):
+        assert np.array_equal(counts[off: off + 4**k], tree.counts[k])
+        off += 4**k
+    if n <= 60_000:  # the oracle's near field is O(n * 9 * leaf) python-side work
+        ref, ost = O.evaluate(x, y, g, s, lv, order, True, dom)
+        assert st.m2l_count == ost["m2l_count"] and st.near_pair_count == ost["near_pair_count"]
+        vmax = np.abs(ref).max()
+        assert vmax == 0.0 or np.abs(vel - ref).max() / vmax <= REL_TOL
+
+
 def _unscale(ws, c, dom):
     """GPU multipoles/locals converted back to the reference convention."""
     n, lv, p = c["x"].size, c["levels"], c["order"]
