@@ -345,6 +345,7 @@ bool make_layout(int64_t n, int levels, int order, Layout* L) {
     L->task_scratch = take(sizeof(int) * L->nleaves);
     L->fill = take(sizeof(int) * L->nleaves);
     L->near_done = take(sizeof(int) * L->nleaves);  // symmetric P2P: writers done per leaf
+    L->unperm_cursor = take(sizeof(int) * kUnpermCursorStride * 1025);  // staged un-permute
     L->scan_state = take(L->scan_state_bytes);
     L->src = take(sizeof(Src) * n);
     L->near_uv = take(sizeof(double2) * n * kNearSlotsAlloc);
@@ -664,8 +665,23 @@ int evaluate_impl(const double* x, const double* y, const double* gamma, const d
             fo = FusedOut{src, keys, perm, ls, near_uv, u, v, xmin, ymin, side};
         }
         rec(5, fs);
+        // Staged un-permute for large whole-domain calls: decided on the device by the
+        // sort path (random input order), see k_unpermute; the records live in the
+        // near-field reaction slots 1-2, free once the slot sums are in slot 0.
+        static const bool unperm_env = !(getenv("VFMM_UNPERM_STAGED") && getenv("VFMM_UNPERM_STAGED")[0] == '0');
+        const bool stage_out = unperm_env && fuse && fo.u && n >= ((int64_t)1 << 22) && rows.lo == 0 &&
+                               rows.hi == (1 << levels) && n <= INT32_MAX && l2l_stageable(L);
+        if (stage_out) {
+            fo.stage = (UnpermRec*)(near_uv + n);
+            fo.stage_cursor = (int*)(ws + L.unperm_cursor);
+            fo.stage_shift = unperm_shift(n);
+            fo.n_total = n;
+            fo.ctr = ctr;
+            launch_unpermute_prepare(L, fo, fs);
+        }
         launch_l2l(L, T, loc, (double2*)(ws + L.leaf_loc), (const double2*)(ws + L.anc), rows, fo,
                    fs);
+        if (stage_out) launch_unpermute(L, fo, fs);
         rec(4, fs);
         if (fuse) {
             if (overlap && up) {

@@ -135,7 +135,12 @@ __device__ __forceinline__ int64_t lvl_off(int k, int P) {
 // CTA size: 128 threads (8 CTAs/SM: config 2's 1,024 CTAs in one wave;
 // downward 0.050 -> 0.043 ms, config 3 1.69 -> 1.47 ms) unless the grid is
 // small (config 1: 64 CTAs, where 256 threads per CTA are faster).
-template <int kL2LThreads>
+// STAGED (large inputs; launch_l2l): when the build found the input order random
+// (the LSD sort path), the un-permuting stores -- 16-byte writes to random
+// sectors of an output far larger than L2, i.e. a DRAM read-modify-write each
+// -- go through k_unpermute's buckets instead (see there).  Its own instance,
+// so the instance every other call uses is unchanged.
+template <int kL2LThreads, bool STAGED = false>
 __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
     k_l2l_fused(double2* __restrict__ loc, double2* __restrict__ leaf_loc,
                 const double2* __restrict__ anc_m2l, int ls, int levels, int P,
@@ -150,6 +155,8 @@ __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
 #endif
     pdl_enter();
     mark();
+    // a staged call launches both instances: each runs only on its sort path
+    if (fo.stage && (fo.ctr->sort_fallback == kSortPathLsdProbe) != STAGED) return;
     extern __shared__ double2 sm[];
     const int depth = levels - ls;
     double2* sF = sm + (size_t)sub_off(depth + 1) * P;  // [4][P]
@@ -341,6 +348,28 @@ __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
     }
     __syncthreads();
     const int total = rp[side];
+    // Staged output: the CTA counts its particles per destination bucket in
+    // shared memory, claims one range per bucket from the global cursors
+    // (~4 particles per claim at config 3 instead of one global atomic each),
+    // then places its records by shared-memory ranks.
+    __shared__ int s_cnt[STAGED ? 1024 : 1], s_base[STAGED ? 1024 : 1];
+    if (STAGED) {
+        const int nbk = (int)(((int64_t)fo.n_total + ((int64_t)1 << fo.stage_shift) - 1) >> fo.stage_shift);
+        for (int b = threadIdx.x; b < nbk; b += kL2LThreads) s_cnt[b] = 0;
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < total; idx += kL2LThreads) {
+            int ly = 0;
+            while (ly + 1 < side && rp[ly + 1] <= idx) ++ly;
+            atomicAdd(&s_cnt[fo.perm[rb[ly] + idx - rp[ly]] >> fo.stage_shift], 1);
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < nbk; b += kL2LThreads) {
+            const int c = s_cnt[b];
+            s_base[b] = c ? atomicAdd(&fo.stage_cursor[(size_t)b * kUnpermCursorStride], c) : 0;
+            s_cnt[b] = 0;
+        }
+        __syncthreads();
+    }
     constexpr int kB = 4;
     for (int base = threadIdx.x; base < total; base += kB * kL2LThreads) {
         int jj[kB], lyy[kB];
@@ -384,7 +413,18 @@ __global__ void __launch_bounds__(kL2LThreads, kL2LThreads == 128 ? 8 : 4)
             const double2 f = ff[u];
             // f_to_velocity: u = Im f / 2pi, v = Re f / 2pi; then far + near
             const double uo = f.y * kInv2Pi + nv[u].x, vo = f.x * kInv2Pi + nv[u].y;
-            if (fo.v) {
+            if (STAGED) {
+                const int b = o[u] >> fo.stage_shift;
+                const int pos = s_base[b] + atomicAdd(&s_cnt[b], 1);
+                VCHECK(pos >= 0 && pos < (1 << fo.stage_shift) &&
+                       (((int64_t)b << fo.stage_shift) + pos) < fo.n_total);
+                UnpermRec rcd;
+                rcd.u = uo;
+                rcd.v = vo;
+                rcd.dest = o[u];
+                rcd.pad[0] = rcd.pad[1] = rcd.pad[2] = 0;
+                fo.stage[((size_t)b << fo.stage_shift) + pos] = rcd;
+            } else if (fo.v) {
                 fo.u[o[u]] = uo;
                 fo.v[o[u]] = vo;
             } else {
@@ -449,10 +489,88 @@ void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_lo
     const size_t shm = sub_smem(L.levels - ls, L.P) + sizeof(double2) * (2 * L.P + 1) +
                        sizeof(double) * (L.P + 1) + sizeof(double2) * (ls - 2) * L.P;
     const unsigned ctas = (unsigned)(1ll << (2 * ls));
+    if (fo.stage && ctas >= 148 * 4) {  // both instances: each returns at once off its path
+        launch_k(k_l2l_fused<128, true>, ctas, 128, shm, s, loc, leaf_loc, anc, ls, L.levels, L.P, T, rows, fo);
+        note_launches(1);
+    }
     if (ctas >= 148 * 4)
         launch_k(k_l2l_fused<128>, ctas, 128, shm, s, loc, leaf_loc, anc, ls, L.levels, L.P, T, rows, fo);
     else
         launch_k(k_l2l_fused<256>, ctas, 256, shm, s, loc, leaf_loc, anc, ls, L.levels, L.P, T, rows, fo);
+    note_launches(1);
+}
+
+// ---------------------------------------------------------------------------
+// Staged un-permute.  With a random input order the fused L2P's output stores
+// are 16-byte writes to random sectors of an array far larger than L2: every
+// store becomes a DRAM read-modify-write (config 3: the downward pass read
+// 2.1 GB and wrote 1.3 GB for 0.27 GB of velocities).  Staged: the fused L2P
+// appends (u, v, destination) records -- 32 bytes, a full sector each -- to the
+// bucket of its destination's high bits (every bucket of a permutation fills
+// exactly, so bucket b owns records [b 2^shift, (b + 1) 2^shift)), and this
+// kernel walks the records in bucket order: the CTAs resident at any time
+// write into a window of a few buckets (tens of MB), where the two halves of an
+// output sector meet in L2 before it is written back once.
+#ifndef VFMM_UNPERM_PER
+#define VFMM_UNPERM_PER 2  // records per thread: 1 / 2 / 4 -> config 3 downward 0.998 / 1.041 / 1.093 ms, idle launch (coherent order) +0.09 / +0.055 / +0.04 ms
+#endif
+constexpr int kUnpermPer = VFMM_UNPERM_PER;
+constexpr int kUnpermChunk = 256 * kUnpermPer;
+__global__ void __launch_bounds__(256)
+    k_unpermute(const UnpermRec* __restrict__ stage, int64_t n, double* __restrict__ u,
+                double* __restrict__ v, const Counters* __restrict__ ctr) {
+    pdl_enter();
+    if (ctr->sort_fallback != kSortPathLsdProbe) return;
+    // a CTA owns kUnpermChunk consecutive records (one bucket's, mostly), its
+    // threads kUnpermPer of them each, all loads in flight together; CTAs run in
+    // index order, so the records being written at any time are a sliding window
+    // of a few buckets
+    const int64_t base = (int64_t)blockIdx.x * kUnpermChunk + threadIdx.x;
+    UnpermRec r[kUnpermPer];
+#pragma unroll
+    for (int k = 0; k < kUnpermPer; ++k) {
+        const int64_t t = base + k * 256;
+        if (t < n) r[k] = stage[t];
+    }
+#pragma unroll
+    for (int k = 0; k < kUnpermPer; ++k) {
+        const int64_t t = base + k * 256;
+        if (t >= n) break;
+        if (v) {
+            u[r[k].dest] = r[k].u;
+            v[r[k].dest] = r[k].v;
+        } else {
+            reinterpret_cast<double2*>(u)[r[k].dest] = make_double2(r[k].u, r[k].v);
+        }
+    }
+}
+
+__global__ void k_unpermute_zero(int* __restrict__ cursor, int nbuckets, const Counters* __restrict__ ctr) {
+    pdl_enter();
+    if (ctr->sort_fallback != kSortPathLsdProbe) return;
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nbuckets; b += gridDim.x * blockDim.x)
+        cursor[(size_t)b * kUnpermCursorStride] = 0;
+}
+
+bool l2l_stageable(const Layout& L) {  // the fused L2L's large-grid instance has the staged variant
+    return L.levels > 2 && (1ll << (2 * l2l_split_level(L.levels, L.P))) >= 148 * 4;
+}
+
+int unperm_shift(int64_t n) {
+    int shift = 16;
+    while ((n >> shift) >= 1024) ++shift;
+    return shift;
+}
+
+void launch_unpermute_prepare(const Layout& L, const FusedOut& fo, cudaStream_t s) {
+    const int nb = (int)((L.n + ((int64_t)1 << fo.stage_shift) - 1) >> fo.stage_shift);
+    launch_k(k_unpermute_zero, 4, 256, 0, s, fo.stage_cursor, nb, fo.ctr);
+    note_launches(1);
+}
+
+void launch_unpermute(const Layout& L, const FusedOut& fo, cudaStream_t s) {
+    launch_k(k_unpermute, (unsigned)((L.n + kUnpermChunk - 1) / kUnpermChunk), 256, 0, s,
+             (const UnpermRec*)fo.stage, L.n, fo.u, fo.v, fo.ctr);
     note_launches(1);
 }
 

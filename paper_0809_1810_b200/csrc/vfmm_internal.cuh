@@ -77,6 +77,7 @@ struct Layout {
     int levels, order, P;  // P = order + 1
     int digit_bits, passes, wc, nchunks;
     size_t nleaves;
+    size_t unperm_cursor;
     size_t key_a, key_b, val_a, val_b, hist, task_scratch, fill, near_done, scan_state, src, near_uv, leaf_starts, anc,
         counts, mult, loc, leaf_loc, tasks, stage, counters, total;
     size_t scan_state_tiles, scan_state_bytes, hist_bytes;  // per scan instance: 1 ticket + tiles
@@ -213,6 +214,14 @@ void launch_m2l(const Layout& L, const Tables* T, const double2* mult, const int
 int l2l_split_level(int levels, int P);
 // L2P + combine fused into the finest L2L level (single-GPU evaluates): the
 // near-field totals must be complete when the L2L runs.
+// One staged output record: 32 bytes, one full sector per store.
+struct __align__(16) UnpermRec {
+    double u, v;
+    int dest;
+    int pad[3];
+};
+constexpr int kUnpermCursorStride = 32;  // ints: a cursor per 128-byte line
+constexpr int kSortPathLsdProbe = 1;     // Counters::sort_fallback: random input order (tree.cu)
 struct FusedOut {
     const Src* src;
     const int* keys;
@@ -222,9 +231,22 @@ struct FusedOut {
     double* u;            // null: not fused (leaf_loc only)
     double* v;            // null: interleaved (N, 2) output
     double xmin, ymin, side;
+    // staged un-permute (large random-order inputs, see k_unpermute): records go to
+    // buckets of 2^stage_shift destination indices first; null = write straight to u / v
+    UnpermRec* stage = nullptr;
+    int* stage_cursor = nullptr;  // one cursor per bucket, kUnpermCursorStride ints apart
+    int stage_shift = 0;
+    int64_t n_total = 0;
+    const Counters* ctr = nullptr;
 };
 void launch_l2l(const Layout& L, const Tables* T, double2* loc, double2* leaf_loc,
                 const double2* anc, Rows rows, const FusedOut& fo, cudaStream_t s);
+// Second pass of the staged un-permute (after launch_l2l with fo.stage set).
+void launch_unpermute(const Layout& L, const FusedOut& fo, cudaStream_t s);
+// Zero the bucket cursors (enqueued before the fused L2L of a staged call).
+void launch_unpermute_prepare(const Layout& L, const FusedOut& fo, cudaStream_t s);
+bool l2l_stageable(const Layout& L);
+int unperm_shift(int64_t n);  // log2 of the bucket size: 2^16 destinations, <= 1024 buckets
 int p2p_targets_per_lane();  // 1 or 2 (env VFMM_P2P_TPT, default 1)
 // the near field: P2P kernels and the per-particle near-field totals (slot 0)
 void launch_p2p(const Layout& L, const Tables* T, const Src* src, const int* leaf_starts,

@@ -15,7 +15,16 @@ cfg_idx = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 15
 w = W.by_index(cfg_idx)
 dev = torch.device("cuda", 0)
-xd, yd, gd, sd = (torch.from_numpy(a).to(dev) for a in (w.x, w.y, w.gamma, w.sigma))
+xs, ys, gs, ss = w.x, w.y, w.gamma, w.sigma
+if os.environ.get("PROBE_PRESORT"):  # the same particles in leaf order (a coherent input order)
+    import numpy as np
+
+    m = 1 << w.levels
+    ix = np.minimum(((xs + 1.0) / 2.0 * m).astype(np.int64), m - 1)
+    iy = np.minimum(((ys + 1.0) / 2.0 * m).astype(np.int64), m - 1)
+    o = np.argsort(iy * m + ix, kind="stable")
+    xs, ys, gs, ss = xs[o], ys[o], gs[o], ss[o]
+xd, yd, gd, sd = (torch.from_numpy(a).to(dev) for a in (xs, ys, gs, ss))
 cfg = vf.FmmConfig(w.levels, w.order, vf.KernelKind.GAUSSIAN_BLOB)
 keys = ("t_build", "t_upward", "t_m2l", "t_downward", "t_near", "t_total")
 rows = {k: [] for k in keys}
