@@ -101,6 +101,21 @@ def test_to_arrays_and_enclosing_domain():
     assert vf.enclosing_domain([vf.Particle(0.3, 0.3, 1.0, 0.1)]).side == 1.0
 
 
+def test_to_arrays_accepts_ints_tuples_and_duck_typed_particles():
+    """Integer fields, a tuple instead of a list and objects that only share the
+    reference's field names (model.py:29-36, 125-137) all unpack to float64 arrays."""
+    from types import SimpleNamespace
+
+    parts = (vf.Particle(1, 2, 3, 1), SimpleNamespace(x=0.25, y=-0.5, gamma=np.float32(0.5), sigma=0.125))
+    x, y, g, s = vf.to_arrays(parts)
+    for a in (x, y, g, s):
+        assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"] and a.shape == (2,)
+    assert x.tolist() == [1.0, 0.25] and y.tolist() == [2.0, -0.5]
+    assert g.tolist() == [3.0, 0.5] and s.tolist() == [1.0, 0.125]
+    with pytest.raises((TypeError, ValueError)):
+        vf.to_arrays([vf.Particle(0.0, None, 1.0, 0.1)])
+
+
 def test_grid_indices_floor_rule_and_clamp():
     dom = vf.Domain(0.0, 0.0, 1.0)
     ix, iy = vf.grid_indices(np.array([0.0, 0.5, 1.0, 0.24999999]), np.array([1.0, 0.25, 0.0, 0.75]), 4, dom)
